@@ -1,0 +1,228 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes view of oracle/_ref/libaffmae_ref.so.
+
+That library is the UNMODIFIED reference C++ (``/root/reference/proj/src``)
+compiled by ``oracle/Makefile`` plus our ``ref_shim.cpp``.  Only ``tests/``,
+``__graft_entry__.smoke`` and ``bench.py``'s CPU legs may import this module;
+the product path never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libaffmae_ref.so")
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"reference oracle not built: {LIB_PATH} (run make -C oracle)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.ref_last_error.restype = C.c_char_p
+        _lib.ref_retained_count.restype = C.c_int64
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().ref_last_error().decode()
+        if rc == 2:
+            raise ValueError(msg)
+        if rc == 3:
+            raise ArithmeticError(msg)
+        raise RuntimeError(msg)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def sfc_order(coords):
+    coords = _f32(coords)
+    n = coords.shape[0]
+    perm = np.empty(n, np.int64)
+    _check(lib().ref_sfc_order(_p(coords), C.c_int64(n), _p(perm)))
+    return perm
+
+
+def cluster_shape(n, size, groups):
+    out = [C.c_int64() for _ in range(4)]
+    _check(lib().ref_cluster_shape(C.c_int64(n), C.c_int64(size), C.c_int64(groups),
+                                   *[C.byref(o) for o in out]))
+    return tuple(o.value for o in out)  # (C, groups_eff, max_size, width)
+
+
+def cluster_index(coords, size, groups):
+    """balanced_clusters + cluster_neighborhood.
+
+    Returns dict(cluster_of[n] i32, members[n] i64 (curve order), member_off[C+1],
+    idx[n, M] i64, valid[n, M] u8, width M).
+    """
+    coords = _f32(coords)
+    n = coords.shape[0]
+    c, g, mx, width = cluster_shape(n, size, groups)
+    cluster_of = np.empty(n, np.int32)
+    members = np.empty(n, np.int64)
+    off = np.empty(c + 1, np.int64)
+    idx = np.empty((n, width), np.int64)
+    valid = np.empty((n, width), np.uint8)
+    _check(lib().ref_cluster_index(_p(coords), C.c_int64(n), C.c_int64(size), C.c_int64(groups),
+                                   _p(cluster_of), _p(members), _p(off), _p(idx), _p(valid),
+                                   C.c_int64(width)))
+    return dict(cluster_of=cluster_of, members=members, member_off=off, idx=idx, valid=valid,
+                width=width, n_clusters=c, groups=g, max_size=mx)
+
+
+def knn(queries, keys, k):
+    queries, keys = _f32(queries), _f32(keys)
+    nq, nk = queries.shape[0], keys.shape[0]
+    idx = np.empty((nq, k), np.int64)
+    valid = np.empty((nq, k), np.uint8)
+    _check(lib().ref_knn(_p(queries), C.c_int64(nq), _p(keys), C.c_int64(nk), C.c_int64(k),
+                         _p(idx), _p(valid)))
+    return idx, valid
+
+
+def _attn_args(q, k, v, bk, bv, coords, idx, valid, bias, heads, head_dim, patch):
+    q, k, v, bk, bv = (_f64(x) for x in (q, k, v, bk, bv))
+    coords = _f32(coords)
+    idx = _i64(idx)
+    valid = np.ascontiguousarray(valid, dtype=np.uint8)
+    w1, b1, w2, b2, blank = (_f64(bias[x]) for x in ("w1", "b1", "w2", "b2", "blank"))
+    n, m = idx.shape
+    hidden = w1.shape[1] // 2
+    keep = (q, k, v, bk, bv, coords, idx, valid, w1, b1, w2, b2, blank)
+    args = [C.c_int64(n), C.c_int64(m), C.c_int(heads), C.c_int(head_dim), C.c_int(hidden),
+            C.c_double(patch), _p(q), _p(k), _p(v), _p(bk), _p(bv), _p(coords), _p(idx),
+            _p(valid), _p(w1), _p(b1), _p(w2), _p(b2), _p(blank)]
+    return args, keep, n
+
+
+def attn_fwd(q, k, v, bk, bv, coords, idx, valid, bias, heads, head_dim, patch=8.0, prec=32,
+             mode=0):
+    """nbhd_attn_streaming (mode 0), nbhd_attn_naive (1), streaming half_io (2)."""
+    args, keep, n = _attn_args(q, k, v, bk, bv, coords, idx, valid, bias, heads, head_dim, patch)
+    out = np.empty((n, heads * head_dim), np.float64)
+    _check(lib().ref_attn_fwd(*args, C.c_int(prec), C.c_int(mode), _p(out)))
+    return out
+
+
+def attn_bwd(q, k, v, bk, bv, coords, idx, valid, bias, heads, head_dim, dout, patch=8.0,
+             prec=32):
+    args, keep, n = _attn_args(q, k, v, bk, bv, coords, idx, valid, bias, heads, head_dim, patch)
+    dout = _f64(dout)
+    hd = heads * head_dim
+    hidden = keep[8].shape[1] // 2
+    g = dict(dq=np.empty((n, hd)), dk=np.empty((n, hd)), dv=np.empty((n, hd)),
+             dblank_k=np.empty((heads, head_dim)), dblank_v=np.empty((heads, head_dim)),
+             dw1=np.empty((heads, 2 * hidden)), db1=np.empty((heads, hidden)),
+             dw2=np.empty((heads, hidden)), db2=np.empty((heads, 1)), dblank=np.empty((heads, 1)))
+    order = ("dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")
+    _check(lib().ref_attn_bwd(*args, C.c_int(prec), _p(dout), *[_p(g[o]) for o in order]))
+    return g
+
+
+def retained_count(n, d_s):
+    r = lib().ref_retained_count(C.c_int64(n), C.c_double(d_s))
+    if r < 0:
+        raise ValueError(lib().ref_last_error().decode())
+    return r
+
+
+def select_retained(scores, d_s, prec=64):
+    scores = _f64(scores).reshape(-1)
+    n = scores.shape[0]
+    out = np.empty(n, np.int64)
+    cnt = C.c_int64()
+    _check(lib().ref_select_retained(_p(scores), C.c_int64(n), C.c_double(d_s), C.c_int(prec),
+                                     _p(out), C.byref(cnt)))
+    return out[: cnt.value]
+
+
+def merge_plan(coords, retained, k_m):
+    coords = _f32(coords)
+    retained = _i64(retained)
+    n, r = coords.shape[0], retained.shape[0]
+    dropped = np.empty(n - r, np.int64)
+    target = np.empty(n - r, np.int64)
+    pool_idx = np.empty((r, k_m), np.int64)
+    pool_dist = np.empty((r, k_m), np.float64)
+    pool_cnt = np.empty(r, np.int32)
+    _check(lib().ref_merge_plan(_p(coords), C.c_int64(n), _p(retained), C.c_int64(r),
+                                C.c_int(k_m), _p(dropped), _p(target), _p(pool_idx),
+                                _p(pool_dist), _p(pool_cnt)))
+    return dict(retained=retained, dropped=dropped, target=target, pool_idx=pool_idx,
+                pool_dist=pool_dist, pool_cnt=pool_cnt)
+
+
+def merge_pool_fwd(plan, feats, scores, p, prec=64):
+    feats, scores = _f64(feats), _f64(scores).reshape(-1)
+    n, dim = feats.shape
+    r, k_m = plan["pool_idx"].shape
+    out = np.empty((r, 2 * dim))
+    _check(lib().ref_merge_pool_fwd(C.c_int64(n), C.c_int64(dim), C.c_int64(r), C.c_int(k_m),
+                                    _p(_i64(plan["retained"])), _p(_i64(plan["pool_idx"])),
+                                    _p(_f64(plan["pool_dist"])),
+                                    _p(np.ascontiguousarray(plan["pool_cnt"], np.int32)),
+                                    _p(feats), _p(scores), C.c_double(p), C.c_int(prec), _p(out)))
+    return out
+
+
+def merge_pool_bwd(plan, feats, scores, p, dout, prec=64):
+    feats, scores, dout = _f64(feats), _f64(scores).reshape(-1), _f64(dout)
+    n, dim = feats.shape
+    r, k_m = plan["pool_idx"].shape
+    df = np.empty((n, dim))
+    ds = np.empty(n)
+    dp = C.c_double()
+    keep = (_i64(plan["retained"]), _i64(plan["pool_idx"]), _f64(plan["pool_dist"]),
+            np.ascontiguousarray(plan["pool_cnt"], np.int32))
+    _check(lib().ref_merge_pool_bwd(C.c_int64(n), C.c_int64(dim), C.c_int64(r), C.c_int(k_m),
+                                    *[_p(x) for x in keep], _p(feats), _p(scores), C.c_double(p),
+                                    C.c_int(prec), _p(dout), _p(df), _p(ds), C.byref(dp)))
+    return df, ds, dp.value
+
+
+def perlin_mask(grid, ratio, seed):
+    m = np.empty(grid * grid, np.uint8)
+    _check(lib().ref_perlin_mask(C.c_int64(grid), C.c_double(ratio), C.c_uint64(seed), _p(m)))
+    return m.reshape(grid, grid)
+
+
+def hotpath_batch(images, threads, stages, coords, q, k, v, dout, scores, bk, bv, bias,
+                  heads, head_dim, patch, cluster, groups, d_s, k_m, p):
+    """Runs the reference hot path over `images` images on `threads` threads."""
+    n = coords.shape[1]
+    arrs = [_f32(coords)] + [_f64(x) for x in (q, k, v, dout, scores, bk, bv, bias["w1"],
+                                               bias["b1"], bias["w2"], bias["b2"],
+                                               bias["blank"])]
+    hidden = arrs[8].shape[1] // 2
+    cs = C.c_double()
+    _check(lib().ref_hotpath_batch(C.c_int64(images), C.c_int(threads), C.c_int(stages),
+                                   C.c_int64(n), C.c_int(heads), C.c_int(head_dim),
+                                   C.c_int(hidden), C.c_double(patch), C.c_int64(cluster),
+                                   C.c_int64(groups), C.c_double(d_s), C.c_int(k_m),
+                                   *[_p(a) for a in arrs], C.c_double(p), C.byref(cs)))
+    return cs.value
