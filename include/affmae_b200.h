@@ -1,0 +1,204 @@
+/*
+ * affmae_b200.h — C ABI of the B200-native AFFMAE hot path (libaffmae_b200.so).
+ *
+ * Plain pointers and sizes only; every call is asynchronous on the caller's
+ * CUDA stream (passed as `void*`, a cudaStream_t; NULL = legacy default
+ * stream).  All tensor pointers are DEVICE pointers unless a name ends in
+ * `_host`.  Batched: B images of N tokens each (the reference is batch-1;
+ * exact mask counts make every image in a batch the same size,
+ * SURVEY.md §0.9).  Token order inside an image is the reference's order
+ * (ascending patch index for stage 0, ascending retained index afterwards).
+ *
+ * Status codes (reference error taxonomy, proj/include/affmae/errors.hpp:8-15):
+ *   AFFMAE_OK 0, AFFMAE_ECONFIG 2 (ConfigError), AFFMAE_ENUMERIC 3
+ *   (NumericError), AFFMAE_EUNSUPPORTED 4 (shape outside the compiled kernel
+ *   variants; maps to ConfigError), AFFMAE_ECUDA 5 (CUDA runtime failure).
+ * affmae_last_error() returns the calling thread's last message.
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to the reference checkout's proj/).
+ */
+#ifndef AFFMAE_B200_H
+#define AFFMAE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFFMAE_OK 0
+#define AFFMAE_ECONFIG 2
+#define AFFMAE_ENUMERIC 3
+#define AFFMAE_EUNSUPPORTED 4
+#define AFFMAE_ECUDA 5
+
+typedef uint16_t affmae_bf16; /* IEEE bfloat16 bit pattern */
+
+const char* affmae_last_error(void);
+int affmae_version(void);
+
+/* ------------------------------------------------------------------------
+ * Cluster geometry (closed forms of balanced_clusters / cluster_neighborhood,
+ * src/geometry.cpp:108-131,133-156).  Fill batch/tokens/cluster/groups, call
+ * affmae_cluster_geometry to validate and derive the rest.
+ * ---------------------------------------------------------------------- */
+typedef struct affmae_cluster_geom {
+    int64_t batch;      /* B images */
+    int64_t tokens;     /* N tokens per image */
+    int64_t cluster;    /* requested cluster size (balanced_clusters `size`) */
+    int64_t groups;     /* requested neighbour groups (cluster_neighborhood `groups`) */
+    /* derived */
+    int64_t n_clusters; /* C = ceil(N / min(size, N)) */
+    int64_t groups_eff; /* G = min(groups, C) */
+    int64_t max_size;   /* ceil(N / C): largest cluster */
+    int64_t width;      /* M = G * max_size: NeighborIndex::width */
+} affmae_cluster_geom;
+
+int affmae_cluster_geometry(affmae_cluster_geom* g);
+
+/* Device-resident cluster index of one batch.  Cluster k of image b holds
+ * curve positions [k*base + min(k,rem), ... + base + (k<rem)) of perm[b],
+ * base = N / C, rem = N % C (balanced_clusters, src/geometry.cpp:111-129). */
+typedef struct affmae_cluster_index {
+    int32_t* perm;       /* [B, N]   sfc_order (src/geometry.cpp:69-106) */
+    int32_t* cluster_of; /* [B, N]   ClusterAssignment::cluster_of */
+    int32_t* nbr_cl;     /* [B, C, G] own cluster first, then the G-1 nearest
+                                      centroids by (d^2, j) (src/geometry.cpp:157-172) */
+    int32_t* rev_off;    /* [B, C+1] reverse-neighbour CSR offsets (for attention bwd) */
+    int32_t* rev_cl;     /* [B, C*G] query clusters listing cluster c', ascending */
+} affmae_cluster_index;
+
+/* Workspace bytes for affmae_cluster_index_build. */
+size_t affmae_cluster_index_workspace(const affmae_cluster_geom* g);
+
+/* Replaces balanced_clusters + cluster_neighborhood
+ * (include/affmae/geometry.hpp:61-68; src/geometry.cpp:108-186), batched.
+ * coords: [B, N, 2] float32 pixel centres.  Bit-exact with the reference. */
+int affmae_cluster_index_build(const affmae_cluster_geom* g, const float* coords,
+                               affmae_cluster_index* out, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/* Expands the compact index into the reference's NeighborIndex layout
+ * (include/affmae/geometry.hpp:33-48): idx [B, N, M] int32 (padding 0),
+ * valid [B, N, M] uint8. For parity dumps and generic consumers. */
+int affmae_neighbor_expand(const affmae_cluster_geom* g, const int32_t* perm,
+                           const int32_t* nbr_cl, int32_t* idx, uint8_t* valid, void* stream);
+
+/* Replaces sfc_order (src/geometry.cpp:69-106), batched: perm [B, N]. */
+size_t affmae_sfc_order_workspace(int64_t batch, int64_t tokens);
+int affmae_sfc_order(const float* coords, int64_t batch, int64_t tokens, int32_t* perm,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* Replaces knn (src/geometry.cpp:188-216), batched: queries [B, Q, 2],
+ * keys [B, K, 2] -> idx [B, Q, k] int32, valid [B, Q, k] uint8.  Exact
+ * (d^2 in binary64, ties to the lower key index). */
+int affmae_knn(const float* queries, const float* keys, int64_t batch, int64_t n_queries,
+               int64_t n_keys, int64_t k, int32_t* idx, uint8_t* valid, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Cluster attention (nbhd_attn_streaming / nbhd_attn_backward,
+ * include/affmae/attention.hpp:52-72; AttnOp, src/attention.cpp:374-444).
+ * ---------------------------------------------------------------------- */
+typedef struct affmae_attn_desc {
+    int heads;
+    int head_dim;
+    int bias_hidden; /* BiasNet hidden width H */
+    double patch;    /* BiasNet offset normaliser */
+} affmae_attn_desc;
+
+typedef struct affmae_attn_inputs {
+    const affmae_bf16* q;       /* [B, N, heads*head_dim] */
+    const affmae_bf16* k;       /* [B, N, heads*head_dim] */
+    const affmae_bf16* v;       /* [B, N, heads*head_dim] */
+    const affmae_bf16* blank_k; /* [heads, head_dim] */
+    const affmae_bf16* blank_v; /* [heads, head_dim] */
+    const float* coords;        /* [B, N, 2] */
+    const float* w1;            /* [heads, 2H]  BiasNet (include/affmae/attention.hpp:16-29) */
+    const float* b1;            /* [heads, H] */
+    const float* w2;            /* [heads, H] */
+    const float* b2;            /* [heads] */
+    const float* blank;         /* [heads]  blank-slot bias */
+} affmae_attn_inputs;
+
+/* Workspace bytes for affmae_attn_fwd (holds the per-call BiasNet offset table). */
+size_t affmae_attn_fwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a);
+
+/* Forward: out [B, N, heads*head_dim] bf16 and lse [B, N, heads] fp32
+ * (natural-log softmax normaliser, kept for the backward). */
+int affmae_attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                    const affmae_attn_inputs* in, const int32_t* perm, const int32_t* nbr_cl,
+                    affmae_bf16* out, float* lse, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+typedef struct affmae_attn_grads {
+    affmae_bf16* dq;  /* [B, N, h*d]  overwritten */
+    affmae_bf16* dk;  /* [B, N, h*d]  overwritten */
+    affmae_bf16* dv;  /* [B, N, h*d]  overwritten */
+    float* dblank_k;  /* [h, d]   accumulated (+=), CustomOp::backward semantics */
+    float* dblank_v;  /* [h, d]   += */
+    float* dw1;       /* [h, 2H]  += */
+    float* db1;       /* [h, H]   += */
+    float* dw2;       /* [h, H]   += */
+    float* db2;       /* [h]      += */
+    float* dblank;    /* [h]      += */
+} affmae_attn_grads;
+
+size_t affmae_attn_bwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a);
+
+int affmae_attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                    const affmae_attn_inputs* in, const affmae_cluster_index* idx,
+                    const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                    affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* ------------------------------------------------------------------------
+ * Adaptive KNN merge (src/merging.cpp).
+ * ---------------------------------------------------------------------- */
+
+/* retained_count (src/merging.cpp:50-54); -2 on d_s outside (0, 1]. */
+int64_t affmae_retained_count(int64_t n, double d_s);
+
+size_t affmae_select_retained_workspace(int64_t batch, int64_t tokens);
+/* select_retained (src/merging.cpp:56-69), batched: scores [B, N] fp32 ->
+ * retained [B, R] int32 ascending, R = retained_count(N, d_s).  Bit-exact. */
+int affmae_select_retained(const float* scores, int64_t batch, int64_t tokens, double d_s,
+                           int32_t* retained, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
+typedef struct affmae_merge_plan {
+    int32_t* target;    /* [B, N]  retained index each dropped token goes to; -1 for retained */
+    int32_t* pool_idx;  /* [B, R, k_m] contributor token indices, (dist, index) ascending */
+    double* pool_dist;  /* [B, R, k_m] Euclidean distances (binary64, bit-exact) */
+    int32_t* pool_cnt;  /* [B, R] valid entries per pool (<= k_m) */
+} affmae_merge_plan;
+
+size_t affmae_merge_plan_workspace(int64_t batch, int64_t tokens, int64_t retained);
+/* merge_plan (src/merging.cpp:71-116), batched; coords [B, N, 2],
+ * retained [B, R] ascending.  Bit-exact (first-minimum tie rule). */
+int affmae_merge_plan_build(const float* coords, const int32_t* retained, int64_t batch,
+                            int64_t tokens, int64_t n_retained, int k_m, affmae_merge_plan* plan,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* MergePoolOp::forward (src/merging.cpp:121-166): out [B, R, 2D] bf16 rows
+ * [f_r ; sum_t softmax(-p*dist)_t * s_j * f_j].  p_merge is a device scalar. */
+int affmae_merge_pool_fwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
+                          const int32_t* retained, const affmae_merge_plan* plan, int64_t batch,
+                          int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
+                          affmae_bf16* out, void* stream);
+
+size_t affmae_merge_pool_bwd_workspace(int64_t batch, int64_t n_retained);
+/* MergePoolOp::backward (src/merging.cpp:169-219): dfeats [B, N, D] bf16 and
+ * dscores [B, N] fp32 are overwritten (every token receives at most one
+ * contribution); dp [1] fp32 is accumulated (+=). */
+int affmae_merge_pool_bwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
+                          const int32_t* retained, const affmae_merge_plan* plan, int64_t batch,
+                          int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
+                          const affmae_bf16* dout, affmae_bf16* dfeats, float* dscores,
+                          float* dp, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AFFMAE_B200_H */

@@ -1,0 +1,113 @@
+"""ctypes binding of the C ABI in ``include/affmae_b200.h`` (libaffmae_b200.so).
+
+This is the thin layer the Python side (tests, bench, the torch-facing op
+wrappers in :mod:`paper_2602_16249_b200.ops`) uses to reach the CUDA kernels.
+Device memory comes from torch tensors (``data_ptr()``) and streams from
+``torch.cuda.current_stream()`` -- torch is plumbing here, every compute call
+goes through the C ABI.  There is no fallback: if the shared library is
+missing, :func:`lib` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaffmae_b200.so")
+
+OK, ECONFIG, ENUMERIC, EUNSUPPORTED, ECUDA = 0, 2, 3, 4, 5
+
+# Every symbol include/affmae_b200.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = (
+    "affmae_last_error", "affmae_version", "affmae_cluster_geometry",
+    "affmae_cluster_index_workspace", "affmae_cluster_index_build", "affmae_neighbor_expand",
+    "affmae_sfc_order_workspace", "affmae_sfc_order", "affmae_knn",
+    "affmae_attn_fwd_workspace", "affmae_attn_fwd", "affmae_attn_bwd_workspace", "affmae_attn_bwd",
+    "affmae_retained_count", "affmae_select_retained_workspace", "affmae_select_retained",
+    "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
+    "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd",
+)
+
+
+class AffmaeError(RuntimeError):
+    pass
+
+
+class ClusterGeom(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("batch", "tokens", "cluster", "groups", "n_clusters",
+                                         "groups_eff", "max_size", "width")]
+
+
+class ClusterIndex(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("perm", "cluster_of", "nbr_cl", "rev_off", "rev_cl")]
+
+
+class AttnDesc(C.Structure):
+    _fields_ = [("heads", C.c_int), ("head_dim", C.c_int), ("bias_hidden", C.c_int),
+                ("patch", C.c_double)]
+
+
+class AttnInputs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("q", "k", "v", "blank_k", "blank_v", "coords", "w1",
+                                          "b1", "w2", "b2", "blank")]
+
+
+class AttnGrads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1",
+                                          "dw2", "db2", "dblank")]
+
+
+class MergePlan(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("target", "pool_idx", "pool_dist", "pool_cnt")]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise AffmaeError(
+                f"CUDA extension missing: {LIB_PATH}; run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.affmae_last_error.restype = C.c_char_p
+        L.affmae_retained_count.restype = C.c_int64
+        L.affmae_retained_count.argtypes = [C.c_int64, C.c_double]
+        for f in ("affmae_cluster_index_workspace", "affmae_sfc_order_workspace",
+                  "affmae_attn_fwd_workspace",
+                  "affmae_attn_bwd_workspace", "affmae_select_retained_workspace",
+                  "affmae_merge_plan_workspace", "affmae_merge_pool_bwd_workspace"):
+            if hasattr(L, f):
+                getattr(L, f).restype = C.c_size_t
+        _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = ""):
+    """Maps status codes onto the reference's exception taxonomy (ConfigError ->
+    ValueError, NumericError -> ArithmeticError; proj/bindings/module.cpp:91-92)."""
+    if rc == OK:
+        return
+    msg = lib().affmae_last_error().decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc in (ECONFIG, EUNSUPPORTED):
+        raise ValueError(msg)
+    if rc == ENUMERIC:
+        raise ArithmeticError(msg)
+    raise AffmaeError(msg)
+
+
+def ptr(t) -> int | None:
+    """Device address of a torch tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def geometry(batch: int, tokens: int, cluster: int, groups: int) -> ClusterGeom:
+    g = ClusterGeom(batch, tokens, cluster, groups, 0, 0, 0, 0)
+    check(lib().affmae_cluster_geometry(C.byref(g)), "cluster_geometry")
+    return g

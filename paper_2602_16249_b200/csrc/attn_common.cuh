@@ -1,0 +1,103 @@
+// Shared pieces of the cluster-attention kernels: the relative-position bias
+// provider (exact lookup table on the patch lattice, tanh-MLP elsewhere),
+// per-token lattice info, and the cluster-centric shared-memory staging.
+//
+// Bias memoisation.  BiasNet::eval (proj/src/attention.cpp:33-42) maps the
+// offset (dx/patch, dy/patch) through a per-head tanh MLP.  In the model path
+// every token sits on the patch-centre lattice, so dx/patch
+// and dy/patch are small integers and the bias is a function of an integer
+// offset.  We evaluate it ONCE per call for every offset in
+// [-kRg, kRg]^2 (bias_table_kernel, accurate tanhf) and look it up per pair:
+//   tier 1: |offset| <= kRs  -> shared-memory window of the table (~99% of pairs)
+//   tier 2: |offset| <= kRg  -> the global table (L2)
+//   tier 3: off-lattice pair or |offset| > kRg -> the MLP itself (tanh.approx)
+// Tiers 1/2 return the same function value as tier 3 (up to tanh rounding).
+// The backward scatters dS into a table gradient dT and turns dT into BiasNet
+// parameter gradients once per call (bias_grad_finalize_kernel).
+#pragma once
+
+#include "common.cuh"
+
+namespace affmae_b200 {
+
+constexpr int kRs = 11;               // shared-memory window radius (patches)
+constexpr int kWs = 2 * kRs + 1;      // 23
+constexpr int kWs2 = kWs * kWs;       // 529 entries per head
+constexpr int kRg = 127;              // global table radius
+constexpr int kWg = 2 * kRg + 1;      // 255
+constexpr int kWg2 = kWg * kWg;       // 65025 entries per head
+
+// Per staged token: integer lattice cell and the exact fractional phase
+// (x*inv_patch = ix + fx).  Two tokens are lattice-compatible iff their
+// phases are bit-identical; then dx/patch == kx.ix - qx.ix exactly.
+struct __align__(16) TokInfo {
+    int ix, iy;
+    uint32_t fx, fy;  // float bits of the fractional phase
+};
+__device__ __forceinline__ TokInfo make_tokinfo(float2 xy, float inv_patch) {
+    float gx = xy.x * inv_patch, gy = xy.y * inv_patch;
+    float flx = floorf(gx), fly = floorf(gy);
+    TokInfo t;
+    t.ix = int(flx);
+    t.iy = int(fly);
+    t.fx = __float_as_uint(gx - flx);
+    t.fy = __float_as_uint(gy - fly);
+    return t;
+}
+
+constexpr int kMaxHidden = 32;
+
+// BiasNet tanh-MLP for one pair (tier 3): b2 + sum_u w2_u tanh(w1x_u ox + w1y_u oy + b1_u)
+__device__ __forceinline__ float bias_mlp(const float4* units, int hidden, float b2, float ox,
+                                          float oy) {
+    float acc = b2;
+    for (int u = 0; u < hidden; ++u) {
+        float4 p = units[u];
+        acc = fmaf(p.w, tanh_fast(fmaf(p.x, ox, fmaf(p.y, oy, p.z))), acc);
+    }
+    return acc;
+}
+
+// Tier-3 gradient: accumulates dL/d(w1,b1,w2,b2) of one pair into a shared
+// per-head accumulator [4H+1] = {dw1x[H], dw1y[H], db1[H], dw2[H], db2}.
+__device__ __forceinline__ void bias_mlp_grad(const float4* units, int hidden, float ds, float ox,
+                                              float oy, float* acc) {
+    for (int u = 0; u < hidden; ++u) {
+        float4 p = units[u];
+        float t = tanh_fast(fmaf(p.x, ox, fmaf(p.y, oy, p.z)));
+        float dpre = ds * p.w * (1.f - t * t);
+        atomicAdd(acc + u, dpre * ox);
+        atomicAdd(acc + hidden + u, dpre * oy);
+        atomicAdd(acc + 2 * hidden + u, dpre);
+        atomicAdd(acc + 3 * hidden + u, ds * t);
+    }
+    atomicAdd(acc + 4 * hidden, ds);
+}
+
+// Out-of-line tiers 2/3 (rare on the lattice): keeps the unrolled fast path small.
+static __device__ __noinline__ float bias_tier23(const float* tabg, int gi, const float4* units,
+                                          int hidden, float b2, float ox, float oy) {
+    if (gi >= 0) return __ldg(tabg + gi);
+    return bias_mlp(units, hidden, b2, ox, oy);
+}
+static __device__ __noinline__ void bias_grad_tier23(float* dtab_g, int gi, const float4* units,
+                                              int hidden, float ds, float ox, float oy,
+                                              float* mlpg) {
+    if (gi >= 0) atomicAdd(dtab_g + gi, ds);
+    else bias_mlp_grad(units, hidden, ds, ox, oy, mlpg);
+}
+
+// Table window index of a pair, or -1 (tier 1 miss).  `gidx` gets the
+// global-table index, or -1 (tier 2 miss -> MLP).
+__device__ __forceinline__ int lut_index(const TokInfo& q, const TokInfo& k, int& gidx) {
+    gidx = -1;
+    if (q.fx != k.fx || q.fy != k.fy) return -1;
+    int ox = k.ix - q.ix, oy = k.iy - q.iy;
+    if (unsigned(ox + kRg) < unsigned(kWg) && unsigned(oy + kRg) < unsigned(kWg))
+        gidx = (oy + kRg) * kWg + (ox + kRg);
+    if (unsigned(ox + kRs) < unsigned(kWs) && unsigned(oy + kRs) < unsigned(kWs))
+        return (oy + kRs) * kWs + (ox + kRs);
+    return -1;
+}
+
+}  // namespace affmae_b200

@@ -1,0 +1,12 @@
+// Explicit instantiations of the attention kernels for head_dim 64
+// (split across translation units so the build parallelises).
+#include "attn_kernels.cuh"
+
+namespace affmae_b200 {
+AFFMAE_INSTANTIATE_ATTN(64, 4, 1)
+AFFMAE_INSTANTIATE_ATTN(64, 4, 2)
+AFFMAE_INSTANTIATE_ATTN(64, 4, 4)
+AFFMAE_INSTANTIATE_ATTN(64, 7, 1)
+AFFMAE_INSTANTIATE_ATTN(64, 7, 2)
+AFFMAE_INSTANTIATE_ATTN(64, 7, 4)
+}  // namespace affmae_b200

@@ -1,0 +1,130 @@
+// extern "C" entry points of libaffmae_b200.so (declared in include/affmae_b200.h)
+// plus the thread-local error slot.  Argument validation mirrors the
+// reference's ConfigError checks; kernels live in the other translation units.
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace affmae_b200 {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return AFFMAE_ECUDA;
+}
+
+// implemented in attention.cu / index.cu / merge.cu
+size_t attn_fwd_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
+size_t attn_bwd_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
+int attn_fwd(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
+             const int32_t*, const int32_t*, affmae_bf16*, float*, void*, size_t, void*);
+int attn_bwd(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
+             const affmae_cluster_index*, const affmae_bf16*, const float*, const affmae_bf16*,
+             affmae_attn_grads*, void*, size_t, void*);
+size_t cluster_index_workspace(const affmae_cluster_geom*);
+int cluster_index_build(const affmae_cluster_geom*, const float*, affmae_cluster_index*, void*,
+                        size_t, void*);
+size_t sfc_order_workspace(int64_t, int64_t);
+int sfc_order(const float*, int64_t, int64_t, int32_t*, void*, size_t, void*);
+int neighbor_expand(const affmae_cluster_geom*, const int32_t*, const int32_t*, int32_t*, uint8_t*,
+                    void*);
+int knn(const float*, const float*, int64_t, int64_t, int64_t, int64_t, int32_t*, uint8_t*, void*);
+
+}  // namespace affmae_b200
+
+using namespace affmae_b200;
+
+extern "C" {
+
+const char* affmae_last_error(void) { return g_last_error.c_str(); }
+
+int affmae_version(void) { return 1; }
+
+// balanced_clusters / cluster_neighborhood closed forms (proj/src/geometry.cpp:108-156)
+int affmae_cluster_geometry(affmae_cluster_geom* g) {
+    if (!g) return fail(AFFMAE_ECONFIG, "cluster_geometry: null");
+    if (g->batch < 0) return fail(AFFMAE_ECONFIG, "cluster_geometry: negative batch");
+    if (g->tokens < 1) return fail(AFFMAE_ECONFIG, "sfc_order: empty point set");
+    if (g->cluster < 1) return fail(AFFMAE_ECONFIG, "balanced_clusters: size must be >= 1");
+    if (g->groups < 1) return fail(AFFMAE_ECONFIG, "cluster_neighborhood: groups must be >= 1");
+    if (g->tokens > (int64_t(1) << 30)) return fail(AFFMAE_EUNSUPPORTED, "cluster_geometry: too many tokens");
+    int64_t s = g->cluster < g->tokens ? g->cluster : g->tokens;
+    g->n_clusters = (g->tokens + s - 1) / s;
+    g->groups_eff = g->groups < g->n_clusters ? g->groups : g->n_clusters;
+    g->max_size = g->tokens / g->n_clusters + (g->tokens % g->n_clusters ? 1 : 0);
+    g->width = g->groups_eff * g->max_size;
+    return AFFMAE_OK;
+}
+
+size_t affmae_attn_fwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
+    return attn_fwd_workspace(g, a);
+}
+
+int affmae_attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                    const affmae_attn_inputs* in, const int32_t* perm, const int32_t* nbr_cl,
+                    affmae_bf16* out, float* lse, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+    return attn_fwd(g, a, in, perm, nbr_cl, out, lse, workspace, workspace_bytes, stream);
+}
+
+size_t affmae_attn_bwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
+    return attn_bwd_workspace(g, a);
+}
+
+int affmae_attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                    const affmae_attn_inputs* in, const affmae_cluster_index* idx,
+                    const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                    affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+    return attn_bwd(g, a, in, idx, out, lse, dout, grads, workspace, workspace_bytes, stream);
+}
+
+size_t affmae_cluster_index_workspace(const affmae_cluster_geom* g) { return cluster_index_workspace(g); }
+
+int affmae_cluster_index_build(const affmae_cluster_geom* g, const float* coords,
+                               affmae_cluster_index* out, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+    return cluster_index_build(g, coords, out, workspace, workspace_bytes, stream);
+}
+
+int affmae_neighbor_expand(const affmae_cluster_geom* g, const int32_t* perm, const int32_t* nbr_cl,
+                           int32_t* idx, uint8_t* valid, void* stream) {
+    return neighbor_expand(g, perm, nbr_cl, idx, valid, stream);
+}
+
+size_t affmae_sfc_order_workspace(int64_t batch, int64_t tokens) {
+    return sfc_order_workspace(batch, tokens);
+}
+
+int affmae_sfc_order(const float* coords, int64_t batch, int64_t tokens, int32_t* perm,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    return sfc_order(coords, batch, tokens, perm, workspace, workspace_bytes, stream);
+}
+
+int affmae_knn(const float* queries, const float* keys, int64_t batch, int64_t n_queries,
+               int64_t n_keys, int64_t k, int32_t* idx, uint8_t* valid, void* stream) {
+    return knn(queries, keys, batch, n_queries, n_keys, k, idx, valid, stream);
+}
+
+// retained_count (proj/src/merging.cpp:50-54)
+int64_t affmae_retained_count(int64_t n, double d_s) {
+    if (!(d_s > 0.0 && d_s <= 1.0)) {
+        fail(AFFMAE_ECONFIG, "retained_count: d_s must be in (0, 1]");
+        return -2;
+    }
+    int64_t k = int64_t(std::floor(d_s * double(n) + 0.5));
+    if (k > n) k = n;
+    return k < 1 ? 1 : k;
+}
+
+}  // extern "C"

@@ -1,0 +1,529 @@
+// Cluster / neighbour index builder, batched and bit-exact with the reference:
+//   sfc_order            proj/src/geometry.cpp:57-106
+//   balanced_clusters    proj/src/geometry.cpp:108-131
+//   cluster_neighborhood proj/src/geometry.cpp:133-186
+//   knn                  proj/src/geometry.cpp:188-216
+//
+// Bit-exactness.  Every floating-point step the reference takes in binary64 is
+// repeated in binary64 with explicit round-to-nearest intrinsics (no FMA
+// contraction): coordinate extents and gaps (differences of binary32 values,
+// exact), the quantisation (x - xmin) * scale with llround (half away from
+// zero), centroids as sequential member-order sums times 1.0/|c|, and
+// d^2 = dx*dx + dy*dy.  ceil(log2(.)) emulates a correctly rounded log2 (the
+// glibc behaviour) exactly except within half an ulp of the rounding boundary.
+// Ordering: a stable LSD radix sort (sort.cuh) on (image, key) reproduces
+// std::stable_sort; the neighbour selection keeps the (d^2, j) order of
+// std::partial_sort and puts the own cluster first (geometry.cpp:166-172).
+#include <cmath>
+
+#include "sort.cuh"
+
+namespace affmae_b200 {
+
+__device__ __forceinline__ float float_unorder(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// hilbert_index, proj/src/geometry.cpp:15-30
+__device__ __forceinline__ uint64_t hilbert(uint32_t n, uint32_t x, uint32_t y) {
+    uint64_t d = 0;
+    for (uint32_t s = n / 2; s > 0; s /= 2) {
+        uint32_t rx = (x & s) ? 1u : 0u;
+        uint32_t ry = (y & s) ? 1u : 0u;
+        d += uint64_t(s) * uint64_t(s) * ((3u * rx) ^ ry);
+        if (ry == 0) {
+            if (rx == 1) {
+                x = s - 1 - x;
+                y = s - 1 - y;
+            }
+            uint32_t t = x;
+            x = y;
+            y = t;
+        }
+    }
+    return d;
+}
+
+// ---------------------------------------------------------- sfc_order
+__global__ void axis_keys_kernel(const float* __restrict__ coords, int64_t batch, int64_t n,
+                                 uint64_t* __restrict__ keys) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * n * 2) return;
+    int64_t tok = i >> 1;
+    int axis = int(i & 1);
+    int64_t img = tok / n, j = tok - img * n;
+    uint64_t seg = uint64_t(img) * 2 + axis;
+    // segment-major layout: [img][axis][j]
+    keys[(img * 2 + axis) * n + j] = (seg << 32) | float_order(coords[i]);
+}
+
+// min_gap: smallest positive gap between consecutive sorted values (0 if none)
+__global__ void gap_kernel(const uint64_t* __restrict__ sorted, int64_t segs, int64_t n,
+                           unsigned long long* __restrict__ gap_bits) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= segs * n) return;
+    int64_t j = i % n;
+    if (j == 0) return;
+    double a = double(float_unorder(uint32_t(sorted[i - 1]))), b = double(float_unorder(uint32_t(sorted[i])));
+    double d = __dsub_rn(b, a);
+    if (d > 0.0) atomicMin(gap_bits + i / n, (unsigned long long)__double_as_longlong(d));
+}
+
+struct SfcParams {
+    double xmin, ymin, scale;
+    uint32_t side;  // 0 -> identity order (n == 1 or all points coincide)
+    uint32_t pad;
+};
+
+// ceil(log2(x)) for x >= 2 as a correctly rounded log2 followed by ceil
+__device__ int ceil_log2_cr(double x) {
+    int e = ilogb(x);
+    double m = scalbn(x, -e);  // exact, in [1, 2)
+    if (m == 1.0) return e;
+    double u = scalbn(1.0, ilogb(double(e)) - 52);  // ulp of e
+    return ((m - 1.0) * 1.4426950408889634 < 0.5 * u) ? e : e + 1;
+}
+
+__global__ void sfc_params_kernel(const uint64_t* __restrict__ sorted, int64_t batch, int64_t n,
+                                  const unsigned long long* __restrict__ gap_bits,
+                                  SfcParams* __restrict__ out) {
+    int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    SfcParams p{};
+    const uint64_t* xs = sorted + (b * 2) * n;
+    const uint64_t* ys = sorted + (b * 2 + 1) * n;
+    double xmin = float_unorder(uint32_t(xs[0])), xmax = float_unorder(uint32_t(xs[n - 1]));
+    double ymin = float_unorder(uint32_t(ys[0])), ymax = float_unorder(uint32_t(ys[n - 1]));
+    double ex = __dsub_rn(xmax, xmin), ey = __dsub_rn(ymax, ymin);
+    double extent = ex < ey ? ey : ex;
+    p.xmin = xmin;
+    p.ymin = ymin;
+    if (n == 1 || extent <= 0.0) {
+        p.side = 0;
+    } else {
+        unsigned long long gx = gap_bits[b * 2], gy = gap_bits[b * 2 + 1];
+        double dgx = gx == ~0ull ? 0.0 : __longlong_as_double((long long)gx);
+        double dgy = gy == ~0ull ? 0.0 : __longlong_as_double((long long)gy);
+        double spacing = dgx < dgy ? dgy : dgx;
+        if (spacing <= 0.0) spacing = extent;
+        double arg = __dadd_rn(__ddiv_rn(extent, spacing), 1.0);
+        if (2.0 > arg) arg = 2.0;
+        int bb = ceil_log2_cr(arg);
+        bb = bb < 1 ? 1 : (bb > 16 ? 16 : bb);
+        p.side = 1u << bb;
+        p.scale = __ddiv_rn(double(p.side - 1), extent);
+    }
+    out[b] = p;
+}
+
+__global__ void hilbert_keys_kernel(const float* __restrict__ coords, int64_t batch, int64_t n,
+                                    const SfcParams* __restrict__ prm, uint64_t* __restrict__ keys,
+                                    uint32_t* __restrict__ vals) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * n) return;
+    int64_t b = i / n;
+    const SfcParams p = prm[b];
+    uint64_t key = 0;
+    if (p.side) {
+        double x = coords[2 * i], y = coords[2 * i + 1];
+        uint32_t qx = uint32_t(llround(__dmul_rn(__dsub_rn(x, p.xmin), p.scale)));
+        uint32_t qy = uint32_t(llround(__dmul_rn(__dsub_rn(y, p.ymin), p.scale)));
+        key = hilbert(p.side, qx, qy);
+    }
+    keys[i] = (uint64_t(b) << 32) | key;
+    vals[i] = uint32_t(i - b * n);
+}
+
+// ------------------------------------------------ clusters + neighbours
+__global__ void perm_kernel(const uint32_t* __restrict__ sorted_vals, int64_t batch, ClusterShape cs,
+                            int32_t* __restrict__ perm, int32_t* __restrict__ cluster_of) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * cs.n) return;
+    int64_t b = i / cs.n;
+    int pos = int(i - b * cs.n);
+    int tok = int(sorted_vals[i]);
+    perm[i] = tok;
+    if (cluster_of) cluster_of[b * cs.n + tok] = cs.cluster_at(pos);
+}
+
+// centroid = (sequential member-order sum) * (1.0 / |c|)   (geometry.cpp:140-150)
+__global__ void centroid_kernel(const float* __restrict__ coords, const int32_t* __restrict__ perm,
+                                int64_t batch, ClusterShape cs, double2* __restrict__ cent) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * cs.c) return;
+    int64_t b = i / cs.c;
+    int k = int(i - b * cs.c);
+    const int32_t* pm = perm + b * cs.n + cs.off(k);
+    const float2* xy = reinterpret_cast<const float2*>(coords) + b * cs.n;
+    double sx = 0.0, sy = 0.0;
+    int len = cs.len(k);
+    for (int j = 0; j < len; ++j) {
+        float2 v = xy[pm[j]];
+        sx = __dadd_rn(sx, double(v.x));
+        sy = __dadd_rn(sy, double(v.y));
+    }
+    double inv = __ddiv_rn(1.0, double(len));
+    cent[i] = make_double2(__dmul_rn(sx, inv), __dmul_rn(sy, inv));
+}
+
+constexpr int kMaxGroups = 8;
+
+__device__ __forceinline__ bool pair_lt(double da, int ja, double db, int jb) {
+    return da < db || (!(db < da) && ja < jb);
+}
+
+// Merges per-lane sorted top-G lists into the warp's top-G (ascending (d, j)).
+template <int G>
+__device__ __forceinline__ void warp_topk(double (&d)[G], int (&j)[G], int g, double* outd, int* outj) {
+    int head = 0;
+    for (int r = 0; r < g; ++r) {
+        double bd = head < g ? d[head] : INFINITY;
+        int bj = head < g ? j[head] : INT32_MAX;
+        for (int o = 16; o > 0; o >>= 1) {
+            double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (pair_lt(od, oj, bd, bj)) {
+                bd = od;
+                bj = oj;
+            }
+        }
+        if (head < g && d[head] == bd && j[head] == bj) ++head;
+        outd[r] = bd;
+        outj[r] = bj;
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void topk_insert(double (&d)[G], int (&j)[G], int g, double nd, int nj) {
+    if (!pair_lt(nd, nj, d[g - 1], j[g - 1])) return;
+    int p = g - 1;
+    while (p > 0 && pair_lt(nd, nj, d[p - 1], j[p - 1])) {
+        d[p] = d[p - 1];
+        j[p] = j[p - 1];
+        --p;
+    }
+    d[p] = nd;
+    j[p] = nj;
+}
+
+// one warp per (image, cluster k): the G smallest (d^2, j) over all centroids,
+// then own cluster first (proj/src/geometry.cpp:157-172)
+__global__ void nbr_kernel(const double2* __restrict__ cent, int64_t batch, ClusterShape cs,
+                           int32_t* __restrict__ nbr_cl) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= batch * cs.c) return;
+    int64_t b = w / cs.c;
+    int k = int(w - b * cs.c);
+    const double2* cb = cent + b * cs.c;
+    const double2 ck = cb[k];
+    const int g = cs.g;
+    double d[kMaxGroups];
+    int jj[kMaxGroups];
+    for (int r = 0; r < kMaxGroups; ++r) {
+        d[r] = INFINITY;
+        jj[r] = INT32_MAX;
+    }
+    for (int j = lane; j < cs.c; j += 32) {
+        double2 cj = cb[j];
+        double dx = __dsub_rn(cj.x, ck.x), dy = __dsub_rn(cj.y, ck.y);
+        double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        topk_insert<kMaxGroups>(d, jj, g, d2, j);
+    }
+    double od[kMaxGroups];
+    int oj[kMaxGroups];
+    warp_topk<kMaxGroups>(d, jj, g, od, oj);
+    if (lane == 0) {
+        int32_t* sel = nbr_cl + w * g;
+        int ns = 0;
+        sel[ns++] = k;
+        for (int r = 0; r < g && ns < g; ++r)
+            if (oj[r] != k) sel[ns++] = oj[r];
+    }
+}
+
+// reverse-neighbour CSR: in-degree, per-image scan, fill, per-list sort
+__global__ void indeg_kernel(const int32_t* __restrict__ nbr_cl, int64_t batch, ClusterShape cs,
+                             int32_t* __restrict__ cnt) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * cs.c * cs.g) return;
+    int64_t b = i / (int64_t(cs.c) * cs.g);
+    atomicAdd(cnt + b * (cs.c + 1) + nbr_cl[i], 1);
+}
+
+__global__ void rev_scan_kernel(int32_t* __restrict__ cnt, ClusterShape cs) {
+    // one CTA per image: exclusive scan of cnt[0..C] in place (cnt[C] = total)
+    __shared__ int32_t part[1024];
+    int32_t* c = cnt + int64_t(blockIdx.x) * (cs.c + 1);
+    const int t = threadIdx.x, nt = blockDim.x, len = cs.c + 1;
+    const int per = (len + nt - 1) / nt, b = t * per, e = min(len, b + per);
+    int32_t s = 0;
+    for (int i = b; i < e; ++i) s += c[i];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < nt; o <<= 1) {
+        int32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - s;
+    for (int i = b; i < e; ++i) {
+        int32_t v = c[i];
+        c[i] = run;
+        run += v;
+    }
+}
+
+__global__ void rev_fill_kernel(const int32_t* __restrict__ nbr_cl, int64_t batch, ClusterShape cs,
+                                const int32_t* __restrict__ off, int32_t* __restrict__ cursor,
+                                int32_t* __restrict__ rev_cl) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * cs.c * cs.g) return;
+    const int64_t per = int64_t(cs.c) * cs.g;
+    int64_t b = i / per;
+    int k = int((i - b * per) / cs.g);
+    int t = nbr_cl[i];
+    int slot = atomicAdd(cursor + b * (cs.c + 1) + t, 1);
+    rev_cl[b * per + off[b * (cs.c + 1) + t] + slot] = k;
+}
+
+__global__ void rev_sort_kernel(const int32_t* __restrict__ off, int64_t batch, ClusterShape cs,
+                                int32_t* __restrict__ rev_cl) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * cs.c) return;
+    int64_t b = i / cs.c;
+    int c = int(i - b * cs.c);
+    const int32_t* o = off + b * (cs.c + 1);
+    int32_t* l = rev_cl + b * int64_t(cs.c) * cs.g;
+    for (int x = o[c] + 1; x < o[c + 1]; ++x) {
+        int v = l[x], y = x;
+        while (y > o[c] && l[y - 1] > v) {
+            l[y] = l[y - 1];
+            --y;
+        }
+        l[y] = v;
+    }
+}
+
+// ------------------------------------------------------ NeighborIndex expand
+__global__ void expand_rows_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ nbr_cl,
+                                   int64_t batch, ClusterShape cs, int32_t* __restrict__ idx,
+                                   uint8_t* __restrict__ valid) {
+    // one thread per (image, curve position, slot): the row of token perm[pos]
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int M = cs.width;
+    if (i >= batch * cs.n * M) return;
+    int64_t pp = i / M;
+    int s = int(i - pp * M);
+    int64_t b = pp / cs.n;
+    int pos = int(pp - b * cs.n);
+    int k = cs.cluster_at(pos);
+    const int32_t* nb = nbr_cl + (b * cs.c + k) * cs.g;
+    const int32_t* pm = perm + b * cs.n;
+    int start = 0, key = 0, ok = 0;
+    for (int g = 0; g < cs.g; ++g) {
+        int cl = nb[g], len = cs.len(cl);
+        if (s < start + len) {
+            key = pm[cs.off(cl) + s - start];
+            ok = 1;
+            break;
+        }
+        start += len;
+    }
+    int64_t row = b * cs.n + pm[pos];
+    idx[row * M + s] = key;
+    valid[row * M + s] = uint8_t(ok);
+}
+
+// ----------------------------------------------------------------- knn
+// one warp per query: per-lane sorted top-k over a strided key subset, then
+// a warp merge; (d^2 binary64, j) order (proj/src/geometry.cpp:196-214)
+constexpr int kKnnMax = 32;
+__global__ void knn_kernel(const float* __restrict__ queries, const float* __restrict__ keys,
+                           int64_t batch, int64_t nq, int64_t nk, int k, int32_t* __restrict__ idx,
+                           uint8_t* __restrict__ valid) {
+    const int lane = threadIdx.x & 31;
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= batch * nq) return;
+    int64_t b = w / nq;
+    const float2 q = reinterpret_cast<const float2*>(queries)[w];
+    const float2* kb = reinterpret_cast<const float2*>(keys) + b * nk;
+    const int kept = int(k < nk ? k : nk);
+    double d[kKnnMax];
+    int jj[kKnnMax];
+    for (int r = 0; r < kKnnMax; ++r) {
+        d[r] = INFINITY;
+        jj[r] = INT32_MAX;
+    }
+    for (int64_t j = lane; j < nk; j += 32) {
+        float2 p = kb[j];
+        double dx = __dsub_rn(double(p.x), double(q.x)), dy = __dsub_rn(double(p.y), double(q.y));
+        double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        topk_insert<kKnnMax>(d, jj, kept, d2, int(j));
+    }
+    double od[kKnnMax];
+    int oj[kKnnMax];
+    warp_topk<kKnnMax>(d, jj, kept, od, oj);
+    // every lane holds the merged list; lane s writes slot s (k <= 32)
+    int jv = 0;
+#pragma unroll
+    for (int t = 0; t < kKnnMax; ++t)
+        if (t == lane) jv = oj[t];
+    if (lane < k) {
+        idx[w * k + lane] = lane < kept ? jv : 0;
+        valid[w * k + lane] = lane < kept ? 1 : 0;
+    }
+}
+
+// ================================================================= host
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct IndexWs {
+    uint64_t* keys[2];
+    uint32_t* vals[2];
+    uint32_t* hist;
+    unsigned long long* gaps;
+    SfcParams* prm;
+    double2* cent;
+    int32_t* cursor;
+    size_t bytes;
+};
+
+static IndexWs carve(int64_t batch, int64_t n, int64_t c, void* base) {
+    IndexWs w{};
+    uint8_t* p = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p ? p + off : nullptr;
+        off += align256(bytes);
+        return r;
+    };
+    const size_t e = size_t(batch) * n * 2;  // x and y segments
+    w.keys[0] = reinterpret_cast<uint64_t*>(take(e * 8));
+    w.keys[1] = reinterpret_cast<uint64_t*>(take(e * 8));
+    w.vals[0] = reinterpret_cast<uint32_t*>(take(e * 4));
+    w.vals[1] = reinterpret_cast<uint32_t*>(take(e * 4));
+    w.hist = reinterpret_cast<uint32_t*>(take(radix_hist_elems(int64_t(e)) * 4));
+    w.gaps = reinterpret_cast<unsigned long long*>(take(size_t(batch) * 2 * 8));
+    w.prm = reinterpret_cast<SfcParams*>(take(size_t(batch) * sizeof(SfcParams)));
+    w.cent = reinterpret_cast<double2*>(take(size_t(batch) * c * sizeof(double2)));
+    w.cursor = reinterpret_cast<int32_t*>(take(size_t(batch) * (c + 1) * 4));
+    w.bytes = off;
+    return w;
+}
+
+static unsigned blocks(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+// sfc_order for the batch; leaves the sorted token ids in *sorted_vals
+static int sfc_core(const float* coords, int64_t batch, int64_t n, IndexWs& w, uint32_t** sorted_vals,
+                    cudaStream_t st) {
+    const int64_t e = batch * n * 2;
+    axis_keys_kernel<<<blocks(e), 256, 0, st>>>(coords, batch, n, w.keys[0]);
+    AFFMAE_LAUNCH_CHECK("axis_keys_kernel");
+    uint64_t* k = w.keys[0];
+    uint32_t* v = nullptr;
+    int rc = radix_sort(k, v, w.keys[1], nullptr, e, 32 + bits_for(batch * 2), w.hist, st);
+    if (rc) return rc;
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.gaps, 0xFF, size_t(batch) * 2 * 8, st));
+    gap_kernel<<<blocks(e), 256, 0, st>>>(k, batch * 2, n, w.gaps);
+    sfc_params_kernel<<<blocks(batch, 128), 128, 0, st>>>(k, batch, n, w.gaps, w.prm);
+    AFFMAE_LAUNCH_CHECK("sfc_params_kernel");
+    hilbert_keys_kernel<<<blocks(batch * n), 256, 0, st>>>(coords, batch, n, w.prm, w.keys[0], w.vals[0]);
+    AFFMAE_LAUNCH_CHECK("hilbert_keys_kernel");
+    k = w.keys[0];
+    v = w.vals[0];
+    rc = radix_sort(k, v, w.keys[1], w.vals[1], batch * n, 32 + bits_for(batch), w.hist, st);
+    if (rc) return rc;
+    *sorted_vals = v;
+    return AFFMAE_OK;
+}
+
+size_t cluster_index_workspace(const affmae_cluster_geom* g) {
+    if (!g || g->n_clusters <= 0) return 0;
+    return carve(g->batch, g->tokens, g->n_clusters, nullptr).bytes;
+}
+
+int cluster_index_build(const affmae_cluster_geom* g, const float* coords, affmae_cluster_index* out,
+                        void* workspace, size_t ws_bytes, void* stream) {
+    if (!g || g->n_clusters <= 0) return fail(AFFMAE_ECONFIG, "cluster_index: geometry not derived");
+    if (!coords || !out || !out->perm || !out->cluster_of || !out->nbr_cl || !out->rev_off || !out->rev_cl)
+        return fail(AFFMAE_ECONFIG, "cluster_index: null pointer");
+    if (g->groups_eff > kMaxGroups)
+        return fail(AFFMAE_EUNSUPPORTED, "cluster_index: groups > 8 not compiled");
+    if (g->tokens >= (int64_t(1) << 31)) return fail(AFFMAE_EUNSUPPORTED, "cluster_index: too many tokens");
+    IndexWs w = carve(g->batch, g->tokens, g->n_clusters, workspace);
+    if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "cluster_index: workspace too small");
+    if (g->batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    const ClusterShape cs = make_shape(*g);
+    const int64_t B = g->batch, n = g->tokens;
+    uint32_t* sv = nullptr;
+    int rc = sfc_core(coords, B, n, w, &sv, st);
+    if (rc) return rc;
+    perm_kernel<<<blocks(B * n), 256, 0, st>>>(sv, B, cs, out->perm, out->cluster_of);
+    centroid_kernel<<<blocks(B * cs.c), 256, 0, st>>>(coords, out->perm, B, cs, w.cent);
+    nbr_kernel<<<blocks(B * cs.c * 32), 256, 0, st>>>(w.cent, B, cs, out->nbr_cl);
+    AFFMAE_LAUNCH_CHECK("nbr_kernel");
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(out->rev_off, 0, size_t(B) * (cs.c + 1) * 4, st));
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.cursor, 0, size_t(B) * (cs.c + 1) * 4, st));
+    const int64_t pairs = B * cs.c * cs.g;
+    indeg_kernel<<<blocks(pairs), 256, 0, st>>>(out->nbr_cl, B, cs, out->rev_off);
+    rev_scan_kernel<<<unsigned(B), 1024, 0, st>>>(out->rev_off, cs);
+    rev_fill_kernel<<<blocks(pairs), 256, 0, st>>>(out->nbr_cl, B, cs, out->rev_off, w.cursor, out->rev_cl);
+    rev_sort_kernel<<<blocks(B * cs.c), 256, 0, st>>>(out->rev_off, B, cs, out->rev_cl);
+    AFFMAE_LAUNCH_CHECK("reverse CSR");
+    return AFFMAE_OK;
+}
+
+size_t sfc_order_workspace(int64_t batch, int64_t tokens) {
+    if (batch < 0 || tokens < 1) return 0;
+    return carve(batch, tokens, 1, nullptr).bytes;
+}
+
+int sfc_order(const float* coords, int64_t batch, int64_t n, int32_t* perm, void* workspace,
+              size_t ws_bytes, void* stream) {
+    if (n < 1) return fail(AFFMAE_ECONFIG, "sfc_order: empty point set");
+    if (!coords || !perm) return fail(AFFMAE_ECONFIG, "sfc_order: null pointer");
+    IndexWs w = carve(batch, n, 1, workspace);
+    if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "sfc_order: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    uint32_t* sv = nullptr;
+    int rc = sfc_core(coords, batch, n, w, &sv, st);
+    if (rc) return rc;
+    ClusterShape cs{};
+    cs.n = int32_t(n);
+    cs.c = 1;
+    cs.base = int32_t(n);
+    perm_kernel<<<blocks(batch * n), 256, 0, st>>>(sv, batch, cs, perm, nullptr);
+    AFFMAE_LAUNCH_CHECK("perm_kernel");
+    return AFFMAE_OK;
+}
+
+int neighbor_expand(const affmae_cluster_geom* g, const int32_t* perm, const int32_t* nbr_cl,
+                    int32_t* idx, uint8_t* valid, void* stream) {
+    if (!g || g->n_clusters <= 0) return fail(AFFMAE_ECONFIG, "neighbor_expand: geometry not derived");
+    if (!perm || !nbr_cl || !idx || !valid) return fail(AFFMAE_ECONFIG, "neighbor_expand: null pointer");
+    const ClusterShape cs = make_shape(*g);
+    const int64_t total = g->batch * g->tokens * g->width;
+    if (total == 0) return AFFMAE_OK;
+    expand_rows_kernel<<<blocks(total), 256, 0, as_stream(stream)>>>(perm, nbr_cl, g->batch, cs, idx, valid);
+    AFFMAE_LAUNCH_CHECK("expand_rows_kernel");
+    return AFFMAE_OK;
+}
+
+int knn(const float* queries, const float* keys, int64_t batch, int64_t nq, int64_t nk, int64_t k,
+        int32_t* idx, uint8_t* valid, void* stream) {
+    if (nk < 1) return fail(AFFMAE_ECONFIG, "knn: empty key set");
+    if (k < 1) return fail(AFFMAE_ECONFIG, "knn: k must be >= 1");
+    if (k > kKnnMax) return fail(AFFMAE_EUNSUPPORTED, "knn: k > 32 not compiled");
+    if (!queries || !keys || !idx || !valid) return fail(AFFMAE_ECONFIG, "knn: null pointer");
+    if (batch * nq == 0) return AFFMAE_OK;
+    knn_kernel<<<blocks(batch * nq * 32), 256, 0, as_stream(stream)>>>(queries, keys, batch, nq, nk,
+                                                                       int(k), idx, valid);
+    AFFMAE_LAUNCH_CHECK("knn_kernel");
+    return AFFMAE_OK;
+}
+
+}  // namespace affmae_b200

@@ -1,0 +1,238 @@
+"""Torch-facing wrappers of the C ABI (device-resident hot path).
+
+Every function here takes CUDA torch tensors, allocates outputs/workspace with
+torch, and launches through :mod:`paper_2602_16249_b200.capi` on the current
+torch stream.  No computation happens in Python or torch; if the CUDA library
+is absent the first call raises (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import capi
+
+BF16 = torch.bfloat16
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _req(t, dtype, name):
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+@dataclass
+class ClusterIndex:
+    """Device-resident cluster index (include/affmae_b200.h: affmae_cluster_index)."""
+    geom: capi.ClusterGeom
+    perm: torch.Tensor        # [B, N] int32
+    cluster_of: torch.Tensor  # [B, N] int32
+    nbr_cl: torch.Tensor      # [B, C, G] int32
+    rev_off: torch.Tensor     # [B, C+1] int32
+    rev_cl: torch.Tensor      # [B, C*G] int32
+
+    def c_struct(self):
+        return capi.ClusterIndex(*(capi.ptr(t) for t in (self.perm, self.cluster_of, self.nbr_cl,
+                                                          self.rev_off, self.rev_cl)))
+
+
+def geometry(batch, tokens, cluster, groups):
+    return capi.geometry(batch, tokens, cluster, groups)
+
+
+def empty_index(geom, device="cuda"):
+    B, N, Cn, G = geom.batch, geom.tokens, geom.n_clusters, geom.groups_eff
+    i32 = dict(dtype=torch.int32, device=device)
+    return ClusterIndex(geom, torch.empty((B, N), **i32), torch.empty((B, N), **i32),
+                        torch.empty((B, Cn, G), **i32), torch.empty((B, Cn + 1), **i32),
+                        torch.empty((B, Cn * G), **i32))
+
+
+@dataclass
+class BiasNet:
+    """BiasNet parameters (proj/include/affmae/attention.hpp:16-29) as fp32 device tensors."""
+    w1: torch.Tensor     # [h, 2H]
+    b1: torch.Tensor     # [h, H]
+    w2: torch.Tensor     # [h, H]
+    b2: torch.Tensor     # [h] or [h, 1]
+    blank: torch.Tensor  # [h] or [h, 1]
+    patch: float = 8.0
+
+    @property
+    def hidden(self):
+        return self.w1.shape[1] // 2
+
+    @staticmethod
+    def from_numpy(d, device="cuda", patch=8.0):
+        t = {k: torch.as_tensor(d[k], dtype=torch.float32, device=device).contiguous()
+             for k in ("w1", "b1", "w2", "b2", "blank")}
+        return BiasNet(patch=patch, **t)
+
+
+def _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim):
+    for t, n in ((q, "q"), (k, "k"), (v, "v"), (blank_k, "blank_k"), (blank_v, "blank_v")):
+        _req(t, BF16, n)
+    _req(coords, torch.float32, "coords")
+    for n in ("w1", "b1", "w2", "b2", "blank"):
+        _req(getattr(bias, n), torch.float32, f"bias.{n}")
+    desc = capi.AttnDesc(heads, head_dim, bias.hidden, float(bias.patch))
+    ins = capi.AttnInputs(*(capi.ptr(t) for t in (q, k, v, blank_k, blank_v, coords, bias.w1,
+                                                   bias.b1, bias.w2, bias.b2, bias.blank)))
+    return desc, ins
+
+
+def _workspace(nbytes, device):
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def attn_fwd(geom, q, k, v, blank_k, blank_v, coords, perm, nbr_cl, bias: BiasNet, heads,
+             head_dim, out=None, lse=None, workspace=None, stream=None):
+    """Cluster attention forward (nbhd_attn_streaming, proj/src/attention.cpp:199).
+    q/k/v [B, N, h*d] bf16 -> (out [B, N, h*d] bf16, lse [B, N, h] fp32)."""
+    desc, ins = _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim)
+    _req(perm, torch.int32, "perm")
+    _req(nbr_cl, torch.int32, "nbr_cl")
+    B, N = geom.batch, geom.tokens
+    if out is None:
+        out = torch.empty((B, N, heads * head_dim), dtype=BF16, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, N, heads), dtype=torch.float32, device=q.device)
+    L = capi.lib()
+    nbytes = L.affmae_attn_fwd_workspace(C.byref(geom), C.byref(desc))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = _workspace(nbytes, q.device)
+    capi.check(L.affmae_attn_fwd(C.byref(geom), C.byref(desc), C.byref(ins),
+                                 C.c_void_p(perm.data_ptr()), C.c_void_p(nbr_cl.data_ptr()),
+                                 C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),
+                                 C.c_void_p(workspace.data_ptr()), C.c_size_t(workspace.numel()),
+                                 _stream(stream)), "attn_fwd")
+    return out, lse
+
+
+@dataclass
+class AttnGrads:
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+    dblank_k: torch.Tensor
+    dblank_v: torch.Tensor
+    dw1: torch.Tensor
+    db1: torch.Tensor
+    dw2: torch.Tensor
+    db2: torch.Tensor
+    dblank: torch.Tensor
+
+    @staticmethod
+    def zeros_like(q, blank_k, bias: BiasNet):
+        f32 = dict(dtype=torch.float32, device=q.device)
+        h = bias.w1.shape[0]
+        return AttnGrads(torch.empty_like(q), torch.empty_like(q), torch.empty_like(q),
+                         torch.zeros(blank_k.shape, **f32), torch.zeros(blank_k.shape, **f32),
+                         torch.zeros(bias.w1.shape, **f32), torch.zeros(bias.b1.shape, **f32),
+                         torch.zeros(bias.w2.shape, **f32), torch.zeros(h, **f32),
+                         torch.zeros(h, **f32))
+
+
+def attn_bwd(geom, q, k, v, blank_k, blank_v, coords, index: ClusterIndex, bias: BiasNet, heads,
+             head_dim, out, lse, dout, grads: AttnGrads | None = None, workspace=None,
+             stream=None):
+    """Cluster attention backward (nbhd_attn_backward, proj/src/attention.cpp:241-358).
+    dq/dk/dv are overwritten; BiasNet and blank gradients accumulate (+=), like
+    CustomOp::backward (proj/include/affmae/tape.hpp:29-31)."""
+    desc, ins = _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim)
+    for t, n in ((out, "out"), (dout, "dout")):
+        _req(t, BF16, n)
+    _req(lse, torch.float32, "lse")
+    if grads is None:
+        grads = AttnGrads.zeros_like(q, blank_k, bias)
+    L = capi.lib()
+    nbytes = L.affmae_attn_bwd_workspace(C.byref(geom), C.byref(desc))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = _workspace(nbytes, q.device)
+    g = capi.AttnGrads(*(capi.ptr(getattr(grads, n)) for n in (
+        "dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")))
+    idx = index.c_struct()
+    capi.check(L.affmae_attn_bwd(C.byref(geom), C.byref(desc), C.byref(ins), C.byref(idx),
+                                 C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),
+                                 C.c_void_p(dout.data_ptr()), C.byref(g),
+                                 C.c_void_p(workspace.data_ptr()), C.c_size_t(workspace.numel()),
+                                 _stream(stream)), "attn_bwd")
+    return grads
+
+
+# --------------------------------------------------------------- index build
+def cluster_index(coords, cluster, groups, workspace=None, stream=None) -> ClusterIndex:
+    """balanced_clusters + cluster_neighborhood on device, batched
+    (proj/src/geometry.cpp:108-186).  coords [B, N, 2] fp32 -> ClusterIndex."""
+    _req(coords, torch.float32, "coords")
+    B, N, two = coords.shape
+    if two != 2:
+        raise ValueError("coords must be [B, N, 2]")
+    geom = geometry(B, N, cluster, groups)
+    idx = empty_index(geom, coords.device)
+    L = capi.lib()
+    nbytes = L.affmae_cluster_index_workspace(C.byref(geom))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = _workspace(nbytes, coords.device)
+    cs = idx.c_struct()
+    capi.check(L.affmae_cluster_index_build(C.byref(geom), C.c_void_p(coords.data_ptr()),
+                                            C.byref(cs), C.c_void_p(workspace.data_ptr()),
+                                            C.c_size_t(workspace.numel()), _stream(stream)),
+               "cluster_index_build")
+    return idx
+
+
+def neighbor_expand(index: ClusterIndex, stream=None):
+    """The reference's per-token NeighborIndex (idx [B, N, M] int32, valid uint8)."""
+    g = index.geom
+    idx = torch.empty((g.batch, g.tokens, g.width), dtype=torch.int32, device=index.perm.device)
+    valid = torch.empty((g.batch, g.tokens, g.width), dtype=torch.uint8, device=index.perm.device)
+    capi.check(capi.lib().affmae_neighbor_expand(C.byref(g), C.c_void_p(index.perm.data_ptr()),
+                                                 C.c_void_p(index.nbr_cl.data_ptr()),
+                                                 C.c_void_p(idx.data_ptr()),
+                                                 C.c_void_p(valid.data_ptr()), _stream(stream)),
+               "neighbor_expand")
+    return idx, valid
+
+
+def sfc_order(coords, stream=None):
+    """sfc_order (proj/src/geometry.cpp:69-106), batched: [B, N, 2] -> perm [B, N] int32."""
+    _req(coords, torch.float32, "coords")
+    B, N, _ = coords.shape
+    L = capi.lib()
+    nbytes = L.affmae_sfc_order_workspace(C.c_int64(B), C.c_int64(N))
+    ws = _workspace(nbytes, coords.device)
+    perm = torch.empty((B, N), dtype=torch.int32, device=coords.device)
+    capi.check(L.affmae_sfc_order(C.c_void_p(coords.data_ptr()), C.c_int64(B), C.c_int64(N),
+                                  C.c_void_p(perm.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                  C.c_size_t(ws.numel()), _stream(stream)), "sfc_order")
+    return perm
+
+
+def knn(queries, keys, k, stream=None):
+    """Exact brute-force KNN (proj/src/geometry.cpp:188-216), batched:
+    queries [B, Q, 2], keys [B, K, 2] -> (idx [B, Q, k] int32, valid [B, Q, k] uint8)."""
+    _req(queries, torch.float32, "queries")
+    _req(keys, torch.float32, "keys")
+    B, Q, _ = queries.shape
+    K = keys.shape[1]
+    idx = torch.empty((B, Q, k), dtype=torch.int32, device=queries.device)
+    valid = torch.empty((B, Q, k), dtype=torch.uint8, device=queries.device)
+    capi.check(capi.lib().affmae_knn(C.c_void_p(queries.data_ptr()), C.c_void_p(keys.data_ptr()),
+                                     C.c_int64(B), C.c_int64(Q), C.c_int64(K), C.c_int64(k),
+                                     C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()),
+                                     _stream(stream)), "knn")
+    return idx, valid
