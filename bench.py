@@ -1,0 +1,518 @@
+#!/usr/bin/env python3
+"""Benchmark of the AFFMAE hot path on B200 (driver contract: one JSON line).
+
+Workload = BASELINE.json configs[1], the standalone cluster-attention + KNN-merge
+op sweep, at its headline point: per GPU B images of a 256x256 patch grid with a
+75% Perlin mask (N = 16384 visible tokens per image, exact mask counts), D = 128
+(4 heads x 32), K = 48 neighbours (cluster 16 x groups 3), BiasNet hidden 8,
+merge d_s = 0.4, k_m = 8.  One step = the whole hot path over the batch:
+    cluster index build -> cluster attention fwd -> attention bwd ->
+    select_retained -> merge_plan -> merge pool fwd -> merge pool bwd
+(synthetic inputs; q/k/v/blanks ~ 0.5 N(0,1) bf16, dO ~ N(0,1), scores ~ U(0.1, 0.9);
+merge features = the attention output).  Inputs per step (q, k, v, dO: 4 x B x N x D
+bf16 = 537 MB at B = 32) exceed the 126 MB L2, so no flush is needed.
+
+value  device-resident tokens/s (all ranks' tokens / max-over-ranks device time)
+e2e    the same through the C ABI with HOST buffers: pinned H2D of every input and
+       D2H of every output inside the timed region.
+--impl reference  times the reference's own CPU implementation (oracle/_ref, the
+       unmodified reference C++ compiled by oracle/Makefile) on all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "cluster-attn tokens/s fwd+bwd"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=32, help="images per GPU")
+    ap.add_argument("--grid", type=int, default=256, help="patch grid side (75%% masked)")
+    ap.add_argument("--heads", type=int, default=4)
+    ap.add_argument("--head-dim", type=int, default=32)
+    ap.add_argument("--cluster", type=int, default=16)
+    ap.add_argument("--groups", type=int, default=3)
+    ap.add_argument("--hidden", type=int, default=8)
+    ap.add_argument("--d-s", type=float, default=0.4)
+    ap.add_argument("--k-m", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
+    return ap.parse_args()
+
+
+def workload_config(a, world):
+    return {"workload": "configs[1] op sweep point: cluster index + cluster attention fwd+bwd "
+                        "+ KNN merge (select, plan, pool fwd+bwd)",
+            "images_per_gpu": a.batch, "global_images": a.batch * world,
+            "grid": a.grid, "mask_ratio": 0.75, "tokens_per_image": None,
+            "dim": a.heads * a.head_dim, "heads": a.heads, "head_dim": a.head_dim,
+            "neighbours": a.cluster * a.groups, "cluster": a.cluster, "groups": a.groups,
+            "bias_hidden": a.hidden, "d_s": a.d_s, "k_m": a.k_m,
+            "l2": "inputs per step > 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{world} (images sharded, no data-path collective)"}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self._proc = None
+        self._thr = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self._proc = None
+            return
+        self._thr = threading.Thread(target=self._read, daemon=True)
+        self._thr.start()
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+        if self._thr is not None:
+            self._thr.join(timeout=2)
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i - 2] for s in self.samples for i in range(2, 6)
+                          if s[i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- workload
+def make_inputs(a, rank):
+    from paper_2602_16249_b200 import inputs
+    rng = np.random.default_rng(1234 + rank)
+    coords = inputs.lattice_batch(a.batch, a.grid, 0.75, 8, seed0=1000 + rank * a.batch)
+    B, N, _ = coords.shape
+    hd = a.heads * a.head_dim
+    host = dict(
+        coords=coords,
+        q=(0.5 * rng.standard_normal((B, N, hd))).astype(np.float32),
+        k=(0.5 * rng.standard_normal((B, N, hd))).astype(np.float32),
+        v=(0.5 * rng.standard_normal((B, N, hd))).astype(np.float32),
+        dout=rng.standard_normal((B, N, hd)).astype(np.float32),
+        bk=(0.5 * rng.standard_normal((a.heads, a.head_dim))).astype(np.float32),
+        bv=(0.5 * rng.standard_normal((a.heads, a.head_dim))).astype(np.float32),
+        scores=rng.uniform(0.1, 0.9, (B, N)).astype(np.float32),
+        bias=inputs.bias_params(a.heads, a.hidden, rng),
+    )
+    return host
+
+
+def algorithmic_bytes(a, N):
+    """Per-token algorithmic HBM bytes: what each op must read/write once."""
+    D, h = a.heads * a.head_dim, a.heads
+    return {
+        "attn_fwd": 8 * D + 4 * h + 8,         # q,k,v read + o write (bf16), lse write, coords
+        "attn_bwd": 14 * D + 4 * h + 8,        # q,k,v,dO read + dq,dk,dv write, lse, coords
+        "index": 8 + 4 + 4 + 4 * a.groups / a.cluster,  # coords in; perm, cluster_of, nbr ids out
+        "merge": 4 + 8 + 2 * D + 4 + a.d_s * (4 + 4 * D + 12 * a.k_m),  # fwd side
+    }
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(a, rank, world, dist):
+    import torch
+    from paper_2602_16249_b200 import ops
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    host = make_inputs(a, rank)
+    B, N, _ = host["coords"].shape
+    bf = torch.bfloat16
+
+    def to_dev(x, dt):
+        return torch.as_tensor(x, dtype=dt, device=dev).contiguous()
+
+    coords = to_dev(host["coords"], torch.float32)
+    q, k, v, dout = (to_dev(host[n], bf) for n in ("q", "k", "v", "dout"))
+    bk, bv = to_dev(host["bk"], bf), to_dev(host["bv"], bf)
+    scores = to_dev(host["scores"], torch.float32)
+    bias = ops.BiasNet.from_numpy(host["bias"], device=dev)
+    p_merge = torch.tensor([1.0], dtype=torch.float32, device=dev)
+    h, d = a.heads, a.head_dim
+    geom = ops.geometry(B, N, a.cluster, a.groups)
+    R = ops.retained_count(N, a.d_s)
+    dpooled = torch.randn((B, R, 2 * h * d), device=dev).to(bf)
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out_buf = torch.empty_like(q)
+    lse_buf = torch.empty((B, N, h), dtype=torch.float32, device=dev)
+    grads = ops.AttnGrads.zeros_like(q, bk, bias)
+
+    phases = ["index", "attn_fwd", "attn_bwd", "merge"]
+
+    def step(ev=None):
+        if ev:
+            ev[0].record()
+        idx = ops.cluster_index(coords, a.cluster, a.groups, workspace=ws)
+        if ev:
+            ev[1].record()
+        out, lse = ops.attn_fwd(geom, q, k, v, bk, bv, coords, idx.perm, idx.nbr_cl, bias, h, d,
+                                out=out_buf, lse=lse_buf, workspace=ws)
+        if ev:
+            ev[2].record()
+        ops.attn_bwd(geom, q, k, v, bk, bv, coords, idx, bias, h, d, out, lse, dout, grads=grads,
+                     workspace=ws)
+        if ev:
+            ev[3].record()
+        ret = ops.select_retained(scores, a.d_s)
+        plan = ops.merge_plan(coords, ret, a.k_m)
+        pooled = ops.merge_pool_fwd(out, scores, p_merge, plan)
+        dfe, dsc, dp = ops.merge_pool_bwd(out, scores, p_merge, plan, dpooled)
+        if ev:
+            ev[4].record()
+        return out, lse, grads, pooled, dfe, dsc, dp
+
+    # warm-up (also primes the caching allocator) + per-phase timing pass
+    for _ in range(max(1, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    n_ph = 5
+    phase_ms = {p: [] for p in phases}
+    for _ in range(3):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_ph)]
+        step(ev)
+        torch.cuda.synchronize()
+        for i, p in enumerate(phases):
+            phase_ms[p].append(ev[i].elapsed_time(ev[i + 1]))
+
+    # CUDA graph of one step (launch-bound small kernels), eager fallback
+    graph = None
+    launches = None
+    if not a.no_graph:
+        try:
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                step()
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            torch.cuda.synchronize()
+            launches = count_graph_kernels(graph)
+        except Exception as e:  # pragma: no cover - capture is best effort
+            print(f"[bench] CUDA graph capture failed ({e}); eager launches", file=sys.stderr)
+            graph = None
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
+    for _ in range(a.warmup):
+        run_step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        run_step()
+    e1.record()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    clocks.stop()
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    tokens_all = B * N * world
+    value = tokens_all / (ms_max * 1e-3)
+
+    # e2e through the C ABI with host buffers (pinned H2D + D2H inside the timed region)
+    e2e = run_e2e(a, host, dev, geom, h, d, ws, world, dist)
+
+    res = dict(value=value, ms=ms_max, phase_ms={p: float(np.median(v)) for p, v in phase_ms.items()},
+               clocks=clocks.summary(), e2e=e2e, N=N, B=B, launches=launches,
+               graph=graph is not None)
+    return res
+
+
+def count_graph_kernels(graph):
+    """Kernel nodes in the captured step (our launches; the step holds no torch compute)."""
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:  # pragma: no cover
+        try:
+            from cuda import cudart as rt
+        except ImportError:
+            return None
+    try:
+        g = graph.raw_cuda_graph()
+        err, nodes, n = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, n = rt.cudaGraphGetNodes(g, n)
+        kern = 0
+        for nd in nodes:
+            err, ty = rt.cudaGraphNodeGetType(nd)
+            if ty == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+                kern += 1
+        return kern
+    except Exception:
+        return None
+
+
+def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
+    import torch
+    from paper_2602_16249_b200 import ops
+    bf = torch.bfloat16
+    pin = {}
+    for n in ("q", "k", "v", "dout"):
+        pin[n] = torch.from_numpy(host[n]).to(bf).pin_memory()
+    pin["coords"] = torch.from_numpy(host["coords"]).pin_memory()
+    pin["scores"] = torch.from_numpy(host["scores"]).pin_memory()
+    B, N = pin["scores"].shape
+    R = ops.retained_count(N, a.d_s)
+    pin["dpooled"] = torch.randn((B, R, 2 * h * d)).to(bf).pin_memory()
+    small = {n: torch.from_numpy(host[n]).to(bf).pin_memory() for n in ("bk", "bv")}
+    hb = {n: torch.from_numpy(np.ascontiguousarray(host["bias"][n])).pin_memory()
+          for n in ("w1", "b1", "w2", "b2", "blank")}
+    hd_ = h * d
+    outs_h = dict(out=torch.empty((B, N, hd_), dtype=bf).pin_memory(),
+                  lse=torch.empty((B, N, h), dtype=torch.float32).pin_memory(),
+                  dq=torch.empty((B, N, hd_), dtype=bf).pin_memory(),
+                  dk=torch.empty((B, N, hd_), dtype=bf).pin_memory(),
+                  dv=torch.empty((B, N, hd_), dtype=bf).pin_memory(),
+                  pooled=torch.empty((B, R, 2 * hd_), dtype=bf).pin_memory(),
+                  dfeats=torch.empty((B, N, hd_), dtype=bf).pin_memory(),
+                  dscores=torch.empty((B, N), dtype=torch.float32).pin_memory())
+    h2d = sum(t.numel() * t.element_size() for t in list(pin.values()) + list(small.values())
+              + list(hb.values()))
+    d2h = sum(t.numel() * t.element_size() for t in outs_h.values())
+
+    def e2e_step():
+        dv_ = {n: t.to(dev, non_blocking=True) for n, t in pin.items()}
+        sm = {n: t.to(dev, non_blocking=True) for n, t in small.items()}
+        bias = ops.BiasNet(**{n: t.to(dev, non_blocking=True) for n, t in hb.items()})
+        p_merge = torch.ones(1, dtype=torch.float32, device=dev)
+        idx = ops.cluster_index(dv_["coords"], a.cluster, a.groups, workspace=ws)
+        out, lse = ops.attn_fwd(geom, dv_["q"], dv_["k"], dv_["v"], sm["bk"], sm["bv"], dv_["coords"],
+                                idx.perm, idx.nbr_cl, bias, h, d, workspace=ws)
+        g = ops.attn_bwd(geom, dv_["q"], dv_["k"], dv_["v"], sm["bk"], sm["bv"], dv_["coords"], idx,
+                         bias, h, d, out, lse, dv_["dout"], workspace=ws)
+        ret = ops.select_retained(dv_["scores"], a.d_s)
+        plan = ops.merge_plan(dv_["coords"], ret, a.k_m)
+        pooled = ops.merge_pool_fwd(out, dv_["scores"], p_merge, plan)
+        dfe, dsc, _ = ops.merge_pool_bwd(out, dv_["scores"], p_merge, plan, dv_["dpooled"])
+        for name, t in (("out", out), ("lse", lse), ("dq", g.dq), ("dk", g.dk), ("dv", g.dv),
+                        ("pooled", pooled), ("dfeats", dfe), ("dscores", dsc)):
+            outs_h[name].copy_(t, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.e2e_steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.e2e_steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": B * N * world / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms}
+
+
+# ------------------------------------------------------------- reference
+def ref_sample(a, images, threads):
+    """Times oracle/_ref (the unmodified reference, compiled) on `images` images."""
+    from oracle import ref
+    host = make_inputs(argparse.Namespace(**{**vars(a), "batch": images}), 0)
+    f64 = lambda x: np.asarray(x, np.float64)
+    t0 = time.perf_counter()
+    ref.hotpath_batch(images, threads, 15, host["coords"], f64(host["q"]), f64(host["k"]),
+                      f64(host["v"]), f64(host["dout"]), f64(host["scores"]), f64(host["bk"]),
+                      f64(host["bv"]), host["bias"], a.heads, a.head_dim, 8.0, a.cluster,
+                      a.groups, a.d_s, a.k_m, 1.0)
+    dt = time.perf_counter() - t0
+    n = host["coords"].shape[1]
+    return images * n / dt, dt, n
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(a):
+    from oracle import ref
+    if not ref.available():
+        return None
+    th = host_threads()
+    imgs = th  # one image per thread: ~3.5 s of single-core work each at N = 16384
+    val, dt, n = ref_sample(a, imgs, th)
+    return {"value": val, "unit": UNIT, "cores": th, "kind": "reference",
+            "sample": f"{imgs} images x {n} tokens (index + attn fwd+bwd + merge), "
+                      f"{th} std::threads, {dt:.1f} s wall"}
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the reference's CPU path on all host threads (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    th = host_threads()
+    for _ in range(a.warmup):
+        ref_sample(a, th, th)
+    vals, dts = [], []
+    n = None
+    for _ in range(a.steps):
+        v, dt, n = ref_sample(a, th, th)
+        vals.append(v)
+        dts.append(dt)
+    total_tokens = th * n * a.steps
+    value = total_tokens / sum(dts)
+    cfg = workload_config(a, 1)
+    cfg["tokens_per_image"] = n
+    cfg["images_per_gpu"] = th
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * sum(dts) / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "reference",
+                             "sample": f"{th} images x {n} tokens per step on {th} std::threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def load_traffic(kernel, cfg_key):
+    """dram bytes per token from a committed ncu --set full capture (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        e = t.get(cfg_key, {}).get(kernel)
+        return e
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    res = run_ours(a, rank, world, dist)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    N, B = res["N"], res["B"]
+    algo = algorithmic_bytes(a, N)
+    ph = res["phase_ms"]
+    dom = max(("attn_fwd", "attn_bwd"), key=lambda p: ph[p])
+    peak, peak_kind = load_peaks()
+    achieved = algo[dom] * B * N / (ph[dom] * 1e-3) / 1e9
+    cfg_key = f"B{B}_g{a.grid}_D{a.heads * a.head_dim}"
+    traffic = load_traffic(dom, cfg_key)
+    cfg = workload_config(a, world)
+    cfg["tokens_per_image"] = N
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": res["ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg,
+        "e2e": {k: v for k, v in res["e2e"].items() if k != "ms_per_step"},
+        "gpu_launches": (res["launches"] * a.steps) if res["launches"] else None,
+        "roofline": {"kernel": f"{dom} op (all kernels of the C-ABI call)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_token": algo[dom]},
+        "phase_ms": ph,
+        "clocks": res["clocks"],
+        "cuda_graph": res["graph"],
+    }
+    if not a.no_cpu_baseline and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(a)
+        except Exception as e:  # pragma: no cover
+            line["cpu_baseline"] = {"error": str(e)}
+    else:
+        line["cpu_baseline"] = None
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -172,6 +172,8 @@ typedef struct affmae_merge_plan {
     int32_t* pool_idx;  /* [B, R, k_m] contributor token indices, (dist, index) ascending */
     double* pool_dist;  /* [B, R, k_m] Euclidean distances (binary64, bit-exact) */
     int32_t* pool_cnt;  /* [B, R] valid entries per pool (<= k_m) */
+    int32_t* row_of;    /* [B, N]  output row a token feeds: retained -> its own row, pooled
+                                   dropped -> its pool's row, truncated dropped -> -1 */
 } affmae_merge_plan;
 
 size_t affmae_merge_plan_workspace(int64_t batch, int64_t tokens, int64_t retained);

@@ -58,7 +58,7 @@ class AttnGrads(C.Structure):
 
 
 class MergePlan(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("target", "pool_idx", "pool_dist", "pool_cnt")]
+    _fields_ = [(n, C.c_void_p) for n in ("target", "pool_idx", "pool_dist", "pool_cnt", "row_of")]
 
 
 _lib = None

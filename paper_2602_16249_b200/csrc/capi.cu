@@ -39,6 +39,19 @@ int sfc_order(const float*, int64_t, int64_t, int32_t*, void*, size_t, void*);
 int neighbor_expand(const affmae_cluster_geom*, const int32_t*, const int32_t*, int32_t*, uint8_t*,
                     void*);
 int knn(const float*, const float*, int64_t, int64_t, int64_t, int64_t, int32_t*, uint8_t*, void*);
+int64_t retained_count_impl(int64_t, double);
+size_t select_retained_workspace(int64_t, int64_t);
+int select_retained(const float*, int64_t, int64_t, double, int32_t*, void*, size_t, void*);
+size_t merge_plan_workspace(int64_t, int64_t, int64_t);
+int merge_plan_build(const float*, const int32_t*, int64_t, int64_t, int64_t, int, affmae_merge_plan*,
+                     void*, size_t, void*);
+int merge_pool_fwd(const affmae_bf16*, const float*, const float*, const int32_t*,
+                   const affmae_merge_plan*, int64_t, int64_t, int64_t, int64_t, int, affmae_bf16*,
+                   void*);
+size_t merge_pool_bwd_workspace(int64_t, int64_t);
+int merge_pool_bwd(const affmae_bf16*, const float*, const float*, const int32_t*,
+                   const affmae_merge_plan*, int64_t, int64_t, int64_t, int64_t, int,
+                   const affmae_bf16*, affmae_bf16*, float*, float*, void*, size_t, void*);
 
 }  // namespace affmae_b200
 
@@ -118,13 +131,50 @@ int affmae_knn(const float* queries, const float* keys, int64_t batch, int64_t n
 
 // retained_count (proj/src/merging.cpp:50-54)
 int64_t affmae_retained_count(int64_t n, double d_s) {
-    if (!(d_s > 0.0 && d_s <= 1.0)) {
-        fail(AFFMAE_ECONFIG, "retained_count: d_s must be in (0, 1]");
-        return -2;
-    }
-    int64_t k = int64_t(std::floor(d_s * double(n) + 0.5));
-    if (k > n) k = n;
-    return k < 1 ? 1 : k;
+    int64_t r = retained_count_impl(n, d_s);
+    if (r < 0) fail(AFFMAE_ECONFIG, "retained_count: d_s must be in (0, 1]");
+    return r;
+}
+
+size_t affmae_select_retained_workspace(int64_t batch, int64_t tokens) {
+    return select_retained_workspace(batch, tokens);
+}
+
+int affmae_select_retained(const float* scores, int64_t batch, int64_t tokens, double d_s,
+                           int32_t* retained, void* workspace, size_t workspace_bytes, void* stream) {
+    return select_retained(scores, batch, tokens, d_s, retained, workspace, workspace_bytes, stream);
+}
+
+size_t affmae_merge_plan_workspace(int64_t batch, int64_t tokens, int64_t retained) {
+    return merge_plan_workspace(batch, tokens, retained);
+}
+
+int affmae_merge_plan_build(const float* coords, const int32_t* retained, int64_t batch,
+                            int64_t tokens, int64_t n_retained, int k_m, affmae_merge_plan* plan,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+    return merge_plan_build(coords, retained, batch, tokens, n_retained, k_m, plan, workspace,
+                            workspace_bytes, stream);
+}
+
+int affmae_merge_pool_fwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
+                          const int32_t* retained, const affmae_merge_plan* plan, int64_t batch,
+                          int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
+                          affmae_bf16* out, void* stream) {
+    return merge_pool_fwd(feats, scores, p_merge, retained, plan, batch, tokens, n_retained, dim,
+                          k_m, out, stream);
+}
+
+size_t affmae_merge_pool_bwd_workspace(int64_t batch, int64_t n_retained) {
+    return merge_pool_bwd_workspace(batch, n_retained);
+}
+
+int affmae_merge_pool_bwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
+                          const int32_t* retained, const affmae_merge_plan* plan, int64_t batch,
+                          int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
+                          const affmae_bf16* dout, affmae_bf16* dfeats, float* dscores,
+                          float* dp, void* workspace, size_t workspace_bytes, void* stream) {
+    return merge_pool_bwd(feats, scores, p_merge, retained, plan, batch, tokens, n_retained, dim,
+                          k_m, dout, dfeats, dscores, dp, workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

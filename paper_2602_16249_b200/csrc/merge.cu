@@ -1,0 +1,627 @@
+// Adaptive KNN token merge, batched (proj/src/merging.cpp):
+//   retained_count / select_retained   merging.cpp:50-69   bit-exact
+//   merge_plan                         merging.cpp:71-116  bit-exact
+//   MergePoolOp forward / backward     merging.cpp:121-220 fp32 (values), exact indices
+//
+// select_retained: one stable radix sort of (image, descending-score key) with
+// the token index as payload reproduces std::stable_sort's "score desc, ties
+// to the lower index"; the first R of each image are flagged and compacted in
+// index order (ascending output).
+//
+// merge_plan: the reference scans all R retained tokens for every dropped
+// token (O(N R)).  Here the retained tokens of an image are bucketed in a
+// uniform grid (~1 per cell) and each dropped token searches rings of cells
+// around its own cell until the best (d^2, retained position) candidate is
+// provably optimal: strictly closer than every unsearched cell, with a safety
+// margin far above rounding.  d^2 is dx*dx + dy*dy in binary64 without FMA
+// contraction, ties go to the lowest retained position, exactly the
+// reference's first-minimum scan.  Pools collect (sqrt(d^2), j), are sorted
+// by (dist, index) and truncated to k_m.
+#include <cmath>
+
+#include "sort.cuh"
+
+namespace affmae_b200 {
+
+static unsigned blocks_of(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------- select_retained
+__global__ void score_keys_kernel(const float* __restrict__ scores, int64_t batch, int64_t n,
+                                  uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * n) return;
+    int64_t b = i / n;
+    keys[i] = (uint64_t(b) << 32) | uint32_t(~float_order(scores[i]));  // larger score first
+    vals[i] = uint32_t(i - b * n);
+}
+
+__global__ void keep_flags_kernel(const uint32_t* __restrict__ sorted_vals, int64_t batch, int64_t n,
+                                  int64_t r, uint8_t* __restrict__ keep) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * n) return;
+    int64_t b = i / n, pos = i - b * n;
+    keep[b * n + sorted_vals[i]] = pos < r ? 1 : 0;
+}
+
+// one CTA per image: ascending compaction of the kept flags
+__global__ void compact_kernel(const uint8_t* __restrict__ keep, int64_t n, int64_t r,
+                               int32_t* __restrict__ out) {
+    __shared__ int32_t part[1024];
+    const int t = threadIdx.x, nt = blockDim.x;
+    const uint8_t* k = keep + int64_t(blockIdx.x) * n;
+    const int64_t per = (n + nt - 1) / nt, b = t * per, e = (b + per < n) ? b + per : n;
+    int32_t s = 0;
+    for (int64_t i = b; i < e; ++i) s += k[i];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < nt; o <<= 1) {
+        int32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t pos = part[t] - s;
+    int32_t* o = out + int64_t(blockIdx.x) * r;
+    for (int64_t i = b; i < e; ++i)
+        if (k[i]) o[pos++] = int32_t(i);
+}
+
+// --------------------------------------------------------------- merge_plan
+struct GridPrm {
+    double x0, y0, w;  // origin and cell width
+};
+
+// per image bounding box -> grid of G x G cells (one CTA per image)
+__global__ void grid_prm_kernel(const float* __restrict__ coords, int64_t n, int g,
+                                GridPrm* __restrict__ prm) {
+    __shared__ float red[4][32];
+    const float2* xy = reinterpret_cast<const float2*>(coords) + int64_t(blockIdx.x) * n;
+    float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        float2 v = xy[i];
+        mnx = fminf(mnx, v.x);
+        mny = fminf(mny, v.y);
+        mxx = fmaxf(mxx, v.x);
+        mxy = fmaxf(mxy, v.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = mnx;
+        red[1][warp] = mny;
+        red[2][warp] = mxx;
+        red[3][warp] = mxy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w) {
+            mnx = fminf(mnx, red[0][w]);
+            mny = fminf(mny, red[1][w]);
+            mxx = fmaxf(mxx, red[2][w]);
+            mxy = fmaxf(mxy, red[3][w]);
+        }
+        double ext = fmax(double(mxx) - double(mnx), double(mxy) - double(mny));
+        GridPrm p;
+        p.x0 = mnx;
+        p.y0 = mny;
+        p.w = ext > 0.0 ? ext / g * (1.0 + 1e-9) : 1.0;
+        prm[blockIdx.x] = p;
+    }
+}
+
+__device__ __forceinline__ int cell_of(double v, double v0, double w, int g) {
+    int c = int(floor((v - v0) / w));
+    return c < 0 ? 0 : (c >= g ? g - 1 : c);
+}
+
+__global__ void mark_retained_kernel(const int32_t* __restrict__ retained, int64_t batch, int64_t n,
+                                     int64_t r, int32_t* __restrict__ ret_pos) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * r) return;
+    int64_t b = i / r;
+    ret_pos[b * n + retained[i]] = int32_t(i - b * r);
+}
+
+__global__ void cell_count_kernel(const float* __restrict__ coords, const int32_t* __restrict__ retained,
+                                  int64_t batch, int64_t n, int64_t r, int g,
+                                  const GridPrm* __restrict__ prm, int32_t* __restrict__ cnt) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * r) return;
+    int64_t b = i / r;
+    const GridPrm p = prm[b];
+    float2 v = reinterpret_cast<const float2*>(coords)[b * n + retained[i]];
+    int cx = cell_of(v.x, p.x0, p.w, g), cy = cell_of(v.y, p.y0, p.w, g);
+    atomicAdd(cnt + b * (int64_t(g) * g + 1) + cy * g + cx, 1);
+}
+
+// one CTA per segment: exclusive scan in place over len entries
+__global__ void seg_scan_kernel(int32_t* __restrict__ cnt, int64_t len) {
+    __shared__ int32_t part[1024];
+    int32_t* c = cnt + int64_t(blockIdx.x) * len;
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int64_t per = (len + nt - 1) / nt, b = t * per, e = (b + per < len) ? b + per : len;
+    int32_t s = 0;
+    for (int64_t i = b; i < e; ++i) s += c[i];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < nt; o <<= 1) {
+        int32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - s;
+    for (int64_t i = b; i < e; ++i) {
+        int32_t v = c[i];
+        c[i] = run;
+        run += v;
+    }
+}
+
+__global__ void cell_fill_kernel(const float* __restrict__ coords, const int32_t* __restrict__ retained,
+                                 int64_t batch, int64_t n, int64_t r, int g,
+                                 const GridPrm* __restrict__ prm, const int32_t* __restrict__ off,
+                                 int32_t* __restrict__ cursor, int32_t* __restrict__ items) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * r) return;
+    int64_t b = i / r;
+    const GridPrm p = prm[b];
+    float2 v = reinterpret_cast<const float2*>(coords)[b * n + retained[i]];
+    int cx = cell_of(v.x, p.x0, p.w, g), cy = cell_of(v.y, p.y0, p.w, g);
+    int64_t cell = b * (int64_t(g) * g + 1) + cy * g + cx;
+    int slot = atomicAdd(cursor + cell, 1);
+    items[b * r + off[cell] + slot] = int32_t(i - b * r);
+}
+
+__device__ __forceinline__ bool better(double d, int ri, double bd, int bri) {
+    return bri < 0 || d < bd || (d == bd && ri < bri);
+}
+
+// exact nearest retained token of every dropped token (first-minimum rule)
+__global__ void assign_kernel(const float* __restrict__ coords, const int32_t* __restrict__ retained,
+                              const int32_t* __restrict__ ret_pos, int64_t batch, int64_t n, int64_t r,
+                              int g, const GridPrm* __restrict__ prm, const int32_t* __restrict__ off,
+                              const int32_t* __restrict__ items, int32_t* __restrict__ target,
+                              int32_t* __restrict__ best_of, double* __restrict__ d2_of,
+                              int32_t* __restrict__ pool_cnt_all) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * n) return;
+    int64_t b = i / n;
+    if (ret_pos[i] >= 0) {
+        target[i] = -1;
+        best_of[i] = -1;
+        return;
+    }
+    const GridPrm p = prm[b];
+    const float2* xy = reinterpret_cast<const float2*>(coords) + b * n;
+    const int32_t* ret = retained + b * r;
+    const int32_t* co = off + b * (int64_t(g) * g + 1);
+    const int32_t* it = items + b * r;
+    const float2 q = xy[i - b * n];
+    const double qx = q.x, qy = q.y;
+    const int qcx = cell_of(qx, p.x0, p.w, g), qcy = cell_of(qy, p.y0, p.w, g);
+    double bd = 0.0;
+    int bri = -1;
+    for (int ring = 0; ring <= g; ++ring) {
+        const int x0 = qcx - ring, x1 = qcx + ring, y0 = qcy - ring, y1 = qcy + ring;
+        auto visit = [&](int cx, int cy) {
+            const int cell = cy * g + cx;
+            for (int t = co[cell]; t < co[cell + 1]; ++t) {
+                const int ri = it[t];
+                const float2 v = xy[ret[ri]];
+                const double dx = __dsub_rn(double(v.x), qx), dy = __dsub_rn(double(v.y), qy);
+                const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+                if (better(d2, ri, bd, bri)) {
+                    bd = d2;
+                    bri = ri;
+                }
+            }
+        };
+        // perimeter of the (2 ring + 1)^2 block, clipped to the grid
+        for (int cy = max(y0, 0); cy <= min(y1, g - 1); ++cy) {
+            if (cy == y0 || cy == y1) {
+                for (int cx = max(x0, 0); cx <= min(x1, g - 1); ++cx) visit(cx, cy);
+            } else {
+                if (x0 >= 0) visit(x0, cy);
+                if (x1 <= g - 1 && x1 != x0) visit(x1, cy);
+            }
+        }
+        if (bri >= 0) {
+            // distance from q to the outside of the searched (2 ring + 1)^2 block
+            double lb = INFINITY;
+            if (x0 > 0) lb = fmin(lb, qx - (p.x0 + x0 * p.w));
+            if (x1 < g - 1) lb = fmin(lb, p.x0 + (x1 + 1) * p.w - qx);
+            if (y0 > 0) lb = fmin(lb, qy - (p.y0 + y0 * p.w));
+            if (y1 < g - 1) lb = fmin(lb, p.y0 + (y1 + 1) * p.w - qy);
+            if (lb == INFINITY) break;  // whole grid searched
+            lb -= 1e-6 * p.w;
+            if (lb > 0.0 && bd < lb * lb) break;
+        }
+    }
+    target[i] = ret[bri];
+    best_of[i] = bri;
+    d2_of[i] = bd;
+    atomicAdd(pool_cnt_all + b * (r + 1) + bri, 1);
+}
+
+__global__ void pool_fill_kernel(const int32_t* __restrict__ best_of, const double* __restrict__ d2_of,
+                                 int64_t batch, int64_t n, int64_t r, const int32_t* __restrict__ off,
+                                 int32_t* __restrict__ cursor, double* __restrict__ ldist,
+                                 int32_t* __restrict__ lidx) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * n) return;
+    int ri = best_of[i];
+    if (ri < 0) return;
+    int64_t b = i / n;
+    int64_t seg = b * (r + 1) + ri;
+    int slot = atomicAdd(cursor + seg, 1);
+    int64_t pos = b * n + off[seg] + slot;
+    ldist[pos] = __dsqrt_rn(d2_of[i]);
+    lidx[pos] = int32_t(i - b * n);
+}
+
+// per retained token: sort its list by (dist, index), keep k_m
+__global__ void pool_sort_kernel(const int32_t* __restrict__ off, int64_t batch, int64_t n, int64_t r,
+                                 int k_m, double* __restrict__ ldist, int32_t* __restrict__ lidx,
+                                 int32_t* __restrict__ pool_idx, double* __restrict__ pool_dist,
+                                 int32_t* __restrict__ pool_cnt, int32_t* __restrict__ row_of,
+                                 const int32_t* __restrict__ retained) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * r) return;
+    int64_t b = i / r;
+    int ri = int(i - b * r);
+    const int32_t* o = off + b * (r + 1);
+    double* ld = ldist + b * n;
+    int32_t* li = lidx + b * n;
+    const int s = o[ri], e = o[ri + 1];
+    for (int x = s + 1; x < e; ++x) {
+        double dv = ld[x];
+        int iv = li[x], y = x;
+        while (y > s && (ld[y - 1] > dv || (ld[y - 1] == dv && li[y - 1] > iv))) {
+            ld[y] = ld[y - 1];
+            li[y] = li[y - 1];
+            --y;
+        }
+        ld[y] = dv;
+        li[y] = iv;
+    }
+    const int keep = min(e - s, k_m);
+    pool_cnt[i] = keep;
+    for (int t = 0; t < k_m; ++t) {
+        pool_idx[i * k_m + t] = t < keep ? li[s + t] : -1;
+        pool_dist[i * k_m + t] = t < keep ? ld[s + t] : 0.0;
+    }
+    row_of[b * n + retained[i]] = ri;
+    for (int t = 0; t < e - s; ++t) row_of[b * n + li[s + t]] = t < keep ? ri : -1;
+}
+
+// ---------------------------------------------------- pool forward/backward
+// pool weights of one retained row: softmax(-p * dist) over its pool
+__device__ __forceinline__ int pool_weights(const double* dist, int cnt, float p, float* w) {
+    float m = -INFINITY;
+    for (int t = 0; t < cnt; ++t) m = fmaxf(m, -p * float(dist[t]));
+    float l = 0.f;
+    for (int t = 0; t < cnt; ++t) {
+        w[t] = __expf(-p * float(dist[t]) - m);
+        l += w[t];
+    }
+    const float il = 1.f / l;
+    for (int t = 0; t < cnt; ++t) w[t] *= il;
+    return cnt;
+}
+
+constexpr int kMaxKm = 16;
+
+// one warp per retained row: out = [f_r ; sum_t w_t s_j f_j]   (merging.cpp:121-149)
+__global__ void pool_fwd_kernel(const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores,
+                                const float* __restrict__ p_merge, const int32_t* __restrict__ retained,
+                                const int32_t* __restrict__ pool_idx, const double* __restrict__ pool_dist,
+                                const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n, int64_t r,
+                                int dim, int k_m, __nv_bfloat16* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (row >= batch * r) return;
+    int64_t b = row / r;
+    const float p = *p_merge;
+    const int cnt = pool_cnt[row];
+    float w[kMaxKm];
+    pool_weights(pool_dist + row * k_m, cnt, p, w);
+    const __nv_bfloat16* fb = feats + b * n * dim;
+    const int32_t* pi = pool_idx + row * k_m;
+    __nv_bfloat16* o = out + row * 2 * dim;
+    const __nv_bfloat16* fr = fb + int64_t(retained[row]) * dim;
+    for (int c = lane * 2; c < dim; c += 64) {
+        *reinterpret_cast<__nv_bfloat162*>(o + c) = *reinterpret_cast<const __nv_bfloat162*>(fr + c);
+        float a0 = 0.f, a1 = 0.f;
+        for (int t = 0; t < cnt; ++t) {
+            const int j = pi[t];
+            const float g = w[t] * scores[b * n + j];
+            float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(fb + int64_t(j) * dim + c));
+            a0 = fmaf(g, f.x, a0);
+            a1 = fmaf(g, f.y, a1);
+        }
+        *reinterpret_cast<__nv_bfloat162*>(o + dim + c) = __floats2bfloat162_rn(a0, a1);
+    }
+}
+
+// one warp per retained row (MergePoolOp::backward, merging.cpp:169-219):
+//   df[r] = g_left;  df[j] = g_right w_t s_j;  ds[j] = w_t <g_right, f_j>;
+//   dp += sum_t w_t (dw_t - sum w dw) (-dist_t),  dw_t = s_j <g_right, f_j>
+__global__ void pool_bwd_kernel(const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores,
+                                const float* __restrict__ p_merge, const int32_t* __restrict__ retained,
+                                const int32_t* __restrict__ pool_idx, const double* __restrict__ pool_dist,
+                                const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n, int64_t r,
+                                int dim, int k_m, const __nv_bfloat16* __restrict__ dout,
+                                __nv_bfloat16* __restrict__ dfeats, float* __restrict__ dscores,
+                                float* __restrict__ dp_part) {
+    const int lane = threadIdx.x & 31;
+    int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    float dp = 0.f;
+    if (row < batch * r) {
+        int64_t b = row / r;
+        const float p = *p_merge;
+        const int cnt = pool_cnt[row];
+        const double* dist = pool_dist + row * k_m;
+        float w[kMaxKm];
+        pool_weights(dist, cnt, p, w);
+        const __nv_bfloat16* fb = feats + b * n * dim;
+        const __nv_bfloat16* g = dout + row * 2 * dim;
+        const int32_t* pi = pool_idx + row * k_m;
+        __nv_bfloat16* dfb = dfeats + b * n * dim;
+        const int64_t rtok = retained[row];
+        for (int c = lane * 2; c < dim; c += 64)
+            *reinterpret_cast<__nv_bfloat162*>(dfb + rtok * dim + c) =
+                *reinterpret_cast<const __nv_bfloat162*>(g + c);
+        if (lane == 0) dscores[b * n + rtok] = 0.f;
+        float dw[kMaxKm];
+        float wdot = 0.f;
+        for (int t = 0; t < cnt; ++t) {
+            const int64_t j = pi[t];
+            const float sj = scores[b * n + j];
+            float dot = 0.f;
+            for (int c = lane * 2; c < dim; c += 64) {
+                float2 go = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g + dim + c));
+                float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(fb + j * dim + c));
+                dot = fmaf(go.x, f.x, fmaf(go.y, f.y, dot));
+                const float k = w[t] * sj;
+                *reinterpret_cast<__nv_bfloat162*>(dfb + j * dim + c) = __floats2bfloat162_rn(go.x * k, go.y * k);
+            }
+            dot = warp_sum(dot);
+            if (lane == 0) dscores[b * n + j] = w[t] * dot;
+            dw[t] = sj * dot;
+            wdot = fmaf(w[t], dw[t], wdot);
+        }
+        for (int t = 0; t < cnt; ++t) dp = fmaf(w[t] * (dw[t] - wdot), -float(dist[t]), dp);
+    }
+    // block partial of dp (deterministic order inside the block)
+    __shared__ float red[32];
+    const int warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = dp;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.f;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+        dp_part[blockIdx.x] = s;
+    }
+}
+
+// tokens that feed no output row (truncated pool members) get zero gradient
+__global__ void pool_bwd_zero_kernel(const int32_t* __restrict__ row_of, int64_t total, int dim,
+                                     __nv_bfloat16* __restrict__ dfeats, float* __restrict__ dscores) {
+    const int lane = threadIdx.x & 31;
+    int64_t tok = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (tok >= total || row_of[tok] >= 0) return;
+    for (int c = lane * 2; c < dim; c += 64)
+        *reinterpret_cast<__nv_bfloat162*>(dfeats + tok * dim + c) = __floats2bfloat162_rn(0.f, 0.f);
+    if (lane == 0) dscores[tok] = 0.f;
+}
+
+// dp += sum of block partials (fixed order, single thread)
+__global__ void dp_reduce_kernel(const float* __restrict__ part, int nparts, float* __restrict__ dp) {
+    float s = 0.f;
+    for (int i = 0; i < nparts; ++i) s += part[i];
+    *dp += s;
+}
+
+// ===================================================================== host
+struct SelWs {
+    uint64_t* keys[2];
+    uint32_t* vals[2];
+    uint32_t* hist;
+    uint8_t* keep;
+    size_t bytes;
+};
+static SelWs carve_sel(int64_t batch, int64_t n, void* base) {
+    SelWs w{};
+    uint8_t* p = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* q = p ? p + off : nullptr;
+        off += al256(bytes);
+        return q;
+    };
+    const size_t e = size_t(batch) * n;
+    w.keys[0] = reinterpret_cast<uint64_t*>(take(e * 8));
+    w.keys[1] = reinterpret_cast<uint64_t*>(take(e * 8));
+    w.vals[0] = reinterpret_cast<uint32_t*>(take(e * 4));
+    w.vals[1] = reinterpret_cast<uint32_t*>(take(e * 4));
+    w.hist = reinterpret_cast<uint32_t*>(take(radix_hist_elems(int64_t(e)) * 4));
+    w.keep = reinterpret_cast<uint8_t*>(take(e));
+    w.bytes = off;
+    return w;
+}
+
+int64_t retained_count_impl(int64_t n, double d_s) {
+    if (!(d_s > 0.0 && d_s <= 1.0)) return -2;
+    int64_t k = int64_t(std::floor(d_s * double(n) + 0.5));
+    if (k > n) k = n;
+    return k < 1 ? 1 : k;
+}
+
+size_t select_retained_workspace(int64_t batch, int64_t n) {
+    if (batch < 0 || n < 1) return 0;
+    return carve_sel(batch, n, nullptr).bytes;
+}
+
+int select_retained(const float* scores, int64_t batch, int64_t n, double d_s, int32_t* retained,
+                    void* workspace, size_t ws_bytes, void* stream) {
+    const int64_t r = retained_count_impl(n, d_s);
+    if (r < 0) return fail(AFFMAE_ECONFIG, "retained_count: d_s must be in (0, 1]");
+    if (n < 1) return fail(AFFMAE_ECONFIG, "select_retained: empty score set");
+    if (!scores || !retained) return fail(AFFMAE_ECONFIG, "select_retained: null pointer");
+    SelWs w = carve_sel(batch, n, workspace);
+    if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "select_retained: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    score_keys_kernel<<<blocks_of(batch * n), 256, 0, st>>>(scores, batch, n, w.keys[0], w.vals[0]);
+    uint64_t* k = w.keys[0];
+    uint32_t* v = w.vals[0];
+    int rc = radix_sort(k, v, w.keys[1], w.vals[1], batch * n, 32 + bits_for(batch), w.hist, st);
+    if (rc) return rc;
+    keep_flags_kernel<<<blocks_of(batch * n), 256, 0, st>>>(v, batch, n, r, w.keep);
+    compact_kernel<<<unsigned(batch), 1024, 0, st>>>(w.keep, n, r, retained);
+    AFFMAE_LAUNCH_CHECK("select_retained");
+    return AFFMAE_OK;
+}
+
+struct PlanWs {
+    GridPrm* prm;
+    int32_t* ret_pos;
+    int32_t* cell_off;
+    int32_t* cell_cur;
+    int32_t* items;
+    int32_t* best_of;
+    double* d2_of;
+    int32_t* pool_off;
+    int32_t* pool_cur;
+    double* ldist;
+    int32_t* lidx;
+    size_t bytes;
+};
+
+static int grid_side(int64_t r) {
+    int g = int(std::ceil(std::sqrt(double(r))));
+    return g < 1 ? 1 : g;
+}
+
+static PlanWs carve_plan(int64_t batch, int64_t n, int64_t r, void* base) {
+    PlanWs w{};
+    uint8_t* p = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* q = p ? p + off : nullptr;
+        off += al256(bytes);
+        return q;
+    };
+    const int64_t g = grid_side(r);
+    const size_t cells = size_t(batch) * (g * g + 1);
+    w.prm = reinterpret_cast<GridPrm*>(take(size_t(batch) * sizeof(GridPrm)));
+    w.ret_pos = reinterpret_cast<int32_t*>(take(size_t(batch) * n * 4));
+    w.cell_off = reinterpret_cast<int32_t*>(take(cells * 4));
+    w.cell_cur = reinterpret_cast<int32_t*>(take(cells * 4));
+    w.items = reinterpret_cast<int32_t*>(take(size_t(batch) * r * 4));
+    w.best_of = reinterpret_cast<int32_t*>(take(size_t(batch) * n * 4));
+    w.d2_of = reinterpret_cast<double*>(take(size_t(batch) * n * 8));
+    w.pool_off = reinterpret_cast<int32_t*>(take(size_t(batch) * (r + 1) * 4));
+    w.pool_cur = reinterpret_cast<int32_t*>(take(size_t(batch) * (r + 1) * 4));
+    w.ldist = reinterpret_cast<double*>(take(size_t(batch) * n * 8));
+    w.lidx = reinterpret_cast<int32_t*>(take(size_t(batch) * n * 4));
+    w.bytes = off;
+    return w;
+}
+
+size_t merge_plan_workspace(int64_t batch, int64_t n, int64_t r) {
+    if (batch < 0 || n < 1 || r < 1) return 0;
+    return carve_plan(batch, n, r, nullptr).bytes;
+}
+
+int merge_plan_build(const float* coords, const int32_t* retained, int64_t batch, int64_t n, int64_t r,
+                     int k_m, affmae_merge_plan* plan, void* workspace, size_t ws_bytes, void* stream) {
+    if (r < 1) return fail(AFFMAE_ECONFIG, "merge_plan: retained set empty");
+    if (k_m < 1) return fail(AFFMAE_ECONFIG, "merge_plan: k_m must be >= 1");
+    if (k_m > kMaxKm) return fail(AFFMAE_EUNSUPPORTED, "merge_plan: k_m > 16 not compiled");
+    if (r > n) return fail(AFFMAE_ECONFIG, "merge_plan: more retained than tokens");
+    if (!coords || !retained || !plan || !plan->target || !plan->pool_idx || !plan->pool_dist ||
+        !plan->pool_cnt || !plan->row_of)
+        return fail(AFFMAE_ECONFIG, "merge_plan: null pointer");
+    PlanWs w = carve_plan(batch, n, r, workspace);
+    if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "merge_plan: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    const int g = grid_side(r);
+    const int64_t cells = int64_t(g) * g + 1;
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.ret_pos, 0xFF, size_t(batch) * n * 4, st));
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.cell_off, 0, size_t(batch) * cells * 4, st));
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.cell_cur, 0, size_t(batch) * cells * 4, st));
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.pool_off, 0, size_t(batch) * (r + 1) * 4, st));
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.pool_cur, 0, size_t(batch) * (r + 1) * 4, st));
+    grid_prm_kernel<<<unsigned(batch), 256, 0, st>>>(coords, n, g, w.prm);
+    mark_retained_kernel<<<blocks_of(batch * r), 256, 0, st>>>(retained, batch, n, r, w.ret_pos);
+    cell_count_kernel<<<blocks_of(batch * r), 256, 0, st>>>(coords, retained, batch, n, r, g, w.prm, w.cell_off);
+    seg_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(w.cell_off, cells);
+    cell_fill_kernel<<<blocks_of(batch * r), 256, 0, st>>>(coords, retained, batch, n, r, g, w.prm,
+                                                           w.cell_off, w.cell_cur, w.items);
+    assign_kernel<<<blocks_of(batch * n, 128), 128, 0, st>>>(coords, retained, w.ret_pos, batch, n, r, g, w.prm,
+                                                        w.cell_off, w.items, plan->target, w.best_of,
+                                                        w.d2_of, w.pool_off);
+    seg_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(w.pool_off, r + 1);
+    pool_fill_kernel<<<blocks_of(batch * n), 256, 0, st>>>(w.best_of, w.d2_of, batch, n, r, w.pool_off,
+                                                           w.pool_cur, w.ldist, w.lidx);
+    pool_sort_kernel<<<blocks_of(batch * r, 128), 128, 0, st>>>(w.pool_off, batch, n, r, k_m, w.ldist, w.lidx,
+                                                           plan->pool_idx, plan->pool_dist,
+                                                           plan->pool_cnt, plan->row_of, retained);
+    AFFMAE_LAUNCH_CHECK("merge_plan");
+    return AFFMAE_OK;
+}
+
+int merge_pool_fwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
+                   const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
+                   int64_t r, int64_t dim, int k_m, affmae_bf16* out, void* stream) {
+    if (!feats || !scores || !p_merge || !retained || !plan || !out)
+        return fail(AFFMAE_ECONFIG, "merge_pool: null pointer");
+    if (dim < 2 || dim % 2) return fail(AFFMAE_EUNSUPPORTED, "merge_pool: dim must be even");
+    if (k_m < 1 || k_m > kMaxKm) return fail(AFFMAE_EUNSUPPORTED, "merge_pool: k_m must be in [1, 16]");
+    if (batch * r == 0) return AFFMAE_OK;
+    pool_fwd_kernel<<<blocks_of(batch * r * 32), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const __nv_bfloat16*>(feats), scores, p_merge, retained, plan->pool_idx,
+        plan->pool_dist, plan->pool_cnt, batch, n, r, int(dim), k_m, reinterpret_cast<__nv_bfloat16*>(out));
+    AFFMAE_LAUNCH_CHECK("pool_fwd_kernel");
+    return AFFMAE_OK;
+}
+
+size_t merge_pool_bwd_workspace(int64_t batch, int64_t r) {
+    return al256(size_t(blocks_of(batch * r * 32)) * 4 + 4);
+}
+
+int merge_pool_bwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
+                   const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
+                   int64_t r, int64_t dim, int k_m, const affmae_bf16* dout, affmae_bf16* dfeats,
+                   float* dscores, float* dp, void* workspace, size_t ws_bytes, void* stream) {
+    if (!feats || !scores || !p_merge || !retained || !plan || !dout || !dfeats || !dscores || !dp)
+        return fail(AFFMAE_ECONFIG, "merge_pool bwd: null pointer");
+    if (dim < 2 || dim % 2) return fail(AFFMAE_EUNSUPPORTED, "merge_pool: dim must be even");
+    if (k_m < 1 || k_m > kMaxKm) return fail(AFFMAE_EUNSUPPORTED, "merge_pool: k_m must be in [1, 16]");
+    if (!workspace || ws_bytes < merge_pool_bwd_workspace(batch, r))
+        return fail(AFFMAE_ECONFIG, "merge_pool bwd: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    const unsigned nb = blocks_of(batch * r * 32);
+    float* part = static_cast<float*>(workspace);
+    pool_bwd_zero_kernel<<<blocks_of(batch * n * 32), 256, 0, st>>>(
+        plan->row_of, batch * n, int(dim), reinterpret_cast<__nv_bfloat16*>(dfeats), dscores);
+    pool_bwd_kernel<<<nb, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(feats), scores, p_merge,
+                                        retained, plan->pool_idx, plan->pool_dist, plan->pool_cnt, batch,
+                                        n, r, int(dim), k_m, reinterpret_cast<const __nv_bfloat16*>(dout),
+                                        reinterpret_cast<__nv_bfloat16*>(dfeats), dscores, part);
+    dp_reduce_kernel<<<1, 1, 0, st>>>(part, int(nb), dp);
+    AFFMAE_LAUNCH_CHECK("pool_bwd_kernel");
+    return AFFMAE_OK;
+}
+
+}  // namespace affmae_b200

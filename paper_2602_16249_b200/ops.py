@@ -236,3 +236,115 @@ def knn(queries, keys, k, stream=None):
                                      C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()),
                                      _stream(stream)), "knn")
     return idx, valid
+
+
+# -------------------------------------------------------------------- merge
+def retained_count(n, d_s):
+    """retained_count (proj/src/merging.cpp:50-54): clamp(floor(d_s*n + 0.5), 1, n)."""
+    r = capi.lib().affmae_retained_count(n, d_s)
+    if r < 0:
+        raise ValueError("retained_count: d_s must be in (0, 1]")
+    return int(r)
+
+
+def select_retained(scores, d_s, stream=None):
+    """select_retained (proj/src/merging.cpp:56-69), batched: scores [B, N] fp32 ->
+    retained [B, R] int32 ascending (top round(d_s N) scores, ties to lower index)."""
+    _req(scores, torch.float32, "scores")
+    B, N = scores.shape
+    R = retained_count(N, d_s)
+    L = capi.lib()
+    ws = _workspace(L.affmae_select_retained_workspace(C.c_int64(B), C.c_int64(N)), scores.device)
+    out = torch.empty((B, R), dtype=torch.int32, device=scores.device)
+    capi.check(L.affmae_select_retained(C.c_void_p(scores.data_ptr()), C.c_int64(B), C.c_int64(N),
+                                        C.c_double(d_s), C.c_void_p(out.data_ptr()),
+                                        C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()),
+                                        _stream(stream)), "select_retained")
+    return out
+
+
+@dataclass
+class MergePlan:
+    """Device merge plan (include/affmae_b200.h: affmae_merge_plan)."""
+    retained: torch.Tensor   # [B, R] int32
+    target: torch.Tensor     # [B, N] int32
+    pool_idx: torch.Tensor   # [B, R, k_m] int32
+    pool_dist: torch.Tensor  # [B, R, k_m] float64
+    pool_cnt: torch.Tensor   # [B, R] int32
+    row_of: torch.Tensor     # [B, N] int32
+    k_m: int
+
+    def c_struct(self):
+        return capi.MergePlan(*(capi.ptr(t) for t in (self.target, self.pool_idx, self.pool_dist,
+                                                       self.pool_cnt, self.row_of)))
+
+
+def merge_plan(coords, retained, k_m, workspace=None, stream=None) -> MergePlan:
+    """merge_plan (proj/src/merging.cpp:71-116), batched, bit-exact."""
+    _req(coords, torch.float32, "coords")
+    _req(retained, torch.int32, "retained")
+    B, N, _ = coords.shape
+    R = retained.shape[1]
+    dev = coords.device
+    i32 = dict(dtype=torch.int32, device=dev)
+    plan = MergePlan(retained, torch.empty((B, N), **i32), torch.empty((B, R, k_m), **i32),
+                     torch.empty((B, R, k_m), dtype=torch.float64, device=dev),
+                     torch.empty((B, R), **i32), torch.empty((B, N), **i32), k_m)
+    L = capi.lib()
+    nbytes = L.affmae_merge_plan_workspace(C.c_int64(B), C.c_int64(N), C.c_int64(R))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = _workspace(nbytes, dev)
+    ps = plan.c_struct()
+    capi.check(L.affmae_merge_plan_build(C.c_void_p(coords.data_ptr()),
+                                         C.c_void_p(retained.data_ptr()), C.c_int64(B),
+                                         C.c_int64(N), C.c_int64(R), C.c_int(k_m), C.byref(ps),
+                                         C.c_void_p(workspace.data_ptr()),
+                                         C.c_size_t(workspace.numel()), _stream(stream)),
+               "merge_plan")
+    return plan
+
+
+def merge_pool_fwd(feats, scores, p_merge, plan: MergePlan, out=None, stream=None):
+    """MergePoolOp::forward (proj/src/merging.cpp:121-166): [B, R, 2D] bf16."""
+    _req(feats, BF16, "feats")
+    _req(scores, torch.float32, "scores")
+    _req(p_merge, torch.float32, "p_merge")
+    B, N, D = feats.shape
+    R = plan.retained.shape[1]
+    if out is None:
+        out = torch.empty((B, R, 2 * D), dtype=BF16, device=feats.device)
+    ps = plan.c_struct()
+    capi.check(capi.lib().affmae_merge_pool_fwd(
+        C.c_void_p(feats.data_ptr()), C.c_void_p(scores.data_ptr()), C.c_void_p(p_merge.data_ptr()),
+        C.c_void_p(plan.retained.data_ptr()), C.byref(ps), C.c_int64(B), C.c_int64(N), C.c_int64(R),
+        C.c_int64(D), C.c_int(plan.k_m), C.c_void_p(out.data_ptr()), _stream(stream)),
+        "merge_pool_fwd")
+    return out
+
+
+def merge_pool_bwd(feats, scores, p_merge, plan: MergePlan, dout, dfeats=None, dscores=None,
+                   dp=None, workspace=None, stream=None):
+    """MergePoolOp::backward (proj/src/merging.cpp:169-219): dfeats [B, N, D] bf16 and
+    dscores [B, N] are overwritten, dp [1] accumulates (+=)."""
+    _req(dout, BF16, "dout")
+    B, N, D = feats.shape
+    R = plan.retained.shape[1]
+    dev = feats.device
+    if dfeats is None:
+        dfeats = torch.empty_like(feats)
+    if dscores is None:
+        dscores = torch.empty((B, N), dtype=torch.float32, device=dev)
+    if dp is None:
+        dp = torch.zeros(1, dtype=torch.float32, device=dev)
+    L = capi.lib()
+    nbytes = L.affmae_merge_pool_bwd_workspace(C.c_int64(B), C.c_int64(R))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = _workspace(nbytes, dev)
+    ps = plan.c_struct()
+    capi.check(L.affmae_merge_pool_bwd(
+        C.c_void_p(feats.data_ptr()), C.c_void_p(scores.data_ptr()), C.c_void_p(p_merge.data_ptr()),
+        C.c_void_p(plan.retained.data_ptr()), C.byref(ps), C.c_int64(B), C.c_int64(N), C.c_int64(R),
+        C.c_int64(D), C.c_int(plan.k_m), C.c_void_p(dout.data_ptr()), C.c_void_p(dfeats.data_ptr()),
+        C.c_void_p(dscores.data_ptr()), C.c_void_p(dp.data_ptr()), C.c_void_p(workspace.data_ptr()),
+        C.c_size_t(workspace.numel()), _stream(stream)), "merge_pool_bwd")
+    return dfeats, dscores, dp
