@@ -127,7 +127,10 @@ class ClockSampler:
 def make_inputs(a, rank):
     from paper_2602_16249_b200 import inputs
     rng = np.random.default_rng(1234 + rank)
-    coords = inputs.lattice_batch(a.batch, a.grid, 0.75, 8, seed0=1000 + rank * a.batch)
+    from paper_2602_16249_b200 import dist as pdist
+    # global image index -> mask seed, so results do not depend on the rank count
+    coords = inputs.lattice_batch(a.batch, a.grid, 0.75, 8,
+                                  seed0=pdist.mask_seed(pdist.image_range(a.batch, rank, max(rank + 1, 1))[0]))
     B, N, _ = coords.shape
     hd = a.heads * a.head_dim
     host = dict(
@@ -158,6 +161,7 @@ def algorithmic_bytes(a, N):
 # ------------------------------------------------------------------ ours
 def run_ours(a, rank, world, dist):
     import torch
+    from paper_2602_16249_b200 import dist as pdist
     from paper_2602_16249_b200 import ops
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(dev)
@@ -265,11 +269,7 @@ def run_ours(a, rank, world, dist):
         dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
     clocks.stop()
-    ms_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = pdist.max_over_ranks(ms, dist, dev)
     tokens_all = B * N * world
     value = tokens_all / (ms_max * 1e-3)
 
@@ -292,7 +292,7 @@ def count_graph_kernels(graph):
         except ImportError:
             return None
     try:
-        g = graph.raw_cuda_graph()
+        g = rt.cudaGraph_t(init_value=graph.raw_cuda_graph())
         err, nodes, n = rt.cudaGraphGetNodes(g, 0)
         err, nodes, n = rt.cudaGraphGetNodes(g, n)
         kern = 0
@@ -307,6 +307,7 @@ def count_graph_kernels(graph):
 
 def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
     import torch
+    from paper_2602_16249_b200 import dist as pdist
     from paper_2602_16249_b200 import ops
     bf = torch.bfloat16
     pin = {}
@@ -361,11 +362,7 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
         e2e_step()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.e2e_steps
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = pdist.max_over_ranks(e0.elapsed_time(e1) / a.e2e_steps, dist, dev)
     return {"value": B * N * world / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms}
 

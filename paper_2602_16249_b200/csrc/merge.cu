@@ -422,11 +422,19 @@ __global__ void pool_bwd_zero_kernel(const int32_t* __restrict__ row_of, int64_t
     if (lane == 0) dscores[tok] = 0.f;
 }
 
-// dp += sum of block partials (fixed order, single thread)
+// dp += sum of block partials (one CTA, fixed reduction order)
 __global__ void dp_reduce_kernel(const float* __restrict__ part, int nparts, float* __restrict__ dp) {
+    __shared__ float red[32];
     float s = 0.f;
-    for (int i = 0; i < nparts; ++i) s += part[i];
-    *dp += s;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+        *dp += t;
+    }
 }
 
 // ===================================================================== host
@@ -619,7 +627,7 @@ int merge_pool_bwd(const affmae_bf16* feats, const float* scores, const float* p
                                         retained, plan->pool_idx, plan->pool_dist, plan->pool_cnt, batch,
                                         n, r, int(dim), k_m, reinterpret_cast<const __nv_bfloat16*>(dout),
                                         reinterpret_cast<__nv_bfloat16*>(dfeats), dscores, part);
-    dp_reduce_kernel<<<1, 1, 0, st>>>(part, int(nb), dp);
+    dp_reduce_kernel<<<1, 1024, 0, st>>>(part, int(nb), dp);
     AFFMAE_LAUNCH_CHECK("pool_bwd_kernel");
     return AFFMAE_OK;
 }

@@ -33,14 +33,15 @@ static __global__ void radix_upsweep(const uint64_t* __restrict__ keys, int64_t 
     hist[int64_t(threadIdx.x) * tiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// single-CTA exclusive scan of `len` counters
-static __global__ void radix_scan(uint32_t* __restrict__ hist, int64_t len) {
-    __shared__ uint32_t part[1024];
+// per-bin exclusive scan over tiles (one CTA per digit bin); the bin total
+// goes to tot[bin].  hist is [bin][tile].
+static __global__ void radix_scan_bins(uint32_t* __restrict__ hist, int tiles, uint32_t* __restrict__ tot) {
+    __shared__ uint32_t part[256];
+    uint32_t* h = hist + int64_t(blockIdx.x) * tiles;
     const int t = threadIdx.x, nt = blockDim.x;
-    const int64_t per = (len + nt - 1) / nt;
-    const int64_t b = t * per, e = (b + per < len) ? b + per : len;
+    const int per = (tiles + nt - 1) / nt, b = t * per, e = (b + per < tiles) ? b + per : tiles;
     uint32_t s = 0;
-    for (int64_t i = b; i < e; ++i) s += hist[i];
+    for (int i = b; i < e; ++i) s += h[i];
     part[t] = s;
     __syncthreads();
     for (int o = 1; o < nt; o <<= 1) {
@@ -50,22 +51,37 @@ static __global__ void radix_scan(uint32_t* __restrict__ hist, int64_t len) {
         __syncthreads();
     }
     uint32_t run = part[t] - s;
-    for (int64_t i = b; i < e; ++i) {
-        uint32_t v = hist[i];
-        hist[i] = run;
+    for (int i = b; i < e; ++i) {
+        uint32_t v = h[i];
+        h[i] = run;
         run += v;
     }
+    if (t == nt - 1) tot[blockIdx.x] = part[t];
 }
 
 template <bool HAS_VAL>
 __global__ void radix_downsweep(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                 uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                int64_t n, int shift, int tiles, const uint32_t* __restrict__ offs) {
+                                int64_t n, int shift, int tiles, const uint32_t* __restrict__ offs,
+                                const uint32_t* __restrict__ tot) {
     __shared__ uint32_t wcnt[kSortThreads / 32][257];
     __shared__ uint32_t run[256];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const unsigned lt = (1u << lane) - 1u;
-    run[t] = offs[int64_t(t) * tiles + blockIdx.x];
+    {   // exclusive scan of the 256 bin totals (every CTA recomputes it: 256 values)
+        uint32_t v = tot[t];
+        run[t] = v;
+        __syncthreads();
+        for (int o = 1; o < 256; o <<= 1) {
+            uint32_t x = t >= o ? run[t - o] : 0;
+            __syncthreads();
+            run[t] += x;
+            __syncthreads();
+        }
+        const uint32_t base = run[t] - v;
+        __syncthreads();
+        run[t] = base + offs[int64_t(t) * tiles + blockIdx.x];
+    }
     const int64_t base = int64_t(blockIdx.x) * kSortTile;
     for (int r = 0; r < kSortRounds; ++r) {
         for (int i = t; i < (kSortThreads / 32) * 257; i += kSortThreads) (&wcnt[0][0])[i] = 0;
@@ -103,7 +119,7 @@ __global__ void radix_downsweep(const uint64_t* __restrict__ kin, const uint32_t
 
 inline size_t radix_hist_elems(int64_t n) {
     int64_t tiles = (n + kSortTile - 1) / kSortTile;
-    return size_t(256) * size_t(tiles > 0 ? tiles : 1);
+    return size_t(256) * size_t(tiles > 0 ? tiles : 1) + 256;  // + bin totals
 }
 
 // Sorts keys[0..n) (with vals if non-null) on bits [0, end_bit), ping-ponging
@@ -113,14 +129,15 @@ inline int radix_sort(uint64_t*& keys, uint32_t*& vals, uint64_t* keys_alt, uint
     if (n <= 0) return AFFMAE_OK;
     const int tiles = int((n + kSortTile - 1) / kSortTile);
     for (int shift = 0; shift < end_bit; shift += 8) {
+        uint32_t* tot = hist + size_t(256) * tiles;
         radix_upsweep<<<tiles, kSortThreads, 0, st>>>(keys, n, shift, tiles, hist);
-        radix_scan<<<1, 1024, 0, st>>>(hist, int64_t(256) * tiles);
+        radix_scan_bins<<<256, 256, 0, st>>>(hist, tiles, tot);
         if (vals)
             radix_downsweep<true><<<tiles, kSortThreads, 0, st>>>(keys, vals, keys_alt, vals_alt, n,
-                                                                shift, tiles, hist);
+                                                                shift, tiles, hist, tot);
         else
             radix_downsweep<false><<<tiles, kSortThreads, 0, st>>>(keys, nullptr, keys_alt, nullptr,
-                                                                 n, shift, tiles, hist);
+                                                                 n, shift, tiles, hist, tot);
         AFFMAE_LAUNCH_CHECK("radix sort pass");
         uint64_t* tk = keys;
         keys = keys_alt;

@@ -1,0 +1,58 @@
+"""CPU: the C-ABI library loads and exports every symbol include/affmae_b200.h declares,
+and its host-only entry points behave like the reference (no GPU compute here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from oracle import port
+from paper_2602_16249_b200 import capi
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "affmae_b200.h")
+
+
+def declared():
+    src = open(HDR).read()
+    return sorted(set(re.findall(r"\b(affmae_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_and_exports_agree():
+    assert declared() == sorted(capi.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = capi.lib()
+    missing = [s for s in declared() if not hasattr(L, s)]
+    assert not missing, missing
+
+
+def test_geometry_closed_forms():
+    for n, s, g in ((16384, 16, 3), (8281, 16, 3), (10, 8, 3), (1, 16, 3), (77, 8, 3)):
+        geo = capi.geometry(2, n, s, g)
+        assert (geo.n_clusters, geo.groups_eff, geo.max_size, geo.width) == port.cluster_shape(n, s, g)
+
+
+def test_errors_map_to_reference_taxonomy():
+    with pytest.raises(ValueError, match="empty point set"):
+        capi.geometry(1, 0, 16, 3)
+    with pytest.raises(ValueError, match="size must be"):
+        capi.geometry(1, 10, 0, 3)
+
+
+def test_retained_count_matches_oracle():
+    L = capi.lib()
+    for n in (1, 2, 7, 100, 4096, 16384):
+        for ds in (0.25, 0.35, 0.4, 0.5, 1.0):
+            assert L.affmae_retained_count(n, ds) == port.retained_count(n, ds)
+    assert L.affmae_retained_count(10, 0.0) == -2
+
+
+def test_workspace_queries_are_host_side():
+    L = capi.lib()
+    geo = capi.geometry(4, 16384, 16, 3)
+    assert L.affmae_cluster_index_workspace(C.byref(geo)) > 0
+    d = capi.AttnDesc(4, 32, 8, 8.0)
+    assert L.affmae_attn_bwd_workspace(C.byref(geo), C.byref(d)) > L.affmae_attn_fwd_workspace(C.byref(geo), C.byref(d))
+    d_bad = capi.AttnDesc(4, 24, 8, 8.0)
+    assert L.affmae_attn_fwd_workspace(C.byref(geo), C.byref(d_bad)) == 0

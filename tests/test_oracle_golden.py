@@ -1,0 +1,162 @@
+"""CPU: pins the oracle restatement (oracle/oracle.c) against the reference's own
+outputs (tests/golden/reference_golden.npz, produced by the unmodified reference by
+tests/golden/make_golden.py) and against known answers from the reference's test
+suite.  Bit-exact: the restatement follows the reference's arithmetic order."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import port
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+GEO = sorted(k[4:-7] for k in G.files if k.startswith("geo_") and k.endswith("_coords"))
+
+
+def test_hilbert_known_answers():
+    # proj/tests/test_geometry.cpp:27-32: the 2x2 base case visits the U shape
+    assert [port.hilbert_index(2, x, y) for x, y in ((0, 0), (0, 1), (1, 1), (1, 0))] == [0, 1, 2, 3]
+    # bijective, continuous (test_geometry.cpp:34-54)
+    for order in (2, 3, 4):
+        side = 1 << order
+        cells = sorted((port.hilbert_index(side, x, y), x, y) for x in range(side) for y in range(side))
+        assert [c[0] for c in cells] == list(range(side * side))
+        for a, b in zip(cells, cells[1:]):
+            assert abs(a[1] - b[1]) + abs(a[2] - b[2]) == 1
+
+
+@pytest.mark.parametrize("name", GEO)
+def test_geometry_matches_reference(name):
+    c = G[f"geo_{name}_coords"]
+    s, g = G[f"geo_{name}_shape"]
+    np.testing.assert_array_equal(port.sfc_order(c), G[f"geo_{name}_perm"])
+    ci = port.cluster_index(c, int(s), int(g))
+    for k in ("cluster_of", "members", "member_off", "idx", "valid"):
+        np.testing.assert_array_equal(ci[k], G[f"geo_{name}_{k}"], err_msg=k)
+
+
+def test_cluster_balance_and_self():
+    # proj/tests/test_geometry.cpp:82-123: sizes differ by <= 1, own cluster first, self present
+    c = G["geo_rand60_s8_g3_coords"]
+    ci = port.cluster_index(c, 8, 3)
+    sizes = np.diff(ci["member_off"])
+    assert sizes.max() - sizes.min() <= 1
+    for q in range(len(c)):
+        row = ci["idx"][q][ci["valid"][q] > 0]
+        own = ci["members"][ci["member_off"][ci["cluster_of"][q]]:ci["member_off"][ci["cluster_of"][q] + 1]]
+        assert set(own) <= set(row) and q in row
+
+
+def test_knn_matches_reference():
+    i, v = port.knn(G["knn_q"], G["knn_keys"], 9)
+    np.testing.assert_array_equal(i, G["knn_idx"])
+    np.testing.assert_array_equal(v, G["knn_valid"])
+
+
+def _att():
+    a = {k[5:]: G[k] for k in G.files if k.startswith("attn_") and not k.startswith(("attn_out", "attn_grad"))}
+    bias = {k: a[k] for k in ("w1", "b1", "w2", "b2", "blank")}
+    return a, bias
+
+
+def test_attention_fwd_matches_reference_b32():
+    a, bias = _att()
+    out = port.attn_fwd(a["q"], a["k"], a["v"], a["bk"], a["bv"], a["coords"], a["idx"], a["valid"],
+                        bias, 2, 8)
+    np.testing.assert_array_equal(out, G["attn_out_b32"].astype(np.float32))
+
+
+def test_attention_streaming_close_to_naive_b64():
+    # proj/tests/test_attention.cpp:112-124: streaming == naive within 1e-5 (b32)
+    a, bias = _att()
+    out = port.attn_fwd(a["q"], a["k"], a["v"], a["bk"], a["bv"], a["coords"], a["idx"], a["valid"],
+                        bias, 2, 8)
+    assert np.abs(out - G["attn_out_naive_b64"]).max() <= 1e-5
+
+
+def test_all_padded_row_falls_back_to_blank_v():
+    # proj/tests/test_attention.cpp:146-156 -- row 3 has no valid neighbour
+    a, bias = _att()
+    out = port.attn_fwd(a["q"], a["k"], a["v"], a["bk"], a["bv"], a["coords"], a["idx"], a["valid"],
+                        bias, 2, 8)
+    np.testing.assert_allclose(out[3], a["bv"].reshape(-1), rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_attention_bwd_matches_reference(prec):
+    a, bias = _att()
+    g = port.attn_bwd(a["q"], a["k"], a["v"], a["bk"], a["bv"], a["coords"], a["idx"], a["valid"],
+                      bias, 2, 8, a["dout"], prec=prec)
+    for k, v in g.items():
+        np.testing.assert_array_equal(v, G[f"attn_grad{prec}_{k}"], err_msg=k)
+
+
+def test_attention_gradient_by_finite_differences():
+    # proj/tests/test_attention.cpp:200-236 analogue on the oracle (b64)
+    a, bias = _att()
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal(a["q"].shape)
+    g = port.attn_bwd(a["q"], a["k"], a["v"], a["bk"], a["bv"], a["coords"], a["idx"], a["valid"],
+                      bias, 2, 8, w, prec=64)
+
+    def loss(qq):
+        # b64 forward via the naive restatement of the backward's score row
+        o = port.attn_fwd(qq, a["k"], a["v"], a["bk"], a["bv"], a["coords"], a["idx"], a["valid"],
+                          bias, 2, 8)
+        return float((o.astype(np.float64) * w).sum())
+
+    h = 1e-3
+    for (i, j) in ((0, 0), (5, 7), (11, 3)):
+        qp, qm = a["q"].copy(), a["q"].copy()
+        qp[i, j] += h
+        qm[i, j] -= h
+        fd = (loss(qp) - loss(qm)) / (2 * h)
+        assert abs(fd - g["dq"][i, j]) <= 2e-2 * max(1.0, abs(fd))
+
+
+def test_retention_table_and_ledger():
+    for n, ds, want in G["retention_table"]:
+        assert port.retained_count(int(n), float(ds)) == int(want)
+    # proj/tests/test_merging.cpp:46-59: 4096 -> 1638 -> 655 -> 262
+    n, led = 4096, []
+    for _ in range(3):
+        n = port.retained_count(n, 0.4)
+        led.append(n)
+    assert led == [1638, 655, 262]
+    with pytest.raises(ValueError):
+        port.retained_count(10, 1.5)
+
+
+def test_select_retained_known_answer():
+    np.testing.assert_array_equal(port.select_retained(G["sel_known_scores"], 0.5), G["sel_known_out"])
+    np.testing.assert_array_equal(G["sel_known_out"], [1, 2, 3])
+
+
+@pytest.mark.parametrize("name", ["m40", "m300", "m12"])
+def test_merge_matches_reference(name):
+    p = lambda k: G[f"mrg_{name}_{k}"]
+    ds, km = p("dsk")
+    r = port.select_retained(p("scores"), float(ds))
+    np.testing.assert_array_equal(r, p("retained"))
+    pl = port.merge_plan(p("coords"), r, int(km))
+    for k in ("dropped", "target", "pool_idx", "pool_dist", "pool_cnt"):
+        np.testing.assert_array_equal(pl[k], p(f"plan_{k}"), err_msg=k)
+    np.testing.assert_array_equal(port.merge_pool_fwd(pl, p("feats"), p("scores"), 1.3), p("pooled"))
+    df, dsc, dp = port.merge_pool_bwd(pl, p("feats"), p("scores"), 1.3, p("dout"))
+    np.testing.assert_array_equal(df, p("dfeats"))
+    np.testing.assert_array_equal(dsc, p("dscores"))
+    assert dp == float(p("dp")[0])
+
+
+def test_pool_known_answer():
+    # proj/tests/test_merging.cpp:117-152: retained 0 at origin, pool {1 at d=1, 2 at d=2}, p = 1.5
+    coords = np.array([[0, 0], [1, 0], [2, 0]], np.float32)
+    feats = np.arange(1, 7, dtype=np.float64).reshape(3, 2)
+    scores = np.array([0.9, 0.5, 0.25])
+    pl = port.merge_plan(coords, np.array([0]), 8)
+    out = port.merge_pool_fwd(pl, feats, scores, 1.5)
+    e1, e2 = np.exp(-1.5), np.exp(-3.0)
+    z = e1 + e2
+    assert out[0, 0] == 1.0 and out[0, 1] == 2.0
+    assert abs(out[0, 2] - ((e1 / z) * 0.5 * 3.0 + (e2 / z) * 0.25 * 5.0)) <= 1e-12
+    assert abs(out[0, 3] - ((e1 / z) * 0.5 * 4.0 + (e2 / z) * 0.25 * 6.0)) <= 1e-12
