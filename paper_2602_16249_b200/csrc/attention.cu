@@ -1,6 +1,8 @@
 // Host side of the cluster attention: validation, workspace layout, BiasNet
 // table build, kernel-variant dispatch and the gradient finalisation launches.
 // Kernels: attn_kernels.cuh (instantiated per head_dim in attn_inst_d*.cu).
+#include <cstdlib>
+
 #include "attn_kernels.cuh"
 
 namespace affmae_b200 {
@@ -125,6 +127,12 @@ int pick_nt(int width) {
 }
 
 static int heads_per_cta(int heads) {
+    // AFFMAE_HPC (1, 2 or 4) overrides the head-group width for experiments
+    static int force = [] {
+        const char* e = getenv("AFFMAE_HPC");
+        return e ? atoi(e) : 0;
+    }();
+    if ((force == 1 || force == 2 || force == 4) && heads % force == 0) return force;
     if (heads % 4 == 0) return 4;
     if (heads % 2 == 0) return 2;
     return 1;

@@ -175,6 +175,7 @@ struct QSmem {
     int32_t qlin[16];  // lattice cell iy*kWs + ix of each query
     int32_t klin[NS];  // ... and of each key slot
     int32_t meta[16];  // [0] nk; [1..12] lattice bbox / phase reductions; [13] fast
+    const __nv_bfloat16* rowsrc[(BWD ? 32 : 16) + 2 * NS];  // gather source of every staged row
     BiasTab<HPC> bt;
 };
 
@@ -247,7 +248,6 @@ __device__ __forceinline__ void stage_item(QSmem<HD, NT, HPC, BWD>& sm,
                                            int n_items, int h0) {
     using S = QSmem<HD, NT, HPC, BWD>;
     constexpr int NS = S::NS, RW = S::RW, NF = S::NF, NTHR = 32 * HPC;
-    constexpr int CH = HPC * HD / 8, RPP = NTHR / CH;  // 16-byte columns, rows per pass
     using PFT = TokPrefetch<NS, NTHR>;
     int img, c;
     item_coords(item, p.cs.c, img, c);
@@ -258,13 +258,25 @@ __device__ __forceinline__ void stage_item(QSmem<HD, NT, HPC, BWD>& sm,
 
     __syncthreads();  // (A) previous item fully consumed
     float2 xy[PFT::PF];
+    constexpr int QR = BWD ? 32 : 16;
 #pragma unroll
     for (int j = 0; j < PFT::PF; ++j) {
         int e = tid + j * NTHR, t = pf.v[j];
         xy[j] = make_float2(0.f, 0.f);
-        if (e < 16) sm.qtok[e] = t;
-        else if (e < 16 + NS) sm.ktok[e - 16] = t;
-        else if (e == 16 + NS) sm.meta[0] = t;
+        if (e < 16) {
+            sm.qtok[e] = t;
+            sm.rowsrc[e] = t >= 0 ? p.q + (img_tok + t) * hd_all + h0 * HD : nullptr;
+            if (BWD) sm.rowsrc[16 + e] = t >= 0 ? p.dout + (img_tok + t) * hd_all + h0 * HD : nullptr;
+        } else if (e < 16 + NS) {
+            const int slot = e - 16;
+            sm.ktok[slot] = t;
+            sm.rowsrc[QR + slot] = t >= 0 ? p.k + (img_tok + t) * hd_all + h0 * HD
+                                 : slot == M ? p.bk + h0 * HD : nullptr;
+            sm.rowsrc[QR + NS + slot] = t >= 0 ? p.v + (img_tok + t) * hd_all + h0 * HD
+                                      : slot == M ? p.bv + h0 * HD : nullptr;
+        } else if (e == 16 + NS) {
+            sm.meta[0] = t;
+        }
         if (e < 16 + NS && t >= 0) xy[j] = __ldg(reinterpret_cast<const float2*>(p.coords) + img_tok + t);
     }
     if (tid == 0) lattice_meta_init(sm.meta);
@@ -282,26 +294,22 @@ __device__ __forceinline__ void stage_item(QSmem<HD, NT, HPC, BWD>& sm,
     __syncthreads();  // (B) tokens visible
 
     const int nk = sm.meta[0];
-    {
-        constexpr int QR = BWD ? 32 : 16;
-        const int ch = tid % CH;
-        for (int r = tid / CH; r < QR + 2 * NS; r += RPP) {
-            __nv_bfloat16* dst;
-            const __nv_bfloat16* src = nullptr;
-            if (r < QR) {
-                const bool isdo = BWD && r >= 16;
-                const int tok = sm.qtok[r & 15];
-                dst = (isdo ? sm.dO : sm.Q) + (r & 15) * RW;
-                if (tok >= 0) src = (isdo ? p.dout : p.q) + (img_tok + tok) * hd_all;
-            } else {
-                const int kr = r - QR;
-                const bool isv = kr >= NS;
-                const int slot = isv ? kr - NS : kr, tok = sm.ktok[slot];
-                dst = (isv ? sm.V : sm.K) + slot * RW;
-                if (tok >= 0) src = (isv ? p.v : p.k) + (img_tok + tok) * hd_all;
-                else if (slot == M) src = isv ? p.bv : p.bk;
+    {   // gather: one warp instruction moves 32 / CH whole rows (CH 16-byte chunks each)
+        constexpr int CH = HPC * HD / 8, RPI = CH >= 32 ? 1 : 32 / CH, NW = NTHR / 32;
+        constexpr int ROWS = QR + 2 * NS, GROUPS = (ROWS + RPI - 1) / RPI;
+        const int wp = tid >> 5, ln = tid & 31, sub = ln / CH, ch = ln % CH;
+        for (int gi = wp; gi < GROUPS; gi += NW) {
+            const int r = gi * RPI + sub;
+            if (sub < RPI && r < ROWS) {
+                const __nv_bfloat16* src = sm.rowsrc[r];
+                __nv_bfloat16* dst = r < 16 ? sm.Q + r * RW
+                                   : r < QR ? sm.dO + (r - 16) * RW
+                                   : r < QR + NS ? sm.K + (r - QR) * RW : sm.V + (r - QR - NS) * RW;
+                if (src) cp_async16(dst + ch * 8, src + ch * 8);
+                if (CH > 32)
+                    for (int c2 = ch + 32; c2 < CH; c2 += 32)
+                        if (src) cp_async16(dst + c2 * 8, src + c2 * 8);
             }
-            if (src) cp_async16(dst + ch * 8, src + h0 * HD + ch * 8);
         }
         cp_async_commit();
     }
@@ -426,7 +434,6 @@ __global__ void __launch_bounds__(32 * HPC) attn_fwd_kernel(AttnParams p) {
                                        n_items, h0);
         int img, c;
         item_coords(item, p.cs.c, img, c);
-
         float s[NT][4];
         cluster_scores<HD, NT, HPC, false>(sm, p.scale, hh, s);
 
@@ -631,12 +638,30 @@ __global__ void __launch_bounds__(32 * HPC) attn_bwd_dq_kernel(AttnParams p) {
         }
         if (fast) {
             __syncwarp();
+            // Within one query row every key cell differs, so the offsets of a row
+            // are distinct table entries: plain read-modify-write, no atomics.  A
+            // duplicate key coordinate (two tokens on one cell) would alias two
+            // lanes, so such items fall back to atomics.
+            const int ka = lane < nk ? sm.klin[lane] : INT32_MIN + lane;
+            const int kb = lane + 32 < nk ? sm.klin[lane + 32] : INT32_MIN + 32 + lane;
+            const bool dup = __popc(__match_any_sync(0xffffffffu, ka)) > 1 ||
+                             __popc(__match_any_sync(0xffffffffu, kb)) > 1;
+            const bool dupw = __any_sync(0xffffffffu, dup);
+            const float* dsr = sm.bias + hh * NF;
             for (int r = 0; r < qlen; ++r) {
                 const int ql = kWinC - sm.qlin[r];
-                for (int slot = lane; slot < nk; slot += 32) {
-                    const int f = ((slot >> 3) << 7) + ((((r & 7) << 2) | ((slot & 7) >> 1)) << 2) +
-                                  ((r >> 3) << 1) + (slot & 1);
-                    atomicAdd(dtab_s + sm.klin[slot] + ql, sm.bias[hh * NF + f]);
+                const int fr = (((r & 7) << 2) << 2) + ((r >> 3) << 1);
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int slot = lane + 32 * half;
+                    if (slot < nk) {
+                        const int f = ((slot >> 3) << 7) + fr + (((slot & 7) >> 1) << 2) + (slot & 1);
+                        float* a = dtab_s + (half ? kb : ka) + ql;
+                        const float v = dsr[f];
+                        if (dupw) atomicAdd(a, v);
+                        else *a += v;
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -739,6 +764,7 @@ struct KSmem {
     int32_t klin[16];
     int32_t qlin[KDEG * 16];
     int32_t meta[16];  // [14] rb, [15] re; [1..12] lattice reductions of the round
+    uint64_t bar;
     BiasTab<HPC> bt;
 };
 
@@ -746,7 +772,6 @@ template <int HD, int HPC>
 __global__ void __launch_bounds__(32 * HPC) attn_bwd_dkdv_kernel(AttnParams p) {
     using S = KSmem<HD, HPC>;
     constexpr int RW = S::RW, CH = HPC * HD / 8, NTHR = 32 * HPC, NF = S::NF;
-    constexpr int RPP = NTHR / CH;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     S& sm = *reinterpret_cast<S*>(smem_raw);
     const int h0 = blockIdx.y * HPC;
@@ -760,6 +785,12 @@ __global__ void __launch_bounds__(32 * HPC) attn_bwd_dkdv_kernel(AttnParams p) {
     zero_smem(sm);
     __syncthreads();
     load_bias_tab(reinterpret_cast<float*>(sm.bt.tab), sm.bt.units, sm.bt.b2, sm.bt.blank, p, h0, HPC);
+    if (tid == 0) {
+        mbar_init(&sm.bar, 1);
+        fence_barrier_init();
+    }
+    uint32_t phase = 0;
+    constexpr uint32_t ROWB = HPC * HD * 2;
     // item prefetch: key tokens (tid < 16), reverse range (tid 16, 17)
     auto item_pf = [&](int item) -> int {
         if (item >= n_items || tid >= 18) return -1;
@@ -774,6 +805,7 @@ __global__ void __launch_bounds__(32 * HPC) attn_bwd_dkdv_kernel(AttnParams p) {
         item_coords(item, cs.c, img, ck);
         const int64_t img_tok = int64_t(img) * cs.n;
         const int klen = cs.len(ck);
+        fence_proxy_async();
         __syncthreads();
         if (tid < 16) {
             sm.ktok[tid] = ipf;
@@ -799,33 +831,36 @@ __global__ void __launch_bounds__(32 * HPC) attn_bwd_dkdv_kernel(AttnParams p) {
         for (int rs = rb; rs < re; rs += KDEG) {
             const int np = min(KDEG, re - rs);
             const bool first = rs == rb;
-            if (!first) __syncthreads();
+            if (!first) {
+                fence_proxy_async();
+                __syncthreads();
+            }
             // query tokens of this round, then their rows, coords, LSE and D
             for (int e = tid; e < KDEG * 16; e += NTHR)
                 sm.qtok[e] = e < np * 16 ? p.inq[(int64_t(img) * pairs_per_img + rs) * 16 + e] : -1;
             if (tid == 0) lattice_meta_init(sm.meta);
             __syncthreads();
-            {
-                const int ch = tid % CH;
-                const int rows = np * 32 + (first ? 32 : 0);
-                for (int r = tid / CH; r < rows; r += RPP) {
-                    __nv_bfloat16* dst;
-                    const __nv_bfloat16* src = nullptr;
-                    if (r < np * 32) {
-                        const bool isdo = r >= np * 16;
-                        const int qr = isdo ? r - np * 16 : r, tok = sm.qtok[qr];
-                        dst = (isdo ? sm.dO : sm.Q) + qr * RW;
-                        if (tok >= 0) src = (isdo ? p.dout : p.q) + (img_tok + tok) * hd_all;
-                    } else {
-                        const int kr = r - np * 32;
-                        const bool isv = kr >= 16;
-                        const int tok = sm.ktok[kr & 15];
-                        dst = (isv ? sm.V : sm.K) + (kr & 15) * RW;
-                        if (tok >= 0) src = (isv ? p.v : p.k) + (img_tok + tok) * hd_all;
-                    }
-                    if (src) cp_async16(dst + ch * 8, src + h0 * HD + ch * 8);
+            if (tid == 0) {
+                int nrows = 0;
+                for (int i = 0; i < np * 16; ++i) nrows += sm.qtok[i] >= 0;
+                mbar_arrive_expect_tx(&sm.bar, uint32_t(2 * nrows + (first ? 2 * klen : 0)) * ROWB);
+            }
+            for (int r = tid; r < np * 32 + (first ? 32 : 0); r += NTHR) {
+                __nv_bfloat16* dst;
+                const __nv_bfloat16* src = nullptr;
+                if (r < np * 32) {
+                    const bool isdo = r >= np * 16;
+                    const int qr = isdo ? r - np * 16 : r, tok = sm.qtok[qr];
+                    dst = (isdo ? sm.dO : sm.Q) + qr * RW;
+                    if (tok >= 0) src = (isdo ? p.dout : p.q) + (img_tok + tok) * hd_all + h0 * HD;
+                } else {
+                    const int kr = r - np * 32;
+                    const bool isv = kr >= 16;
+                    const int tok = sm.ktok[kr & 15];
+                    dst = (isv ? sm.V : sm.K) + (kr & 15) * RW;
+                    if (tok >= 0) src = (isv ? p.v : p.k) + (img_tok + tok) * hd_all + h0 * HD;
                 }
-                cp_async_commit();
+                if (src) bulk_g2s(dst, src, ROWB, &sm.bar);
             }
             for (int e = tid; e < np * 16; e += NTHR) {
                 const int qt = sm.qtok[e];
@@ -871,8 +906,9 @@ __global__ void __launch_bounds__(32 * HPC) attn_bwd_dkdv_kernel(AttnParams p) {
 #pragma unroll
                 for (int q = 0; q < HPC; ++q) sm.bias[(pr * HPC + q) * NF + g] = b[q];
             }
-            cp_async_wait<0>();
             __syncthreads();
+            mbar_wait(&sm.bar, phase);
+            phase ^= 1;
             if (first) {
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
