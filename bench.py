@@ -235,11 +235,19 @@ def run_ours(a, rank, world, dist):
                 step()
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
+            try:
+                graph = torch.cuda.CUDAGraph(keep_graph=True)
+            except TypeError:  # older torch
+                graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 step()
             torch.cuda.synchronize()
             launches = count_graph_kernels(graph)
+            if hasattr(graph, "instantiate"):
+                try:
+                    graph.instantiate()
+                except RuntimeError:
+                    pass
         except Exception as e:  # pragma: no cover - capture is best effort
             print(f"[bench] CUDA graph capture failed ({e}); eager launches", file=sys.stderr)
             graph = None

@@ -1,0 +1,394 @@
+// Reference-side adapters over the B200 C ABI (see affmae_cuda_ops.hpp).
+#include "affmae_cuda_ops.hpp"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "affmae/errors.hpp"
+#include "affmae_b200.h"
+
+namespace affmae::cuda {
+namespace {
+
+void check(int rc, const char* what) {
+    if (rc == AFFMAE_OK) return;
+    std::string msg = std::string(what) + ": " + affmae_last_error();
+    if (rc == AFFMAE_ECONFIG || rc == AFFMAE_EUNSUPPORTED) throw ConfigError(msg);
+    if (rc == AFFMAE_ENUMERIC) throw NumericError(msg);
+    throw std::runtime_error(msg);
+}
+void ccheck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// owning device buffer
+struct Dev {
+    void* p = nullptr;
+    size_t n = 0;
+    explicit Dev(size_t bytes) : n(bytes) { ccheck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc"); }
+    ~Dev() { cudaFree(p); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+std::unique_ptr<Dev> upload(const std::vector<T>& h) {
+    auto d = std::make_unique<Dev>(h.size() * sizeof(T));
+    ccheck(cudaMemcpy(d->p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    return d;
+}
+template <class T>
+std::vector<T> download(const Dev& d, size_t n) {
+    std::vector<T> h(n);
+    ccheck(cudaMemcpy(h.data(), d.p, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+    return h;
+}
+std::vector<float> f32(const Tensor& t) {
+    std::vector<float> v(size_t(t.numel()));
+    for (int64_t i = 0; i < t.numel(); ++i) v[size_t(i)] = float(t.get(i));
+    return v;
+}
+std::vector<uint16_t> bf16(const Tensor& t) {
+    std::vector<uint16_t> v(size_t(t.numel()));
+    for (int64_t i = 0; i < t.numel(); ++i) {
+        __nv_bfloat16 b = __float2bfloat16(float(t.get(i)));
+        std::memcpy(&v[size_t(i)], &b, 2);
+    }
+    return v;
+}
+float bf16_to_float(uint16_t u) {
+    uint32_t x = uint32_t(u) << 16;
+    float f;
+    std::memcpy(&f, &x, 4);
+    return f;
+}
+
+struct DeviceIndex {
+    affmae_cluster_geom g{};
+    std::unique_ptr<Dev> perm, cof, nbr, roff, rcl;
+    affmae_cluster_index idx{};
+};
+
+DeviceIndex build_index(const Dev& coords, int64_t n, int64_t size, int64_t groups) {
+    DeviceIndex d;
+    d.g.batch = 1;
+    d.g.tokens = n;
+    d.g.cluster = size;
+    d.g.groups = groups;
+    check(affmae_cluster_geometry(&d.g), "cluster_geometry");
+    d.perm = std::make_unique<Dev>(n * 4);
+    d.cof = std::make_unique<Dev>(n * 4);
+    d.nbr = std::make_unique<Dev>(d.g.n_clusters * d.g.groups_eff * 4);
+    d.roff = std::make_unique<Dev>((d.g.n_clusters + 1) * 4);
+    d.rcl = std::make_unique<Dev>(d.g.n_clusters * d.g.groups_eff * 4);
+    d.idx = {d.perm->as<int32_t>(), d.cof->as<int32_t>(), d.nbr->as<int32_t>(), d.roff->as<int32_t>(),
+             d.rcl->as<int32_t>()};
+    Dev ws(affmae_cluster_index_workspace(&d.g));
+    check(affmae_cluster_index_build(&d.g, coords.as<float>(), &d.idx, ws.p, ws.n, nullptr), "cluster_index_build");
+    return d;
+}
+
+}  // namespace
+
+ClusterAssignment balanced_clusters(const PointSet& points, int64_t size) {
+    const int64_t n = points.count();
+    if (size < 1) throw ConfigError("balanced_clusters: size must be >= 1");
+    auto c = upload(f32(points.coords));
+    DeviceIndex d = build_index(*c, n, size, 1);
+    ccheck(cudaDeviceSynchronize(), "sync");
+    auto perm = download<int32_t>(*d.perm, size_t(n));
+    ClusterAssignment a;
+    a.target = std::min(size, n);
+    a.cluster_of = download<int32_t>(*d.cof, size_t(n));
+    a.members.resize(size_t(d.g.n_clusters));
+    const int64_t base = n / d.g.n_clusters, rem = n % d.g.n_clusters;
+    int64_t pos = 0;
+    for (int64_t k = 0; k < d.g.n_clusters; ++k)
+        for (int64_t j = 0; j < base + (k < rem ? 1 : 0); ++j) a.members[size_t(k)].push_back(perm[size_t(pos++)]);
+    return a;
+}
+
+NeighborIndex cluster_neighborhood_from_coords(const PointSet& points, int64_t size, int64_t groups) {
+    const int64_t n = points.count();
+    auto c = upload(f32(points.coords));
+    DeviceIndex d = build_index(*c, n, size, groups);
+    const int64_t m = d.g.width;
+    Dev idx(n * m * 4), valid(n * m);
+    check(affmae_neighbor_expand(&d.g, d.perm->as<int32_t>(), d.nbr->as<int32_t>(), idx.as<int32_t>(),
+                                 valid.as<uint8_t>(), nullptr), "neighbor_expand");
+    ccheck(cudaDeviceSynchronize(), "sync");
+    NeighborIndex nb;
+    nb.width = m;
+    auto hi = download<int32_t>(idx, size_t(n * m));
+    auto hv = download<uint8_t>(valid, size_t(n * m));
+    nb.idx.assign(hi.begin(), hi.end());
+    nb.valid.assign(hv.begin(), hv.end());
+    return nb;
+}
+
+std::vector<int64_t> sfc_order(const PointSet& points) {
+    const int64_t n = points.count();
+    if (n < 1) throw ConfigError("sfc_order: empty point set");
+    auto c = upload(f32(points.coords));
+    Dev perm(n * 4), ws(affmae_sfc_order_workspace(1, n));
+    check(affmae_sfc_order(c->as<float>(), 1, n, perm.as<int32_t>(), ws.p, ws.n, nullptr), "sfc_order");
+    auto h = download<int32_t>(perm, size_t(n));
+    return std::vector<int64_t>(h.begin(), h.end());
+}
+
+NeighborIndex knn(const Tensor& queries, const PointSet& keys, int64_t k) {
+    const int64_t nq = queries.dim(0), nk = keys.count();
+    auto q = upload(f32(queries));
+    auto kk = upload(f32(keys.coords));
+    Dev idx(std::max<int64_t>(nq * k, 1) * 4), valid(std::max<int64_t>(nq * k, 1));
+    check(affmae_knn(q->as<float>(), kk->as<float>(), 1, nq, nk, k, idx.as<int32_t>(), valid.as<uint8_t>(), nullptr), "knn");
+    NeighborIndex nb;
+    nb.width = k;
+    auto hi = download<int32_t>(idx, size_t(nq * k));
+    auto hv = download<uint8_t>(valid, size_t(nq * k));
+    nb.idx.assign(hi.begin(), hi.end());
+    nb.valid.assign(hv.begin(), hv.end());
+    return nb;
+}
+
+namespace {
+
+// Tape op: inputs {q, k, v, blank_k, blank_v, w1, b1, w2, b2, blank}
+// (src/attention.cpp:374-444 ordering)
+struct ClusterAttnOp final : CustomOp {
+    Tensor coords;
+    int64_t cluster, groups;
+    int heads, head_dim, hidden;
+    double patch;
+
+    std::string name() const override { return "cluster_attention_b200"; }
+
+    affmae_attn_desc desc() const { return {heads, head_dim, hidden, patch}; }
+
+    Tensor forward(const std::vector<const Tensor*>& in) override {
+        if (in.size() != 10) throw ConfigError("attention op: want 10 inputs");
+        const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
+        auto dc = upload(f32(coords));
+        DeviceIndex d = build_index(*dc, n, cluster, groups);
+        std::unique_ptr<Dev> t[10];
+        for (int i = 0; i < 5; ++i) t[i] = upload(bf16(*in[size_t(i)]));
+        for (int i = 5; i < 10; ++i) t[i] = upload(f32(*in[size_t(i)]));
+        affmae_attn_inputs ai{t[0]->as<affmae_bf16>(), t[1]->as<affmae_bf16>(), t[2]->as<affmae_bf16>(),
+                              t[3]->as<affmae_bf16>(), t[4]->as<affmae_bf16>(), dc->as<float>(),
+                              t[5]->as<float>(), t[6]->as<float>(), t[7]->as<float>(), t[8]->as<float>(),
+                              t[9]->as<float>()};
+        affmae_attn_desc a = desc();
+        Dev out(n * hd * 2), lse(n * heads * 4), ws(affmae_attn_fwd_workspace(&d.g, &a));
+        check(affmae_attn_fwd(&d.g, &a, &ai, d.perm->as<int32_t>(), d.nbr->as<int32_t>(),
+                              out.as<affmae_bf16>(), lse.as<float>(), ws.p, ws.n, nullptr), "attn_fwd");
+        auto h = download<uint16_t>(out, size_t(n * hd));
+        Tensor o = Tensor::zeros({n, hd}, in[0]->precision());
+        for (int64_t i = 0; i < n * hd; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+        return o;
+    }
+
+    void backward(const Tensor& out_grad, const std::vector<const Tensor*>& in,
+                  const std::vector<Tensor*>& in_grads) override {
+        const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
+        auto dc = upload(f32(coords));
+        DeviceIndex d = build_index(*dc, n, cluster, groups);
+        std::unique_ptr<Dev> t[10];
+        for (int i = 0; i < 5; ++i) t[i] = upload(bf16(*in[size_t(i)]));
+        for (int i = 5; i < 10; ++i) t[i] = upload(f32(*in[size_t(i)]));
+        affmae_attn_inputs ai{t[0]->as<affmae_bf16>(), t[1]->as<affmae_bf16>(), t[2]->as<affmae_bf16>(),
+                              t[3]->as<affmae_bf16>(), t[4]->as<affmae_bf16>(), dc->as<float>(),
+                              t[5]->as<float>(), t[6]->as<float>(), t[7]->as<float>(), t[8]->as<float>(),
+                              t[9]->as<float>()};
+        affmae_attn_desc a = desc();
+        Dev out(n * hd * 2), lse(n * heads * 4), wsf(affmae_attn_fwd_workspace(&d.g, &a));
+        check(affmae_attn_fwd(&d.g, &a, &ai, d.perm->as<int32_t>(), d.nbr->as<int32_t>(),
+                              out.as<affmae_bf16>(), lse.as<float>(), wsf.p, wsf.n, nullptr), "attn_fwd");
+        auto dout = upload(bf16(out_grad));
+        Dev dq(n * hd * 2), dk(n * hd * 2), dv(n * hd * 2);
+        std::unique_ptr<Dev> pg[7];
+        const int64_t psz[7] = {int64_t(heads) * head_dim, int64_t(heads) * head_dim, heads * 2 * int64_t(hidden),
+                                int64_t(heads) * hidden, int64_t(heads) * hidden, heads, heads};
+        for (int i = 0; i < 7; ++i) {
+            pg[i] = std::make_unique<Dev>(psz[i] * 4);
+            ccheck(cudaMemset(pg[i]->p, 0, psz[i] * 4), "memset");
+        }
+        affmae_attn_grads g{dq.as<affmae_bf16>(), dk.as<affmae_bf16>(), dv.as<affmae_bf16>(),
+                            pg[0]->as<float>(), pg[1]->as<float>(), pg[2]->as<float>(), pg[3]->as<float>(),
+                            pg[4]->as<float>(), pg[5]->as<float>(), pg[6]->as<float>()};
+        Dev wsb(affmae_attn_bwd_workspace(&d.g, &a));
+        check(affmae_attn_bwd(&d.g, &a, &ai, &d.idx, out.as<affmae_bf16>(), lse.as<float>(),
+                              dout->as<affmae_bf16>(), &g, wsb.p, wsb.n, nullptr), "attn_bwd");
+        ccheck(cudaDeviceSynchronize(), "sync");
+        // accumulate (+=) into non-null in_grads (include/affmae/tape.hpp:29-31)
+        const Dev* act[3] = {&dq, &dk, &dv};
+        for (int i = 0; i < 3; ++i) {
+            if (!in_grads[size_t(i)]) continue;
+            auto h = download<uint16_t>(*act[i], size_t(n * hd));
+            for (int64_t j = 0; j < n * hd; ++j)
+                in_grads[size_t(i)]->set(j, in_grads[size_t(i)]->get(j) + bf16_to_float(h[size_t(j)]));
+        }
+        for (int i = 0; i < 7; ++i) {
+            Tensor* dst = in_grads[size_t(3 + i)];
+            if (!dst) continue;
+            auto h = download<float>(*pg[i], size_t(psz[i]));
+            for (int64_t j = 0; j < psz[i]; ++j) dst->set(j, dst->get(j) + h[size_t(j)]);
+        }
+    }
+};
+
+}  // namespace
+
+std::shared_ptr<CustomOp> make_cluster_attn_op(Tensor coords, int64_t cluster, int64_t groups, int heads,
+                                               int head_dim, int bias_hidden, double patch) {
+    auto op = std::make_shared<ClusterAttnOp>();
+    op->coords = std::move(coords);
+    op->cluster = cluster;
+    op->groups = groups;
+    op->heads = heads;
+    op->head_dim = head_dim;
+    op->hidden = bias_hidden;
+    op->patch = patch;
+    return op;
+}
+
+std::vector<int64_t> select_retained(const Tensor& scores, double d_s) {
+    const int64_t n = scores.rows();
+    const int64_t r = affmae_retained_count(n, d_s);
+    if (r < 0) throw ConfigError("retained_count: d_s must be in (0, 1]");
+    auto s = upload(f32(scores));
+    Dev out(r * 4), ws(affmae_select_retained_workspace(1, n));
+    check(affmae_select_retained(s->as<float>(), 1, n, d_s, out.as<int32_t>(), ws.p, ws.n, nullptr), "select_retained");
+    auto h = download<int32_t>(out, size_t(r));
+    return std::vector<int64_t>(h.begin(), h.end());
+}
+
+MergePlan merge_plan(const PointSet& ps, std::span<const int64_t> retained, int k_m) {
+    const int64_t n = ps.count(), r = int64_t(retained.size());
+    if (r < 1) throw ConfigError("merge_plan: retained set empty");
+    auto c = upload(f32(ps.coords));
+    std::vector<int32_t> rv(retained.begin(), retained.end());
+    auto dr = upload(rv);
+    Dev tgt(n * 4), pidx(r * k_m * 4), pdist(r * k_m * 8), pcnt(r * 4), rowof(n * 4),
+        ws(affmae_merge_plan_workspace(1, n, r));
+    affmae_merge_plan pl{tgt.as<int32_t>(), pidx.as<int32_t>(), pdist.as<double>(), pcnt.as<int32_t>(),
+                         rowof.as<int32_t>()};
+    check(affmae_merge_plan_build(c->as<float>(), dr->as<int32_t>(), 1, n, r, k_m, &pl, ws.p, ws.n, nullptr),
+          "merge_plan");
+    auto ht = download<int32_t>(tgt, size_t(n));
+    auto hi = download<int32_t>(pidx, size_t(r * k_m));
+    auto hd = download<double>(pdist, size_t(r * k_m));
+    auto hc = download<int32_t>(pcnt, size_t(r));
+    MergePlan plan;
+    plan.retained.assign(retained.begin(), retained.end());
+    for (int64_t j = 0; j < n; ++j)
+        if (ht[size_t(j)] >= 0) {
+            plan.dropped.push_back(j);
+            plan.target.push_back(ht[size_t(j)]);
+        }
+    plan.pool.resize(size_t(r));
+    plan.pool_dist.resize(size_t(r));
+    for (int64_t i = 0; i < r; ++i)
+        for (int t = 0; t < hc[size_t(i)]; ++t) {
+            plan.pool[size_t(i)].push_back(hi[size_t(i * k_m + t)]);
+            plan.pool_dist[size_t(i)].push_back(hd[size_t(i * k_m + t)]);
+        }
+    return plan;
+}
+
+std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords) {
+    // The device pool kernels consume the device plan; rebuild it from the host plan.
+    struct PoolOp final : CustomOp {
+        MergePlan plan;
+        Tensor coords;
+        std::string name() const override { return "merge_pool_b200"; }
+        int km() const {
+            size_t m = 1;
+            for (auto& p : plan.pool) m = std::max(m, p.size());
+            return int(m);
+        }
+        struct DevPlan {
+            std::unique_ptr<Dev> ret, tgt, pidx, pdist, pcnt, rowof;
+            affmae_merge_plan pl{};
+        };
+        DevPlan upload_plan(int64_t n, int k_m) const {
+            const int64_t r = int64_t(plan.retained.size());
+            std::vector<int32_t> ret(plan.retained.begin(), plan.retained.end());
+            std::vector<int32_t> tgt(static_cast<size_t>(n), -1), rowof(static_cast<size_t>(n), -1);
+            std::vector<int32_t> pidx(static_cast<size_t>(r * k_m), -1), pcnt(static_cast<size_t>(r), 0);
+            std::vector<double> pdist(static_cast<size_t>(r * k_m), 0.0);
+            for (size_t i = 0; i < plan.dropped.size(); ++i) tgt[size_t(plan.dropped[i])] = int32_t(plan.target[i]);
+            for (int64_t i = 0; i < r; ++i) {
+                rowof[size_t(plan.retained[size_t(i)])] = int32_t(i);
+                pcnt[size_t(i)] = int32_t(plan.pool[size_t(i)].size());
+                for (size_t t = 0; t < plan.pool[size_t(i)].size(); ++t) {
+                    pidx[size_t(i * k_m) + t] = int32_t(plan.pool[size_t(i)][t]);
+                    pdist[size_t(i * k_m) + t] = plan.pool_dist[size_t(i)][t];
+                    rowof[size_t(plan.pool[size_t(i)][t])] = int32_t(i);
+                }
+            }
+            DevPlan d;
+            d.ret = upload(ret);
+            d.tgt = upload(tgt);
+            d.pidx = upload(pidx);
+            d.pdist = upload(pdist);
+            d.pcnt = upload(pcnt);
+            d.rowof = upload(rowof);
+            d.pl = {d.tgt->as<int32_t>(), d.pidx->as<int32_t>(), d.pdist->as<double>(), d.pcnt->as<int32_t>(),
+                    d.rowof->as<int32_t>()};
+            return d;
+        }
+        Tensor forward(const std::vector<const Tensor*>& in) override {
+            const Tensor& feats = *in[0];
+            const int64_t n = feats.rows(), dim = feats.cols(), r = int64_t(plan.retained.size());
+            const int k_m = km();
+            DevPlan d = upload_plan(n, k_m);
+            auto f = upload(bf16(feats));
+            auto s = upload(f32(*in[1]));
+            auto pm = upload(f32(*in[2]));
+            Dev out(r * 2 * dim * 2);
+            check(affmae_merge_pool_fwd(f->as<affmae_bf16>(), s->as<float>(), pm->as<float>(), d.ret->as<int32_t>(),
+                                        &d.pl, 1, n, r, dim, k_m, out.as<affmae_bf16>(), nullptr), "merge_pool_fwd");
+            auto h = download<uint16_t>(out, size_t(r * 2 * dim));
+            Tensor o = Tensor::zeros({r, 2 * dim}, feats.precision());
+            for (int64_t i = 0; i < r * 2 * dim; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+            return o;
+        }
+        void backward(const Tensor& g, const std::vector<const Tensor*>& in,
+                      const std::vector<Tensor*>& in_grads) override {
+            const Tensor& feats = *in[0];
+            const int64_t n = feats.rows(), dim = feats.cols(), r = int64_t(plan.retained.size());
+            const int k_m = km();
+            DevPlan d = upload_plan(n, k_m);
+            auto f = upload(bf16(feats));
+            auto s = upload(f32(*in[1]));
+            auto pm = upload(f32(*in[2]));
+            auto dg = upload(bf16(g));
+            Dev df(n * dim * 2), ds(n * 4), dp(4), ws(affmae_merge_pool_bwd_workspace(1, r));
+            ccheck(cudaMemset(dp.p, 0, 4), "memset");
+            check(affmae_merge_pool_bwd(f->as<affmae_bf16>(), s->as<float>(), pm->as<float>(), d.ret->as<int32_t>(),
+                                        &d.pl, 1, n, r, dim, k_m, dg->as<affmae_bf16>(), df.as<affmae_bf16>(),
+                                        ds.as<float>(), dp.as<float>(), ws.p, ws.n, nullptr), "merge_pool_bwd");
+            if (in_grads[0]) {
+                auto h = download<uint16_t>(df, size_t(n * dim));
+                for (int64_t i = 0; i < n * dim; ++i) in_grads[0]->set(i, in_grads[0]->get(i) + bf16_to_float(h[size_t(i)]));
+            }
+            if (in_grads[1]) {
+                auto h = download<float>(ds, size_t(n));
+                for (int64_t i = 0; i < n; ++i) in_grads[1]->set(i, in_grads[1]->get(i) + h[size_t(i)]);
+            }
+            if (in_grads[2]) in_grads[2]->set(0, in_grads[2]->get(0) + download<float>(dp, 1)[0]);
+        }
+    };
+    auto op = std::make_shared<PoolOp>();
+    op->plan = std::move(plan);
+    op->coords = std::move(coords);
+    return op;
+}
+
+}  // namespace affmae::cuda

@@ -1,0 +1,45 @@
+// affmae_cuda_ops.hpp -- reference-side adapters for libaffmae_b200.so.
+//
+// This is the binding a maintainer adds to the REFERENCE tree (it includes the
+// reference's own headers): every factory/free function keeps the reference's
+// signature and CustomOp semantics (include/affmae/tape.hpp:29-38 -- backward
+// accumulates into non-null in_grads), but runs on the B200 through the C ABI
+// declared in include/affmae_b200.h.  Host Tensors are copied to the device per
+// call (bf16 activations, fp32 parameters), exactly the "host buffers" path.
+// Status codes map back onto the reference taxonomy (ConfigError /
+// NumericError, include/affmae/errors.hpp:8-15).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "affmae/attention.hpp"
+#include "affmae/geometry.hpp"
+#include "affmae/merging.hpp"
+#include "affmae/tape.hpp"
+
+namespace affmae::cuda {
+
+// balanced_clusters / cluster_neighborhood (include/affmae/geometry.hpp:61-68)
+ClusterAssignment balanced_clusters(const PointSet& points, int64_t size);
+NeighborIndex cluster_neighborhood_from_coords(const PointSet& points, int64_t size, int64_t groups);
+// sfc_order / knn (include/affmae/geometry.hpp:59,72)
+std::vector<int64_t> sfc_order(const PointSet& points);
+NeighborIndex knn(const Tensor& queries, const PointSet& keys, int64_t k);
+
+// Cluster attention as a tape op (make_attn_op, include/affmae/attention.hpp:84-86).
+// The cluster structure (size, groups) is what Model::encode passes to
+// balanced_clusters/cluster_neighborhood right before building the op
+// (proj/src/pipeline.cpp:442-444); the device index is rebuilt from `coords`.
+std::shared_ptr<CustomOp> make_cluster_attn_op(Tensor coords, int64_t cluster, int64_t groups,
+                                               int heads, int head_dim, int bias_hidden,
+                                               double patch);
+
+// select_retained / merge_plan / make_merge_pool_op (include/affmae/merging.hpp:32-68)
+std::vector<int64_t> select_retained(const Tensor& scores, double d_s);
+MergePlan merge_plan(const PointSet& ps, std::span<const int64_t> retained, int k_m);
+std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords);
+
+}  // namespace affmae::cuda

@@ -1,0 +1,104 @@
+"""Drop-in at the reference's own operator boundary: the REFERENCE Tape
+(proj/src/tape.cpp) runs one attention layer and one merge with the B200 ops from
+integration/affmae_cuda_ops.cpp plugged in as CustomOps, against the same Tape
+with the reference's CPU ops (make_attn_op / make_merge_pool_op).  Also checks
+the geometry adapters return the reference's exact ClusterAssignment /
+NeighborIndex / knn results."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from paper_2602_16249_b200 import inputs
+from tests.problems import rel_l2
+
+LIB = os.path.join(os.path.dirname(os.path.dirname(__file__)), "integration", "libaffmae_integration.so")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.exists(LIB), reason="integration library not built")]
+
+
+def _lib():
+    L = C.CDLL(LIB)
+    L.integ_last_error.restype = C.c_char_p
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _ok(L, rc):
+    assert rc == 0, L.integ_last_error().decode()
+
+
+@pytest.mark.parametrize("grid,seed", [(64, 3), (128, 9)])
+def test_geometry_adapters_bit_exact(grid, seed):
+    L = _lib()
+    c = inputs.lattice_batch(1, grid, 0.75, 8, seed0=seed)[0]
+    bad = C.c_int64(-1)
+    _ok(L, L.integ_geometry(_p(c), C.c_int64(len(c)), C.c_int64(16), C.c_int64(3), C.byref(bad)))
+    assert bad.value == 0
+    rng = np.random.default_rng(seed)
+    r = rng.uniform(0, 100, (500, 2)).astype(np.float32)
+    _ok(L, L.integ_geometry(_p(r), C.c_int64(500), C.c_int64(8), C.c_int64(3), C.byref(bad)))
+    assert bad.value == 0
+
+
+def _attn(L, use_cuda, n, heads, d, hidden, coords, ins, w):
+    out = np.zeros((n, heads * d))
+    shapes = [(n, heads * d)] * 3 + [(heads, d)] * 2 + [(heads, 2 * hidden), (heads, hidden),
+                                                         (heads, hidden), (heads, 1), (heads, 1)]
+    grads = [np.zeros(s) for s in shapes]
+    ins_p = (C.c_void_p * 10)(*[_p(x) for x in ins])
+    g_p = (C.c_void_p * 10)(*[_p(x) for x in grads])
+    _ok(L, L.integ_attn_tape(C.c_int(use_cuda), C.c_int64(n), C.c_int(heads), C.c_int(d), C.c_int(hidden),
+                             C.c_double(8.0), C.c_int64(16), C.c_int64(3), _p(coords), ins_p, _p(w),
+                             _p(out), g_p))
+    return out, grads
+
+
+def test_attention_custom_op_on_reference_tape():
+    L = _lib()
+    rng = np.random.default_rng(11)
+    coords = inputs.lattice_batch(1, 64, 0.75, 8, seed0=21)[0]
+    n, heads, d, hidden = len(coords), 2, 32, 8
+    bf = lambda *s: inputs.bf16_round(0.5 * rng.standard_normal(s).astype(np.float32)).astype(np.float64)
+    b = inputs.bias_params(heads, hidden, rng)
+    ins = [bf(n, heads * d), bf(n, heads * d), bf(n, heads * d), bf(heads, d), bf(heads, d)] + \
+          [b[k].astype(np.float64) for k in ("w1", "b1", "w2", "b2", "blank")]
+    w = inputs.bf16_round(rng.standard_normal((n, heads * d)).astype(np.float32)).astype(np.float64)
+    o_ref, g_ref = _attn(L, 0, n, heads, d, hidden, coords, ins, w)
+    o_gpu, g_gpu = _attn(L, 1, n, heads, d, hidden, coords, ins, w)
+    assert rel_l2(o_gpu, o_ref) <= 1e-2
+    names = ("dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")
+    errs = {nm: rel_l2(a, r) for nm, a, r in zip(names, g_gpu, g_ref)}
+    assert all(e <= 1e-2 for e in errs.values()), errs
+
+
+def test_merge_custom_op_on_reference_tape():
+    L = _lib()
+    rng = np.random.default_rng(5)
+    coords = inputs.lattice_batch(1, 64, 0.75, 8, seed0=4)[0]
+    n, dim, k_m, d_s, p = len(coords), 32, 8, 0.4, 1.2
+    feats = inputs.bf16_round(rng.standard_normal((n, dim)).astype(np.float32)).astype(np.float64)
+    scores = rng.uniform(0.1, 0.9, n).astype(np.float32).astype(np.float64)
+    R = int(np.floor(d_s * n + 0.5))
+    w = inputs.bf16_round(rng.standard_normal((R, 2 * dim)).astype(np.float32)).astype(np.float64)
+    res = []
+    for use in (0, 1):
+        ret = np.zeros(n, np.int64)
+        nr = C.c_int64()
+        pidx = np.zeros((n, k_m), np.int64)
+        pooled = np.zeros((R, 2 * dim))
+        df, ds, dp = np.zeros((n, dim)), np.zeros(n), C.c_double()
+        _ok(L, L.integ_merge_tape(C.c_int(use), C.c_int64(n), C.c_int64(dim), C.c_double(d_s), C.c_int(k_m),
+                                  _p(coords), _p(feats), _p(scores), C.c_double(p), _p(w), _p(ret),
+                                  C.byref(nr), _p(pidx), _p(pooled), _p(df), _p(ds), C.byref(dp)))
+        res.append((ret[: nr.value], pidx[: nr.value], pooled, df, ds, dp.value))
+    (r0, p0, o0, f0, s0, d0), (r1, p1, o1, f1, s1, d1) = res
+    np.testing.assert_array_equal(r1, r0)
+    np.testing.assert_array_equal(p1, p0)
+    assert rel_l2(o1, o0) <= 1e-2 and rel_l2(f1, f0) <= 1e-2 and rel_l2(s1, s0) <= 1e-2
+    assert abs(d1 - d0) <= 1e-2 * max(1.0, abs(d0))
