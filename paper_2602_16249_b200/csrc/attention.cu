@@ -1,6 +1,8 @@
 // Host side of the cluster attention: validation, workspace layout, BiasNet
-// table build, kernel-variant dispatch and the gradient finalisation launches.
+// table build, the per-call plan records the kernels stream through, kernel
+// variant dispatch and the (fixed-order) gradient finalisation.
 // Kernels: attn_kernels.cuh (instantiated per head_dim in attn_inst_d*.cu).
+#include <climits>
 #include <cstdlib>
 
 #include "attn_kernels.cuh"
@@ -26,9 +28,213 @@ __global__ void bias_table_kernel(const float* __restrict__ w1, const float* __r
     tab[i] = acc;
 }
 
+// -------------------------------------------------------------- plan records
+// Lattice cell of a token (window coordinates): iy * kWs + ix.  Two tokens of
+// one phase have window offset kcell - qcell == (dy * kWs + dx).
+__device__ __forceinline__ int tok_cell(const TokInfo& t) { return t.iy * kWs + t.ix; }
+
+struct Bbox {
+    int xmin, xmax, ymin, ymax;
+};
+__device__ __forceinline__ Bbox warp_bbox(bool valid, const TokInfo& t) {
+    Bbox b;
+    b.xmin = __reduce_min_sync(0xffffffffu, valid ? t.ix : INT_MAX);
+    b.xmax = __reduce_max_sync(0xffffffffu, valid ? t.ix : INT_MIN);
+    b.ymin = __reduce_min_sync(0xffffffffu, valid ? t.iy : INT_MAX);
+    b.ymax = __reduce_max_sync(0xffffffffu, valid ? t.iy : INT_MIN);
+    return b;
+}
+__device__ __forceinline__ bool bbox_fits(const Bbox& q, const Bbox& k) {
+    // every key-minus-query offset inside [-kRs, kRs]^2 (64-bit: no overflow on far tokens)
+    return int64_t(k.xmax) - q.xmin <= kRs && int64_t(q.xmax) - k.xmin <= kRs &&
+           int64_t(k.ymax) - q.ymin <= kRs && int64_t(q.ymax) - k.ymin <= kRs;
+}
+__device__ __forceinline__ bool warp_one_phase(bool valid, const TokInfo& t) {
+    const uint32_t fx0 = __reduce_min_sync(0xffffffffu, valid ? t.fx : 0xffffffffu);
+    const uint32_t fx1 = __reduce_max_sync(0xffffffffu, valid ? t.fx : 0u);
+    const uint32_t fy0 = __reduce_min_sync(0xffffffffu, valid ? t.fy : 0xffffffffu);
+    const uint32_t fy1 = __reduce_max_sync(0xffffffffu, valid ? t.fy : 0u);
+    return fx0 == fx1 && fy0 == fy1;
+}
+// Bounding boxes / phase of up to two warp-chunks of tokens combined.
+struct TokAgg {
+    int qx0 = INT_MAX, qx1 = INT_MIN, qy0 = INT_MAX, qy1 = INT_MIN;
+    int kx0 = INT_MAX, kx1 = INT_MIN, ky0 = INT_MAX, ky1 = INT_MIN;
+    uint32_t fx0 = 0xffffffffu, fx1 = 0, fy0 = 0xffffffffu, fy1 = 0;
+    __device__ void add(const TokInfo& t, bool is_key) {
+        if (is_key) {
+            kx0 = min(kx0, t.ix); kx1 = max(kx1, t.ix); ky0 = min(ky0, t.iy); ky1 = max(ky1, t.iy);
+        } else {
+            qx0 = min(qx0, t.ix); qx1 = max(qx1, t.ix); qy0 = min(qy0, t.iy); qy1 = max(qy1, t.iy);
+        }
+        fx0 = min(fx0, t.fx); fx1 = max(fx1, t.fx); fy0 = min(fy0, t.fy); fy1 = max(fy1, t.fy);
+    }
+    __device__ bool fast() const {
+        Bbox q{__reduce_min_sync(0xffffffffu, qx0), __reduce_max_sync(0xffffffffu, qx1),
+               __reduce_min_sync(0xffffffffu, qy0), __reduce_max_sync(0xffffffffu, qy1)};
+        Bbox k{__reduce_min_sync(0xffffffffu, kx0), __reduce_max_sync(0xffffffffu, kx1),
+               __reduce_min_sync(0xffffffffu, ky0), __reduce_max_sync(0xffffffffu, ky1)};
+        const bool ph = __reduce_min_sync(0xffffffffu, fx0) == __reduce_max_sync(0xffffffffu, fx1) &&
+                        __reduce_min_sync(0xffffffffu, fy0) == __reduce_max_sync(0xffffffffu, fy1);
+        return ph && bbox_fits(q, k);
+    }
+};
+
+// Query-cluster records (one warp per (image, cluster)): query tokens, the
+// key token of every neighbourhood slot in reference order
+// (cluster_neighborhood, proj/src/geometry.cpp:173-183), lattice cells, nk,
+// qlen, the lattice-fast flag and duplicate-cell flags of the two key halves.
+template <int KP>
+__global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ nbr_cl, ClusterShape cs, int64_t items,
+                                 float inv_patch, int32_t* __restrict__ qrec) {
+    using R = QRec<KP>;
+    constexpr int E = 16 + KP, J = (E + 31) / 32;
+    __shared__ int cellbuf[4][E];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t item = int64_t(blockIdx.x) * 4 + warp;
+    if (item >= items) return;
+    const int img = int(item / cs.c), c = int(item - int64_t(img) * cs.c);
+    const int64_t img_tok = int64_t(img) * cs.n;
+    const int32_t* nb = nbr_cl + item * cs.g;
+    int32_t* out = qrec + item * R::WORDS;
+    const int qlen = cs.len(c);
+    int nk = 0;
+    for (int g = 0; g < cs.g; ++g) nk += cs.len(nb[g]);
+    TokAgg agg;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int e = lane + 32 * j;
+        int tok = -1;
+        if (e < 16) {
+            if (e < qlen) tok = perm[img_tok + cs.off(c) + e];
+        } else if (e < E && e - 16 < nk) {
+            int s = e - 16;
+            for (int g = 0; g < cs.g; ++g) {
+                const int cl = nb[g], len = cs.len(cl);
+                if (s < len) {
+                    tok = perm[img_tok + cs.off(cl) + s];
+                    break;
+                }
+                s -= len;
+            }
+        }
+        int cell = 0;
+        if (tok >= 0) {
+            const TokInfo t = make_tokinfo(reinterpret_cast<const float2*>(coords)[img_tok + tok], inv_patch);
+            cell = tok_cell(t);
+            agg.add(t, e >= 16);
+        }
+        if (e < E) {
+            out[e < 16 ? R::QTOK + e : R::KTOK + e - 16] = tok;
+            cellbuf[warp][e] = cell;
+        }
+    }
+    const bool fast = agg.fast();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E) {
+            const bool valid = e < 16 ? e < qlen : e - 16 < nk;
+            const int cell = valid ? cellbuf[warp][e] : cellbuf[warp][e < 16 ? 0 : 16];
+            out[e < 16 ? R::QCELL + e : R::KCELL + e - 16] = cell;
+        }
+    }
+    const int ka = lane < nk ? cellbuf[warp][16 + lane] : INT_MIN + lane;
+    const int kb = lane + 32 < nk ? cellbuf[warp][16 + lane + 32] : INT_MIN + 32 + lane;
+    const bool dup0 = __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, ka)) > 1);
+    const bool dup1 = __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, kb)) > 1);
+    if (lane < 8) {
+        const int v = lane == kHNk ? nk : lane == kHQlen ? qlen : lane == kHFast ? int(fast)
+                    : lane == kHDup0 ? int(dup0) : lane == kHDup1 ? int(dup1) : 0;
+        out[R::HDR + lane] = v;
+    }
+}
+
+// Key-cluster records and reverse-pair records (one warp per key cluster c'):
+// lanes 0..15 hold the key tokens, lanes 16..31 the query tokens of each pair
+// (query clusters listing c' in their neighbourhood, CSR order).
+__global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ rev_off, const int32_t* __restrict__ rev_cl,
+                                 ClusterShape cs, int64_t items, float inv_patch,
+                                 int32_t* __restrict__ krec, int32_t* __restrict__ prec) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t item = int64_t(blockIdx.x) * 4 + warp;
+    if (item >= items) return;
+    const int img = int(item / cs.c), ck = int(item - int64_t(img) * cs.c);
+    const int64_t img_tok = int64_t(img) * cs.n;
+    const int64_t pairs = int64_t(cs.c) * cs.g;
+    const int klen = cs.len(ck);
+    const int rb = rev_off[int64_t(img) * (cs.c + 1) + ck], re = rev_off[int64_t(img) * (cs.c + 1) + ck + 1];
+    int32_t* ko = krec + item * KRec::WORDS;
+    // key side (lanes < 16)
+    const bool kvalid = lane < klen;
+    int ktok = -1;
+    TokInfo kt{};
+    if (kvalid) {
+        ktok = perm[img_tok + cs.off(ck) + lane];
+        kt = make_tokinfo(reinterpret_cast<const float2*>(coords)[img_tok + ktok], inv_patch);
+    }
+    const int kc = kvalid ? tok_cell(kt) : 0;
+    const int kc0 = __shfl_sync(0xffffffffu, kc, 0);
+    if (lane < 16) {
+        ko[KRec::KTOK + lane] = ktok;
+        ko[KRec::KCELL + lane] = kvalid ? kc : kc0;
+    }
+    if (lane < 8) ko[KRec::HDR + lane] = lane == 0 ? klen : lane == 1 ? rb : lane == 2 ? re : 0;
+    const Bbox kb = warp_bbox(kvalid, kt);
+    for (int pr = rb; pr < re; ++pr) {
+        const int qc = rev_cl[int64_t(img) * pairs + pr];
+        const int qlen = cs.len(qc);
+        const int qi = lane - 16;
+        const bool qvalid = lane >= 16 && qi < qlen;
+        int qtok = -1;
+        TokInfo qt{};
+        if (qvalid) {
+            qtok = perm[img_tok + cs.off(qc) + qi];
+            qt = make_tokinfo(reinterpret_cast<const float2*>(coords)[img_tok + qtok], inv_patch);
+        }
+        const int qcell = qvalid ? tok_cell(qt) : 0;
+        const int qcell0 = __shfl_sync(0xffffffffu, qcell, 16);
+        const Bbox qb = warp_bbox(qvalid, qt);
+        const bool fast = warp_one_phase(kvalid || qvalid, kvalid ? kt : qt) && bbox_fits(qb, kb);
+        int32_t* po = prec + (int64_t(img) * pairs + pr) * PRec::WORDS;
+        if (lane >= 16) {
+            po[PRec::QTOK + qi] = qtok;
+            po[PRec::QCELL + qi] = qvalid ? qcell : qcell0;
+        }
+        if (lane < 4) po[PRec::HDR + lane] = lane == 0 ? qlen : lane == 1 ? int(fast) : 0;
+    }
+}
+
 // -------------------------------------------- BiasNet gradient finalize
-// dL/dtheta = sum over table entries of dT * dT/dtheta, plus the tier-3
-// partials; accumulated (+=) into the caller's gradients.
+// Per-CTA partials -> workspace gradient buffers, summed over CTAs in a fixed
+// order (deterministic): window entries are added into the global table
+// gradient (which also holds the tier-2 atomics), MLP and blank partials
+// are written to their buffers.
+__global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx, int hpc, int hd,
+                                        int hidden, float* __restrict__ dtab_g,
+                                        float* __restrict__ mlp_grad, float* __restrict__ blank_grad) {
+    const int h = blockIdx.y, hy = h / hpc, hh = h - hy * hpc;
+    const int pw = part_width(hd);
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= pw) return;
+    float s = 0.f;
+    for (int x = 0; x < gx; ++x) s += part[((size_t(hy) * gx + x) * hpc + hh) * pw + j];
+    if (j < kWs2) {
+        const int oy = j / kWs - kRs, ox = j % kWs - kRs;
+        dtab_g[size_t(h) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] += s;
+    } else if (j < kWs2 + kMG) {
+        const int u = j - kWs2;
+        if (u <= 4 * hidden) mlp_grad[h * (4 * hidden + 1) + u] = s;
+    } else {
+        blank_grad[h * (2 * hd + 1) + (j - kWs2 - kMG)] = s;
+    }
+}
+
+// dL/dtheta = sum over table entries of dT * dT/dtheta, accumulated (+=)
+// into the caller's gradients.
 __global__ void bias_grad_finalize_kernel(const float* __restrict__ dtab, const float* __restrict__ w1,
                                           const float* __restrict__ b1, const float* __restrict__ w2,
                                           int hidden, float* dw1, float* db1, float* dw2, float* db2) {
@@ -36,7 +242,6 @@ __global__ void bias_grad_finalize_kernel(const float* __restrict__ dtab, const 
     const float* dt = dtab + size_t(h) * kWg2;
     __shared__ float red[5][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // db2
     {
         float acc = 0.f;
         for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kWg2; e += gridDim.x * blockDim.x) acc += dt[e];
@@ -113,28 +318,32 @@ __global__ void attn_grad_epilogue_kernel(const float* __restrict__ mlp_grad,
     }
 }
 
-
-template <int HD, int NT, int HPC>
+template <int HD, int KP, int HPC>
 int launch_fwd(const AttnParams& p, cudaStream_t st);
-template <int HD, int NT, int HPC>
-int launch_bwd(const AttnParams& p, cudaStream_t st);
+template <int HD, int KP, int HPC>
+int launch_bwd_q(const AttnParams& p, cudaStream_t st, int& grid_x);
+template <int HD, int HPC>
+int launch_bwd_kv(const AttnParams& p, cudaStream_t st);
 
-int pick_nt(int width) {
-    int need = (width + 1 + 7) / 8;
-    if (need <= 4) return 4;
-    if (need <= 7) return 7;
+// Key slots rounded up to a multiple of 16 (the blank sits at slot KP).
+static int pick_kp(int64_t width) {
+    if (width <= 16) return 16;
+    if (width <= 32) return 32;
+    if (width <= 48) return 48;
+    if (width <= 64) return 64;
     return -1;
 }
 
-static int heads_per_cta(int heads) {
+static int heads_per_cta(int heads, int head_dim) {
     // AFFMAE_HPC (1, 2 or 4) overrides the head-group width for experiments
     static int force = [] {
         const char* e = getenv("AFFMAE_HPC");
         return e ? atoi(e) : 0;
     }();
-    if ((force == 1 || force == 2 || force == 4) && heads % force == 0) return force;
-    if (heads % 4 == 0) return 4;
-    if (heads % 2 == 0) return 2;
+    auto ok = [&](int h) { return heads % h == 0 && h * head_dim <= 128; };
+    if ((force == 1 || force == 2 || force == 4) && ok(force)) return force;
+    for (int h : {4, 2, 1})
+        if (ok(h)) return h;
     return 1;
 }
 
@@ -147,8 +356,8 @@ static int attn_check(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
         return fail(AFFMAE_EUNSUPPORTED, "attention: head_dim must be 16, 32 or 64");
     if (g->max_size > 16)
         return fail(AFFMAE_EUNSUPPORTED, "attention: clusters larger than 16 tokens not compiled");
-    if (pick_nt(int(g->width)) < 0)
-        return fail(AFFMAE_EUNSUPPORTED, "attention: neighbourhood width > 55 not compiled");
+    if (pick_kp(g->width) < 0)
+        return fail(AFFMAE_EUNSUPPORTED, "attention: neighbourhood width > 64 not compiled");
     if (a->bias_hidden > kMaxHidden) return fail(AFFMAE_EUNSUPPORTED, "attention: bias_hidden > 32");
     return AFFMAE_OK;
 }
@@ -157,12 +366,14 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct AttnWs {
     float* tab_g;
-    int32_t* keylist;
+    int32_t* qrec;
+    int32_t* krec;
+    int32_t* prec;
     float* dtab_g;
     float* dsum;
+    float* part;
     float* mlp_grad;
     float* blank_grad;
-    int32_t* inq;
     size_t bytes;
 };
 
@@ -176,54 +387,22 @@ static AttnWs carve_ws(const affmae_cluster_geom* g, const affmae_attn_desc* a, 
         return r;
     };
     const size_t items = size_t(g->batch) * g->n_clusters;
+    const int kp = pick_kp(g->width);
+    const size_t qwords = size_t(32 + 2 * kp + 8);
     w.tab_g = reinterpret_cast<float*>(take(size_t(a->heads) * kWg2 * 4));
-    w.keylist = reinterpret_cast<int32_t*>(take(items * (g->width + 1) * 4));
+    w.qrec = reinterpret_cast<int32_t*>(take(items * qwords * 4));
     if (bwd) {
+        w.krec = reinterpret_cast<int32_t*>(take(items * KRec::WORDS * 4));
+        w.prec = reinterpret_cast<int32_t*>(take(items * g->groups_eff * PRec::WORDS * 4));
         w.dtab_g = reinterpret_cast<float*>(take(size_t(a->heads) * kWg2 * 4));
         w.dsum = reinterpret_cast<float*>(take(size_t(g->batch) * g->tokens * a->heads * 4));
+        w.part = reinterpret_cast<float*>(
+            take(size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));
         w.mlp_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
         w.blank_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
-        w.inq = reinterpret_cast<int32_t*>(take(items * g->groups_eff * 16 * 4));
     }
     w.bytes = off;
     return w;
-}
-
-// Per cluster: the key token of every neighbourhood slot (reference slot
-// order, -1 padding) and, in entry M, the key count nk
-// (cluster_neighborhood, proj/src/geometry.cpp:173-183).
-__global__ void keylist_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ nbr_cl,
-                               ClusterShape cs, int64_t items, int32_t* __restrict__ keylist) {
-    const int M = cs.width;
-    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= items * (M + 1)) return;
-    int64_t item = i / (M + 1);
-    int slot = int(i - item * (M + 1));
-    int img = int(item / cs.c);
-    const int32_t* nb = nbr_cl + item * cs.g;
-    int start = 0, tok = -1;
-    for (int g = 0; g < cs.g; ++g) {
-        int cl = nb[g], len = cs.len(cl);
-        if (slot < M && slot < start + len) {
-            tok = perm[int64_t(img) * cs.n + cs.off(cl) + slot - start];
-            break;
-        }
-        start += len;
-    }
-    keylist[i] = slot == M ? start : tok;
-}
-
-// Per reverse pair (CSR order of rev_cl): the query tokens of the pair's query cluster.
-__global__ void inq_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ rev_cl,
-                           ClusterShape cs, int64_t batch, int32_t* __restrict__ inq) {
-    const int64_t pairs = int64_t(cs.c) * cs.g;
-    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= batch * pairs * 16) return;
-    int j = int(i & 15);
-    int64_t pr = i >> 4;
-    int img = int(pr / pairs);
-    int c = rev_cl[pr];
-    inq[i] = j < cs.len(c) ? perm[int64_t(img) * cs.n + cs.off(c) + j] : -1;
 }
 
 static void fill_common(AttnParams& p, const affmae_cluster_geom* g, const affmae_attn_desc* a,
@@ -255,41 +434,82 @@ static int check_inputs(const affmae_attn_inputs* in) {
     return AFFMAE_OK;
 }
 
-template <bool BWD>
-static int dispatch(const AttnParams& p, int head_dim, int width, cudaStream_t st) {
-    const int nt = pick_nt(width), hpc = heads_per_cta(p.heads);
-#define AFFMAE_CASE(HD_, NT_, HPC_)                                         \
-    if (head_dim == HD_ && nt == NT_ && hpc == HPC_)                        \
-        return BWD ? launch_bwd<HD_, NT_, HPC_>(p, st) : launch_fwd<HD_, NT_, HPC_>(p, st);
-#define AFFMAE_CASE_NT(HD_, HPC_) AFFMAE_CASE(HD_, 4, HPC_) AFFMAE_CASE(HD_, 7, HPC_)
-#define AFFMAE_CASE_HD(HD_) AFFMAE_CASE_NT(HD_, 1) AFFMAE_CASE_NT(HD_, 2) AFFMAE_CASE_NT(HD_, 4)
-    AFFMAE_CASE_HD(16)
-    AFFMAE_CASE_HD(32)
-    AFFMAE_CASE_HD(64)
-#undef AFFMAE_CASE_HD
-#undef AFFMAE_CASE_NT
-#undef AFFMAE_CASE
-    return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
-}
-
+// bias table + query-cluster records (+ key/pair records for the backward)
 static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const int32_t* nbr_cl,
-                   const int32_t* rev_cl, int64_t batch, cudaStream_t st) {
-    int n = p.heads * kWg2;
+                   const int32_t* rev_off, const int32_t* rev_cl, int64_t width, cudaStream_t st) {
+    const int n = p.heads * kWg2;
     bias_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.heads, p.hidden, w.tab_g);
     AFFMAE_LAUNCH_CHECK("bias_table_kernel");
-    int64_t items = batch * p.cs.c;
-    int64_t nk = items * (p.cs.width + 1);
-    keylist_kernel<<<unsigned((nk + 255) / 256), 256, 0, st>>>(perm, nbr_cl, p.cs, items, w.keylist);
-    AFFMAE_LAUNCH_CHECK("keylist_kernel");
+    const int64_t items = int64_t(p.batch) * p.cs.c;
+    const unsigned blocks = unsigned((items + 3) / 4);
+    switch (pick_kp(width)) {
+#define AFFMAE_QREC(KP_)                                                                          \
+    case KP_:                                                                                     \
+        attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(p.coords, perm, nbr_cl, p.cs, items,        \
+                                                      p.inv_patch, w.qrec);                       \
+        break;
+        AFFMAE_QREC(16)
+        AFFMAE_QREC(32)
+        AFFMAE_QREC(48)
+        AFFMAE_QREC(64)
+#undef AFFMAE_QREC
+        default:
+            return fail(AFFMAE_EUNSUPPORTED, "attention: width");
+    }
+    AFFMAE_LAUNCH_CHECK("attn_qrec_kernel");
     if (rev_cl) {
-        int64_t nq = items * p.cs.g * 16;
-        inq_kernel<<<unsigned((nq + 255) / 256), 256, 0, st>>>(perm, rev_cl, p.cs, batch, w.inq);
-        AFFMAE_LAUNCH_CHECK("inq_kernel");
+        attn_krec_kernel<<<blocks, 128, 0, st>>>(p.coords, perm, rev_off, rev_cl, p.cs, items,
+                                                 p.inv_patch, w.krec, w.prec);
+        AFFMAE_LAUNCH_CHECK("attn_krec_kernel");
     }
     p.tab_g = w.tab_g;
-    p.keylist = w.keylist;
-    p.inq = w.inq;
+    p.qrec = w.qrec;
+    p.krec = w.krec;
+    p.prec = w.prec;
     return AFFMAE_OK;
+}
+
+#define AFFMAE_DISPATCH_QK(CALL)                                                              \
+    do {                                                                                      \
+        const int kp = pick_kp(width);                                                        \
+        const int hpc = heads_per_cta(p.heads, head_dim);                                     \
+        AFFMAE_CASE_HD(16, CALL)                                                              \
+        AFFMAE_CASE_HD(32, CALL)                                                              \
+        AFFMAE_CASE_HD(64, CALL)                                                              \
+        return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");            \
+    } while (0)
+#define AFFMAE_CASE(HD_, KP_, HPC_, CALL) \
+    if (head_dim == HD_ && kp == KP_ && hpc == HPC_) return CALL(HD_, KP_, HPC_);
+#define AFFMAE_CASE_KP(HD_, HPC_, CALL)                                                      \
+    AFFMAE_CASE(HD_, 16, HPC_, CALL) AFFMAE_CASE(HD_, 32, HPC_, CALL) AFFMAE_CASE(HD_, 48, HPC_, CALL) \
+    AFFMAE_CASE(HD_, 64, HPC_, CALL)
+#define AFFMAE_CASE_HD(HD_, CALL) \
+    AFFMAE_CASE_KP(HD_, 1, CALL) AFFMAE_CASE_KP(HD_, 2, CALL) AFFMAE_CASE_KP(HD_, 4, CALL)
+
+template <int HD, int KP, int HPC>
+static int call_fwd(const AttnParams& p, cudaStream_t st) {
+    if constexpr (HD * HPC > 128) return fail(AFFMAE_EUNSUPPORTED, "attention: head group too wide");
+    else return launch_fwd<HD, KP, HPC>(p, st);
+}
+template <int HD, int KP, int HPC>
+static int call_bwd(const AttnParams& p, cudaStream_t st, int& gx) {
+    if constexpr (HD * HPC > 128) return fail(AFFMAE_EUNSUPPORTED, "attention: head group too wide");
+    else {
+        int rc = launch_bwd_q<HD, KP, HPC>(p, st, gx);
+        if (rc) return rc;
+        return launch_bwd_kv<HD, HPC>(p, st);
+    }
+}
+
+static int dispatch_fwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st) {
+#define FWD_CALL(HD_, KP_, HPC_) call_fwd<HD_, KP_, HPC_>(p, st)
+    AFFMAE_DISPATCH_QK(FWD_CALL);
+#undef FWD_CALL
+}
+static int dispatch_bwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st, int& gx) {
+#define BWD_CALL(HD_, KP_, HPC_) call_bwd<HD_, KP_, HPC_>(p, st, gx)
+    AFFMAE_DISPATCH_QK(BWD_CALL);
+#undef BWD_CALL
 }
 
 size_t attn_fwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
@@ -314,12 +534,11 @@ int attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
     if (g->batch == 0) return AFFMAE_OK;
     AttnParams p;
     fill_common(p, g, a, in);
-    p.perm = perm;
     p.out = reinterpret_cast<__nv_bfloat16*>(out);
     p.lse = lse;
     cudaStream_t st = as_stream(stream);
-    if ((rc = prepare(p, w, perm, nbr_cl, nullptr, g->batch, st))) return rc;
-    return dispatch<false>(p, a->head_dim, int(g->width), st);
+    if ((rc = prepare(p, w, perm, nbr_cl, nullptr, nullptr, g->width, st))) return rc;
+    return dispatch_fwd(p, a->head_dim, g->width, st);
 }
 
 int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
@@ -338,9 +557,6 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
     if (g->batch == 0) return AFFMAE_OK;
     AttnParams p;
     fill_common(p, g, a, in);
-    p.perm = idx->perm;
-    p.rev_off = idx->rev_off;
-    p.out = const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(out));
     p.lse = const_cast<float*>(lse);
     p.dout = reinterpret_cast<const __nv_bfloat16*>(dout);
     p.dq = reinterpret_cast<__nv_bfloat16*>(gr->dq);
@@ -348,14 +564,17 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
     p.dv = reinterpret_cast<__nv_bfloat16*>(gr->dv);
     p.dsum = w.dsum;
     p.dtab_g = w.dtab_g;
-    p.mlp_grad = w.mlp_grad;
-    p.blank_grad = w.blank_grad;
+    p.part = w.part;
     cudaStream_t st = as_stream(stream);
-    if ((rc = prepare(p, w, idx->perm, idx->nbr_cl, idx->rev_cl, g->batch, st))) return rc;
+    if ((rc = prepare(p, w, idx->perm, idx->nbr_cl, idx->rev_off, idx->rev_cl, g->width, st))) return rc;
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.dtab_g, 0, size_t(a->heads) * kWg2 * 4, st));
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.mlp_grad, 0, size_t(a->heads) * (4 * a->bias_hidden + 1) * 4, st));
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.blank_grad, 0, size_t(a->heads) * (2 * a->head_dim + 1) * 4, st));
-    if ((rc = dispatch<true>(p, a->head_dim, int(g->width), st))) return rc;
+    int gx = 0;
+    if ((rc = dispatch_bwd(p, a->head_dim, g->width, st, gx))) return rc;
+    const int hpc = heads_per_cta(a->heads, a->head_dim);
+    const int pw = part_width(a->head_dim);
+    attn_part_reduce_kernel<<<dim3((pw + 127) / 128, a->heads), 128, 0, st>>>(
+        w.part, gx, hpc, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
+    AFFMAE_LAUNCH_CHECK("attn_part_reduce_kernel");
     bias_grad_finalize_kernel<<<dim3(16, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
                                                                   a->bias_hidden, gr->dw1, gr->db1,
                                                                   gr->dw2, gr->db2);

@@ -3,10 +3,14 @@
 #include "attn_kernels.cuh"
 
 namespace affmae_b200 {
-AFFMAE_INSTANTIATE_ATTN(64, 4, 1)
-AFFMAE_INSTANTIATE_ATTN(64, 4, 2)
-AFFMAE_INSTANTIATE_ATTN(64, 4, 4)
-AFFMAE_INSTANTIATE_ATTN(64, 7, 1)
-AFFMAE_INSTANTIATE_ATTN(64, 7, 2)
-AFFMAE_INSTANTIATE_ATTN(64, 7, 4)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 16, 1)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 32, 1)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 48, 1)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 64, 1)
+AFFMAE_INSTANTIATE_ATTN_KV(64, 1)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 16, 2)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 32, 2)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 48, 2)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 64, 2)
+AFFMAE_INSTANTIATE_ATTN_KV(64, 2)
 }  // namespace affmae_b200
