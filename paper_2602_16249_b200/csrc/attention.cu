@@ -147,7 +147,8 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     const bool dup1 = __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, kb)) > 1);
     if (lane < 8) {
         const int v = lane == kHNk ? nk : lane == kHQlen ? qlen : lane == kHFast ? int(fast)
-                    : lane == kHDup0 ? int(dup0) : lane == kHDup1 ? int(dup1) : 0;
+                    : lane == kHDup0 ? int(dup0) : lane == kHDup1 ? int(dup1)
+                    : lane == kHImgTok ? int(img_tok) : 0;
         out[R::HDR + lane] = v;
     }
 }
@@ -182,7 +183,9 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
         ko[KRec::KTOK + lane] = ktok;
         ko[KRec::KCELL + lane] = kvalid ? kc : kc0;
     }
-    if (lane < 8) ko[KRec::HDR + lane] = lane == 0 ? klen : lane == 1 ? rb : lane == 2 ? re : 0;
+    if (lane < 8)
+        ko[KRec::HDR + lane] = lane == 0 ? klen : lane == 1 ? rb : lane == 2 ? re
+                             : lane == 3 ? int(int64_t(img) * pairs + rb) : 0;
     const Bbox kb = warp_bbox(kvalid, kt);
     for (int pr = rb; pr < re; ++pr) {
         const int qc = rev_cl[int64_t(img) * pairs + pr];
@@ -204,7 +207,12 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
             po[PRec::QTOK + qi] = qtok;
             po[PRec::QCELL + qi] = qvalid ? qcell : qcell0;
         }
-        if (lane < 4) po[PRec::HDR + lane] = lane == 0 ? qlen : lane == 1 ? int(fast) : 0;
+        if (lane < 8) {
+            const int v = lane == kPQlen ? qlen : lane == kPFast ? int(fast) : lane == kPFirst ? int(pr == rb)
+                        : lane == kPLast ? int(pr == re - 1) : lane == kPItem ? int(item)
+                        : lane == kPIdx ? int(int64_t(img) * pairs + pr) : 0;
+            po[PRec::HDR + lane] = v;
+        }
     }
 }
 
@@ -213,15 +221,15 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
 // order (deterministic): window entries are added into the global table
 // gradient (which also holds the tier-2 atomics), MLP and blank partials
 // are written to their buffers.
-__global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx, int hpc, int hd,
-                                        int hidden, float* __restrict__ dtab_g,
-                                        float* __restrict__ mlp_grad, float* __restrict__ blank_grad) {
-    const int h = blockIdx.y, hy = h / hpc, hh = h - hy * hpc;
+__global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx, int hd, int hidden,
+                                        float* __restrict__ dtab_g, float* __restrict__ mlp_grad,
+                                        float* __restrict__ blank_grad) {
+    const int h = blockIdx.y;
     const int pw = part_width(hd);
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= pw) return;
     float s = 0.f;
-    for (int x = 0; x < gx; ++x) s += part[((size_t(hy) * gx + x) * hpc + hh) * pw + j];
+    for (int x = 0; x < gx; ++x) s += part[(size_t(h) * gx + x) * pw + j];
     if (j < kWs2) {
         const int oy = j / kWs - kRs, ox = j % kWs - kRs;
         dtab_g[size_t(h) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] += s;
@@ -318,11 +326,11 @@ __global__ void attn_grad_epilogue_kernel(const float* __restrict__ mlp_grad,
     }
 }
 
-template <int HD, int KP, int HPC>
+template <int HD, int KP>
 int launch_fwd(const AttnParams& p, cudaStream_t st);
-template <int HD, int KP, int HPC>
+template <int HD, int KP>
 int launch_bwd_q(const AttnParams& p, cudaStream_t st, int& grid_x);
-template <int HD, int HPC>
+template <int HD>
 int launch_bwd_kv(const AttnParams& p, cudaStream_t st);
 
 // Key slots rounded up to a multiple of 16 (the blank sits at slot KP).
@@ -332,19 +340,6 @@ static int pick_kp(int64_t width) {
     if (width <= 48) return 48;
     if (width <= 64) return 64;
     return -1;
-}
-
-static int heads_per_cta(int heads, int head_dim) {
-    // AFFMAE_HPC (1, 2 or 4) overrides the head-group width for experiments
-    static int force = [] {
-        const char* e = getenv("AFFMAE_HPC");
-        return e ? atoi(e) : 0;
-    }();
-    auto ok = [&](int h) { return heads % h == 0 && h * head_dim <= 128; };
-    if ((force == 1 || force == 2 || force == 4) && ok(force)) return force;
-    for (int h : {4, 2, 1})
-        if (ok(h)) return h;
-    return 1;
 }
 
 static int attn_check(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
@@ -397,7 +392,7 @@ static AttnWs carve_ws(const affmae_cluster_geom* g, const affmae_attn_desc* a, 
         w.dtab_g = reinterpret_cast<float*>(take(size_t(a->heads) * kWg2 * 4));
         w.dsum = reinterpret_cast<float*>(take(size_t(g->batch) * g->tokens * a->heads * 4));
         w.part = reinterpret_cast<float*>(
-            take(size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));
+            take(size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [h][CTA]
         w.mlp_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
         w.blank_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
     }
@@ -469,47 +464,30 @@ static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const in
     return AFFMAE_OK;
 }
 
-#define AFFMAE_DISPATCH_QK(CALL)                                                              \
-    do {                                                                                      \
-        const int kp = pick_kp(width);                                                        \
-        const int hpc = heads_per_cta(p.heads, head_dim);                                     \
-        AFFMAE_CASE_HD(16, CALL)                                                              \
-        AFFMAE_CASE_HD(32, CALL)                                                              \
-        AFFMAE_CASE_HD(64, CALL)                                                              \
-        return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");            \
-    } while (0)
-#define AFFMAE_CASE(HD_, KP_, HPC_, CALL) \
-    if (head_dim == HD_ && kp == KP_ && hpc == HPC_) return CALL(HD_, KP_, HPC_);
-#define AFFMAE_CASE_KP(HD_, HPC_, CALL)                                                      \
-    AFFMAE_CASE(HD_, 16, HPC_, CALL) AFFMAE_CASE(HD_, 32, HPC_, CALL) AFFMAE_CASE(HD_, 48, HPC_, CALL) \
-    AFFMAE_CASE(HD_, 64, HPC_, CALL)
-#define AFFMAE_CASE_HD(HD_, CALL) \
-    AFFMAE_CASE_KP(HD_, 1, CALL) AFFMAE_CASE_KP(HD_, 2, CALL) AFFMAE_CASE_KP(HD_, 4, CALL)
-
-template <int HD, int KP, int HPC>
-static int call_fwd(const AttnParams& p, cudaStream_t st) {
-    if constexpr (HD * HPC > 128) return fail(AFFMAE_EUNSUPPORTED, "attention: head group too wide");
-    else return launch_fwd<HD, KP, HPC>(p, st);
-}
-template <int HD, int KP, int HPC>
-static int call_bwd(const AttnParams& p, cudaStream_t st, int& gx) {
-    if constexpr (HD * HPC > 128) return fail(AFFMAE_EUNSUPPORTED, "attention: head group too wide");
-    else {
-        int rc = launch_bwd_q<HD, KP, HPC>(p, st, gx);
-        if (rc) return rc;
-        return launch_bwd_kv<HD, HPC>(p, st);
-    }
-}
-
 static int dispatch_fwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st) {
-#define FWD_CALL(HD_, KP_, HPC_) call_fwd<HD_, KP_, HPC_>(p, st)
-    AFFMAE_DISPATCH_QK(FWD_CALL);
-#undef FWD_CALL
+    const int kp = pick_kp(width);
+#define AFFMAE_CASE(HD_, KP_) \
+    if (head_dim == HD_ && kp == KP_) return launch_fwd<HD_, KP_>(p, st);
+#define AFFMAE_CASE_HD(HD_) AFFMAE_CASE(HD_, 16) AFFMAE_CASE(HD_, 32) AFFMAE_CASE(HD_, 48) AFFMAE_CASE(HD_, 64)
+    AFFMAE_CASE_HD(16)
+    AFFMAE_CASE_HD(32)
+    AFFMAE_CASE_HD(64)
+#undef AFFMAE_CASE
+    return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
 }
 static int dispatch_bwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st, int& gx) {
-#define BWD_CALL(HD_, KP_, HPC_) call_bwd<HD_, KP_, HPC_>(p, st, gx)
-    AFFMAE_DISPATCH_QK(BWD_CALL);
-#undef BWD_CALL
+    const int kp = pick_kp(width);
+#define AFFMAE_CASE(HD_, KP_)                                  \
+    if (head_dim == HD_ && kp == KP_) {                        \
+        int rc = launch_bwd_q<HD_, KP_>(p, st, gx);            \
+        return rc ? rc : launch_bwd_kv<HD_>(p, st);            \
+    }
+    AFFMAE_CASE_HD(16)
+    AFFMAE_CASE_HD(32)
+    AFFMAE_CASE_HD(64)
+#undef AFFMAE_CASE
+#undef AFFMAE_CASE_HD
+    return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
 }
 
 size_t attn_fwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
@@ -570,10 +548,9 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.dtab_g, 0, size_t(a->heads) * kWg2 * 4, st));
     int gx = 0;
     if ((rc = dispatch_bwd(p, a->head_dim, g->width, st, gx))) return rc;
-    const int hpc = heads_per_cta(a->heads, a->head_dim);
     const int pw = part_width(a->head_dim);
     attn_part_reduce_kernel<<<dim3((pw + 127) / 128, a->heads), 128, 0, st>>>(
-        w.part, gx, hpc, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
+        w.part, gx, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
     AFFMAE_LAUNCH_CHECK("attn_part_reduce_kernel");
     bias_grad_finalize_kernel<<<dim3(16, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
                                                                   a->bias_hidden, gr->dw1, gr->db1,

@@ -3,19 +3,9 @@
 #include "attn_kernels.cuh"
 
 namespace affmae_b200 {
-AFFMAE_INSTANTIATE_ATTN_QK(16, 16, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 32, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 48, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 64, 1)
-AFFMAE_INSTANTIATE_ATTN_KV(16, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 16, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 32, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 48, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 64, 2)
-AFFMAE_INSTANTIATE_ATTN_KV(16, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 16, 4)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 32, 4)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 48, 4)
-AFFMAE_INSTANTIATE_ATTN_QK(16, 64, 4)
-AFFMAE_INSTANTIATE_ATTN_KV(16, 4)
+AFFMAE_INSTANTIATE_ATTN_QK(16, 16)
+AFFMAE_INSTANTIATE_ATTN_QK(16, 32)
+AFFMAE_INSTANTIATE_ATTN_QK(16, 48)
+AFFMAE_INSTANTIATE_ATTN_QK(16, 64)
+AFFMAE_INSTANTIATE_ATTN_KV(16)
 }  // namespace affmae_b200

@@ -3,19 +3,9 @@
 #include "attn_kernels.cuh"
 
 namespace affmae_b200 {
-AFFMAE_INSTANTIATE_ATTN_QK(32, 16, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 32, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 48, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 64, 1)
-AFFMAE_INSTANTIATE_ATTN_KV(32, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 16, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 32, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 48, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 64, 2)
-AFFMAE_INSTANTIATE_ATTN_KV(32, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 16, 4)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 32, 4)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 48, 4)
-AFFMAE_INSTANTIATE_ATTN_QK(32, 64, 4)
-AFFMAE_INSTANTIATE_ATTN_KV(32, 4)
+AFFMAE_INSTANTIATE_ATTN_QK(32, 16)
+AFFMAE_INSTANTIATE_ATTN_QK(32, 32)
+AFFMAE_INSTANTIATE_ATTN_QK(32, 48)
+AFFMAE_INSTANTIATE_ATTN_QK(32, 64)
+AFFMAE_INSTANTIATE_ATTN_KV(32)
 }  // namespace affmae_b200

@@ -3,14 +3,9 @@
 #include "attn_kernels.cuh"
 
 namespace affmae_b200 {
-AFFMAE_INSTANTIATE_ATTN_QK(64, 16, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 32, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 48, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 64, 1)
-AFFMAE_INSTANTIATE_ATTN_KV(64, 1)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 16, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 32, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 48, 2)
-AFFMAE_INSTANTIATE_ATTN_QK(64, 64, 2)
-AFFMAE_INSTANTIATE_ATTN_KV(64, 2)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 16)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 32)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 48)
+AFFMAE_INSTANTIATE_ATTN_QK(64, 64)
+AFFMAE_INSTANTIATE_ATTN_KV(64)
 }  // namespace affmae_b200

@@ -9,24 +9,24 @@
 //     S = Q_c (16 x d) . [K_nb ; blank_k]^T + bias,   O = softmax(S) . [V_nb ; blank_v]
 // on one m16 tensor-core tile (mma.sync m16n8k16 bf16, fp32 accumulate).
 //
-// Pipeline.  Every kernel is persistent (grid = SMs x resident CTAs; blockIdx.y
-// = head group of HPC heads) and warp-specialised:
-//   * one PRODUCER warp walks the CTA's items, copies the item's plan record
-//     (token ids, lattice cells, flags; built once per call by the plan
-//     kernels in attention.cu) into a ring stage and gathers every row the
-//     item needs (HPC*d bf16 per token) with 16-byte cp.async, whose
-//     completion the stage's `full` mbarrier tracks (cp.async.mbarrier.arrive);
-//   * HPC CONSUMER warps (one per head) wait on `full`, run the tile maths
-//     from shared memory, write their outputs and release the stage on
-//     `empty`.
-// With STAGES ring slots the gathers of the next item(s) overlap the maths of
-// the current one; there is no CTA-wide barrier inside the item loop.
+// Execution model: warp-autonomous.  A CTA is ONE warp that owns ONE head
+// (blockIdx.y) and walks the items blockIdx.x, +gridDim.x, ... (persistent
+// grid, ~SMs x resident warps).  The warp gathers only its head's d-column
+// slice of every row (HD*2 bytes: 8 rows per 16-byte cp.async instruction at
+// d = 32) into padded shared rows (ldmatrix conflict-free), so warps never
+// wait on each other -- the heads of a token row are independent slices.
+// Software pipeline, per warp, with cp.async groups:
+//     plan record of item i+2 -> record ring (3)      (issued at iteration i)
+//     rows of item i+1        -> row ring (2)         (tokens from record i+1)
+//     compute item i                                  (rows landed: wait_group 2)
+// so the gathers of the next item overlap the maths of the current one and
+// the record latency is hidden two items deep.
 //
 // Slot layout of a query-cluster item (KP = key slots rounded up to 16):
 //   slots [0, nk) keys in reference order, [nk, KP) padding (masked),
-//   slot KP the blank (K/V rows KP..KP+7 are static: blank row + zeros).
-// The blank is one column of the score tile; its P.V contribution is a rank-1
-// FFMA update (P_blank x blank_v), so V needs only KP rows in the forward.
+//   slot KP the blank: a static 8-row tile (blank row + zeros) forms the last
+//   n-tile of the score product; its P.V / dS.K contributions are rank-1
+//   FFMA updates, so the row ring holds only KP key/value rows.
 //
 // Relative-position bias (attn_common.cuh): on lattice-"fast" items (every
 // token on one patch-lattice phase, every pair offset inside the shared
@@ -38,12 +38,12 @@
 //   attn_bwd_q_kernel  (per query cluster) recomputes P = exp(S - LSE),
 //       dP = dO.V^T, D = rowsum(P o dP), dS = P (dP - D); writes dQ = dS.K/sqrt(d)
 //       and D; blank grads (tensor-core rank-1 products); scatters dS into the
-//       CTA's bias-table gradient window (row-major, conflict-free).
+//       warp's bias-table gradient window (row-major, conflict-free).
 //   attn_bwd_kv_kernel (per key cluster c') walks the reverse-neighbour pairs
-//       (query clusters whose neighbourhood holds c', ascending; up to KDEG per
-//       ring stage) and accumulates dK = dS^T.Q/sqrt(d), dV = P^T.dO in
+//       (query clusters whose neighbourhood holds c', ascending), one pair per
+//       pipeline round, and accumulates dK = dS^T.Q/sqrt(d), dV = P^T.dO in
 //       registers: every key row is written once, in a fixed order.
-// Per-CTA parameter-gradient partials (bias-table window, blank, BiasNet MLP
+// Per-warp parameter-gradient partials (bias-table window, blank, BiasNet MLP
 // tier) go to a [CTA] buffer reduced in a fixed order afterwards: the
 // backward is deterministic except for tier-2 (far-offset, same-phase) pairs.
 #pragma once
@@ -58,17 +58,19 @@ namespace affmae_b200 {
 template <int KP>
 struct QRec {
     static constexpr int QTOK = 0, KTOK = 16, QCELL = 16 + KP, KCELL = 32 + KP, HDR = 32 + 2 * KP;
-    static constexpr int WORDS = HDR + 8;  // multiple of 4 (16-byte rows)
+    static constexpr int WORDS = HDR + 8;  // multiple of 4 (16-byte copies)
 };
-enum { kHNk = 0, kHQlen = 1, kHFast = 2, kHDup0 = 3, kHDup1 = 4 };
-// Key-cluster record: ktok[16] kcell[16] hdr{klen, rb, re}
+enum { kHNk = 0, kHQlen = 1, kHFast = 2, kHDup0 = 3, kHDup1 = 4, kHImgTok = 5 };  // img_tok = image * N
+// Key-cluster record: ktok[16] kcell[16] hdr{klen, rb, re, first pair (global)}
 struct KRec {
     static constexpr int KTOK = 0, KCELL = 16, HDR = 32, WORDS = 40;
 };
-// Reverse pair record (CSR order of rev_cl): qtok[16] qcell[16] hdr{qlen, fast}
+// Reverse pair record (CSR order of rev_cl):
+//   qtok[16] qcell[16] hdr{qlen, fast, first, last, key item, global pair index}
 struct PRec {
-    static constexpr int QTOK = 0, QCELL = 16, HDR = 32, WORDS = 36;
+    static constexpr int QTOK = 0, QCELL = 16, HDR = 32, WORDS = 40;
 };
+enum { kPQlen = 0, kPFast = 1, kPFirst = 2, kPLast = 3, kPItem = 4, kPIdx = 5 };
 constexpr int kWinC = kRs * kWs + kRs;  // window index of offset (0, 0)
 constexpr int kMG = 4 * kMaxHidden + 1;  // tier-3 MLP grad accumulator per head
 
@@ -79,9 +81,9 @@ struct AttnParams {
     const __nv_bfloat16* bk;
     const __nv_bfloat16* bv;
     const float* coords;
-    const int32_t* qrec;     // [B*C][QRec::WORDS]
-    const int32_t* krec;     // [B*C][KRec::WORDS]
-    const int32_t* prec;     // [B][C*G][PRec::WORDS]
+    const int32_t* qrec;  // [B*C][QRec::WORDS]
+    const int32_t* krec;  // [B*C][KRec::WORDS]
+    const int32_t* prec;  // [B*C*G][PRec::WORDS]
     const float* w1;
     const float* b1;
     const float* w2;
@@ -94,9 +96,9 @@ struct AttnParams {
     __nv_bfloat16* dq;
     __nv_bfloat16* dk;
     __nv_bfloat16* dv;
-    float* dsum;     // [B, N, heads]  D = rowsum(P o dP)
-    float* dtab_g;   // [heads][kWg2] tier-2 gradient (atomics)
-    float* part;     // [CTAs][HPC][kPartW] per-CTA gradient partials
+    float* dsum;    // [B, N, heads]  D = rowsum(P o dP)
+    float* dtab_g;  // [heads][kWg2] tier-2 gradient (atomics)
+    float* part;    // [heads][CTAs][part_width] per-warp gradient partials
     ClusterShape cs;
     int batch;
     int heads;
@@ -104,75 +106,39 @@ struct AttnParams {
     float inv_patch;
     float scale;  // 1/sqrt(d)
 };
-// per-CTA, per-head partial: window dT [kWs2] | MLP grads [kMG] | blank {dbk[d], dbv[d], dblank}
+// per-warp partial: window dT [kWs2] | MLP grads [kMG] | blank {dbk[d], dbv[d], dblank}
 __host__ __device__ constexpr int part_width(int hd) { return kWs2 + kMG + 2 * hd + 1; }
 
 // ---------------------------------------------------------------- helpers
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ int4 ldg_nc4(const int32_t* p) {
-    return __ldg(reinterpret_cast<const int4*>(p));
-}
-// Arrive on `bar` once every cp.async this thread issued so far has landed
-// (pending count +1 now, -1 at completion: the phase cannot complete early).
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Producer-warp row gather: `nrows` rows of ROWB bytes, row r from
-// src(r) (global) to dst(r) (shared), as 16-byte cp.async -- each warp
-// instruction moves 32 / (ROWB/16) whole rows.  (One cp.async.bulk per row
-// is TMA-request-bound at these 128-256 B rows.)
-template <int ROWB, typename SrcDst>
-__device__ __forceinline__ void gather_rows(int nrows, int lane, SrcDst f) {
-    constexpr int CPR = ROWB / 16, RPI = 32 / CPR;
-    const int sub = lane / CPR, ch = lane - sub * CPR;
-    for (int r = sub; r < nrows; r += RPI) {
-        const __nv_bfloat16* src;
-        __nv_bfloat16* dst;
-        f(r, src, dst);
-        cp_async16(dst + ch * 8, src + ch * 8);
-    }
-}
-
-// Zero a shared-memory range (16-byte granules) with the whole CTA.
+// Zero a shared-memory range (16-byte granules) with the warp.
 __device__ __forceinline__ void zero_shared(void* base, size_t bytes) {
     uint4* p = reinterpret_cast<uint4*>(base);
-    for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+    for (size_t i = threadIdx.x; i < bytes / 16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
 }
-
-// Bias-table window of heads h0..h0+HPC into shared memory, pre-scaled by log2(e).
-template <int HPC>
-__device__ __forceinline__ void load_window(float* tab, const AttnParams& p, int h0) {
-    for (int i = threadIdx.x; i < HPC * kWs2; i += blockDim.x) {
-        const int hh = i / kWs2, e = i - hh * kWs2;
+// Record words -> shared (16-byte cp.async chunks).
+template <int WORDS>
+__device__ __forceinline__ void copy_rec(int32_t* dst, const int32_t* src, int lane) {
+    static_assert(WORDS % 4 == 0, "record rows are 16-byte multiples");
+#pragma unroll
+    for (int c = lane; c < WORDS / 4; c += 32) cp_async16(dst + 4 * c, src + 4 * c);
+}
+// Bias-table window of head h into shared memory, pre-scaled by log2(e), and
+// the head's BiasNet MLP parameters (tier 3).
+__device__ __forceinline__ void load_head_bias(float* tab, float4* units, const AttnParams& p, int h) {
+    for (int e = threadIdx.x; e < kWs2; e += 32) {
         const int oy = e / kWs - kRs, ox = e % kWs - kRs;
-        tab[i] = p.tab_g[size_t(h0 + hh) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] * kLog2e;
+        tab[e] = p.tab_g[size_t(h) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] * kLog2e;
     }
-}
-// BiasNet MLP parameters (tier 3) of heads h0..h0+HPC.
-template <int HPC>
-__device__ __forceinline__ void load_units(float4* units, float* b2s, const AttnParams& p, int h0) {
-    for (int i = threadIdx.x; i < HPC * p.hidden; i += blockDim.x) {
-        const int hh = i / p.hidden, u = i - hh * p.hidden, h = h0 + hh;
-        units[hh * kMaxHidden + u] =
-            make_float4(p.w1[h * 2 * p.hidden + u], p.w1[h * 2 * p.hidden + p.hidden + u],
-                        p.b1[h * p.hidden + u], p.w2[h * p.hidden + u]);
-    }
-    for (int i = threadIdx.x; i < HPC; i += blockDim.x) b2s[i] = p.b2[h0 + i];
+    for (int u = threadIdx.x; u < p.hidden; u += 32)
+        units[u] = make_float4(p.w1[h * 2 * p.hidden + u], p.w1[h * 2 * p.hidden + p.hidden + u],
+                               p.b1[h * p.hidden + u], p.w2[h * p.hidden + u]);
 }
 
 // Exact bias (times log2 e) of one pair on a non-fast item: window, global
 // table or the BiasNet MLP itself (tiers of attn_common.cuh).
 static __device__ __noinline__ float slow_bias2(const AttnParams& p, const float* tab_s,
-                                                const float4* units, float b2, int h,
-                                                int64_t img_tok, int qt, int kt) {
+                                                const float4* units, int h, int64_t img_tok, int qt,
+                                                int kt) {
     const float2 qxy = __ldg(reinterpret_cast<const float2*>(p.coords) + img_tok + qt);
     const float2 kxy = __ldg(reinterpret_cast<const float2*>(p.coords) + img_tok + kt);
     const TokInfo qi = make_tokinfo(qxy, p.inv_patch), ki = make_tokinfo(kxy, p.inv_patch);
@@ -180,10 +146,10 @@ static __device__ __noinline__ float slow_bias2(const AttnParams& p, const float
     const int li = lut_index(qi, ki, gi);
     if (li >= 0) return tab_s[li];
     if (gi >= 0) return __ldg(p.tab_g + size_t(h) * kWg2 + gi) * kLog2e;
-    return bias_mlp(units, p.hidden, b2, (kxy.x - qxy.x) * p.inv_patch, (kxy.y - qxy.y) * p.inv_patch) *
-           kLog2e;
+    return bias_mlp(units, p.hidden, p.b2[h], (kxy.x - qxy.x) * p.inv_patch,
+                    (kxy.y - qxy.y) * p.inv_patch) * kLog2e;
 }
-// Its gradient: += ds into the CTA window / the global table / the MLP partials.
+// Its gradient: += ds into the warp window / the global table / the MLP partials.
 static __device__ __noinline__ void slow_bias_grad(const AttnParams& p, float* dtab_s,
                                                    const float4* units, float* mlpg, int h,
                                                    int64_t img_tok, int qt, int kt, float ds) {
@@ -197,21 +163,22 @@ static __device__ __noinline__ void slow_bias_grad(const AttnParams& p, float* d
     else bias_mlp_grad(units, p.hidden, ds, (kxy.x - qxy.x) * p.inv_patch, (kxy.y - qxy.y) * p.inv_patch, mlpg);
 }
 
-// A-operand fragments of a 16-row tile (rows at stride RW, columns from `base`).
+// A-operand fragments of a 16-row tile (rows at stride RW).
 template <int HD, int RW>
 __device__ __forceinline__ void load_a16(uint32_t (&a)[HD / 16][4], const __nv_bfloat16* base, int lane) {
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk)
         ldmatrix_x4(a[kk][0], a[kk][1], a[kk][2], a[kk][3], base + (lane & 15) * RW + kk * 16 + (lane >> 4) * 8);
 }
-// s[nt] = A(16 x HD) . B(rows nt*8 .. nt*8+7)^T for nt < NT.
+// s[nt] = A(16 x HD) . B_nt^T, B_nt = rows nt*8.. of `b` (nt < NT-1) or the
+// 8-row tile `blast` (nt = NT-1; pass b + (NT-1)*8*RW for one contiguous buffer).
 template <int HD, int NT, int RW>
 __device__ __forceinline__ void mma_abt(float (&s)[NT][4], const uint32_t (&a)[HD / 16][4],
-                                        const __nv_bfloat16* b, int lane) {
+                                        const __nv_bfloat16* b, const __nv_bfloat16* blast, int lane) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
         s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-        const __nv_bfloat16* kb = b + (nt * 8 + (lane & 7)) * RW;
+        const __nv_bfloat16* kb = (nt == NT - 1 ? blast : b + nt * 8 * RW) + (lane & 7) * RW;
         if constexpr (HD >= 32) {
 #pragma unroll
             for (int k2 = 0; k2 < HD / 32; ++k2) {
@@ -258,16 +225,34 @@ __device__ __forceinline__ void frags_to_rows(__nv_bfloat16* sm, const float (&o
         *reinterpret_cast<uint32_t*>(sm + (r0 + 8) * RW + nd * 8 + c0) = pack_bf16(o[nd][2] * m1, o[nd][3] * m1);
     }
 }
-// Shared rows (this head's HD columns) -> global token rows, 16-byte stores.
+// Shared rows (HD columns) -> global token rows `g + tok*ld`, 16-byte stores.
 template <int HD, int RW>
-__device__ __forceinline__ void rows_to_global(__nv_bfloat16* g, int64_t img_tok, int hd_all, int hcol,
-                                               const __nv_bfloat16* sm, const int32_t* tok, int nrows,
-                                               int lane) {
+__device__ __forceinline__ void rows_to_global(__nv_bfloat16* g, int64_t ld, const __nv_bfloat16* sm,
+                                               const int32_t* tok, int nrows, int lane) {
     constexpr int CPR = HD / 8;
     for (int i = lane; i < nrows * CPR; i += 32) {
         const int r = i / CPR, ch = i - r * CPR;
-        *reinterpret_cast<uint4*>(g + (img_tok + tok[r]) * hd_all + hcol + ch * 8) =
+        *reinterpret_cast<uint4*>(g + int64_t(tok[r]) * ld + ch * 8) =
             *reinterpret_cast<const uint4*>(sm + r * RW + ch * 8);
+    }
+}
+// Gather rows [0, NROWS) of a virtual row list: row r is token tok(r) of the
+// image slice `src(r)` into `dst(r)`; tok < 0 rows are skipped.  Each warp
+// instruction moves 32 / (HD/8) rows (16-byte cp.async per lane).
+template <int HD, int NROWS, typename F>
+__device__ __forceinline__ void gather(int lane, int64_t ld, F f) {
+    constexpr int CPR = HD / 8, RPI = 32 / CPR;
+    const int sub = lane / CPR, ch = lane - sub * CPR;
+#pragma unroll
+    for (int j = 0; j < (NROWS + RPI - 1) / RPI; ++j) {
+        const int r = sub + j * RPI;
+        if (r < NROWS) {
+            int tok;
+            const __nv_bfloat16* src;
+            __nv_bfloat16* dst;
+            f(r, tok, src, dst);
+            if (tok >= 0) cp_async16(dst + ch * 8, src + int64_t(tok) * ld + ch * 8);
+        }
     }
 }
 
@@ -276,8 +261,8 @@ __device__ __forceinline__ void rows_to_global(__nv_bfloat16* g, int64_t img_tok
 template <int KP, int NT>
 __device__ __forceinline__ void score_bias(float (&s)[NT][4], const int32_t* rec, const float* tab,
                                            float scale2, float blank2, int nk, bool fast, int lane,
-                                           const AttnParams& p, const float4* units, float b2,
-                                           int h, int64_t img_tok) {
+                                           const AttnParams& p, const float4* units, int h,
+                                           int64_t img_tok) {
     using R = QRec<KP>;
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
     if (fast) {
@@ -299,8 +284,7 @@ __device__ __forceinline__ void score_bias(float (&s)[NT][4], const int32_t* rec
             for (int e = 0; e < 4; ++e) {
                 const int slot = nt * 8 + c0 + (e & 1);
                 const int kt = slot < nk ? rec[R::KTOK + slot] : rec[R::KTOK];
-                s[nt][e] = fmaf(s[nt][e], scale2,
-                                slow_bias2(p, tab, units, b2, h, img_tok, e >= 2 ? qb : qa, kt));
+                s[nt][e] = fmaf(s[nt][e], scale2, slow_bias2(p, tab, units, h, img_tok, e >= 2 ? qb : qa, kt));
             }
         }
     }
@@ -318,116 +302,353 @@ __device__ __forceinline__ void score_bias(float (&s)[NT][4], const int32_t* rec
     s[NT - 1][1] = s[NT - 1][3] = -INFINITY;
 }
 
+// Static blank tile: row 0 = blank vector of head h, rows 1..7 zero.
+template <int HD, int RW>
+__device__ __forceinline__ void init_blank_tile(__nv_bfloat16* t, const __nv_bfloat16* blank, int h) {
+    for (int i = threadIdx.x; i < 8 * RW; i += 32) {
+        const int r = i / RW, c = i - r * RW;
+        t[i] = (r == 0 && c < HD) ? blank[h * HD + c] : __float2bfloat16(0.f);
+    }
+}
+
+// ======================================================= swizzled row tiles
+// Dense rows of HD bf16 (HD*2 bytes = CPR 16-byte chunks), chunk c of row r
+// stored at chunk c ^ sw(r): 8 consecutive rows read at one logical chunk hit
+// 8 distinct 16-byte bank groups (ldmatrix / ldmatrix.trans conflict-free
+// without padding).  For 8-row-aligned tiles sw(r) depends on r & 7 only, so
+// every lane's swizzle term is a per-lane constant.
+template <int HD>
+struct Swz {
+    static constexpr int CPR = HD / 8;                       // chunks per row
+    static constexpr int SH = CPR == 8 ? 0 : CPR == 4 ? 1 : 2;  // log2(8 / CPR)
+    __device__ static __forceinline__ int sw(int r) { return (r >> SH) & (CPR - 1); }
+    // element offset of (row r, logical chunk c)
+    __device__ static __forceinline__ int at(int r, int c) { return r * HD + ((c ^ sw(r)) << 3); }
+};
+
+template <int HD>
+__device__ __forceinline__ void sw_load_a16(uint32_t (&a)[HD / 16][4], const __nv_bfloat16* base, int lane) {
+    using S = Swz<HD>;
+    const int r = lane & 15;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk)
+        ldmatrix_x4(a[kk][0], a[kk][1], a[kk][2], a[kk][3], base + S::at(r, 2 * kk + (lane >> 4)));
+}
+// s[nt] = A(16 x HD) . B_nt^T; B_nt = rows nt*8.. of `b` (nt < NT-1), or the tile `blast`.
+template <int HD, int NT>
+__device__ __forceinline__ void sw_mma_abt(float (&s)[NT][4], const uint32_t (&a)[HD / 16][4],
+                                           const __nv_bfloat16* b, const __nv_bfloat16* blast, int lane) {
+    using S = Swz<HD>;
+    const int r = lane & 7;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+        const __nv_bfloat16* kb = nt == NT - 1 ? blast : b + nt * 8 * HD;
+        if constexpr (HD >= 32) {
+#pragma unroll
+            for (int k2 = 0; k2 < HD / 32; ++k2) {
+                uint32_t bb[4];
+                ldmatrix_x4(bb[0], bb[1], bb[2], bb[3], kb + S::at(r, 4 * k2 + (lane >> 3)));
+                mma_bf16_16816(s[nt], a[2 * k2], bb);
+                mma_bf16_16816(s[nt], a[2 * k2 + 1], bb + 2);
+            }
+        } else {
+            uint32_t bb[2];
+            ldmatrix_x2(bb[0], bb[1], kb + S::at(r, (lane >> 3) & 1));
+            mma_bf16_16816(s[nt], a[0], bb);
+        }
+    }
+}
+// o += P(16 x 16*KS) . V(rows 0 .. 16*KS-1); P in accumulator layout.
+template <int HD, int KS, int NT>
+__device__ __forceinline__ void sw_mma_pv(float (&o)[HD / 8][4], const float (&pm)[NT][4],
+                                          const __nv_bfloat16* v, int lane) {
+    using S = Swz<HD>;
+    const int r = lane & 15;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+        uint32_t pa[4];
+        pa[0] = pack_bf16(pm[2 * ks][0], pm[2 * ks][1]);
+        pa[1] = pack_bf16(pm[2 * ks][2], pm[2 * ks][3]);
+        pa[2] = pack_bf16(pm[2 * ks + 1][0], pm[2 * ks + 1][1]);
+        pa[3] = pack_bf16(pm[2 * ks + 1][2], pm[2 * ks + 1][3]);
+#pragma unroll
+        for (int nd = 0; nd < HD / 8; nd += 2) {
+            uint32_t b[4];
+            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], v + ks * 16 * HD + S::at(r, nd + (lane >> 4)));
+            mma_bf16_16816(o[nd], pa, b);
+            mma_bf16_16816(o[nd + 1], pa, b + 2);
+        }
+    }
+}
+// Fragments (rows r0 / r0+8) -> swizzled bf16 rows, scaled per row.
+template <int HD>
+__device__ __forceinline__ void sw_frags_to_rows(__nv_bfloat16* sm, const float (&o)[HD / 8][4], float m0,
+                                                 float m1, int lane) {
+    using S = Swz<HD>;
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+#pragma unroll
+    for (int nd = 0; nd < HD / 8; ++nd) {
+        *reinterpret_cast<uint32_t*>(sm + S::at(r0, nd) + c0) = pack_bf16(o[nd][0] * m0, o[nd][1] * m0);
+        *reinterpret_cast<uint32_t*>(sm + S::at(r0 + 8, nd) + c0) = pack_bf16(o[nd][2] * m1, o[nd][3] * m1);
+    }
+}
+// Swizzled rows -> global token rows (`g` = row 0 of the image slice, rowbytes
+// per token row), 16-byte stores.
+template <int HD>
+__device__ __forceinline__ void sw_rows_to_global(__nv_bfloat16* g, uint32_t rowbytes, const __nv_bfloat16* sm,
+                                                  const int32_t* tok, int nrows, int lane) {
+    using S = Swz<HD>;
+    constexpr int CPR = S::CPR, RPI = 32 / CPR;
+    const int sub = lane / CPR, ch = lane - sub * CPR;
+    char* base = reinterpret_cast<char*>(g) + ch * 16;
+#pragma unroll
+    for (int j = 0; j < 16 / RPI; ++j) {
+        const int r = sub + j * RPI;
+        if (r < nrows)
+            *reinterpret_cast<uint4*>(base + uint32_t(tok[r]) * rowbytes) =
+                *reinterpret_cast<const uint4*>(sm + S::at(r, ch));
+    }
+}
+// Gather token rows into a swizzled tile: tile row r <- token tok[r] of the
+// image slice at `src` (rowbytes per token row), tok < 0 skipped.  One 32-bit
+// multiply-add per row (image slices are < 4 GB).
+template <int HD, int NROWS>
+__device__ __forceinline__ void sw_gather(__nv_bfloat16* dst, const __nv_bfloat16* src, uint32_t rowbytes,
+                                          const int32_t* tok, int lane) {
+    using S = Swz<HD>;
+    constexpr int CPR = S::CPR, RPI = 32 / CPR;
+    const int sub = lane / CPR, ch = lane - sub * CPR;
+    const char* base = reinterpret_cast<const char*>(src) + ch * 16;
+    const uint32_t sdst = smem_u32(dst);
+#pragma unroll
+    for (int j = 0; j < (NROWS + RPI - 1) / RPI; ++j) {
+        const int r = sub + j * RPI;
+        if (NROWS % RPI == 0 || r < NROWS) {
+            const int t = tok[r];
+            if (t >= 0)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + 2 * S::at(r, ch)),
+                             "l"(base + uint32_t(t) * rowbytes)
+                             : "memory");
+        }
+    }
+}
+// Static blank tile (swizzled): row 0 = blank vector of head h, rows 1..7 zero.
+template <int HD>
+__device__ __forceinline__ void sw_init_blank_tile(__nv_bfloat16* t, const __nv_bfloat16* blank, int h) {
+    for (int i = threadIdx.x; i < 8 * HD; i += 32) t[i] = __float2bfloat16(0.f);
+    __syncwarp();
+    for (int c = threadIdx.x; c < HD; c += 32) t[Swz<HD>::at(0, c >> 3) + (c & 7)] = blank[h * HD + c];
+}
+
+static __device__ __noinline__ void bias_mlp_grad_ool(const float4* units, int hidden, float ds, float ox,
+                                                      float oy, float* acc) {
+    bias_mlp_grad(units, hidden, ds, ox, oy, acc);
+}
+static __device__ __noinline__ float bias_mlp_ool(const float4* units, int hidden, float b2, float ox, float oy) {
+    return bias_mlp(units, hidden, b2, ox, oy) * kLog2e;
+}
+// Bias of the lane's score fragment on a non-fast item (log2 domain): the
+// coordinates of the lane's 2 query rows and 2*(NT-1) key slots are loaded
+// at once, then each pair takes tier 1 (window) / 2 (global table) / 3 (MLP).
+template <int KP, int NT>
+__device__ __forceinline__ void slow_bias_frag(float (&s)[NT][4], const int32_t* qtok, const int32_t* ktok,
+                                               int nk, const float* tab, const float4* units,
+                                               const AttnParams& p, int h, int64_t img_tok, float scale2,
+                                               int lane) {
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const float2* xy = reinterpret_cast<const float2*>(p.coords) + img_tok;
+    const int qa = qtok[r0] >= 0 ? qtok[r0] : qtok[0], qb = qtok[r0 + 8] >= 0 ? qtok[r0 + 8] : qtok[0];
+    const float2 q0 = __ldg(xy + qa), q1 = __ldg(xy + qb);
+    float2 kx[KP / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < KP / 8; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int sl = nt * 8 + c0 + j;
+            kx[nt][j] = __ldg(xy + (sl < nk ? ktok[sl] : ktok[0]));
+        }
+    const TokInfo ti0 = make_tokinfo(q0, p.inv_patch), ti1 = make_tokinfo(q1, p.inv_patch);
+    const float* tg = p.tab_g + size_t(h) * kWg2;
+#pragma unroll
+    for (int nt = 0; nt < KP / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 q = e >= 2 ? q1 : q0, k = kx[nt][e & 1];
+            const TokInfo ki = make_tokinfo(k, p.inv_patch);
+            int gi;
+            const int li = lut_index(e >= 2 ? ti1 : ti0, ki, gi);
+            float b;
+            if (li >= 0) b = tab[li];
+            else if (gi >= 0) b = __ldg(tg + gi) * kLog2e;
+            else b = bias_mlp_ool(units, p.hidden, p.b2[h], (k.x - q.x) * p.inv_patch, (k.y - q.y) * p.inv_patch);
+            s[nt][e] = fmaf(s[nt][e], scale2, b);
+        }
+}
+
+// Bias-table gradient of the lane's dS fragment on a non-fast item: tier 1 ->
+// warp window (shared atomics), tier 2 -> global table, tier 3 -> MLP partials.
+template <int KP, int NT>
+__device__ __forceinline__ void slow_bias_grad_frag(const float (&s)[NT][4], const int32_t* qtok,
+                                                    const int32_t* ktok, int nk, int qlen, float* dtab,
+                                                    const float4* units, float* mlpg, const AttnParams& p,
+                                                    int h, int64_t img_tok, int lane) {
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const float2* xy = reinterpret_cast<const float2*>(p.coords) + img_tok;
+    const int qa = qtok[r0] >= 0 ? qtok[r0] : qtok[0], qb = qtok[r0 + 8] >= 0 ? qtok[r0 + 8] : qtok[0];
+    const float2 q0 = __ldg(xy + qa), q1 = __ldg(xy + qb);
+    const TokInfo ti0 = make_tokinfo(q0, p.inv_patch), ti1 = make_tokinfo(q1, p.inv_patch);
+    float* tg = p.dtab_g + size_t(h) * kWg2;
+#pragma unroll
+    for (int nt = 0; nt < KP / 8; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int sl = nt * 8 + c0 + j;
+            if (sl >= nk) continue;
+            const float2 k = __ldg(xy + ktok[sl]);
+            const TokInfo ki = make_tokinfo(k, p.inv_patch);
+#pragma unroll
+            for (int hi = 0; hi < 2; ++hi) {
+                const float ds = s[nt][2 * hi + j];
+                if (r0 + 8 * hi >= qlen || ds == 0.f) continue;
+                int gi;
+                const int li = lut_index(hi ? ti1 : ti0, ki, gi);
+                const float2 q = hi ? q1 : q0;
+                if (li >= 0) atomicAdd(dtab + li, ds);
+                else if (gi >= 0) atomicAdd(tg + gi, ds);
+                else bias_mlp_grad_ool(units, p.hidden, ds, (k.x - q.x) * p.inv_patch, (k.y - q.y) * p.inv_patch, mlpg);
+            }
+        }
+}
+// Masks of the score fragment: padding slots [nk, KP), blank tile (slot KP only).
+template <int KP, int NT>
+__device__ __forceinline__ void mask_slots(float (&s)[NT][4], int nk, float scale2, float blank2, int lane) {
+    const int c0 = 2 * (lane & 3);
+    if (nk < KP) {
+#pragma unroll
+        for (int nt = 0; nt < KP / 8; ++nt) {
+            const int sl = nt * 8 + c0;
+            if (sl >= nk) s[nt][0] = s[nt][2] = -INFINITY;
+            if (sl + 1 >= nk) s[nt][1] = s[nt][3] = -INFINITY;
+        }
+    }
+    const bool bl = c0 == 0;
+    s[NT - 1][0] = bl ? fmaf(s[NT - 1][0], scale2, blank2) : -INFINITY;
+    s[NT - 1][2] = bl ? fmaf(s[NT - 1][2], scale2, blank2) : -INFINITY;
+    s[NT - 1][1] = s[NT - 1][3] = -INFINITY;
+}
+// Fast-item bias: window lookups by lattice cell difference.
+template <int KP, int NT>
+__device__ __forceinline__ void fast_bias_frag(float (&s)[NT][4], const int32_t* qcell, const int32_t* kcell,
+                                               const float* tab, float scale2, int lane) {
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const int q0 = kWinC - qcell[r0], q1 = kWinC - qcell[r0 + 8];
+#pragma unroll
+    for (int nt = 0; nt < KP / 8; ++nt) {
+        const int2 kc = *reinterpret_cast<const int2*>(kcell + nt * 8 + c0);
+        s[nt][0] = fmaf(s[nt][0], scale2, tab[kc.x + q0]);
+        s[nt][1] = fmaf(s[nt][1], scale2, tab[kc.y + q0]);
+        s[nt][2] = fmaf(s[nt][2], scale2, tab[kc.x + q1]);
+        s[nt][3] = fmaf(s[nt][3], scale2, tab[kc.y + q1]);
+    }
+}
+
 // ======================================================= forward
-template <int HD, int KP, int HPC>
+template <int HD, int KP>
 struct FwdCfg {
-    static constexpr int RW = HPC * HD + 8;          // padded row (bf16 elements)
-    static constexpr uint32_t ROWB = HPC * HD * 2;  // bytes per gathered row
     static constexpr int NT = KP / 8 + 1;
     static constexpr int QW = QRec<KP>::WORDS;
-    static constexpr int STAGES = 2;
-    struct alignas(16) Stage {
-        __nv_bfloat16 Q[16 * RW];
-        __nv_bfloat16 K[(KP + 8) * RW];
-        __nv_bfloat16 V[KP * RW];
-        int32_t rec[QW];
-        uint64_t full, empty;
-        uint64_t pad_;
-    };
     struct alignas(16) Smem {
-        Stage st[STAGES];
-        float tab[HPC * kWs2];
-        float4 units[HPC * kMaxHidden];
-        float b2[HPC];
+        __nv_bfloat16 Q[16 * HD];
+        __nv_bfloat16 K[KP * HD];
+        __nv_bfloat16 V[KP * HD];
+        __nv_bfloat16 Kb[8 * HD];   // blank key tile
+        __nv_bfloat16 O[16 * HD];   // output staging
+        int32_t rec[3][QW];
+        float tab[kWs2];
+        float4 units[kMaxHidden];
     };
 };
 
-template <int HD, int KP, int HPC>
-__global__ void __launch_bounds__(32 * (HPC + 1)) attn_fwd_kernel(AttnParams p) {
-    using C = FwdCfg<HD, KP, HPC>;
+// Per warp, item i: [Q,K(i) landed] S = QK^T -> issue Q,K(i+1) -> softmax ->
+// [V(i) landed] O = PV -> issue V(i+1) -> store O; records two items ahead.
+template <int HD, int KP>
+__global__ void __launch_bounds__(32, 14) attn_fwd_kernel(AttnParams p) {
+    using C = FwdCfg<HD, KP>;
     using R = QRec<KP>;
-    constexpr int RW = C::RW, NT = C::NT, S = C::STAGES;
+    constexpr int NT = C::NT;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
-    const int h0 = blockIdx.y * HPC;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_items = p.batch * p.cs.c;
-    const int hd_all = p.heads * HD;
-
-    zero_shared(sm.st, sizeof(sm.st));
-    __syncthreads();
-    for (int i = threadIdx.x; i < S * HPC * HD; i += blockDim.x) {
-        const int s = i / (HPC * HD), j = i - s * (HPC * HD);
-        sm.st[s].K[KP * RW + j] = p.bk[h0 * HD + j];  // blank key row; rows KP+1.. stay 0
-    }
-    load_window<HPC>(sm.tab, p, h0);
-    load_units<HPC>(sm.units, sm.b2, p, h0);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&sm.st[s].full, 32);
-            mbar_init(&sm.st[s].empty, HPC);
-        }
-        fence_barrier_init();
-    }
-    fence_proxy_async();
-    __syncthreads();
-
-    if (warp == HPC) {  // ------------------------------------------ producer
-        int it = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-            auto& st = sm.st[it % S];
-            if (it >= S) mbar_wait(&st.empty, ((it / S) & 1) ^ 1);
-            const int32_t* g = p.qrec + size_t(item) * C::QW;
-            for (int w = lane * 4; w < C::QW; w += 128) *reinterpret_cast<int4*>(st.rec + w) = ldg_nc4(g + w);
-            const int nk = __ldg(g + R::HDR + kHNk), qlen = __ldg(g + R::HDR + kHQlen);
-            const __nv_bfloat16* qb = p.q + int64_t(item / p.cs.c) * p.cs.n * hd_all + h0 * HD;
-            const __nv_bfloat16* kb = p.k + (qb - p.q);
-            const __nv_bfloat16* vb = p.v + (qb - p.q);
-            __syncwarp();
-            const int32_t* rec = st.rec;
-            gather_rows<C::ROWB>(qlen + 2 * nk, lane, [&](int r, const __nv_bfloat16*& src, __nv_bfloat16*& dst) {
-                if (r < qlen) {
-                    src = qb + int64_t(rec[R::QTOK + r]) * hd_all;
-                    dst = st.Q + r * RW;
-                } else {
-                    const bool isv = r >= qlen + nk;
-                    const int sl = r - qlen - (isv ? nk : 0);
-                    src = (isv ? vb : kb) + int64_t(rec[R::KTOK + sl]) * hd_all;
-                    dst = (isv ? st.V : st.K) + sl * RW;
-                }
-            });
-            cp_async_mbar_arrive(&st.full);
-            mbar_arrive(&st.full);
-        }
-        return;
-    }
-
-    // --------------------------------------------------------- consumers
-    const int hh = warp, h = h0 + hh;
+    const int lane = threadIdx.x, h = blockIdx.y;
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const int n_items = p.batch * p.cs.c, stride = gridDim.x;
+    const int64_t ld = int64_t(p.heads) * HD;
+    const uint32_t rowb = uint32_t(ld * 2);
+    const __nv_bfloat16* qg = p.q + h * HD;
+    const __nv_bfloat16* kg = p.k + h * HD;
+    const __nv_bfloat16* vg = p.v + h * HD;
+
+    zero_shared(&sm, sizeof(sm));
+    __syncwarp();
+    sw_init_blank_tile<HD>(sm.Kb, p.bk, h);
+    load_head_bias(sm.tab, sm.units, p, h);
     const float scale2 = p.scale * kLog2e, blank2 = p.blank[h] * kLog2e;
-    const float* tab = sm.tab + hh * kWs2;
     float bvr[HD / 8][2];
 #pragma unroll
     for (int nd = 0; nd < HD / 8; ++nd) {
         bvr[nd][0] = __bfloat162float(p.bv[h * HD + nd * 8 + c0]);
         bvr[nd][1] = __bfloat162float(p.bv[h * HD + nd * 8 + c0 + 1]);
     }
+    auto rec_of = [&](int it) -> int32_t* { return sm.rec[it % 3]; };
+    auto copy_item_rec = [&](int item, int it) {
+        if (item < n_items) copy_rec<C::QW>(rec_of(it), p.qrec + size_t(item) * C::QW, lane);
+    };
+
+    const int i0 = blockIdx.x;
+    copy_item_rec(i0, 0);
+    copy_item_rec(i0 + stride, 1);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    if (i0 < n_items) {
+        const int64_t io = int64_t(rec_of(0)[R::HDR + kHImgTok]) * ld;
+        sw_gather<HD, 16>(sm.Q, qg + io, rowb, rec_of(0) + R::QTOK, lane);
+        sw_gather<HD, KP>(sm.K, kg + io, rowb, rec_of(0) + R::KTOK, lane);
+        cp_async_commit();
+        sw_gather<HD, KP>(sm.V, vg + io, rowb, rec_of(0) + R::KTOK, lane);
+    } else {
+        cp_async_commit();
+    }
+    cp_async_commit();
+
     int it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        auto& st = sm.st[it % S];
-        mbar_wait(&st.full, (it / S) & 1);
-        const int32_t* rec = st.rec;
+    for (int item = i0; item < n_items; item += stride, ++it) {
+        const int i1 = item + stride;
+        cp_async_wait<1>();  // Q, K (and record i+1) landed; V may be in flight
+        __syncwarp();
+        copy_item_rec(item + 2 * stride, it + 2);
+        cp_async_commit();
+        const int32_t* rec = rec_of(it);
+        const int32_t* rec1 = rec_of(it + 1);
         const int nk = rec[R::HDR + kHNk], qlen = rec[R::HDR + kHQlen];
         const bool fast = rec[R::HDR + kHFast] != 0;
-        const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
+        const int64_t img_tok = rec[R::HDR + kHImgTok], io_cur = img_tok * ld;
+        const int64_t io_nxt = int64_t(rec1[R::HDR + kHImgTok]) * ld;
 
         uint32_t qa[HD / 16][4];
-        load_a16<HD, RW>(qa, st.Q + hh * HD, lane);
+        sw_load_a16<HD>(qa, sm.Q, lane);
         float s[NT][4];
-        mma_abt<HD, NT, RW>(s, qa, st.K + hh * HD, lane);
-        score_bias<KP, NT>(s, rec, tab, scale2, blank2, nk, fast, lane, p, sm.units + hh * kMaxHidden,
-                           sm.b2[hh], h, img_tok);
+        sw_mma_abt<HD, NT>(s, qa, sm.K, sm.Kb, lane);
+        __syncwarp();  // Q, K consumed: reload them for item i+1
+        if (i1 < n_items) {
+            sw_gather<HD, 16>(sm.Q, qg + io_nxt, rowb, rec1 + R::QTOK, lane);
+            sw_gather<HD, KP>(sm.K, kg + io_nxt, rowb, rec1 + R::KTOK, lane);
+        }
+        cp_async_commit();
+        if (fast) fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
+        else slow_bias_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, sm.tab, sm.units, p, h,
+                                    img_tok, scale2, lane);
+        mask_slots<KP, NT>(s, nk, scale2, blank2, lane);
 
         float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
@@ -455,10 +676,15 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_fwd_kernel(AttnParams p) 
             l0 += __shfl_xor_sync(0xffffffffu, l0, o);
             l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
+        cp_async_wait<2>();  // V(i) landed
+        __syncwarp();
         float o[HD / 8][4];
 #pragma unroll
         for (int nd = 0; nd < HD / 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
-        mma_pv<HD, KP / 16, NT, RW>(o, s, st.V + hh * HD, lane);
+        sw_mma_pv<HD, KP / 16, NT>(o, s, sm.V, lane);
+        __syncwarp();  // V consumed: reload it for item i+1
+        if (i1 < n_items) sw_gather<HD, KP>(sm.V, vg + io_nxt, rowb, rec1 + R::KTOK, lane);
+        cp_async_commit();
         // blank slot: rank-1 update P_blank x blank_v
         const float pb0 = __shfl_sync(0xffffffffu, s[NT - 1][0], lane & ~3);
         const float pb1 = __shfl_sync(0xffffffffu, s[NT - 1][2], lane & ~3);
@@ -469,154 +695,137 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_fwd_kernel(AttnParams p) 
             o[nd][2] = fmaf(pb1, bvr[nd][0], o[nd][2]);
             o[nd][3] = fmaf(pb1, bvr[nd][1], o[nd][3]);
         }
-        frags_to_rows<HD, RW>(st.Q + hh * HD, o, 1.f / l0, 1.f / l1, lane);
+        sw_frags_to_rows<HD>(sm.O, o, 1.f / l0, 1.f / l1, lane);
         if ((lane & 3) == 0) {
-            if (r0 < qlen) p.lse[(img_tok + rec[R::QTOK + r0]) * p.heads + h] = (m0 + __log2f(l0)) * kLn2;
-            if (r0 + 8 < qlen) p.lse[(img_tok + rec[R::QTOK + r0 + 8]) * p.heads + h] = (m1 + __log2f(l1)) * kLn2;
+            float* lse_img = p.lse + img_tok * p.heads + h;
+            if (r0 < qlen) lse_img[uint32_t(rec[R::QTOK + r0]) * uint32_t(p.heads)] = (m0 + __log2f(l0)) * kLn2;
+            if (r0 + 8 < qlen) lse_img[uint32_t(rec[R::QTOK + r0 + 8]) * uint32_t(p.heads)] = (m1 + __log2f(l1)) * kLn2;
         }
         __syncwarp();
-        rows_to_global<HD, RW>(p.out, img_tok, hd_all, h * HD, st.Q + hh * HD, rec + R::QTOK, qlen, lane);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&st.empty);
+        sw_rows_to_global<HD>(p.out + io_cur + h * HD, rowb, sm.O, rec + R::QTOK, qlen, lane);
     }
+    cp_async_wait<0>();
 }
 
 // ======================================================= backward, query side
-template <int HD, int KP, int HPC>
+template <int HD, int KP>
 struct BwdQCfg {
-    static constexpr int RW = HPC * HD + 8;
-    static constexpr uint32_t ROWB = HPC * HD * 2;
     static constexpr int NT = KP / 8 + 1;
     static constexpr int QW = QRec<KP>::WORDS;
-    static constexpr int STAGES = 2;
-    struct alignas(16) Stage {
-        __nv_bfloat16 Q[16 * RW];
-        __nv_bfloat16 dO[16 * RW];
-        __nv_bfloat16 K[(KP + 8) * RW];
-        __nv_bfloat16 V[(KP + 8) * RW];
-        int32_t rec[QW];
-        float lse[16 * HPC];
-        uint64_t full, empty;
-    };
     struct alignas(16) Smem {
-        Stage st[STAGES];
-        float tab[HPC * kWs2];
-        float dtab[HPC * kWs2];
-        float scr[HPC * 8 * KP];  // dS rows of one half tile, per head
-        float4 units[HPC * kMaxHidden];
-        float mlpg[HPC * kMG];
-        float b2[HPC];
+        __nv_bfloat16 Q[16 * HD];
+        __nv_bfloat16 dO[16 * HD];
+        __nv_bfloat16 K[KP * HD];
+        __nv_bfloat16 V[KP * HD];
+        __nv_bfloat16 Kb[8 * HD];  // blank key / value tiles
+        __nv_bfloat16 Vb[8 * HD];
+        __nv_bfloat16 O[16 * HD];  // dQ staging
+        float scr[8 * KP];         // dS rows of one half tile (bias-table gradient pass)
+        float lse[16];
+        int32_t rec[3][QW];
+        float tab[kWs2];
+        float dtab[kWs2];
+        float4 units[kMaxHidden];
+        float mlpg[kMG];
     };
 };
 
-template <int HD, int KP, int HPC>
-__global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p) {
-    using C = BwdQCfg<HD, KP, HPC>;
+// Per warp, item i (everything of i landed):  S = QK^T, dP = dO.V^T ->
+// issue V(i+1) -> P, D, dS -> dQ = dS.K -> issue K(i+1) -> blank grads (Q, dO)
+// -> issue Q, dO, LSE(i+1) -> bias-table gradient -> store dQ.
+template <int HD, int KP>
+__global__ void __launch_bounds__(32, 11) attn_bwd_q_kernel(AttnParams p) {
+    using C = BwdQCfg<HD, KP>;
     using R = QRec<KP>;
-    constexpr int RW = C::RW, NT = C::NT, S = C::STAGES;
+    constexpr int NT = C::NT;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
-    const int h0 = blockIdx.y * HPC;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_items = p.batch * p.cs.c;
-    const int hd_all = p.heads * HD;
+    const int lane = threadIdx.x, h = blockIdx.y;
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const int n_items = p.batch * p.cs.c, stride = gridDim.x;
+    const int64_t ld = int64_t(p.heads) * HD;
+    const uint32_t rowb = uint32_t(ld * 2);
+    const __nv_bfloat16* qg = p.q + h * HD;
+    const __nv_bfloat16* og = p.dout + h * HD;
+    const __nv_bfloat16* kg = p.k + h * HD;
+    const __nv_bfloat16* vg = p.v + h * HD;
 
     zero_shared(&sm, sizeof(sm));
-    __syncthreads();
-    for (int i = threadIdx.x; i < S * HPC * HD; i += blockDim.x) {
-        const int s = i / (HPC * HD), j = i - s * (HPC * HD);
-        sm.st[s].K[KP * RW + j] = p.bk[h0 * HD + j];
-        sm.st[s].V[KP * RW + j] = p.bv[h0 * HD + j];
-    }
-    load_window<HPC>(sm.tab, p, h0);
-    load_units<HPC>(sm.units, sm.b2, p, h0);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&sm.st[s].full, 32);
-            mbar_init(&sm.st[s].empty, HPC);
-        }
-        fence_barrier_init();
-    }
-    fence_proxy_async();
-    __syncthreads();
-
-    if (warp == HPC) {  // ------------------------------------------ producer
-        int it = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-            auto& st = sm.st[it % S];
-            if (it >= S) mbar_wait(&st.empty, ((it / S) & 1) ^ 1);
-            const int32_t* g = p.qrec + size_t(item) * C::QW;
-            for (int w = lane * 4; w < C::QW; w += 128) *reinterpret_cast<int4*>(st.rec + w) = ldg_nc4(g + w);
-            const int nk = __ldg(g + R::HDR + kHNk), qlen = __ldg(g + R::HDR + kHQlen);
-            const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
-            const int qt = lane < qlen ? __ldg(g + R::QTOK + lane) : -1;
-            if (lane < 16) {
-#pragma unroll
-                for (int hq = 0; hq < HPC; ++hq)
-                    st.lse[lane * HPC + hq] = qt >= 0 ? __ldg(p.lse + (img_tok + qt) * p.heads + h0 + hq) : INFINITY;
-            }
-            __syncwarp();
-            const int32_t* rec = st.rec;
-            const int64_t ib = int64_t(item / p.cs.c) * p.cs.n * hd_all + h0 * HD;
-            gather_rows<C::ROWB>(2 * qlen + 2 * nk, lane, [&](int r, const __nv_bfloat16*& src, __nv_bfloat16*& dst) {
-                if (r < 2 * qlen) {
-                    const bool iso = r >= qlen;
-                    const int qr = r - (iso ? qlen : 0);
-                    src = (iso ? p.dout : p.q) + ib + int64_t(rec[R::QTOK + qr]) * hd_all;
-                    dst = (iso ? st.dO : st.Q) + qr * RW;
-                } else {
-                    const bool isv = r >= 2 * qlen + nk;
-                    const int sl = r - 2 * qlen - (isv ? nk : 0);
-                    src = (isv ? p.v : p.k) + ib + int64_t(rec[R::KTOK + sl]) * hd_all;
-                    dst = (isv ? st.V : st.K) + sl * RW;
-                }
-            });
-            cp_async_mbar_arrive(&st.full);
-            mbar_arrive(&st.full);
-        }
-        return;
-    }
-
-    // --------------------------------------------------------- consumers
-    const int hh = warp, h = h0 + hh;
-    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    __syncwarp();
+    sw_init_blank_tile<HD>(sm.Kb, p.bk, h);
+    sw_init_blank_tile<HD>(sm.Vb, p.bv, h);
+    load_head_bias(sm.tab, sm.units, p, h);
     const float scale2 = p.scale * kLog2e, blank2 = p.blank[h] * kLog2e;
-    const float* tab = sm.tab + hh * kWs2;
-    float* dtab = sm.dtab + hh * kWs2;
-    float* scr = sm.scr + hh * 8 * KP;
-    float* mlpg = sm.mlpg + hh * kMG;
-    const float4* units = sm.units + hh * kMaxHidden;
     float bkr[HD / 8][2];
 #pragma unroll
     for (int nd = 0; nd < HD / 8; ++nd) {
         bkr[nd][0] = __bfloat162float(p.bk[h * HD + nd * 8 + c0]);
         bkr[nd][1] = __bfloat162float(p.bk[h * HD + nd * 8 + c0 + 1]);
     }
-    float gbk[HD / 8][2], gbv[HD / 8][2];  // blank grads, row 0 of a rank-1 mma (lanes 0..3)
+    float gbk[HD / 8][2], gbv[HD / 8][2];  // blank grads: row 0 of a rank-1 mma (lanes 0..3)
 #pragma unroll
     for (int nd = 0; nd < HD / 8; ++nd) gbk[nd][0] = gbk[nd][1] = gbv[nd][0] = gbv[nd][1] = 0.f;
     float gblank = 0.f;
 
-    int it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        auto& st = sm.st[it % S];
-        mbar_wait(&st.full, (it / S) & 1);
-        const int32_t* rec = st.rec;
+    auto copy_item_rec = [&](int item, int32_t* dst) {
+        if (item < n_items) copy_rec<C::QW>(dst, p.qrec + size_t(item) * C::QW, lane);
+    };
+    auto issue_qo = [&](const int32_t* rec, int64_t img_tok) {
+        sw_gather<HD, 16>(sm.Q, qg + img_tok * ld, rowb, rec + R::QTOK, lane);
+        sw_gather<HD, 16>(sm.dO, og + img_tok * ld, rowb, rec + R::QTOK, lane);
+        if (lane < 16) {
+            const int qt = rec[R::QTOK + lane];
+            if (qt >= 0) cp_async4(sm.lse + lane, p.lse + (img_tok + qt) * p.heads + h);
+            else sm.lse[lane] = INFINITY;
+        }
+    };
+
+    const int i0 = blockIdx.x;
+    int rc = 0;  // ring slot of the current item's record
+    copy_item_rec(i0, sm.rec[0]);
+    copy_item_rec(i0 + stride, sm.rec[1]);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    if (i0 < n_items) {
+        const int64_t it0 = sm.rec[0][R::HDR + kHImgTok];
+        issue_qo(sm.rec[0], it0);
+        sw_gather<HD, KP>(sm.K, kg + it0 * ld, rowb, sm.rec[0] + R::KTOK, lane);
+        sw_gather<HD, KP>(sm.V, vg + it0 * ld, rowb, sm.rec[0] + R::KTOK, lane);
+    }
+    cp_async_commit();
+
+    float* dtab = sm.dtab;
+    for (int item = i0; item < n_items; item += stride) {
+        const int r1 = rc == 2 ? 0 : rc + 1, r2 = r1 == 2 ? 0 : r1 + 1;
+        cp_async_wait<0>();  // rows of this item and the record of the next one landed
+        __syncwarp();
+        copy_item_rec(item + 2 * stride, sm.rec[r2]);
+        cp_async_commit();
+        const int32_t* rec = sm.rec[rc];
+        const int32_t* rec1 = sm.rec[r1];
+        const bool more = item + stride < n_items;
         const int nk = rec[R::HDR + kHNk], qlen = rec[R::HDR + kHQlen];
         const bool fast = rec[R::HDR + kHFast] != 0;
-        const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
+        const int64_t img_tok = rec[R::HDR + kHImgTok];
+        const int64_t nxt_tok = rec1[R::HDR + kHImgTok];
 
         uint32_t qa[HD / 16][4], oa[HD / 16][4];
-        load_a16<HD, RW>(qa, st.Q + hh * HD, lane);
-        load_a16<HD, RW>(oa, st.dO + hh * HD, lane);
+        sw_load_a16<HD>(qa, sm.Q, lane);
+        sw_load_a16<HD>(oa, sm.dO, lane);
         float s[NT][4], dp[NT][4];
-        mma_abt<HD, NT, RW>(s, qa, st.K + hh * HD, lane);
-        mma_abt<HD, NT, RW>(dp, oa, st.V + hh * HD, lane);
-        score_bias<KP, NT>(s, rec, tab, scale2, blank2, nk, fast, lane, p, units, sm.b2[hh], h, img_tok);
+        sw_mma_abt<HD, NT>(s, qa, sm.K, sm.Kb, lane);
+        sw_mma_abt<HD, NT>(dp, oa, sm.V, sm.Vb, lane);
+        __syncwarp();  // V consumed
+        if (more) sw_gather<HD, KP>(sm.V, vg + nxt_tok * ld, rowb, rec1 + R::KTOK, lane);
+        cp_async_commit();
+        if (fast) fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
+        else slow_bias_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, sm.tab, sm.units, p, h, img_tok,
+                                    scale2, lane);
+        mask_slots<KP, NT>(s, nk, scale2, blank2, lane);
 
         // P = exp(S - LSE);  D = rowsum(P o dP)
-        const float ls0 = st.lse[r0 * HPC + hh] * kLog2e, ls1 = st.lse[(r0 + 8) * HPC + hh] * kLog2e;
+        const float ls0 = sm.lse[r0] * kLog2e, ls1 = sm.lse[r0 + 8] * kLog2e;
         float D0 = 0.f, D1 = 0.f;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -633,8 +842,9 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p
             D1 += __shfl_xor_sync(0xffffffffu, D1, o);
         }
         if ((lane & 3) == 0) {
-            if (r0 < qlen) p.dsum[(img_tok + rec[R::QTOK + r0]) * p.heads + h] = D0;
-            if (r0 + 8 < qlen) p.dsum[(img_tok + rec[R::QTOK + r0 + 8]) * p.heads + h] = D1;
+            float* ds_img = p.dsum + img_tok * p.heads + h;
+            if (r0 < qlen) ds_img[uint32_t(rec[R::QTOK + r0]) * uint32_t(p.heads)] = D0;
+            if (r0 + 8 < qlen) ds_img[uint32_t(rec[R::QTOK + r0 + 8]) * uint32_t(p.heads)] = D1;
         }
         // dS = P (dP - D), in place of P; keep the blank column's P
         const float pbl0 = s[NT - 1][0], pbl1 = s[NT - 1][2];
@@ -644,6 +854,25 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p
             s[nt][1] *= dp[nt][1] - D0;
             s[nt][2] *= dp[nt][2] - D1;
             s[nt][3] *= dp[nt][3] - D1;
+        }
+        // ---- dQ = dS . K / sqrt(d)  (+ blank rank-1 dS_b x blank_k)
+        float dqa[HD / 8][4];
+#pragma unroll
+        for (int nd = 0; nd < HD / 8; ++nd) dqa[nd][0] = dqa[nd][1] = dqa[nd][2] = dqa[nd][3] = 0.f;
+        sw_mma_pv<HD, KP / 16, NT>(dqa, s, sm.K, lane);
+        __syncwarp();  // K consumed
+        if (more) sw_gather<HD, KP>(sm.K, kg + nxt_tok * ld, rowb, rec1 + R::KTOK, lane);
+        cp_async_commit();
+        {
+            const float b0 = __shfl_sync(0xffffffffu, s[NT - 1][0], lane & ~3);
+            const float b1 = __shfl_sync(0xffffffffu, s[NT - 1][2], lane & ~3);
+#pragma unroll
+            for (int nd = 0; nd < HD / 8; ++nd) {
+                dqa[nd][0] = fmaf(b0, bkr[nd][0], dqa[nd][0]);
+                dqa[nd][1] = fmaf(b0, bkr[nd][1], dqa[nd][1]);
+                dqa[nd][2] = fmaf(b1, bkr[nd][0], dqa[nd][2]);
+                dqa[nd][3] = fmaf(b1, bkr[nd][1], dqa[nd][3]);
+            }
         }
         // ---- blank grads: dblank += sum dS_b; dbk += dS_b^T Q; dbv += P_b^T dO (rank-1 mma)
         {
@@ -657,11 +886,13 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p
             const bool row0 = lane < 4;
             const uint32_t ax[4] = {row0 ? pack_bf16(x0, x1) : 0u, 0u, row0 ? pack_bf16(x2, x3) : 0u, 0u};
             const uint32_t ay[4] = {row0 ? pack_bf16(y0, y1) : 0u, 0u, row0 ? pack_bf16(y2, y3) : 0u, 0u};
+            using S = Swz<HD>;
+            const int rr = lane & 15;
 #pragma unroll
             for (int nd = 0; nd < HD / 8; nd += 2) {
                 uint32_t b[4], bo[4];
-                ldmatrix_x4_trans(b[0], b[1], b[2], b[3], st.Q + (lane & 15) * RW + hh * HD + nd * 8 + (lane >> 4) * 8);
-                ldmatrix_x4_trans(bo[0], bo[1], bo[2], bo[3], st.dO + (lane & 15) * RW + hh * HD + nd * 8 + (lane >> 4) * 8);
+                ldmatrix_x4_trans(b[0], b[1], b[2], b[3], sm.Q + S::at(rr, nd + (lane >> 4)));
+                ldmatrix_x4_trans(bo[0], bo[1], bo[2], bo[3], sm.dO + S::at(rr, nd + (lane >> 4)));
                 float t0[4] = {0.f, 0.f, 0.f, 0.f}, t1[4] = {0.f, 0.f, 0.f, 0.f};
                 float u0[4] = {0.f, 0.f, 0.f, 0.f}, u1[4] = {0.f, 0.f, 0.f, 0.f};
                 mma_bf16_16816(t0, ax, b);
@@ -678,32 +909,21 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p
                 gbv[nd + 1][1] += u1[1];
             }
         }
-        // ---- dQ = dS . K / sqrt(d)  (+ blank rank-1 dS_b x blank_k)
-        float dqa[HD / 8][4];
-#pragma unroll
-        for (int nd = 0; nd < HD / 8; ++nd) dqa[nd][0] = dqa[nd][1] = dqa[nd][2] = dqa[nd][3] = 0.f;
-        mma_pv<HD, KP / 16, NT, RW>(dqa, s, st.K + hh * HD, lane);
-        {
-            const float b0 = __shfl_sync(0xffffffffu, s[NT - 1][0], lane & ~3);
-            const float b1 = __shfl_sync(0xffffffffu, s[NT - 1][2], lane & ~3);
-#pragma unroll
-            for (int nd = 0; nd < HD / 8; ++nd) {
-                dqa[nd][0] = fmaf(b0, bkr[nd][0], dqa[nd][0]);
-                dqa[nd][1] = fmaf(b0, bkr[nd][1], dqa[nd][1]);
-                dqa[nd][2] = fmaf(b1, bkr[nd][0], dqa[nd][2]);
-                dqa[nd][3] = fmaf(b1, bkr[nd][1], dqa[nd][3]);
-            }
-        }
+        __syncwarp();  // Q, dO, LSE consumed
+        if (more) issue_qo(rec1, nxt_tok);
+        cp_async_commit();
         // ---- bias-table gradient
         if (fast) {
             // Rows of one query hold pairwise-distinct key cells, so a row-major
             // pass writes distinct window entries per instruction: plain RMW
             // (duplicate key coordinates -> the rec flags force atomics).
+            float* scr = sm.scr;
             const bool dup0 = rec[R::HDR + kHDup0] != 0, dup1 = rec[R::HDR + kHDup1] != 0;
             const int ka = lane < nk ? rec[R::KCELL + lane] + kWinC : 0;
             const int kb = lane + 32 < nk ? rec[R::KCELL + lane + 32] + kWinC : 0;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
+                __syncwarp();
 #pragma unroll
                 for (int nt = 0; nt < KP / 8; ++nt)
                     *reinterpret_cast<float2*>(scr + r0 * KP + nt * 8 + c0) =
@@ -729,33 +949,22 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p
                 }
             }
         } else {
-#pragma unroll
-            for (int nt = 0; nt < KP / 8; ++nt) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int row = r0 + ((e >> 1) << 3), slot = nt * 8 + c0 + (e & 1);
-                    if (row < qlen && slot < nk && s[nt][e] != 0.f)
-                        slow_bias_grad(p, dtab, units, mlpg, h, img_tok, rec[R::QTOK + row],
-                                       rec[R::KTOK + slot], s[nt][e]);
-                }
-            }
+            slow_bias_grad_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, qlen, dtab, sm.units, sm.mlpg,
+                                        p, h, img_tok, lane);
         }
-        // ---- write dQ (this head's columns) through the stage's Q rows
+        // ---- store dQ
+        sw_frags_to_rows<HD>(sm.O, dqa, p.scale, p.scale, lane);
         __syncwarp();
-        frags_to_rows<HD, RW>(st.Q + hh * HD, dqa, p.scale, p.scale, lane);
-        __syncwarp();
-        rows_to_global<HD, RW>(p.dq, img_tok, hd_all, h * HD, st.Q + hh * HD, rec + R::QTOK, qlen, lane);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&st.empty);
+        sw_rows_to_global<HD>(p.dq + img_tok * ld + h * HD, rowb, sm.O, rec + R::QTOK, qlen, lane);
+        rc = r1;
     }
+    cp_async_wait<0>();
 
-    // ---- per-CTA partials (reduced in a fixed order by attn_part_reduce_kernel)
+    // ---- per-warp partials (reduced in a fixed order by attn_part_reduce_kernel)
     __syncwarp();
-    float* part = p.part + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * HPC * part_width(HD) +
-                  size_t(hh) * part_width(HD);
+    float* part = p.part + (size_t(h) * gridDim.x + blockIdx.x) * part_width(HD);
     for (int i = lane; i < kWs2; i += 32) part[i] = dtab[i];
-    for (int i = lane; i < kMG; i += 32) part[kWs2 + i] = mlpg[i];
+    for (int i = lane; i < kMG; i += 32) part[kWs2 + i] = sm.mlpg[i];
     float* pb = part + kWs2 + kMG;
     gblank += __shfl_xor_sync(0xffffffffu, gblank, 4);
     gblank += __shfl_xor_sync(0xffffffffu, gblank, 8);
@@ -773,301 +982,265 @@ __global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_q_kernel(AttnParams p
 }
 
 // ======================================================= backward, key side
-constexpr int KDEG = 3;  // reverse pairs per ring stage
-
-template <int HD, int HPC>
+// One pipeline round = one reverse pair (key cluster c', query cluster c).
+template <int HD>
 struct BwdKCfg {
-    static constexpr int RW = HPC * HD + 8;
-    static constexpr uint32_t ROWB = HPC * HD * 2;
-    static constexpr int STAGES = 2;
-    static constexpr int LQ = KDEG * 16;
-    struct alignas(16) Stage {
-        __nv_bfloat16 K[16 * RW];
+    static constexpr int RW = HD + 8;
+    static constexpr int RECW = PRec::WORDS + KRec::WORDS;  // pair record | key record
+    struct alignas(16) Rows {
+        __nv_bfloat16 Q[16 * RW];
+        __nv_bfloat16 dO[16 * RW];
+        __nv_bfloat16 K[16 * RW];  // first round of a key cluster; dK staging on its last
         __nv_bfloat16 V[16 * RW];
-        __nv_bfloat16 Q[LQ * RW];
-        __nv_bfloat16 dO[LQ * RW];
-        float lse[HPC * LQ];  // [head][pair*16 + query], log2 domain
-        float dsum[HPC * LQ];
-        int32_t krec[KRec::WORDS];
-        int32_t prec[KDEG * PRec::WORDS];
-        int32_t hdr[4];  // item (-1: end), np, first, last
-        uint64_t full, empty;
+        float lse[16];
+        float dsum[16];
     };
     struct alignas(16) Smem {
-        Stage st[STAGES];
-        float tab[HPC * kWs2];
-        float4 units[HPC * kMaxHidden];
-        float b2[HPC];
+        Rows rows[2];
+        int32_t rec[3][RECW];
+        float tab[kWs2];
+        float4 units[kMaxHidden];
     };
 };
 
-template <int HD, int HPC>
-__global__ void __launch_bounds__(32 * (HPC + 1)) attn_bwd_kv_kernel(AttnParams p) {
-    using C = BwdKCfg<HD, HPC>;
-    constexpr int RW = C::RW, S = C::STAGES, LQ = C::LQ;
+template <int HD>
+__global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
+    using C = BwdKCfg<HD>;
+    constexpr int RW = C::RW, KR = PRec::WORDS;  // key record offset inside a round record
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
-    const int h0 = blockIdx.y * HPC;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_items = p.batch * p.cs.c;
-    const int hd_all = p.heads * HD;
-    const int pairs_per_img = p.cs.c * p.cs.g;
+    const int lane = threadIdx.x, h = blockIdx.y;
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const int n_items = p.batch * p.cs.c, stride = gridDim.x;
+    const int64_t ld = int64_t(p.heads) * HD;
 
-    zero_shared(sm.st, sizeof(sm.st));
-    __syncthreads();
-    load_window<HPC>(sm.tab, p, h0);
-    load_units<HPC>(sm.units, sm.b2, p, h0);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&sm.st[s].full, 32);
-            mbar_init(&sm.st[s].empty, HPC);
-        }
-        fence_barrier_init();
-    }
-    fence_proxy_async();
-    __syncthreads();
+    zero_shared(sm.rows, sizeof(sm.rows));
+    load_head_bias(sm.tab, sm.units, p, h);
+    const float scale2 = p.scale * kLog2e;
 
-    if (warp == HPC) {  // ------------------------------------------ producer
-        int rr = 0;
-        auto acquire = [&](int r) -> typename C::Stage& {
-            auto& st = sm.st[r % S];
-            if (r >= S) mbar_wait(&st.empty, ((r / S) & 1) ^ 1);
-            return st;
-        };
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-            const int img = item / p.cs.c;
-            const int64_t img_tok = int64_t(img) * p.cs.n;
-            const int32_t* kg = p.krec + size_t(item) * KRec::WORDS;
-            const int klen = __ldg(kg + KRec::HDR), rb = __ldg(kg + KRec::HDR + 1), re = __ldg(kg + KRec::HDR + 2);
-            for (int rs = rb; rs < re; rs += KDEG, ++rr) {
-                auto& st = acquire(rr);
-                const int np = min(KDEG, re - rs);
-                const bool first = rs == rb;
-                for (int w = lane * 4; w < KRec::WORDS; w += 128)
-                    *reinterpret_cast<int4*>(st.krec + w) = ldg_nc4(kg + w);
-                const int32_t* pg = p.prec + (size_t(img) * pairs_per_img + rs) * PRec::WORDS;
-                for (int w = lane * 4; w < np * PRec::WORDS; w += 128)
-                    *reinterpret_cast<int4*>(st.prec + w) = ldg_nc4(pg + w);
-                if (lane == 0) {
-                    st.hdr[0] = item;
-                    st.hdr[1] = np;
-                    st.hdr[2] = first;
-                    st.hdr[3] = rs + KDEG >= re;
-                }
-                // LSE / D of the round's queries: lane -> (pair e/16, query e%16)
-#pragma unroll
-                for (int j = 0; j < (LQ + 31) / 32; ++j) {
-                    const int e = lane + 32 * j, pr = e >> 4, qi = e & 15;
-                    if (e < LQ) {
-                        const int qt = pr < np ? __ldg(pg + pr * PRec::WORDS + PRec::QTOK + qi) : -1;
-#pragma unroll
-                        for (int hq = 0; hq < HPC; ++hq) {
-                            st.lse[hq * LQ + e] =
-                                qt >= 0 ? __ldg(p.lse + (img_tok + qt) * p.heads + h0 + hq) * kLog2e : INFINITY;
-                            st.dsum[hq * LQ + e] = qt >= 0 ? __ldg(p.dsum + (img_tok + qt) * p.heads + h0 + hq) : 0.f;
-                        }
-                    }
-                }
-                __syncwarp();
-                // rows: [K 16 | V 16] on the item's first round, then per pair [Q 16 | dO 16]
-                const int kv = first ? 32 : 0;
-                const int64_t ib = img_tok * hd_all + h0 * HD;
-                constexpr int CPR = C::ROWB / 16, RPI = 32 / CPR;
-                const int sub = lane / CPR, ch = lane - sub * CPR;
-                for (int r = sub; r < kv + np * 32; r += RPI) {
-                    int tok;
-                    const __nv_bfloat16* src;
-                    __nv_bfloat16* dst;
-                    if (r < kv) {
-                        const int kr = r & 15;
-                        tok = st.krec[KRec::KTOK + kr];
-                        src = r < 16 ? p.k : p.v;
-                        dst = (r < 16 ? st.K : st.V) + kr * RW;
-                    } else {
-                        const int x = r - kv, pr = x >> 5, qi = x & 15;
-                        tok = st.prec[pr * PRec::WORDS + PRec::QTOK + qi];
-                        src = (x & 16) ? p.dout : p.q;
-                        dst = ((x & 16) ? st.dO : st.Q) + (pr * 16 + qi) * RW;
-                    }
-                    if (tok >= 0) cp_async16(dst + ch * 8, src + ib + int64_t(tok) * hd_all + ch * 8);
-                }
-                cp_async_mbar_arrive(&st.full);
-                mbar_arrive(&st.full);
+    // Round cursor: global pair index of a round, -1 past the end.
+    auto first_pair = [&](int item) -> int {
+        return item < n_items ? __ldg(p.krec + size_t(item) * KRec::WORDS + KRec::HDR + 3) : -1;
+    };
+    auto copy_round = [&](int pair, int item, int32_t* dst) {
+        if (pair < 0) return;
+        copy_rec<PRec::WORDS>(dst, p.prec + size_t(pair) * PRec::WORDS, lane);
+        copy_rec<KRec::WORDS>(dst + KR, p.krec + size_t(item) * KRec::WORDS, lane);
+    };
+    // Round after the round whose record is `rec` (landed): the next pair of the
+    // same key cluster, else the first pair of the cluster `stride` further on
+    // (nx_first, prefetched one cluster ahead).
+    int nx_first = -1;
+    auto advance = [&](const int32_t* rec, int& item) -> int {
+        item = rec[PRec::HDR + kPItem];
+        if (!rec[PRec::HDR + kPLast]) return rec[PRec::HDR + kPIdx] + 1;
+        const int r = nx_first;
+        item += stride;
+        nx_first = first_pair(item + stride);
+        return r;
+    };
+    auto issue_rows = [&](typename C::Rows& rw, const int32_t* rec) {
+        const int item = rec[PRec::HDR + kPItem];
+        const bool first = rec[PRec::HDR + kPFirst] != 0;
+        const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
+        const int64_t base = img_tok * ld + h * HD;
+        const int32_t* krec = rec + KR;
+        gather<HD, 64>(lane, ld, [&](int r, int& tok, const __nv_bfloat16*& src, __nv_bfloat16*& dst) {
+            const int i = r & 15, part = r >> 4;  // 0 Q, 1 dO, 2 K, 3 V
+            tok = part < 2 ? rec[PRec::QTOK + i] : (first ? krec[KRec::KTOK + i] : -1);
+            src = (part == 0 ? p.q : part == 1 ? p.dout : part == 2 ? p.k : p.v) + base;
+            dst = (part == 0 ? rw.Q : part == 1 ? rw.dO : part == 2 ? rw.K : rw.V) + i * RW;
+        });
+        if (lane < 16) {
+            const int qt = rec[PRec::QTOK + lane];
+            if (qt >= 0) {
+                cp_async4(rw.lse + lane, p.lse + (img_tok + qt) * p.heads + h);
+                cp_async4(rw.dsum + lane, p.dsum + (img_tok + qt) * p.heads + h);
+            } else {
+                rw.lse[lane] = INFINITY;
+                rw.dsum[lane] = 0.f;
             }
         }
-        // end marker
-        auto& st = acquire(rr);
-        if (lane == 0) st.hdr[0] = -1;
-        __syncwarp();
-        mbar_arrive(&st.full);
-        return;
-    }
+    };
 
-    // --------------------------------------------------------- consumers
-    const int hh = warp, h = h0 + hh;
-    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
-    const float scale2 = p.scale * kLog2e;
-    const float* tab = sm.tab + hh * kWs2;
-    const float4* units = sm.units + hh * kMaxHidden;
+    // prologue: records of rounds 0 and 1, rows of round 0
+    int pr0 = first_pair(blockIdx.x), it1 = 0;
+    nx_first = first_pair(blockIdx.x + stride);
+    copy_round(pr0, blockIdx.x, sm.rec[0]);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    int pr1 = pr0 >= 0 ? advance(sm.rec[0], it1) : -1;
+    copy_round(pr1, it1, sm.rec[1]);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    if (pr0 >= 0) issue_rows(sm.rows[0], sm.rec[0]);
+    cp_async_commit();
+
     uint32_t ka[HD / 16][4], va[HD / 16][4];
     float dk[HD / 8][4], dv[HD / 8][4];
-    int kq0 = 0, kq1 = 0, klen = 0, kt0 = 0, kt1 = 0;
-    for (int rr = 0;; ++rr) {
-        auto& st = sm.st[rr % S];
-        mbar_wait(&st.full, (rr / S) & 1);
-        const int item = st.hdr[0];
-        if (item < 0) break;
-        const int np = st.hdr[1];
-        const bool first = st.hdr[2] != 0, last = st.hdr[3] != 0;
+    int kq0 = 0, kq1 = 0, kt0 = 0, kt1 = 0;
+    for (int it = 0; pr0 >= 0; ++it) {
+        cp_async_wait<1>();  // record of round it+1 landed
+        __syncwarp();
+        int it2 = 0;
+        const int pr2 = pr1 >= 0 ? advance(sm.rec[(it + 1) % 3], it2) : -1;
+        copy_round(pr2, it2, sm.rec[(it + 2) % 3]);
+        cp_async_commit();
+        if (pr1 >= 0) issue_rows(sm.rows[(it + 1) & 1], sm.rec[(it + 1) % 3]);
+        cp_async_commit();
+        cp_async_wait<2>();  // rows of round it landed
+        __syncwarp();
+
+        auto& rw = sm.rows[it & 1];
+        const int32_t* rec = sm.rec[it % 3];
+        const int32_t* krec = rec + KR;
+        const bool first = rec[PRec::HDR + kPFirst] != 0, last = rec[PRec::HDR + kPLast] != 0;
+        const int item = rec[PRec::HDR + kPItem];
         const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
         if (first) {
-            load_a16<HD, RW>(ka, st.K + hh * HD, lane);
-            load_a16<HD, RW>(va, st.V + hh * HD, lane);
+            load_a16<HD, RW>(ka, rw.K, lane);
+            load_a16<HD, RW>(va, rw.V, lane);
 #pragma unroll
             for (int nd = 0; nd < HD / 8; ++nd)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) dk[nd][e] = dv[nd][e] = 0.f;
-            klen = st.krec[KRec::HDR];
-            kq0 = st.krec[KRec::KCELL + r0] + kWinC;
-            kq1 = st.krec[KRec::KCELL + r0 + 8] + kWinC;
-            kt0 = st.krec[KRec::KTOK + (r0 < klen ? r0 : 0)];
-            kt1 = st.krec[KRec::KTOK + (r0 + 8 < klen ? r0 + 8 : 0)];
+            const int klen = krec[KRec::HDR];
+            kq0 = krec[KRec::KCELL + r0] + kWinC;
+            kq1 = krec[KRec::KCELL + r0 + 8] + kWinC;
+            kt0 = krec[KRec::KTOK + (r0 < klen ? r0 : 0)];
+            kt1 = krec[KRec::KTOK + (r0 + 8 < klen ? r0 + 8 : 0)];
         }
-        for (int pr = 0; pr < np; ++pr) {
-            const __nv_bfloat16* Qp = st.Q + pr * 16 * RW + hh * HD;
-            const __nv_bfloat16* Op = st.dO + pr * 16 * RW + hh * HD;
-            const int32_t* prc = st.prec + pr * PRec::WORDS;
-            float sT[2][4], dpT[2][4];
-            mma_abt<HD, 2, RW>(sT, ka, Qp, lane);
-            mma_abt<HD, 2, RW>(dpT, va, Op, lane);
-            const bool fast = prc[PRec::HDR + 1] != 0;
-            const float* lsp = st.lse + hh * LQ + pr * 16;
-            const float* dsp = st.dsum + hh * LQ + pr * 16;
+        float sT[2][4], dpT[2][4];
+        mma_abt<HD, 2, RW>(sT, ka, rw.Q, rw.Q + 8 * RW, lane);
+        mma_abt<HD, 2, RW>(dpT, va, rw.dO, rw.dO + 8 * RW, lane);
+        const bool fast = rec[PRec::HDR + kPFast] != 0;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int qc = nt * 8 + c0;
-                float b[4];
-                if (fast) {
-                    const int2 qcl = *reinterpret_cast<const int2*>(prc + PRec::QCELL + qc);
-                    b[0] = tab[kq0 - qcl.x];
-                    b[1] = tab[kq0 - qcl.y];
-                    b[2] = tab[kq1 - qcl.x];
-                    b[3] = tab[kq1 - qcl.y];
-                } else {
-                    const int qlen = prc[PRec::HDR];
-                    const int qa = prc[PRec::QTOK + (qc < qlen ? qc : 0)];
-                    const int qb = prc[PRec::QTOK + (qc + 1 < qlen ? qc + 1 : 0)];
-                    b[0] = slow_bias2(p, tab, units, sm.b2[hh], h, img_tok, qa, kt0);
-                    b[1] = slow_bias2(p, tab, units, sm.b2[hh], h, img_tok, qb, kt0);
-                    b[2] = slow_bias2(p, tab, units, sm.b2[hh], h, img_tok, qa, kt1);
-                    b[3] = slow_bias2(p, tab, units, sm.b2[hh], h, img_tok, qb, kt1);
-                }
-                const float2 l2 = *reinterpret_cast<const float2*>(lsp + qc);
-                const float2 d2 = *reinterpret_cast<const float2*>(dsp + qc);
-                const float lv[4] = {l2.x, l2.y, l2.x, l2.y}, dvv[4] = {d2.x, d2.y, d2.x, d2.y};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float pr_ = ex2_fast(fmaf(sT[nt][e], scale2, b[e]) - lv[e]);
-                    sT[nt][e] = pr_;
-                    dpT[nt][e] = pr_ * (dpT[nt][e] - dvv[e]);
-                }
+        for (int nt = 0; nt < 2; ++nt) {
+            const int qc = nt * 8 + c0;
+            float b[4];
+            if (fast) {
+                const int2 qcl = *reinterpret_cast<const int2*>(rec + PRec::QCELL + qc);
+                b[0] = sm.tab[kq0 - qcl.x];
+                b[1] = sm.tab[kq0 - qcl.y];
+                b[2] = sm.tab[kq1 - qcl.x];
+                b[3] = sm.tab[kq1 - qcl.y];
+            } else {
+                const int qlen = rec[PRec::HDR + kPQlen];
+                const int qa = rec[PRec::QTOK + (qc < qlen ? qc : 0)];
+                const int qb = rec[PRec::QTOK + (qc + 1 < qlen ? qc + 1 : 0)];
+                b[0] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qa, kt0);
+                b[1] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qb, kt0);
+                b[2] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qa, kt1);
+                b[3] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qb, kt1);
             }
-            uint32_t pa[4], da[4];
-            pa[0] = pack_bf16(sT[0][0], sT[0][1]);
-            pa[1] = pack_bf16(sT[0][2], sT[0][3]);
-            pa[2] = pack_bf16(sT[1][0], sT[1][1]);
-            pa[3] = pack_bf16(sT[1][2], sT[1][3]);
-            da[0] = pack_bf16(dpT[0][0], dpT[0][1]);
-            da[1] = pack_bf16(dpT[0][2], dpT[0][3]);
-            da[2] = pack_bf16(dpT[1][0], dpT[1][1]);
-            da[3] = pack_bf16(dpT[1][2], dpT[1][3]);
+            const float2 l2 = *reinterpret_cast<const float2*>(rw.lse + qc);
+            const float2 d2 = *reinterpret_cast<const float2*>(rw.dsum + qc);
+            const float lv[4] = {l2.x * kLog2e, l2.y * kLog2e, l2.x * kLog2e, l2.y * kLog2e};
+            const float dvv[4] = {d2.x, d2.y, d2.x, d2.y};
 #pragma unroll
-            for (int nd = 0; nd < HD / 8; nd += 2) {
-                uint32_t b[4], bq[4];
-                ldmatrix_x4_trans(b[0], b[1], b[2], b[3], Op + (lane & 15) * RW + nd * 8 + (lane >> 4) * 8);
-                ldmatrix_x4_trans(bq[0], bq[1], bq[2], bq[3], Qp + (lane & 15) * RW + nd * 8 + (lane >> 4) * 8);
-                mma_bf16_16816(dv[nd], pa, b);
-                mma_bf16_16816(dv[nd + 1], pa, b + 2);
-                mma_bf16_16816(dk[nd], da, bq);
-                mma_bf16_16816(dk[nd + 1], da, bq + 2);
+            for (int e = 0; e < 4; ++e) {
+                const float pr_ = ex2_fast(fmaf(sT[nt][e], scale2, b[e]) - lv[e]);
+                sT[nt][e] = pr_;
+                dpT[nt][e] = pr_ * (dpT[nt][e] - dvv[e]);
             }
+        }
+        uint32_t pa[4], da[4];
+        pa[0] = pack_bf16(sT[0][0], sT[0][1]);
+        pa[1] = pack_bf16(sT[0][2], sT[0][3]);
+        pa[2] = pack_bf16(sT[1][0], sT[1][1]);
+        pa[3] = pack_bf16(sT[1][2], sT[1][3]);
+        da[0] = pack_bf16(dpT[0][0], dpT[0][1]);
+        da[1] = pack_bf16(dpT[0][2], dpT[0][3]);
+        da[2] = pack_bf16(dpT[1][0], dpT[1][1]);
+        da[3] = pack_bf16(dpT[1][2], dpT[1][3]);
+#pragma unroll
+        for (int nd = 0; nd < HD / 8; nd += 2) {
+            uint32_t b[4], bq[4];
+            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], rw.dO + (lane & 15) * RW + nd * 8 + (lane >> 4) * 8);
+            ldmatrix_x4_trans(bq[0], bq[1], bq[2], bq[3], rw.Q + (lane & 15) * RW + nd * 8 + (lane >> 4) * 8);
+            mma_bf16_16816(dv[nd], pa, b);
+            mma_bf16_16816(dv[nd + 1], pa, b + 2);
+            mma_bf16_16816(dk[nd], da, bq);
+            mma_bf16_16816(dk[nd + 1], da, bq + 2);
         }
         if (last) {
             __syncwarp();
-            frags_to_rows<HD, RW>(st.K + hh * HD, dk, p.scale, p.scale, lane);
-            frags_to_rows<HD, RW>(st.V + hh * HD, dv, 1.f, 1.f, lane);
+            frags_to_rows<HD, RW>(rw.K, dk, p.scale, p.scale, lane);
+            frags_to_rows<HD, RW>(rw.V, dv, 1.f, 1.f, lane);
             __syncwarp();
-            rows_to_global<HD, RW>(p.dk, img_tok, hd_all, h * HD, st.K + hh * HD, st.krec + KRec::KTOK, klen, lane);
-            rows_to_global<HD, RW>(p.dv, img_tok, hd_all, h * HD, st.V + hh * HD, st.krec + KRec::KTOK, klen, lane);
-            fence_proxy_async();
+            const int klen = krec[KRec::HDR];
+            rows_to_global<HD, RW>(p.dk + img_tok * ld + h * HD, ld, rw.K, krec + KRec::KTOK, klen, lane);
+            rows_to_global<HD, RW>(p.dv + img_tok * ld + h * HD, ld, rw.V, krec + KRec::KTOK, klen, lane);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&st.empty);
+        pr0 = pr1;
+        pr1 = pr2;
     }
+    cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------ launchers
 template <typename K>
-inline int persistent_grid(K kern, int threads, size_t smem, int items, int hgroups, dim3& grid) {
+inline int persistent_grid(K kern, size_t smem, int items, int heads, dim3& grid) {
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
     }
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem);
     if (e != cudaSuccess) return cuda_status(e, "occupancy");
     if (occ < 1) return fail(AFFMAE_EUNSUPPORTED, "attention: kernel does not fit on an SM");
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms < 1) sms = kNumSMs;
-    const int per_group = std::max(1, std::min(occ * sms / hgroups, kMaxCtasPerGroup));
-    grid = dim3(unsigned(std::min(items, per_group)), unsigned(hgroups), 1);
+    const int per_head = std::max(1, std::min(occ * sms / heads, kMaxCtasPerGroup));
+    grid = dim3(unsigned(std::min(items, per_head)), unsigned(heads), 1);
     return AFFMAE_OK;
 }
 
-template <int HD, int KP, int HPC>
+template <int HD, int KP>
 int launch_fwd(const AttnParams& p, cudaStream_t st) {
-    auto kern = attn_fwd_kernel<HD, KP, HPC>;
-    const size_t smem = sizeof(typename FwdCfg<HD, KP, HPC>::Smem);
+    auto kern = attn_fwd_kernel<HD, KP>;
+    const size_t smem = sizeof(typename FwdCfg<HD, KP>::Smem);
     dim3 grid;
-    int rc = persistent_grid(kern, 32 * (HPC + 1), smem, p.batch * p.cs.c, p.heads / HPC, grid);
+    int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
     if (rc) return rc;
-    kern<<<grid, 32 * (HPC + 1), smem, st>>>(p);
+    kern<<<grid, 32, smem, st>>>(p);
     AFFMAE_LAUNCH_CHECK("attn_fwd_kernel");
     return AFFMAE_OK;
 }
 
-// Launches the query-side kernel; `grid_x` returns its CTA count per head group.
-template <int HD, int KP, int HPC>
+// Launches the query-side kernel; `grid_x` returns its CTA count per head.
+template <int HD, int KP>
 int launch_bwd_q(const AttnParams& p, cudaStream_t st, int& grid_x) {
-    auto kern = attn_bwd_q_kernel<HD, KP, HPC>;
-    const size_t smem = sizeof(typename BwdQCfg<HD, KP, HPC>::Smem);
+    auto kern = attn_bwd_q_kernel<HD, KP>;
+    const size_t smem = sizeof(typename BwdQCfg<HD, KP>::Smem);
     dim3 grid;
-    int rc = persistent_grid(kern, 32 * (HPC + 1), smem, p.batch * p.cs.c, p.heads / HPC, grid);
+    int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
     if (rc) return rc;
-    kern<<<grid, 32 * (HPC + 1), smem, st>>>(p);
+    kern<<<grid, 32, smem, st>>>(p);
     AFFMAE_LAUNCH_CHECK("attn_bwd_q_kernel");
     grid_x = int(grid.x);
     return AFFMAE_OK;
 }
 
-template <int HD, int HPC>
+template <int HD>
 int launch_bwd_kv(const AttnParams& p, cudaStream_t st) {
-    auto kern = attn_bwd_kv_kernel<HD, HPC>;
-    const size_t smem = sizeof(typename BwdKCfg<HD, HPC>::Smem);
+    auto kern = attn_bwd_kv_kernel<HD>;
+    const size_t smem = sizeof(typename BwdKCfg<HD>::Smem);
     dim3 grid;
-    int rc = persistent_grid(kern, 32 * (HPC + 1), smem, p.batch * p.cs.c, p.heads / HPC, grid);
+    int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
     if (rc) return rc;
-    kern<<<grid, 32 * (HPC + 1), smem, st>>>(p);
+    kern<<<grid, 32, smem, st>>>(p);
     AFFMAE_LAUNCH_CHECK("attn_bwd_kv_kernel");
     return AFFMAE_OK;
 }
 
-#define AFFMAE_INSTANTIATE_ATTN_QK(HD_, KP_, HPC_)                                   \
-    template int launch_fwd<HD_, KP_, HPC_>(const AttnParams&, cudaStream_t); \
-    template int launch_bwd_q<HD_, KP_, HPC_>(const AttnParams&, cudaStream_t, int&);
-#define AFFMAE_INSTANTIATE_ATTN_KV(HD_, HPC_) \
-    template int launch_bwd_kv<HD_, HPC_>(const AttnParams&, cudaStream_t);
+#define AFFMAE_INSTANTIATE_ATTN_QK(HD_, KP_)                               \
+    template int launch_fwd<HD_, KP_>(const AttnParams&, cudaStream_t); \
+    template int launch_bwd_q<HD_, KP_>(const AttnParams&, cudaStream_t, int&);
+#define AFFMAE_INSTANTIATE_ATTN_KV(HD_) template int launch_bwd_kv<HD_>(const AttnParams&, cudaStream_t);
 
 }  // namespace affmae_b200
