@@ -185,7 +185,7 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
     }
     if (lane < 8)
         ko[KRec::HDR + lane] = lane == 0 ? klen : lane == 1 ? rb : lane == 2 ? re
-                             : lane == 3 ? int(int64_t(img) * pairs + rb) : 0;
+                             : lane == 3 ? int(int64_t(img) * pairs + rb) : lane == 4 ? int(img_tok) : 0;
     const Bbox kb = warp_bbox(kvalid, kt);
     for (int pr = rb; pr < re; ++pr) {
         const int qc = rev_cl[int64_t(img) * pairs + pr];

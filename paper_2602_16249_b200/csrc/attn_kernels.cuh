@@ -61,7 +61,7 @@ struct QRec {
     static constexpr int WORDS = HDR + 8;  // multiple of 4 (16-byte copies)
 };
 enum { kHNk = 0, kHQlen = 1, kHFast = 2, kHDup0 = 3, kHDup1 = 4, kHImgTok = 5 };  // img_tok = image * N
-// Key-cluster record: ktok[16] kcell[16] hdr{klen, rb, re, first pair (global)}
+// Key-cluster record: ktok[16] kcell[16] hdr{klen, rb, re, first pair (global), img_tok}
 struct KRec {
     static constexpr int KTOK = 0, KCELL = 16, HDR = 32, WORDS = 40;
 };
@@ -110,6 +110,10 @@ struct AttnParams {
 __host__ __device__ constexpr int part_width(int hd) { return kWs2 + kMG + 2 * hd + 1; }
 
 // ---------------------------------------------------------------- helpers
+// Token offset (image * N) of a reverse-pair round's key cluster (key record hdr[4]).
+__device__ __forceinline__ int item_tok(const int32_t* round_rec, const AttnParams&) {
+    return round_rec[PRec::WORDS + KRec::HDR + 4];
+}
 // Zero a shared-memory range (16-byte granules) with the warp.
 __device__ __forceinline__ void zero_shared(void* base, size_t bytes) {
     uint4* p = reinterpret_cast<uint4*>(base);
@@ -573,7 +577,7 @@ struct FwdCfg {
 // Per warp, item i: [Q,K(i) landed] S = QK^T -> issue Q,K(i+1) -> softmax ->
 // [V(i) landed] O = PV -> issue V(i+1) -> store O; records two items ahead.
 template <int HD, int KP>
-__global__ void __launch_bounds__(32, 14) attn_fwd_kernel(AttnParams p) {
+__global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnParams p) {
     using C = FwdCfg<HD, KP>;
     using R = QRec<KP>;
     constexpr int NT = C::NT;
@@ -734,7 +738,7 @@ struct BwdQCfg {
 // issue V(i+1) -> P, D, dS -> dQ = dS.K -> issue K(i+1) -> blank grads (Q, dO)
 // -> issue Q, dO, LSE(i+1) -> bias-table gradient -> store dQ.
 template <int HD, int KP>
-__global__ void __launch_bounds__(32, 11) attn_bwd_q_kernel(AttnParams p) {
+__global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnParams p) {
     using C = BwdQCfg<HD, KP>;
     using R = QRec<KP>;
     constexpr int NT = C::NT;
@@ -985,36 +989,40 @@ __global__ void __launch_bounds__(32, 11) attn_bwd_q_kernel(AttnParams p) {
 // One pipeline round = one reverse pair (key cluster c', query cluster c).
 template <int HD>
 struct BwdKCfg {
-    static constexpr int RW = HD + 8;
     static constexpr int RECW = PRec::WORDS + KRec::WORDS;  // pair record | key record
-    struct alignas(16) Rows {
-        __nv_bfloat16 Q[16 * RW];
-        __nv_bfloat16 dO[16 * RW];
-        __nv_bfloat16 K[16 * RW];  // first round of a key cluster; dK staging on its last
-        __nv_bfloat16 V[16 * RW];
-        float lse[16];
-        float dsum[16];
-    };
     struct alignas(16) Smem {
-        Rows rows[2];
+        __nv_bfloat16 Q[2][16 * HD];   // per round (double-buffered)
+        __nv_bfloat16 dO[2][16 * HD];
+        __nv_bfloat16 K[16 * HD];      // first round of a key cluster
+        __nv_bfloat16 V[16 * HD];
+        __nv_bfloat16 dK[16 * HD];     // output staging (last round)
+        __nv_bfloat16 dV[16 * HD];
+        float lse[2][16];
+        float dsum[2][16];
         int32_t rec[3][RECW];
         float tab[kWs2];
         float4 units[kMaxHidden];
     };
 };
 
+// Per warp, round r (everything of r landed): [first: K, V -> registers] ->
+// issue record r+2 and the rows of round r+1 -> S^T = K Q^T, dP^T = V dO^T ->
+// P^T, dS^T -> dV += P^T dO, dK += dS^T Q -> [last: store dK, dV].
 template <int HD>
-__global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
+__global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(AttnParams p) {
     using C = BwdKCfg<HD>;
-    constexpr int RW = C::RW, KR = PRec::WORDS;  // key record offset inside a round record
+    constexpr int KR = PRec::WORDS;  // key record offset inside a round record
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
     const int lane = threadIdx.x, h = blockIdx.y;
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
     const int n_items = p.batch * p.cs.c, stride = gridDim.x;
     const int64_t ld = int64_t(p.heads) * HD;
+    const uint32_t rowb = uint32_t(ld * 2);
+    using S = Swz<HD>;
 
-    zero_shared(sm.rows, sizeof(sm.rows));
+    zero_shared(&sm, sizeof(sm));
+    __syncwarp();
     load_head_bias(sm.tab, sm.units, p, h);
     const float scale2 = p.scale * kLog2e;
 
@@ -1039,26 +1047,23 @@ __global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
         nx_first = first_pair(item + stride);
         return r;
     };
-    auto issue_rows = [&](typename C::Rows& rw, const int32_t* rec) {
-        const int item = rec[PRec::HDR + kPItem];
-        const bool first = rec[PRec::HDR + kPFirst] != 0;
-        const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
+    auto issue_rows = [&](int buf, const int32_t* rec) {
+        const int64_t img_tok = int64_t(item_tok(rec, p));
         const int64_t base = img_tok * ld + h * HD;
-        const int32_t* krec = rec + KR;
-        gather<HD, 64>(lane, ld, [&](int r, int& tok, const __nv_bfloat16*& src, __nv_bfloat16*& dst) {
-            const int i = r & 15, part = r >> 4;  // 0 Q, 1 dO, 2 K, 3 V
-            tok = part < 2 ? rec[PRec::QTOK + i] : (first ? krec[KRec::KTOK + i] : -1);
-            src = (part == 0 ? p.q : part == 1 ? p.dout : part == 2 ? p.k : p.v) + base;
-            dst = (part == 0 ? rw.Q : part == 1 ? rw.dO : part == 2 ? rw.K : rw.V) + i * RW;
-        });
+        sw_gather<HD, 16>(sm.Q[buf], p.q + base, rowb, rec + PRec::QTOK, lane);
+        sw_gather<HD, 16>(sm.dO[buf], p.dout + base, rowb, rec + PRec::QTOK, lane);
+        if (rec[PRec::HDR + kPFirst]) {
+            sw_gather<HD, 16>(sm.K, p.k + base, rowb, rec + KR + KRec::KTOK, lane);
+            sw_gather<HD, 16>(sm.V, p.v + base, rowb, rec + KR + KRec::KTOK, lane);
+        }
         if (lane < 16) {
             const int qt = rec[PRec::QTOK + lane];
             if (qt >= 0) {
-                cp_async4(rw.lse + lane, p.lse + (img_tok + qt) * p.heads + h);
-                cp_async4(rw.dsum + lane, p.dsum + (img_tok + qt) * p.heads + h);
+                cp_async4(sm.lse[buf] + lane, p.lse + (img_tok + qt) * p.heads + h);
+                cp_async4(sm.dsum[buf] + lane, p.dsum + (img_tok + qt) * p.heads + h);
             } else {
-                rw.lse[lane] = INFINITY;
-                rw.dsum[lane] = 0.f;
+                sm.lse[buf][lane] = INFINITY;
+                sm.dsum[buf][lane] = 0.f;
             }
         }
     };
@@ -1072,36 +1077,25 @@ __global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
     __syncwarp();
     int pr1 = pr0 >= 0 ? advance(sm.rec[0], it1) : -1;
     copy_round(pr1, it1, sm.rec[1]);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    if (pr0 >= 0) issue_rows(sm.rows[0], sm.rec[0]);
+    if (pr0 >= 0) issue_rows(0, sm.rec[0]);
     cp_async_commit();
 
     uint32_t ka[HD / 16][4], va[HD / 16][4];
     float dk[HD / 8][4], dv[HD / 8][4];
     int kq0 = 0, kq1 = 0, kt0 = 0, kt1 = 0;
+    int rc = 0;
     for (int it = 0; pr0 >= 0; ++it) {
-        cp_async_wait<1>();  // record of round it+1 landed
+        const int r1 = rc == 2 ? 0 : rc + 1, r2 = r1 == 2 ? 0 : r1 + 1;
+        const int buf = it & 1;
+        cp_async_wait<0>();  // rows of round it, record of round it+1
         __syncwarp();
-        int it2 = 0;
-        const int pr2 = pr1 >= 0 ? advance(sm.rec[(it + 1) % 3], it2) : -1;
-        copy_round(pr2, it2, sm.rec[(it + 2) % 3]);
-        cp_async_commit();
-        if (pr1 >= 0) issue_rows(sm.rows[(it + 1) & 1], sm.rec[(it + 1) % 3]);
-        cp_async_commit();
-        cp_async_wait<2>();  // rows of round it landed
-        __syncwarp();
-
-        auto& rw = sm.rows[it & 1];
-        const int32_t* rec = sm.rec[it % 3];
+        const int32_t* rec = sm.rec[rc];
         const int32_t* krec = rec + KR;
         const bool first = rec[PRec::HDR + kPFirst] != 0, last = rec[PRec::HDR + kPLast] != 0;
-        const int item = rec[PRec::HDR + kPItem];
-        const int64_t img_tok = int64_t(item / p.cs.c) * p.cs.n;
+        const int64_t img_tok = item_tok(rec, p);
         if (first) {
-            load_a16<HD, RW>(ka, rw.K, lane);
-            load_a16<HD, RW>(va, rw.V, lane);
+            sw_load_a16<HD>(ka, sm.K, lane);
+            sw_load_a16<HD>(va, sm.V, lane);
 #pragma unroll
             for (int nd = 0; nd < HD / 8; ++nd)
 #pragma unroll
@@ -1111,10 +1105,19 @@ __global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
             kq1 = krec[KRec::KCELL + r0 + 8] + kWinC;
             kt0 = krec[KRec::KTOK + (r0 < klen ? r0 : 0)];
             kt1 = krec[KRec::KTOK + (r0 + 8 < klen ? r0 + 8 : 0)];
+            __syncwarp();  // K, V consumed
         }
+        int it2 = 0;
+        const int pr2 = pr1 >= 0 ? advance(sm.rec[r1], it2) : -1;
+        copy_round(pr2, it2, sm.rec[r2]);
+        if (pr1 >= 0) issue_rows(buf ^ 1, sm.rec[r1]);
+        cp_async_commit();
+
+        const __nv_bfloat16* Qb = sm.Q[buf];
+        const __nv_bfloat16* Ob = sm.dO[buf];
         float sT[2][4], dpT[2][4];
-        mma_abt<HD, 2, RW>(sT, ka, rw.Q, rw.Q + 8 * RW, lane);
-        mma_abt<HD, 2, RW>(dpT, va, rw.dO, rw.dO + 8 * RW, lane);
+        sw_mma_abt<HD, 2>(sT, ka, Qb, Qb + 8 * HD, lane);
+        sw_mma_abt<HD, 2>(dpT, va, Ob, Ob + 8 * HD, lane);
         const bool fast = rec[PRec::HDR + kPFast] != 0;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -1135,8 +1138,8 @@ __global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
                 b[2] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qa, kt1);
                 b[3] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qb, kt1);
             }
-            const float2 l2 = *reinterpret_cast<const float2*>(rw.lse + qc);
-            const float2 d2 = *reinterpret_cast<const float2*>(rw.dsum + qc);
+            const float2 l2 = *reinterpret_cast<const float2*>(sm.lse[buf] + qc);
+            const float2 d2 = *reinterpret_cast<const float2*>(sm.dsum[buf] + qc);
             const float lv[4] = {l2.x * kLog2e, l2.y * kLog2e, l2.x * kLog2e, l2.y * kLog2e};
             const float dvv[4] = {d2.x, d2.y, d2.x, d2.y};
 #pragma unroll
@@ -1155,27 +1158,29 @@ __global__ void __launch_bounds__(32) attn_bwd_kv_kernel(AttnParams p) {
         da[1] = pack_bf16(dpT[0][2], dpT[0][3]);
         da[2] = pack_bf16(dpT[1][0], dpT[1][1]);
         da[3] = pack_bf16(dpT[1][2], dpT[1][3]);
+        const int rr = lane & 15;
 #pragma unroll
         for (int nd = 0; nd < HD / 8; nd += 2) {
             uint32_t b[4], bq[4];
-            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], rw.dO + (lane & 15) * RW + nd * 8 + (lane >> 4) * 8);
-            ldmatrix_x4_trans(bq[0], bq[1], bq[2], bq[3], rw.Q + (lane & 15) * RW + nd * 8 + (lane >> 4) * 8);
+            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], Ob + S::at(rr, nd + (lane >> 4)));
+            ldmatrix_x4_trans(bq[0], bq[1], bq[2], bq[3], Qb + S::at(rr, nd + (lane >> 4)));
             mma_bf16_16816(dv[nd], pa, b);
             mma_bf16_16816(dv[nd + 1], pa, b + 2);
             mma_bf16_16816(dk[nd], da, bq);
             mma_bf16_16816(dk[nd + 1], da, bq + 2);
         }
         if (last) {
-            __syncwarp();
-            frags_to_rows<HD, RW>(rw.K, dk, p.scale, p.scale, lane);
-            frags_to_rows<HD, RW>(rw.V, dv, 1.f, 1.f, lane);
+            sw_frags_to_rows<HD>(sm.dK, dk, p.scale, p.scale, lane);
+            sw_frags_to_rows<HD>(sm.dV, dv, 1.f, 1.f, lane);
             __syncwarp();
             const int klen = krec[KRec::HDR];
-            rows_to_global<HD, RW>(p.dk + img_tok * ld + h * HD, ld, rw.K, krec + KRec::KTOK, klen, lane);
-            rows_to_global<HD, RW>(p.dv + img_tok * ld + h * HD, ld, rw.V, krec + KRec::KTOK, klen, lane);
+            sw_rows_to_global<HD>(p.dk + img_tok * ld + h * HD, rowb, sm.dK, krec + KRec::KTOK, klen, lane);
+            sw_rows_to_global<HD>(p.dv + img_tok * ld + h * HD, rowb, sm.dV, krec + KRec::KTOK, klen, lane);
+            __syncwarp();
         }
         pr0 = pr1;
         pr1 = pr2;
+        rc = r1;
     }
     cp_async_wait<0>();
 }
