@@ -32,6 +32,11 @@ __global__ void bias_table_kernel(const float* __restrict__ w1, const float* __r
 // Lattice cell of a token (window coordinates): iy * kWs + ix.  Two tokens of
 // one phase have window offset kcell - qcell == (dy * kWs + dx).
 __device__ __forceinline__ int tok_cell(const TokInfo& t) { return t.iy * kWs + t.ix; }
+// Packed lattice cell (iy + 2048) << 16 | (ix + 2048) of a "medium" record (attn_kernels.cuh).
+__device__ __forceinline__ int tok_pcell(const TokInfo& t) { return ((t.iy + 2048) << 16) | (t.ix + 2048); }
+__device__ __forceinline__ bool pcell_ok(const TokInfo& t) {
+    return unsigned(t.ix + 2048) < 4096u && unsigned(t.iy + 2048) < 4096u;
+}
 
 struct Bbox {
     int xmin, xmax, ymin, ymax;
@@ -48,6 +53,10 @@ __device__ __forceinline__ bool bbox_fits(const Bbox& q, const Bbox& k) {
     // every key-minus-query offset inside [-kRs, kRs]^2 (64-bit: no overflow on far tokens)
     return int64_t(k.xmax) - q.xmin <= kRs && int64_t(q.xmax) - k.xmin <= kRs &&
            int64_t(k.ymax) - q.ymin <= kRs && int64_t(q.ymax) - k.ymin <= kRs;
+}
+__device__ __forceinline__ bool bbox_fits_r(const Bbox& q, const Bbox& k, int r) {
+    return int64_t(k.xmax) - q.xmin <= r && int64_t(q.xmax) - k.xmin <= r &&
+           int64_t(k.ymax) - q.ymin <= r && int64_t(q.ymax) - k.ymin <= r;
 }
 __device__ __forceinline__ bool warp_one_phase(bool valid, const TokInfo& t) {
     const uint32_t fx0 = __reduce_min_sync(0xffffffffu, valid ? t.fx : 0xffffffffu);
@@ -69,14 +78,20 @@ struct TokAgg {
         }
         fx0 = min(fx0, t.fx); fx1 = max(fx1, t.fx); fy0 = min(fy0, t.fy); fy1 = max(fy1, t.fy);
     }
-    __device__ bool fast() const {
+    bool far = false;  // a token outside the packed-cell range
+    // 1: lattice-fast (one phase, offsets inside the shared window); 2: medium
+    // (one phase, offsets inside the global table); 0: general.
+    __device__ int cls() const {
         Bbox q{__reduce_min_sync(0xffffffffu, qx0), __reduce_max_sync(0xffffffffu, qx1),
                __reduce_min_sync(0xffffffffu, qy0), __reduce_max_sync(0xffffffffu, qy1)};
         Bbox k{__reduce_min_sync(0xffffffffu, kx0), __reduce_max_sync(0xffffffffu, kx1),
                __reduce_min_sync(0xffffffffu, ky0), __reduce_max_sync(0xffffffffu, ky1)};
         const bool ph = __reduce_min_sync(0xffffffffu, fx0) == __reduce_max_sync(0xffffffffu, fx1) &&
                         __reduce_min_sync(0xffffffffu, fy0) == __reduce_max_sync(0xffffffffu, fy1);
-        return ph && bbox_fits(q, k);
+        const bool anyfar = __any_sync(0xffffffffu, far);
+        if (!ph) return 0;
+        if (bbox_fits(q, k)) return 1;
+        return !anyfar && bbox_fits_r(q, k, kRg) ? 2 : 0;
     }
 };
 
@@ -91,6 +106,7 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     using R = QRec<KP>;
     constexpr int E = 16 + KP, J = (E + 31) / 32;
     __shared__ int cellbuf[4][E];
+    __shared__ int pcellbuf[4][E];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = int64_t(blockIdx.x) * 4 + warp;
     if (item >= items) return;
@@ -119,38 +135,98 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
                 s -= len;
             }
         }
-        int cell = 0;
+        int cell = 0, pcell = 0;
         if (tok >= 0) {
             const TokInfo t = make_tokinfo(reinterpret_cast<const float2*>(coords)[img_tok + tok], inv_patch);
             cell = tok_cell(t);
+            pcell = tok_pcell(t);
+            agg.far |= !pcell_ok(t);
             agg.add(t, e >= 16);
         }
         if (e < E) {
             out[e < 16 ? R::QTOK + e : R::KTOK + e - 16] = tok;
             cellbuf[warp][e] = cell;
+            pcellbuf[warp][e] = pcell;
         }
     }
-    const bool fast = agg.fast();
+    const int cls = agg.cls();
     __syncwarp();
+    const int(*cb)[E] = cls == 2 ? pcellbuf : cellbuf;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int e = lane + 32 * j;
         if (e < E) {
             const bool valid = e < 16 ? e < qlen : e - 16 < nk;
-            const int cell = valid ? cellbuf[warp][e] : cellbuf[warp][e < 16 ? 0 : 16];
+            const int cell = valid ? cb[warp][e] : cb[warp][e < 16 ? 0 : 16];
             out[e < 16 ? R::QCELL + e : R::KCELL + e - 16] = cell;
         }
     }
-    const int ka = lane < nk ? cellbuf[warp][16 + lane] : INT_MIN + lane;
-    const int kb = lane + 32 < nk ? cellbuf[warp][16 + lane + 32] : INT_MIN + 32 + lane;
-    const bool dup0 = __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, ka)) > 1);
-    const bool dup1 = __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, kb)) > 1);
+    // duplicate key coordinates (exact packed cells; window cells alias beyond the window)
+    const int ka = lane < nk ? pcellbuf[warp][16 + lane] : INT_MIN + lane;
+    const int kb = lane + 32 < nk ? pcellbuf[warp][16 + lane + 32] : INT_MIN + 32 + lane;
+    const bool anyfar = __any_sync(0xffffffffu, agg.far);
+    const bool dup0 = anyfar || __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, ka)) > 1);
+    const bool dup1 = anyfar || __any_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, kb)) > 1);
     if (lane < 8) {
-        const int v = lane == kHNk ? nk : lane == kHQlen ? qlen : lane == kHFast ? int(fast)
+        const int v = lane == kHNk ? nk : lane == kHQlen ? qlen : lane == kHFast ? cls
                     : lane == kHDup0 ? int(dup0) : lane == kHDup1 ? int(dup1)
                     : lane == kHImgTok ? int(img_tok) : 0;
         out[R::HDR + lane] = v;
     }
+}
+
+// Item lists, deterministic order: lattice-fast query clusters at
+// list[0, n_fast), general ones at list[items, items + n_general), ascending.
+// Pass 1 counts per 1024-item block, pass 2 offsets each block by the counts
+// of the blocks before it and scatters.
+__device__ __forceinline__ void block_flags_scan(bool fast, bool valid, int& pf, int& pg, int* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned bf = __ballot_sync(0xffffffffu, fast), bg = __ballot_sync(0xffffffffu, valid && !fast);
+    if (lane == 0) {
+        wsum[warp] = __popc(bf);
+        wsum[32 + warp] = __popc(bg);
+    }
+    __syncthreads();
+    int af = 0, ag = 0;
+    for (int w = 0; w < warp; ++w) {
+        af += wsum[w];
+        ag += wsum[32 + w];
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    pf = af + __popc(bf & lt);
+    pg = ag + __popc(bg & lt);
+}
+__global__ void attn_item_count_kernel(const int32_t* __restrict__ qrec, int words, int hdr_fast, int items,
+                                       int32_t* __restrict__ blk) {
+    __shared__ int wsum[64];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < items;
+    const bool fast = valid && qrec[size_t(i) * words + hdr_fast] == 1;
+    int pf, pg;
+    block_flags_scan(fast, valid, pf, pg, wsum);
+    if (threadIdx.x == blockDim.x - 1) {
+        blk[2 * blockIdx.x] = pf + int(fast);
+        blk[2 * blockIdx.x + 1] = pg + int(valid && !fast);
+    }
+}
+__global__ void attn_item_scatter_kernel(const int32_t* __restrict__ qrec, int words, int hdr_fast, int items,
+                                         const int32_t* __restrict__ blk, int32_t* __restrict__ list,
+                                         int32_t* __restrict__ count) {
+    __shared__ int wsum[64];
+    __shared__ int base[2];
+    if (threadIdx.x < 2) {
+        int b = 0;
+        for (int k = 0; k < int(blockIdx.x); ++k) b += blk[2 * k + threadIdx.x];
+        base[threadIdx.x] = b;
+        if (blockIdx.x == gridDim.x - 1) count[threadIdx.x] = b + blk[2 * blockIdx.x + threadIdx.x];
+    }
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < items;
+    const bool fast = valid && qrec[size_t(i) * words + hdr_fast] == 1;
+    int pf, pg;
+    block_flags_scan(fast, valid, pf, pg, wsum);
+    if (fast) list[base[0] + pf] = i;
+    else if (valid) list[items + base[1] + pg] = i;
 }
 
 // Key-cluster records and reverse-pair records (one warp per key cluster c'):
@@ -179,9 +255,13 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
     }
     const int kc = kvalid ? tok_cell(kt) : 0;
     const int kc0 = __shfl_sync(0xffffffffu, kc, 0);
+    const int kpc = kvalid ? tok_pcell(kt) : 0;
+    const int kpc0 = __shfl_sync(0xffffffffu, kpc, 0);
+    const bool kfar = __any_sync(0xffffffffu, kvalid && !pcell_ok(kt));
     if (lane < 16) {
         ko[KRec::KTOK + lane] = ktok;
         ko[KRec::KCELL + lane] = kvalid ? kc : kc0;
+        ko[KRec::KPCELL + lane] = kvalid ? kpc : kpc0;
     }
     if (lane < 8)
         ko[KRec::HDR + lane] = lane == 0 ? klen : lane == 1 ? rb : lane == 2 ? re
@@ -198,10 +278,13 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
             qtok = perm[img_tok + cs.off(qc) + qi];
             qt = make_tokinfo(reinterpret_cast<const float2*>(coords)[img_tok + qtok], inv_patch);
         }
-        const int qcell = qvalid ? tok_cell(qt) : 0;
-        const int qcell0 = __shfl_sync(0xffffffffu, qcell, 16);
         const Bbox qb = warp_bbox(qvalid, qt);
-        const bool fast = warp_one_phase(kvalid || qvalid, kvalid ? kt : qt) && bbox_fits(qb, kb);
+        const bool ph = warp_one_phase(kvalid || qvalid, kvalid ? kt : qt);
+        const bool qfar = __any_sync(0xffffffffu, qvalid && !pcell_ok(qt));
+        const int cls = !ph ? 0 : bbox_fits(qb, kb) ? 1 : (!kfar && !qfar && bbox_fits_r(qb, kb, kRg)) ? 2 : 0;
+        const int qcell = qvalid ? (cls == 2 ? tok_pcell(qt) : tok_cell(qt)) : 0;
+        const int qcell0 = __shfl_sync(0xffffffffu, qcell, 16);
+        const int fast = cls;
         int32_t* po = prec + (int64_t(img) * pairs + pr) * PRec::WORDS;
         if (lane >= 16) {
             po[PRec::QTOK + qi] = qtok;
@@ -221,15 +304,27 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
 // order (deterministic): window entries are added into the global table
 // gradient (which also holds the tier-2 atomics), MLP and blank partials
 // are written to their buffers.
-__global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx, int hd, int hidden,
-                                        float* __restrict__ dtab_g, float* __restrict__ mlp_grad,
+// Block (entry chunk of 32, head): 8 warps split the CTA partials, fixed-order
+// tree at the end (deterministic).
+__global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx0, int gx1, int heads, int hd,
+                                        int hidden, float* __restrict__ dtab_g, float* __restrict__ mlp_grad,
                                         float* __restrict__ blank_grad) {
+    __shared__ float red[8][33];
     const int h = blockIdx.y;
     const int pw = part_width(hd);
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= pw) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + lane;
+    float acc = 0.f;
+    if (j < pw) {
+        const float* p1 = part + size_t(heads) * gx0 * pw;
+        for (int x = warp; x < gx0 + gx1; x += 8)
+            acc += x < gx0 ? part[(size_t(h) * gx0 + x) * pw + j] : p1[(size_t(h) * gx1 + x - gx0) * pw + j];
+    }
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp != 0 || j >= pw) return;
     float s = 0.f;
-    for (int x = 0; x < gx; ++x) s += part[(size_t(h) * gx + x) * pw + j];
+    for (int w = 0; w < 8; ++w) s += red[w][lane];
     if (j < kWs2) {
         const int oy = j / kWs - kRs, ox = j % kWs - kRs;
         dtab_g[size_t(h) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] += s;
@@ -243,6 +338,15 @@ __global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx, 
 
 // dL/dtheta = sum over table entries of dT * dT/dtheta, accumulated (+=)
 // into the caller's gradients.
+// Sums the kTabReplicas copies of the table gradient into copy 0 (fixed order).
+__global__ void dtab_replica_sum_kernel(float* __restrict__ dtab, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float s = dtab[i];
+    for (int r = 1; r < kTabReplicas; ++r) s += dtab[size_t(r) * n + i];
+    dtab[i] = s;
+}
+
 __global__ void bias_grad_finalize_kernel(const float* __restrict__ dtab, const float* __restrict__ w1,
                                           const float* __restrict__ b1, const float* __restrict__ w2,
                                           int hidden, float* dw1, float* db1, float* dw2, float* db2) {
@@ -329,7 +433,7 @@ __global__ void attn_grad_epilogue_kernel(const float* __restrict__ mlp_grad,
 template <int HD, int KP>
 int launch_fwd(const AttnParams& p, cudaStream_t st);
 template <int HD, int KP>
-int launch_bwd_q(const AttnParams& p, cudaStream_t st, int& grid_x);
+int launch_bwd_q(const AttnParams& p, cudaStream_t st, int* grid_x);
 template <int HD>
 int launch_bwd_kv(const AttnParams& p, cudaStream_t st);
 
@@ -362,6 +466,9 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 struct AttnWs {
     float* tab_g;
     int32_t* qrec;
+    int32_t* items;
+    int32_t* item_count;
+    int32_t* item_blk;
     int32_t* krec;
     int32_t* prec;
     float* dtab_g;
@@ -386,13 +493,16 @@ static AttnWs carve_ws(const affmae_cluster_geom* g, const affmae_attn_desc* a, 
     const size_t qwords = size_t(32 + 2 * kp + 8);
     w.tab_g = reinterpret_cast<float*>(take(size_t(a->heads) * kWg2 * 4));
     w.qrec = reinterpret_cast<int32_t*>(take(items * qwords * 4));
+    w.items = reinterpret_cast<int32_t*>(take(2 * items * 4));
+    w.item_count = reinterpret_cast<int32_t*>(take(2 * 4));
+    w.item_blk = reinterpret_cast<int32_t*>(take(2 * ((items + 1023) / 1024) * 4));
     if (bwd) {
         w.krec = reinterpret_cast<int32_t*>(take(items * KRec::WORDS * 4));
         w.prec = reinterpret_cast<int32_t*>(take(items * g->groups_eff * PRec::WORDS * 4));
-        w.dtab_g = reinterpret_cast<float*>(take(size_t(a->heads) * kWg2 * 4));
+        w.dtab_g = reinterpret_cast<float*>(take(size_t(kTabReplicas) * a->heads * kWg2 * 4));
         w.dsum = reinterpret_cast<float*>(take(size_t(g->batch) * g->tokens * a->heads * 4));
         w.part = reinterpret_cast<float*>(
-            take(size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [h][CTA]
+            take(2 * size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [launch][h][CTA]
         w.mlp_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
         w.blank_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
     }
@@ -420,6 +530,11 @@ static void fill_common(AttnParams& p, const affmae_cluster_geom* g, const affma
     p.hidden = a->bias_hidden;
     p.inv_patch = float(1.0 / a->patch);
     p.scale = float(1.0 / sqrt(double(a->head_dim)));
+    static const int exp_flags = [] {
+        const char* e = getenv("AFFMAE_EXP");
+        return e ? atoi(e) : 0;
+    }();
+    p.exp_flags = exp_flags;
 }
 
 static int check_inputs(const affmae_attn_inputs* in) {
@@ -452,6 +567,15 @@ static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const in
             return fail(AFFMAE_EUNSUPPORTED, "attention: width");
     }
     AFFMAE_LAUNCH_CHECK("attn_qrec_kernel");
+    {
+        const int words = 32 + 2 * pick_kp(width) + 8, hf = 32 + 2 * pick_kp(width) + kHFast;
+        const unsigned nb = unsigned((items + 1023) / 1024);
+        attn_item_count_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk);
+        AFFMAE_LAUNCH_CHECK("attn_item_count_kernel");
+        attn_item_scatter_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk, w.items,
+                                                      w.item_count);
+        AFFMAE_LAUNCH_CHECK("attn_item_scatter_kernel");
+    }
     if (rev_cl) {
         attn_krec_kernel<<<blocks, 128, 0, st>>>(p.coords, perm, rev_off, rev_cl, p.cs, items,
                                                  p.inv_patch, w.krec, w.prec);
@@ -459,6 +583,8 @@ static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const in
     }
     p.tab_g = w.tab_g;
     p.qrec = w.qrec;
+    p.items = w.items;
+    p.item_count = w.item_count;
     p.krec = w.krec;
     p.prec = w.prec;
     return AFFMAE_OK;
@@ -475,7 +601,7 @@ static int dispatch_fwd(const AttnParams& p, int head_dim, int64_t width, cudaSt
 #undef AFFMAE_CASE
     return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
 }
-static int dispatch_bwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st, int& gx) {
+static int dispatch_bwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st, int* gx) {
     const int kp = pick_kp(width);
 #define AFFMAE_CASE(HD_, KP_)                                  \
     if (head_dim == HD_ && kp == KP_) {                        \
@@ -545,13 +671,18 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
     p.part = w.part;
     cudaStream_t st = as_stream(stream);
     if ((rc = prepare(p, w, idx->perm, idx->nbr_cl, idx->rev_off, idx->rev_cl, g->width, st))) return rc;
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.dtab_g, 0, size_t(a->heads) * kWg2 * 4, st));
-    int gx = 0;
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.dtab_g, 0, size_t(kTabReplicas) * a->heads * kWg2 * 4, st));
+    int gx[2] = {0, 0};
     if ((rc = dispatch_bwd(p, a->head_dim, g->width, st, gx))) return rc;
     const int pw = part_width(a->head_dim);
-    attn_part_reduce_kernel<<<dim3((pw + 127) / 128, a->heads), 128, 0, st>>>(
-        w.part, gx, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
+    attn_part_reduce_kernel<<<dim3((pw + 31) / 32, a->heads), 256, 0, st>>>(
+        w.part, gx[0], gx[1], a->heads, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
     AFFMAE_LAUNCH_CHECK("attn_part_reduce_kernel");
+    {
+        const int n = a->heads * kWg2;
+        dtab_replica_sum_kernel<<<(n + 255) / 256, 256, 0, st>>>(w.dtab_g, n);
+        AFFMAE_LAUNCH_CHECK("dtab_replica_sum_kernel");
+    }
     bias_grad_finalize_kernel<<<dim3(16, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
                                                                   a->bias_hidden, gr->dw1, gr->db1,
                                                                   gr->dw2, gr->db2);

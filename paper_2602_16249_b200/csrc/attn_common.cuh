@@ -23,9 +23,9 @@ namespace affmae_b200 {
 constexpr int kRs = 11;               // shared-memory window radius (patches)
 constexpr int kWs = 2 * kRs + 1;      // 23
 constexpr int kWs2 = kWs * kWs;       // 529 entries per head
-constexpr int kRg = 127;              // global table radius
-constexpr int kWg = 2 * kRg + 1;      // 255
-constexpr int kWg2 = kWg * kWg;       // 65025 entries per head
+constexpr int kRg = 255;              // global table radius (covers a 256-patch image)
+constexpr int kWg = 2 * kRg + 1;      // 511
+constexpr int kWg2 = kWg * kWg;       // 261121 entries per head
 
 // Per staged token: integer lattice cell and the exact fractional phase
 // (x*inv_patch = ix + fx).  Two tokens are lattice-compatible iff their
@@ -72,19 +72,6 @@ __device__ __forceinline__ void bias_mlp_grad(const float4* units, int hidden, f
         atomicAdd(acc + 3 * hidden + u, ds * t);
     }
     atomicAdd(acc + 4 * hidden, ds);
-}
-
-// Out-of-line tiers 2/3 (rare on the lattice): keeps the unrolled fast path small.
-static __device__ __noinline__ float bias_tier23(const float* tabg, int gi, const float4* units,
-                                          int hidden, float b2, float ox, float oy) {
-    if (gi >= 0) return __ldg(tabg + gi);
-    return bias_mlp(units, hidden, b2, ox, oy);
-}
-static __device__ __noinline__ void bias_grad_tier23(float* dtab_g, int gi, const float4* units,
-                                              int hidden, float ds, float ox, float oy,
-                                              float* mlpg) {
-    if (gi >= 0) atomicAdd(dtab_g + gi, ds);
-    else bias_mlp_grad(units, hidden, ds, ox, oy, mlpg);
 }
 
 // Table window index of a pair, or -1 (tier 1 miss).  `gidx` gets the

@@ -61,18 +61,22 @@ struct QRec {
     static constexpr int WORDS = HDR + 8;  // multiple of 4 (16-byte copies)
 };
 enum { kHNk = 0, kHQlen = 1, kHFast = 2, kHDup0 = 3, kHDup1 = 4, kHImgTok = 5 };  // img_tok = image * N
-// Key-cluster record: ktok[16] kcell[16] hdr{klen, rb, re, first pair (global), img_tok}
+// Key-cluster record: ktok[16] kcell[16] kpcell[16] hdr{klen, rb, re, first pair (global), img_tok}
 struct KRec {
-    static constexpr int KTOK = 0, KCELL = 16, HDR = 32, WORDS = 40;
+    static constexpr int KTOK = 0, KCELL = 16, KPCELL = 32, HDR = 48, WORDS = 56;
 };
 // Reverse pair record (CSR order of rev_cl):
-//   qtok[16] qcell[16] hdr{qlen, fast, first, last, key item, global pair index}
+//   qtok[16] qcell[16] hdr{qlen, class, first, last, key item, global pair index}
+// Record classes (hdr kHFast / kPFast): 1 lattice-fast (window cells iy*kWs+ix),
+// 2 medium (one phase, offsets within the global table: packed cells
+// (iy+2048)<<16 | (ix+2048)), 0 general (coordinates).
 struct PRec {
     static constexpr int QTOK = 0, QCELL = 16, HDR = 32, WORDS = 40;
 };
 enum { kPQlen = 0, kPFast = 1, kPFirst = 2, kPLast = 3, kPItem = 4, kPIdx = 5 };
 constexpr int kWinC = kRs * kWs + kRs;  // window index of offset (0, 0)
 constexpr int kMG = 4 * kMaxHidden + 1;  // tier-3 MLP grad accumulator per head
+constexpr int kTabReplicas = 4;          // global tier-2 gradient table copies (spread atomics)
 
 struct AttnParams {
     const __nv_bfloat16* q;
@@ -84,6 +88,8 @@ struct AttnParams {
     const int32_t* qrec;  // [B*C][QRec::WORDS]
     const int32_t* krec;  // [B*C][KRec::WORDS]
     const int32_t* prec;  // [B*C*G][PRec::WORDS]
+    const int32_t* items;       // [2][B*C]: lattice-fast query clusters, then general ones (ascending)
+    const int32_t* item_count;  // [2]: fast, general
     const float* w1;
     const float* b1;
     const float* w2;
@@ -97,14 +103,15 @@ struct AttnParams {
     __nv_bfloat16* dk;
     __nv_bfloat16* dv;
     float* dsum;    // [B, N, heads]  D = rowsum(P o dP)
-    float* dtab_g;  // [heads][kWg2] tier-2 gradient (atomics)
-    float* part;    // [heads][CTAs][part_width] per-warp gradient partials
+    float* dtab_g;  // [kTabReplicas][heads][kWg2] tier-2 gradient (atomics)
+    float* part;    // [heads][CTAs][part_width] per-warp gradient partials (of this launch)
     ClusterShape cs;
     int batch;
     int heads;
     int hidden;
     float inv_patch;
-    float scale;  // 1/sqrt(d)
+    float scale;      // 1/sqrt(d)
+    int exp_flags;    // development experiments (AFFMAE_EXP), 0 in production
 };
 // per-warp partial: window dT [kWs2] | MLP grads [kMG] | blank {dbk[d], dbv[d], dblank}
 __host__ __device__ constexpr int part_width(int hd) { return kWs2 + kMG + 2 * hd + 1; }
@@ -153,168 +160,6 @@ static __device__ __noinline__ float slow_bias2(const AttnParams& p, const float
     return bias_mlp(units, p.hidden, p.b2[h], (kxy.x - qxy.x) * p.inv_patch,
                     (kxy.y - qxy.y) * p.inv_patch) * kLog2e;
 }
-// Its gradient: += ds into the warp window / the global table / the MLP partials.
-static __device__ __noinline__ void slow_bias_grad(const AttnParams& p, float* dtab_s,
-                                                   const float4* units, float* mlpg, int h,
-                                                   int64_t img_tok, int qt, int kt, float ds) {
-    const float2 qxy = __ldg(reinterpret_cast<const float2*>(p.coords) + img_tok + qt);
-    const float2 kxy = __ldg(reinterpret_cast<const float2*>(p.coords) + img_tok + kt);
-    const TokInfo qi = make_tokinfo(qxy, p.inv_patch), ki = make_tokinfo(kxy, p.inv_patch);
-    int gi;
-    const int li = lut_index(qi, ki, gi);
-    if (li >= 0) atomicAdd(dtab_s + li, ds);
-    else if (gi >= 0) atomicAdd(p.dtab_g + size_t(h) * kWg2 + gi, ds);
-    else bias_mlp_grad(units, p.hidden, ds, (kxy.x - qxy.x) * p.inv_patch, (kxy.y - qxy.y) * p.inv_patch, mlpg);
-}
-
-// A-operand fragments of a 16-row tile (rows at stride RW).
-template <int HD, int RW>
-__device__ __forceinline__ void load_a16(uint32_t (&a)[HD / 16][4], const __nv_bfloat16* base, int lane) {
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk)
-        ldmatrix_x4(a[kk][0], a[kk][1], a[kk][2], a[kk][3], base + (lane & 15) * RW + kk * 16 + (lane >> 4) * 8);
-}
-// s[nt] = A(16 x HD) . B_nt^T, B_nt = rows nt*8.. of `b` (nt < NT-1) or the
-// 8-row tile `blast` (nt = NT-1; pass b + (NT-1)*8*RW for one contiguous buffer).
-template <int HD, int NT, int RW>
-__device__ __forceinline__ void mma_abt(float (&s)[NT][4], const uint32_t (&a)[HD / 16][4],
-                                        const __nv_bfloat16* b, const __nv_bfloat16* blast, int lane) {
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-        const __nv_bfloat16* kb = (nt == NT - 1 ? blast : b + nt * 8 * RW) + (lane & 7) * RW;
-        if constexpr (HD >= 32) {
-#pragma unroll
-            for (int k2 = 0; k2 < HD / 32; ++k2) {
-                uint32_t bb[4];
-                ldmatrix_x4(bb[0], bb[1], bb[2], bb[3], kb + k2 * 32 + (lane >> 3) * 8);
-                mma_bf16_16816(s[nt], a[2 * k2], bb);
-                mma_bf16_16816(s[nt], a[2 * k2 + 1], bb + 2);
-            }
-        } else {
-            uint32_t bb[2];
-            ldmatrix_x2(bb[0], bb[1], kb + ((lane >> 3) & 1) * 8);
-            mma_bf16_16816(s[nt], a[0], bb);
-        }
-    }
-}
-// o += P(16 x 16*KS) . V(rows 0 .. 16*KS-1, HD); P in accumulator layout.
-template <int HD, int KS, int NT, int RW>
-__device__ __forceinline__ void mma_pv(float (&o)[HD / 8][4], const float (&pm)[NT][4],
-                                       const __nv_bfloat16* v, int lane) {
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-        uint32_t pa[4];
-        pa[0] = pack_bf16(pm[2 * ks][0], pm[2 * ks][1]);
-        pa[1] = pack_bf16(pm[2 * ks][2], pm[2 * ks][3]);
-        pa[2] = pack_bf16(pm[2 * ks + 1][0], pm[2 * ks + 1][1]);
-        pa[3] = pack_bf16(pm[2 * ks + 1][2], pm[2 * ks + 1][3]);
-#pragma unroll
-        for (int nd = 0; nd < HD / 8; nd += 2) {
-            uint32_t b[4];
-            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], v + (ks * 16 + (lane & 15)) * RW + nd * 8 + (lane >> 4) * 8);
-            mma_bf16_16816(o[nd], pa, b);
-            mma_bf16_16816(o[nd + 1], pa, b + 2);
-        }
-    }
-}
-// Fragments (rows r0 / r0+8) -> bf16 rows in shared memory, scaled per row.
-template <int HD, int RW>
-__device__ __forceinline__ void frags_to_rows(__nv_bfloat16* sm, const float (&o)[HD / 8][4], float m0,
-                                              float m1, int lane) {
-    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
-#pragma unroll
-    for (int nd = 0; nd < HD / 8; ++nd) {
-        *reinterpret_cast<uint32_t*>(sm + r0 * RW + nd * 8 + c0) = pack_bf16(o[nd][0] * m0, o[nd][1] * m0);
-        *reinterpret_cast<uint32_t*>(sm + (r0 + 8) * RW + nd * 8 + c0) = pack_bf16(o[nd][2] * m1, o[nd][3] * m1);
-    }
-}
-// Shared rows (HD columns) -> global token rows `g + tok*ld`, 16-byte stores.
-template <int HD, int RW>
-__device__ __forceinline__ void rows_to_global(__nv_bfloat16* g, int64_t ld, const __nv_bfloat16* sm,
-                                               const int32_t* tok, int nrows, int lane) {
-    constexpr int CPR = HD / 8;
-    for (int i = lane; i < nrows * CPR; i += 32) {
-        const int r = i / CPR, ch = i - r * CPR;
-        *reinterpret_cast<uint4*>(g + int64_t(tok[r]) * ld + ch * 8) =
-            *reinterpret_cast<const uint4*>(sm + r * RW + ch * 8);
-    }
-}
-// Gather rows [0, NROWS) of a virtual row list: row r is token tok(r) of the
-// image slice `src(r)` into `dst(r)`; tok < 0 rows are skipped.  Each warp
-// instruction moves 32 / (HD/8) rows (16-byte cp.async per lane).
-template <int HD, int NROWS, typename F>
-__device__ __forceinline__ void gather(int lane, int64_t ld, F f) {
-    constexpr int CPR = HD / 8, RPI = 32 / CPR;
-    const int sub = lane / CPR, ch = lane - sub * CPR;
-#pragma unroll
-    for (int j = 0; j < (NROWS + RPI - 1) / RPI; ++j) {
-        const int r = sub + j * RPI;
-        if (r < NROWS) {
-            int tok;
-            const __nv_bfloat16* src;
-            __nv_bfloat16* dst;
-            f(r, tok, src, dst);
-            if (tok >= 0) cp_async16(dst + ch * 8, src + int64_t(tok) * ld + ch * 8);
-        }
-    }
-}
-
-// Scaled scores + bias (log2 domain) + slot mask, accumulator layout:
-// s[nt][e] <-> (row r0 + 8*(e>=2), slot nt*8 + c0 + (e&1)); tile KP/8 = blank.
-template <int KP, int NT>
-__device__ __forceinline__ void score_bias(float (&s)[NT][4], const int32_t* rec, const float* tab,
-                                           float scale2, float blank2, int nk, bool fast, int lane,
-                                           const AttnParams& p, const float4* units, int h,
-                                           int64_t img_tok) {
-    using R = QRec<KP>;
-    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
-    if (fast) {
-        const int q0 = kWinC - rec[R::QCELL + r0], q1 = kWinC - rec[R::QCELL + r0 + 8];
-#pragma unroll
-        for (int nt = 0; nt < KP / 8; ++nt) {
-            const int2 kc = *reinterpret_cast<const int2*>(rec + R::KCELL + nt * 8 + c0);
-            s[nt][0] = fmaf(s[nt][0], scale2, tab[kc.x + q0]);
-            s[nt][1] = fmaf(s[nt][1], scale2, tab[kc.y + q0]);
-            s[nt][2] = fmaf(s[nt][2], scale2, tab[kc.x + q1]);
-            s[nt][3] = fmaf(s[nt][3], scale2, tab[kc.y + q1]);
-        }
-    } else {
-        const int qt0 = rec[R::QTOK + r0], qt1 = rec[R::QTOK + r0 + 8];
-        const int qa = qt0 >= 0 ? qt0 : rec[R::QTOK], qb = qt1 >= 0 ? qt1 : rec[R::QTOK];
-#pragma unroll
-        for (int nt = 0; nt < KP / 8; ++nt) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int slot = nt * 8 + c0 + (e & 1);
-                const int kt = slot < nk ? rec[R::KTOK + slot] : rec[R::KTOK];
-                s[nt][e] = fmaf(s[nt][e], scale2, slow_bias2(p, tab, units, h, img_tok, e >= 2 ? qb : qa, kt));
-            }
-        }
-    }
-    if (nk < KP) {
-#pragma unroll
-        for (int nt = 0; nt < KP / 8; ++nt) {
-            const int sl = nt * 8 + c0;
-            if (sl >= nk) s[nt][0] = s[nt][2] = -INFINITY;
-            if (sl + 1 >= nk) s[nt][1] = s[nt][3] = -INFINITY;
-        }
-    }
-    const bool bl = c0 == 0;
-    s[NT - 1][0] = bl ? fmaf(s[NT - 1][0], scale2, blank2) : -INFINITY;
-    s[NT - 1][2] = bl ? fmaf(s[NT - 1][2], scale2, blank2) : -INFINITY;
-    s[NT - 1][1] = s[NT - 1][3] = -INFINITY;
-}
-
-// Static blank tile: row 0 = blank vector of head h, rows 1..7 zero.
-template <int HD, int RW>
-__device__ __forceinline__ void init_blank_tile(__nv_bfloat16* t, const __nv_bfloat16* blank, int h) {
-    for (int i = threadIdx.x; i < 8 * RW; i += 32) {
-        const int r = i / RW, c = i - r * RW;
-        t[i] = (r == 0 && c < HD) ? blank[h * HD + c] : __float2bfloat16(0.f);
-    }
-}
-
 // ======================================================= swizzled row tiles
 // Dense rows of HD bf16 (HD*2 bytes = CPR 16-byte chunks), chunk c of row r
 // stored at chunk c ^ sw(r): 8 consecutive rows read at one logical chunk hit
@@ -445,10 +290,6 @@ __device__ __forceinline__ void sw_init_blank_tile(__nv_bfloat16* t, const __nv_
     for (int c = threadIdx.x; c < HD; c += 32) t[Swz<HD>::at(0, c >> 3) + (c & 7)] = blank[h * HD + c];
 }
 
-static __device__ __noinline__ void bias_mlp_grad_ool(const float4* units, int hidden, float ds, float ox,
-                                                      float oy, float* acc) {
-    bias_mlp_grad(units, hidden, ds, ox, oy, acc);
-}
 static __device__ __noinline__ float bias_mlp_ool(const float4* units, int hidden, float b2, float ox, float oy) {
     return bias_mlp(units, hidden, b2, ox, oy) * kLog2e;
 }
@@ -490,40 +331,123 @@ __device__ __forceinline__ void slow_bias_frag(float (&s)[NT][4], const int32_t*
         }
 }
 
-// Bias-table gradient of the lane's dS fragment on a non-fast item: tier 1 ->
-// warp window (shared atomics), tier 2 -> global table, tier 3 -> MLP partials.
-template <int KP, int NT>
-__device__ __forceinline__ void slow_bias_grad_frag(const float (&s)[NT][4], const int32_t* qtok,
-                                                    const int32_t* ktok, int nk, int qlen, float* dtab,
-                                                    const float4* units, float* mlpg, const AttnParams& p,
-                                                    int h, int64_t img_tok, int lane) {
-    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+// Bias-table gradient of a general (non-fast) item from the row-major dS tile
+// `scr` [16][KP]: per query row, lanes walk the key slots (slot lane, lane+32),
+// so same-phase keys of one row hit distinct window cells (plain RMW unless
+// the record flags duplicate cells); far same-phase pairs go to a global table
+// replica (REDG), off-lattice pairs to the MLP partials.
+template <int KP>
+__device__ __forceinline__ void general_grad_rowpass(const float* scr, const int32_t* qtok, const int32_t* ktok,
+                                                     int nk, int qlen, bool dup, float* dtab, float* dtab_rep,
+                                                     const float4* units, float* mlpg, const AttnParams& p,
+                                                     int64_t img_tok, int lane) {
     const float2* xy = reinterpret_cast<const float2*>(p.coords) + img_tok;
-    const int qa = qtok[r0] >= 0 ? qtok[r0] : qtok[0], qb = qtok[r0 + 8] >= 0 ? qtok[r0 + 8] : qtok[0];
-    const float2 q0 = __ldg(xy + qa), q1 = __ldg(xy + qb);
-    const TokInfo ti0 = make_tokinfo(q0, p.inv_patch), ti1 = make_tokinfo(q1, p.inv_patch);
-    float* tg = p.dtab_g + size_t(h) * kWg2;
+    const bool va = lane < nk, vb = KP > 32 && lane + 32 < nk;
+    const float2 ka = __ldg(xy + (va ? ktok[lane] : ktok[0]));
+    const float2 kb = __ldg(xy + (vb ? ktok[lane + 32] : ktok[0]));
+    const float2 qx = __ldg(xy + (lane < qlen ? qtok[lane] : qtok[0]));
+    const TokInfo kia = make_tokinfo(ka, p.inv_patch), kib = make_tokinfo(kb, p.inv_patch);
+    for (int r = 0; r < qlen; ++r) {
+        const float2 q = make_float2(__shfl_sync(0xffffffffu, qx.x, r), __shfl_sync(0xffffffffu, qx.y, r));
+        const TokInfo qi = make_tokinfo(q, p.inv_patch);
 #pragma unroll
-    for (int nt = 0; nt < KP / 8; ++nt)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const int sl = nt * 8 + c0 + j;
-            if (sl >= nk) continue;
-            const float2 k = __ldg(xy + ktok[sl]);
-            const TokInfo ki = make_tokinfo(k, p.inv_patch);
-#pragma unroll
-            for (int hi = 0; hi < 2; ++hi) {
-                const float ds = s[nt][2 * hi + j];
-                if (r0 + 8 * hi >= qlen || ds == 0.f) continue;
-                int gi;
-                const int li = lut_index(hi ? ti1 : ti0, ki, gi);
-                const float2 q = hi ? q1 : q0;
-                if (li >= 0) atomicAdd(dtab + li, ds);
-                else if (gi >= 0) atomicAdd(tg + gi, ds);
-                else bias_mlp_grad_ool(units, p.hidden, ds, (k.x - q.x) * p.inv_patch, (k.y - q.y) * p.inv_patch, mlpg);
+        for (int half = 0; half < 2; ++half) {
+            const bool v = half ? vb : va;
+            const float ds = v ? scr[r * KP + lane + 32 * half] : 0.f;
+            const TokInfo& ki = half ? kib : kia;
+            const float2 k = half ? kb : ka;
+            int gi = -1, li = -1;
+            if (v) li = lut_index(qi, ki, gi);
+            if (v && li >= 0) {
+                if (dup) atomicAdd(dtab + li, ds);
+                else dtab[li] += ds;
+            } else if (v && gi >= 0) {
+                atomicAdd(dtab_rep + gi, ds);
             }
+            // tier 3 (off-lattice / beyond the table): warp-aggregated MLP gradient
+            const bool t3 = v && li < 0 && gi < 0;
+            if (__any_sync(0xffffffffu, t3)) {
+                const float ox = (k.x - q.x) * p.inv_patch, oy = (k.y - q.y) * p.inv_patch;
+                const float d3 = t3 ? ds : 0.f;
+                for (int u = 0; u < p.hidden; ++u) {
+                    const float4 w = units[u];
+                    const float t = tanh_fast(fmaf(w.x, ox, fmaf(w.y, oy, w.z)));
+                    const float dpre = d3 * w.w * (1.f - t * t);
+                    const float a0 = warp_sum(dpre * ox), a1 = warp_sum(dpre * oy);
+                    const float a2 = warp_sum(dpre), a3 = warp_sum(d3 * t);
+                    if (lane == 0) {
+                        mlpg[u] += a0;
+                        mlpg[p.hidden + u] += a1;
+                        mlpg[2 * p.hidden + u] += a2;
+                        mlpg[3 * p.hidden + u] += a3;
+                    }
+                }
+                const float a4 = warp_sum(d3);
+                if (lane == 0) mlpg[4 * p.hidden] += a4;
+            }
+            __syncwarp();
         }
+    }
 }
+
+// Bias (log2 domain) of a same-phase pair from packed cells: shared window
+// when the offset is inside it, else the global table (L2).
+constexpr int kPackC = (kRs << 16) | kRs;
+__device__ __forceinline__ int packed_window(int kp, int qp) {
+    const int d = kp - qp + kPackC;
+    const int lo = d & 0xffff, hi = d >> 16;
+    return (unsigned(lo) <= 2u * kRs && unsigned(hi) <= 2u * kRs) ? hi * kWs + lo : -1;
+}
+__device__ __forceinline__ int packed_global(int kp, int qp) {
+    const int dx = (kp & 0xffff) - (qp & 0xffff), dy = (kp >> 16) - (qp >> 16);
+    return (dy + kRg) * kWg + dx + kRg;
+}
+__device__ __forceinline__ float medium_bias2(int kp, int qp, const float* tab, const float* tabg_h) {
+    const int li = packed_window(kp, qp);
+    return li >= 0 ? tab[li] : __ldg(tabg_h + packed_global(kp, qp)) * kLog2e;
+}
+template <int KP, int NT>
+__device__ __forceinline__ void medium_bias_frag(float (&s)[NT][4], const int32_t* qcell, const int32_t* kcell,
+                                                 const float* tab, const float* tabg_h, float scale2, int lane) {
+    const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+    const int q0 = qcell[r0], q1 = qcell[r0 + 8];
+#pragma unroll
+    for (int nt = 0; nt < KP / 8; ++nt) {
+        const int2 kc = *reinterpret_cast<const int2*>(kcell + nt * 8 + c0);
+        s[nt][0] = fmaf(s[nt][0], scale2, medium_bias2(kc.x, q0, tab, tabg_h));
+        s[nt][1] = fmaf(s[nt][1], scale2, medium_bias2(kc.y, q0, tab, tabg_h));
+        s[nt][2] = fmaf(s[nt][2], scale2, medium_bias2(kc.x, q1, tab, tabg_h));
+        s[nt][3] = fmaf(s[nt][3], scale2, medium_bias2(kc.y, q1, tab, tabg_h));
+    }
+}
+// Bias-table gradient of a medium item from the row-major dS tile.
+template <int KP>
+__device__ __forceinline__ void medium_grad_rowpass(const float* scr, const int32_t* qcell, const int32_t* kcell,
+                                                    int nk, int qlen, bool dup, float* dtab, float* rep, int lane,
+                                                    int exp_flags = 0) {
+    const bool va = lane < nk, vb = KP > 32 && lane + 32 < nk;
+    const int ka = va ? kcell[lane] : 0, kb = vb ? kcell[lane + 32] : 0;
+    const int qcl = lane < 16 ? qcell[lane] : 0;
+    for (int r = 0; r < qlen; ++r) {
+        const int qp = __shfl_sync(0xffffffffu, qcl, r);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            if (half ? vb : va) {
+                const int kp = half ? kb : ka;
+                const float ds = scr[r * KP + lane + 32 * half];
+                const int li = packed_window(kp, qp);
+                if (li >= 0) {
+                    if (dup) atomicAdd(dtab + li, ds);
+                    else dtab[li] += ds;
+                } else if (!(exp_flags & 1)) {
+                    atomicAdd(rep + packed_global(kp, qp), ds);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // Masks of the score fragment: padding slots [nk, KP), blank tile (slot KP only).
 template <int KP, int NT>
 __device__ __forceinline__ void mask_slots(float (&s)[NT][4], int nk, float scale2, float blank2, int lane) {
@@ -576,7 +500,7 @@ struct FwdCfg {
 
 // Per warp, item i: [Q,K(i) landed] S = QK^T -> issue Q,K(i+1) -> softmax ->
 // [V(i) landed] O = PV -> issue V(i+1) -> store O; records two items ahead.
-template <int HD, int KP>
+template <int HD, int KP, bool FAST>
 __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnParams p) {
     using C = FwdCfg<HD, KP>;
     using R = QRec<KP>;
@@ -585,7 +509,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
     auto& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
     const int lane = threadIdx.x, h = blockIdx.y;
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
-    const int n_items = p.batch * p.cs.c, stride = gridDim.x;
+    const int32_t* list = p.items + (FAST ? 0 : p.batch * p.cs.c);
+    const int n_items = __ldg(p.item_count + (FAST ? 0 : 1)), stride = gridDim.x;
     const int64_t ld = int64_t(p.heads) * HD;
     const uint32_t rowb = uint32_t(ld * 2);
     const __nv_bfloat16* qg = p.q + h * HD;
@@ -605,7 +530,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
     }
     auto rec_of = [&](int it) -> int32_t* { return sm.rec[it % 3]; };
     auto copy_item_rec = [&](int item, int it) {
-        if (item < n_items) copy_rec<C::QW>(rec_of(it), p.qrec + size_t(item) * C::QW, lane);
+        if (item < n_items) copy_rec<C::QW>(rec_of(it), p.qrec + size_t(__ldg(list + item)) * C::QW, lane);
     };
 
     const int i0 = blockIdx.x;
@@ -635,7 +560,6 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
         const int32_t* rec = rec_of(it);
         const int32_t* rec1 = rec_of(it + 1);
         const int nk = rec[R::HDR + kHNk], qlen = rec[R::HDR + kHQlen];
-        const bool fast = rec[R::HDR + kHFast] != 0;
         const int64_t img_tok = rec[R::HDR + kHImgTok], io_cur = img_tok * ld;
         const int64_t io_nxt = int64_t(rec1[R::HDR + kHImgTok]) * ld;
 
@@ -649,9 +573,16 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
             sw_gather<HD, KP>(sm.K, kg + io_nxt, rowb, rec1 + R::KTOK, lane);
         }
         cp_async_commit();
-        if (fast) fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
-        else slow_bias_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, sm.tab, sm.units, p, h,
-                                    img_tok, scale2, lane);
+        if constexpr (FAST) {
+            fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
+        } else {
+            if (rec[R::HDR + kHFast] == 2)
+                medium_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, p.tab_g + size_t(h) * kWg2,
+                                         scale2, lane);
+            else
+                slow_bias_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, sm.tab, sm.units, p, h, img_tok,
+                                       scale2, lane);
+        }
         mask_slots<KP, NT>(s, nk, scale2, blank2, lane);
 
         float m0 = -INFINITY, m1 = -INFINITY;
@@ -715,6 +646,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
 template <int HD, int KP>
 struct BwdQCfg {
     static constexpr int NT = KP / 8 + 1;
+    static constexpr int kScrFloats = (16 * KP > 8 * HD ? 16 * KP : 8 * HD);
     static constexpr int QW = QRec<KP>::WORDS;
     struct alignas(16) Smem {
         __nv_bfloat16 Q[16 * HD];
@@ -723,8 +655,7 @@ struct BwdQCfg {
         __nv_bfloat16 V[KP * HD];
         __nv_bfloat16 Kb[8 * HD];  // blank key / value tiles
         __nv_bfloat16 Vb[8 * HD];
-        __nv_bfloat16 O[16 * HD];  // dQ staging
-        float scr[8 * KP];         // dS rows of one half tile (bias-table gradient pass)
+        float scr[kScrFloats];     // dS tile (bias-table gradient pass) / dQ staging
         float lse[16];
         int32_t rec[3][QW];
         float tab[kWs2];
@@ -737,7 +668,7 @@ struct BwdQCfg {
 // Per warp, item i (everything of i landed):  S = QK^T, dP = dO.V^T ->
 // issue V(i+1) -> P, D, dS -> dQ = dS.K -> issue K(i+1) -> blank grads (Q, dO)
 // -> issue Q, dO, LSE(i+1) -> bias-table gradient -> store dQ.
-template <int HD, int KP>
+template <int HD, int KP, bool FAST>
 __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnParams p) {
     using C = BwdQCfg<HD, KP>;
     using R = QRec<KP>;
@@ -746,7 +677,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
     auto& sm = *reinterpret_cast<typename C::Smem*>(smem_raw);
     const int lane = threadIdx.x, h = blockIdx.y;
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
-    const int n_items = p.batch * p.cs.c, stride = gridDim.x;
+    const int32_t* list = p.items + (FAST ? 0 : p.batch * p.cs.c);
+    const int n_items = __ldg(p.item_count + (FAST ? 0 : 1)), stride = gridDim.x;
     const int64_t ld = int64_t(p.heads) * HD;
     const uint32_t rowb = uint32_t(ld * 2);
     const __nv_bfloat16* qg = p.q + h * HD;
@@ -772,7 +704,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
     float gblank = 0.f;
 
     auto copy_item_rec = [&](int item, int32_t* dst) {
-        if (item < n_items) copy_rec<C::QW>(dst, p.qrec + size_t(item) * C::QW, lane);
+        if (item < n_items) copy_rec<C::QW>(dst, p.qrec + size_t(__ldg(list + item)) * C::QW, lane);
     };
     auto issue_qo = [&](const int32_t* rec, int64_t img_tok) {
         sw_gather<HD, 16>(sm.Q, qg + img_tok * ld, rowb, rec + R::QTOK, lane);
@@ -810,7 +742,6 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         const int32_t* rec1 = sm.rec[r1];
         const bool more = item + stride < n_items;
         const int nk = rec[R::HDR + kHNk], qlen = rec[R::HDR + kHQlen];
-        const bool fast = rec[R::HDR + kHFast] != 0;
         const int64_t img_tok = rec[R::HDR + kHImgTok];
         const int64_t nxt_tok = rec1[R::HDR + kHImgTok];
 
@@ -823,9 +754,18 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         __syncwarp();  // V consumed
         if (more) sw_gather<HD, KP>(sm.V, vg + nxt_tok * ld, rowb, rec1 + R::KTOK, lane);
         cp_async_commit();
-        if (fast) fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
-        else slow_bias_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, sm.tab, sm.units, p, h, img_tok,
-                                    scale2, lane);
+        const int cls = rec[R::HDR + kHFast];
+        if constexpr (FAST) {
+            fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
+        } else {
+            if (p.exp_flags & 4) {
+            } else if (cls == 2)
+                medium_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, p.tab_g + size_t(h) * kWg2,
+                                         scale2, lane);
+            else
+                slow_bias_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, sm.tab, sm.units, p, h, img_tok,
+                                       scale2, lane);
+        }
         mask_slots<KP, NT>(s, nk, scale2, blank2, lane);
 
         // P = exp(S - LSE);  D = rowsum(P o dP)
@@ -916,50 +856,56 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         __syncwarp();  // Q, dO, LSE consumed
         if (more) issue_qo(rec1, nxt_tok);
         cp_async_commit();
-        // ---- bias-table gradient
-        if (fast) {
-            // Rows of one query hold pairwise-distinct key cells, so a row-major
-            // pass writes distinct window entries per instruction: plain RMW
-            // (duplicate key coordinates -> the rec flags force atomics).
-            float* scr = sm.scr;
-            const bool dup0 = rec[R::HDR + kHDup0] != 0, dup1 = rec[R::HDR + kHDup1] != 0;
-            const int ka = lane < nk ? rec[R::KCELL + lane] + kWinC : 0;
-            const int kb = lane + 32 < nk ? rec[R::KCELL + lane + 32] + kWinC : 0;
+        // ---- bias-table gradient (dS tile row-major in scratch, then one pass per query row)
+        float* scr = sm.scr;
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                __syncwarp();
-#pragma unroll
-                for (int nt = 0; nt < KP / 8; ++nt)
-                    *reinterpret_cast<float2*>(scr + r0 * KP + nt * 8 + c0) =
-                        make_float2(s[nt][2 * half], s[nt][2 * half + 1]);
-                __syncwarp();
-                const int rows = min(8, qlen - 8 * half);
-                for (int rr = 0; rr < rows; ++rr) {
-                    const int qc = rec[R::QCELL + 8 * half + rr];
-                    if (lane < nk) {
-                        float* a = dtab + ka - qc;
-                        const float v = scr[rr * KP + lane];
-                        if (dup0) atomicAdd(a, v);
-                        else *a += v;
-                    }
+        for (int nt = 0; nt < KP / 8; ++nt) {
+            *reinterpret_cast<float2*>(scr + r0 * KP + nt * 8 + c0) = make_float2(s[nt][0], s[nt][1]);
+            *reinterpret_cast<float2*>(scr + (r0 + 8) * KP + nt * 8 + c0) = make_float2(s[nt][2], s[nt][3]);
+        }
+        __syncwarp();
+        const bool dup = (rec[R::HDR + kHDup0] | rec[R::HDR + kHDup1]) != 0;
+        if constexpr (FAST) {
+            // Rows of one query hold pairwise-distinct key cells, so lanes over the
+            // key slots of one row write distinct window entries: plain RMW
+            // (duplicate key coordinates -> the record flags force atomics).
+            const bool va = lane < nk, vb = KP > 32 && lane + 32 < nk;
+            float* da = dtab + (va ? rec[R::KCELL + lane] + kWinC : 0);
+            float* db = dtab + (vb ? rec[R::KCELL + lane + 32] + kWinC : 0);
+            const int qcl = lane < 16 ? rec[R::QCELL + lane] : 0;
+            if (!dup) {
+                for (int r = 0; r < qlen; ++r) {
+                    const int qc = __shfl_sync(0xffffffffu, qcl, r);
+                    if (va) da[-qc] += scr[r * KP + lane];
+                    if (vb) db[-qc] += scr[r * KP + lane + 32];
                     __syncwarp();
-                    if (KP > 32 && lane + 32 < nk) {
-                        float* a = dtab + kb - qc;
-                        const float v = scr[rr * KP + lane + 32];
-                        if (dup1) atomicAdd(a, v);
-                        else *a += v;
-                    }
+                }
+            } else {
+                for (int r = 0; r < qlen; ++r) {
+                    const int qc = __shfl_sync(0xffffffffu, qcl, r);
+                    if (va) atomicAdd(da - qc, scr[r * KP + lane]);
+                    __syncwarp();
+                    if (vb) atomicAdd(db - qc, scr[r * KP + lane + 32]);
                     __syncwarp();
                 }
             }
         } else {
-            slow_bias_grad_frag<KP, NT>(s, rec + R::QTOK, rec + R::KTOK, nk, qlen, dtab, sm.units, sm.mlpg,
-                                        p, h, img_tok, lane);
+            float* rep = p.dtab_g + (size_t(blockIdx.x & (kTabReplicas - 1)) * p.heads + h) * kWg2;
+            if (p.exp_flags & 2) {
+            } else if (cls == 2)
+                medium_grad_rowpass<KP>(scr, rec + R::QCELL, rec + R::KCELL, nk, qlen, dup, dtab, rep, lane,
+                                        p.exp_flags);
+            else
+                general_grad_rowpass<KP>(scr, rec + R::QTOK, rec + R::KTOK, nk, qlen, dup, dtab, rep, sm.units,
+                                         sm.mlpg, p, img_tok, lane);
         }
-        // ---- store dQ
-        sw_frags_to_rows<HD>(sm.O, dqa, p.scale, p.scale, lane);
         __syncwarp();
-        sw_rows_to_global<HD>(p.dq + img_tok * ld + h * HD, rowb, sm.O, rec + R::QTOK, qlen, lane);
+        // ---- store dQ (staged through the scratch)
+        __nv_bfloat16* Ost = reinterpret_cast<__nv_bfloat16*>(scr);
+        sw_frags_to_rows<HD>(Ost, dqa, p.scale, p.scale, lane);
+        __syncwarp();
+        sw_rows_to_global<HD>(p.dq + img_tok * ld + h * HD, rowb, Ost, rec + R::QTOK, qlen, lane);
+        __syncwarp();
         rc = r1;
     }
     cp_async_wait<0>();
@@ -1082,7 +1028,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
 
     uint32_t ka[HD / 16][4], va[HD / 16][4];
     float dk[HD / 8][4], dv[HD / 8][4];
-    int kq0 = 0, kq1 = 0, kt0 = 0, kt1 = 0;
+    int kq0 = 0, kq1 = 0, kt0 = 0, kt1 = 0, kp0 = 0, kp1 = 0;
+    const float* tabg_h = p.tab_g + size_t(h) * kWg2;
     int rc = 0;
     for (int it = 0; pr0 >= 0; ++it) {
         const int r1 = rc == 2 ? 0 : rc + 1, r2 = r1 == 2 ? 0 : r1 + 1;
@@ -1105,6 +1052,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
             kq1 = krec[KRec::KCELL + r0 + 8] + kWinC;
             kt0 = krec[KRec::KTOK + (r0 < klen ? r0 : 0)];
             kt1 = krec[KRec::KTOK + (r0 + 8 < klen ? r0 + 8 : 0)];
+            kp0 = krec[KRec::KPCELL + r0];
+            kp1 = krec[KRec::KPCELL + r0 + 8];
             __syncwarp();  // K, V consumed
         }
         int it2 = 0;
@@ -1118,12 +1067,18 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
         float sT[2][4], dpT[2][4];
         sw_mma_abt<HD, 2>(sT, ka, Qb, Qb + 8 * HD, lane);
         sw_mma_abt<HD, 2>(dpT, va, Ob, Ob + 8 * HD, lane);
-        const bool fast = rec[PRec::HDR + kPFast] != 0;
+        const int pcls = rec[PRec::HDR + kPFast];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
             const int qc = nt * 8 + c0;
             float b[4];
-            if (fast) {
+            if (pcls == 2) {
+                const int2 qcl = *reinterpret_cast<const int2*>(rec + PRec::QCELL + qc);
+                b[0] = medium_bias2(kp0, qcl.x, sm.tab, tabg_h);
+                b[1] = medium_bias2(kp0, qcl.y, sm.tab, tabg_h);
+                b[2] = medium_bias2(kp1, qcl.x, sm.tab, tabg_h);
+                b[3] = medium_bias2(kp1, qcl.y, sm.tab, tabg_h);
+            } else if (pcls == 1) {
                 const int2 qcl = *reinterpret_cast<const int2*>(rec + PRec::QCELL + qc);
                 b[0] = sm.tab[kq0 - qcl.x];
                 b[1] = sm.tab[kq0 - qcl.y];
@@ -1205,29 +1160,57 @@ inline int persistent_grid(K kern, size_t smem, int items, int heads, dim3& grid
     return AFFMAE_OK;
 }
 
+// Two launches per pass: the lattice-fast item list, then the general list
+// (item counts live on the device, so the launch shapes are capture-safe).
 template <int HD, int KP>
 int launch_fwd(const AttnParams& p, cudaStream_t st) {
-    auto kern = attn_fwd_kernel<HD, KP>;
-    const size_t smem = sizeof(typename FwdCfg<HD, KP>::Smem);
-    dim3 grid;
-    int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
-    if (rc) return rc;
-    kern<<<grid, 32, smem, st>>>(p);
-    AFFMAE_LAUNCH_CHECK("attn_fwd_kernel");
+    {
+        auto kern = attn_fwd_kernel<HD, KP, true>;
+        const size_t smem = sizeof(typename FwdCfg<HD, KP>::Smem);
+        dim3 grid;
+        int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
+        if (rc) return rc;
+        kern<<<grid, 32, smem, st>>>(p);
+        AFFMAE_LAUNCH_CHECK("attn_fwd_kernel<fast>");
+    }
+    {
+        auto kern = attn_fwd_kernel<HD, KP, false>;
+        const size_t smem = sizeof(typename FwdCfg<HD, KP>::Smem);
+        dim3 grid;
+        int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
+        if (rc) return rc;
+        kern<<<grid, 32, smem, st>>>(p);
+        AFFMAE_LAUNCH_CHECK("attn_fwd_kernel<general>");
+    }
     return AFFMAE_OK;
 }
 
-// Launches the query-side kernel; `grid_x` returns its CTA count per head.
+// Launches the query-side kernels; `grid_x[2]` returns their CTA counts per
+// head; their per-warp partials go to part and part + heads*grid_x[0]*part_width.
 template <int HD, int KP>
-int launch_bwd_q(const AttnParams& p, cudaStream_t st, int& grid_x) {
-    auto kern = attn_bwd_q_kernel<HD, KP>;
-    const size_t smem = sizeof(typename BwdQCfg<HD, KP>::Smem);
-    dim3 grid;
-    int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
-    if (rc) return rc;
-    kern<<<grid, 32, smem, st>>>(p);
-    AFFMAE_LAUNCH_CHECK("attn_bwd_q_kernel");
-    grid_x = int(grid.x);
+int launch_bwd_q(const AttnParams& p, cudaStream_t st, int* grid_x) {
+    AttnParams q = p;
+    {
+        auto kern = attn_bwd_q_kernel<HD, KP, true>;
+        const size_t smem = sizeof(typename BwdQCfg<HD, KP>::Smem);
+        dim3 grid;
+        int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
+        if (rc) return rc;
+        kern<<<grid, 32, smem, st>>>(q);
+        AFFMAE_LAUNCH_CHECK("attn_bwd_q_kernel<fast>");
+        grid_x[0] = int(grid.x);
+    }
+    q.part = p.part + size_t(p.heads) * grid_x[0] * part_width(HD);
+    {
+        auto kern = attn_bwd_q_kernel<HD, KP, false>;
+        const size_t smem = sizeof(typename BwdQCfg<HD, KP>::Smem);
+        dim3 grid;
+        int rc = persistent_grid(kern, smem, p.batch * p.cs.c, p.heads, grid);
+        if (rc) return rc;
+        kern<<<grid, 32, smem, st>>>(q);
+        AFFMAE_LAUNCH_CHECK("attn_bwd_q_kernel<general>");
+        grid_x[1] = int(grid.x);
+    }
     return AFFMAE_OK;
 }
 
@@ -1245,7 +1228,7 @@ int launch_bwd_kv(const AttnParams& p, cudaStream_t st) {
 
 #define AFFMAE_INSTANTIATE_ATTN_QK(HD_, KP_)                               \
     template int launch_fwd<HD_, KP_>(const AttnParams&, cudaStream_t); \
-    template int launch_bwd_q<HD_, KP_>(const AttnParams&, cudaStream_t, int&);
+    template int launch_bwd_q<HD_, KP_>(const AttnParams&, cudaStream_t, int*);
 #define AFFMAE_INSTANTIATE_ATTN_KV(HD_) template int launch_bwd_kv<HD_>(const AttnParams&, cudaStream_t);
 
 }  // namespace affmae_b200
