@@ -437,6 +437,235 @@ __global__ void dp_reduce_kernel(const float* __restrict__ part, int nparts, flo
     }
 }
 
+// ------------------------------------------- vectorised pool kernels (dim % 8 == 0)
+// A row of D bf16 is CPR = D/8 16-byte chunks; LPR lanes share a row (one or
+// more chunks each), RPW = 32/LPR rows per warp.  The pool's weights are
+// computed redundantly by the row's lanes (broadcast loads), and every pool
+// member's chunk is loaded before it is used (memory-level parallelism).
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(h[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
+    uint4 v;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return v;
+}
+
+template <int KMAX>
+__device__ __forceinline__ int pool_row_weights(const int32_t* pool_idx, const double* pool_dist,
+                                                const int32_t* pool_cnt, int64_t row, int k_m, float p,
+                                                int (&jj)[KMAX], float (&w)[KMAX], float (&dd)[KMAX]) {
+    const int cnt = pool_cnt[row];
+    float m = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) {
+        jj[t] = t < cnt ? pool_idx[row * k_m + t] : 0;
+        dd[t] = t < cnt ? float(pool_dist[row * k_m + t]) : 0.f;
+        if (t < cnt) m = fmaxf(m, -p * dd[t]);
+    }
+    float l = 0.f;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) {
+        w[t] = t < cnt ? __expf(-p * dd[t] - m) : 0.f;
+        l += w[t];
+    }
+    const float il = cnt > 0 ? 1.f / l : 0.f;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) w[t] *= il;
+    return cnt;
+}
+
+template <int CPR, int KMAX>
+__global__ void __launch_bounds__(256) pool_fwd_v2_kernel(
+    const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
+    const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
+    const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
+    int64_t r, int k_m, __nv_bfloat16* __restrict__ out) {
+    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR, CPL = CPR / LPR;
+    const int lane = threadIdx.x & 31, sl = lane % LPR;
+    const int64_t row = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPW + lane / LPR;
+    if (row >= batch * r) return;
+    const int64_t b = row / r;
+    constexpr int D = CPR * 8;
+    int jj[KMAX];
+    float w[KMAX], dd[KMAX];
+    const int cnt = pool_row_weights<KMAX>(pool_idx, pool_dist, pool_cnt, row, k_m, *p_merge, jj, w, dd);
+    const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * D);
+    const float* sb = scores + b * n;
+    float g[KMAX];
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) g[t] = t < cnt ? w[t] * sb[jj[t]] : 0.f;
+    uint4* o = reinterpret_cast<uint4*>(out + row * 2 * D);
+    const int64_t rt = retained[row];
+#pragma unroll
+    for (int cc = 0; cc < CPL; ++cc) {
+        const int ch = sl + cc * LPR;
+        uint4 v[KMAX];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t)
+            if (t < cnt) v[t] = __ldg(fb + int64_t(jj[t]) * CPR + ch);
+        o[ch] = __ldg(fb + rt * CPR + ch);
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) {
+            if (t < cnt) {
+                float f[8];
+                bf16x8_to_f32(v[t], f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] = fmaf(g[t], f[i], acc[i]);
+            }
+        }
+        o[CPR + ch] = f32_to_bf16x8(acc);
+    }
+}
+
+template <int CPR, int KMAX>
+__global__ void __launch_bounds__(256) pool_bwd_v2_kernel(
+    const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
+    const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
+    const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
+    int64_t r, int k_m, const __nv_bfloat16* __restrict__ dout, __nv_bfloat16* __restrict__ dfeats,
+    float* __restrict__ dscores, float* __restrict__ dp_part) {
+    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR, CPL = CPR / LPR;
+    const int lane = threadIdx.x & 31, sl = lane % LPR;
+    const int64_t row = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPW + lane / LPR;
+    const bool valid = row < batch * r;
+    float dp = 0.f;
+    const int64_t rw = valid ? row : 0;
+    const int64_t b = rw / r;
+    int jj[KMAX];
+    float w[KMAX], dd[KMAX], sj[KMAX], dot[KMAX];
+    const int cnt = valid ? pool_row_weights<KMAX>(pool_idx, pool_dist, pool_cnt, rw, k_m, *p_merge, jj, w, dd) : 0;
+    const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * CPR * 8);
+    uint4* dfb = reinterpret_cast<uint4*>(dfeats + b * n * CPR * 8);
+    const uint4* gr = reinterpret_cast<const uint4*>(dout + rw * 2 * CPR * 8);
+    const float* sb = scores + b * n;
+    float* dsb = dscores + b * n;
+    const int64_t rt = valid ? retained[rw] : 0;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) {
+        sj[t] = t < cnt ? sb[jj[t]] : 0.f;
+        dot[t] = 0.f;
+    }
+    if (valid) {
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+            const int ch = sl + cc * LPR;
+            uint4 v[KMAX];
+#pragma unroll
+            for (int t = 0; t < KMAX; ++t)
+                if (t < cnt) v[t] = __ldg(fb + int64_t(jj[t]) * CPR + ch);
+            dfb[rt * CPR + ch] = __ldg(gr + ch);
+            float go[8];
+            bf16x8_to_f32(__ldg(gr + CPR + ch), go);
+#pragma unroll
+            for (int t = 0; t < KMAX; ++t) {
+                if (t < cnt) {
+                    float f[8], df[8];
+                    bf16x8_to_f32(v[t], f);
+                    const float k = w[t] * sj[t];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        dot[t] = fmaf(go[i], f[i], dot[t]);
+                        df[i] = go[i] * k;
+                    }
+                    dfb[int64_t(jj[t]) * CPR + ch] = f32_to_bf16x8(df);
+                }
+            }
+        }
+    }
+    // row-group reduction of the dots (LPR lanes; every lane participates)
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t)
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) dot[t] += __shfl_xor_sync(0xffffffffu, dot[t], o);
+    if (valid && sl == 0) {
+        dsb[rt] = 0.f;
+        float wdot = 0.f;
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t)
+            if (t < cnt) {
+                dsb[jj[t]] = w[t] * dot[t];
+                wdot = fmaf(w[t], sj[t] * dot[t], wdot);
+            }
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t)
+            if (t < cnt) dp = fmaf(w[t] * (sj[t] * dot[t] - wdot), -dd[t], dp);
+    }
+    // block partial of dp (fixed order)
+    __shared__ float red[8];
+    dp = warp_sum(dp);
+    if (lane == 0) red[threadIdx.x >> 5] = dp;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.f;
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) s += red[i];
+        dp_part[blockIdx.x] = s;
+    }
+}
+
+// tokens that feed no output row (truncated pool members): zero gradient (thread per token)
+template <int CPR>
+__global__ void pool_bwd_zero_v2_kernel(const int32_t* __restrict__ row_of, int64_t total,
+                                        __nv_bfloat16* __restrict__ dfeats, float* __restrict__ dscores) {
+    const int64_t tok = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tok >= total || row_of[tok] >= 0) return;
+    uint4* d = reinterpret_cast<uint4*>(dfeats) + tok * CPR;
+    for (int c = 0; c < CPR; ++c) d[c] = make_uint4(0, 0, 0, 0);
+    dscores[tok] = 0.f;
+}
+
+template <int CPR>
+static int launch_pool_fwd_v2(const __nv_bfloat16* feats, const float* scores, const float* p_merge,
+                              const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
+                              int64_t r, int k_m, __nv_bfloat16* out, cudaStream_t st) {
+    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR;
+    const int64_t warps = (batch * r + RPW - 1) / RPW;
+    const unsigned nb = unsigned((warps + 7) / 8);
+    if (k_m <= 8)
+        pool_fwd_v2_kernel<CPR, 8><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
+                                                        plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, out);
+    else
+        pool_fwd_v2_kernel<CPR, 16><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
+                                                         plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, out);
+    AFFMAE_LAUNCH_CHECK("pool_fwd_v2_kernel");
+    return AFFMAE_OK;
+}
+template <int CPR>
+static unsigned pool_bwd_v2_blocks(int64_t batch, int64_t r) {
+    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR;
+    const int64_t warps = (batch * r + RPW - 1) / RPW;
+    return unsigned((warps + 7) / 8);
+}
+template <int CPR>
+static int launch_pool_bwd_v2(const __nv_bfloat16* feats, const float* scores, const float* p_merge,
+                              const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
+                              int64_t r, int k_m, const __nv_bfloat16* dout, __nv_bfloat16* dfeats,
+                              float* dscores, float* part, cudaStream_t st, unsigned& nb) {
+    nb = pool_bwd_v2_blocks<CPR>(batch, r);
+    pool_bwd_zero_v2_kernel<CPR><<<unsigned((batch * n + 255) / 256), 256, 0, st>>>(plan->row_of, batch * n,
+                                                                                    dfeats, dscores);
+    AFFMAE_LAUNCH_CHECK("pool_bwd_zero_v2_kernel");
+    if (k_m <= 8)
+        pool_bwd_v2_kernel<CPR, 8><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
+                                                        plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, dout,
+                                                        dfeats, dscores, part);
+    else
+        pool_bwd_v2_kernel<CPR, 16><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
+                                                         plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, dout,
+                                                         dfeats, dscores, part);
+    AFFMAE_LAUNCH_CHECK("pool_bwd_v2_kernel");
+    return AFFMAE_OK;
+}
+
 // ===================================================================== host
 struct SelWs {
     uint64_t* keys[2];
@@ -596,6 +825,18 @@ int merge_pool_fwd(const affmae_bf16* feats, const float* scores, const float* p
     if (dim < 2 || dim % 2) return fail(AFFMAE_EUNSUPPORTED, "merge_pool: dim must be even");
     if (k_m < 1 || k_m > kMaxKm) return fail(AFFMAE_EUNSUPPORTED, "merge_pool: k_m must be in [1, 16]");
     if (batch * r == 0) return AFFMAE_OK;
+    {
+        const auto* f = reinterpret_cast<const __nv_bfloat16*>(feats);
+        auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+        cudaStream_t st = as_stream(stream);
+        switch (dim) {
+            case 64: return launch_pool_fwd_v2<8>(f, scores, p_merge, retained, plan, batch, n, r, k_m, o, st);
+            case 128: return launch_pool_fwd_v2<16>(f, scores, p_merge, retained, plan, batch, n, r, k_m, o, st);
+            case 256: return launch_pool_fwd_v2<32>(f, scores, p_merge, retained, plan, batch, n, r, k_m, o, st);
+            case 512: return launch_pool_fwd_v2<64>(f, scores, p_merge, retained, plan, batch, n, r, k_m, o, st);
+            default: break;
+        }
+    }
     pool_fwd_kernel<<<blocks_of(batch * r * 32), 256, 0, as_stream(stream)>>>(
         reinterpret_cast<const __nv_bfloat16*>(feats), scores, p_merge, retained, plan->pool_idx,
         plan->pool_dist, plan->pool_cnt, batch, n, r, int(dim), k_m, reinterpret_cast<__nv_bfloat16*>(out));
@@ -604,7 +845,7 @@ int merge_pool_fwd(const affmae_bf16* feats, const float* scores, const float* p
 }
 
 size_t merge_pool_bwd_workspace(int64_t batch, int64_t r) {
-    return al256(size_t(blocks_of(batch * r * 32)) * 4 + 4);
+    return al256(size_t(blocks_of(batch * r * 32)) * 4 + 4);  // >= every variant's block count
 }
 
 int merge_pool_bwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
@@ -619,8 +860,28 @@ int merge_pool_bwd(const affmae_bf16* feats, const float* scores, const float* p
         return fail(AFFMAE_ECONFIG, "merge_pool bwd: workspace too small");
     if (batch == 0) return AFFMAE_OK;
     cudaStream_t st = as_stream(stream);
-    const unsigned nb = blocks_of(batch * r * 32);
     float* part = static_cast<float*>(workspace);
+    {
+        const auto* f = reinterpret_cast<const __nv_bfloat16*>(feats);
+        const auto* g = reinterpret_cast<const __nv_bfloat16*>(dout);
+        auto* df = reinterpret_cast<__nv_bfloat16*>(dfeats);
+        unsigned nb2 = 0;
+        int rc = -1;
+        switch (dim) {
+            case 64: rc = launch_pool_bwd_v2<8>(f, scores, p_merge, retained, plan, batch, n, r, k_m, g, df, dscores, part, st, nb2); break;
+            case 128: rc = launch_pool_bwd_v2<16>(f, scores, p_merge, retained, plan, batch, n, r, k_m, g, df, dscores, part, st, nb2); break;
+            case 256: rc = launch_pool_bwd_v2<32>(f, scores, p_merge, retained, plan, batch, n, r, k_m, g, df, dscores, part, st, nb2); break;
+            case 512: rc = launch_pool_bwd_v2<64>(f, scores, p_merge, retained, plan, batch, n, r, k_m, g, df, dscores, part, st, nb2); break;
+            default: break;
+        }
+        if (rc > 0) return rc;
+        if (rc == 0) {
+            dp_reduce_kernel<<<1, 1024, 0, st>>>(part, int(nb2), dp);
+            AFFMAE_LAUNCH_CHECK("dp_reduce_kernel");
+            return AFFMAE_OK;
+        }
+    }
+    const unsigned nb = blocks_of(batch * r * 32);
     pool_bwd_zero_kernel<<<blocks_of(batch * n * 32), 256, 0, st>>>(
         plan->row_of, batch * n, int(dim), reinterpret_cast<__nv_bfloat16*>(dfeats), dscores);
     pool_bwd_kernel<<<nb, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(feats), scores, p_merge,
