@@ -347,62 +347,77 @@ __global__ void dtab_replica_sum_kernel(float* __restrict__ dtab, int n) {
     dtab[i] = s;
 }
 
-__global__ void bias_grad_finalize_kernel(const float* __restrict__ dtab, const float* __restrict__ w1,
-                                          const float* __restrict__ b1, const float* __restrict__ w2,
-                                          int hidden, float* dw1, float* db1, float* dw2, float* db2) {
+// dL/dtheta = sum over table entries of dT * dT/dtheta.  Pass 1: each block
+// folds kFinEPB entries into per-block partials {dw1x[H], dw1y[H], db1[H],
+// dw2[H], db2}; pass 2 sums the block partials in a fixed order and adds
+// them (+=) into the caller's gradients (deterministic).
+constexpr int kFinEPB = 1024;
+__global__ void bias_grad_partial_kernel(const float* __restrict__ dtab, const float* __restrict__ w1,
+                                         const float* __restrict__ b1, const float* __restrict__ w2, int hidden,
+                                         float* __restrict__ fpart) {
     const int h = blockIdx.y;
     const float* dt = dtab + size_t(h) * kWg2;
-    __shared__ float red[5][32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    {
-        float acc = 0.f;
-        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kWg2; e += gridDim.x * blockDim.x) acc += dt[e];
-        acc = warp_sum(acc);
-        if (lane == 0) red[0][warp] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            float s = 0.f;
-            for (int w = 0; w < nw; ++w) s += red[0][w];
-            atomicAdd(db2 + h, s);
-        }
-        __syncthreads();
+    __shared__ float red[8][4 * kMaxHidden + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float d[kFinEPB / 256];
+    int e[kFinEPB / 256];
+#pragma unroll
+    for (int i = 0; i < kFinEPB / 256; ++i) {
+        e[i] = blockIdx.x * kFinEPB + i * 256 + threadIdx.x;
+        d[i] = e[i] < kWg2 ? dt[e[i]] : 0.f;
     }
+    float sd = 0.f;
+#pragma unroll
+    for (int i = 0; i < kFinEPB / 256; ++i) sd += d[i];
+    sd = warp_sum(sd);
+    if (lane == 0) red[warp][4 * hidden] = sd;
     for (int u = 0; u < hidden; ++u) {
         const float wx = w1[h * 2 * hidden + u], wy = w1[h * 2 * hidden + hidden + u];
         const float bb = b1[h * hidden + u], ww = w2[h * hidden + u];
         float gx = 0.f, gy = 0.f, gb = 0.f, gw = 0.f;
-        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kWg2; e += gridDim.x * blockDim.x) {
-            float d = dt[e];
-            if (d == 0.f) continue;
-            float ox = float(e % kWg - kRg), oy = float(e / kWg - kRg);
-            float t = tanhf(wx * ox + wy * oy + bb);
-            float dpre = d * ww * (1.f - t * t);
+#pragma unroll
+        for (int i = 0; i < kFinEPB / 256; ++i) {
+            if (d[i] == 0.f) continue;
+            const float ox = float(e[i] % kWg - kRg), oy = float(e[i] / kWg - kRg);
+            const float t = tanhf(wx * ox + wy * oy + bb);
+            const float dpre = d[i] * ww * (1.f - t * t);
             gx = fmaf(dpre, ox, gx);
             gy = fmaf(dpre, oy, gy);
             gb += dpre;
-            gw = fmaf(d, t, gw);
+            gw = fmaf(d[i], t, gw);
         }
         gx = warp_sum(gx);
         gy = warp_sum(gy);
         gb = warp_sum(gb);
         gw = warp_sum(gw);
         if (lane == 0) {
-            red[0][warp] = gx;
-            red[1][warp] = gy;
-            red[2][warp] = gb;
-            red[3][warp] = gw;
+            red[warp][u] = gx;
+            red[warp][hidden + u] = gy;
+            red[warp][2 * hidden + u] = gb;
+            red[warp][3 * hidden + u] = gw;
         }
-        __syncthreads();
-        if (threadIdx.x < 4) {
-            float s = 0.f;
-            for (int w = 0; w < nw; ++w) s += red[threadIdx.x][w];
-            float* dst = threadIdx.x == 0 ? dw1 + h * 2 * hidden + u
-                       : threadIdx.x == 1 ? dw1 + h * 2 * hidden + hidden + u
-                       : threadIdx.x == 2 ? db1 + h * hidden + u
-                                          : dw2 + h * hidden + u;
-            atomicAdd(dst, s);
-        }
-        __syncthreads();
+    }
+    __syncthreads();
+    const int nv = 4 * hidden + 1;
+    for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+        float s = 0.f;
+        for (int w = 0; w < 8; ++w) s += red[w][j];
+        fpart[(size_t(h) * gridDim.x + blockIdx.x) * nv + j] = s;
+    }
+}
+__global__ void bias_grad_final_kernel(const float* __restrict__ fpart, int nblk, int hidden, float* dw1,
+                                       float* db1, float* dw2, float* db2) {
+    const int h = blockIdx.x;
+    const int nv = 4 * hidden + 1;
+    for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+        float s = 0.f;
+        for (int b = 0; b < nblk; ++b) s += fpart[(size_t(h) * nblk + b) * nv + j];
+        const int u = j % hidden, which = j / hidden;
+        if (j == 4 * hidden) db2[h] += s;
+        else if (which == 0) dw1[h * 2 * hidden + u] += s;
+        else if (which == 1) dw1[h * 2 * hidden + hidden + u] += s;
+        else if (which == 2) db1[h * hidden + u] += s;
+        else dw2[h * hidden + u] += s;
     }
 }
 
@@ -476,6 +491,7 @@ struct AttnWs {
     float* part;
     float* mlp_grad;
     float* blank_grad;
+    float* fpart;
     size_t bytes;
 };
 
@@ -505,6 +521,8 @@ static AttnWs carve_ws(const affmae_cluster_geom* g, const affmae_attn_desc* a, 
             take(2 * size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [launch][h][CTA]
         w.mlp_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
         w.blank_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
+        w.fpart = reinterpret_cast<float*>(
+            take(size_t(a->heads) * ((kWg2 + kFinEPB - 1) / kFinEPB) * (4 * a->bias_hidden + 1) * 4));
     }
     w.bytes = off;
     return w;
@@ -683,10 +701,15 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
         dtab_replica_sum_kernel<<<(n + 255) / 256, 256, 0, st>>>(w.dtab_g, n);
         AFFMAE_LAUNCH_CHECK("dtab_replica_sum_kernel");
     }
-    bias_grad_finalize_kernel<<<dim3(16, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
-                                                                  a->bias_hidden, gr->dw1, gr->db1,
-                                                                  gr->dw2, gr->db2);
-    AFFMAE_LAUNCH_CHECK("bias_grad_finalize_kernel");
+    {
+        const int nblk = (kWg2 + kFinEPB - 1) / kFinEPB;
+        bias_grad_partial_kernel<<<dim3(nblk, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
+                                                                       a->bias_hidden, w.fpart);
+        AFFMAE_LAUNCH_CHECK("bias_grad_partial_kernel");
+        bias_grad_final_kernel<<<a->heads, 128, 0, st>>>(w.fpart, nblk, a->bias_hidden, gr->dw1, gr->db1,
+                                                        gr->dw2, gr->db2);
+        AFFMAE_LAUNCH_CHECK("bias_grad_final_kernel");
+    }
     attn_grad_epilogue_kernel<<<a->heads, 64, 0, st>>>(w.mlp_grad, w.blank_grad, a->heads,
                                                        a->bias_hidden, a->head_dim, gr->dw1,
                                                        gr->db1, gr->dw2, gr->db2, gr->dblank_k,

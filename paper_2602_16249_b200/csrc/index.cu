@@ -423,7 +423,7 @@ static int sfc_core(const float* coords, int64_t batch, int64_t n, IndexWs& w, u
     AFFMAE_LAUNCH_CHECK("axis_keys_kernel");
     uint64_t* k = w.keys[0];
     uint32_t* v = nullptr;
-    int rc = radix_sort(k, v, w.keys[1], nullptr, e, 32 + bits_for(batch * 2), w.hist, st);
+    int rc = segmented_sort(k, v, w.keys[1], nullptr, batch * 2, n, 32 + bits_for(batch * 2), w.hist, st);
     if (rc) return rc;
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.gaps, 0xFF, size_t(batch) * 2 * 8, st));
     gap_kernel<<<blocks(e), 256, 0, st>>>(k, batch * 2, n, w.gaps);
@@ -433,7 +433,7 @@ static int sfc_core(const float* coords, int64_t batch, int64_t n, IndexWs& w, u
     AFFMAE_LAUNCH_CHECK("hilbert_keys_kernel");
     k = w.keys[0];
     v = w.vals[0];
-    rc = radix_sort(k, v, w.keys[1], w.vals[1], batch * n, 32 + bits_for(batch), w.hist, st);
+    rc = segmented_sort(k, v, w.keys[1], w.vals[1], batch, n, 32 + bits_for(batch), w.hist, st);
     if (rc) return rc;
     *sorted_vals = v;
     return AFFMAE_OK;

@@ -67,6 +67,155 @@ __global__ void compact_kernel(const uint8_t* __restrict__ keep, int64_t n, int6
         if (k[i]) o[pos++] = int32_t(i);
 }
 
+// ------------------------------------------------- select_retained by radix select
+// One CTA per image (n <= kSegSortMax).  Keys w = ~float_order(score): the
+// retained set is the r smallest keys, ties -> lower index, i.e. the first r of
+// the stable ascending order (std::stable_sort by score desc,
+// proj/src/merging.cpp:56-69).  Four MSB-first 8-bit histogram passes find the
+// r-th key T and how many keys equal to T are taken; a stable compaction then
+// writes the selected indices in ascending order.
+constexpr int kSelWarps = 32;
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* wsum, uint32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t x = lane < kSelWarps ? wsum[lane] : 0u, xi = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, xi, d);
+            if (lane >= d) xi += y;
+        }
+        wsum[lane] = xi - x;
+        if (lane == 31) wsum[32] = xi;
+    }
+    __syncthreads();
+    const uint32_t r = wsum[warp] + inc - v;
+    total = wsum[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kSelWarps * 32) select_topk_kernel(const float* __restrict__ scores, int64_t n,
+                                                                     int64_t r, int32_t* __restrict__ out) {
+    extern __shared__ uint32_t sw[];  // n keys
+    __shared__ uint32_t hist[kSelWarps][257];
+    __shared__ uint32_t wsum[33];
+    __shared__ uint32_t bc[2];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int N = int(n);
+    const float* s = scores + int64_t(blockIdx.x) * n;
+    for (int i0 = t; i0 < N; i0 += 8 * kSelWarps * 32) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * kSelWarps * 32;
+            v[u] = i < N ? __ldg(s + i) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * kSelWarps * 32;
+            if (i < N) sw[i] = ~float_order(v[u]);
+        }
+    }
+    const int per = ((((N + 31) / 32) + kSelWarps - 1) / kSelWarps) * 32;
+    const int w0 = warp * per, w1 = min(w0 + per, N);
+    uint32_t prefix = 0, mask = 0, need = uint32_t(r);
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = t; i < kSelWarps * 257; i += blockDim.x) (&hist[0][0])[i] = 0;
+        __syncthreads();
+        for (int b = w0; b < w1; b += 32) {
+            const int i = b + lane;
+            int d = 256;
+            if (i < w1) {
+                const uint32_t w = sw[i];
+                if ((w & mask) == prefix) d = int((w >> shift) & 0xFF);
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (d < 256 && __popc(peers & lt) == 0) hist[warp][d] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        if (warp == 0) {  // digit where the cumulative count reaches `need`
+            uint32_t c[8], run = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                uint32_t x = 0;
+                for (int w = 0; w < kSelWarps; ++w) x += hist[w][lane * 8 + j];
+                c[j] = x;
+                run += x;
+            }
+            uint32_t inc = run;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += y;
+            }
+            const uint32_t before = inc - run;
+            const unsigned hit = __ballot_sync(0xffffffffu, inc >= need && before < need);
+            if (lane == __ffs(hit) - 1) {
+                uint32_t acc = before;
+                int dsel = 7;
+                for (int j = 0; j < 8; ++j) {
+                    if (acc + c[j] >= need) {
+                        dsel = j;
+                        break;
+                    }
+                    acc += c[j];
+                }
+                bc[0] = uint32_t(lane * 8 + dsel);
+                bc[1] = acc;
+            }
+        }
+        __syncthreads();
+        prefix |= bc[0] << shift;
+        mask |= 0xFFu << shift;
+        need -= bc[1];
+        __syncthreads();
+    }
+    // stable compaction: w < T, or w == T among the first `need` equal keys (index order)
+    const uint32_t T = prefix;
+    uint32_t eq = 0;
+    for (int b = w0; b < w1; b += 32) {
+        const int i = b + lane;
+        eq += __popc(__ballot_sync(0xffffffffu, i < w1 && sw[i] == T));
+    }
+    uint32_t tot;
+    uint32_t eq_before = block_excl_scan(lane == 0 ? eq : 0u, wsum, tot);
+    eq_before = __shfl_sync(0xffffffffu, eq_before, 0);
+    uint32_t sel = 0, eqr = eq_before;
+    for (int b = w0; b < w1; b += 32) {
+        const int i = b + lane;
+        const uint32_t w = i < w1 ? sw[i] : 0xffffffffu;
+        const unsigned be = __ballot_sync(0xffffffffu, i < w1 && w == T);
+        const bool take = i < w1 && (w < T || (w == T && eqr + __popc(be & lt) < need));
+        sel += __popc(__ballot_sync(0xffffffffu, take));
+        eqr += __popc(be);
+    }
+    uint32_t sel_before = block_excl_scan(lane == 0 ? sel : 0u, wsum, tot);
+    sel_before = __shfl_sync(0xffffffffu, sel_before, 0);
+    int32_t* o = out + int64_t(blockIdx.x) * r;
+    uint32_t pos = sel_before;
+    eqr = eq_before;
+    for (int b = w0; b < w1; b += 32) {
+        const int i = b + lane;
+        const uint32_t w = i < w1 ? sw[i] : 0xffffffffu;
+        const unsigned be = __ballot_sync(0xffffffffu, i < w1 && w == T);
+        const bool take = i < w1 && (w < T || (w == T && eqr + __popc(be & lt) < need));
+        const unsigned bt = __ballot_sync(0xffffffffu, take);
+        if (take) o[pos + __popc(bt & lt)] = i;
+        pos += __popc(bt);
+        eqr += __popc(be);
+    }
+}
+
 // --------------------------------------------------------------- merge_plan
 struct GridPrm {
     double x0, y0, w;  // origin and cell width
@@ -463,12 +612,20 @@ template <int KMAX>
 __device__ __forceinline__ int pool_row_weights(const int32_t* pool_idx, const double* pool_dist,
                                                 const int32_t* pool_cnt, int64_t row, int k_m, float p,
                                                 int (&jj)[KMAX], float (&w)[KMAX], float (&dd)[KMAX]) {
-    const int cnt = pool_cnt[row];
+    // all loads independent of cnt (the pool arrays hold k_m slots per row): one round trip
+    int ji[KMAX];
+    double di[KMAX];
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) {
+        ji[t] = t < k_m ? __ldg(pool_idx + row * k_m + t) : 0;
+        di[t] = t < k_m ? __ldg(pool_dist + row * k_m + t) : 0.0;
+    }
+    const int cnt = __ldg(pool_cnt + row);
     float m = -INFINITY;
 #pragma unroll
     for (int t = 0; t < KMAX; ++t) {
-        jj[t] = t < cnt ? pool_idx[row * k_m + t] : 0;
-        dd[t] = t < cnt ? float(pool_dist[row * k_m + t]) : 0.f;
+        jj[t] = t < cnt ? ji[t] : 0;
+        dd[t] = t < cnt ? float(di[t]) : 0.f;
         if (t < cnt) m = fmaxf(m, -p * dd[t]);
     }
     float l = 0.f;
@@ -716,10 +873,22 @@ int select_retained(const float* scores, int64_t batch, int64_t n, double d_s, i
     if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "select_retained: workspace too small");
     if (batch == 0) return AFFMAE_OK;
     cudaStream_t st = as_stream(stream);
+    if (n <= kSegSortMax) {
+        const size_t smem = size_t(n) * 4;
+        static bool attr = false;
+        if (!attr) {
+            AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(kSegSortMax * 4)));
+            attr = true;
+        }
+        select_topk_kernel<<<unsigned(batch), kSelWarps * 32, smem, st>>>(scores, n, r, retained);
+        AFFMAE_LAUNCH_CHECK("select_topk_kernel");
+        return AFFMAE_OK;
+    }
     score_keys_kernel<<<blocks_of(batch * n), 256, 0, st>>>(scores, batch, n, w.keys[0], w.vals[0]);
     uint64_t* k = w.keys[0];
     uint32_t* v = w.vals[0];
-    int rc = radix_sort(k, v, w.keys[1], w.vals[1], batch * n, 32 + bits_for(batch), w.hist, st);
+    int rc = segmented_sort(k, v, w.keys[1], w.vals[1], batch, n, 32 + bits_for(batch), w.hist, st);
     if (rc) return rc;
     keep_flags_kernel<<<blocks_of(batch * n), 256, 0, st>>>(v, batch, n, r, w.keep);
     compact_kernel<<<unsigned(batch), 1024, 0, st>>>(w.keep, n, r, retained);
