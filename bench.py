@@ -187,6 +187,7 @@ def run_ours(a, rank, world, dist):
     out_buf = torch.empty_like(q)
     lse_buf = torch.empty((B, N, h), dtype=torch.float32, device=dev)
     grads = ops.AttnGrads.zeros_like(q, bk, bias)
+    plan_buf = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 
     phases = ["index", "attn_fwd", "attn_bwd", "merge"]
 
@@ -196,12 +197,13 @@ def run_ours(a, rank, world, dist):
         idx = ops.cluster_index(coords, a.cluster, a.groups, workspace=ws)
         if ev:
             ev[1].record()
+        plan = ops.attn_plan(geom, coords, idx, h, d, a.hidden, buf=plan_buf)
         out, lse = ops.attn_fwd(geom, q, k, v, bk, bv, coords, idx.perm, idx.nbr_cl, bias, h, d,
-                                out=out_buf, lse=lse_buf, workspace=ws)
+                                out=out_buf, lse=lse_buf, workspace=ws, plan=plan)
         if ev:
             ev[2].record()
         ops.attn_bwd(geom, q, k, v, bk, bv, coords, idx, bias, h, d, out, lse, dout, grads=grads,
-                     workspace=ws)
+                     workspace=ws, plan=plan)
         if ev:
             ev[3].record()
         ret = ops.select_retained(scores, a.d_s)
@@ -360,6 +362,7 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
     dsmall = {n: torch.empty_like(t, device=dev) for n, t in small.items()}
     dhb = {n: torch.empty_like(t, device=dev) for n, t in hb.items()}
     p_merge = torch.ones(1, dtype=torch.float32, device=dev)
+    plan_buf = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 
     def e2e_step():
         ev_in, ev_cmp = [], []
@@ -382,10 +385,13 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
                 dv_ = dbuf[c]
                 g = cgeom[b1 - b0]
                 idx = ops.cluster_index(dv_["coords"], a.cluster, a.groups, workspace=ws)
+                plan = ops.attn_plan(g, dv_["coords"], idx, h, d, a.hidden, buf=plan_buf)
                 out, lse = ops.attn_fwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
-                                        dv_["coords"], idx.perm, idx.nbr_cl, bias, h, d, workspace=ws)
+                                        dv_["coords"], idx.perm, idx.nbr_cl, bias, h, d, workspace=ws,
+                                        plan=plan)
                 gr = ops.attn_bwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
-                                  dv_["coords"], idx, bias, h, d, out, lse, dv_["dout"], workspace=ws)
+                                  dv_["coords"], idx, bias, h, d, out, lse, dv_["dout"], workspace=ws,
+                                  plan=plan)
                 ret = ops.select_retained(dv_["scores"], a.d_s)
                 plan = ops.merge_plan(dv_["coords"], ret, a.k_m)
                 pooled = ops.merge_pool_fwd(out, dv_["scores"], p_merge, plan)

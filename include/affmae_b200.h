@@ -132,6 +132,30 @@ int affmae_attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
                     affmae_bf16* out, float* lse, void* workspace, size_t workspace_bytes,
                     void* stream);
 
+/* Attention plan: the geometry part of the op (query-cluster records, key /
+ * reverse-pair records, lattice classes), built once per cluster index and
+ * reused by every forward / backward on it -- the reference's AttnOp freezes
+ * coords + NeighborIndex at construction (src/attention.cpp:374-383).  The
+ * caller owns `buf` (device, affmae_attn_plan_workspace bytes); build fills
+ * the descriptor fields, the planned calls check them. */
+typedef struct affmae_attn_plan {
+    void* buf;
+    size_t bytes;
+    int64_t batch, tokens, n_clusters, groups_eff, width; /* filled by build */
+    double patch;
+    int has_reverse; /* built with the reverse CSR (required by the backward) */
+} affmae_attn_plan;
+
+size_t affmae_attn_plan_workspace(const affmae_cluster_geom* g, int with_reverse);
+int affmae_attn_plan_build(const affmae_cluster_geom* g, const affmae_attn_desc* a, const float* coords,
+                           const affmae_cluster_index* idx, int with_reverse, affmae_attn_plan* plan,
+                           void* stream);
+/* Per-call workspace of the planned entry points (BiasNet offset table, backward partials). */
+size_t affmae_attn_fwd_planned_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a);
+int affmae_attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                            const affmae_attn_inputs* in, const affmae_attn_plan* plan, affmae_bf16* out,
+                            float* lse, void* workspace, size_t workspace_bytes, void* stream);
+
 typedef struct affmae_attn_grads {
     affmae_bf16* dq;  /* [B, N, h*d]  overwritten */
     affmae_bf16* dk;  /* [B, N, h*d]  overwritten */
@@ -152,6 +176,13 @@ int affmae_attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
                     const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
                     affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
                     void* stream);
+
+size_t affmae_attn_bwd_planned_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a);
+int affmae_attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                            const affmae_attn_inputs* in, const affmae_attn_plan* plan,
+                            const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                            affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 /* ------------------------------------------------------------------------
  * Adaptive KNN merge (src/merging.cpp).

@@ -23,6 +23,8 @@ EXPORTS = (
     "affmae_cluster_index_workspace", "affmae_cluster_index_build", "affmae_neighbor_expand",
     "affmae_sfc_order_workspace", "affmae_sfc_order", "affmae_knn",
     "affmae_attn_fwd_workspace", "affmae_attn_fwd", "affmae_attn_bwd_workspace", "affmae_attn_bwd",
+    "affmae_attn_plan_workspace", "affmae_attn_plan_build", "affmae_attn_fwd_planned_workspace",
+    "affmae_attn_fwd_planned", "affmae_attn_bwd_planned_workspace", "affmae_attn_bwd_planned",
     "affmae_retained_count", "affmae_select_retained_workspace", "affmae_select_retained",
     "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
     "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd",
@@ -57,6 +59,12 @@ class AttnGrads(C.Structure):
                                           "dw2", "db2", "dblank")]
 
 
+class AttnPlan(C.Structure):
+    _fields_ = [("buf", C.c_void_p), ("bytes", C.c_size_t)] + \
+        [(n, C.c_int64) for n in ("batch", "tokens", "n_clusters", "groups_eff", "width")] + \
+        [("patch", C.c_double), ("has_reverse", C.c_int)]
+
+
 class MergePlan(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("target", "pool_idx", "pool_dist", "pool_cnt", "row_of")]
 
@@ -76,7 +84,8 @@ def lib():
         L.affmae_retained_count.restype = C.c_int64
         L.affmae_retained_count.argtypes = [C.c_int64, C.c_double]
         for f in ("affmae_cluster_index_workspace", "affmae_sfc_order_workspace",
-                  "affmae_attn_fwd_workspace",
+                  "affmae_attn_fwd_workspace", "affmae_attn_plan_workspace",
+                  "affmae_attn_fwd_planned_workspace", "affmae_attn_bwd_planned_workspace",
                   "affmae_attn_bwd_workspace", "affmae_select_retained_workspace",
                   "affmae_merge_plan_workspace", "affmae_merge_pool_bwd_workspace"):
             if hasattr(L, f):

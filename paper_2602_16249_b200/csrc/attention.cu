@@ -407,18 +407,18 @@ __global__ void bias_grad_partial_kernel(const float* __restrict__ dtab, const f
 }
 __global__ void bias_grad_final_kernel(const float* __restrict__ fpart, int nblk, int hidden, float* dw1,
                                        float* db1, float* dw2, float* db2) {
-    const int h = blockIdx.x;
+    const int h = blockIdx.x, j = blockIdx.y;  // one warp per (head, parameter)
     const int nv = 4 * hidden + 1;
-    for (int j = threadIdx.x; j < nv; j += blockDim.x) {
-        float s = 0.f;
-        for (int b = 0; b < nblk; ++b) s += fpart[(size_t(h) * nblk + b) * nv + j];
-        const int u = j % hidden, which = j / hidden;
-        if (j == 4 * hidden) db2[h] += s;
-        else if (which == 0) dw1[h * 2 * hidden + u] += s;
-        else if (which == 1) dw1[h * 2 * hidden + hidden + u] += s;
-        else if (which == 2) db1[h * hidden + u] += s;
-        else dw2[h * hidden + u] += s;
-    }
+    float s = 0.f;
+    for (int b = threadIdx.x; b < nblk; b += 32) s += fpart[(size_t(h) * nblk + b) * nv + j];
+    s = warp_sum(s);
+    if (threadIdx.x != 0) return;
+    const int u = j % hidden, which = j / hidden;
+    if (j == 4 * hidden) db2[h] += s;
+    else if (which == 0) dw1[h * 2 * hidden + u] += s;
+    else if (which == 1) dw1[h * 2 * hidden + hidden + u] += s;
+    else if (which == 2) db1[h * hidden + u] += s;
+    else dw2[h * hidden + u] += s;
 }
 
 // tier-3 partials and blank grads -> caller's gradient buffers (+=)
@@ -478,53 +478,76 @@ static int attn_check(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Plan buffer (geometry only, reusable by every forward/backward on the same
+// cluster index -- the reference's AttnOp freezes coords + NeighborIndex at
+// construction, proj/src/attention.cpp:374-383): query-cluster records |
+// item lists | [key records | pair records].  Its host descriptor
+// (affmae_attn_plan) records what it was built for.
 struct AttnWs {
-    float* tab_g;
     int32_t* qrec;
     int32_t* items;
     int32_t* item_count;
     int32_t* item_blk;
     int32_t* krec;
     int32_t* prec;
+    float* tab_g;
     float* dtab_g;
     float* dsum;
     float* part;
     float* mlp_grad;
     float* blank_grad;
     float* fpart;
-    size_t bytes;
+    size_t plan_bytes, run_bytes;
 };
 
-static AttnWs carve_ws(const affmae_cluster_geom* g, const affmae_attn_desc* a, void* base, bool bwd) {
-    AttnWs w{};
-    uint8_t* p = static_cast<uint8_t*>(base);
+struct Carver {
+    uint8_t* p;
     size_t off = 0;
-    auto take = [&](size_t bytes) {
+    uint8_t* take(size_t bytes) {
         uint8_t* r = p ? p + off : nullptr;
         off += align256(bytes);
         return r;
-    };
+    }
+};
+
+static void carve_plan(const affmae_cluster_geom* g, void* base, bool rev, AttnWs& w) {
+    Carver c{static_cast<uint8_t*>(base)};
     const size_t items = size_t(g->batch) * g->n_clusters;
     const int kp = pick_kp(g->width);
     const size_t qwords = size_t(32 + 2 * kp + 8);
-    w.tab_g = reinterpret_cast<float*>(take(size_t(a->heads) * kWg2 * 4));
-    w.qrec = reinterpret_cast<int32_t*>(take(items * qwords * 4));
-    w.items = reinterpret_cast<int32_t*>(take(2 * items * 4));
-    w.item_count = reinterpret_cast<int32_t*>(take(2 * 4));
-    w.item_blk = reinterpret_cast<int32_t*>(take(2 * ((items + 1023) / 1024) * 4));
-    if (bwd) {
-        w.krec = reinterpret_cast<int32_t*>(take(items * KRec::WORDS * 4));
-        w.prec = reinterpret_cast<int32_t*>(take(items * g->groups_eff * PRec::WORDS * 4));
-        w.dtab_g = reinterpret_cast<float*>(take(size_t(kTabReplicas) * a->heads * kWg2 * 4));
-        w.dsum = reinterpret_cast<float*>(take(size_t(g->batch) * g->tokens * a->heads * 4));
-        w.part = reinterpret_cast<float*>(
-            take(2 * size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [launch][h][CTA]
-        w.mlp_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
-        w.blank_grad = reinterpret_cast<float*>(take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
-        w.fpart = reinterpret_cast<float*>(
-            take(size_t(a->heads) * ((kWg2 + kFinEPB - 1) / kFinEPB) * (4 * a->bias_hidden + 1) * 4));
+    w.qrec = reinterpret_cast<int32_t*>(c.take(items * qwords * 4));
+    w.items = reinterpret_cast<int32_t*>(c.take(2 * items * 4));
+    w.item_count = reinterpret_cast<int32_t*>(c.take(2 * 4));
+    w.item_blk = reinterpret_cast<int32_t*>(c.take(2 * ((items + 1023) / 1024) * 4));
+    if (rev) {
+        w.krec = reinterpret_cast<int32_t*>(c.take(items * KRec::WORDS * 4));
+        w.prec = reinterpret_cast<int32_t*>(c.take(items * g->groups_eff * PRec::WORDS * 4));
     }
-    w.bytes = off;
+    w.plan_bytes = c.off;
+}
+
+static void carve_run(const affmae_cluster_geom* g, const affmae_attn_desc* a, void* base, bool bwd,
+                      AttnWs& w) {
+    Carver c{static_cast<uint8_t*>(base)};
+    w.tab_g = reinterpret_cast<float*>(c.take(size_t(a->heads) * kWg2 * 4));
+    if (bwd) {
+        w.dtab_g = reinterpret_cast<float*>(c.take(size_t(kTabReplicas) * a->heads * kWg2 * 4));
+        w.dsum = reinterpret_cast<float*>(c.take(size_t(g->batch) * g->tokens * a->heads * 4));
+        w.part = reinterpret_cast<float*>(
+            c.take(2 * size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [launch][h][CTA]
+        w.mlp_grad = reinterpret_cast<float*>(c.take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
+        w.blank_grad = reinterpret_cast<float*>(c.take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
+        w.fpart = reinterpret_cast<float*>(
+            c.take(size_t(a->heads) * ((kWg2 + kFinEPB - 1) / kFinEPB) * (4 * a->bias_hidden + 1) * 4));
+    }
+    w.run_bytes = c.off;
+}
+
+// one-shot workspace = plan | run state
+static AttnWs carve_ws(const affmae_cluster_geom* g, const affmae_attn_desc* a, void* base, bool bwd) {
+    AttnWs w{};
+    carve_plan(g, base, bwd, w);
+    carve_run(g, a, base ? static_cast<uint8_t*>(base) + w.plan_bytes : nullptr, bwd, w);
     return w;
 }
 
@@ -562,19 +585,18 @@ static int check_inputs(const affmae_attn_inputs* in) {
     return AFFMAE_OK;
 }
 
-// bias table + query-cluster records (+ key/pair records for the backward)
-static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const int32_t* nbr_cl,
-                   const int32_t* rev_off, const int32_t* rev_cl, int64_t width, cudaStream_t st) {
-    const int n = p.heads * kWg2;
-    bias_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.heads, p.hidden, w.tab_g);
-    AFFMAE_LAUNCH_CHECK("bias_table_kernel");
-    const int64_t items = int64_t(p.batch) * p.cs.c;
+// Geometry plan: query-cluster records, item lists (+ key / pair records).
+static int build_plan(const affmae_cluster_geom* g, float inv_patch, const float* coords, const int32_t* perm,
+                      const int32_t* nbr_cl, const int32_t* rev_off, const int32_t* rev_cl, const AttnWs& w,
+                      cudaStream_t st) {
+    const ClusterShape cs = make_shape(*g);
+    const int64_t items = g->batch * g->n_clusters;
     const unsigned blocks = unsigned((items + 3) / 4);
-    switch (pick_kp(width)) {
-#define AFFMAE_QREC(KP_)                                                                          \
-    case KP_:                                                                                     \
-        attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(p.coords, perm, nbr_cl, p.cs, items,        \
-                                                      p.inv_patch, w.qrec);                       \
+    const int kp = pick_kp(g->width);
+    switch (kp) {
+#define AFFMAE_QREC(KP_)                                                                                 \
+    case KP_:                                                                                            \
+        attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(coords, perm, nbr_cl, cs, items, inv_patch, w.qrec); \
         break;
         AFFMAE_QREC(16)
         AFFMAE_QREC(32)
@@ -586,7 +608,7 @@ static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const in
     }
     AFFMAE_LAUNCH_CHECK("attn_qrec_kernel");
     {
-        const int words = 32 + 2 * pick_kp(width) + 8, hf = 32 + 2 * pick_kp(width) + kHFast;
+        const int words = 32 + 2 * kp + 8, hf = 32 + 2 * kp + kHFast;
         const unsigned nb = unsigned((items + 1023) / 1024);
         attn_item_count_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk);
         AFFMAE_LAUNCH_CHECK("attn_item_count_kernel");
@@ -595,10 +617,18 @@ static int prepare(AttnParams& p, const AttnWs& w, const int32_t* perm, const in
         AFFMAE_LAUNCH_CHECK("attn_item_scatter_kernel");
     }
     if (rev_cl) {
-        attn_krec_kernel<<<blocks, 128, 0, st>>>(p.coords, perm, rev_off, rev_cl, p.cs, items,
-                                                 p.inv_patch, w.krec, w.prec);
+        attn_krec_kernel<<<blocks, 128, 0, st>>>(coords, perm, rev_off, rev_cl, cs, items, inv_patch, w.krec,
+                                                 w.prec);
         AFFMAE_LAUNCH_CHECK("attn_krec_kernel");
     }
+    return AFFMAE_OK;
+}
+
+// per-call state: BiasNet offset table of the current weights; wires the plan in
+static int prepare_run(AttnParams& p, const AttnWs& w, cudaStream_t st) {
+    const int n = p.heads * kWg2;
+    bias_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.heads, p.hidden, w.tab_g);
+    AFFMAE_LAUNCH_CHECK("bias_table_kernel");
     p.tab_g = w.tab_g;
     p.qrec = w.qrec;
     p.items = w.items;
@@ -636,47 +666,74 @@ static int dispatch_bwd(const AttnParams& p, int head_dim, int64_t width, cudaSt
 
 size_t attn_fwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
     if (attn_check(g, a)) return 0;
-    return carve_ws(g, a, nullptr, false).bytes;
+    const AttnWs w = carve_ws(g, a, nullptr, false);
+    return w.plan_bytes + w.run_bytes;
 }
 
 size_t attn_bwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
     if (attn_check(g, a)) return 0;
-    return carve_ws(g, a, nullptr, true).bytes;
+    const AttnWs w = carve_ws(g, a, nullptr, true);
+    return w.plan_bytes + w.run_bytes;
 }
 
-int attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
-             const int32_t* perm, const int32_t* nbr_cl, affmae_bf16* out, float* lse,
-             void* workspace, size_t ws_bytes, void* stream) {
+size_t attn_plan_workspace(const affmae_cluster_geom* g, int with_reverse) {
+    if (!g || g->n_clusters <= 0 || pick_kp(g->width) < 0) return 0;
+    AttnWs w{};
+    carve_plan(g, nullptr, with_reverse != 0, w);
+    return w.plan_bytes;
+}
+size_t attn_fwd_planned_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
+    if (attn_check(g, a)) return 0;
+    AttnWs w{};
+    carve_run(g, a, nullptr, false, w);
+    return w.run_bytes;
+}
+size_t attn_bwd_planned_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
+    if (attn_check(g, a)) return 0;
+    AttnWs w{};
+    carve_run(g, a, nullptr, true, w);
+    return w.run_bytes;
+}
+
+int attn_plan_build(const affmae_cluster_geom* g, const affmae_attn_desc* a, const float* coords,
+                    const affmae_cluster_index* idx, int with_reverse, affmae_attn_plan* plan, void* stream) {
     int rc = attn_check(g, a);
     if (rc) return rc;
-    if ((rc = check_inputs(in))) return rc;
-    if (!perm || !nbr_cl || !out || !lse) return fail(AFFMAE_ECONFIG, "attn_fwd: null pointer");
-    AttnWs w = carve_ws(g, a, workspace, false);
-    if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "attn_fwd: workspace too small");
+    if (!coords || !idx || !idx->perm || !idx->nbr_cl || !plan || !plan->buf)
+        return fail(AFFMAE_ECONFIG, "attn_plan_build: null pointer");
+    if (with_reverse && (!idx->rev_off || !idx->rev_cl))
+        return fail(AFFMAE_ECONFIG, "attn_plan_build: reverse CSR required for a backward plan");
+    AttnWs w{};
+    carve_plan(g, plan->buf, with_reverse != 0, w);
+    if (plan->bytes < w.plan_bytes) return fail(AFFMAE_ECONFIG, "attn_plan_build: plan buffer too small");
+    plan->batch = g->batch;
+    plan->tokens = g->tokens;
+    plan->n_clusters = g->n_clusters;
+    plan->groups_eff = g->groups_eff;
+    plan->width = g->width;
+    plan->patch = a->patch;
+    plan->has_reverse = with_reverse != 0;
     if (g->batch == 0) return AFFMAE_OK;
+    return build_plan(g, float(1.0 / a->patch), coords, idx->perm, idx->nbr_cl,
+                      with_reverse ? idx->rev_off : nullptr, with_reverse ? idx->rev_cl : nullptr, w,
+                      as_stream(stream));
+}
+
+static int run_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
+                   const AttnWs& w, affmae_bf16* out, float* lse, cudaStream_t st) {
     AttnParams p;
     fill_common(p, g, a, in);
     p.out = reinterpret_cast<__nv_bfloat16*>(out);
     p.lse = lse;
-    cudaStream_t st = as_stream(stream);
-    if ((rc = prepare(p, w, perm, nbr_cl, nullptr, nullptr, g->width, st))) return rc;
+    int rc = prepare_run(p, w, st);
+    if (rc) return rc;
     return dispatch_fwd(p, a->head_dim, g->width, st);
 }
 
-int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
-             const affmae_cluster_index* idx, const affmae_bf16* out, const float* lse,
-             const affmae_bf16* dout, affmae_attn_grads* gr, void* workspace, size_t ws_bytes,
-             void* stream) {
-    int rc = attn_check(g, a);
-    if (rc) return rc;
-    if ((rc = check_inputs(in))) return rc;
-    if (!idx || !idx->perm || !idx->nbr_cl || !idx->rev_off || !idx->rev_cl || !out || !lse ||
-        !dout || !gr || !gr->dq || !gr->dk || !gr->dv || !gr->dblank_k || !gr->dblank_v ||
-        !gr->dw1 || !gr->db1 || !gr->dw2 || !gr->db2 || !gr->dblank)
-        return fail(AFFMAE_ECONFIG, "attn_bwd: null pointer");
-    AttnWs w = carve_ws(g, a, workspace, true);
-    if (!workspace || ws_bytes < w.bytes) return fail(AFFMAE_ECONFIG, "attn_bwd: workspace too small");
-    if (g->batch == 0) return AFFMAE_OK;
+static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
+                   const AttnWs& w, const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                   affmae_attn_grads* gr, cudaStream_t st) {
+    (void)out;
     AttnParams p;
     fill_common(p, g, a, in);
     p.lse = const_cast<float*>(lse);
@@ -687,8 +744,8 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
     p.dsum = w.dsum;
     p.dtab_g = w.dtab_g;
     p.part = w.part;
-    cudaStream_t st = as_stream(stream);
-    if ((rc = prepare(p, w, idx->perm, idx->nbr_cl, idx->rev_off, idx->rev_cl, g->width, st))) return rc;
+    int rc = prepare_run(p, w, st);
+    if (rc) return rc;
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.dtab_g, 0, size_t(kTabReplicas) * a->heads * kWg2 * 4, st));
     int gx[2] = {0, 0};
     if ((rc = dispatch_bwd(p, a->head_dim, g->width, st, gx))) return rc;
@@ -706,8 +763,8 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
         bias_grad_partial_kernel<<<dim3(nblk, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
                                                                        a->bias_hidden, w.fpart);
         AFFMAE_LAUNCH_CHECK("bias_grad_partial_kernel");
-        bias_grad_final_kernel<<<a->heads, 128, 0, st>>>(w.fpart, nblk, a->bias_hidden, gr->dw1, gr->db1,
-                                                        gr->dw2, gr->db2);
+        bias_grad_final_kernel<<<dim3(a->heads, 4 * a->bias_hidden + 1), 32, 0, st>>>(
+            w.fpart, nblk, a->bias_hidden, gr->dw1, gr->db1, gr->dw2, gr->db2);
         AFFMAE_LAUNCH_CHECK("bias_grad_final_kernel");
     }
     attn_grad_epilogue_kernel<<<a->heads, 64, 0, st>>>(w.mlp_grad, w.blank_grad, a->heads,
@@ -716,6 +773,96 @@ int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affm
                                                        gr->dblank_v, gr->dblank);
     AFFMAE_LAUNCH_CHECK("attn_grad_epilogue_kernel");
     return AFFMAE_OK;
+}
+
+static int check_bwd_ptrs(const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                          const affmae_attn_grads* gr) {
+    if (!out || !lse || !dout || !gr || !gr->dq || !gr->dk || !gr->dv || !gr->dblank_k || !gr->dblank_v ||
+        !gr->dw1 || !gr->db1 || !gr->dw2 || !gr->db2 || !gr->dblank)
+        return fail(AFFMAE_ECONFIG, "attn_bwd: null pointer");
+    return AFFMAE_OK;
+}
+
+// A plan must have been built for this geometry / patch (and with the reverse CSR for a backward).
+static int check_plan(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_plan* plan,
+                      bool bwd, AttnWs& w) {
+    if (!plan || !plan->buf) return fail(AFFMAE_ECONFIG, "attention: null plan");
+    if (plan->batch != g->batch || plan->tokens != g->tokens || plan->n_clusters != g->n_clusters ||
+        plan->groups_eff != g->groups_eff || plan->width != g->width || plan->patch != a->patch)
+        return fail(AFFMAE_ECONFIG, "attention: plan was built for another geometry / patch");
+    if (bwd && !plan->has_reverse)
+        return fail(AFFMAE_ECONFIG, "attention: backward needs a plan built with the reverse CSR");
+    carve_plan(g, plan->buf, plan->has_reverse != 0, w);
+    return AFFMAE_OK;
+}
+
+int attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
+                     const affmae_attn_plan* plan, affmae_bf16* out, float* lse, void* workspace, size_t ws_bytes,
+                     void* stream) {
+    int rc = attn_check(g, a);
+    if (rc) return rc;
+    if ((rc = check_inputs(in))) return rc;
+    if (!out || !lse) return fail(AFFMAE_ECONFIG, "attn_fwd: null pointer");
+    cudaStream_t st = as_stream(stream);
+    AttnWs w{};
+    if ((rc = check_plan(g, a, plan, false, w))) return rc;
+    carve_run(g, a, workspace, false, w);
+    if (!workspace || ws_bytes < w.run_bytes) return fail(AFFMAE_ECONFIG, "attn_fwd: workspace too small");
+    if (g->batch == 0) return AFFMAE_OK;
+    return run_fwd(g, a, in, w, out, lse, st);
+}
+
+int attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
+                     const affmae_attn_plan* plan, const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                     affmae_attn_grads* gr, void* workspace, size_t ws_bytes, void* stream) {
+    int rc = attn_check(g, a);
+    if (rc) return rc;
+    if ((rc = check_inputs(in))) return rc;
+    if ((rc = check_bwd_ptrs(out, lse, dout, gr))) return rc;
+    cudaStream_t st = as_stream(stream);
+    AttnWs w{};
+    if ((rc = check_plan(g, a, plan, true, w))) return rc;
+    carve_run(g, a, workspace, true, w);
+    if (!workspace || ws_bytes < w.run_bytes) return fail(AFFMAE_ECONFIG, "attn_bwd: workspace too small");
+    if (g->batch == 0) return AFFMAE_OK;
+    return run_bwd(g, a, in, w, out, lse, dout, gr, st);
+}
+
+int attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
+             const int32_t* perm, const int32_t* nbr_cl, affmae_bf16* out, float* lse,
+             void* workspace, size_t ws_bytes, void* stream) {
+    int rc = attn_check(g, a);
+    if (rc) return rc;
+    if ((rc = check_inputs(in))) return rc;
+    if (!perm || !nbr_cl || !out || !lse) return fail(AFFMAE_ECONFIG, "attn_fwd: null pointer");
+    AttnWs w = carve_ws(g, a, workspace, false);
+    if (!workspace || ws_bytes < w.plan_bytes + w.run_bytes)
+        return fail(AFFMAE_ECONFIG, "attn_fwd: workspace too small");
+    if (g->batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    if ((rc = build_plan(g, float(1.0 / a->patch), in->coords, perm, nbr_cl, nullptr, nullptr, w, st))) return rc;
+    return run_fwd(g, a, in, w, out, lse, st);
+}
+
+int attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
+             const affmae_cluster_index* idx, const affmae_bf16* out, const float* lse,
+             const affmae_bf16* dout, affmae_attn_grads* gr, void* workspace, size_t ws_bytes,
+             void* stream) {
+    int rc = attn_check(g, a);
+    if (rc) return rc;
+    if ((rc = check_inputs(in))) return rc;
+    if (!idx || !idx->perm || !idx->nbr_cl || !idx->rev_off || !idx->rev_cl)
+        return fail(AFFMAE_ECONFIG, "attn_bwd: null pointer");
+    if ((rc = check_bwd_ptrs(out, lse, dout, gr))) return rc;
+    AttnWs w = carve_ws(g, a, workspace, true);
+    if (!workspace || ws_bytes < w.plan_bytes + w.run_bytes)
+        return fail(AFFMAE_ECONFIG, "attn_bwd: workspace too small");
+    if (g->batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    if ((rc = build_plan(g, float(1.0 / a->patch), in->coords, idx->perm, idx->nbr_cl, idx->rev_off, idx->rev_cl,
+                         w, st)))
+        return rc;
+    return run_bwd(g, a, in, w, out, lse, dout, gr, st);
 }
 
 }  // namespace affmae_b200

@@ -31,6 +31,16 @@ int attn_fwd(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_a
 int attn_bwd(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
              const affmae_cluster_index*, const affmae_bf16*, const float*, const affmae_bf16*,
              affmae_attn_grads*, void*, size_t, void*);
+size_t attn_plan_workspace(const affmae_cluster_geom*, int);
+int attn_plan_build(const affmae_cluster_geom*, const affmae_attn_desc*, const float*,
+                    const affmae_cluster_index*, int, affmae_attn_plan*, void*);
+size_t attn_fwd_planned_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
+size_t attn_bwd_planned_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
+int attn_fwd_planned(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
+                     const affmae_attn_plan*, affmae_bf16*, float*, void*, size_t, void*);
+int attn_bwd_planned(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
+                     const affmae_attn_plan*, const affmae_bf16*, const float*, const affmae_bf16*,
+                     affmae_attn_grads*, void*, size_t, void*);
 size_t cluster_index_workspace(const affmae_cluster_geom*);
 int cluster_index_build(const affmae_cluster_geom*, const float*, affmae_cluster_index*, void*,
                         size_t, void*);
@@ -100,6 +110,33 @@ int affmae_attn_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
                     affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
                     void* stream) {
     return attn_bwd(g, a, in, idx, out, lse, dout, grads, workspace, workspace_bytes, stream);
+}
+
+size_t affmae_attn_plan_workspace(const affmae_cluster_geom* g, int with_reverse) {
+    return attn_plan_workspace(g, with_reverse);
+}
+int affmae_attn_plan_build(const affmae_cluster_geom* g, const affmae_attn_desc* a, const float* coords,
+                           const affmae_cluster_index* idx, int with_reverse, affmae_attn_plan* plan,
+                           void* stream) {
+    return attn_plan_build(g, a, coords, idx, with_reverse, plan, stream);
+}
+size_t affmae_attn_fwd_planned_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
+    return attn_fwd_planned_workspace(g, a);
+}
+int affmae_attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                            const affmae_attn_inputs* in, const affmae_attn_plan* plan, affmae_bf16* out,
+                            float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+    return attn_fwd_planned(g, a, in, plan, out, lse, workspace, workspace_bytes, stream);
+}
+size_t affmae_attn_bwd_planned_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
+    return attn_bwd_planned_workspace(g, a);
+}
+int affmae_attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a,
+                            const affmae_attn_inputs* in, const affmae_attn_plan* plan,
+                            const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
+                            affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+    return attn_bwd_planned(g, a, in, plan, out, lse, dout, grads, workspace, workspace_bytes, stream);
 }
 
 size_t affmae_cluster_index_workspace(const affmae_cluster_geom* g) { return cluster_index_workspace(g); }

@@ -98,19 +98,57 @@ def _workspace(nbytes, device):
     return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
+@dataclass
+class AttnPlan:
+    """Geometry plan of the attention op (affmae_attn_plan): built once per cluster index,
+    reused by forward and backward (the reference's AttnOp freezes coords + NeighborIndex at
+    construction, proj/src/attention.cpp:374-383)."""
+    c: capi.AttnPlan
+    buf: torch.Tensor
+
+
+def attn_plan(geom, coords, index: ClusterIndex, heads, head_dim, hidden, patch=8.0,
+              with_reverse=True, buf=None, stream=None) -> AttnPlan:
+    _req(coords, torch.float32, "coords")
+    L = capi.lib()
+    desc = capi.AttnDesc(heads, head_dim, hidden, float(patch))
+    nbytes = L.affmae_attn_plan_workspace(C.byref(geom), C.c_int(int(with_reverse)))
+    if buf is None or buf.numel() < nbytes:
+        buf = _workspace(nbytes, coords.device)
+    pl = capi.AttnPlan()
+    pl.buf = C.c_void_p(buf.data_ptr())
+    pl.bytes = C.c_size_t(buf.numel())
+    idx = index.c_struct()
+    capi.check(L.affmae_attn_plan_build(C.byref(geom), C.byref(desc), C.c_void_p(coords.data_ptr()),
+                                        C.byref(idx), C.c_int(int(with_reverse)), C.byref(pl),
+                                        _stream(stream)), "attn_plan_build")
+    return AttnPlan(pl, buf)
+
+
 def attn_fwd(geom, q, k, v, blank_k, blank_v, coords, perm, nbr_cl, bias: BiasNet, heads,
-             head_dim, out=None, lse=None, workspace=None, stream=None):
+             head_dim, out=None, lse=None, workspace=None, stream=None, plan: AttnPlan | None = None):
     """Cluster attention forward (nbhd_attn_streaming, proj/src/attention.cpp:199).
-    q/k/v [B, N, h*d] bf16 -> (out [B, N, h*d] bf16, lse [B, N, h] fp32)."""
+    q/k/v [B, N, h*d] bf16 -> (out [B, N, h*d] bf16, lse [B, N, h] fp32).  With `plan`
+    the geometry records come from the plan (perm / nbr_cl are then not read)."""
     desc, ins = _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim)
-    _req(perm, torch.int32, "perm")
-    _req(nbr_cl, torch.int32, "nbr_cl")
     B, N = geom.batch, geom.tokens
     if out is None:
         out = torch.empty((B, N, heads * head_dim), dtype=BF16, device=q.device)
     if lse is None:
         lse = torch.empty((B, N, heads), dtype=torch.float32, device=q.device)
     L = capi.lib()
+    if plan is not None:
+        nbytes = L.affmae_attn_fwd_planned_workspace(C.byref(geom), C.byref(desc))
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = _workspace(nbytes, q.device)
+        capi.check(L.affmae_attn_fwd_planned(C.byref(geom), C.byref(desc), C.byref(ins), C.byref(plan.c),
+                                             C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),
+                                             C.c_void_p(workspace.data_ptr()),
+                                             C.c_size_t(workspace.numel()), _stream(stream)),
+                   "attn_fwd_planned")
+        return out, lse
+    _req(perm, torch.int32, "perm")
+    _req(nbr_cl, torch.int32, "nbr_cl")
     nbytes = L.affmae_attn_fwd_workspace(C.byref(geom), C.byref(desc))
     if workspace is None or workspace.numel() < nbytes:
         workspace = _workspace(nbytes, q.device)
@@ -148,7 +186,7 @@ class AttnGrads:
 
 def attn_bwd(geom, q, k, v, blank_k, blank_v, coords, index: ClusterIndex, bias: BiasNet, heads,
              head_dim, out, lse, dout, grads: AttnGrads | None = None, workspace=None,
-             stream=None):
+             stream=None, plan: AttnPlan | None = None):
     """Cluster attention backward (nbhd_attn_backward, proj/src/attention.cpp:241-358).
     dq/dk/dv are overwritten; BiasNet and blank gradients accumulate (+=), like
     CustomOp::backward (proj/include/affmae/tape.hpp:29-31)."""
@@ -159,11 +197,22 @@ def attn_bwd(geom, q, k, v, blank_k, blank_v, coords, index: ClusterIndex, bias:
     if grads is None:
         grads = AttnGrads.zeros_like(q, blank_k, bias)
     L = capi.lib()
+    g = capi.AttnGrads(*(capi.ptr(getattr(grads, n)) for n in (
+        "dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")))
+    if plan is not None:
+        nbytes = L.affmae_attn_bwd_planned_workspace(C.byref(geom), C.byref(desc))
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = _workspace(nbytes, q.device)
+        capi.check(L.affmae_attn_bwd_planned(C.byref(geom), C.byref(desc), C.byref(ins), C.byref(plan.c),
+                                             C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),
+                                             C.c_void_p(dout.data_ptr()), C.byref(g),
+                                             C.c_void_p(workspace.data_ptr()),
+                                             C.c_size_t(workspace.numel()), _stream(stream)),
+                   "attn_bwd_planned")
+        return grads
     nbytes = L.affmae_attn_bwd_workspace(C.byref(geom), C.byref(desc))
     if workspace is None or workspace.numel() < nbytes:
         workspace = _workspace(nbytes, q.device)
-    g = capi.AttnGrads(*(capi.ptr(getattr(grads, n)) for n in (
-        "dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")))
     idx = index.c_struct()
     capi.check(L.affmae_attn_bwd(C.byref(geom), C.byref(desc), C.byref(ins), C.byref(idx),
                                  C.c_void_p(out.data_ptr()), C.c_void_p(lse.data_ptr()),

@@ -174,3 +174,63 @@ def test_attn_bwd_matches_oracle(case):
         report[n] = rel_l2(g, w)
     bad = {n: e for n, e in report.items() if e > REL_TOL}
     assert not bad, f"rel-L2 over {REL_TOL}: {bad} (all: {report})"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [CASES[0], CASES[3]], ids=[CASES[0][0], CASES[3][0]])
+def test_attn_planned_equals_oneshot(case):
+    """The plan API (built once per cluster index, like the reference AttnOp freezing its
+    geometry) gives bit-identical outputs and gradients to the one-shot calls."""
+    torch = _torch()
+    from paper_2602_16249_b200 import ops
+    name, mk, heads, hd, hidden, cluster, groups = case
+    rng = np.random.default_rng(zlib.crc32(name.encode()) + 1)
+    pb = attn_problem(mk(rng), heads, hd, hidden, rng)
+    coords = pb["coords"]
+    B, N, _ = coords.shape
+    geom = ops.geometry(B, N, cluster, groups)
+    perm, cof, nbr, roff, rcl = (_dev(a, torch.int32) for a in _host_index(coords, cluster, groups))
+    index = ops.ClusterIndex(geom, perm, cof, nbr, roff, rcl)
+    bf = torch.bfloat16
+    q, k, v, bk, bv = (_dev(pb[n], bf) for n in ("q", "k", "v", "bk", "bv"))
+    c = _dev(coords, torch.float32)
+    do = _dev(pb["dout"], bf)
+    bias = ops.BiasNet.from_numpy(pb["bias"])
+    o1, l1 = ops.attn_fwd(geom, q, k, v, bk, bv, c, perm, nbr, bias, heads, hd)
+    g1 = ops.attn_bwd(geom, q, k, v, bk, bv, c, index, bias, heads, hd, o1, l1, do)
+    plan = ops.attn_plan(geom, c, index, heads, hd, hidden)
+    o2, l2 = ops.attn_fwd(geom, q, k, v, bk, bv, c, None, None, bias, heads, hd, plan=plan)
+    g2 = ops.attn_bwd(geom, q, k, v, bk, bv, c, index, bias, heads, hd, o2, l2, do, plan=plan)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    for n in ("dq", "dk", "dv", "dblank_k", "dblank_v", "dblank"):
+        assert torch.equal(getattr(g1, n), getattr(g2, n)), n
+    # BiasNet parameter gradients: far same-phase pairs (beyond the shared window)
+    # accumulate through global atomics, so only the summation order may differ
+    for n in ("dw1", "db1", "dw2", "db2"):
+        assert torch.allclose(getattr(g1, n), getattr(g2, n), rtol=1e-5, atol=1e-5), n
+
+
+@pytest.mark.gpu
+def test_attn_plan_mismatch_raises():
+    torch = _torch()
+    from paper_2602_16249_b200 import ops
+    rng = np.random.default_rng(3)
+    pb = attn_problem(lattice_coords(1, 32), 2, 32, 8, rng)
+    coords = pb["coords"]
+    B, N, _ = coords.shape
+    geom = ops.geometry(B, N, 16, 3)
+    perm, cof, nbr, roff, rcl = (_dev(a, torch.int32) for a in _host_index(coords, 16, 3))
+    index = ops.ClusterIndex(geom, perm, cof, nbr, roff, rcl)
+    c = _dev(coords, torch.float32)
+    fwd_only = ops.attn_plan(geom, c, index, 2, 32, 8, with_reverse=False)
+    bf = torch.bfloat16
+    q = _dev(pb["q"], bf)
+    bias = ops.BiasNet.from_numpy(pb["bias"])
+    bk = _dev(pb["bk"], bf)
+    o, l = ops.attn_fwd(geom, q, q, q, bk, bk, c, None, None, bias, 2, 32, plan=fwd_only)
+    with pytest.raises(ValueError):  # backward needs the reverse CSR
+        ops.attn_bwd(geom, q, q, q, bk, bk, c, index, bias, 2, 32, o, l, q, plan=fwd_only)
+    other = ops.geometry(B, N, 8, 3)
+    with pytest.raises(ValueError):  # plan built for another geometry
+        ops.attn_fwd(other, q, q, q, bk, bk, c, None, None, bias, 2, 32, plan=fwd_only)
