@@ -242,6 +242,93 @@ __global__ void nbr_kernel(const double2* __restrict__ cent, int64_t batch, Clus
     }
 }
 
+// v2: one CTA per (image, block of clusters).  The image's centroids are
+// staged in shared memory; each warp keeps a lane-local top-G in registers
+// (branch-free insertion network, compile-time G) and merges with warp_topk.
+// Same (d^2, j) order and own-first selection as nbr_kernel.
+template <int G>
+__device__ __forceinline__ void topk_push(double (&d)[G], int (&j)[G], double nd, int nj) {
+#pragma unroll
+    for (int p = 0; p < G; ++p) {
+        if (pair_lt(nd, nj, d[p], j[p])) {
+            const double td = d[p];
+            const int tj = j[p];
+            d[p] = nd;
+            j[p] = nj;
+            nd = td;
+            nj = tj;
+        }
+    }
+}
+constexpr int kNbrWarps = 8, kNbrPerWarp = 4;
+template <int G>
+__global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* __restrict__ cent, ClusterShape cs,
+                                                                 int32_t* __restrict__ nbr_cl) {
+    extern __shared__ double2 sc[];
+    const int b = blockIdx.y;
+    const double2* cb = cent + int64_t(b) * cs.c;
+    for (int i = threadIdx.x; i < cs.c; i += blockDim.x) sc[i] = cb[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k0 = (blockIdx.x * kNbrWarps + warp) * kNbrPerWarp;
+    for (int k = k0; k < min(k0 + kNbrPerWarp, cs.c); ++k) {
+        const double2 ck = sc[k];
+        double d[G];
+        int jj[G];
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            d[r] = INFINITY;
+            jj[r] = INT32_MAX;
+        }
+        for (int j = lane; j < cs.c; j += 32) {
+            const double2 cj = sc[j];
+            const double dx = __dsub_rn(cj.x, ck.x), dy = __dsub_rn(cj.y, ck.y);
+            const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+            if (pair_lt(d2, j, d[G - 1], jj[G - 1])) topk_push<G>(d, jj, d2, j);
+        }
+        double od[G];
+        int oj[G];
+        warp_topk<G>(d, jj, G, od, oj);
+        if (lane == 0) {
+            int32_t* sel = nbr_cl + (int64_t(b) * cs.c + k) * G;
+            int ns = 0;
+            sel[ns++] = k;
+#pragma unroll
+            for (int r = 0; r < G; ++r)
+                if (ns < G && oj[r] != k) sel[ns++] = oj[r];
+        }
+    }
+}
+
+static int launch_nbr(const double2* cent, int64_t batch, const ClusterShape& cs, int32_t* nbr, cudaStream_t st) {
+    const size_t smem = size_t(cs.c) * sizeof(double2);
+    if (smem > 200 * 1024) return -1;  // very large images: the generic kernel
+    const dim3 grid(unsigned((cs.c + kNbrWarps * kNbrPerWarp - 1) / (kNbrWarps * kNbrPerWarp)), unsigned(batch));
+    switch (cs.g) {
+#define AFFMAE_NBR(G_)                                                                                       \
+    case G_: {                                                                                               \
+        if (smem > 48 * 1024)                                                                                \
+            AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(nbr_v2_kernel<G_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                   int(smem)));                                              \
+        nbr_v2_kernel<G_><<<grid, kNbrWarps * 32, smem, st>>>(cent, cs, nbr);                                \
+        break;                                                                                               \
+    }
+        AFFMAE_NBR(1)
+        AFFMAE_NBR(2)
+        AFFMAE_NBR(3)
+        AFFMAE_NBR(4)
+        AFFMAE_NBR(5)
+        AFFMAE_NBR(6)
+        AFFMAE_NBR(7)
+        AFFMAE_NBR(8)
+#undef AFFMAE_NBR
+        default:
+            return -1;
+    }
+    AFFMAE_LAUNCH_CHECK("nbr_v2_kernel");
+    return AFFMAE_OK;
+}
+
 // reverse-neighbour CSR: in-degree, per-image scan, fill, per-list sort
 __global__ void indeg_kernel(const int32_t* __restrict__ nbr_cl, int64_t batch, ClusterShape cs,
                              int32_t* __restrict__ cnt) {
@@ -463,7 +550,11 @@ int cluster_index_build(const affmae_cluster_geom* g, const float* coords, affma
     if (rc) return rc;
     perm_kernel<<<blocks(B * n), 256, 0, st>>>(sv, B, cs, out->perm, out->cluster_of);
     centroid_kernel<<<blocks(B * cs.c), 256, 0, st>>>(coords, out->perm, B, cs, w.cent);
-    nbr_kernel<<<blocks(B * cs.c * 32), 256, 0, st>>>(w.cent, B, cs, out->nbr_cl);
+    {
+        const int rc = launch_nbr(w.cent, B, cs, out->nbr_cl, st);
+        if (rc > 0) return rc;
+        if (rc < 0) nbr_kernel<<<blocks(B * cs.c * 32), 256, 0, st>>>(w.cent, B, cs, out->nbr_cl);
+    }
     AFFMAE_LAUNCH_CHECK("nbr_kernel");
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(out->rev_off, 0, size_t(B) * (cs.c + 1) * 4, st));
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.cursor, 0, size_t(B) * (cs.c + 1) * 4, st));
