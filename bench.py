@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--d-s", type=float, default=0.4)
     ap.add_argument("--k-m", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="image chunks pipelined H2D|compute|D2H")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="image chunks pipelined H2D|compute|D2H")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
@@ -364,6 +364,46 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
     p_merge = torch.ones(1, dtype=torch.float32, device=dev)
     plan_buf = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
 
+    bias = ops.BiasNet(**dhb)
+    outs_d = [None] * nch
+
+    def chunk_compute(c):
+        """The op chain of one chunk (device buffers in, device results out)."""
+        b0, b1 = bounds[c]
+        dv_ = dbuf[c]
+        g = cgeom[b1 - b0]
+        idx = ops.cluster_index(dv_["coords"], a.cluster, a.groups, workspace=ws)
+        plan = ops.attn_plan(g, dv_["coords"], idx, h, d, a.hidden, buf=plan_buf)
+        out, lse = ops.attn_fwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
+                                dv_["coords"], idx.perm, idx.nbr_cl, bias, h, d, workspace=ws, plan=plan)
+        gr = ops.attn_bwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
+                          dv_["coords"], idx, bias, h, d, out, lse, dv_["dout"], workspace=ws, plan=plan)
+        ret = ops.select_retained(dv_["scores"], a.d_s)
+        mplan = ops.merge_plan(dv_["coords"], ret, a.k_m)
+        pooled = ops.merge_pool_fwd(out, dv_["scores"], p_merge, mplan)
+        dfe, dsc, _ = ops.merge_pool_bwd(out, dv_["scores"], p_merge, mplan, dv_["dpooled"])
+        outs_d[c] = dict(out=out, lse=lse, dq=gr.dq, dk=gr.dk, dv=gr.dv, pooled=pooled, dfeats=dfe,
+                         dscores=dsc)
+
+    # one CUDA graph per chunk (static shapes and buffers): the per-chunk launch cost is a
+    # single graph launch, so the chunks can be short and the PCIe fill / drain small
+    graphs = [None] * nch
+    if not a.no_graph:
+        try:
+            with torch.cuda.stream(s_cmp):
+                for c in range(nch):
+                    chunk_compute(c)  # warm-up (allocator, lazy attributes)
+            torch.cuda.synchronize()
+            for c in range(nch):
+                gph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gph, stream=s_cmp):
+                    chunk_compute(c)
+                graphs[c] = gph
+            torch.cuda.synchronize()
+        except Exception as e:  # pragma: no cover - capture is best effort
+            print(f"[bench] e2e graph capture failed ({e}); eager chunks", file=sys.stderr)
+            graphs = [None] * nch
+
     def e2e_step():
         ev_in, ev_cmp = [], []
         with torch.cuda.stream(s_in):
@@ -378,34 +418,20 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
                 e = torch.cuda.Event()
                 e.record(s_in)
                 ev_in.append(e)
-        bias = ops.BiasNet(**dhb)
         for c, (b0, b1) in enumerate(bounds):
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ev_in[c])
-                dv_ = dbuf[c]
-                g = cgeom[b1 - b0]
-                idx = ops.cluster_index(dv_["coords"], a.cluster, a.groups, workspace=ws)
-                plan = ops.attn_plan(g, dv_["coords"], idx, h, d, a.hidden, buf=plan_buf)
-                out, lse = ops.attn_fwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
-                                        dv_["coords"], idx.perm, idx.nbr_cl, bias, h, d, workspace=ws,
-                                        plan=plan)
-                gr = ops.attn_bwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
-                                  dv_["coords"], idx, bias, h, d, out, lse, dv_["dout"], workspace=ws,
-                                  plan=plan)
-                ret = ops.select_retained(dv_["scores"], a.d_s)
-                plan = ops.merge_plan(dv_["coords"], ret, a.k_m)
-                pooled = ops.merge_pool_fwd(out, dv_["scores"], p_merge, plan)
-                dfe, dsc, _ = ops.merge_pool_bwd(out, dv_["scores"], p_merge, plan, dv_["dpooled"])
-                res = dict(out=out, lse=lse, dq=gr.dq, dk=gr.dk, dv=gr.dv, pooled=pooled, dfeats=dfe,
-                           dscores=dsc)
+                if graphs[c] is not None:
+                    graphs[c].replay()
+                else:
+                    chunk_compute(c)
                 e = torch.cuda.Event()
                 e.record(s_cmp)
                 ev_cmp.append(e)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cmp[c])
-                for name, t in res.items():
+                for name, t in outs_d[c].items():
                     outs_h[name][b0:b1].copy_(t, non_blocking=True)
-                    t.record_stream(s_out)
         torch.cuda.current_stream(dev).wait_stream(s_out)
 
     e2e_step()
@@ -419,8 +445,31 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
     e1.record()
     torch.cuda.synchronize()
     ms = pdist.max_over_ranks(e0.elapsed_time(e1) / a.e2e_steps, dist, dev)
+    # PCIe floor of the step: the same byte counts copied H2D and D2H concurrently (pinned)
+    hi = torch.empty(int(h2d), dtype=torch.uint8).pin_memory()
+    ho = torch.empty(int(d2h), dtype=torch.uint8).pin_memory()
+    di = torch.empty(int(h2d), dtype=torch.uint8, device=dev)
+    do = torch.empty(int(d2h), dtype=torch.uint8, device=dev)
+    floor = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        s_in.wait_stream(torch.cuda.current_stream(dev))
+        s_out.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s_in):
+            di.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            ho.copy_(do, non_blocking=True)
+        torch.cuda.current_stream(dev).wait_stream(s_in)
+        torch.cuda.current_stream(dev).wait_stream(s_out)
+        f1.record()
+        torch.cuda.synchronize()
+        floor.append(f0.elapsed_time(f1))
+    del hi, ho, di, do
     return {"value": B * N * world / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "chunks": nch}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "chunks": nch,
+            "pcie_floor_ms": min(floor), "pcie_floor_frac": min(floor) / ms}
 
 
 # ------------------------------------------------------------- reference
