@@ -9,23 +9,43 @@
 
 namespace affmae_b200 {
 
+constexpr int kFinBlocks = 64;  // blocks per head of the BiasNet-gradient finalize pass
+
 // ------------------------------------------------------------ bias table
 // T[h][(oy+kRg)*kWg + (ox+kRg)] = b2 + sum_u w2 tanh(w1x ox + w1y oy + b1)
 // (BiasNet::eval at integer patch offsets, proj/src/attention.cpp:33-42).
+// Only the box |offset| <= R of the table is ever read, R = max(plan radius,
+// window radius): the plan records the largest pair offset of its items.
+__device__ __forceinline__ int used_radius(const int32_t* rmax) {
+    const int r = *rmax;
+    return r < kRs ? kRs : (r > kRg ? kRg : r);
+}
 __global__ void bias_table_kernel(const float* __restrict__ w1, const float* __restrict__ b1,
                                   const float* __restrict__ w2, const float* __restrict__ b2,
-                                  int heads, int hidden, float* __restrict__ tab) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= heads * kWg2) return;
-    int h = i / kWg2, e = i - h * kWg2;
-    float ox = float(e % kWg - kRg), oy = float(e / kWg - kRg);
-    float acc = b2[h];
-    for (int u = 0; u < hidden; ++u) {
-        float pre = w1[h * 2 * hidden + u] * ox + w1[h * 2 * hidden + hidden + u] * oy +
-                    b1[h * hidden + u];
-        acc += w2[h * hidden + u] * tanhf(pre);
+                                  int heads, int hidden, const int32_t* __restrict__ rmax,
+                                  float* __restrict__ tab) {
+    const int R = used_radius(rmax), side = 2 * R + 1, box = side * side;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < heads * box; i += gridDim.x * blockDim.x) {
+        const int h = i / box, e = i - h * box;
+        const int oy = e / side - R, ox = e - (e / side) * side - R;
+        float acc = b2[h];
+        for (int u = 0; u < hidden; ++u) {
+            const float pre = w1[h * 2 * hidden + u] * float(ox) + w1[h * 2 * hidden + hidden + u] * float(oy) +
+                              b1[h * hidden + u];
+            acc += w2[h * hidden + u] * tanhf(pre);
+        }
+        tab[size_t(h) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] = acc;
     }
-    tab[i] = acc;
+}
+// zero the used box of every replica of the table gradient
+__global__ void dtab_zero_kernel(float* __restrict__ dtab, int heads, const int32_t* __restrict__ rmax) {
+    const int R = used_radius(rmax), side = 2 * R + 1, box = side * side;
+    const int n = kTabReplicas * heads * box;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int rh = i / box, e = i - rh * box;
+        const int oy = e / side - R, ox = e - (e / side) * side - R;
+        dtab[size_t(rh) * kWg2 + (oy + kRg) * kWg + (ox + kRg)] = 0.f;
+    }
 }
 
 // -------------------------------------------------------------- plan records
@@ -81,11 +101,18 @@ struct TokAgg {
     bool far = false;  // a token outside the packed-cell range
     // 1: lattice-fast (one phase, offsets inside the shared window); 2: medium
     // (one phase, offsets inside the global table); 0: general.
-    __device__ int cls() const {
+    __device__ int cls(int* radius) const {
         Bbox q{__reduce_min_sync(0xffffffffu, qx0), __reduce_max_sync(0xffffffffu, qx1),
                __reduce_min_sync(0xffffffffu, qy0), __reduce_max_sync(0xffffffffu, qy1)};
         Bbox k{__reduce_min_sync(0xffffffffu, kx0), __reduce_max_sync(0xffffffffu, kx1),
                __reduce_min_sync(0xffffffffu, ky0), __reduce_max_sync(0xffffffffu, ky1)};
+        {   // largest |key - query| offset along either axis
+            int64_t rr = int64_t(k.xmax) - q.xmin;
+            rr = max(rr, int64_t(q.xmax) - k.xmin);
+            rr = max(rr, int64_t(k.ymax) - q.ymin);
+            rr = max(rr, int64_t(q.ymax) - k.ymin);
+            *radius = int(min(max(rr, int64_t(0)), int64_t(kRg)));
+        }
         const bool ph = __reduce_min_sync(0xffffffffu, fx0) == __reduce_max_sync(0xffffffffu, fx1) &&
                         __reduce_min_sync(0xffffffffu, fy0) == __reduce_max_sync(0xffffffffu, fy1);
         const bool anyfar = __any_sync(0xffffffffu, far);
@@ -102,7 +129,7 @@ struct TokAgg {
 template <int KP>
 __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ nbr_cl, ClusterShape cs, int64_t items,
-                                 float inv_patch, int32_t* __restrict__ qrec) {
+                                 float inv_patch, int32_t* __restrict__ qrec, int32_t* __restrict__ rmax) {
     using R = QRec<KP>;
     constexpr int E = 16 + KP, J = (E + 31) / 32;
     __shared__ int cellbuf[4][E];
@@ -149,7 +176,9 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
             pcellbuf[warp][e] = pcell;
         }
     }
-    const int cls = agg.cls();
+    int radius = 0;
+    const int cls = agg.cls(&radius);
+    if (lane == 0) atomicMax(rmax, cls == 0 ? kRg : radius);
     __syncwarp();
     const int(*cb)[E] = cls == 2 ? pcellbuf : cellbuf;
 #pragma unroll
@@ -338,53 +367,59 @@ __global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx0,
 
 // dL/dtheta = sum over table entries of dT * dT/dtheta, accumulated (+=)
 // into the caller's gradients.
-// Sums the kTabReplicas copies of the table gradient into copy 0 (fixed order).
-__global__ void dtab_replica_sum_kernel(float* __restrict__ dtab, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float s = dtab[i];
-    for (int r = 1; r < kTabReplicas; ++r) s += dtab[size_t(r) * n + i];
-    dtab[i] = s;
+// Sums the kTabReplicas copies of the table gradient into copy 0 (fixed order), used box only.
+__global__ void dtab_replica_sum_kernel(float* __restrict__ dtab, int heads, const int32_t* __restrict__ rmax) {
+    const int R = used_radius(rmax), side = 2 * R + 1, box = side * side;
+    const size_t n = size_t(heads) * kWg2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < heads * box; i += gridDim.x * blockDim.x) {
+        const int h = i / box, e = i - h * box;
+        const int oy = e / side - R, ox = e - (e / side) * side - R;
+        const size_t j = size_t(h) * kWg2 + (oy + kRg) * kWg + (ox + kRg);
+        float v = dtab[j];
+        for (int r = 1; r < kTabReplicas; ++r) v += dtab[r * n + j];
+        dtab[j] = v;
+    }
 }
 
-// dL/dtheta = sum over table entries of dT * dT/dtheta.  Pass 1: each block
-// folds kFinEPB entries into per-block partials {dw1x[H], dw1y[H], db1[H],
-// dw2[H], db2}; pass 2 sums the block partials in a fixed order and adds
-// them (+=) into the caller's gradients (deterministic).
-constexpr int kFinEPB = 1024;
+// dL/dtheta = sum over table entries of dT * dT/dtheta.  Pass 1: block b of head h
+// folds the used-box entries b, b + nblk*256, ... into per-block partials
+// {dw1x[H], dw1y[H], db1[H], dw2[H], db2}; pass 2 sums the block partials in a
+// fixed order and adds them (+=) into the caller's gradients (deterministic).
 __global__ void bias_grad_partial_kernel(const float* __restrict__ dtab, const float* __restrict__ w1,
                                          const float* __restrict__ b1, const float* __restrict__ w2, int hidden,
-                                         float* __restrict__ fpart) {
+                                         const int32_t* __restrict__ rmax, float* __restrict__ fpart) {
     const int h = blockIdx.y;
     const float* dt = dtab + size_t(h) * kWg2;
+    const int R = used_radius(rmax), side = 2 * R + 1, box = side * side;
     __shared__ float red[8][4 * kMaxHidden + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float d[kFinEPB / 256];
-    int e[kFinEPB / 256];
-#pragma unroll
-    for (int i = 0; i < kFinEPB / 256; ++i) {
-        e[i] = blockIdx.x * kFinEPB + i * 256 + threadIdx.x;
-        d[i] = e[i] < kWg2 ? dt[e[i]] : 0.f;
+    const int stride = gridDim.x * blockDim.x, e0 = blockIdx.x * blockDim.x + threadIdx.x;
+    auto entry = [&](int e, float& ox, float& oy) -> float {
+        const int oyi = e / side, oxi = e - oyi * side;
+        ox = float(oxi - R);
+        oy = float(oyi - R);
+        return dt[(oyi - R + kRg) * kWg + (oxi - R + kRg)];
+    };
+    {
+        float sd = 0.f, ox, oy;
+        for (int e = e0; e < box; e += stride) sd += entry(e, ox, oy);
+        sd = warp_sum(sd);
+        if (lane == 0) red[warp][4 * hidden] = sd;
     }
-    float sd = 0.f;
-#pragma unroll
-    for (int i = 0; i < kFinEPB / 256; ++i) sd += d[i];
-    sd = warp_sum(sd);
-    if (lane == 0) red[warp][4 * hidden] = sd;
     for (int u = 0; u < hidden; ++u) {
         const float wx = w1[h * 2 * hidden + u], wy = w1[h * 2 * hidden + hidden + u];
         const float bb = b1[h * hidden + u], ww = w2[h * hidden + u];
         float gx = 0.f, gy = 0.f, gb = 0.f, gw = 0.f;
-#pragma unroll
-        for (int i = 0; i < kFinEPB / 256; ++i) {
-            if (d[i] == 0.f) continue;
-            const float ox = float(e[i] % kWg - kRg), oy = float(e[i] / kWg - kRg);
+        for (int e = e0; e < box; e += stride) {
+            float ox, oy;
+            const float d = entry(e, ox, oy);
+            if (d == 0.f) continue;
             const float t = tanhf(wx * ox + wy * oy + bb);
-            const float dpre = d[i] * ww * (1.f - t * t);
+            const float dpre = d * ww * (1.f - t * t);
             gx = fmaf(dpre, ox, gx);
             gy = fmaf(dpre, oy, gy);
             gb += dpre;
-            gw = fmaf(d[i], t, gw);
+            gw = fmaf(d, t, gw);
         }
         gx = warp_sum(gx);
         gy = warp_sum(gy);
@@ -488,6 +523,7 @@ struct AttnWs {
     int32_t* items;
     int32_t* item_count;
     int32_t* item_blk;
+    int32_t* rmax;  // largest pair offset radius of the plan's items (bounds the BiasNet table box)
     int32_t* krec;
     int32_t* prec;
     float* tab_g;
@@ -519,6 +555,7 @@ static void carve_plan(const affmae_cluster_geom* g, void* base, bool rev, AttnW
     w.items = reinterpret_cast<int32_t*>(c.take(2 * items * 4));
     w.item_count = reinterpret_cast<int32_t*>(c.take(2 * 4));
     w.item_blk = reinterpret_cast<int32_t*>(c.take(2 * ((items + 1023) / 1024) * 4));
+    w.rmax = reinterpret_cast<int32_t*>(c.take(16));
     if (rev) {
         w.krec = reinterpret_cast<int32_t*>(c.take(items * KRec::WORDS * 4));
         w.prec = reinterpret_cast<int32_t*>(c.take(items * g->groups_eff * PRec::WORDS * 4));
@@ -538,7 +575,7 @@ static void carve_run(const affmae_cluster_geom* g, const affmae_attn_desc* a, v
         w.mlp_grad = reinterpret_cast<float*>(c.take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
         w.blank_grad = reinterpret_cast<float*>(c.take(size_t(a->heads) * (2 * a->head_dim + 1) * 4));
         w.fpart = reinterpret_cast<float*>(
-            c.take(size_t(a->heads) * ((kWg2 + kFinEPB - 1) / kFinEPB) * (4 * a->bias_hidden + 1) * 4));
+            c.take(size_t(a->heads) * kFinBlocks * (4 * a->bias_hidden + 1) * 4));
     }
     w.run_bytes = c.off;
 }
@@ -593,10 +630,12 @@ static int build_plan(const affmae_cluster_geom* g, float inv_patch, const float
     const int64_t items = g->batch * g->n_clusters;
     const unsigned blocks = unsigned((items + 3) / 4);
     const int kp = pick_kp(g->width);
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.rmax, 0, 16, st));
     switch (kp) {
 #define AFFMAE_QREC(KP_)                                                                                 \
     case KP_:                                                                                            \
-        attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(coords, perm, nbr_cl, cs, items, inv_patch, w.qrec); \
+        attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(coords, perm, nbr_cl, cs, items, inv_patch, w.qrec, \
+                                                      w.rmax);                                           \
         break;
         AFFMAE_QREC(16)
         AFFMAE_QREC(32)
@@ -627,7 +666,8 @@ static int build_plan(const affmae_cluster_geom* g, float inv_patch, const float
 // per-call state: BiasNet offset table of the current weights; wires the plan in
 static int prepare_run(AttnParams& p, const AttnWs& w, cudaStream_t st) {
     const int n = p.heads * kWg2;
-    bias_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.heads, p.hidden, w.tab_g);
+    (void)n;
+    bias_table_kernel<<<4 * kNumSMs, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.heads, p.hidden, w.rmax, w.tab_g);
     AFFMAE_LAUNCH_CHECK("bias_table_kernel");
     p.tab_g = w.tab_g;
     p.qrec = w.qrec;
@@ -746,7 +786,8 @@ static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, cons
     p.part = w.part;
     int rc = prepare_run(p, w, st);
     if (rc) return rc;
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.dtab_g, 0, size_t(kTabReplicas) * a->heads * kWg2 * 4, st));
+    dtab_zero_kernel<<<4 * kNumSMs, 256, 0, st>>>(w.dtab_g, a->heads, w.rmax);
+    AFFMAE_LAUNCH_CHECK("dtab_zero_kernel");
     int gx[2] = {0, 0};
     if ((rc = dispatch_bwd(p, a->head_dim, g->width, st, gx))) return rc;
     const int pw = part_width(a->head_dim);
@@ -754,14 +795,13 @@ static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, cons
         w.part, gx[0], gx[1], a->heads, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
     AFFMAE_LAUNCH_CHECK("attn_part_reduce_kernel");
     {
-        const int n = a->heads * kWg2;
-        dtab_replica_sum_kernel<<<(n + 255) / 256, 256, 0, st>>>(w.dtab_g, n);
+        dtab_replica_sum_kernel<<<2 * kNumSMs, 256, 0, st>>>(w.dtab_g, a->heads, w.rmax);
         AFFMAE_LAUNCH_CHECK("dtab_replica_sum_kernel");
     }
     {
-        const int nblk = (kWg2 + kFinEPB - 1) / kFinEPB;
+        const int nblk = kFinBlocks;
         bias_grad_partial_kernel<<<dim3(nblk, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
-                                                                       a->bias_hidden, w.fpart);
+                                                                       a->bias_hidden, w.rmax, w.fpart);
         AFFMAE_LAUNCH_CHECK("bias_grad_partial_kernel");
         bias_grad_final_kernel<<<dim3(a->heads, 4 * a->bias_hidden + 1), 32, 0, st>>>(
             w.fpart, nblk, a->bias_hidden, gr->dw1, gr->db1, gr->dw2, gr->db2);
