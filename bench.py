@@ -41,7 +41,7 @@ UNIT = "tokens/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
@@ -75,53 +75,81 @@ def workload_config(a, world):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML polled from a
+    thread every 5 ms (the timed region of a default run is tens of ms), nvidia-smi as the
+    fallback."""
+
+    REASONS = {  # NVML clocks-event-reason bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown",
+    }
 
     def __init__(self, gpu_index=0):
         self.gpu = gpu_index
-        self.samples = []
-        self._proc = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons set)
+        self._stop = threading.Event()
         self._thr = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        except Exception:
+            self._nvml = None
 
-    def start(self):
+    def _poll_nvml(self):
+        nv = self._nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                try:
+                    bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                except AttributeError:
+                    bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                rs = {n for b, n in self.REASONS.items() if bits & b}
+                self.samples.append((float(sm), float(mx), rs))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
+    def _poll_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
-        try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self._proc = None
-            return
-        self._thr = threading.Thread(target=self._read, daemon=True)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout
+                parts = [x.strip() for x in out.strip().split(",")]
+                if len(parts) >= 6 and parts[0].replace(".", "").isdigit():
+                    rs = {names[i - 2] for i in range(2, 6) if parts[i].lower() == "active"}
+                    self.samples.append((float(parts[0]), float(parts[1]), rs))
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._thr = threading.Thread(target=self._poll_nvml if self._nvml else self._poll_smi, daemon=True)
         self._thr.start()
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 6:
-                self.samples.append(parts)
-
     def stop(self):
-        if self._proc is not None:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
         if self._thr is not None:
-            self._thr.join(timeout=2)
+            self._thr.join(timeout=10)
 
     def summary(self):
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        reasons = sorted({names[i - 2] for s in self.samples for i in range(2, 6)
-                          if s[i].lower() == "active"})
+        sm = [x[0] for x in self.samples]
+        mx = [x[1] for x in self.samples]
+        reasons = sorted(set().union(*[x[2] for x in self.samples])) if self.samples else []
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi",
+                "window": "timed region + 0.25 s of the same step" if getattr(self, "extended", False)
+                          else "timed region"}
 
 
 # --------------------------------------------------------------- workload
@@ -265,12 +293,11 @@ def run_ours(a, rank, world, dist):
         run_step()
     torch.cuda.synchronize()
     clocks = ClockSampler(dev.index)
-    clocks.start()
-    time.sleep(0.3)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
     e0.record()
     for _ in range(a.steps):
         run_step()
@@ -280,6 +307,19 @@ def run_ours(a, rank, world, dist):
         dist.barrier()
     ms = e0.elapsed_time(e1) / a.steps
     clocks.stop()
+    if len(clocks.samples) < 3:
+        # timed region shorter than the sampler can resolve: keep the same step running
+        # (untimed) for ~0.25 s under the sampler so the clock record reflects this load
+        ext = ClockSampler(dev.index)
+        ext.start()
+        t_end = time.perf_counter() + 0.25
+        while time.perf_counter() < t_end:
+            for _ in range(10):
+                run_step()
+            torch.cuda.synchronize()
+        ext.stop()
+        clocks.samples += ext.samples
+        clocks.extended = True
     ms_max = pdist.max_over_ranks(ms, dist, dev)
     tokens_all = B * N * world
     value = tokens_all / (ms_max * 1e-3)
