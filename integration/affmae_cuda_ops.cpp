@@ -160,33 +160,70 @@ NeighborIndex knn(const Tensor& queries, const PointSet& keys, int64_t k) {
 namespace {
 
 // Tape op: inputs {q, k, v, blank_k, blank_v, w1, b1, w2, b2, blank}
-// (src/attention.cpp:374-444 ordering)
+// (src/attention.cpp:374-444 ordering).  Like the reference's AttnOp, the op's
+// geometry is frozen: the device coordinates, the cluster index and the
+// attention plan (affmae_attn_plan_build) are built once, on first use, and
+// reused by every forward and backward of the op.
 struct ClusterAttnOp final : CustomOp {
     Tensor coords;
     int64_t cluster, groups;
     int heads, head_dim, hidden;
     double patch;
 
+    struct Geometry {
+        std::unique_ptr<Dev> coords;
+        DeviceIndex d;
+        std::unique_ptr<Dev> plan_buf;
+        affmae_attn_plan plan{};
+    };
+    std::shared_ptr<Geometry> geo;
+
     std::string name() const override { return "cluster_attention_b200"; }
 
     affmae_attn_desc desc() const { return {heads, head_dim, hidden, patch}; }
 
+    Geometry& geometry(int64_t n) {
+        if (!geo) {
+            auto g = std::make_shared<Geometry>();
+            g->coords = upload(f32(coords));
+            g->d = build_index(*g->coords, n, cluster, groups);
+            affmae_attn_desc a = desc();
+            g->plan_buf = std::make_unique<Dev>(affmae_attn_plan_workspace(&g->d.g, 1));
+            g->plan.buf = g->plan_buf->p;
+            g->plan.bytes = g->plan_buf->n;
+            check(affmae_attn_plan_build(&g->d.g, &a, g->coords->as<float>(), &g->d.idx, 1, &g->plan, nullptr),
+                  "attn_plan_build");
+            geo = g;
+        }
+        return *geo;
+    }
+
+    // uploads the 10 inputs; `t` owns the device copies
+    affmae_attn_inputs inputs(const std::vector<const Tensor*>& in, Geometry& G, std::unique_ptr<Dev> (&t)[10]) {
+        for (int i = 0; i < 5; ++i) t[i] = upload(bf16(*in[size_t(i)]));
+        for (int i = 5; i < 10; ++i) t[i] = upload(f32(*in[size_t(i)]));
+        return {t[0]->as<affmae_bf16>(), t[1]->as<affmae_bf16>(), t[2]->as<affmae_bf16>(),
+                t[3]->as<affmae_bf16>(), t[4]->as<affmae_bf16>(), G.coords->as<float>(),
+                t[5]->as<float>(), t[6]->as<float>(), t[7]->as<float>(), t[8]->as<float>(),
+                t[9]->as<float>()};
+    }
+
+    void run_forward(Geometry& G, const affmae_attn_inputs& ai, Dev& out, Dev& lse) {
+        affmae_attn_desc a = desc();
+        Dev ws(affmae_attn_fwd_planned_workspace(&G.d.g, &a));
+        check(affmae_attn_fwd_planned(&G.d.g, &a, &ai, &G.plan, out.as<affmae_bf16>(), lse.as<float>(), ws.p, ws.n,
+                                      nullptr),
+              "attn_fwd");
+    }
+
     Tensor forward(const std::vector<const Tensor*>& in) override {
         if (in.size() != 10) throw ConfigError("attention op: want 10 inputs");
         const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
-        auto dc = upload(f32(coords));
-        DeviceIndex d = build_index(*dc, n, cluster, groups);
+        Geometry& G = geometry(n);
         std::unique_ptr<Dev> t[10];
-        for (int i = 0; i < 5; ++i) t[i] = upload(bf16(*in[size_t(i)]));
-        for (int i = 5; i < 10; ++i) t[i] = upload(f32(*in[size_t(i)]));
-        affmae_attn_inputs ai{t[0]->as<affmae_bf16>(), t[1]->as<affmae_bf16>(), t[2]->as<affmae_bf16>(),
-                              t[3]->as<affmae_bf16>(), t[4]->as<affmae_bf16>(), dc->as<float>(),
-                              t[5]->as<float>(), t[6]->as<float>(), t[7]->as<float>(), t[8]->as<float>(),
-                              t[9]->as<float>()};
-        affmae_attn_desc a = desc();
-        Dev out(n * hd * 2), lse(n * heads * 4), ws(affmae_attn_fwd_workspace(&d.g, &a));
-        check(affmae_attn_fwd(&d.g, &a, &ai, d.perm->as<int32_t>(), d.nbr->as<int32_t>(),
-                              out.as<affmae_bf16>(), lse.as<float>(), ws.p, ws.n, nullptr), "attn_fwd");
+        affmae_attn_inputs ai = inputs(in, G, t);
+        Dev out(n * hd * 2), lse(n * heads * 4);
+        run_forward(G, ai, out, lse);
         auto h = download<uint16_t>(out, size_t(n * hd));
         Tensor o = Tensor::zeros({n, hd}, in[0]->precision());
         for (int64_t i = 0; i < n * hd; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
@@ -196,19 +233,13 @@ struct ClusterAttnOp final : CustomOp {
     void backward(const Tensor& out_grad, const std::vector<const Tensor*>& in,
                   const std::vector<Tensor*>& in_grads) override {
         const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
-        auto dc = upload(f32(coords));
-        DeviceIndex d = build_index(*dc, n, cluster, groups);
+        Geometry& G = geometry(n);
         std::unique_ptr<Dev> t[10];
-        for (int i = 0; i < 5; ++i) t[i] = upload(bf16(*in[size_t(i)]));
-        for (int i = 5; i < 10; ++i) t[i] = upload(f32(*in[size_t(i)]));
-        affmae_attn_inputs ai{t[0]->as<affmae_bf16>(), t[1]->as<affmae_bf16>(), t[2]->as<affmae_bf16>(),
-                              t[3]->as<affmae_bf16>(), t[4]->as<affmae_bf16>(), dc->as<float>(),
-                              t[5]->as<float>(), t[6]->as<float>(), t[7]->as<float>(), t[8]->as<float>(),
-                              t[9]->as<float>()};
+        affmae_attn_inputs ai = inputs(in, G, t);
         affmae_attn_desc a = desc();
-        Dev out(n * hd * 2), lse(n * heads * 4), wsf(affmae_attn_fwd_workspace(&d.g, &a));
-        check(affmae_attn_fwd(&d.g, &a, &ai, d.perm->as<int32_t>(), d.nbr->as<int32_t>(),
-                              out.as<affmae_bf16>(), lse.as<float>(), wsf.p, wsf.n, nullptr), "attn_fwd");
+        // the backward needs O and LSE: recomputed from the inputs (the op keeps no activations)
+        Dev out(n * hd * 2), lse(n * heads * 4);
+        run_forward(G, ai, out, lse);
         auto dout = upload(bf16(out_grad));
         Dev dq(n * hd * 2), dk(n * hd * 2), dv(n * hd * 2);
         std::unique_ptr<Dev> pg[7];
@@ -221,9 +252,10 @@ struct ClusterAttnOp final : CustomOp {
         affmae_attn_grads g{dq.as<affmae_bf16>(), dk.as<affmae_bf16>(), dv.as<affmae_bf16>(),
                             pg[0]->as<float>(), pg[1]->as<float>(), pg[2]->as<float>(), pg[3]->as<float>(),
                             pg[4]->as<float>(), pg[5]->as<float>(), pg[6]->as<float>()};
-        Dev wsb(affmae_attn_bwd_workspace(&d.g, &a));
-        check(affmae_attn_bwd(&d.g, &a, &ai, &d.idx, out.as<affmae_bf16>(), lse.as<float>(),
-                              dout->as<affmae_bf16>(), &g, wsb.p, wsb.n, nullptr), "attn_bwd");
+        Dev wsb(affmae_attn_bwd_planned_workspace(&G.d.g, &a));
+        check(affmae_attn_bwd_planned(&G.d.g, &a, &ai, &G.plan, out.as<affmae_bf16>(), lse.as<float>(),
+                                      dout->as<affmae_bf16>(), &g, wsb.p, wsb.n, nullptr),
+              "attn_bwd");
         ccheck(cudaDeviceSynchronize(), "sync");
         // accumulate (+=) into non-null in_grads (include/affmae/tape.hpp:29-31)
         const Dev* act[3] = {&dq, &dk, &dv};
