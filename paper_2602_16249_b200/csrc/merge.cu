@@ -17,6 +17,7 @@
 // contraction, ties go to the lowest retained position, exactly the
 // reference's first-minimum scan.  Pools collect (sqrt(d^2), j), are sorted
 // by (dist, index) and truncated to k_m.
+#include <algorithm>
 #include <cmath>
 
 #include "sort.cuh"
@@ -640,6 +641,45 @@ __device__ __forceinline__ int pool_row_weights(const int32_t* pool_idx, const d
     return cnt;
 }
 
+// Pool indices / distances / count of one row: loaded one row ahead (registers).
+template <int KMAX>
+struct PoolRowIdx {
+    int ji[KMAX];
+    double di[KMAX];
+    int cnt, rt;
+    __device__ __forceinline__ void load(const int32_t* pool_idx, const double* pool_dist, const int32_t* pool_cnt,
+                                         const int32_t* retained, int64_t row, int k_m, bool ok) {
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) {
+            ji[t] = ok && t < k_m ? __ldg(pool_idx + row * k_m + t) : 0;
+            di[t] = ok && t < k_m ? __ldg(pool_dist + row * k_m + t) : 0.0;
+        }
+        cnt = ok ? __ldg(pool_cnt + row) : 0;
+        rt = ok ? __ldg(retained + row) : 0;
+    }
+    // softmax(-p * dist) weights (merging.cpp:121-149)
+    __device__ __forceinline__ void weights(float p, int (&jj)[KMAX], float (&w)[KMAX], float (&dd)[KMAX]) const {
+        float m = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) {
+            jj[t] = t < cnt ? ji[t] : 0;
+            dd[t] = t < cnt ? float(di[t]) : 0.f;
+            if (t < cnt) m = fmaxf(m, -p * dd[t]);
+        }
+        float l = 0.f;
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) {
+            w[t] = t < cnt ? __expf(-p * dd[t] - m) : 0.f;
+            l += w[t];
+        }
+        const float il = cnt > 0 ? 1.f / l : 0.f;
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) w[t] *= il;
+    }
+};
+
+// Persistent: each row group (LPR lanes) walks rows g, g + G, ... ; the next
+// row's indices are loaded while the current row's gathers are in flight.
 template <int CPR, int KMAX>
 __global__ void __launch_bounds__(256) pool_fwd_v2_kernel(
     const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
@@ -647,40 +687,55 @@ __global__ void __launch_bounds__(256) pool_fwd_v2_kernel(
     const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
     int64_t r, int k_m, __nv_bfloat16* __restrict__ out) {
     constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR, CPL = CPR / LPR;
-    const int lane = threadIdx.x & 31, sl = lane % LPR;
-    const int64_t row = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPW + lane / LPR;
-    if (row >= batch * r) return;
-    const int64_t b = row / r;
     constexpr int D = CPR * 8;
-    int jj[KMAX];
-    float w[KMAX], dd[KMAX];
-    const int cnt = pool_row_weights<KMAX>(pool_idx, pool_dist, pool_cnt, row, k_m, *p_merge, jj, w, dd);
-    const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * D);
-    const float* sb = scores + b * n;
-    float g[KMAX];
+    const int lane = threadIdx.x & 31, sl = lane % LPR;
+    const int64_t groups = int64_t(gridDim.x) * (blockDim.x >> 5) * RPW;
+    const int64_t total = batch * r;
+    int64_t row = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPW + lane / LPR;
+    const float p = *p_merge;
+    PoolRowIdx<KMAX> cur;
+    cur.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, row < total);
+    for (; row < total; row += groups) {
+        const int64_t b = row / r;
+        int jj[KMAX];
+        float w[KMAX], dd[KMAX];
+        cur.weights(p, jj, w, dd);
+        const int cnt = cur.cnt;
+        const int64_t rt = cur.rt;
+        const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * D);
+        const float* sb = scores + b * n;
+        float sj[KMAX];
 #pragma unroll
-    for (int t = 0; t < KMAX; ++t) g[t] = t < cnt ? w[t] * sb[jj[t]] : 0.f;
-    uint4* o = reinterpret_cast<uint4*>(out + row * 2 * D);
-    const int64_t rt = retained[row];
+        for (int t = 0; t < KMAX; ++t) sj[t] = t < cnt ? __ldg(sb + jj[t]) : 0.f;
+        uint4 v[CPL][KMAX], own[CPL];
 #pragma unroll
-    for (int cc = 0; cc < CPL; ++cc) {
-        const int ch = sl + cc * LPR;
-        uint4 v[KMAX];
+        for (int cc = 0; cc < CPL; ++cc) {
+            const int ch = sl + cc * LPR;
 #pragma unroll
-        for (int t = 0; t < KMAX; ++t)
-            if (t < cnt) v[t] = __ldg(fb + int64_t(jj[t]) * CPR + ch);
-        o[ch] = __ldg(fb + rt * CPR + ch);
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) {
-            if (t < cnt) {
-                float f[8];
-                bf16x8_to_f32(v[t], f);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] = fmaf(g[t], f[i], acc[i]);
-            }
+            for (int t = 0; t < KMAX; ++t)
+                if (t < cnt) v[cc][t] = __ldg(fb + int64_t(jj[t]) * CPR + ch);
+            own[cc] = __ldg(fb + rt * CPR + ch);
         }
-        o[CPR + ch] = f32_to_bf16x8(acc);
+        const int64_t nxt = row + groups;
+        cur.load(pool_idx, pool_dist, pool_cnt, retained, nxt, k_m, nxt < total);  // overlaps the gathers
+        uint4* o = reinterpret_cast<uint4*>(out + row * 2 * D);
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+            const int ch = sl + cc * LPR;
+            o[ch] = own[cc];
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int t = 0; t < KMAX; ++t) {
+                if (t < cnt) {
+                    float f[8];
+                    bf16x8_to_f32(v[cc][t], f);
+                    const float g = w[t] * sj[t];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = fmaf(g, f[i], acc[i]);
+                }
+            }
+            o[CPR + ch] = f32_to_bf16x8(acc);
+        }
     }
 }
 
@@ -786,7 +841,7 @@ static int launch_pool_fwd_v2(const __nv_bfloat16* feats, const float* scores, c
                               int64_t r, int k_m, __nv_bfloat16* out, cudaStream_t st) {
     constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR;
     const int64_t warps = (batch * r + RPW - 1) / RPW;
-    const unsigned nb = unsigned((warps + 7) / 8);
+    const unsigned nb = unsigned(std::min<int64_t>((warps + 7) / 8, int64_t(kNumSMs) * 8));
     if (k_m <= 8)
         pool_fwd_v2_kernel<CPR, 8><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
                                                         plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, out);
