@@ -346,8 +346,19 @@ __global__ void attn_part_reduce_kernel(const float* __restrict__ part, int gx0,
     float acc = 0.f;
     if (j < pw) {
         const float* p1 = part + size_t(heads) * gx0 * pw;
-        for (int x = warp; x < gx0 + gx1; x += 8)
-            acc += x < gx0 ? part[(size_t(h) * gx0 + x) * pw + j] : p1[(size_t(h) * gx1 + x - gx0) * pw + j];
+        auto at = [&](int x) {
+            return x < gx0 ? part[(size_t(h) * gx0 + x) * pw + j] : p1[(size_t(h) * gx1 + x - gx0) * pw + j];
+        };
+        const int nx = gx0 + gx1;
+        float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains, fixed order
+        int x = warp;
+        for (; x + 7 * 8 < nx; x += 64) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] += at(x + u * 8);
+        }
+        for (; x < nx; x += 8) a[0] += at(x);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += a[u];
     }
     red[warp][lane] = acc;
     __syncthreads();
