@@ -264,15 +264,66 @@ constexpr int kNbrWarps = 8, kNbrPerWarp = 4;
 template <int G>
 __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* __restrict__ cent, ClusterShape cs,
                                                                  int32_t* __restrict__ nbr_cl) {
+    // smem: binary64 centroids, then their fp32 copies
     extern __shared__ double2 sc[];
+    float2* sf = reinterpret_cast<float2*>(sc + cs.c);
+    __shared__ unsigned int smax;
     const int b = blockIdx.y;
     const double2* cb = cent + int64_t(b) * cs.c;
-    for (int i = threadIdx.x; i < cs.c; i += blockDim.x) sc[i] = cb[i];
+    if (threadIdx.x == 0) smax = 0u;
     __syncthreads();
+    float lmax = 0.f;
+    for (int i = threadIdx.x; i < cs.c; i += blockDim.x) {
+        const double2 c = cb[i];
+        sc[i] = c;
+        sf[i] = make_float2(float(c.x), float(c.y));
+        lmax = fmaxf(lmax, fmaxf(fabsf(float(c.x)), fabsf(float(c.y))));
+    }
+    atomicMax(&smax, __float_as_uint(lmax));  // non-negative floats order like their bits
+    __syncthreads();
+    // |d2_fp32 - d2_fp64| <= ~5e-7 * maxc^2 (rounding of the coordinates and of d2): margin 4x that
+    const float maxc = __uint_as_float(smax) + 1.f;
+    const float margin = 1.f + 2e-6f * maxc * maxc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k0 = (blockIdx.x * kNbrWarps + warp) * kNbrPerWarp;
     for (int k = k0; k < min(k0 + kNbrPerWarp, cs.c); ++k) {
         const double2 ck = sc[k];
+        const float2 fk = sf[k];
+        // pass 1 (fp32): the G-th smallest approximate d^2 over all centroids
+        float fd[G];
+#pragma unroll
+        for (int r = 0; r < G; ++r) fd[r] = INFINITY;
+        for (int j = lane; j < cs.c; j += 32) {
+            const float2 fj = sf[j];
+            const float dx = fj.x - fk.x, dy = fj.y - fk.y;
+            float v = fmaf(dx, dx, dy * dy);
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                const float lo = fminf(v, fd[r]);
+                v = fmaxf(v, fd[r]);
+                fd[r] = lo;
+            }
+        }
+        // warp-wide G-th smallest: repeatedly extract the minimum
+        float thr = INFINITY;
+        {
+            int head = 0;
+#pragma unroll
+            for (int r = 0; r < G; ++r) {
+                float mine = fd[0];
+#pragma unroll
+                for (int q = 1; q < G; ++q) mine = q == head ? fd[q] : mine;
+                if (head >= G) mine = INFINITY;
+                float m = mine;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                const unsigned who = __ballot_sync(0xffffffffu, mine == m && head < G);
+                if (lane == __ffs(who) - 1) ++head;
+                thr = m;
+            }
+        }
+        thr = thr * 1.0001f + margin;
+        // pass 2 (exact binary64) over the candidates under the threshold only
         double d[G];
         int jj[G];
 #pragma unroll
@@ -281,6 +332,9 @@ __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* _
             jj[r] = INT32_MAX;
         }
         for (int j = lane; j < cs.c; j += 32) {
+            const float2 fj = sf[j];
+            const float fx = fj.x - fk.x, fy = fj.y - fk.y;
+            if (fmaf(fx, fx, fy * fy) > thr) continue;
             const double2 cj = sc[j];
             const double dx = __dsub_rn(cj.x, ck.x), dy = __dsub_rn(cj.y, ck.y);
             const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
@@ -301,7 +355,7 @@ __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* _
 }
 
 static int launch_nbr(const double2* cent, int64_t batch, const ClusterShape& cs, int32_t* nbr, cudaStream_t st) {
-    const size_t smem = size_t(cs.c) * sizeof(double2);
+    const size_t smem = size_t(cs.c) * (sizeof(double2) + sizeof(float2));
     if (smem > 200 * 1024) return -1;  // very large images: the generic kernel
     const dim3 grid(unsigned((cs.c + kNbrWarps * kNbrPerWarp - 1) / (kNbrWarps * kNbrPerWarp)), unsigned(batch));
     switch (cs.g) {
