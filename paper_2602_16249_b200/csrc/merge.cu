@@ -317,7 +317,8 @@ __global__ void seg_scan_kernel(int32_t* __restrict__ cnt, int64_t len) {
 __global__ void cell_fill_kernel(const float* __restrict__ coords, const int32_t* __restrict__ retained,
                                  int64_t batch, int64_t n, int64_t r, int g,
                                  const GridPrm* __restrict__ prm, const int32_t* __restrict__ off,
-                                 int32_t* __restrict__ cursor, int32_t* __restrict__ items) {
+                                 int32_t* __restrict__ cursor, int32_t* __restrict__ items,
+                                 float2* __restrict__ item_xy) {
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= batch * r) return;
     int64_t b = i / r;
@@ -327,6 +328,7 @@ __global__ void cell_fill_kernel(const float* __restrict__ coords, const int32_t
     int64_t cell = b * (int64_t(g) * g + 1) + cy * g + cx;
     int slot = atomicAdd(cursor + cell, 1);
     items[b * r + off[cell] + slot] = int32_t(i - b * r);
+    item_xy[b * r + off[cell] + slot] = v;  // candidate coordinates beside the index: one load per candidate
 }
 
 __device__ __forceinline__ bool better(double d, int ri, double bd, int bri) {
@@ -337,7 +339,8 @@ __device__ __forceinline__ bool better(double d, int ri, double bd, int bri) {
 __global__ void assign_kernel(const float* __restrict__ coords, const int32_t* __restrict__ retained,
                               const int32_t* __restrict__ ret_pos, int64_t batch, int64_t n, int64_t r,
                               int g, const GridPrm* __restrict__ prm, const int32_t* __restrict__ off,
-                              const int32_t* __restrict__ items, int32_t* __restrict__ target,
+                              const int32_t* __restrict__ items, const float2* __restrict__ item_xy,
+                              int32_t* __restrict__ target,
                               int32_t* __restrict__ best_of, double* __restrict__ d2_of,
                               int32_t* __restrict__ pool_cnt_all) {
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -353,6 +356,7 @@ __global__ void assign_kernel(const float* __restrict__ coords, const int32_t* _
     const int32_t* ret = retained + b * r;
     const int32_t* co = off + b * (int64_t(g) * g + 1);
     const int32_t* it = items + b * r;
+    const float2* ixy = item_xy + b * r;
     const float2 q = xy[i - b * n];
     const double qx = q.x, qy = q.y;
     const int qcx = cell_of(qx, p.x0, p.w, g), qcy = cell_of(qy, p.y0, p.w, g);
@@ -364,7 +368,7 @@ __global__ void assign_kernel(const float* __restrict__ coords, const int32_t* _
             const int cell = cy * g + cx;
             for (int t = co[cell]; t < co[cell + 1]; ++t) {
                 const int ri = it[t];
-                const float2 v = xy[ret[ri]];
+                const float2 v = ixy[t];
                 const double dx = __dsub_rn(double(v.x), qx), dy = __dsub_rn(double(v.y), qy);
                 const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
                 if (better(d2, ri, bd, bri)) {
@@ -957,6 +961,7 @@ struct PlanWs {
     int32_t* cell_off;
     int32_t* cell_cur;
     int32_t* items;
+    float2* item_xy;
     int32_t* best_of;
     double* d2_of;
     int32_t* pool_off;
@@ -987,6 +992,7 @@ static PlanWs carve_plan(int64_t batch, int64_t n, int64_t r, void* base) {
     w.cell_off = reinterpret_cast<int32_t*>(take(cells * 4));
     w.cell_cur = reinterpret_cast<int32_t*>(take(cells * 4));
     w.items = reinterpret_cast<int32_t*>(take(size_t(batch) * r * 4));
+    w.item_xy = reinterpret_cast<float2*>(take(size_t(batch) * r * 8));
     w.best_of = reinterpret_cast<int32_t*>(take(size_t(batch) * n * 4));
     w.d2_of = reinterpret_cast<double*>(take(size_t(batch) * n * 8));
     w.pool_off = reinterpret_cast<int32_t*>(take(size_t(batch) * (r + 1) * 4));
@@ -1027,9 +1033,9 @@ int merge_plan_build(const float* coords, const int32_t* retained, int64_t batch
     cell_count_kernel<<<blocks_of(batch * r), 256, 0, st>>>(coords, retained, batch, n, r, g, w.prm, w.cell_off);
     seg_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(w.cell_off, cells);
     cell_fill_kernel<<<blocks_of(batch * r), 256, 0, st>>>(coords, retained, batch, n, r, g, w.prm,
-                                                           w.cell_off, w.cell_cur, w.items);
+                                                           w.cell_off, w.cell_cur, w.items, w.item_xy);
     assign_kernel<<<blocks_of(batch * n, 128), 128, 0, st>>>(coords, retained, w.ret_pos, batch, n, r, g, w.prm,
-                                                        w.cell_off, w.items, plan->target, w.best_of,
+                                                        w.cell_off, w.items, w.item_xy, plan->target, w.best_of,
                                                         w.d2_of, w.pool_off);
     seg_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(w.pool_off, r + 1);
     pool_fill_kernel<<<blocks_of(batch * n), 256, 0, st>>>(w.best_of, w.d2_of, batch, n, r, w.pool_off,
