@@ -242,9 +242,36 @@ def run_ours(a, rank, world, dist):
             ev[4].record()
         return out, lse, grads, pooled, dfe, dsc, dp
 
-    # warm-up (also primes the caching allocator) + per-phase timing pass
+    side = torch.cuda.Stream(device=dev)
+
+    def step_dag():
+        """The same step as a two-stream DAG: selection + merge plan depend only on scores
+        and coordinates, the pool fwd/bwd only on the attention output, so they run beside the
+        index build and the attention backward."""
+        cur = torch.cuda.current_stream(dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            ret = ops.select_retained(scores, a.d_s)
+            mplan = ops.merge_plan(coords, ret, a.k_m)
+        idx = ops.cluster_index(coords, a.cluster, a.groups, workspace=ws)
+        plan = ops.attn_plan(geom, coords, idx, h, d, a.hidden, buf=plan_buf)
+        out, lse = ops.attn_fwd(geom, q, k, v, bk, bv, coords, idx.perm, idx.nbr_cl, bias, h, d,
+                                out=out_buf, lse=lse_buf, workspace=ws, plan=plan)
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(cur)
+        with torch.cuda.stream(side):
+            side.wait_event(fwd_done)
+            pooled = ops.merge_pool_fwd(out, scores, p_merge, mplan)
+            dfe, dsc, dp = ops.merge_pool_bwd(out, scores, p_merge, mplan, dpooled)
+        ops.attn_bwd(geom, q, k, v, bk, bv, coords, idx, bias, h, d, out, lse, dout, grads=grads,
+                     workspace=ws, plan=plan)
+        cur.wait_stream(side)
+        return out, lse, grads, pooled, dfe, dsc, dp
+
+    # warm-up (also primes the caching allocator) + per-phase timing pass (sequential)
     for _ in range(max(1, a.warmup)):
         step()
+        step_dag()
     torch.cuda.synchronize()
     n_ph = 5
     phase_ms = {p: [] for p in phases}
@@ -263,7 +290,7 @@ def run_ours(a, rank, world, dist):
             s = torch.cuda.Stream(device=dev)
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
-                step()
+                step_dag()
             torch.cuda.current_stream().wait_stream(s)
             torch.cuda.synchronize()
             try:
@@ -271,7 +298,7 @@ def run_ours(a, rank, world, dist):
             except TypeError:  # older torch
                 graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
-                step()
+                step_dag()
             torch.cuda.synchronize()
             launches = count_graph_kernels(graph)
             if hasattr(graph, "instantiate"):
@@ -287,7 +314,7 @@ def run_ours(a, rank, world, dist):
         if graph is not None:
             graph.replay()
         else:
-            step()
+            step_dag()
 
     for _ in range(a.warmup):
         run_step()
@@ -407,21 +434,32 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
     bias = ops.BiasNet(**dhb)
     outs_d = [None] * nch
 
+    s_side = torch.cuda.Stream(device=dev)
+
     def chunk_compute(c):
-        """The op chain of one chunk (device buffers in, device results out)."""
+        """The op chain of one chunk (device buffers in, device results out), as the same
+        two-stream DAG as the device-resident step."""
         b0, b1 = bounds[c]
         dv_ = dbuf[c]
         g = cgeom[b1 - b0]
+        cur = torch.cuda.current_stream(dev)
+        s_side.wait_stream(cur)
+        with torch.cuda.stream(s_side):
+            ret = ops.select_retained(dv_["scores"], a.d_s)
+            mplan = ops.merge_plan(dv_["coords"], ret, a.k_m)
         idx = ops.cluster_index(dv_["coords"], a.cluster, a.groups, workspace=ws)
         plan = ops.attn_plan(g, dv_["coords"], idx, h, d, a.hidden, buf=plan_buf)
         out, lse = ops.attn_fwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
                                 dv_["coords"], idx.perm, idx.nbr_cl, bias, h, d, workspace=ws, plan=plan)
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(cur)
+        with torch.cuda.stream(s_side):
+            s_side.wait_event(fwd_done)
+            pooled = ops.merge_pool_fwd(out, dv_["scores"], p_merge, mplan)
+            dfe, dsc, _ = ops.merge_pool_bwd(out, dv_["scores"], p_merge, mplan, dv_["dpooled"])
         gr = ops.attn_bwd(g, dv_["q"], dv_["k"], dv_["v"], dsmall["bk"], dsmall["bv"],
                           dv_["coords"], idx, bias, h, d, out, lse, dv_["dout"], workspace=ws, plan=plan)
-        ret = ops.select_retained(dv_["scores"], a.d_s)
-        mplan = ops.merge_plan(dv_["coords"], ret, a.k_m)
-        pooled = ops.merge_pool_fwd(out, dv_["scores"], p_merge, mplan)
-        dfe, dsc, _ = ops.merge_pool_bwd(out, dv_["scores"], p_merge, mplan, dv_["dpooled"])
+        cur.wait_stream(s_side)
         outs_d[c] = dict(out=out, lse=lse, dq=gr.dq, dk=gr.dk, dv=gr.dv, pooled=pooled, dfeats=dfe,
                          dscores=dsc)
 
