@@ -641,37 +641,46 @@ static int build_plan(const affmae_cluster_geom* g, float inv_patch, const float
     const int64_t items = g->batch * g->n_clusters;
     const unsigned blocks = unsigned((items + 3) / 4);
     const int kp = pick_kp(g->width);
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.rmax, 0, 16, st));
-    switch (kp) {
+    // the key-side records (backward only) are independent of the query side:
+    // build them concurrently on the forked side stream
+    auto query_side = [&](cudaStream_t st) -> int {
+        AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.rmax, 0, 16, st));
+        switch (kp) {
 #define AFFMAE_QREC(KP_)                                                                                 \
-    case KP_:                                                                                            \
-        attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(coords, perm, nbr_cl, cs, items, inv_patch, w.qrec, \
-                                                      w.rmax);                                           \
-        break;
-        AFFMAE_QREC(16)
-        AFFMAE_QREC(32)
-        AFFMAE_QREC(48)
-        AFFMAE_QREC(64)
+        case KP_:                                                                                            \
+            attn_qrec_kernel<KP_><<<blocks, 128, 0, st>>>(coords, perm, nbr_cl, cs, items, inv_patch, w.qrec, \
+                                                          w.rmax);                                           \
+            break;
+            AFFMAE_QREC(16)
+            AFFMAE_QREC(32)
+            AFFMAE_QREC(48)
+            AFFMAE_QREC(64)
 #undef AFFMAE_QREC
-        default:
-            return fail(AFFMAE_EUNSUPPORTED, "attention: width");
-    }
-    AFFMAE_LAUNCH_CHECK("attn_qrec_kernel");
-    {
-        const int words = 32 + 2 * kp + 8, hf = 32 + 2 * kp + kHFast;
-        const unsigned nb = unsigned((items + 1023) / 1024);
-        attn_item_count_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk);
-        AFFMAE_LAUNCH_CHECK("attn_item_count_kernel");
-        attn_item_scatter_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk, w.items,
-                                                      w.item_count);
-        AFFMAE_LAUNCH_CHECK("attn_item_scatter_kernel");
-    }
-    if (rev_cl) {
-        attn_krec_kernel<<<blocks, 128, 0, st>>>(coords, perm, rev_off, rev_cl, cs, items, inv_patch, w.krec,
-                                                 w.prec);
-        AFFMAE_LAUNCH_CHECK("attn_krec_kernel");
-    }
-    return AFFMAE_OK;
+            default:
+                return fail(AFFMAE_EUNSUPPORTED, "attention: width");
+        }
+        AFFMAE_LAUNCH_CHECK("attn_qrec_kernel");
+        {
+            const int words = 32 + 2 * kp + 8, hf = 32 + 2 * kp + kHFast;
+            const unsigned nb = unsigned((items + 1023) / 1024);
+            attn_item_count_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk);
+            AFFMAE_LAUNCH_CHECK("attn_item_count_kernel");
+            attn_item_scatter_kernel<<<nb, 1024, 0, st>>>(w.qrec, words, hf, int(items), w.item_blk, w.items,
+                                                          w.item_count);
+            AFFMAE_LAUNCH_CHECK("attn_item_scatter_kernel");
+        }
+        return AFFMAE_OK;
+    };
+    if (!rev_cl) return query_side(st);
+    return launch_forked(
+        st,
+        [&](cudaStream_t s) {
+            attn_krec_kernel<<<blocks, 128, 0, s>>>(coords, perm, rev_off, rev_cl, cs, items, inv_patch, w.krec,
+                                                    w.prec);
+            AFFMAE_LAUNCH_CHECK("attn_krec_kernel");
+            return AFFMAE_OK;
+        },
+        query_side);
 }
 
 // per-call state: BiasNet offset table of the current weights; wires the plan in
