@@ -124,16 +124,20 @@ struct TokAgg {
 
 // Query-cluster records (one warp per (image, cluster)): query tokens, the
 // key token of every neighbourhood slot in reference order
-// (cluster_neighborhood, proj/src/geometry.cpp:173-183), lattice cells, nk,
+// (cluster_neighborhood, proj/src/geometry.cpp:173-183; lattice-fast items
+// permute it, see below), lattice cells, nk,
 // qlen, the lattice-fast flag and duplicate-cell flags of the two key halves.
 template <int KP>
 __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t* __restrict__ perm,
                                  const int32_t* __restrict__ nbr_cl, ClusterShape cs, int64_t items,
                                  float inv_patch, int32_t* __restrict__ qrec, int32_t* __restrict__ rmax) {
     using R = QRec<KP>;
+    static_assert(KP <= 64, "two key slots per lane");
     constexpr int E = 16 + KP, J = (E + 31) / 32;
     __shared__ int cellbuf[4][E];
     __shared__ int pcellbuf[4][E];
+    __shared__ int tokbuf[4][E];
+    __shared__ int keybuf[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = int64_t(blockIdx.x) * 4 + warp;
     if (item >= items) return;
@@ -171,15 +175,64 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
             agg.add(t, e >= 16);
         }
         if (e < E) {
-            out[e < 16 ? R::QTOK + e : R::KTOK + e - 16] = tok;
+            tokbuf[warp][e] = tok;
             cellbuf[warp][e] = cell;
             pcellbuf[warp][e] = pcell;
         }
     }
     int radius = 0;
     const int cls = agg.cls(&radius);
-    if (lane == 0) atomicMax(rmax, cls == 0 ? kRg : radius);
+    {   // one address for the whole grid: skip the atomic when it cannot raise the max
+        const int rv = cls == 0 ? kRg : radius;
+        if (lane == 0 && rv > *reinterpret_cast<volatile int*>(rmax)) atomicMax(rmax, rv);
+    }
     __syncwarp();
+    if (cls == 1) {
+        // Lattice-fast: reorder the key slots by (occurrence of the window
+        // cell's residue mod 32, slot), so each 32-slot half holds distinct
+        // residues where possible -- the backward's per-query-row table RMW
+        // (lanes over key slots, bank = cell mod 32 + const) is then nearly
+        // conflict-free.  Attention is invariant to the key order.
+        const unsigned lt = (1u << lane) - 1u;
+        const bool v0 = lane < nk, v1 = lane + 32 < nk;
+        const int res0 = cellbuf[warp][16 + (lane < KP ? lane : 0)] & 31;
+        const int res1 = KP > 32 ? cellbuf[warp][16 + (lane + 32 < KP ? lane + 32 : 0)] & 31 : 0;
+        const unsigned m0 = __match_any_sync(0xffffffffu, v0 ? res0 : 64 + lane);
+        const unsigned m1 = __match_any_sync(0xffffffffu, v1 ? res1 : 64 + lane);
+        keybuf[warp][lane] = 0;  // per-residue count of the first half
+        __syncwarp();
+        if (v0) keybuf[warp][res0] = __popc(m0);
+        __syncwarp();
+        const int o0 = __popc(m0 & lt), o1 = (v1 ? keybuf[warp][res1] : 0) + __popc(m1 & lt);
+        const int levels = __reduce_max_sync(0xffffffffu, max(v0 ? o0 : 0, v1 ? o1 : 0)) + 1;
+        int npos[2] = {lane, lane + 32}, base = 0;
+        for (int L = 0; L < levels; ++L) {
+            const unsigned b0 = __ballot_sync(0xffffffffu, v0 && o0 == L);
+            const unsigned b1 = __ballot_sync(0xffffffffu, v1 && o1 == L);
+            if (v0 && o0 == L) npos[0] = base + __popc(b0 & lt);
+            if (v1 && o1 == L) npos[1] = base + __popc(b0) + __popc(b1 & lt);
+            base += __popc(b0) + __popc(b1);
+        }
+        int ntok[2], ncell[2], npcell[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int sl = lane + 32 * j;
+            if (sl < nk) {
+                ntok[j] = tokbuf[warp][16 + sl];
+                ncell[j] = cellbuf[warp][16 + sl];
+                npcell[j] = pcellbuf[warp][16 + sl];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            if (lane + 32 * j < nk) {
+                tokbuf[warp][16 + npos[j]] = ntok[j];
+                cellbuf[warp][16 + npos[j]] = ncell[j];
+                pcellbuf[warp][16 + npos[j]] = npcell[j];
+            }
+        __syncwarp();
+    }
     const int(*cb)[E] = cls == 2 ? pcellbuf : cellbuf;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -187,6 +240,7 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
         if (e < E) {
             const bool valid = e < 16 ? e < qlen : e - 16 < nk;
             const int cell = valid ? cb[warp][e] : cb[warp][e < 16 ? 0 : 16];
+            out[e < 16 ? R::QTOK + e : R::KTOK + e - 16] = tokbuf[warp][e];
             out[e < 16 ? R::QCELL + e : R::KCELL + e - 16] = cell;
         }
     }
@@ -199,7 +253,7 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     if (lane < 8) {
         const int v = lane == kHNk ? nk : lane == kHQlen ? qlen : lane == kHFast ? cls
                     : lane == kHDup0 ? int(dup0) : lane == kHDup1 ? int(dup1)
-                    : lane == kHImgTok ? int(img_tok) : 0;
+                    : lane == kHImgTok ? int(img_tok) : lane == kHItem ? int(item) : 0;
         out[R::HDR + lane] = v;
     }
 }
@@ -322,7 +376,8 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
         if (lane < 8) {
             const int v = lane == kPQlen ? qlen : lane == kPFast ? int(fast) : lane == kPFirst ? int(pr == rb)
                         : lane == kPLast ? int(pr == re - 1) : lane == kPItem ? int(item)
-                        : lane == kPIdx ? int(int64_t(img) * pairs + pr) : 0;
+                        : lane == kPIdx ? int(int64_t(img) * pairs + pr)
+                        : lane == kPQItem ? int(int64_t(img) * cs.c + qc) : 0;
             po[PRec::HDR + lane] = v;
         }
     }
@@ -539,7 +594,7 @@ struct AttnWs {
     int32_t* prec;
     float* tab_g;
     float* dtab_g;
-    float* dsum;
+    float2* lsd;
     float* part;
     float* mlp_grad;
     float* blank_grad;
@@ -580,7 +635,7 @@ static void carve_run(const affmae_cluster_geom* g, const affmae_attn_desc* a, v
     w.tab_g = reinterpret_cast<float*>(c.take(size_t(a->heads) * kWg2 * 4));
     if (bwd) {
         w.dtab_g = reinterpret_cast<float*>(c.take(size_t(kTabReplicas) * a->heads * kWg2 * 4));
-        w.dsum = reinterpret_cast<float*>(c.take(size_t(g->batch) * g->tokens * a->heads * 4));
+        w.lsd = reinterpret_cast<float2*>(c.take(size_t(g->batch) * g->n_clusters * a->heads * 16 * 8));
         w.part = reinterpret_cast<float*>(
             c.take(2 * size_t(kMaxCtasPerGroup) * a->heads * part_width(a->head_dim) * 4));  // [launch][h][CTA]
         w.mlp_grad = reinterpret_cast<float*>(c.take(size_t(a->heads) * (4 * a->bias_hidden + 1) * 4));
@@ -801,7 +856,7 @@ static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, cons
     p.dq = reinterpret_cast<__nv_bfloat16*>(gr->dq);
     p.dk = reinterpret_cast<__nv_bfloat16*>(gr->dk);
     p.dv = reinterpret_cast<__nv_bfloat16*>(gr->dv);
-    p.dsum = w.dsum;
+    p.lsd = w.lsd;
     p.dtab_g = w.dtab_g;
     p.part = w.part;
     int rc = prepare_run(p, w, st);

@@ -60,20 +60,20 @@ struct QRec {
     static constexpr int QTOK = 0, KTOK = 16, QCELL = 16 + KP, KCELL = 32 + KP, HDR = 32 + 2 * KP;
     static constexpr int WORDS = HDR + 8;  // multiple of 4 (16-byte copies)
 };
-enum { kHNk = 0, kHQlen = 1, kHFast = 2, kHDup0 = 3, kHDup1 = 4, kHImgTok = 5 };  // img_tok = image * N
+enum { kHNk = 0, kHQlen = 1, kHFast = 2, kHDup0 = 3, kHDup1 = 4, kHImgTok = 5, kHItem = 6 };  // img_tok = image * N
 // Key-cluster record: ktok[16] kcell[16] kpcell[16] hdr{klen, rb, re, first pair (global), img_tok}
 struct KRec {
     static constexpr int KTOK = 0, KCELL = 16, KPCELL = 32, HDR = 48, WORDS = 56;
 };
 // Reverse pair record (CSR order of rev_cl):
-//   qtok[16] qcell[16] hdr{qlen, class, first, last, key item, global pair index}
+//   qtok[16] qcell[16] hdr{qlen, class, first, last, key item, global pair index, query item}
 // Record classes (hdr kHFast / kPFast): 1 lattice-fast (window cells iy*kWs+ix),
 // 2 medium (one phase, offsets within the global table: packed cells
 // (iy+2048)<<16 | (ix+2048)), 0 general (coordinates).
 struct PRec {
     static constexpr int QTOK = 0, QCELL = 16, HDR = 32, WORDS = 40;
 };
-enum { kPQlen = 0, kPFast = 1, kPFirst = 2, kPLast = 3, kPItem = 4, kPIdx = 5 };
+enum { kPQlen = 0, kPFast = 1, kPFirst = 2, kPLast = 3, kPItem = 4, kPIdx = 5, kPQItem = 6 };
 constexpr int kWinC = kRs * kWs + kRs;  // window index of offset (0, 0)
 constexpr int kMG = 4 * kMaxHidden + 1;  // tier-3 MLP grad accumulator per head
 constexpr int kTabReplicas = 4;          // global tier-2 gradient table copies (spread atomics)
@@ -102,7 +102,8 @@ struct AttnParams {
     __nv_bfloat16* dq;
     __nv_bfloat16* dk;
     __nv_bfloat16* dv;
-    float* dsum;    // [B, N, heads]  D = rowsum(P o dP)
+    float2* lsd;    // [B*C, heads, 16] per query-cluster row: {LSE*log2(e), D = rowsum(P o dP)}
+                    // (written by the query side, read contiguously by the key side)
     float* dtab_g;  // [kTabReplicas][heads][kWg2] tier-2 gradient (atomics)
     float* part;    // [heads][CTAs][part_width] per-warp gradient partials (of this launch)
     ClusterShape cs;
@@ -331,6 +332,11 @@ __device__ __forceinline__ void slow_bias_frag(float (&s)[NT][4], const int32_t*
         }
 }
 
+// Row stride (floats) of the dS scratch tile: KP + 8 puts the four rows of a
+// float2 fragment-store phase in disjoint 8-bank groups (conflict-free).
+template <int KP>
+constexpr int scr_stride() { return KP + 8; }
+
 // Bias-table gradient of a general (non-fast) item from the row-major dS tile
 // `scr` [16][KP]: per query row, lanes walk the key slots (slot lane, lane+32),
 // so same-phase keys of one row hit distinct window cells (plain RMW unless
@@ -353,7 +359,7 @@ __device__ __forceinline__ void general_grad_rowpass(const float* scr, const int
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
             const bool v = half ? vb : va;
-            const float ds = v ? scr[r * KP + lane + 32 * half] : 0.f;
+            const float ds = v ? scr[r * scr_stride<KP>() + lane + 32 * half] : 0.f;
             const TokInfo& ki = half ? kib : kia;
             const float2 k = half ? kb : ka;
             int gi = -1, li = -1;
@@ -434,7 +440,7 @@ __device__ __forceinline__ void medium_grad_rowpass(const float* scr, const int3
         for (int half = 0; half < 2; ++half) {
             if (half ? vb : va) {
                 const int kp = half ? kb : ka;
-                const float ds = scr[r * KP + lane + 32 * half];
+                const float ds = scr[r * scr_stride<KP>() + lane + 32 * half];
                 const int li = packed_window(kp, qp);
                 if (li >= 0) {
                     if (dup) atomicAdd(dtab + li, ds);
@@ -646,7 +652,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
 template <int HD, int KP>
 struct BwdQCfg {
     static constexpr int NT = KP / 8 + 1;
-    static constexpr int kScrFloats = (16 * KP > 8 * HD ? 16 * KP : 8 * HD);
+    static constexpr int kScrFloats = (16 * (KP + 8) > 8 * HD ? 16 * (KP + 8) : 8 * HD);
     static constexpr int QW = QRec<KP>::WORDS;
     struct alignas(16) Smem {
         __nv_bfloat16 Q[16 * HD];
@@ -785,10 +791,10 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
             D0 += __shfl_xor_sync(0xffffffffu, D0, o);
             D1 += __shfl_xor_sync(0xffffffffu, D1, o);
         }
-        if ((lane & 3) == 0) {
-            float* ds_img = p.dsum + img_tok * p.heads + h;
-            if (r0 < qlen) ds_img[uint32_t(rec[R::QTOK + r0]) * uint32_t(p.heads)] = D0;
-            if (r0 + 8 < qlen) ds_img[uint32_t(rec[R::QTOK + r0 + 8]) * uint32_t(p.heads)] = D1;
+        if ((lane & 3) == 0) {  // padding rows get {+inf, 0}: P = 0 on the key side
+            float2* l = p.lsd + (size_t(rec[R::HDR + kHItem]) * p.heads + h) * 16;
+            l[r0] = r0 < qlen ? make_float2(ls0, D0) : make_float2(INFINITY, 0.f);
+            l[r0 + 8] = r0 + 8 < qlen ? make_float2(ls1, D1) : make_float2(INFINITY, 0.f);
         }
         // dS = P (dP - D), in place of P; keep the blank column's P
         const float pbl0 = s[NT - 1][0], pbl1 = s[NT - 1][2];
@@ -858,10 +864,11 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         cp_async_commit();
         // ---- bias-table gradient (dS tile row-major in scratch, then one pass per query row)
         float* scr = sm.scr;
+        constexpr int SS = scr_stride<KP>();
 #pragma unroll
         for (int nt = 0; nt < KP / 8; ++nt) {
-            *reinterpret_cast<float2*>(scr + r0 * KP + nt * 8 + c0) = make_float2(s[nt][0], s[nt][1]);
-            *reinterpret_cast<float2*>(scr + (r0 + 8) * KP + nt * 8 + c0) = make_float2(s[nt][2], s[nt][3]);
+            *reinterpret_cast<float2*>(scr + r0 * SS + nt * 8 + c0) = make_float2(s[nt][0], s[nt][1]);
+            *reinterpret_cast<float2*>(scr + (r0 + 8) * SS + nt * 8 + c0) = make_float2(s[nt][2], s[nt][3]);
         }
         __syncwarp();
         const bool dup = (rec[R::HDR + kHDup0] | rec[R::HDR + kHDup1]) != 0;
@@ -876,16 +883,16 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
             if (!dup) {
                 for (int r = 0; r < qlen; ++r) {
                     const int qc = __shfl_sync(0xffffffffu, qcl, r);
-                    if (va) da[-qc] += scr[r * KP + lane];
-                    if (vb) db[-qc] += scr[r * KP + lane + 32];
+                    if (va) da[-qc] += scr[r * SS + lane];
+                    if (vb) db[-qc] += scr[r * SS + lane + 32];
                     __syncwarp();
                 }
             } else {
                 for (int r = 0; r < qlen; ++r) {
                     const int qc = __shfl_sync(0xffffffffu, qcl, r);
-                    if (va) atomicAdd(da - qc, scr[r * KP + lane]);
+                    if (va) atomicAdd(da - qc, scr[r * SS + lane]);
                     __syncwarp();
-                    if (vb) atomicAdd(db - qc, scr[r * KP + lane + 32]);
+                    if (vb) atomicAdd(db - qc, scr[r * SS + lane + 32]);
                     __syncwarp();
                 }
             }
@@ -943,8 +950,7 @@ struct BwdKCfg {
         __nv_bfloat16 V[16 * HD];
         __nv_bfloat16 dK[16 * HD];     // output staging (last round)
         __nv_bfloat16 dV[16 * HD];
-        float lse[2][16];
-        float dsum[2][16];
+        float2 lsd[2][16];             // {LSE*log2(e), D} of the round's query rows
         int32_t rec[3][RECW];
         float tab[kWs2];
         float4 units[kMaxHidden];
@@ -1002,16 +1008,9 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
             sw_gather<HD, 16>(sm.K, p.k + base, rowb, rec + KR + KRec::KTOK, lane);
             sw_gather<HD, 16>(sm.V, p.v + base, rowb, rec + KR + KRec::KTOK, lane);
         }
-        if (lane < 16) {
-            const int qt = rec[PRec::QTOK + lane];
-            if (qt >= 0) {
-                cp_async4(sm.lse[buf] + lane, p.lse + (img_tok + qt) * p.heads + h);
-                cp_async4(sm.dsum[buf] + lane, p.dsum + (img_tok + qt) * p.heads + h);
-            } else {
-                sm.lse[buf][lane] = INFINITY;
-                sm.dsum[buf][lane] = 0.f;
-            }
-        }
+        if (lane < 8)
+            cp_async16(sm.lsd[buf] + 2 * lane,
+                       p.lsd + (size_t(rec[PRec::HDR + kPQItem]) * p.heads + h) * 16 + 2 * lane);
     };
 
     // prologue: records of rounds 0 and 1, rows of round 0
@@ -1093,10 +1092,9 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
                 b[2] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qa, kt1);
                 b[3] = slow_bias2(p, sm.tab, sm.units, h, img_tok, qb, kt1);
             }
-            const float2 l2 = *reinterpret_cast<const float2*>(sm.lse[buf] + qc);
-            const float2 d2 = *reinterpret_cast<const float2*>(sm.dsum[buf] + qc);
-            const float lv[4] = {l2.x * kLog2e, l2.y * kLog2e, l2.x * kLog2e, l2.y * kLog2e};
-            const float dvv[4] = {d2.x, d2.y, d2.x, d2.y};
+            const float4 ld4 = *reinterpret_cast<const float4*>(sm.lsd[buf] + qc);  // rows qc, qc+1
+            const float lv[4] = {ld4.x, ld4.z, ld4.x, ld4.z};
+            const float dvv[4] = {ld4.y, ld4.w, ld4.y, ld4.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const float pr_ = ex2_fast(fmaf(sT[nt][e], scale2, b[e]) - lv[e]);

@@ -3,10 +3,12 @@
 # burn the box), then the full GPU suite, the bench line and a launch list.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
+if [ -z "$SKIP_TESTS" ]; then
 timeout 300 python -m pytest tests/test_attention_gpu.py -x -q > gpurun_out/pytest_attn.log 2>&1; echo "attn tests rc=$?"
 tail -5 gpurun_out/pytest_attn.log
 timeout 600 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "gpu tests rc=$?"
 tail -3 gpurun_out/pytest_gpu.log
+fi
 timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 tail -1 gpurun_out/bench.json; tail -3 gpurun_out/bench.err
 if [ "${NCU:-1}" = 1 ]; then

@@ -1,6 +1,6 @@
 """Maps an ncu SASS source-page CSV onto CUDA source lines (nvdisasm -g line info).
 usage: ncu_lines.py <ncu source csv> <cubin> <mangled kernel> [kernel-index]"""
-import csv, re, subprocess, sys
+import csv, os, re, subprocess, sys
 from collections import Counter
 csvf, cubin, kname = sys.argv[1:4]
 kidx = int(sys.argv[4]) if len(sys.argv) > 4 else 0
@@ -25,6 +25,11 @@ hdr = rows[hi]
 ia, ist = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
 base = None
 ci, cs = Counter(), Counter()
+# EXTRA="L1 Wavefronts Shared,L1 Wavefronts Shared Excessive": also sum these
+# columns per line and rank by the first of them
+extra = [c for c in os.environ.get("EXTRA", "").split(",") if c]
+ix = [hdr.index(c) for c in extra]
+ce = [Counter() for _ in extra]
 for r in rows[hi + 1:end]:
     try:
         a = int(r[0], 16); n = float(r[ia] or 0); s = float(r[ist] or 0)
@@ -33,6 +38,11 @@ for r in rows[hi + 1:end]:
     base = a if base is None else base
     k = a2l.get(a - base, "?")
     ci[k] += n; cs[k] += s
+    for c, j in zip(ce, ix):
+        try:
+            c[k] += float(r[j] or 0)
+        except ValueError:
+            pass
 tot, ts = sum(ci.values()), sum(cs.values())
 import os
 srcdir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2602_16249_b200", "csrc")
@@ -42,6 +52,15 @@ for k in list(ci):
     if f not in src and os.path.exists(os.path.join(srcdir, f)):
         src[f] = open(os.path.join(srcdir, f)).read().split("\n")
 print(f"total warp-instructions {tot/1e6:.2f}M")
+if extra:
+    te = [sum(c.values()) or 1 for c in ce]
+    print("extra totals:", ", ".join(f"{n}={t/1e6:.2f}M" for n, t in zip(extra, te)))
+    for k, _ in sorted(ce[0].items(), key=lambda kv: -kv[1])[:int(os.environ.get("TOP", 30))]:
+        f, l = (k.split(":") + ["0"])[:2]
+        text = src[f][int(l) - 1].strip()[:60] if f in src else ""
+        vals = " ".join(f"{100*c[k]/t:5.1f}%" for c, t in zip(ce, te))
+        print(f"{vals} {k}: {text}")
+    sys.exit(0)
 for k, v in sorted(ci.items(), key=lambda kv: -(kv[1] / tot + cs[kv[0]] / ts))[:int(os.environ.get("TOP", 30))]:
     f, l = (k.split(":") + ["0"])[:2]
     text = src[f][int(l) - 1].strip()[:70] if f in src else ""
