@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(256) pool_fwd_v2_kernel(
 }
 
 template <int CPR, int KMAX>
-__global__ void __launch_bounds__(256) pool_bwd_v2_kernel(
+__global__ void __launch_bounds__(256, KMAX <= 8 ? 3 : 1) pool_bwd_v2_kernel(
     const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
     const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
     const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,

@@ -149,48 +149,96 @@ inline int radix_sort(uint64_t*& keys, uint32_t*& vals, uint64_t* keys_alt, uint
     return AFFMAE_OK;
 }
 
-// ----------------------------------------------------- segmented CTA sort
-// Segments of <= kSegSortMax keys (one image's tokens) sort inside one CTA's
-// shared memory: stable LSD passes over the LOW 32 bits of the keys, only for
-// the key bytes that vary within the segment (OR ^ AND of the keys), values =
-// segment-local indices (every call site sorts (key, local index) pairs).
-// Each of the 16 warps owns a contiguous element range walked in rounds of
-// 32 in element order, so the per-(warp, digit) offsets give a stable order.
+// ----------------------------------------------------- segmented sort
+// Segments of <= kSegSortMax keys (one image's tokens) sort in shared memory:
+// stable LSD passes over the LOW 32 bits of the keys, only for the key bytes
+// that vary within the segment (OR ^ AND of the keys), values = segment-local
+// indices (every call site sorts (key, local index) pairs).  Each warp owns a
+// contiguous element range walked in rounds of 32 in element order, so the
+// per-(warp, digit) offsets give a stable order.
 constexpr int kSegSortMax = 16384;
 constexpr int kSegWarps = 32;
 
-template <bool WRITE_VALS>
-__global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t* __restrict__ kin, int64_t seglen,
-                                                                  uint64_t* __restrict__ kout,
-                                                                  uint32_t* __restrict__ vout) {
+// One segment is spread over a thread-block
+// cluster of CL CTAs (distributed shared memory): CTA r holds slice
+// [r*S, (r+1)*S) of the segment.  Per 8-bit pass every CTA counts its digits
+// per warp, publishes its digit totals, reads the other CTAs' totals over
+// DSMEM to place its (digit, rank, warp) runs, and scatters keys straight into
+// the owning CTA's next-pass buffer (st.shared::cluster).  Order is
+// (digit, CTA rank, warp, element) -> stable.  With 32-64 segments (one per
+// image or axis) this puts 128-256 CTAs on the 148 SMs instead of 32-64.
+template <int CL>
+struct SegClusterSmem {
+    uint32_t ctot[256];   // this CTA's per-digit totals (read by the cluster)
+    uint32_t tot[256];
+    uint32_t red[2][kSegWarps];
+    uint32_t vary[2];     // this CTA's OR / AND of its keys (read by the cluster)
+};
+inline int seg_slice(int64_t seglen, int cl) { return int((seglen + cl - 1) / cl); }
+inline size_t seg_sort_cl_smem(int64_t seglen, int cl) {
+    const int64_t Sp = (seg_slice(seglen, cl) + 31) & ~31;
+    return size_t(Sp) * (4 + 4 + 2 + 2) + size_t(kSegWarps) * 256 * 4;
+}
+
+__device__ __forceinline__ uint32_t dsmem_map(const void* p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ uint32_t dsmem_ld32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void dsmem_st32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st16(uint32_t addr, uint16_t v) {
+    asm volatile("st.shared::cluster.u16 [%0], %1;\n" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ int cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return int(r);
+}
+
+template <bool WRITE_VALS, int CL>
+__global__ void __launch_bounds__(kSegWarps * 32) seg_sort_cl_kernel(const uint64_t* __restrict__ kin,
+                                                                     int64_t seglen, uint64_t* __restrict__ kout,
+                                                                     uint32_t* __restrict__ vout) {
     extern __shared__ __align__(16) uint8_t sraw[];
-    const int L = int(seglen);
-    const int Lp = (L + 31) & ~31;
+    __shared__ SegClusterSmem<CL> cs;
+    const int rank = cluster_rank();
+    const int64_t seg = blockIdx.x / CL;
+    const int L = int(seglen), S = (L + CL - 1) / CL;
+    const int s0 = min(rank * S, L), n = min(s0 + S, L) - s0;
+    const int Sp = (S + 31) & ~31;
     uint32_t* ka = reinterpret_cast<uint32_t*>(sraw);
-    uint32_t* kb = ka + Lp;
-    uint16_t* va = reinterpret_cast<uint16_t*>(kb + Lp);
-    uint16_t* vb = va + Lp;
-    uint32_t* off = reinterpret_cast<uint32_t*>(vb + Lp);  // [kSegWarps][256]
-    __shared__ uint32_t tot[256];
-    __shared__ uint32_t red[2][kSegWarps];
+    uint32_t* kb = ka + Sp;
+    uint16_t* va = reinterpret_cast<uint16_t*>(kb + Sp);
+    uint16_t* vb = va + Sp;
+    uint32_t* off = reinterpret_cast<uint32_t*>(vb + Sp);  // [kSegWarps][256]
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const uint64_t* src = kin + int64_t(blockIdx.x) * seglen;
+    const uint64_t* src = kin + seg * seglen + s0;
     uint32_t o = 0, a = 0xffffffffu;
-    constexpr int U = 8;  // loads in flight per thread
-    for (int i0 = t; i0 < L; i0 += U * kSegWarps * 32) {
+    constexpr int U = 4;
+    for (int i0 = t; i0 < n; i0 += U * kSegWarps * 32) {
         uint32_t k[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = i0 + u * kSegWarps * 32;
-            k[u] = i < L ? uint32_t(__ldg(src + i)) : 0u;
+            k[u] = i < n ? uint32_t(__ldg(src + i)) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = i0 + u * kSegWarps * 32;
-            if (i < L) {
+            if (i < n) {
                 ka[i] = k[u];
-                va[i] = uint16_t(i);
+                va[i] = uint16_t(s0 + i);
                 o |= k[u];
                 a &= k[u];
             }
@@ -199,27 +247,40 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t
     o = __reduce_or_sync(0xffffffffu, o);
     a = __reduce_and_sync(0xffffffffu, a);
     if (lane == 0) {
-        red[0][warp] = o;
-        red[1][warp] = a;
+        cs.red[0][warp] = o;
+        cs.red[1][warp] = a;
     }
     __syncthreads();
-    uint32_t vary = 0;
-    {
+    if (t == 0) {
         uint32_t oo = 0, aa = 0xffffffffu;
         for (int w = 0; w < kSegWarps; ++w) {
-            oo |= red[0][w];
-            aa &= red[1][w];
+            oo |= cs.red[0][w];
+            aa &= cs.red[1][w];
+        }
+        cs.vary[0] = oo;
+        cs.vary[1] = aa;
+    }
+    cluster_sync_all();
+    uint32_t vary;
+    {
+        uint32_t oo = 0, aa = 0xffffffffu;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+            oo |= dsmem_ld32(dsmem_map(&cs.vary[0], r));
+            aa &= dsmem_ld32(dsmem_map(&cs.vary[1], r));
         }
         vary = oo ^ aa;
     }
-    const int per = ((Lp / 32 + kSegWarps - 1) / kSegWarps) * 32;  // elements per warp (multiple of 32)
-    const int w0 = warp * per, w1 = min(w0 + per, L);
+    // no CTA may leave (or rewrite) while a peer still reads its shared memory:
+    // with constant keys no pass (and no later cluster barrier) follows
+    cluster_sync_all();
+    const int per = ((Sp / 32 + kSegWarps - 1) / kSegWarps) * 32;
+    const int w0 = warp * per, w1 = min(w0 + per, n);
     for (int shift = 0; shift < 32; shift += 8) {
-        if (((vary >> shift) & 0xFFu) == 0) continue;  // uniform across the CTA
+        if (((vary >> shift) & 0xFFu) == 0) continue;  // uniform across the cluster
         for (int i = t; i < kSegWarps * 256; i += blockDim.x) off[i] = 0;
         __syncthreads();
-        // 1. per-warp digit counts
-        for (int b = w0; b < w1 + 0; b += 32) {
+        for (int b = w0; b < w1; b += 32) {
             const int i = b + lane;
             const int d = i < w1 ? int((ka[i] >> shift) & 0xFF) : 256;
             const unsigned peers = __match_any_sync(0xffffffffu, d);
@@ -227,7 +288,6 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t
             __syncwarp();
         }
         __syncthreads();
-        // 2. offsets in (digit, warp) order
         if (t < 256) {
             uint32_t s = 0;
             for (int w = 0; w < kSegWarps; ++w) {
@@ -235,14 +295,26 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t
                 off[w * 256 + t] = s;
                 s += c;
             }
-            tot[t] = s;
+            cs.ctot[t] = s;
+        }
+        cluster_sync_all();  // every CTA's digit totals published
+        uint32_t before = 0;
+        if (t < 256) {
+            uint32_t all = 0;
+#pragma unroll
+            for (int r = 0; r < CL; ++r) {
+                const uint32_t v = r == rank ? cs.ctot[t] : dsmem_ld32(dsmem_map(&cs.ctot[t], r));
+                all += v;
+                before += r < rank ? v : 0u;
+            }
+            cs.tot[t] = all;
         }
         __syncthreads();
-        if (t < 32) {  // exclusive scan of the 256 digit totals by one warp
+        if (t < 32) {  // exclusive scan of the 256 cluster-wide digit totals
             uint32_t v[8], run = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                v[j] = tot[t * 8 + j];
+                v[j] = cs.tot[t * 8 + j];
                 run += v[j];
             }
             uint32_t inc = run;
@@ -254,14 +326,15 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t
             uint32_t base = inc - run;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                tot[t * 8 + j] = base;
+                cs.tot[t * 8 + j] = base;
                 base += v[j];
             }
         }
         __syncthreads();
-        for (int i = t; i < kSegWarps * 256; i += blockDim.x) off[i] += tot[i & 255];
+        if (t < 256) cs.tot[t] += before;
         __syncthreads();
-        // 3. stable scatter
+        for (int i = t; i < kSegWarps * 256; i += blockDim.x) off[i] += cs.tot[i & 255];
+        __syncthreads();
         for (int b = w0; b < w1; b += 32) {
             const int i = b + lane;
             const bool ok = i < w1;
@@ -273,13 +346,14 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t
             __syncwarp();
             if (ok) {
                 const uint32_t pos = base + __popc(peers & lt);
-                kb[pos] = k;
-                vb[pos] = va[i];
+                const int dr = int(pos / uint32_t(S)), dl = int(pos - uint32_t(dr) * uint32_t(S));
+                dsmem_st32(dsmem_map(kb + dl, dr), k);
+                dsmem_st16(dsmem_map(vb + dl, dr), va[i]);
                 if (__popc(peers & lt) == 0) off[warp * 256 + d] = base + __popc(peers);
             }
             __syncwarp();
         }
-        __syncthreads();
+        cluster_sync_all();  // all scatters landed; ctot may be rewritten
         uint32_t* tk = ka;
         ka = kb;
         kb = tk;
@@ -287,18 +361,60 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_kernel(const uint64_t
         va = vb;
         vb = tv;
     }
-    const uint64_t hi = src[0] & 0xffffffff00000000ull;
-    uint64_t* dk = kout + int64_t(blockIdx.x) * seglen;
-    for (int i = t; i < L; i += blockDim.x) {
+    const uint64_t hi = kin[seg * seglen] & 0xffffffff00000000ull;
+    uint64_t* dk = kout + seg * seglen + s0;
+    for (int i = t; i < n; i += blockDim.x) {
         dk[i] = hi | ka[i];
-        if (WRITE_VALS) vout[int64_t(blockIdx.x) * seglen + i] = va[i];
+        if (WRITE_VALS) vout[seg * seglen + s0 + i] = va[i];
     }
 }
 
-inline size_t seg_sort_smem(int64_t seglen) {
-    const int64_t Lp = (seglen + 31) & ~int64_t(31);
-    return size_t(Lp) * (4 + 4 + 2 + 2) + size_t(kSegWarps) * 256 * 4;
+template <bool WRITE_VALS, int CL>
+inline int launch_seg_sort_cl(const uint64_t* kin, int64_t nseg, int64_t seglen, uint64_t* kout, uint32_t* vout,
+                              cudaStream_t st) {
+    auto kern = seg_sort_cl_kernel<WRITE_VALS, CL>;
+    const size_t smem = seg_sort_cl_smem(seglen, CL);
+    static bool attr = false;
+    if (!attr) {
+        AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(seg_sort_cl_smem(kSegSortMax, 1))));
+        AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(nseg * CL));
+    cfg.blockDim = dim3(kSegWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    AFFMAE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, kin, seglen, kout, vout));
+    return AFFMAE_OK;
 }
+
+// CTAs per segment: at most one wave of CTAs on the SMs, slices >= 1024 keys.
+inline int seg_cluster_size(int64_t nseg, int64_t seglen) {
+    int cl = 1;
+    while (cl < 8 && nseg * cl * 2 <= kNumSMs && seglen / (cl * 2) >= 1024) cl *= 2;
+    return cl;
+}
+
+template <bool WRITE_VALS>
+inline int launch_seg_sort(const uint64_t* kin, int64_t nseg, int64_t seglen, uint64_t* kout, uint32_t* vout,
+                           cudaStream_t st) {
+    switch (seg_cluster_size(nseg, seglen)) {
+        case 8: return launch_seg_sort_cl<WRITE_VALS, 8>(kin, nseg, seglen, kout, vout, st);
+        case 4: return launch_seg_sort_cl<WRITE_VALS, 4>(kin, nseg, seglen, kout, vout, st);
+        case 2: return launch_seg_sort_cl<WRITE_VALS, 2>(kin, nseg, seglen, kout, vout, st);
+        default: return launch_seg_sort_cl<WRITE_VALS, 1>(kin, nseg, seglen, kout, vout, st);
+    }
+}
+
 
 // Sorts nseg contiguous segments of seglen keys (key = seg << 32 | low 32 bits,
 // values = segment-local indices) stably by the low bits.  On return
@@ -308,25 +424,10 @@ inline int segmented_sort(uint64_t*& keys, uint32_t*& vals, uint64_t* keys_alt, 
     if (nseg <= 0 || seglen <= 0) return AFFMAE_OK;
     if (seglen > kSegSortMax || seglen > 65536)
         return radix_sort(keys, vals, keys_alt, vals_alt, nseg * seglen, end_bit, hist, st);
-    const size_t smem = seg_sort_smem(seglen);
-    if (vals) {
-        static bool attr = false;
-        if (!attr) {
-            AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(seg_sort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(seg_sort_smem(kSegSortMax))));
-            attr = true;
-        }
-        seg_sort_kernel<true><<<unsigned(nseg), kSegWarps * 32, smem, st>>>(keys, seglen, keys_alt, vals_alt);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(seg_sort_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(seg_sort_smem(kSegSortMax))));
-            attr = true;
-        }
-        seg_sort_kernel<false><<<unsigned(nseg), kSegWarps * 32, smem, st>>>(keys, seglen, keys_alt, nullptr);
-    }
-    AFFMAE_LAUNCH_CHECK("seg_sort_kernel");
+    const int rc = vals ? launch_seg_sort<true>(keys, nseg, seglen, keys_alt, vals_alt, st)
+                        : launch_seg_sort<false>(keys, nseg, seglen, keys_alt, nullptr, st);
+    if (rc) return rc;
+    AFFMAE_LAUNCH_CHECK("seg_sort_cl_kernel");
     uint64_t* tk = keys;
     keys = keys_alt;
     keys_alt = tk;

@@ -26,6 +26,10 @@ CASES = [
     ("tiny_fewer_clusters", lambda rng: random_coords(2, 10, 10.0, rng), 8, 3),
     ("coarse_grid_ties", lambda rng: (np.floor(random_coords(2, 500, 20.0, rng)) * 2.0).astype(np.float32), 16, 3),
     ("negative_coords", lambda rng: random_coords(2, 300, 100.0, rng) - 50.0, 16, 3),
+    # large segments: the sort splits each image over a CTA cluster; constant
+    # keys run no radix pass at all (a CTA must not leave while peers read it)
+    ("constant_large", lambda rng: np.full((2, 8192, 2), 5.0, np.float32), 16, 3),
+    ("random_large", lambda rng: random_coords(2, 12000, 300.0, rng), 16, 3),
 ]
 
 
