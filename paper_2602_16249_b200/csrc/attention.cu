@@ -377,7 +377,8 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
             const int v = lane == kPQlen ? qlen : lane == kPFast ? int(fast) : lane == kPFirst ? int(pr == rb)
                         : lane == kPLast ? int(pr == re - 1) : lane == kPItem ? int(item)
                         : lane == kPIdx ? int(int64_t(img) * pairs + pr)
-                        : lane == kPQItem ? int(int64_t(img) * cs.c + qc) : 0;
+                        : lane == kPQItem ? int(int64_t(img) * cs.c + qc)
+                        : lane == kPImgTok ? int(img_tok) : 0;
             po[PRec::HDR + lane] = v;
         }
     }

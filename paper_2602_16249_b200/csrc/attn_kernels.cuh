@@ -66,14 +66,14 @@ struct KRec {
     static constexpr int KTOK = 0, KCELL = 16, KPCELL = 32, HDR = 48, WORDS = 56;
 };
 // Reverse pair record (CSR order of rev_cl):
-//   qtok[16] qcell[16] hdr{qlen, class, first, last, key item, global pair index, query item}
+//   qtok[16] qcell[16] hdr{qlen, class, first, last, key item, global pair index, query item, image * N}
 // Record classes (hdr kHFast / kPFast): 1 lattice-fast (window cells iy*kWs+ix),
 // 2 medium (one phase, offsets within the global table: packed cells
 // (iy+2048)<<16 | (ix+2048)), 0 general (coordinates).
 struct PRec {
     static constexpr int QTOK = 0, QCELL = 16, HDR = 32, WORDS = 40;
 };
-enum { kPQlen = 0, kPFast = 1, kPFirst = 2, kPLast = 3, kPItem = 4, kPIdx = 5, kPQItem = 6 };
+enum { kPQlen = 0, kPFast = 1, kPFirst = 2, kPLast = 3, kPItem = 4, kPIdx = 5, kPQItem = 6, kPImgTok = 7 };
 constexpr int kWinC = kRs * kWs + kRs;  // window index of offset (0, 0)
 constexpr int kMG = 4 * kMaxHidden + 1;  // tier-3 MLP grad accumulator per head
 constexpr int kTabReplicas = 4;          // global tier-2 gradient table copies (spread atomics)
@@ -118,9 +118,9 @@ struct AttnParams {
 __host__ __device__ constexpr int part_width(int hd) { return kWs2 + kMG + 2 * hd + 1; }
 
 // ---------------------------------------------------------------- helpers
-// Token offset (image * N) of a reverse-pair round's key cluster (key record hdr[4]).
+// Token offset (image * N) of a reverse-pair round.
 __device__ __forceinline__ int item_tok(const int32_t* round_rec, const AttnParams&) {
-    return round_rec[PRec::WORDS + KRec::HDR + 4];
+    return round_rec[PRec::HDR + kPImgTok];
 }
 // Zero a shared-memory range (16-byte granules) with the warp.
 __device__ __forceinline__ void zero_shared(void* base, size_t bytes) {
@@ -257,6 +257,24 @@ __device__ __forceinline__ void sw_rows_to_global(__nv_bfloat16* g, uint32_t row
         const int r = sub + j * RPI;
         if (r < nrows)
             *reinterpret_cast<uint4*>(base + uint32_t(tok[r]) * rowbytes) =
+                *reinterpret_cast<const uint4*>(sm + S::at(r, ch));
+    }
+}
+// The same with the lane's row tokens already in registers (tk[j] = token of
+// row lane / CPR + j * RPI).
+template <int HD>
+__device__ __forceinline__ void sw_rows_to_global_t(__nv_bfloat16* g, uint32_t rowbytes, const __nv_bfloat16* sm,
+                                                    const int (&tk)[16 / (32 / Swz<HD>::CPR)], int nrows,
+                                                    int lane) {
+    using S = Swz<HD>;
+    constexpr int CPR = S::CPR, RPI = 32 / CPR;
+    const int sub = lane / CPR, ch = lane - sub * CPR;
+    char* base = reinterpret_cast<char*>(g) + ch * 16;
+#pragma unroll
+    for (int j = 0; j < 16 / RPI; ++j) {
+        const int r = sub + j * RPI;
+        if (r < nrows)
+            *reinterpret_cast<uint4*>(base + uint32_t(tk[j]) * rowbytes) =
                 *reinterpret_cast<const uint4*>(sm + S::at(r, ch));
     }
 }
@@ -982,18 +1000,20 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
     auto first_pair = [&](int item) -> int {
         return item < n_items ? __ldg(p.krec + size_t(item) * KRec::WORDS + KRec::HDR + 3) : -1;
     };
-    auto copy_round = [&](int pair, int item, int32_t* dst) {
+    // the key record only rides along with the first round of its cluster
+    auto copy_round = [&](int pair, int item, bool with_krec, int32_t* dst) {
         if (pair < 0) return;
         copy_rec<PRec::WORDS>(dst, p.prec + size_t(pair) * PRec::WORDS, lane);
-        copy_rec<KRec::WORDS>(dst + KR, p.krec + size_t(item) * KRec::WORDS, lane);
+        if (with_krec) copy_rec<KRec::WORDS>(dst + KR, p.krec + size_t(item) * KRec::WORDS, lane);
     };
     // Round after the round whose record is `rec` (landed): the next pair of the
     // same key cluster, else the first pair of the cluster `stride` further on
     // (nx_first, prefetched one cluster ahead).
     int nx_first = -1;
-    auto advance = [&](const int32_t* rec, int& item) -> int {
+    auto advance = [&](const int32_t* rec, int& item, bool& newc) -> int {
         item = rec[PRec::HDR + kPItem];
-        if (!rec[PRec::HDR + kPLast]) return rec[PRec::HDR + kPIdx] + 1;
+        newc = rec[PRec::HDR + kPLast] != 0;
+        if (!newc) return rec[PRec::HDR + kPIdx] + 1;
         const int r = nx_first;
         item += stride;
         nx_first = first_pair(item + stride);
@@ -1016,18 +1036,21 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
     // prologue: records of rounds 0 and 1, rows of round 0
     int pr0 = first_pair(blockIdx.x), it1 = 0;
     nx_first = first_pair(blockIdx.x + stride);
-    copy_round(pr0, blockIdx.x, sm.rec[0]);
+    copy_round(pr0, blockIdx.x, true, sm.rec[0]);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
-    int pr1 = pr0 >= 0 ? advance(sm.rec[0], it1) : -1;
-    copy_round(pr1, it1, sm.rec[1]);
+    bool nc1 = false;
+    int pr1 = pr0 >= 0 ? advance(sm.rec[0], it1, nc1) : -1;
+    copy_round(pr1, it1, nc1, sm.rec[1]);
     if (pr0 >= 0) issue_rows(0, sm.rec[0]);
     cp_async_commit();
 
     uint32_t ka[HD / 16][4], va[HD / 16][4];
     float dk[HD / 8][4], dv[HD / 8][4];
-    int kq0 = 0, kq1 = 0, kt0 = 0, kt1 = 0, kp0 = 0, kp1 = 0;
+    int kq0 = 0, kq1 = 0, kt0 = 0, kt1 = 0, kp0 = 0, kp1 = 0, klen = 0;
+    constexpr int SRPI = 32 / Swz<HD>::CPR;  // rows per dK/dV store instruction
+    int stok[16 / SRPI];                      // key tokens of the lane's store rows
     const float* tabg_h = p.tab_g + size_t(h) * kWg2;
     int rc = 0;
     for (int it = 0; pr0 >= 0; ++it) {
@@ -1046,7 +1069,9 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
             for (int nd = 0; nd < HD / 8; ++nd)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) dk[nd][e] = dv[nd][e] = 0.f;
-            const int klen = krec[KRec::HDR];
+            klen = krec[KRec::HDR];
+#pragma unroll
+            for (int j = 0; j < 16 / SRPI; ++j) stok[j] = krec[KRec::KTOK + lane / Swz<HD>::CPR + j * SRPI];
             kq0 = krec[KRec::KCELL + r0] + kWinC;
             kq1 = krec[KRec::KCELL + r0 + 8] + kWinC;
             kt0 = krec[KRec::KTOK + (r0 < klen ? r0 : 0)];
@@ -1056,8 +1081,9 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
             __syncwarp();  // K, V consumed
         }
         int it2 = 0;
-        const int pr2 = pr1 >= 0 ? advance(sm.rec[r1], it2) : -1;
-        copy_round(pr2, it2, sm.rec[r2]);
+        bool nc2 = false;
+        const int pr2 = pr1 >= 0 ? advance(sm.rec[r1], it2, nc2) : -1;
+        copy_round(pr2, it2, nc2, sm.rec[r2]);
         if (pr1 >= 0) issue_rows(buf ^ 1, sm.rec[r1]);
         cp_async_commit();
 
@@ -1126,9 +1152,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
             sw_frags_to_rows<HD>(sm.dK, dk, p.scale, p.scale, lane);
             sw_frags_to_rows<HD>(sm.dV, dv, 1.f, 1.f, lane);
             __syncwarp();
-            const int klen = krec[KRec::HDR];
-            sw_rows_to_global<HD>(p.dk + img_tok * ld + h * HD, rowb, sm.dK, krec + KRec::KTOK, klen, lane);
-            sw_rows_to_global<HD>(p.dv + img_tok * ld + h * HD, rowb, sm.dV, krec + KRec::KTOK, klen, lane);
+            sw_rows_to_global_t<HD>(p.dk + img_tok * ld + h * HD, rowb, sm.dK, stok, klen, lane);
+            sw_rows_to_global_t<HD>(p.dv + img_tok * ld + h * HD, rowb, sm.dV, stok, klen, lane);
             __syncwarp();
         }
         pr0 = pr1;
