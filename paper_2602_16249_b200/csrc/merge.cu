@@ -592,10 +592,7 @@ __global__ void dp_reduce_kernel(const float* __restrict__ part, int nparts, flo
 }
 
 // ------------------------------------------- vectorised pool kernels (dim % 8 == 0)
-// A row of D bf16 is CPR = D/8 16-byte chunks; LPR lanes share a row (one or
-// more chunks each), RPW = 32/LPR rows per warp.  The pool's weights are
-// computed redundantly by the row's lanes (broadcast loads), and every pool
-// member's chunk is loaded before it is used (memory-level parallelism).
+// A row of D bf16 is CPR = D/8 16-byte chunks (MergePoolOp, merging.cpp:121-220).
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
@@ -613,224 +610,9 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float (&f)[8]) {
     return v;
 }
 
-template <int KMAX>
-__device__ __forceinline__ int pool_row_weights(const int32_t* pool_idx, const double* pool_dist,
-                                                const int32_t* pool_cnt, int64_t row, int k_m, float p,
-                                                int (&jj)[KMAX], float (&w)[KMAX], float (&dd)[KMAX]) {
-    // all loads independent of cnt (the pool arrays hold k_m slots per row): one round trip
-    int ji[KMAX];
-    double di[KMAX];
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) {
-        ji[t] = t < k_m ? __ldg(pool_idx + row * k_m + t) : 0;
-        di[t] = t < k_m ? __ldg(pool_dist + row * k_m + t) : 0.0;
-    }
-    const int cnt = __ldg(pool_cnt + row);
-    float m = -INFINITY;
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) {
-        jj[t] = t < cnt ? ji[t] : 0;
-        dd[t] = t < cnt ? float(di[t]) : 0.f;
-        if (t < cnt) m = fmaxf(m, -p * dd[t]);
-    }
-    float l = 0.f;
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) {
-        w[t] = t < cnt ? __expf(-p * dd[t] - m) : 0.f;
-        l += w[t];
-    }
-    const float il = cnt > 0 ? 1.f / l : 0.f;
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) w[t] *= il;
-    return cnt;
-}
-
-// Pool indices / distances / count of one row: loaded one row ahead (registers).
-template <int KMAX>
-struct PoolRowIdx {
-    int ji[KMAX];
-    double di[KMAX];
-    int cnt, rt;
-    __device__ __forceinline__ void load(const int32_t* pool_idx, const double* pool_dist, const int32_t* pool_cnt,
-                                         const int32_t* retained, int64_t row, int k_m, bool ok) {
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) {
-            ji[t] = ok && t < k_m ? __ldg(pool_idx + row * k_m + t) : 0;
-            di[t] = ok && t < k_m ? __ldg(pool_dist + row * k_m + t) : 0.0;
-        }
-        cnt = ok ? __ldg(pool_cnt + row) : 0;
-        rt = ok ? __ldg(retained + row) : 0;
-    }
-    // softmax(-p * dist) weights (merging.cpp:121-149)
-    __device__ __forceinline__ void weights(float p, int (&jj)[KMAX], float (&w)[KMAX], float (&dd)[KMAX]) const {
-        float m = -INFINITY;
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) {
-            jj[t] = t < cnt ? ji[t] : 0;
-            dd[t] = t < cnt ? float(di[t]) : 0.f;
-            if (t < cnt) m = fmaxf(m, -p * dd[t]);
-        }
-        float l = 0.f;
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) {
-            w[t] = t < cnt ? __expf(-p * dd[t] - m) : 0.f;
-            l += w[t];
-        }
-        const float il = cnt > 0 ? 1.f / l : 0.f;
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) w[t] *= il;
-    }
-};
-
-// Persistent: each row group (LPR lanes) walks rows g, g + G, ... ; the next
-// row's indices are loaded while the current row's gathers are in flight.
-template <int CPR, int KMAX>
-__global__ void __launch_bounds__(256) pool_fwd_v2_kernel(
-    const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
-    const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
-    const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
-    int64_t r, int k_m, __nv_bfloat16* __restrict__ out) {
-    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR, CPL = CPR / LPR;
-    constexpr int D = CPR * 8;
-    const int lane = threadIdx.x & 31, sl = lane % LPR;
-    const int64_t groups = int64_t(gridDim.x) * (blockDim.x >> 5) * RPW;
-    const int64_t total = batch * r;
-    int64_t row = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPW + lane / LPR;
-    const float p = *p_merge;
-    PoolRowIdx<KMAX> cur;
-    cur.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, row < total);
-    for (; row < total; row += groups) {
-        const int64_t b = row / r;
-        int jj[KMAX];
-        float w[KMAX], dd[KMAX];
-        cur.weights(p, jj, w, dd);
-        const int cnt = cur.cnt;
-        const int64_t rt = cur.rt;
-        const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * D);
-        const float* sb = scores + b * n;
-        float sj[KMAX];
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t) sj[t] = t < cnt ? __ldg(sb + jj[t]) : 0.f;
-        uint4 v[CPL][KMAX], own[CPL];
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const int ch = sl + cc * LPR;
-#pragma unroll
-            for (int t = 0; t < KMAX; ++t)
-                if (t < cnt) v[cc][t] = __ldg(fb + int64_t(jj[t]) * CPR + ch);
-            own[cc] = __ldg(fb + rt * CPR + ch);
-        }
-        const int64_t nxt = row + groups;
-        cur.load(pool_idx, pool_dist, pool_cnt, retained, nxt, k_m, nxt < total);  // overlaps the gathers
-        uint4* o = reinterpret_cast<uint4*>(out + row * 2 * D);
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const int ch = sl + cc * LPR;
-            o[ch] = own[cc];
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int t = 0; t < KMAX; ++t) {
-                if (t < cnt) {
-                    float f[8];
-                    bf16x8_to_f32(v[cc][t], f);
-                    const float g = w[t] * sj[t];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[i] = fmaf(g, f[i], acc[i]);
-                }
-            }
-            o[CPR + ch] = f32_to_bf16x8(acc);
-        }
-    }
-}
-
-template <int CPR, int KMAX>
-__global__ void __launch_bounds__(256, KMAX <= 8 ? 3 : 1) pool_bwd_v2_kernel(
-    const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
-    const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
-    const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
-    int64_t r, int k_m, const __nv_bfloat16* __restrict__ dout, __nv_bfloat16* __restrict__ dfeats,
-    float* __restrict__ dscores, float* __restrict__ dp_part) {
-    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR, CPL = CPR / LPR;
-    const int lane = threadIdx.x & 31, sl = lane % LPR;
-    const int64_t row = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * RPW + lane / LPR;
-    const bool valid = row < batch * r;
-    float dp = 0.f;
-    const int64_t rw = valid ? row : 0;
-    const int64_t b = rw / r;
-    int jj[KMAX];
-    float w[KMAX], dd[KMAX], sj[KMAX], dot[KMAX];
-    const int cnt = valid ? pool_row_weights<KMAX>(pool_idx, pool_dist, pool_cnt, rw, k_m, *p_merge, jj, w, dd) : 0;
-    const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * CPR * 8);
-    uint4* dfb = reinterpret_cast<uint4*>(dfeats + b * n * CPR * 8);
-    const uint4* gr = reinterpret_cast<const uint4*>(dout + rw * 2 * CPR * 8);
-    const float* sb = scores + b * n;
-    float* dsb = dscores + b * n;
-    const int64_t rt = valid ? retained[rw] : 0;
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) {
-        sj[t] = t < cnt ? sb[jj[t]] : 0.f;
-        dot[t] = 0.f;
-    }
-    if (valid) {
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const int ch = sl + cc * LPR;
-            uint4 v[KMAX];
-#pragma unroll
-            for (int t = 0; t < KMAX; ++t)
-                if (t < cnt) v[t] = __ldg(fb + int64_t(jj[t]) * CPR + ch);
-            dfb[rt * CPR + ch] = __ldg(gr + ch);
-            float go[8];
-            bf16x8_to_f32(__ldg(gr + CPR + ch), go);
-#pragma unroll
-            for (int t = 0; t < KMAX; ++t) {
-                if (t < cnt) {
-                    float f[8], df[8];
-                    bf16x8_to_f32(v[t], f);
-                    const float k = w[t] * sj[t];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        dot[t] = fmaf(go[i], f[i], dot[t]);
-                        df[i] = go[i] * k;
-                    }
-                    dfb[int64_t(jj[t]) * CPR + ch] = f32_to_bf16x8(df);
-                }
-            }
-        }
-    }
-    // row-group reduction of the dots (LPR lanes; every lane participates)
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t)
-#pragma unroll
-        for (int o = LPR / 2; o > 0; o >>= 1) dot[t] += __shfl_xor_sync(0xffffffffu, dot[t], o);
-    if (valid && sl == 0) {
-        dsb[rt] = 0.f;
-        float wdot = 0.f;
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t)
-            if (t < cnt) {
-                dsb[jj[t]] = w[t] * dot[t];
-                wdot = fmaf(w[t], sj[t] * dot[t], wdot);
-            }
-#pragma unroll
-        for (int t = 0; t < KMAX; ++t)
-            if (t < cnt) dp = fmaf(w[t] * (sj[t] * dot[t] - wdot), -dd[t], dp);
-    }
-    // block partial of dp (fixed order)
-    __shared__ float red[8];
-    dp = warp_sum(dp);
-    if (lane == 0) red[threadIdx.x >> 5] = dp;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float s = 0.f;
-        for (int i = 0; i < int(blockDim.x >> 5); ++i) s += red[i];
-        dp_part[blockIdx.x] = s;
-    }
-}
-
 // tokens that feed no output row (truncated pool members): zero gradient (thread per token)
 template <int CPR>
-__global__ void pool_bwd_zero_v2_kernel(const int32_t* __restrict__ row_of, int64_t total,
+__global__ void pool_bwd_zero_vec_kernel(const int32_t* __restrict__ row_of, int64_t total,
                                         __nv_bfloat16* __restrict__ dfeats, float* __restrict__ dscores) {
     const int64_t tok = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tok >= total || row_of[tok] >= 0) return;
@@ -839,47 +621,388 @@ __global__ void pool_bwd_zero_v2_kernel(const int32_t* __restrict__ row_of, int6
     dscores[tok] = 0.f;
 }
 
+// ------------------------------------------- staged pool kernels (persistent)
+// Each warp walks rounds of RPW retained rows (LPR lanes per row, CPL 16-byte
+// chunks per lane).  Round i+1's member rows (and the pool metadata: member
+// ids, softmax weights, distances, member scores) are gathered by cp.async
+// into a per-warp two-stage shared-memory ring while round i computes, and the
+// pool indices of round i+2 load into registers one round earlier still -- so
+// the in-flight data lives in shared memory, not in registers, and every warp
+// keeps two rounds of gathers in flight.  Same arithmetic, same order as the
+// v2 kernels (the results are bit-identical).
+template <int CPR>
+struct PoolGeo {
+    static constexpr int LPR = CPR < 16 ? CPR : 16;  // lanes per row
+    static constexpr int RPW = 32 / LPR;             // rows per warp round
+    static constexpr int CPL = CPR / LPR;            // chunks per lane
+    static constexpr int WARPS = CPR <= 16 ? 8 : CPR == 32 ? 4 : 2;
+};
+template <int KMAX>
+struct PoolMeta {  // per staged row
+    int32_t jj[KMAX];
+    float w[KMAX], dd[KMAX], sj[KMAX];
+    int32_t cnt, rt, pad[2];
+};
+template <int CPR, int KMAX, int LEAD>  // LEAD: chunks staged before the members (fwd 1 own row, bwd 2 grad halves)
+struct PoolRing {
+    static constexpr int SROW = (LEAD + KMAX) * CPR;  // uint4 chunks per staged row
+    static constexpr size_t kRowBytes = size_t(SROW) * 16 + sizeof(PoolMeta<KMAX>);
+    static constexpr size_t kWarpBytes = 2 * PoolGeo<CPR>::RPW * kRowBytes;
+    static constexpr size_t kBytes = PoolGeo<CPR>::WARPS * kWarpBytes;
+};
+
+// Pool indices of one row spread over its LPR lanes: lane sl holds members
+// sl, sl + LPR, ... (MPL per lane); loaded one round ahead of their gathers.
+template <int CPR, int KMAX>
+struct PoolLaneIdx {
+    static constexpr int LPR = PoolGeo<CPR>::LPR, MPL = (KMAX + LPR - 1) / LPR;
+    int j[MPL];
+    double d[MPL];
+    int cnt, rt;
+    __device__ __forceinline__ void load(const int32_t* pool_idx, const double* pool_dist, const int32_t* pool_cnt,
+                                         const int32_t* retained, int64_t row, int k_m, bool ok, int sl) {
+#pragma unroll
+        for (int i = 0; i < MPL; ++i) {
+            const int t = sl + i * LPR;
+            const bool v = ok && t < k_m;
+            j[i] = v ? __ldg(pool_idx + row * k_m + t) : 0;
+            d[i] = v ? __ldg(pool_dist + row * k_m + t) : 0.0;
+        }
+        cnt = ok ? __ldg(pool_cnt + row) : 0;
+        rt = ok ? __ldg(retained + row) : 0;
+    }
+};
+
+// Issue the gathers of one row into a stage slot: LEAD chunks from `lead_src`
+// (16-byte chunk pointer of the row's own data), member chunks (zero-filled
+// past the row's count, up to the warp's largest count `tmax`), metadata.
+// softmax(-p * dist) weights as merging.cpp:121-149: max, exp, sum in member
+// order, normalise (the same operation order as the per-thread form).
+template <int CPR, int KMAX, int LEAD>
+__device__ __forceinline__ void pool_issue_row(uint8_t* slot, const PoolLaneIdx<CPR, KMAX>& ix, float p, bool ok,
+                                               int tmax, const uint4* lead_src, const uint4* fb, const float* sb,
+                                               int lane) {
+    using G = PoolGeo<CPR>;
+    using Rg = PoolRing<CPR, KMAX, LEAD>;
+    constexpr int MPL = PoolLaneIdx<CPR, KMAX>::MPL;
+    const int sl = lane % G::LPR, base = lane - sl;
+    uint4* ch16 = reinterpret_cast<uint4*>(slot);
+    PoolMeta<KMAX>* m = reinterpret_cast<PoolMeta<KMAX>*>(slot + size_t(Rg::SROW) * 16);
+    const int cnt = ok ? ix.cnt : 0;
+    float e[MPL], dd[MPL];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
+        const int t = sl + i * G::LPR;
+        dd[i] = t < cnt ? float(ix.d[i]) : 0.f;
+        if (t < cnt) mx = fmaxf(mx, -p * dd[i]);
+    }
+#pragma unroll
+    for (int o = G::LPR / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) e[i] = (sl + i * G::LPR) < cnt ? __expf(-p * dd[i] - mx) : 0.f;
+    float l = 0.f;  // sum in member order (every lane of the row gets the same value)
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) l += __shfl_sync(0xffffffffu, e[t / G::LPR], base + t % G::LPR);
+    const float il = cnt > 0 ? 1.f / l : 0.f;
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
+        const int t = sl + i * G::LPR;
+        if (t < KMAX) {
+            m->jj[t] = t < cnt ? ix.j[i] : 0;
+            m->w[t] = e[i] * il;
+            m->dd[t] = dd[i];
+            if (t < cnt) cp_async4(&m->sj[t], sb + ix.j[i]);
+            else m->sj[t] = 0.f;
+        }
+    }
+    if (sl == 0) {
+        m->cnt = ok ? cnt : -1;
+        m->rt = ix.rt;
+    }
+    if (ok) {
+#pragma unroll
+        for (int cc = 0; cc < G::CPL; ++cc) {
+            const int ch = sl + cc * G::LPR;
+#pragma unroll
+            for (int l2 = 0; l2 < LEAD; ++l2) cp_async16(ch16 + l2 * CPR + ch, lead_src + l2 * CPR + ch);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) {
+        if (t >= tmax) break;  // warp-uniform
+        const int jt = __shfl_sync(0xffffffffu, ix.j[t / G::LPR], base + t % G::LPR);
+        const uint32_t nb = t < cnt ? 16u : 0u;
+#pragma unroll
+        for (int cc = 0; cc < G::CPL; ++cc) {
+            const int ch = sl + cc * G::LPR;
+            cp_async16_zfill(ch16 + (LEAD + t) * CPR + ch, fb + int64_t(nb ? jt : 0) * CPR + ch, nb);
+        }
+    }
+}
+
+template <int CPR, int KMAX>
+__global__ void __launch_bounds__(PoolGeo<CPR>::WARPS * 32) pool_fwd_v3_kernel(
+    const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
+    const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
+    const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
+    int64_t r, int k_m, __nv_bfloat16* __restrict__ out) {
+    using G = PoolGeo<CPR>;
+    using Rg = PoolRing<CPR, KMAX, 1>;
+    extern __shared__ __align__(16) uint8_t pool_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / G::LPR, sl = lane % G::LPR;
+    uint8_t* ring = pool_smem + size_t(warp) * Rg::kWarpBytes;
+    const int64_t total = batch * r;
+    const int64_t GW = int64_t(gridDim.x) * G::WARPS;
+    const float p = *p_merge;
+    auto slot_of = [&](int stage) { return ring + size_t(stage * G::RPW + sub) * Rg::kRowBytes; };
+    auto issue = [&](int64_t rd, int stage, const PoolLaneIdx<CPR, KMAX>& ix) {
+        const int64_t row = rd * G::RPW + sub;
+        const bool ok = row < total;
+        const int64_t b = ok ? row / r : 0;
+        const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * CPR * 8);
+        const int tmax = __reduce_max_sync(0xffffffffu, ok ? ix.cnt : 0);
+        pool_issue_row<CPR, KMAX, 1>(slot_of(stage), ix, p, ok, tmax, fb + int64_t(ix.rt) * CPR, fb,
+                                     scores + b * n, lane);
+    };
+    int64_t rd = int64_t(blockIdx.x) * G::WARPS + warp;
+    const int64_t nrounds = (total + G::RPW - 1) / G::RPW;
+    PoolLaneIdx<CPR, KMAX> ix;
+    {
+        const int64_t row = rd * G::RPW + sub;
+        ix.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, rd < nrounds && row < total, sl);
+    }
+    if (rd < nrounds) issue(rd, 0, ix);
+    cp_async_commit();
+    {
+        const int64_t row = (rd + GW) * G::RPW + sub;
+        ix.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, rd + GW < nrounds && row < total, sl);
+    }
+    for (int k = 0; rd < nrounds; ++k, rd += GW) {
+        const int cur = k & 1;
+        if (rd + GW < nrounds) issue(rd + GW, cur ^ 1, ix);
+        cp_async_commit();
+        {
+            const int64_t row = (rd + 2 * GW) * G::RPW + sub;
+            ix.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, rd + 2 * GW < nrounds && row < total, sl);
+        }
+        cp_async_wait<1>();
+        __syncwarp();
+        const uint8_t* slot = slot_of(cur);
+        const uint4* src = reinterpret_cast<const uint4*>(slot);
+        const PoolMeta<KMAX>* m = reinterpret_cast<const PoolMeta<KMAX>*>(slot + size_t(Rg::SROW) * 16);
+        const int cnt = m->cnt;
+        const int tmax = __reduce_max_sync(0xffffffffu, cnt);
+        {
+            const int64_t row = rd * G::RPW + sub;
+            uint4* o = reinterpret_cast<uint4*>(out + (cnt >= 0 ? row : 0) * 2 * CPR * 8);
+#pragma unroll
+            for (int cc = 0; cc < G::CPL; ++cc) {
+                const int ch = sl + cc * G::LPR;
+                float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) {
+                    if (t >= tmax) break;  // warp-uniform; members past the row's count are zero-filled
+                    const float g = t < cnt ? m->w[t] * m->sj[t] : 0.f;
+                    float f[8];
+                    bf16x8_to_f32(src[(1 + t) * CPR + ch], f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = fmaf(g, f[i], acc[i]);
+                }
+                if (cnt >= 0) {
+                    o[ch] = src[ch];
+                    o[CPR + ch] = f32_to_bf16x8(acc);
+                }
+            }
+        }
+        __syncwarp();  // slot `cur` is reissued next round
+    }
+    cp_async_wait<0>();
+}
+
+template <int CPR, int KMAX>
+__global__ void __launch_bounds__(PoolGeo<CPR>::WARPS * 32) pool_bwd_v3_kernel(
+    const __nv_bfloat16* __restrict__ feats, const float* __restrict__ scores, const float* __restrict__ p_merge,
+    const int32_t* __restrict__ retained, const int32_t* __restrict__ pool_idx,
+    const double* __restrict__ pool_dist, const int32_t* __restrict__ pool_cnt, int64_t batch, int64_t n,
+    int64_t r, int k_m, const __nv_bfloat16* __restrict__ dout, __nv_bfloat16* __restrict__ dfeats,
+    float* __restrict__ dscores, float* __restrict__ dp_part) {
+    using G = PoolGeo<CPR>;
+    using Rg = PoolRing<CPR, KMAX, 2>;
+    extern __shared__ __align__(16) uint8_t pool_smem[];
+    __shared__ float red[G::WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane / G::LPR, sl = lane % G::LPR;
+    uint8_t* ring = pool_smem + size_t(warp) * Rg::kWarpBytes;
+    const int64_t total = batch * r;
+    const int64_t GW = int64_t(gridDim.x) * G::WARPS;
+    const float p = *p_merge;
+    auto slot_of = [&](int stage) { return ring + size_t(stage * G::RPW + sub) * Rg::kRowBytes; };
+    auto issue = [&](int64_t rd, int stage, const PoolLaneIdx<CPR, KMAX>& ix) {
+        const int64_t row = rd * G::RPW + sub;
+        const bool ok = row < total;
+        const int64_t b = ok ? row / r : 0;
+        const uint4* fb = reinterpret_cast<const uint4*>(feats + b * n * CPR * 8);
+        const uint4* gr = reinterpret_cast<const uint4*>(dout + (ok ? row : 0) * 2 * CPR * 8);
+        const int tmax = __reduce_max_sync(0xffffffffu, ok ? ix.cnt : 0);
+        pool_issue_row<CPR, KMAX, 2>(slot_of(stage), ix, p, ok, tmax, gr, fb, scores + b * n, lane);
+    };
+    float dp = 0.f;
+    int64_t rd = int64_t(blockIdx.x) * G::WARPS + warp;
+    const int64_t nrounds = (total + G::RPW - 1) / G::RPW;
+    PoolLaneIdx<CPR, KMAX> ix;
+    {
+        const int64_t row = rd * G::RPW + sub;
+        ix.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, rd < nrounds && row < total, sl);
+    }
+    if (rd < nrounds) issue(rd, 0, ix);
+    cp_async_commit();
+    {
+        const int64_t row = (rd + GW) * G::RPW + sub;
+        ix.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, rd + GW < nrounds && row < total, sl);
+    }
+    for (int k = 0; rd < nrounds; ++k, rd += GW) {
+        const int cur = k & 1;
+        if (rd + GW < nrounds) issue(rd + GW, cur ^ 1, ix);
+        cp_async_commit();
+        {
+            const int64_t row = (rd + 2 * GW) * G::RPW + sub;
+            ix.load(pool_idx, pool_dist, pool_cnt, retained, row, k_m, rd + 2 * GW < nrounds && row < total, sl);
+        }
+        cp_async_wait<1>();
+        __syncwarp();
+        const uint8_t* slot = slot_of(cur);
+        const uint4* src = reinterpret_cast<const uint4*>(slot);
+        const PoolMeta<KMAX>* m = reinterpret_cast<const PoolMeta<KMAX>*>(slot + size_t(Rg::SROW) * 16);
+        const int cnt = m->cnt;
+        const bool valid = cnt >= 0;
+        const int64_t row = rd * G::RPW + sub;
+        const int64_t b = valid ? row / r : 0;
+        uint4* dfb = reinterpret_cast<uint4*>(dfeats + b * n * CPR * 8);
+        float dot[KMAX];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) dot[t] = 0.f;
+        const int tmax = __reduce_max_sync(0xffffffffu, cnt);
+        {
+            const int64_t rt = valid ? m->rt : 0;
+#pragma unroll
+            for (int cc = 0; cc < G::CPL; ++cc) {
+                const int ch = sl + cc * G::LPR;
+                if (valid) dfb[rt * CPR + ch] = src[ch];
+                float go[8];
+                bf16x8_to_f32(src[CPR + ch], go);
+#pragma unroll
+                for (int t = 0; t < KMAX; ++t) {
+                    if (t >= tmax) break;  // warp-uniform; members past the row's count are zero-filled
+                    const float kt = t < cnt ? m->w[t] * m->sj[t] : 0.f;
+                    float f[8], df[8];
+                    bf16x8_to_f32(src[(2 + t) * CPR + ch], f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        dot[t] = fmaf(go[i], f[i], dot[t]);
+                        df[i] = go[i] * kt;
+                    }
+                    if (t < cnt) dfb[int64_t(m->jj[t]) * CPR + ch] = f32_to_bf16x8(df);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t)
+#pragma unroll
+            for (int o = G::LPR / 2; o > 0; o >>= 1) dot[t] += __shfl_xor_sync(0xffffffffu, dot[t], o);
+        if (valid && sl == 0) {
+            float* dsb = dscores + b * n;
+            dsb[m->rt] = 0.f;
+            float wdot = 0.f;
+#pragma unroll
+            for (int t = 0; t < KMAX; ++t)
+                if (t < cnt) {
+                    dsb[m->jj[t]] = m->w[t] * dot[t];
+                    wdot = fmaf(m->w[t], m->sj[t] * dot[t], wdot);
+                }
+#pragma unroll
+            for (int t = 0; t < KMAX; ++t)
+                if (t < cnt) dp = fmaf(m->w[t] * (m->sj[t] * dot[t] - wdot), -m->dd[t], dp);
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+    dp = warp_sum(dp);
+    if (lane == 0) red[warp] = dp;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.f;
+        for (int i = 0; i < G::WARPS; ++i) s += red[i];
+        dp_part[blockIdx.x] = s;
+    }
+}
+
+// persistent grid: resident blocks per SM x SMs (never more blocks than rounds)
+template <typename K>
+static int pool_v3_grid(K kern, size_t smem, int warps, int64_t rounds, unsigned& nb) {
+    static_assert(sizeof(K) > 0, "");
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return fail(AFFMAE_ECUDA, std::string("pool: ") + cudaGetErrorString(e));
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem);
+    if (occ < 1) return fail(AFFMAE_EUNSUPPORTED, "pool: kernel does not fit on an SM");
+    const int64_t want = (rounds + warps - 1) / warps;
+    nb = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(occ) * kNumSMs)));
+    return AFFMAE_OK;
+}
+
+template <int CPR, int KMAX>
+static int launch_pool_fwd_v3(const __nv_bfloat16* feats, const float* scores, const float* p_merge,
+                              const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
+                              int64_t r, int k_m, __nv_bfloat16* out, cudaStream_t st) {
+    using G = PoolGeo<CPR>;
+    auto kern = pool_fwd_v3_kernel<CPR, KMAX>;
+    const size_t smem = PoolRing<CPR, KMAX, 1>::kBytes;
+    unsigned nb = 0;
+    int rc = pool_v3_grid(kern, smem, G::WARPS, (batch * r + G::RPW - 1) / G::RPW, nb);
+    if (rc) return rc;
+    kern<<<nb, G::WARPS * 32, smem, st>>>(feats, scores, p_merge, retained, plan->pool_idx, plan->pool_dist,
+                                          plan->pool_cnt, batch, n, r, k_m, out);
+    AFFMAE_LAUNCH_CHECK("pool_fwd_v3_kernel");
+    return AFFMAE_OK;
+}
 template <int CPR>
 static int launch_pool_fwd_v2(const __nv_bfloat16* feats, const float* scores, const float* p_merge,
                               const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
                               int64_t r, int k_m, __nv_bfloat16* out, cudaStream_t st) {
-    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR;
-    const int64_t warps = (batch * r + RPW - 1) / RPW;
-    const unsigned nb = unsigned(std::min<int64_t>((warps + 7) / 8, int64_t(kNumSMs) * 8));
-    if (k_m <= 8)
-        pool_fwd_v2_kernel<CPR, 8><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
-                                                        plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, out);
-    else
-        pool_fwd_v2_kernel<CPR, 16><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
-                                                         plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, out);
-    AFFMAE_LAUNCH_CHECK("pool_fwd_v2_kernel");
-    return AFFMAE_OK;
+    return k_m <= 8 ? launch_pool_fwd_v3<CPR, 8>(feats, scores, p_merge, retained, plan, batch, n, r, k_m, out, st)
+                    : launch_pool_fwd_v3<CPR, 16>(feats, scores, p_merge, retained, plan, batch, n, r, k_m, out, st);
 }
-template <int CPR>
-static unsigned pool_bwd_v2_blocks(int64_t batch, int64_t r) {
-    constexpr int LPR = CPR < 32 ? CPR : 32, RPW = 32 / LPR;
-    const int64_t warps = (batch * r + RPW - 1) / RPW;
-    return unsigned((warps + 7) / 8);
+template <int CPR, int KMAX>
+static int launch_pool_bwd_v3(const __nv_bfloat16* feats, const float* scores, const float* p_merge,
+                              const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
+                              int64_t r, int k_m, const __nv_bfloat16* dout, __nv_bfloat16* dfeats,
+                              float* dscores, float* part, cudaStream_t st, unsigned& nb) {
+    using G = PoolGeo<CPR>;
+    auto kern = pool_bwd_v3_kernel<CPR, KMAX>;
+    const size_t smem = PoolRing<CPR, KMAX, 2>::kBytes;
+    int rc = pool_v3_grid(kern, smem, G::WARPS, (batch * r + G::RPW - 1) / G::RPW, nb);
+    if (rc) return rc;
+    kern<<<nb, G::WARPS * 32, smem, st>>>(feats, scores, p_merge, retained, plan->pool_idx, plan->pool_dist,
+                                          plan->pool_cnt, batch, n, r, k_m, dout, dfeats, dscores, part);
+    AFFMAE_LAUNCH_CHECK("pool_bwd_v3_kernel");
+    return AFFMAE_OK;
 }
 template <int CPR>
 static int launch_pool_bwd_v2(const __nv_bfloat16* feats, const float* scores, const float* p_merge,
                               const int32_t* retained, const affmae_merge_plan* plan, int64_t batch, int64_t n,
                               int64_t r, int k_m, const __nv_bfloat16* dout, __nv_bfloat16* dfeats,
                               float* dscores, float* part, cudaStream_t st, unsigned& nb) {
-    nb = pool_bwd_v2_blocks<CPR>(batch, r);
-    pool_bwd_zero_v2_kernel<CPR><<<unsigned((batch * n + 255) / 256), 256, 0, st>>>(plan->row_of, batch * n,
+    pool_bwd_zero_vec_kernel<CPR><<<unsigned((batch * n + 255) / 256), 256, 0, st>>>(plan->row_of, batch * n,
                                                                                     dfeats, dscores);
-    AFFMAE_LAUNCH_CHECK("pool_bwd_zero_v2_kernel");
-    if (k_m <= 8)
-        pool_bwd_v2_kernel<CPR, 8><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
-                                                        plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, dout,
-                                                        dfeats, dscores, part);
-    else
-        pool_bwd_v2_kernel<CPR, 16><<<nb, 256, 0, st>>>(feats, scores, p_merge, retained, plan->pool_idx,
-                                                         plan->pool_dist, plan->pool_cnt, batch, n, r, k_m, dout,
-                                                         dfeats, dscores, part);
-    AFFMAE_LAUNCH_CHECK("pool_bwd_v2_kernel");
-    return AFFMAE_OK;
+    AFFMAE_LAUNCH_CHECK("pool_bwd_zero_vec_kernel");
+    return k_m <= 8 ? launch_pool_bwd_v3<CPR, 8>(feats, scores, p_merge, retained, plan, batch, n, r, k_m, dout,
+                                                 dfeats, dscores, part, st, nb)
+                    : launch_pool_bwd_v3<CPR, 16>(feats, scores, p_merge, retained, plan, batch, n, r, k_m, dout,
+                                                  dfeats, dscores, part, st, nb);
 }
 
 // ===================================================================== host
