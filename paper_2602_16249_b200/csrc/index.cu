@@ -173,12 +173,24 @@ __device__ __forceinline__ bool pair_lt(double da, int ja, double db, int jb) {
 }
 
 // Merges per-lane sorted top-G lists into the warp's top-G (ascending (d, j)).
+// Register-only: the lane's list head is selected with unrolled compares.
 template <int G>
 __device__ __forceinline__ void warp_topk(double (&d)[G], int (&j)[G], int g, double* outd, int* outj) {
     int head = 0;
-    for (int r = 0; r < g; ++r) {
-        double bd = head < g ? d[head] : INFINITY;
-        int bj = head < g ? j[head] : INT32_MAX;
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        if (r >= g) break;
+        double md = INFINITY;
+        int mj = INT32_MAX;
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+            if (q == head && q < g) {
+                md = d[q];
+                mj = j[q];
+            }
+        double bd = md;
+        int bj = mj;
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             double od = __shfl_xor_sync(0xffffffffu, bd, o);
             int oj = __shfl_xor_sync(0xffffffffu, bj, o);
@@ -187,7 +199,7 @@ __device__ __forceinline__ void warp_topk(double (&d)[G], int (&j)[G], int g, do
                 bj = oj;
             }
         }
-        if (head < g && d[head] == bd && j[head] == bj) ++head;
+        if (head < g && md == bd && mj == bj) ++head;
         outd[r] = bd;
         outj[r] = bj;
     }
