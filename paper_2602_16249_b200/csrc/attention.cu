@@ -765,19 +765,24 @@ static int dispatch_fwd(const AttnParams& p, int head_dim, int64_t width, cudaSt
 #undef AFFMAE_CASE
     return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
 }
-static int dispatch_bwd(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st, int* gx) {
+static int dispatch_bwd_q(const AttnParams& p, int head_dim, int64_t width, cudaStream_t st, int* gx) {
     const int kp = pick_kp(width);
-#define AFFMAE_CASE(HD_, KP_)                                  \
-    if (head_dim == HD_ && kp == KP_) {                        \
-        int rc = launch_bwd_q<HD_, KP_>(p, st, gx);            \
-        return rc ? rc : launch_bwd_kv<HD_>(p, st);            \
-    }
+#define AFFMAE_CASE(HD_, KP_) \
+    if (head_dim == HD_ && kp == KP_) return launch_bwd_q<HD_, KP_>(p, st, gx);
     AFFMAE_CASE_HD(16)
     AFFMAE_CASE_HD(32)
     AFFMAE_CASE_HD(64)
 #undef AFFMAE_CASE
 #undef AFFMAE_CASE_HD
     return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
+}
+static int dispatch_bwd_kv(const AttnParams& p, int head_dim, cudaStream_t st) {
+    switch (head_dim) {
+        case 16: return launch_bwd_kv<16>(p, st);
+        case 32: return launch_bwd_kv<32>(p, st);
+        case 64: return launch_bwd_kv<64>(p, st);
+        default: return fail(AFFMAE_EUNSUPPORTED, "attention: no compiled kernel variant");
+    }
 }
 
 size_t attn_fwd_workspace(const affmae_cluster_geom* g, const affmae_attn_desc* a) {
@@ -865,30 +870,30 @@ static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, cons
     dtab_zero_kernel<<<4 * kNumSMs, 256, 0, st>>>(w.dtab_g, a->heads, w.rmax);
     AFFMAE_LAUNCH_CHECK("dtab_zero_kernel");
     int gx[2] = {0, 0};
-    if ((rc = dispatch_bwd(p, a->head_dim, g->width, st, gx))) return rc;
-    const int pw = part_width(a->head_dim);
-    attn_part_reduce_kernel<<<dim3((pw + 31) / 32, a->heads), 256, 0, st>>>(
-        w.part, gx[0], gx[1], a->heads, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
-    AFFMAE_LAUNCH_CHECK("attn_part_reduce_kernel");
-    {
-        dtab_replica_sum_kernel<<<2 * kNumSMs, 256, 0, st>>>(w.dtab_g, a->heads, w.rmax);
+    if ((rc = dispatch_bwd_q(p, a->head_dim, g->width, st, gx))) return rc;
+    // The parameter-gradient chain needs only the query side's partials: it runs on
+    // the forked side stream while the key-side kernel (dK, dV) runs on `st`.
+    auto param_grads = [&](cudaStream_t s) -> int {
+        const int pw = part_width(a->head_dim);
+        attn_part_reduce_kernel<<<dim3((pw + 31) / 32, a->heads), 256, 0, s>>>(
+            w.part, gx[0], gx[1], a->heads, a->head_dim, a->bias_hidden, w.dtab_g, w.mlp_grad, w.blank_grad);
+        AFFMAE_LAUNCH_CHECK("attn_part_reduce_kernel");
+        dtab_replica_sum_kernel<<<2 * kNumSMs, 256, 0, s>>>(w.dtab_g, a->heads, w.rmax);
         AFFMAE_LAUNCH_CHECK("dtab_replica_sum_kernel");
-    }
-    {
         const int nblk = kFinBlocks;
-        bias_grad_partial_kernel<<<dim3(nblk, a->heads), 256, 0, st>>>(w.dtab_g, in->w1, in->b1, in->w2,
-                                                                       a->bias_hidden, w.rmax, w.fpart);
+        bias_grad_partial_kernel<<<dim3(nblk, a->heads), 256, 0, s>>>(w.dtab_g, in->w1, in->b1, in->w2,
+                                                                     a->bias_hidden, w.rmax, w.fpart);
         AFFMAE_LAUNCH_CHECK("bias_grad_partial_kernel");
-        bias_grad_final_kernel<<<dim3(a->heads, 4 * a->bias_hidden + 1), 32, 0, st>>>(
+        bias_grad_final_kernel<<<dim3(a->heads, 4 * a->bias_hidden + 1), 32, 0, s>>>(
             w.fpart, nblk, a->bias_hidden, gr->dw1, gr->db1, gr->dw2, gr->db2);
         AFFMAE_LAUNCH_CHECK("bias_grad_final_kernel");
-    }
-    attn_grad_epilogue_kernel<<<a->heads, 64, 0, st>>>(w.mlp_grad, w.blank_grad, a->heads,
-                                                       a->bias_hidden, a->head_dim, gr->dw1,
-                                                       gr->db1, gr->dw2, gr->db2, gr->dblank_k,
-                                                       gr->dblank_v, gr->dblank);
-    AFFMAE_LAUNCH_CHECK("attn_grad_epilogue_kernel");
-    return AFFMAE_OK;
+        attn_grad_epilogue_kernel<<<a->heads, 64, 0, s>>>(w.mlp_grad, w.blank_grad, a->heads, a->bias_hidden,
+                                                          a->head_dim, gr->dw1, gr->db1, gr->dw2, gr->db2,
+                                                          gr->dblank_k, gr->dblank_v, gr->dblank);
+        AFFMAE_LAUNCH_CHECK("attn_grad_epilogue_kernel");
+        return AFFMAE_OK;
+    };
+    return launch_forked(st, param_grads, [&](cudaStream_t s) { return dispatch_bwd_kv(p, a->head_dim, s); });
 }
 
 static int check_bwd_ptrs(const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
