@@ -141,7 +141,7 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = int64_t(blockIdx.x) * 4 + warp;
     if (item >= items) return;
-    const int img = int(item / cs.c), c = int(item - int64_t(img) * cs.c);
+    const int img = int(uint32_t(item) / uint32_t(cs.c)), c = int(item) - img * cs.c;  // items < 2^31
     const int64_t img_tok = int64_t(img) * cs.n;
     const int32_t* nb = nbr_cl + item * cs.g;
     int32_t* out = qrec + item * R::WORDS;
@@ -322,7 +322,7 @@ __global__ void attn_krec_kernel(const float* __restrict__ coords, const int32_t
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = int64_t(blockIdx.x) * 4 + warp;
     if (item >= items) return;
-    const int img = int(item / cs.c), ck = int(item - int64_t(img) * cs.c);
+    const int img = int(uint32_t(item) / uint32_t(cs.c)), ck = int(item) - img * cs.c;  // items < 2^31
     const int64_t img_tok = int64_t(img) * cs.n;
     const int64_t pairs = int64_t(cs.c) * cs.g;
     const int klen = cs.len(ck);
