@@ -30,6 +30,8 @@ CASES = [
     # keys run no radix pass at all (a CTA must not leave while peers read it)
     ("constant_large", lambda rng: np.full((2, 8192, 2), 5.0, np.float32), 16, 3),
     ("random_large", lambda rng: random_coords(2, 12000, 300.0, rng), 16, 3),
+    # 20 images: clusters of 4 CTAs for the Hilbert sort, of 2 for the axis sorts
+    ("batch20", lambda rng: random_coords(20, 5000, 200.0, rng), 16, 3),
 ]
 
 

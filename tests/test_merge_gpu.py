@@ -95,12 +95,26 @@ def test_merge_plan_bit_exact(case):
 @pytest.mark.parametrize("case", PLAN_CASES[:4], ids=[c[0] for c in PLAN_CASES[:4]])
 def test_merge_pool_fwd_bwd(case):
     """Values within bf16 tolerance of MergePoolOp (rel-L2 <= 1e-2)."""
+    _pool_case(case, 64)
+
+
+# every compiled row width of the staged pool kernels (16-byte chunks per row 8..64,
+# 8 or 16 pool slots) and a width that takes the scalar kernels
+POOL_DIMS = [(128, 8), (256, 8), (512, 8), (128, 12), (512, 16), (40, 8)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,k_m", POOL_DIMS, ids=[f"D{d}_km{k}" for d, k in POOL_DIMS])
+def test_merge_pool_dims(dim, k_m):
+    _pool_case(("random_dims", lambda rng: random_coords(2, 700, 60.0, rng), 0.3, k_m), dim)
+
+
+def _pool_case(case, D):
     import torch
     from paper_2602_16249_b200 import ops
     name, mk, d_s, k_m = case
     rng, coords, scores = _plan_problem(name, mk, d_s)
     B, N, _ = coords.shape
-    D = 64
     feats = bf16_round(rng.standard_normal((B, N, D)).astype(np.float32))
     p = 1.3
     ret = ops.select_retained(_dev(scores, torch.float32), d_s)
