@@ -20,10 +20,6 @@
 
 namespace affmae_b200 {
 
-__device__ __forceinline__ float float_unorder(uint32_t u) {
-    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
-}
-
 // hilbert_index, proj/src/geometry.cpp:15-30
 __device__ __forceinline__ uint64_t hilbert(uint32_t n, uint32_t x, uint32_t y) {
     uint64_t d = 0;
@@ -84,11 +80,10 @@ __device__ int ceil_log2_cr(double x) {
     return ((m - 1.0) * 1.4426950408889634 < 0.5 * u) ? e : e + 1;
 }
 
-__global__ void sfc_params_kernel(const uint64_t* __restrict__ sorted, int64_t batch, int64_t n,
-                                  const unsigned long long* __restrict__ gap_bits,
-                                  SfcParams* __restrict__ out) {
-    int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
+// sfc_order quantisation parameters of image b (geometry.cpp:87-101) from its
+// sorted axes and min gaps
+__device__ SfcParams sfc_params(const uint64_t* __restrict__ sorted, int64_t b, int64_t n,
+                                const unsigned long long* __restrict__ gap_bits) {
     SfcParams p{};
     const uint64_t* xs = sorted + (b * 2) * n;
     const uint64_t* ys = sorted + (b * 2 + 1) * n;
@@ -113,16 +108,19 @@ __global__ void sfc_params_kernel(const uint64_t* __restrict__ sorted, int64_t b
         p.side = 1u << bb;
         p.scale = __ddiv_rn(double(p.side - 1), extent);
     }
-    out[b] = p;
+    return p;
 }
 
+// Hilbert keys; every thread derives its image's parameters (a few broadcast
+// loads and binary64 ops) instead of a separate one-thread-per-image kernel.
 __global__ void hilbert_keys_kernel(const float* __restrict__ coords, int64_t batch, int64_t n,
-                                    const SfcParams* __restrict__ prm, uint64_t* __restrict__ keys,
+                                    const uint64_t* __restrict__ sorted_axes,
+                                    const unsigned long long* __restrict__ gap_bits, uint64_t* __restrict__ keys,
                                     uint32_t* __restrict__ vals) {
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= batch * n) return;
     int64_t b = i / n;
-    const SfcParams p = prm[b];
+    const SfcParams p = sfc_params(sorted_axes, b, n, gap_bits);
     uint64_t key = 0;
     if (p.side) {
         double x = coords[2 * i], y = coords[2 * i + 1];
@@ -146,23 +144,29 @@ __global__ void perm_kernel(const uint32_t* __restrict__ sorted_vals, int64_t ba
     if (cluster_of) cluster_of[b * cs.n + tok] = cs.cluster_at(pos);
 }
 
-// centroid = (sequential member-order sum) * (1.0 / |c|)   (geometry.cpp:140-150)
-__global__ void centroid_kernel(const float* __restrict__ coords, const int32_t* __restrict__ perm,
-                                int64_t batch, ClusterShape cs, double2* __restrict__ cent) {
-    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// perm + cluster_of + centroid in one pass, thread per cluster (the cluster's
+// centroid = (sequential member-order sum) * (1.0 / |c|), geometry.cpp:140-150;
+// curve positions are contiguous): the sorted token ids are read once.
+__global__ void perm_centroid_kernel(const uint32_t* __restrict__ sorted_vals, const float* __restrict__ coords,
+                                     int64_t batch, ClusterShape cs, int32_t* __restrict__ perm,
+                                     int32_t* __restrict__ cluster_of, double2* __restrict__ cent) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= batch * cs.c) return;
-    int64_t b = i / cs.c;
-    int k = int(i - b * cs.c);
-    const int32_t* pm = perm + b * cs.n + cs.off(k);
+    const int64_t b = i / cs.c;
+    const int k = int(i - b * cs.c);
+    const int64_t base = b * cs.n + cs.off(k);
     const float2* xy = reinterpret_cast<const float2*>(coords) + b * cs.n;
     double sx = 0.0, sy = 0.0;
-    int len = cs.len(k);
+    const int len = cs.len(k);
     for (int j = 0; j < len; ++j) {
-        float2 v = xy[pm[j]];
+        const int tok = int(sorted_vals[base + j]);
+        perm[base + j] = tok;
+        cluster_of[b * cs.n + tok] = k;
+        const float2 v = xy[tok];
         sx = __dadd_rn(sx, double(v.x));
         sy = __dadd_rn(sy, double(v.y));
     }
-    double inv = __ddiv_rn(1.0, double(len));
+    const double inv = __ddiv_rn(1.0, double(len));
     cent[i] = make_double2(__dmul_rn(sx, inv), __dmul_rn(sy, inv));
 }
 
@@ -459,6 +463,60 @@ __global__ void rev_sort_kernel(const int32_t* __restrict__ off, int64_t batch, 
     }
 }
 
+// Whole reverse CSR of one image in one CTA (shared-memory in-degree counts,
+// scan, atomic fill, per-list insertion sort) -- the four kernels above fused
+// for images whose counts fit in shared memory.
+__global__ void __launch_bounds__(1024) rev_csr_kernel(const int32_t* __restrict__ nbr_cl, ClusterShape cs,
+                                                       int32_t* __restrict__ rev_off, int32_t* __restrict__ rev_cl) {
+    extern __shared__ int32_t rsm[];
+    __shared__ int32_t part[1024];
+    const int C = cs.c, t = threadIdx.x, nt = blockDim.x;
+    int32_t* cnt = rsm;          // [C + 1] counts -> offsets
+    int32_t* cur = rsm + C + 1;  // [C] fill cursors
+    const int64_t per = int64_t(C) * cs.g;
+    const int32_t* nb = nbr_cl + blockIdx.x * per;
+    int32_t* off = rev_off + int64_t(blockIdx.x) * (C + 1);
+    int32_t* rl = rev_cl + blockIdx.x * per;
+    for (int i = t; i <= C; i += nt) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t i = t; i < per; i += nt) atomicAdd(&cnt[nb[i]], 1);
+    __syncthreads();
+    const int len = C + 1, chunk = (len + nt - 1) / nt, b0 = t * chunk, e0 = min(len, b0 + chunk);
+    int32_t sum = 0;
+    for (int i = b0; i < e0; ++i) sum += cnt[i];
+    part[t] = sum;
+    __syncthreads();
+    for (int o = 1; o < nt; o <<= 1) {
+        const int32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - sum;
+    for (int i = b0; i < e0; ++i) {
+        const int32_t v = cnt[i];
+        cnt[i] = run;
+        off[i] = run;
+        if (i < C) cur[i] = run;
+        run += v;
+    }
+    __syncthreads();
+    for (int64_t i = t; i < per; i += nt) rl[atomicAdd(&cur[nb[i]], 1)] = int(i / cs.g);
+    __syncthreads();
+    for (int c = t; c < C; c += nt) {  // ascending query clusters per list
+        const int lo = cnt[c], hi = cnt[c + 1];
+        for (int x = lo + 1; x < hi; ++x) {
+            const int v = rl[x];
+            int y = x;
+            while (y > lo && rl[y - 1] > v) {
+                rl[y] = rl[y - 1];
+                --y;
+            }
+            rl[y] = v;
+        }
+    }
+}
+
 // ------------------------------------------------------ NeighborIndex expand
 __global__ void expand_rows_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ nbr_cl,
                                    int64_t batch, ClusterShape cs, int32_t* __restrict__ idx,
@@ -537,7 +595,6 @@ struct IndexWs {
     uint32_t* vals[2];
     uint32_t* hist;
     unsigned long long* gaps;
-    SfcParams* prm;
     double2* cent;
     int32_t* cursor;
     size_t bytes;
@@ -559,7 +616,6 @@ static IndexWs carve(int64_t batch, int64_t n, int64_t c, void* base) {
     w.vals[1] = reinterpret_cast<uint32_t*>(take(e * 4));
     w.hist = reinterpret_cast<uint32_t*>(take(radix_hist_elems(int64_t(e)) * 4));
     w.gaps = reinterpret_cast<unsigned long long*>(take(size_t(batch) * 2 * 8));
-    w.prm = reinterpret_cast<SfcParams*>(take(size_t(batch) * sizeof(SfcParams)));
     w.cent = reinterpret_cast<double2*>(take(size_t(batch) * c * sizeof(double2)));
     w.cursor = reinterpret_cast<int32_t*>(take(size_t(batch) * (c + 1) * 4));
     w.bytes = off;
@@ -576,17 +632,20 @@ static int sfc_core(const float* coords, int64_t batch, int64_t n, IndexWs& w, u
     AFFMAE_LAUNCH_CHECK("axis_keys_kernel");
     uint64_t* k = w.keys[0];
     uint32_t* v = nullptr;
-    int rc = segmented_sort(k, v, w.keys[1], nullptr, batch * 2, n, 32 + bits_for(batch * 2), w.hist, st);
-    if (rc) return rc;
     AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.gaps, 0xFF, size_t(batch) * 2 * 8, st));
-    gap_kernel<<<blocks(e), 256, 0, st>>>(k, batch * 2, n, w.gaps);
-    sfc_params_kernel<<<blocks(batch, 128), 128, 0, st>>>(k, batch, n, w.gaps, w.prm);
-    AFFMAE_LAUNCH_CHECK("sfc_params_kernel");
-    hilbert_keys_kernel<<<blocks(batch * n), 256, 0, st>>>(coords, batch, n, w.prm, w.keys[0], w.vals[0]);
+    bool gaps_done = false;
+    int rc = segmented_sort(k, v, w.keys[1], nullptr, batch * 2, n, 32 + bits_for(batch * 2), w.hist, st,
+                            w.gaps, &gaps_done);
+    if (rc) return rc;
+    if (!gaps_done) gap_kernel<<<blocks(e), 256, 0, st>>>(k, batch * 2, n, w.gaps);
+    // the sorted axes live in w.keys[0] or w.keys[1]; the Hilbert keys go to the other buffer
+    uint64_t* hk = k == w.keys[0] ? w.keys[1] : w.keys[0];
+    hilbert_keys_kernel<<<blocks(batch * n), 256, 0, st>>>(coords, batch, n, k, w.gaps, hk, w.vals[0]);
     AFFMAE_LAUNCH_CHECK("hilbert_keys_kernel");
-    k = w.keys[0];
+    k = hk;
     v = w.vals[0];
-    rc = segmented_sort(k, v, w.keys[1], w.vals[1], batch, n, 32 + bits_for(batch), w.hist, st);
+    rc = segmented_sort(k, v, hk == w.keys[0] ? w.keys[1] : w.keys[0], w.vals[1], batch, n, 32 + bits_for(batch),
+                        w.hist, st);
     if (rc) return rc;
     *sorted_vals = v;
     return AFFMAE_OK;
@@ -614,21 +673,25 @@ int cluster_index_build(const affmae_cluster_geom* g, const float* coords, affma
     uint32_t* sv = nullptr;
     int rc = sfc_core(coords, B, n, w, &sv, st);
     if (rc) return rc;
-    perm_kernel<<<blocks(B * n), 256, 0, st>>>(sv, B, cs, out->perm, out->cluster_of);
-    centroid_kernel<<<blocks(B * cs.c), 256, 0, st>>>(coords, out->perm, B, cs, w.cent);
+    perm_centroid_kernel<<<blocks(B * cs.c), 256, 0, st>>>(sv, coords, B, cs, out->perm, out->cluster_of, w.cent);
     {
         const int rc = launch_nbr(w.cent, B, cs, out->nbr_cl, st);
         if (rc > 0) return rc;
         if (rc < 0) nbr_kernel<<<blocks(B * cs.c * 32), 256, 0, st>>>(w.cent, B, cs, out->nbr_cl);
     }
     AFFMAE_LAUNCH_CHECK("nbr_kernel");
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(out->rev_off, 0, size_t(B) * (cs.c + 1) * 4, st));
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.cursor, 0, size_t(B) * (cs.c + 1) * 4, st));
-    const int64_t pairs = B * cs.c * cs.g;
-    indeg_kernel<<<blocks(pairs), 256, 0, st>>>(out->nbr_cl, B, cs, out->rev_off);
-    rev_scan_kernel<<<unsigned(B), 1024, 0, st>>>(out->rev_off, cs);
-    rev_fill_kernel<<<blocks(pairs), 256, 0, st>>>(out->nbr_cl, B, cs, out->rev_off, w.cursor, out->rev_cl);
-    rev_sort_kernel<<<blocks(B * cs.c), 256, 0, st>>>(out->rev_off, B, cs, out->rev_cl);
+    const size_t rsmem = size_t(2 * cs.c + 1) * 4;
+    if (rsmem <= 48 * 1024) {
+        rev_csr_kernel<<<unsigned(B), 1024, rsmem, st>>>(out->nbr_cl, cs, out->rev_off, out->rev_cl);
+    } else {  // very large images: global-memory passes
+        AFFMAE_CUDA_CHECK(cudaMemsetAsync(out->rev_off, 0, size_t(B) * (cs.c + 1) * 4, st));
+        AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.cursor, 0, size_t(B) * (cs.c + 1) * 4, st));
+        const int64_t pairs = B * cs.c * cs.g;
+        indeg_kernel<<<blocks(pairs), 256, 0, st>>>(out->nbr_cl, B, cs, out->rev_off);
+        rev_scan_kernel<<<unsigned(B), 1024, 0, st>>>(out->rev_off, cs);
+        rev_fill_kernel<<<blocks(pairs), 256, 0, st>>>(out->nbr_cl, B, cs, out->rev_off, w.cursor, out->rev_cl);
+        rev_sort_kernel<<<blocks(B * cs.c), 256, 0, st>>>(out->rev_off, B, cs, out->rev_cl);
+    }
     AFFMAE_LAUNCH_CHECK("reverse CSR");
     return AFFMAE_OK;
 }

@@ -14,6 +14,17 @@
 
 namespace affmae_b200 {
 
+// inverse of float_order
+__device__ __forceinline__ float float_unorder(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// order-preserving float -> uint32 map (ascending)
+__device__ __forceinline__ uint32_t float_order(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 constexpr int kSortThreads = 256;
 constexpr int kSortRounds = 8;
 constexpr int kSortTile = kSortThreads * kSortRounds;  // 2048
@@ -205,10 +216,14 @@ __device__ __forceinline__ int cluster_rank() {
     return int(r);
 }
 
+// `gap_out` (optional, pre-set to ~0): per segment, the smallest positive
+// difference of consecutive sorted keys read as float_order'ed floats
+// (min_gap, proj/src/geometry.cpp:57-65), as binary64 bits.
 template <bool WRITE_VALS, int CL>
 __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_cl_kernel(const uint64_t* __restrict__ kin,
                                                                      int64_t seglen, uint64_t* __restrict__ kout,
-                                                                     uint32_t* __restrict__ vout) {
+                                                                     uint32_t* __restrict__ vout,
+                                                                     unsigned long long* __restrict__ gap_out) {
     extern __shared__ __align__(16) uint8_t sraw[];
     __shared__ SegClusterSmem<CL> cs;
     const int rank = cluster_rank();
@@ -361,6 +376,21 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_cl_kernel(const uint6
         va = vb;
         vb = tv;
     }
+    if (gap_out) {
+        // the previous slice's last key (DSMEM) closes the gap across the slice boundary
+        const uint32_t prev = (CL > 1 && rank > 0 && n > 0) ? dsmem_ld32(dsmem_map(ka + (S - 1), rank - 1)) : 0u;
+        unsigned long long best = ~0ull;
+        for (int i = t; i < n; i += blockDim.x) {
+            if (s0 + i == 0) continue;
+            const double a = double(float_unorder(i > 0 ? ka[i - 1] : prev)), b = double(float_unorder(ka[i]));
+            const double d = __dsub_rn(b, a);
+            if (d > 0.0) best = min(best, (unsigned long long)__double_as_longlong(d));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0 && best != ~0ull) atomicMin(gap_out + seg, best);
+        if (CL > 1) cluster_sync_all();  // peers have read our last key
+    }
     const uint64_t hi = kin[seg * seglen] & 0xffffffff00000000ull;
     uint64_t* dk = kout + seg * seglen + s0;
     for (int i = t; i < n; i += blockDim.x) {
@@ -371,7 +401,7 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_cl_kernel(const uint6
 
 template <bool WRITE_VALS, int CL>
 inline int launch_seg_sort_cl(const uint64_t* kin, int64_t nseg, int64_t seglen, uint64_t* kout, uint32_t* vout,
-                              cudaStream_t st) {
+                              unsigned long long* gap_out, cudaStream_t st) {
     auto kern = seg_sort_cl_kernel<WRITE_VALS, CL>;
     const size_t smem = seg_sort_cl_smem(seglen, CL);
     static bool attr = false;
@@ -393,7 +423,7 @@ inline int launch_seg_sort_cl(const uint64_t* kin, int64_t nseg, int64_t seglen,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    AFFMAE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, kin, seglen, kout, vout));
+    AFFMAE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, kin, seglen, kout, vout, gap_out));
     return AFFMAE_OK;
 }
 
@@ -406,26 +436,31 @@ inline int seg_cluster_size(int64_t nseg, int64_t seglen) {
 
 template <bool WRITE_VALS>
 inline int launch_seg_sort(const uint64_t* kin, int64_t nseg, int64_t seglen, uint64_t* kout, uint32_t* vout,
-                           cudaStream_t st) {
+                           unsigned long long* gap_out, cudaStream_t st) {
     switch (seg_cluster_size(nseg, seglen)) {
-        case 8: return launch_seg_sort_cl<WRITE_VALS, 8>(kin, nseg, seglen, kout, vout, st);
-        case 4: return launch_seg_sort_cl<WRITE_VALS, 4>(kin, nseg, seglen, kout, vout, st);
-        case 2: return launch_seg_sort_cl<WRITE_VALS, 2>(kin, nseg, seglen, kout, vout, st);
-        default: return launch_seg_sort_cl<WRITE_VALS, 1>(kin, nseg, seglen, kout, vout, st);
+        case 8: return launch_seg_sort_cl<WRITE_VALS, 8>(kin, nseg, seglen, kout, vout, gap_out, st);
+        case 4: return launch_seg_sort_cl<WRITE_VALS, 4>(kin, nseg, seglen, kout, vout, gap_out, st);
+        case 2: return launch_seg_sort_cl<WRITE_VALS, 2>(kin, nseg, seglen, kout, vout, gap_out, st);
+        default: return launch_seg_sort_cl<WRITE_VALS, 1>(kin, nseg, seglen, kout, vout, gap_out, st);
     }
 }
 
 
 // Sorts nseg contiguous segments of seglen keys (key = seg << 32 | low 32 bits,
 // values = segment-local indices) stably by the low bits.  On return
-// keys/vals point at the sorted data (vals only if non-null).
+// keys/vals point at the sorted data (vals only if non-null).  With `gap_out`
+// the shared-memory path also writes the per-segment min_gap and sets
+// *gaps_done; the global fallback leaves that to the caller.
 inline int segmented_sort(uint64_t*& keys, uint32_t*& vals, uint64_t* keys_alt, uint32_t* vals_alt,
-                          int64_t nseg, int64_t seglen, int end_bit, uint32_t* hist, cudaStream_t st) {
+                          int64_t nseg, int64_t seglen, int end_bit, uint32_t* hist, cudaStream_t st,
+                          unsigned long long* gap_out = nullptr, bool* gaps_done = nullptr) {
+    if (gaps_done) *gaps_done = false;
     if (nseg <= 0 || seglen <= 0) return AFFMAE_OK;
     if (seglen > kSegSortMax || seglen > 65536)
         return radix_sort(keys, vals, keys_alt, vals_alt, nseg * seglen, end_bit, hist, st);
-    const int rc = vals ? launch_seg_sort<true>(keys, nseg, seglen, keys_alt, vals_alt, st)
-                        : launch_seg_sort<false>(keys, nseg, seglen, keys_alt, nullptr, st);
+    const int rc = vals ? launch_seg_sort<true>(keys, nseg, seglen, keys_alt, vals_alt, gap_out, st)
+                        : launch_seg_sort<false>(keys, nseg, seglen, keys_alt, nullptr, gap_out, st);
+    if (gaps_done) *gaps_done = gap_out != nullptr;
     if (rc) return rc;
     AFFMAE_LAUNCH_CHECK("seg_sort_cl_kernel");
     uint64_t* tk = keys;
@@ -445,10 +480,5 @@ inline int bits_for(int64_t v) {
     return b;
 }
 
-// order-preserving float -> uint32 map (ascending)
-__device__ __forceinline__ uint32_t float_order(float f) {
-    uint32_t u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 }  // namespace affmae_b200
