@@ -305,11 +305,14 @@ __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* _
     for (int k = k0; k < min(k0 + kNbrPerWarp, cs.c); ++k) {
         const double2 ck = sc[k];
         const float2 fk = sf[k];
-        // pass 1 (fp32): the G-th smallest approximate d^2 over all centroids
+        // pass 1 (fp32): the G-th smallest approximate d^2 over the 64 clusters around k
+        // in curve order (Hilbert neighbours are spatial neighbours) -- an upper bound
+        // of the true G-th smallest, so pass 2's filter still keeps every true candidate
         float fd[G];
 #pragma unroll
         for (int r = 0; r < G; ++r) fd[r] = INFINITY;
-        for (int j = lane; j < cs.c; j += 32) {
+        const int w0 = max(0, min(k - 32, cs.c - 64));
+        for (int j = w0 + lane; j < min(w0 + 64, cs.c); j += 32) {
             const float2 fj = sf[j];
             const float dx = fj.x - fk.x, dy = fj.y - fk.y;
             float v = fmaf(dx, dx, dy * dy);
