@@ -168,7 +168,7 @@ inline int radix_sort(uint64_t*& keys, uint32_t*& vals, uint64_t* keys_alt, uint
 // contiguous element range walked in rounds of 32 in element order, so the
 // per-(warp, digit) offsets give a stable order.
 constexpr int kSegSortMax = 16384;
-constexpr int kSegWarps = 32;
+constexpr int kSegWarps = 16;
 
 // One segment is spread over a thread-block
 // cluster of CL CTAs (distributed shared memory): CTA r holds slice
@@ -430,7 +430,7 @@ inline int launch_seg_sort_cl(const uint64_t* kin, int64_t nseg, int64_t seglen,
 // CTAs per segment: at most one wave of CTAs on the SMs, slices >= 1024 keys.
 inline int seg_cluster_size(int64_t nseg, int64_t seglen) {
     int cl = 1;
-    while (cl < 8 && nseg * cl * 2 <= kNumSMs && seglen / (cl * 2) >= 1024) cl *= 2;
+    while (cl < 8 && nseg * cl * 2 <= 2 * kNumSMs && seglen / (cl * 2) >= 1024) cl *= 2;
     return cl;
 }
 
