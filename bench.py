@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--k-m", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunks", type=int, default=8, help="image chunks pipelined H2D|compute|D2H")
+    ap.add_argument("--e2e-ramp", type=str, default="",
+                    help="image counts of the first chunks (and, reversed, the last ones): small chunks "
+                         "at both ends shorten the pipeline fill and drain")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
@@ -383,6 +386,26 @@ def count_graph_kernels(graph):
         return None
 
 
+def e2e_bounds(B, chunks, ramp):
+    """Image ranges of the e2e chunks: `ramp` sizes first, the same reversed last, and the rest
+    split into `chunks` near-equal chunks (the D2H stream can start after one small chunk and
+    the last results leave right after the last small chunk's compute)."""
+    rs = [int(x) for x in str(ramp).split(",") if x.strip()] if ramp else []
+    if sum(rs) * 2 >= B:
+        rs = []
+    sizes = list(rs)
+    mid = B - 2 * sum(rs)
+    nmid = max(1, min(chunks, mid))
+    sizes += [mid * (c + 1) // nmid - mid * c // nmid for c in range(nmid)]
+    sizes += rs[::-1]
+    bounds, b0 = [], 0
+    for sz in sizes:
+        if sz > 0:
+            bounds.append((b0, b0 + sz))
+            b0 += sz
+    return bounds
+
+
 def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
     """The same step through the C ABI from HOST buffers: every input H2D and every output D2H
     inside the timed region.  Images are independent, so the batch is processed in chunks on
@@ -416,8 +439,8 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
               + list(hb.values()))
     d2h = sum(t.numel() * t.element_size() for t in outs_h.values())
 
-    nch = max(1, min(a.e2e_chunks, B))
-    bounds = [(B * c // nch, B * (c + 1) // nch) for c in range(nch)]
+    bounds = e2e_bounds(B, a.e2e_chunks, a.e2e_ramp)
+    nch = len(bounds)
     cgeom = {}
     for (b0, b1) in bounds:
         if b1 - b0 not in cgeom:
