@@ -675,11 +675,6 @@ static void fill_common(AttnParams& p, const affmae_cluster_geom* g, const affma
     p.hidden = a->bias_hidden;
     p.inv_patch = float(1.0 / a->patch);
     p.scale = float(1.0 / sqrt(double(a->head_dim)));
-    static const int exp_flags = [] {
-        const char* e = getenv("AFFMAE_EXP");
-        return e ? atoi(e) : 0;
-    }();
-    p.exp_flags = exp_flags;
 }
 
 static int check_inputs(const affmae_attn_inputs* in) {

@@ -112,7 +112,6 @@ struct AttnParams {
     int hidden;
     float inv_patch;
     float scale;      // 1/sqrt(d)
-    int exp_flags;    // development experiments (AFFMAE_EXP), 0 in production
 };
 // per-warp partial: window dT [kWs2] | MLP grads [kMG] | blank {dbk[d], dbv[d], dblank}
 __host__ __device__ constexpr int part_width(int hd) { return kWs2 + kMG + 2 * hd + 1; }
@@ -447,8 +446,7 @@ __device__ __forceinline__ void medium_bias_frag(float (&s)[NT][4], const int32_
 // Bias-table gradient of a medium item from the row-major dS tile.
 template <int KP>
 __device__ __forceinline__ void medium_grad_rowpass(const float* scr, const int32_t* qcell, const int32_t* kcell,
-                                                    int nk, int qlen, bool dup, float* dtab, float* rep, int lane,
-                                                    int exp_flags = 0) {
+                                                    int nk, int qlen, bool dup, float* dtab, float* rep, int lane) {
     const bool va = lane < nk, vb = KP > 32 && lane + 32 < nk;
     const int ka = va ? kcell[lane] : 0, kb = vb ? kcell[lane + 32] : 0;
     const int qcl = lane < 16 ? qcell[lane] : 0;
@@ -463,7 +461,7 @@ __device__ __forceinline__ void medium_grad_rowpass(const float* scr, const int3
                 if (li >= 0) {
                     if (dup) atomicAdd(dtab + li, ds);
                     else dtab[li] += ds;
-                } else if (!(exp_flags & 1)) {
+                } else {
                     atomicAdd(rep + packed_global(kp, qp), ds);
                 }
             }
@@ -782,8 +780,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         if constexpr (FAST) {
             fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
         } else {
-            if (p.exp_flags & 4) {
-            } else if (cls == 2)
+            if (cls == 2)
                 medium_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, p.tab_g + size_t(h) * kWg2,
                                          scale2, lane);
             else
@@ -916,10 +913,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
             }
         } else {
             float* rep = p.dtab_g + (size_t(blockIdx.x & (kTabReplicas - 1)) * p.heads + h) * kWg2;
-            if (p.exp_flags & 2) {
-            } else if (cls == 2)
-                medium_grad_rowpass<KP>(scr, rec + R::QCELL, rec + R::KCELL, nk, qlen, dup, dtab, rep, lane,
-                                        p.exp_flags);
+            if (cls == 2)
+                medium_grad_rowpass<KP>(scr, rec + R::QCELL, rec + R::KCELL, nk, qlen, dup, dtab, rep, lane);
             else
                 general_grad_rowpass<KP>(scr, rec + R::QTOK, rec + R::KTOK, nk, qlen, dup, dtab, rep, sm.units,
                                          sm.mlpg, p, img_tok, lane);
