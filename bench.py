@@ -59,6 +59,9 @@ def parse():
                     help="image counts of the first chunks (and, reversed, the last ones): small chunks "
                          "at both ends shorten the pipeline fill and drain")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="independent image groups per GPU, each on its own stream pair (images never "
+                         "interact, so the groups' latency-bound phases overlap each other)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
     return ap.parse_args()
@@ -73,7 +76,8 @@ def workload_config(a, world):
             "neighbours": a.cluster * a.groups, "cluster": a.cluster, "groups": a.groups,
             "bias_hidden": a.hidden, "d_s": a.d_s, "k_m": a.k_m,
             "l2": "inputs per step > 126 MB L2 (no flush needed)",
-            "parallelism": f"dp{world} (images sharded, no data-path collective)"}
+            "parallelism": f"dp{world} (images sharded, no data-path collective)",
+            "image_streams": getattr(a, "streams", 1)}
 
 
 # ----------------------------------------------------------------- clocks
@@ -270,6 +274,70 @@ def run_ours(a, rank, world, dist):
                      workspace=ws, plan=plan)
         cur.wait_stream(side)
         return out, lse, grads, pooled, dfe, dsc, dp
+
+    # --streams S: the batch as S independent image groups, each the same DAG on its own
+    # stream pair, sharing nothing but the (read-only) inputs; every group writes its own slice
+    # of the outputs and its own parameter-gradient partials, summed at the end of the step
+    S = max(1, min(a.streams, B))
+    gb = [(B * g // S, B * (g + 1) // S) for g in range(S)]
+    groups = []
+    if S > 1:
+        for (b0, b1) in gb:
+            gq = dict(geom=ops.geometry(b1 - b0, N, a.cluster, a.groups),
+                      ws=torch.empty(256 << 20, dtype=torch.uint8, device=dev),
+                      plan_buf=torch.empty(64 << 20, dtype=torch.uint8, device=dev),
+                      main=torch.cuda.Stream(device=dev), side=torch.cuda.Stream(device=dev),
+                      grads=ops.AttnGrads(grads.dq[b0:b1], grads.dk[b0:b1], grads.dv[b0:b1],
+                                          *[torch.zeros_like(t) for t in (grads.dblank_k, grads.dblank_v,
+                                                                          grads.dw1, grads.db1, grads.dw2,
+                                                                          grads.db2, grads.dblank)]),
+                      pooled=None)
+            groups.append(gq)
+
+    def group_dag(g):
+        b0, b1 = gb[g]
+        st = groups[g]
+        cur, side_g = st["main"], st["side"]
+        sl = slice(b0, b1)
+        side_g.wait_stream(cur)
+        with torch.cuda.stream(side_g):
+            ret = ops.select_retained(scores[sl], a.d_s)
+            mplan = ops.merge_plan(coords[sl], ret, a.k_m)
+        idx = ops.cluster_index(coords[sl], a.cluster, a.groups, workspace=st["ws"])
+        plan = ops.attn_plan(st["geom"], coords[sl], idx, h, d, a.hidden, buf=st["plan_buf"])
+        out, lse = ops.attn_fwd(st["geom"], q[sl], k[sl], v[sl], bk, bv, coords[sl], idx.perm, idx.nbr_cl, bias,
+                                h, d, out=out_buf[sl], lse=lse_buf[sl], workspace=st["ws"], plan=plan)
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(cur)
+        with torch.cuda.stream(side_g):
+            side_g.wait_event(fwd_done)
+            pooled = ops.merge_pool_fwd(out, scores[sl], p_merge, mplan)
+            dfe, dsc, dp = ops.merge_pool_bwd(out, scores[sl], p_merge, mplan, dpooled[sl])
+        ops.attn_bwd(st["geom"], q[sl], k[sl], v[sl], bk, bv, coords[sl], idx, bias, h, d, out, lse, dout[sl],
+                     grads=st["grads"], workspace=st["ws"], plan=plan)
+        cur.wait_stream(side_g)
+        return pooled, dfe, dsc, dp
+
+    def step_groups():
+        cur = torch.cuda.current_stream(dev)
+        res = []
+        for g in range(S):
+            groups[g]["main"].wait_stream(cur)
+            with torch.cuda.stream(groups[g]["main"]):
+                res.append(group_dag(g))
+        for g in range(S):
+            cur.wait_stream(groups[g]["main"])
+        # parameter-gradient partials of the groups -> the step's gradients
+        for name in ("dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank"):
+            tot = getattr(grads, name)
+            tot.copy_(getattr(groups[0]["grads"], name))
+            for g in range(1, S):
+                tot.add_(getattr(groups[g]["grads"], name))
+        return res
+
+    if S > 1:
+        step_dag_single = step_dag
+        step_dag = step_groups  # noqa: F811 (the timed and captured step)
 
     # warm-up (also primes the caching allocator) + per-phase timing pass (sequential)
     for _ in range(max(1, a.warmup)):
