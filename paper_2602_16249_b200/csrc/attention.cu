@@ -146,8 +146,13 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     const int32_t* nb = nbr_cl + item * cs.g;
     int32_t* out = qrec + item * R::WORDS;
     const int qlen = cs.len(c);
+    // equal-size clusters (N divisible by C, the lattice case): slot s is member s % base
+    // of neighbour s / base, no per-slot walk over the groups
+    const bool uniform = cs.rem == 0;
     int nk = 0;
-    for (int g = 0; g < cs.g; ++g) nk += cs.len(nb[g]);
+    if (uniform) nk = cs.g * cs.base;
+    else
+        for (int g = 0; g < cs.g; ++g) nk += cs.len(nb[g]);
     TokAgg agg;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -157,13 +162,18 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
             if (e < qlen) tok = perm[img_tok + cs.off(c) + e];
         } else if (e < E && e - 16 < nk) {
             int s = e - 16;
-            for (int g = 0; g < cs.g; ++g) {
-                const int cl = nb[g], len = cs.len(cl);
-                if (s < len) {
-                    tok = perm[img_tok + cs.off(cl) + s];
-                    break;
+            if (uniform) {
+                const int g = s / cs.base;
+                tok = perm[img_tok + __ldg(nb + g) * cs.base + (s - g * cs.base)];
+            } else {
+                for (int g = 0; g < cs.g; ++g) {
+                    const int cl = nb[g], len = cs.len(cl);
+                    if (s < len) {
+                        tok = perm[img_tok + cs.off(cl) + s];
+                        break;
+                    }
+                    s -= len;
                 }
-                s -= len;
             }
         }
         int cell = 0, pcell = 0;
