@@ -45,7 +45,7 @@ for r in rows[hi + 1:end]:
             pass
 tot, ts = sum(ci.values()), sum(cs.values())
 import os
-srcdir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2602_16249_b200", "csrc")
+srcdir = os.environ.get("SRCDIR") or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2602_16249_b200", "csrc")
 src = {}
 for k in list(ci):
     f = k.split(":")[0]
