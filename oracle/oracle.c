@@ -676,3 +676,96 @@ int orc_merge_pool_bwd(int64_t n, int64_t dim, int64_t r, int k_m, int prec,
     }
     return 0;
 }
+
+/* ---------------------------------------------------------------- interpolation
+ * make_interp_op (proj/src/interpolation.cpp:192-251): per query, the valid
+ * neighbours of its row; interp_softmax (:51-67) with `prec` rounding after
+ * every step (cast_prec, :12-18; the distance d = sqrt(dx^2 + dy^2) + eps is
+ * rounded once, :21-30), combine (:32-49); backward (:93-142) in binary64 with
+ * the zero subgradient at an exact query/key coincidence. */
+static inline double cprec(double v, int prec) { return prec == 32 ? (double)(float)v : v; }
+
+int orc_interp_fwd(int64_t nq, int64_t dim, int64_t k, int prec, const double* queries, const float* key_coords,
+                   const double* feats, const int64_t* idx, const uint8_t* valid, double p, double eps,
+                   double* out) {
+    double d[256], e[256];
+    int64_t nb[256];
+    if (k > 256) return 2;
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        int64_t m = 0;
+        for (int64_t t = 0; t < k; ++t)
+            if (valid[qi * k + t]) nb[m++] = idx[qi * k + t];
+        if (m == 0) return 2; /* ConfigError: no valid neighbors */
+        const double qx = queries[2 * qi], qy = queries[2 * qi + 1];
+        double mx = -INFINITY;
+        for (int64_t i = 0; i < m; ++i) {
+            double dx = qx - (double)key_coords[2 * nb[i]], dy = qy - (double)key_coords[2 * nb[i] + 1];
+            d[i] = cprec(sqrt(dx * dx + dy * dy) + eps, prec);
+            e[i] = cprec(-p * d[i], prec); /* logit */
+            mx = e[i] > mx ? e[i] : mx;
+        }
+        double s = 0.0;
+        for (int64_t i = 0; i < m; ++i) {
+            e[i] = cprec(exp(e[i] - mx), prec);
+            s = cprec(s + e[i], prec);
+        }
+        for (int64_t i = 0; i < m; ++i) e[i] = cprec(e[i] / s, prec);
+        for (int64_t c = 0; c < dim; ++c) {
+            double acc = 0.0;
+            for (int64_t i = 0; i < m; ++i) acc = cprec(acc + e[i] * feats[nb[i] * dim + c], prec);
+            out[qi * dim + c] = acc;
+        }
+    }
+    return 0;
+}
+
+int orc_interp_bwd(int64_t nq, int64_t dim, int64_t k, const double* queries, const float* key_coords,
+                   const double* feats, const int64_t* idx, const uint8_t* valid, double p, double eps,
+                   const double* dout, double* dfeats, double* dp, double* dq) {
+    double r[256], d[256], w[256], dw[256];
+    int64_t nb[256];
+    if (k > 256) return 2;
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        int64_t m = 0;
+        for (int64_t t = 0; t < k; ++t)
+            if (valid[qi * k + t]) nb[m++] = idx[qi * k + t];
+        if (m == 0) return 2;
+        const double qx = queries[2 * qi], qy = queries[2 * qi + 1];
+        for (int64_t i = 0; i < m; ++i) {
+            double dx = qx - (double)key_coords[2 * nb[i]], dy = qy - (double)key_coords[2 * nb[i] + 1];
+            r[i] = sqrt(dx * dx + dy * dy);
+            d[i] = r[i] + eps;
+        }
+        double mx = -p * d[0];
+        for (int64_t i = 1; i < m; ++i) mx = mx > -p * d[i] ? mx : -p * d[i];
+        double s = 0.0;
+        for (int64_t i = 0; i < m; ++i) {
+            w[i] = exp(-p * d[i] - mx);
+            s += w[i];
+        }
+        for (int64_t i = 0; i < m; ++i) w[i] /= s;
+        const double* g = dout + qi * dim;
+        for (int64_t i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int64_t c = 0; c < dim; ++c) {
+                dfeats[nb[i] * dim + c] += w[i] * g[c];
+                acc += g[c] * feats[nb[i] * dim + c];
+            }
+            dw[i] = acc;
+        }
+        double wdot = 0.0, dpq = 0.0; /* per-query dp, then added (InterpOp::backward, :240) */
+        for (int64_t i = 0; i < m; ++i) wdot += w[i] * dw[i];
+        for (int64_t i = 0; i < m; ++i) {
+            double dl = w[i] * (dw[i] - wdot);
+            dpq += dl * (-d[i]);
+            double dd = dl * (-p);
+            if (r[i] > 0.0) {
+                dq[2 * qi] += dd * (qx - (double)key_coords[2 * nb[i]]) / r[i];
+                dq[2 * qi + 1] += dd * (qy - (double)key_coords[2 * nb[i] + 1]) / r[i];
+            }
+        }
+        *dp += dpq;
+    }
+    return 0;
+}
+

@@ -71,6 +71,14 @@ int orc_merge_pool_bwd(int64_t n, int64_t dim, int64_t r, int k_m, int prec,
                        const int32_t* pool_cnt, const double* feats, const double* scores,
                        double p, const double* dout, double* dfeats, double* dscores, double* dp);
 
+/* make_interp_op forward / backward (interpolation.cpp:192-251) */
+int orc_interp_fwd(int64_t nq, int64_t dim, int64_t k, int prec, const double* queries, const float* key_coords,
+                   const double* feats, const int64_t* idx, const uint8_t* valid, double p, double eps,
+                   double* out);
+int orc_interp_bwd(int64_t nq, int64_t dim, int64_t k, const double* queries, const float* key_coords,
+                   const double* feats, const int64_t* idx, const uint8_t* valid, double p, double eps,
+                   const double* dout, double* dfeats, double* dp, double* dq);
+
 #ifdef __cplusplus
 }
 #endif

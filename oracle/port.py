@@ -208,3 +208,36 @@ def merge_pool_bwd(plan, feats, scores, p, dout, prec=64):
                                     C.c_int(prec), *[_p(x) for x in pa], _p(feats), _p(scores),
                                     C.c_double(p), _p(dout), _p(df), _p(ds), _p(dp)))
     return df, ds, float(dp[0])
+
+
+def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, prec=32):
+    """make_interp_op forward (interpolation.cpp:192-222) restated in oracle.c.  The
+    temperature is a tape tensor, so at b32 it is the float-rounded p."""
+    p = float(np.float32(p)) if prec == 32 else float(p)
+    queries, feats = _f64(queries), _f64(feats)
+    kc = _f32(key_coords)
+    idx, valid = _i64(idx), np.ascontiguousarray(valid, np.uint8)
+    nq, k = idx.shape
+    dim = feats.shape[1]
+    out = np.empty((nq, dim))
+    _check(lib().orc_interp_fwd(C.c_int64(nq), C.c_int64(dim), C.c_int64(k), C.c_int(prec), _p(queries), _p(kc),
+                                _p(feats), _p(idx), _p(valid), C.c_double(p), C.c_double(eps), _p(out)))
+    return out
+
+
+def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, prec=32):
+    """make_interp_op backward (interpolation.cpp:224-251, binary64 math on the tape's
+    values): dfeats, dp, dqueries."""
+    p = float(np.float32(p)) if prec == 32 else float(p)
+    queries, feats, dout = _f64(queries), _f64(feats), _f64(dout)
+    kc = _f32(key_coords)
+    idx, valid = _i64(idx), np.ascontiguousarray(valid, np.uint8)
+    nq, k = idx.shape
+    dim = feats.shape[1]
+    df = np.zeros(feats.shape)
+    dq = np.zeros((nq, 2))
+    dp = np.zeros(1)
+    _check(lib().orc_interp_bwd(C.c_int64(nq), C.c_int64(dim), C.c_int64(k), _p(queries), _p(kc), _p(feats),
+                                _p(idx), _p(valid), C.c_double(p), C.c_double(eps), _p(dout), _p(df), _p(dp),
+                                _p(dq)))
+    return df, float(dp[0]), dq

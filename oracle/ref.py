@@ -205,6 +205,36 @@ def merge_pool_bwd(plan, feats, scores, p, dout, prec=64):
     return df, ds, dp.value
 
 
+def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, prec=32):
+    """make_interp_op forward (interpolation.cpp:192-222) of the compiled reference."""
+    queries, feats = _f64(queries), _f64(feats)
+    kc = _f32(key_coords)
+    idx, valid = _i64(idx), np.ascontiguousarray(valid, np.uint8)
+    nq, k = idx.shape
+    nk, dim = feats.shape
+    out = np.empty((nq, dim))
+    _check(lib().ref_interp_fwd(C.c_int64(nq), C.c_int64(nk), C.c_int64(dim), C.c_int64(k), _p(queries),
+                                _p(kc), _p(feats), _p(idx), _p(valid), C.c_double(p), C.c_double(eps),
+                                C.c_int(prec), _p(out)))
+    return out
+
+
+def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, prec=32):
+    """make_interp_op backward (interpolation.cpp:224-251): dfeats, dp, dqueries."""
+    queries, feats, dout = _f64(queries), _f64(feats), _f64(dout)
+    kc = _f32(key_coords)
+    idx, valid = _i64(idx), np.ascontiguousarray(valid, np.uint8)
+    nq, k = idx.shape
+    nk, dim = feats.shape
+    df = np.empty((nk, dim))
+    dq = np.empty((nq, 2))
+    dp = C.c_double()
+    _check(lib().ref_interp_bwd(C.c_int64(nq), C.c_int64(nk), C.c_int64(dim), C.c_int64(k), _p(queries),
+                                _p(kc), _p(feats), _p(idx), _p(valid), C.c_double(p), C.c_double(eps),
+                                C.c_int(prec), _p(dout), _p(df), C.byref(dp), _p(dq)))
+    return df, dp.value, dq
+
+
 def perlin_mask(grid, ratio, seed):
     m = np.empty(grid * grid, np.uint8)
     _check(lib().ref_perlin_mask(C.c_int64(grid), C.c_double(ratio), C.c_uint64(seed), _p(m)))

@@ -30,6 +30,7 @@
 #include "affmae/attention.hpp"
 #include "affmae/errors.hpp"
 #include "affmae/geometry.hpp"
+#include "affmae/interpolation.hpp"
 #include "affmae/masking.hpp"
 #include "affmae/merging.hpp"
 #include "affmae/tape.hpp"
@@ -321,6 +322,42 @@ int ref_merge_pool_bwd(int64_t n, int64_t dim, int64_t r, int k_m, const int64_t
         to(df, dfeats);
         to(ds, dscores);
         *dp = dpt.get(0);
+    });
+}
+
+// make_interp_op (interpolation.hpp:60) forward / backward: queries [nq,2],
+// key coords [nk,2], feats [nk,dim], neighbour rows idx/valid [nq,k]
+int ref_interp_fwd(int64_t nq, int64_t nk, int64_t dim, int64_t k, const double* queries,
+                   const float* key_coords, const double* feats, const int64_t* idx, const uint8_t* valid,
+                   double p, double eps, int prec, double* out) {
+    return guarded([&] {
+        Precision pr = prec_of(prec);
+        auto op = make_interp_op(from_f(key_coords, {nk, 2}, Precision::b64), nbr_from(idx, valid, nq, k), eps);
+        Tensor f = from(feats, {nk, dim}, pr);
+        Tensor pt = Tensor::full({1, 1}, p, pr);
+        Tensor q = from(queries, {nq, 2}, pr);
+        to(op->forward({&f, &pt, &q}), out);
+    });
+}
+
+int ref_interp_bwd(int64_t nq, int64_t nk, int64_t dim, int64_t k, const double* queries,
+                   const float* key_coords, const double* feats, const int64_t* idx, const uint8_t* valid,
+                   double p, double eps, int prec, const double* dout, double* dfeats, double* dp,
+                   double* dq) {
+    return guarded([&] {
+        Precision pr = prec_of(prec);
+        auto op = make_interp_op(from_f(key_coords, {nk, 2}, Precision::b64), nbr_from(idx, valid, nq, k), eps);
+        Tensor f = from(feats, {nk, dim}, pr);
+        Tensor pt = Tensor::full({1, 1}, p, pr);
+        Tensor q = from(queries, {nq, 2}, pr);
+        Tensor g = from(dout, {nq, dim}, pr);
+        Tensor df = Tensor::zeros({nk, dim}, Precision::b64);
+        Tensor dpt = Tensor::zeros({1, 1}, Precision::b64);
+        Tensor dqt = Tensor::zeros({nq, 2}, Precision::b64);
+        op->backward(g, {&f, &pt, &q}, {&df, &dpt, &dqt});
+        to(df, dfeats);
+        *dp = dpt.get(0);
+        to(dqt, dq);
     });
 }
 

@@ -91,6 +91,23 @@ def main():
                     f"mrg_{name}_dsk": np.array([ds, km])})
         for k_, v_ in pl.items():
             out[f"mrg_{name}_plan_{k_}"] = v_
+    # make_interp_op (interpolation.cpp:192-251) on knn rows, b32 tape; own RNG so the
+    # arrays above do not move when cases are added here
+    irng = np.random.default_rng(2602)
+    for name, (nk, nq, k, dim, p_) in {"i50": (50, 13, 6, 5, 1.5), "i200": (200, 40, 8, 7, 0.7)}.items():
+        kc = rnd_points(irng, nk, 32.0)
+        q = rnd_points(irng, nq, 32.0).astype(np.float64)
+        q[0] = kc[3]  # exact query/key coincidence (zero subgradient)
+        idx, valid = ref.knn(q.astype(np.float32), kc, k)
+        valid[1, k // 2:] = 0  # a short row
+        feats = irng.standard_normal((nk, dim)).astype(np.float32).astype(np.float64)
+        dd = irng.standard_normal((nq, dim)).astype(np.float32).astype(np.float64)
+        io = ref.interp_fwd(q, kc, feats, idx, valid, p_)
+        df, dp, dq = ref.interp_bwd(q, kc, feats, idx, valid, p_, dd)
+        out.update({f"itp_{name}_keys": kc, f"itp_{name}_queries": q, f"itp_{name}_idx": idx,
+                    f"itp_{name}_valid": valid, f"itp_{name}_feats": feats, f"itp_{name}_dout": dd,
+                    f"itp_{name}_p": np.array([p_]), f"itp_{name}_out": io, f"itp_{name}_dfeats": df,
+                    f"itp_{name}_dp": np.array([dp]), f"itp_{name}_dq": dq})
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print(f"wrote {len(out)} arrays")
 

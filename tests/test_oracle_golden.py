@@ -160,3 +160,34 @@ def test_pool_known_answer():
     assert out[0, 0] == 1.0 and out[0, 1] == 2.0
     assert abs(out[0, 2] - ((e1 / z) * 0.5 * 3.0 + (e2 / z) * 0.25 * 5.0)) <= 1e-12
     assert abs(out[0, 3] - ((e1 / z) * 0.5 * 4.0 + (e2 / z) * 0.25 * 6.0)) <= 1e-12
+
+
+ITP = sorted(k[4:-5] for k in G.files if k.startswith("itp_") and k.endswith("_keys"))
+
+
+@pytest.mark.parametrize("name", ITP)
+def test_interp_matches_reference(name):
+    """make_interp_op fwd (b32 tape) and bwd (binary64), bit-exact (interpolation.cpp:192-251)."""
+    g = lambda k: G[f"itp_{name}_{k}"]
+    p = float(g("p")[0])
+    out = port.interp_fwd(g("queries"), g("keys"), g("feats"), g("idx"), g("valid"), p)
+    np.testing.assert_array_equal(out, g("out"))
+    df, dp, dq = port.interp_bwd(g("queries"), g("keys"), g("feats"), g("idx"), g("valid"), p, g("dout"))
+    np.testing.assert_array_equal(df, g("dfeats"))
+    np.testing.assert_array_equal(dq, g("dq"))
+    assert dp == float(g("dp")[0])
+
+
+def test_interp_known_answers():
+    # proj/tests/test_interpolation.cpp:36-46: two points at d = 1, 4 (+eps), p = 2
+    kc = np.array([[1, 0], [4, 0]], np.float32)
+    feats = np.array([[10.0], [-2.0]])
+    out = port.interp_fwd(np.zeros((1, 2)), kc, feats, np.array([[0, 1]]), np.ones((1, 2), np.uint8), 2.0,
+                          prec=64)
+    w0 = 1.0 / (1.0 + np.exp(-2.0 * 3.0))
+    assert abs(out[0, 0] - (w0 * 10.0 + (1 - w0) * -2.0)) <= 1e-12 * 10
+    # :59-74: four equidistant neighbours average evenly
+    kc4 = np.array([[1, 0], [0, 1], [-1, 0], [0, -1]], np.float32)
+    out4 = port.interp_fwd(np.zeros((1, 2)), kc4, np.arange(4.0).reshape(4, 1), np.array([[0, 1, 2, 3]]),
+                           np.ones((1, 4), np.uint8), 5.0, prec=64)
+    assert abs(out4[0, 0] - 1.5) <= 1e-12
