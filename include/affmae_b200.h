@@ -97,6 +97,24 @@ int affmae_sfc_order(const float* coords, int64_t batch, int64_t tokens, int32_t
 int affmae_knn(const float* queries, const float* keys, int64_t batch, int64_t n_queries,
                int64_t n_keys, int64_t k, int32_t* idx, uint8_t* valid, void* stream);
 
+/* Replaces make_interp_op (include/affmae/interpolation.hpp:60; InterpOp,
+ * src/interpolation.cpp:192-251 over interp_softmax :51-67 / interp_backward
+ * :93-142), batched: queries [B, Q, 2], key_coords [B, N, 2], feats [B, N, D]
+ * bf16 (D in {64, 128, 256, 512}), neighbour rows idx/valid [B, Q, K] (K <= 32,
+ * e.g. from affmae_knn), temperature p (device scalar, a tape parameter),
+ * eps (kInterpEps = 1e-6).  out [B, Q, D] bf16 = sum_i softmax(-p d)_i f_i.
+ * The backward ACCUMULATES (+=, CustomOp::backward) into dfeats [B, N, D] fp32,
+ * dp [1] and dqueries [B, Q, 2]; it needs no workspace.  A row without a valid
+ * neighbour yields zeros and no gradient (the reference raises ConfigError). */
+int affmae_interp_fwd(const float* queries, const float* key_coords, const affmae_bf16* feats,
+                      const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
+                      int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
+                      affmae_bf16* out, void* stream);
+int affmae_interp_bwd(const float* queries, const float* key_coords, const affmae_bf16* feats,
+                      const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
+                      int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
+                      const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream);
+
 /* ------------------------------------------------------------------------
  * Cluster attention (nbhd_attn_streaming / nbhd_attn_backward,
  * include/affmae/attention.hpp:52-72; AttnOp, src/attention.cpp:374-444).

@@ -27,7 +27,7 @@ EXPORTS = (
     "affmae_attn_fwd_planned", "affmae_attn_bwd_planned_workspace", "affmae_attn_bwd_planned",
     "affmae_retained_count", "affmae_select_retained_workspace", "affmae_select_retained",
     "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
-    "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd",
+    "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd", "affmae_interp_fwd", "affmae_interp_bwd",
 )
 
 

@@ -49,6 +49,10 @@ int sfc_order(const float*, int64_t, int64_t, int32_t*, void*, size_t, void*);
 int neighbor_expand(const affmae_cluster_geom*, const int32_t*, const int32_t*, int32_t*, uint8_t*,
                     void*);
 int knn(const float*, const float*, int64_t, int64_t, int64_t, int64_t, int32_t*, uint8_t*, void*);
+int interp_fwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
+               int64_t, int64_t, const float*, double, void*, void*);
+int interp_bwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
+               int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*);
 int64_t retained_count_impl(int64_t, double);
 size_t select_retained_workspace(int64_t, int64_t);
 int select_retained(const float*, int64_t, int64_t, double, int32_t*, void*, size_t, void*);
@@ -164,6 +168,22 @@ int affmae_sfc_order(const float* coords, int64_t batch, int64_t tokens, int32_t
 int affmae_knn(const float* queries, const float* keys, int64_t batch, int64_t n_queries,
                int64_t n_keys, int64_t k, int32_t* idx, uint8_t* valid, void* stream) {
     return knn(queries, keys, batch, n_queries, n_keys, k, idx, valid, stream);
+}
+
+// make_interp_op forward / backward (proj/src/interpolation.cpp:192-251)
+int affmae_interp_fwd(const float* queries, const float* key_coords, const affmae_bf16* feats,
+                      const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
+                      int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
+                      affmae_bf16* out, void* stream) {
+    return interp_fwd(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, out,
+                      stream);
+}
+int affmae_interp_bwd(const float* queries, const float* key_coords, const affmae_bf16* feats,
+                      const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
+                      int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
+                      const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream) {
+    return interp_bwd(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
+                      dfeats, dp, dqueries, stream);
 }
 
 // retained_count (proj/src/merging.cpp:50-54)

@@ -287,6 +287,53 @@ def knn(queries, keys, k, stream=None):
     return idx, valid
 
 
+# ------------------------------------------------------------ interpolation
+def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, stream=None):
+    """make_interp_op forward (proj/src/interpolation.cpp:192-222), batched:
+    queries [B, Q, 2] fp32, key_coords [B, N, 2] fp32, feats [B, N, D] bf16, idx/valid
+    [B, Q, K] (e.g. from knn), p [1] fp32 -> out [B, Q, D] bf16."""
+    _req(queries, torch.float32, "queries")
+    _req(key_coords, torch.float32, "key_coords")
+    _req(feats, torch.bfloat16, "feats")
+    _req(idx, torch.int32, "idx")
+    _req(valid, torch.uint8, "valid")
+    _req(p, torch.float32, "p")
+    B, Q, _ = queries.shape
+    N, D = feats.shape[1], feats.shape[2]
+    K = idx.shape[2]
+    out = torch.empty((B, Q, D), dtype=torch.bfloat16, device=feats.device)
+    capi.check(capi.lib().affmae_interp_fwd(
+        C.c_void_p(queries.data_ptr()), C.c_void_p(key_coords.data_ptr()), C.c_void_p(feats.data_ptr()),
+        C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()), C.c_int64(B), C.c_int64(Q), C.c_int64(N),
+        C.c_int64(D), C.c_int64(K), C.c_void_p(p.data_ptr()), C.c_double(eps), C.c_void_p(out.data_ptr()),
+        _stream(stream)), "interp_fwd")
+    return out
+
+
+def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, dfeats=None, dp=None, dqueries=None,
+               stream=None):
+    """make_interp_op backward (proj/src/interpolation.cpp:224-251): accumulates into
+    dfeats [B, N, D] fp32, dp [1] fp32 and dqueries [B, Q, 2] fp32 (zeros if not given)."""
+    _req(dout, torch.bfloat16, "dout")
+    B, Q, _ = queries.shape
+    N, D = feats.shape[1], feats.shape[2]
+    K = idx.shape[2]
+    dev = feats.device
+    if dfeats is None:
+        dfeats = torch.zeros((B, N, D), dtype=torch.float32, device=dev)
+    if dp is None:
+        dp = torch.zeros(1, dtype=torch.float32, device=dev)
+    if dqueries is None:
+        dqueries = torch.zeros((B, Q, 2), dtype=torch.float32, device=dev)
+    capi.check(capi.lib().affmae_interp_bwd(
+        C.c_void_p(queries.data_ptr()), C.c_void_p(key_coords.data_ptr()), C.c_void_p(feats.data_ptr()),
+        C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()), C.c_int64(B), C.c_int64(Q), C.c_int64(N),
+        C.c_int64(D), C.c_int64(K), C.c_void_p(p.data_ptr()), C.c_double(eps), C.c_void_p(dout.data_ptr()),
+        C.c_void_p(dfeats.data_ptr()), C.c_void_p(dp.data_ptr()), C.c_void_p(dqueries.data_ptr()),
+        _stream(stream)), "interp_bwd")
+    return dfeats, dp, dqueries
+
+
 # -------------------------------------------------------------------- merge
 def retained_count(n, d_s):
     """retained_count (proj/src/merging.cpp:50-54): clamp(floor(d_s*n + 0.5), 1, n)."""
