@@ -423,4 +423,83 @@ std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords) {
     return op;
 }
 
+std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, double eps) {
+    struct InterpCudaOp final : CustomOp {
+        Tensor key_coords;
+        NeighborIndex nbrs;
+        double eps = kInterpEps;
+        std::string name() const override { return "interp_softmax_b200"; }
+        struct DevRows {
+            std::unique_ptr<Dev> kc, idx, valid;
+        };
+        DevRows upload_rows() const {
+            if (nbrs.width < 1 || nbrs.width > 32) throw ConfigError("interp op: neighbour width must be in [1, 32]");
+            std::vector<int32_t> idx(nbrs.idx.begin(), nbrs.idx.end());
+            DevRows d;
+            d.kc = upload(f32(key_coords));
+            d.idx = upload(idx);
+            d.valid = upload(nbrs.valid);
+            return d;
+        }
+        void validate(const Tensor& feats, const Tensor& pt, const Tensor& q) const {
+            if (pt.numel() != 1) throw ConfigError("interp op: p must be scalar");
+            if (q.ndim() != 2 || q.dim(1) != 2) throw ConfigError("interp op: queries must be Qx2");
+            if (q.dim(0) != nbrs.queries()) throw ConfigError("interp op: query count does not match neighbor index");
+            for (int64_t qi = 0; qi < nbrs.queries(); ++qi)
+                if (nbrs.row(qi).empty()) throw ConfigError("interp_softmax: no valid neighbors");
+            (void)feats;
+        }
+        Tensor forward(const std::vector<const Tensor*>& in) override {
+            const Tensor& feats = *in[0];
+            validate(feats, *in[1], *in[2]);
+            const int64_t nk = feats.rows(), dim = feats.cols(), nq = in[2]->dim(0);
+            DevRows d = upload_rows();
+            auto f = upload(bf16(feats));
+            auto pt = upload(f32(*in[1]));
+            auto q = upload(f32(*in[2]));
+            Dev out(nq * dim * 2);
+            check(affmae_interp_fwd(q->as<float>(), d.kc->as<float>(), f->as<affmae_bf16>(), d.idx->as<int32_t>(),
+                                    d.valid->as<uint8_t>(), 1, nq, nk, dim, nbrs.width, pt->as<float>(), eps,
+                                    out.as<affmae_bf16>(), nullptr),
+                  "interp_fwd");
+            auto h = download<uint16_t>(out, size_t(nq * dim));
+            Tensor o = Tensor::zeros({nq, dim}, feats.precision());
+            for (int64_t i = 0; i < nq * dim; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+            return o;
+        }
+        void backward(const Tensor& g, const std::vector<const Tensor*>& in,
+                      const std::vector<Tensor*>& in_grads) override {
+            const Tensor& feats = *in[0];
+            const int64_t nk = feats.rows(), dim = feats.cols(), nq = in[2]->dim(0);
+            DevRows d = upload_rows();
+            auto f = upload(bf16(feats));
+            auto pt = upload(f32(*in[1]));
+            auto q = upload(f32(*in[2]));
+            auto dg = upload(bf16(g));
+            Dev df(nk * dim * 4), dp(4), dq(nq * 2 * 4);
+            ccheck(cudaMemset(df.p, 0, size_t(nk * dim * 4)), "memset");
+            ccheck(cudaMemset(dp.p, 0, 4), "memset");
+            ccheck(cudaMemset(dq.p, 0, size_t(nq * 2 * 4)), "memset");
+            check(affmae_interp_bwd(q->as<float>(), d.kc->as<float>(), f->as<affmae_bf16>(), d.idx->as<int32_t>(),
+                                    d.valid->as<uint8_t>(), 1, nq, nk, dim, nbrs.width, pt->as<float>(), eps,
+                                    dg->as<affmae_bf16>(), df.as<float>(), dp.as<float>(), dq.as<float>(), nullptr),
+                  "interp_bwd");
+            if (in_grads[0]) {
+                auto h = download<float>(df, size_t(nk * dim));
+                for (int64_t i = 0; i < nk * dim; ++i) in_grads[0]->set(i, in_grads[0]->get(i) + h[size_t(i)]);
+            }
+            if (in_grads[1]) in_grads[1]->set(0, in_grads[1]->get(0) + download<float>(dp, 1)[0]);
+            if (in_grads[2]) {
+                auto h = download<float>(dq, size_t(nq * 2));
+                for (int64_t i = 0; i < nq * 2; ++i) in_grads[2]->set(i, in_grads[2]->get(i) + h[size_t(i)]);
+            }
+        }
+    };
+    auto op = std::make_shared<InterpCudaOp>();
+    op->key_coords = std::move(key_coords);
+    op->nbrs = std::move(nbrs);
+    op->eps = eps;
+    return op;
+}
+
 }  // namespace affmae::cuda

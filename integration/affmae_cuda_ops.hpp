@@ -17,6 +17,7 @@
 
 #include "affmae/attention.hpp"
 #include "affmae/geometry.hpp"
+#include "affmae/interpolation.hpp"
 #include "affmae/merging.hpp"
 #include "affmae/tape.hpp"
 
@@ -41,5 +42,10 @@ std::shared_ptr<CustomOp> make_cluster_attn_op(Tensor coords, int64_t cluster, i
 std::vector<int64_t> select_retained(const Tensor& scores, double d_s);
 MergePlan merge_plan(const PointSet& ps, std::span<const int64_t> retained, int k_m);
 std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords);
+
+// Softmax interpolation tape op (make_interp_op, include/affmae/interpolation.hpp:60):
+// inputs {feats NxD, p 1x1, queries Qx2}; neighbour rows frozen at construction
+// (width <= 32), gradients to feats, p and the query coordinates.
+std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, double eps = kInterpEps);
 
 }  // namespace affmae::cuda

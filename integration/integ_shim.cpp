@@ -132,4 +132,26 @@ int integ_merge_tape(int use_cuda, int64_t n, int64_t dim, double d_s, int k_m, 
     });
 }
 
+// Decoder-style interpolation on the reference Tape: nbrs = knn(queries, keys, k),
+// out = interp(feats, p, queries), loss = sum(out * w), backward.
+int integ_interp_tape(int use_cuda, int64_t nk, int64_t nq, int64_t dim, int64_t k, const float* keys,
+                      const double* queries, const double* feats, double p, const double* w, double* out,
+                      double* dfeats, double* dp, double* dq) {
+    return guarded([&] {
+        PointSet ks = pts(keys, nk);
+        Tensor qt = from(queries, {nq, 2});
+        NeighborIndex nb = use_cuda ? cuda::knn(qt, ks, k) : knn(qt, ks, k);
+        Tape t(Precision::b32);
+        int f = t.leaf(from(feats, {nk, dim})), pp = t.leaf(Tensor::full({1, 1}, p, Precision::b32)), q = t.leaf(qt);
+        auto op = use_cuda ? cuda::make_interp_op(ks.coords, nb) : make_interp_op(ks.coords, nb);
+        int o = t.custom(op, {f, pp, q});
+        int loss = t.reduce_sum(t.mul(o, t.input(from(w, {nq, dim}))));
+        t.backward(loss);
+        to(t.value(o), out);
+        to(t.grad(f), dfeats);
+        *dp = t.grad(pp).get(0);
+        to(t.grad(q), dq);
+    });
+}
+
 }  // extern "C"

@@ -102,3 +102,27 @@ def test_merge_custom_op_on_reference_tape():
     np.testing.assert_array_equal(p1, p0)
     assert rel_l2(o1, o0) <= 1e-2 and rel_l2(f1, f0) <= 1e-2 and rel_l2(s1, s0) <= 1e-2
     assert abs(d1 - d0) <= 1e-2 * max(1.0, abs(d0))
+
+
+@pytest.mark.gpu
+def test_interp_custom_op_on_reference_tape():
+    """cuda::make_interp_op inside the reference's Tape vs the reference's own InterpOp
+    (knn rows from each side's knn: bit-identical neighbour lists)."""
+    L = _lib()
+    rng = np.random.default_rng(9)
+    keys = inputs.lattice_batch(1, 32, 0.75, 8, seed0=2)[0]
+    nk, dim, k, p = len(keys), 64, 8, 1.1
+    q = (rng.uniform(0, 256, (150, 2))).astype(np.float32).astype(np.float64)
+    q[0] = keys[5]
+    feats = inputs.bf16_round(rng.standard_normal((nk, dim)).astype(np.float32)).astype(np.float64)
+    w = inputs.bf16_round(rng.standard_normal((len(q), dim)).astype(np.float32)).astype(np.float64)
+    res = []
+    for use in (0, 1):
+        out, df, dq, dp = np.zeros((len(q), dim)), np.zeros((nk, dim)), np.zeros((len(q), 2)), C.c_double()
+        _ok(L, L.integ_interp_tape(C.c_int(use), C.c_int64(nk), C.c_int64(len(q)), C.c_int64(dim), C.c_int64(k),
+                                   _p(keys), _p(q), _p(feats), C.c_double(p), _p(w), _p(out), _p(df),
+                                   C.byref(dp), _p(dq)))
+        res.append((out, df, dp.value, dq))
+    (o0, f0, p0, q0), (o1, f1, p1, q1) = res
+    assert rel_l2(o1, o0) <= 1e-2 and rel_l2(f1, f0) <= 1e-2 and rel_l2(q1, q0) <= 1e-2
+    assert abs(p1 - p0) <= 1e-2 * max(1.0, abs(p0))
