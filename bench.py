@@ -63,6 +63,8 @@ def parse():
                     help="independent image groups per GPU, each on its own stream pair (images never "
                          "interact, so the groups' latency-bound phases overlap each other)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--interp-images", type=int, default=8,
+                    help="images of the side measurement of the interpolation op (SURVEY §8(f) #2); 0 = off")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -424,10 +426,11 @@ def run_ours(a, rank, world, dist):
 
     # e2e through the C ABI with host buffers (pinned H2D + D2H inside the timed region)
     e2e = run_e2e(a, host, dev, geom, h, d, ws, world, dist) if a.e2e_steps > 0 else {}
+    interp = run_interp(a, host, dev) if a.interp_images > 0 else None
 
     res = dict(value=value, ms=ms_max, phase_ms={p: float(np.median(v)) for p, v in phase_ms.items()},
                clocks=clocks.summary(), e2e=e2e, N=N, B=B, launches=launches,
-               graph=graph is not None)
+               graph=graph is not None, interp=interp)
     return res
 
 
@@ -452,6 +455,53 @@ def count_graph_kernels(graph):
         return kern
     except Exception:
         return None
+
+
+def run_interp(a, host, dev, k=8, reps=10):
+    """Side measurement (not part of the step): the decoder's softmax interpolation
+    (make_interp_op) of the encoder tokens onto every patch centre of the grid, knn rows
+    built once; fwd and bwd timed with CUDA events over `reps` calls each."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    nb = min(a.interp_images, host["coords"].shape[0])
+    keys = torch.as_tensor(host["coords"][:nb], device=dev).contiguous()
+    g = a.grid
+    cc = (np.arange(g) * 8.0 + 4.0).astype(np.float32)
+    q = np.stack(np.meshgrid(cc, cc), -1).reshape(1, -1, 2)
+    queries = torch.as_tensor(np.repeat(q, nb, 0), device=dev).contiguous()
+    D = a.heads * a.head_dim
+    feats = torch.randn((nb, keys.shape[1], D), device=dev).to(torch.bfloat16)
+    dout = torch.randn((nb, queries.shape[1], D), device=dev).to(torch.bfloat16)
+    p = torch.tensor([1.0], dtype=torch.float32, device=dev)
+    idx, valid = ops.knn(queries, keys, k)
+    dfe = torch.zeros((nb, keys.shape[1], D), dtype=torch.float32, device=dev)
+    dp = torch.zeros(1, dtype=torch.float32, device=dev)
+    dq = torch.zeros((nb, queries.shape[1], 2), dtype=torch.float32, device=dev)
+    for _ in range(2):
+        ops.interp_fwd(queries, keys, feats, idx, valid, p)
+        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    for _ in range(reps):
+        ops.interp_fwd(queries, keys, feats, idx, valid, p)
+    ev[1].record()
+    for _ in range(reps):
+        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq)
+    ev[2].record()
+    torch.cuda.synchronize()
+    fwd_ms, bwd_ms = ev[0].elapsed_time(ev[1]) / reps, ev[1].elapsed_time(ev[2]) / reps
+    nq = nb * queries.shape[1]
+    # algorithmic bytes per query: query xy 8 + k (idx 4 + valid 1) + output row 2D (fwd);
+    # + cotangent row 2D and dq 8 (bwd); each key row read once and (bwd) written once in fp32
+    kb = nb * keys.shape[1]
+    fwd_bytes = nq * (8 + 5 * k + 2 * D) + kb * (8 + 2 * D)
+    bwd_bytes = nq * (8 + 5 * k + 2 * D + 8) + kb * (8 + 2 * D + 2 * 4 * D)
+    return {"images": nb, "queries_per_image": int(queries.shape[1]), "keys_per_image": int(keys.shape[1]),
+            "k": k, "dim": D, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+            "fwd_queries_per_s": nq / (fwd_ms * 1e-3), "bwd_queries_per_s": nq / (bwd_ms * 1e-3),
+            "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
+            "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
 
 
 def e2e_bounds(B, chunks, ramp):
@@ -773,6 +823,8 @@ def main():
         "clocks": res["clocks"],
         "cuda_graph": res["graph"],
     }
+    if res.get("interp"):
+        line["next_ops"] = {"interp": res["interp"]}
     if not a.no_cpu_baseline and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(a)
