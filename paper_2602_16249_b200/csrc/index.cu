@@ -590,6 +590,186 @@ __global__ void knn_kernel(const float* __restrict__ queries, const float* __res
     }
 }
 
+// ---------------------------------------------- grid-accelerated exact knn
+// Large key sets: the image's keys are bucketed once into a uniform grid of
+// ~2 keys per cell (counting sort in global memory); each query (one thread)
+// walks square rings of cells around its own, keeping a sorted top-K of
+// (d^2 binary64, j), and stops once its K-th best d^2 is strictly below the
+// squared distance to every unvisited cell (minus a rounding margin) -- the
+// same selection as the brute-force scan, at O(K) candidates per query.
+struct KnnGrid {
+    double x0, y0, w;  // origin, cell side (square cells)
+    int g;             // cells per side
+    int pad;
+};
+__global__ void knn_grid_prm_kernel(const float* __restrict__ keys, int64_t nk, KnnGrid* __restrict__ prm) {
+    __shared__ float red[4][32];
+    const float2* kb = reinterpret_cast<const float2*>(keys) + int64_t(blockIdx.x) * nk;
+    float x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+    for (int64_t i = threadIdx.x; i < nk; i += blockDim.x) {
+        const float2 v = kb[i];
+        x0 = fminf(x0, v.x); x1 = fmaxf(x1, v.x); y0 = fminf(y0, v.y); y1 = fmaxf(y1, v.y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o)); x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+        y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o)); y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = x0; red[1][warp] = x1; red[2][warp] = y0; red[3][warp] = y1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+            x0 = fminf(x0, red[0][w]); x1 = fmaxf(x1, red[1][w]); y0 = fminf(y0, red[2][w]); y1 = fmaxf(y1, red[3][w]);
+        }
+        KnnGrid p;
+        p.g = max(1, min(1024, int(ceil(sqrt(double(nk) / 2.0)))));
+        const double ext = fmax(double(x1) - double(x0), double(y1) - double(y0));
+        p.w = ext > 0.0 ? ext / p.g * (1.0 + 1e-9) : 1.0;  // keys never land past the last cell
+        p.x0 = double(x0);
+        p.y0 = double(y0);
+        p.pad = 0;
+        prm[blockIdx.x] = p;
+    }
+}
+__device__ __forceinline__ int knn_cell(double v, double v0, double w, int g) {
+    return min(g - 1, max(0, int((v - v0) / w)));
+}
+__global__ void knn_grid_count_kernel(const float* __restrict__ keys, int64_t batch, int64_t nk,
+                                      const KnnGrid* __restrict__ prm, int64_t cells_cap, int32_t* __restrict__ cnt) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * nk) return;
+    const int64_t b = i / nk;
+    const KnnGrid p = prm[b];
+    const float2 v = reinterpret_cast<const float2*>(keys)[i];
+    atomicAdd(cnt + b * cells_cap + knn_cell(v.y, p.y0, p.w, p.g) * p.g + knn_cell(v.x, p.x0, p.w, p.g), 1);
+}
+__global__ void knn_grid_scan_kernel(int32_t* __restrict__ cnt, int64_t cells_cap, int32_t* __restrict__ cur) {
+    __shared__ int32_t part[1024];
+    int32_t* c = cnt + int64_t(blockIdx.x) * cells_cap;
+    int32_t* u = cur + int64_t(blockIdx.x) * cells_cap;
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int64_t per = (cells_cap + nt - 1) / nt, b0 = t * per, e0 = min(cells_cap, b0 + per);
+    int32_t s2 = 0;
+    for (int64_t i = b0; i < e0; ++i) s2 += c[i];
+    part[t] = s2;
+    __syncthreads();
+    for (int o = 1; o < nt; o <<= 1) {
+        const int32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - s2;
+    for (int64_t i = b0; i < e0; ++i) {
+        const int32_t v = c[i];
+        c[i] = run;
+        u[i] = run;
+        run += v;
+    }
+}
+__global__ void knn_grid_fill_kernel(const float* __restrict__ keys, int64_t batch, int64_t nk,
+                                     const KnnGrid* __restrict__ prm, int64_t cells_cap, int32_t* __restrict__ cur,
+                                     int32_t* __restrict__ items, float2* __restrict__ item_xy) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * nk) return;
+    const int64_t b = i / nk;
+    const KnnGrid p = prm[b];
+    const float2 v = reinterpret_cast<const float2*>(keys)[i];
+    const int c = knn_cell(v.y, p.y0, p.w, p.g) * p.g + knn_cell(v.x, p.x0, p.w, p.g);
+    const int pos = atomicAdd(cur + b * cells_cap + c, 1);
+    items[b * nk + pos] = int32_t(i - b * nk);
+    item_xy[b * nk + pos] = v;
+}
+template <int KM>
+__global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __restrict__ queries, int64_t batch,
+                                                             int64_t nq, int64_t nk, int k,
+                                                             const KnnGrid* __restrict__ prm, int64_t cells_cap,
+                                                             const int32_t* __restrict__ off,
+                                                             const int32_t* __restrict__ items,
+                                                             const float2* __restrict__ item_xy,
+                                                             int32_t* __restrict__ idx, uint8_t* __restrict__ valid) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= batch * nq) return;
+    const int64_t b = i / nq;
+    const KnnGrid p = prm[b];
+    const int32_t* co = off + b * cells_cap;
+    const int32_t* it = items + b * nk;
+    const float2* ixy = item_xy + b * nk;
+    const float2 q = reinterpret_cast<const float2*>(queries)[i];
+    const double qx = q.x, qy = q.y;
+    const int kept = int(k < nk ? k : nk);
+    double d[KM];
+    int jj[KM];
+#pragma unroll
+    for (int r = 0; r < KM; ++r) {
+        d[r] = INFINITY;
+        jj[r] = INT32_MAX;
+    }
+    const int g = p.g;
+    const int qcx = knn_cell(qx, p.x0, p.w, g), qcy = knn_cell(qy, p.y0, p.w, g);
+    int found = 0;
+    for (int ring = 0; ring <= g; ++ring) {
+        const int x0 = qcx - ring, x1 = qcx + ring, y0 = qcy - ring, y1 = qcy + ring;
+        // perimeter cells of the ring, row by row, as one flat loop (no lambda: the
+        // top-K list must stay in registers)
+        for (int cy = max(y0, 0); cy <= min(y1, g - 1); ++cy) {
+            const bool edge = cy == y0 || cy == y1;
+            const int ca = edge ? max(x0, 0) : x0, cb = edge ? min(x1, g - 1) : x1;
+            const int step = edge ? 1 : max(1, x1 - x0);
+            for (int cx = ca; cx <= cb; cx += step) {
+                if (cx < 0 || cx > g - 1) continue;
+                const int cell = cy * g + cx;
+                const int t1 = co[cell + 1];
+                for (int t = co[cell]; t < t1; ++t) {
+                    const float2 v = ixy[t];
+                    const int j = it[t];
+                    const double dx = __dsub_rn(double(v.x), qx), dy = __dsub_rn(double(v.y), qy);
+                    const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+                    ++found;
+                    if (!pair_lt(d2, j, d[KM - 1], jj[KM - 1])) continue;
+                    double nd = d2;
+                    int nj = j;
+#pragma unroll
+                    for (int r = 0; r < KM; ++r) {
+                        if (pair_lt(nd, nj, d[r], jj[r])) {
+                            const double td = d[r];
+                            const int tj = jj[r];
+                            d[r] = nd;
+                            jj[r] = nj;
+                            nd = td;
+                            nj = tj;
+                        }
+                    }
+                }
+            }
+        }
+        if (x0 <= 0 && y0 <= 0 && x1 >= g - 1 && y1 >= g - 1) break;  // whole grid searched
+        if (found >= kept) {
+            // distance from q to the outside of the searched (2 ring + 1)^2 block
+            double lb = INFINITY;
+            if (x0 > 0) lb = fmin(lb, qx - (p.x0 + x0 * p.w));
+            if (x1 < g - 1) lb = fmin(lb, p.x0 + (x1 + 1) * p.w - qx);
+            if (y0 > 0) lb = fmin(lb, qy - (p.y0 + y0 * p.w));
+            if (y1 < g - 1) lb = fmin(lb, p.y0 + (y1 + 1) * p.w - qy);
+            lb -= 1e-9 * p.w * g;
+            double dk = INFINITY;
+#pragma unroll
+            for (int r = 0; r < KM; ++r)
+                if (r == kept - 1) dk = d[r];
+            if (lb > 0.0 && dk < lb * lb) break;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < KM; ++r)
+        if (r < k) {
+            idx[i * k + r] = r < kept ? jj[r] : 0;
+            valid[i * k + r] = r < kept ? 1 : 0;
+        }
+}
+
 // ================================================================= host
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -743,9 +923,47 @@ int knn(const float* queries, const float* keys, int64_t batch, int64_t nq, int6
     if (k > kKnnMax) return fail(AFFMAE_EUNSUPPORTED, "knn: k > 32 not compiled");
     if (!queries || !keys || !idx || !valid) return fail(AFFMAE_ECONFIG, "knn: null pointer");
     if (batch * nq == 0) return AFFMAE_OK;
-    knn_kernel<<<blocks(batch * nq * 32), 256, 0, as_stream(stream)>>>(queries, keys, batch, nq, nk,
-                                                                       int(k), idx, valid);
-    AFFMAE_LAUNCH_CHECK("knn_kernel");
+    cudaStream_t st = as_stream(stream);
+    if (nk < 512 || nq * nk < (int64_t(1) << 20)) {  // small problems: brute force
+        knn_kernel<<<blocks(batch * nq * 32), 256, 0, st>>>(queries, keys, batch, nq, nk, int(k), idx, valid);
+        AFFMAE_LAUNCH_CHECK("knn_kernel");
+        return AFFMAE_OK;
+    }
+    // grid state from the stream-ordered allocator (capturable; freed on the stream)
+    const int gmax = max(1, min(1024, int(std::ceil(std::sqrt(double(nk) / 2.0)))));
+    const int64_t cells_cap = int64_t(gmax) * gmax + 1;
+    const size_t bytes = align256(size_t(batch) * sizeof(KnnGrid)) + 2 * align256(size_t(batch) * cells_cap * 4) +
+                         align256(size_t(batch) * nk * 4) + align256(size_t(batch) * nk * 8);
+    uint8_t* base = nullptr;
+    AFFMAE_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&base), bytes, st));
+    uint8_t* q = base;
+    auto take = [&](size_t n) {
+        uint8_t* r = q;
+        q += align256(n);
+        return r;
+    };
+    auto* prm = reinterpret_cast<KnnGrid*>(take(size_t(batch) * sizeof(KnnGrid)));
+    auto* cnt = reinterpret_cast<int32_t*>(take(size_t(batch) * cells_cap * 4));
+    auto* cur = reinterpret_cast<int32_t*>(take(size_t(batch) * cells_cap * 4));
+    auto* items = reinterpret_cast<int32_t*>(take(size_t(batch) * nk * 4));
+    auto* ixy = reinterpret_cast<float2*>(take(size_t(batch) * nk * 8));
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(cnt, 0, size_t(batch) * cells_cap * 4, st));
+    knn_grid_prm_kernel<<<unsigned(batch), 256, 0, st>>>(keys, nk, prm);
+    knn_grid_count_kernel<<<blocks(batch * nk), 256, 0, st>>>(keys, batch, nk, prm, cells_cap, cnt);
+    knn_grid_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(cnt, cells_cap, cur);
+    knn_grid_fill_kernel<<<blocks(batch * nk), 256, 0, st>>>(keys, batch, nk, prm, cells_cap, cur, items, ixy);
+    const unsigned nb = unsigned((batch * nq + 127) / 128);
+    if (k <= 8)
+        knn_grid_query_kernel<8><<<nb, 128, 0, st>>>(queries, batch, nq, nk, int(k), prm, cells_cap, cnt, items, ixy,
+                                                      idx, valid);
+    else if (k <= 16)
+        knn_grid_query_kernel<16><<<nb, 128, 0, st>>>(queries, batch, nq, nk, int(k), prm, cells_cap, cnt, items,
+                                                       ixy, idx, valid);
+    else
+        knn_grid_query_kernel<32><<<nb, 128, 0, st>>>(queries, batch, nq, nk, int(k), prm, cells_cap, cnt, items,
+                                                       ixy, idx, valid);
+    AFFMAE_LAUNCH_CHECK("knn_grid");
+    AFFMAE_CUDA_CHECK(cudaFreeAsync(base, st));
     return AFFMAE_OK;
 }
 

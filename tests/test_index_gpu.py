@@ -79,7 +79,10 @@ def test_sfc_order_bit_exact(n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nq,nk,k", [(10, 40, 12), (50, 7, 10), (64, 300, 32), (5, 5, 3)])
+@pytest.mark.parametrize("nq,nk,k", [(10, 40, 12), (50, 7, 10), (64, 300, 32), (5, 5, 3),
+                                     # grid-accelerated path (nk >= 512, nq*nk >= 2^20, k <= 16)
+                                     (3000, 2000, 8), (1500, 1000, 16), (2100, 600, 5), (2000, 4000, 1),
+                                     (1200, 1500, 32), (1100, 1000, 24)])
 def test_knn_bit_exact(nq, nk, k):
     import torch
     from paper_2602_16249_b200 import ops
