@@ -769,3 +769,39 @@ int orc_interp_bwd(int64_t nq, int64_t dim, int64_t k, const double* queries, co
     return 0;
 }
 
+/* ---------------------------------------------------------------- AdamW
+ * AdamW::lr_at / AdamW::step (proj/src/pipeline.cpp:643-680): linear warmup then
+ * cosine; moments in binary64; decoupled decay for matrices only (rows > 1);
+ * values stored at the tape precision (b32).  One step over n_params tensors
+ * laid out back to back; m/v [P] carry the moments between calls. */
+double orc_adamw_lr(double lr, int64_t warmup, int64_t total, int64_t step) {
+    if (step < warmup) return lr * (double)(step + 1) / (double)warmup;
+    int64_t span = total - warmup > 1 ? total - warmup : 1;
+    double prog = (double)(step - warmup) / (double)span;
+    prog = prog < 1.0 ? prog : 1.0;
+    return lr * 0.5 * (1.0 + cos(3.14159265358979323846 * prog));
+}
+
+int orc_adamw_step(double lr, int64_t warmup, double wd, double beta1, double beta2, int64_t total, int64_t step,
+                   int64_t n_params, const int64_t* rows, const int64_t* cols, const double* grad, double* value,
+                   double* m, double* v) {
+    const double a = orc_adamw_lr(lr, warmup, total, step), n = (double)(step + 1);
+    const double bc1 = 1.0 - pow(beta1, n), bc2 = 1.0 - pow(beta2, n);
+    int64_t o = 0;
+    for (int64_t t = 0; t < n_params; ++t) {
+        const int decay = rows[t] > 1;
+        for (int64_t e = 0; e < rows[t] * cols[t]; ++e, ++o) {
+            double g = grad[o];
+            double mi = beta1 * m[o] + (1.0 - beta1) * g;
+            double vi = beta2 * v[o] + (1.0 - beta2) * g * g;
+            m[o] = mi;
+            v[o] = vi;
+            double upd = (mi / bc1) / (sqrt(vi / bc2) + 1e-8);
+            double val = value[o];
+            if (decay) val -= a * wd * val;
+            value[o] = (double)(float)(val - a * upd);
+        }
+    }
+    return 0;
+}
+

@@ -79,6 +79,12 @@ int orc_interp_bwd(int64_t nq, int64_t dim, int64_t k, const double* queries, co
                    const double* feats, const int64_t* idx, const uint8_t* valid, double p, double eps,
                    const double* dout, double* dfeats, double* dp, double* dq);
 
+/* AdamW::lr_at / AdamW::step (pipeline.cpp:643-680) */
+double orc_adamw_lr(double lr, int64_t warmup, int64_t total, int64_t step);
+int orc_adamw_step(double lr, int64_t warmup, double wd, double beta1, double beta2, int64_t total, int64_t step,
+                   int64_t n_params, const int64_t* rows, const int64_t* cols, const double* grad, double* value,
+                   double* m, double* v);
+
 #ifdef __cplusplus
 }
 #endif

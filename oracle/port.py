@@ -241,3 +241,20 @@ def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, prec=3
                                 _p(idx), _p(valid), C.c_double(p), C.c_double(eps), _p(dout), _p(df), _p(dp),
                                 _p(dq)))
     return df, float(dp[0]), dq
+
+
+
+def adamw(shapes, values, grads, lr=1e-3, warmup=100, wd=0.05, beta1=0.883, beta2=0.935, total=1000):
+    """AdamW::step (pipeline.cpp:650-680) restated in oracle.c, len(grads) steps from zero moments;
+    returns the values and the binary64 moments."""
+    rows = np.array([s[0] for s in shapes], np.int64)
+    cols = np.array([s[1] for s in shapes], np.int64)
+    vals = _f64(values).copy()
+    m = np.zeros_like(vals)
+    v = np.zeros_like(vals)
+    for st, g in enumerate(_f64(grads)):
+        g = np.ascontiguousarray(g.astype(np.float32).astype(np.float64))  # grads live at b32 on the tape
+        _check(lib().orc_adamw_step(C.c_double(lr), C.c_int64(warmup), C.c_double(wd), C.c_double(beta1),
+                                    C.c_double(beta2), C.c_int64(total), C.c_int64(st), C.c_int64(len(shapes)),
+                                    _p(rows), _p(cols), _p(g), _p(vals), _p(m), _p(v)))
+    return vals, m, v

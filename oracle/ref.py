@@ -235,6 +235,18 @@ def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, prec=3
     return df, dp.value, dq
 
 
+def adamw(shapes, values, grads, lr=1e-3, warmup=100, wd=0.05, beta1=0.883, beta2=0.935, total=1000):
+    """AdamW::step of the compiled reference, len(grads) steps; values/grads flat in tensor order."""
+    rows = np.array([s[0] for s in shapes], np.int64)
+    cols = np.array([s[1] for s in shapes], np.int64)
+    vals = _f64(values).copy()
+    g = _f64(grads)
+    _check(lib().ref_adamw(C.c_double(lr), C.c_int64(warmup), C.c_double(wd), C.c_double(beta1),
+                           C.c_double(beta2), C.c_int64(total), C.c_int64(len(shapes)), _p(rows), _p(cols),
+                           C.c_int64(g.shape[0]), _p(g), _p(vals)))
+    return vals
+
+
 def perlin_mask(grid, ratio, seed):
     m = np.empty(grid * grid, np.uint8)
     _check(lib().ref_perlin_mask(C.c_int64(grid), C.c_double(ratio), C.c_uint64(seed), _p(m)))

@@ -33,6 +33,7 @@
 #include "affmae/interpolation.hpp"
 #include "affmae/masking.hpp"
 #include "affmae/merging.hpp"
+#include "affmae/pipeline.hpp"
 #include "affmae/tape.hpp"
 #include "affmae/tensor.hpp"
 
@@ -358,6 +359,44 @@ int ref_interp_bwd(int64_t nq, int64_t nk, int64_t dim, int64_t k, const double*
         to(df, dfeats);
         *dp = dpt.get(0);
         to(dqt, dq);
+    });
+}
+
+// AdamW (pipeline.cpp:639-680): `steps` optimizer steps over n_params tensors of
+// rows[i] x cols[i] (b32 values, decay iff rows > 1), grads [steps][P] in tensor
+// order; values [P] in, updated in place.
+int ref_adamw(double lr, int64_t warmup, double wd, double beta1, double beta2, int64_t total, int64_t n_params,
+              const int64_t* rows, const int64_t* cols, int64_t steps, const double* grads, double* values) {
+    return guarded([&] {
+        OptimConfig oc;
+        oc.lr = lr;
+        oc.warmup = warmup;
+        oc.weight_decay = wd;
+        oc.beta1 = beta1;
+        oc.beta2 = beta2;
+        AdamW opt(oc, total);
+        std::vector<Parameter> ps;
+        int64_t total_el = 0;
+        for (int64_t i = 0; i < n_params; ++i) {
+            Tensor v = from(values + total_el, {rows[i], cols[i]}, Precision::b32);
+            ps.emplace_back("p" + std::to_string(i), v);
+            total_el += rows[i] * cols[i];
+        }
+        std::vector<Parameter*> pp;
+        for (auto& q : ps) pp.push_back(&q);
+        for (int64_t st = 0; st < steps; ++st) {
+            int64_t o = 0;
+            for (auto& q : ps) {
+                for (int64_t e = 0; e < q.value.numel(); ++e) q.grad.set(e, grads[st * total_el + o + e]);
+                o += q.value.numel();
+            }
+            opt.step(pp);
+        }
+        int64_t o = 0;
+        for (auto& q : ps) {
+            for (int64_t e = 0; e < q.value.numel(); ++e) values[o + e] = q.value.get(e);
+            o += q.value.numel();
+        }
     });
 }
 

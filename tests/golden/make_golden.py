@@ -108,6 +108,17 @@ def main():
                     f"itp_{name}_valid": valid, f"itp_{name}_feats": feats, f"itp_{name}_dout": dd,
                     f"itp_{name}_p": np.array([p_]), f"itp_{name}_out": io, f"itp_{name}_dfeats": df,
                     f"itp_{name}_dp": np.array([dp]), f"itp_{name}_dq": dq})
+    # AdamW (pipeline.cpp:639-680): matrices and vectors, warmup and cosine phases
+    arng = np.random.default_rng(680)
+    shapes = [(4, 6), (1, 6), (7, 3), (1, 1), (3, 1)]
+    P = sum(a * b for a, b in shapes)
+    vals = arng.standard_normal(P).astype(np.float32).astype(np.float64)
+    grads = (arng.standard_normal((6, P)) * 0.1).astype(np.float32).astype(np.float64)
+    out["adamw_shapes"] = np.array(shapes, np.int64)
+    out["adamw_values"] = vals
+    out["adamw_grads"] = grads
+    out["adamw_out_w2_t6"] = ref.adamw(shapes, vals, grads, warmup=2, total=6)
+    out["adamw_out_w100_t1000"] = ref.adamw(shapes, vals, grads, warmup=100, total=1000)
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print(f"wrote {len(out)} arrays")
 

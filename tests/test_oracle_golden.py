@@ -191,3 +191,11 @@ def test_interp_known_answers():
     out4 = port.interp_fwd(np.zeros((1, 2)), kc4, np.arange(4.0).reshape(4, 1), np.array([[0, 1, 2, 3]]),
                            np.ones((1, 4), np.uint8), 5.0, prec=64)
     assert abs(out4[0, 0] - 1.5) <= 1e-12
+
+
+def test_adamw_matches_reference():
+    """AdamW::step (pipeline.cpp:639-680): warmup / cosine schedule, matrix-only decay, b32 values."""
+    shapes = [tuple(s) for s in G["adamw_shapes"]]
+    for warm, total, key in ((2, 6, "adamw_out_w2_t6"), (100, 1000, "adamw_out_w100_t1000")):
+        vals, _, _ = port.adamw(shapes, G["adamw_values"], G["adamw_grads"], warmup=warm, total=total)
+        np.testing.assert_array_equal(vals, G[key])
