@@ -427,10 +427,11 @@ def run_ours(a, rank, world, dist):
     # e2e through the C ABI with host buffers (pinned H2D + D2H inside the timed region)
     e2e = run_e2e(a, host, dev, geom, h, d, ws, world, dist) if a.e2e_steps > 0 else {}
     interp = run_interp(a, host, dev) if a.interp_images > 0 else None
+    adamw = run_adamw(dev) if a.interp_images > 0 else None
 
     res = dict(value=value, ms=ms_max, phase_ms={p: float(np.median(v)) for p, v in phase_ms.items()},
                clocks=clocks.summary(), e2e=e2e, N=N, B=B, launches=launches,
-               graph=graph is not None, interp=interp)
+               graph=graph is not None, interp=interp, adamw=adamw)
     return res
 
 
@@ -502,6 +503,40 @@ def run_interp(a, host, dev, k=8, reps=10):
             "fwd_queries_per_s": nq / (fwd_ms * 1e-3), "bwd_queries_per_s": nq / (bwd_ms * 1e-3),
             "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
             "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
+
+
+def run_adamw(dev, params=91_000_000, reps=20):
+    """Side measurement: one fused AdamW step over an AFF-B-sized parameter set
+    (~91 M fp32, matrices and vectors), 28 algorithmic bytes per parameter, against the HBM peak."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    shapes = []
+    left = params
+    while left > 0:  # 1024x1024 matrices plus one bias vector each, like the dense layers
+        n = min(left, 1024 * 1024)
+        shapes.append((max(2, n // 1024), 1024) if n >= 2048 else (n,))
+        left -= int(np.prod(shapes[-1]))
+        if left > 0:
+            shapes.append((1024,))
+            left -= 1024
+    opt = ops.AdamW(shapes, total_steps=1000, device=dev)
+    opt.grad.normal_()
+    opt.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        opt.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    n = sum(int(np.prod(s)) for s in shapes)
+    gbs = 28.0 * n / (ms * 1e-3) / 1e9
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs") or peaks.get("hbm_copy_gbs") or 6553.6
+    return {"params": n, "tensors": len(shapes), "ms": ms, "gbs": gbs, "hbm_frac": gbs / float(peak),
+            "note": "side measurement of SURVEY §8(f) #3 (fused AdamW), not part of the step"}
 
 
 def e2e_bounds(B, chunks, ramp):
@@ -825,6 +860,8 @@ def main():
     }
     if res.get("interp"):
         line["next_ops"] = {"interp": res["interp"]}
+        if res.get("adamw"):
+            line["next_ops"]["adamw"] = res["adamw"]
     if not a.no_cpu_baseline and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(a)

@@ -115,6 +115,25 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream);
 
+/* Replaces AdamW (include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680):
+ * one optimizer step over every parameter tensor at once.  The tensors live back
+ * to back in flat fp32 buffers value/grad/m/v [n] (16-byte aligned; m, v start at
+ * zero like the reference's moments); seg_off [n_segments] (DEVICE, ascending
+ * start offsets, seg_off[0] = 0) and seg_decay [n_segments] (DEVICE, 1 iff the
+ * tensor is a matrix, dim(0) > 1) describe them.  `step` is the number of steps
+ * already taken (AdamW::t_): lr_at(step), bias corrections with n = step + 1. */
+typedef struct affmae_adamw_cfg {
+    double lr;             /* OptimConfig::lr (include/affmae/config.hpp:27-33) */
+    int64_t warmup;
+    double weight_decay;
+    double beta1, beta2;
+    int64_t total_steps;   /* AdamW(cfg, total_steps) */
+} affmae_adamw_cfg;
+double affmae_adamw_lr(const affmae_adamw_cfg* cfg, int64_t step);
+int affmae_adamw_step(const affmae_adamw_cfg* cfg, int64_t step, int64_t n_segments, const int64_t* seg_off,
+                      const uint8_t* seg_decay, int64_t n, float* value, const float* grad, float* m, float* v,
+                      void* stream);
+
 /* ------------------------------------------------------------------------
  * Cluster attention (nbhd_attn_streaming / nbhd_attn_backward,
  * include/affmae/attention.hpp:52-72; AttnOp, src/attention.cpp:374-444).

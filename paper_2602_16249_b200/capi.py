@@ -28,6 +28,7 @@ EXPORTS = (
     "affmae_retained_count", "affmae_select_retained_workspace", "affmae_select_retained",
     "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
     "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd", "affmae_interp_fwd", "affmae_interp_bwd",
+    "affmae_adamw_lr", "affmae_adamw_step",
 )
 
 
@@ -52,6 +53,11 @@ class AttnDesc(C.Structure):
 class AttnInputs(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("q", "k", "v", "blank_k", "blank_v", "coords", "w1",
                                           "b1", "w2", "b2", "blank")]
+
+
+class AdamwCfg(C.Structure):
+    _fields_ = [("lr", C.c_double), ("warmup", C.c_int64), ("weight_decay", C.c_double),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("total_steps", C.c_int64)]
 
 
 class AttnGrads(C.Structure):
@@ -83,6 +89,8 @@ def lib():
         L.affmae_last_error.restype = C.c_char_p
         L.affmae_retained_count.restype = C.c_int64
         L.affmae_retained_count.argtypes = [C.c_int64, C.c_double]
+        if hasattr(L, "affmae_adamw_lr"):
+            L.affmae_adamw_lr.restype = C.c_double
         for f in ("affmae_cluster_index_workspace", "affmae_sfc_order_workspace",
                   "affmae_attn_fwd_workspace", "affmae_attn_plan_workspace",
                   "affmae_attn_fwd_planned_workspace", "affmae_attn_bwd_planned_workspace",

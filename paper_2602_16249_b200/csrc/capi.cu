@@ -54,6 +54,9 @@ int interp_fwd(const float*, const float*, const void*, const int32_t*, const ui
 int interp_bwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
                int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*);
 int64_t retained_count_impl(int64_t, double);
+double adamw_lr(const affmae_adamw_cfg*, int64_t);
+int adamw_step(const affmae_adamw_cfg*, int64_t, int64_t, const int64_t*, const uint8_t*, int64_t, float*, const float*,
+               float*, float*, void*);
 size_t select_retained_workspace(int64_t, int64_t);
 int select_retained(const float*, int64_t, int64_t, double, int32_t*, void*, size_t, void*);
 size_t merge_plan_workspace(int64_t, int64_t, int64_t);
@@ -184,6 +187,14 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream) {
     return interp_bwd(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
                       dfeats, dp, dqueries, stream);
+}
+
+// AdamW::lr_at / AdamW::step (proj/src/pipeline.cpp:643-680)
+double affmae_adamw_lr(const affmae_adamw_cfg* cfg, int64_t step) { return cfg ? adamw_lr(cfg, step) : 0.0; }
+int affmae_adamw_step(const affmae_adamw_cfg* cfg, int64_t step, int64_t n_segments, const int64_t* seg_off,
+                      const uint8_t* seg_decay, int64_t n, float* value, const float* grad, float* m, float* v,
+                      void* stream) {
+    return adamw_step(cfg, step, n_segments, seg_off, seg_decay, n, value, grad, m, v, stream);
 }
 
 // retained_count (proj/src/merging.cpp:50-54)

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import capi
@@ -332,6 +333,40 @@ def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, dfeats
         C.c_void_p(dfeats.data_ptr()), C.c_void_p(dp.data_ptr()), C.c_void_p(dqueries.data_ptr()),
         _stream(stream)), "interp_bwd")
     return dfeats, dp, dqueries
+
+
+# ---------------------------------------------------------------- optimizer
+class AdamW:
+    """AdamW (proj/include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680) over a list of
+    fp32 CUDA parameter tensors: they are packed back to back in one flat buffer (the tensors
+    become views into it), with flat grad / moment buffers, and every step is one fused launch."""
+
+    def __init__(self, shapes, lr=1e-3, warmup=100, weight_decay=0.05, beta1=0.883, beta2=0.935,
+                 total_steps=1000, device="cuda"):
+        self.cfg = capi.AdamwCfg(lr, warmup, weight_decay, beta1, beta2, total_steps)
+        sizes = [int(np.prod(s)) for s in shapes]
+        offs = np.concatenate([[0], np.cumsum([(z + 3) // 4 * 4 for z in sizes])]).astype(np.int64)
+        n = int(offs[-1])
+        f32 = dict(dtype=torch.float32, device=device)
+        self.value, self.grad = torch.zeros(n, **f32), torch.zeros(n, **f32)
+        self.m, self.v = torch.zeros(n, **f32), torch.zeros(n, **f32)
+        self.params = [self.value[o:o + z].view(*s) for o, z, s in zip(offs[:-1], sizes, shapes)]
+        self.grads = [self.grad[o:o + z].view(*s) for o, z, s in zip(offs[:-1], sizes, shapes)]
+        self.seg_off = torch.as_tensor(offs[:-1], device=device)
+        self.seg_decay = torch.as_tensor(np.array([1 if s[0] > 1 else 0 for s in shapes], np.uint8),
+                                         device=device)
+        self.t = 0
+
+    def lr_at(self, step):
+        return capi.lib().affmae_adamw_lr(C.byref(self.cfg), C.c_int64(step))
+
+    def step(self, stream=None):
+        capi.check(capi.lib().affmae_adamw_step(
+            C.byref(self.cfg), C.c_int64(self.t), C.c_int64(len(self.params)), C.c_void_p(self.seg_off.data_ptr()),
+            C.c_void_p(self.seg_decay.data_ptr()), C.c_int64(self.value.numel()), C.c_void_p(self.value.data_ptr()),
+            C.c_void_p(self.grad.data_ptr()), C.c_void_p(self.m.data_ptr()), C.c_void_p(self.v.data_ptr()),
+            _stream(stream)), "adamw_step")
+        self.t += 1
 
 
 # -------------------------------------------------------------------- merge
