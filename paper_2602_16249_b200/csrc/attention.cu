@@ -870,10 +870,16 @@ static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, cons
     p.lsd = w.lsd;
     p.dtab_g = w.dtab_g;
     p.part = w.part;
-    int rc = prepare_run(p, w, st);
+    // BiasNet table (st) and the zeroed table-gradient replicas (side stream) are independent
+    int rc = launch_forked(
+        st,
+        [&](cudaStream_t s) {
+            dtab_zero_kernel<<<4 * kNumSMs, 256, 0, s>>>(w.dtab_g, a->heads, w.rmax);
+            AFFMAE_LAUNCH_CHECK("dtab_zero_kernel");
+            return AFFMAE_OK;
+        },
+        [&](cudaStream_t s) { return prepare_run(p, w, s); });
     if (rc) return rc;
-    dtab_zero_kernel<<<4 * kNumSMs, 256, 0, st>>>(w.dtab_g, a->heads, w.rmax);
-    AFFMAE_LAUNCH_CHECK("dtab_zero_kernel");
     int gx[2] = {0, 0};
     if ((rc = dispatch_bwd_q(p, a->head_dim, g->width, st, gx))) return rc;
     // The parameter-gradient chain needs only the query side's partials: it runs on
