@@ -711,7 +711,9 @@ __global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __rest
     const int g = p.g;
     const int qcx = knn_cell(qx, p.x0, p.w, g), qcy = knn_cell(qy, p.y0, p.w, g);
     int found = 0;
-    for (int ring = 0; ring <= g; ++ring) {
+    bool done = false;
+    constexpr int kMaxRings = 24;  // far / clumped cases: exact scan of all keys instead
+    for (int ring = 0; ring <= min(g, kMaxRings); ++ring) {
         const int x0 = qcx - ring, x1 = qcx + ring, y0 = qcy - ring, y1 = qcy + ring;
         // perimeter cells of the ring, row by row, as one flat loop (no lambda: the
         // top-K list must stay in registers)
@@ -746,7 +748,10 @@ __global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __rest
                 }
             }
         }
-        if (x0 <= 0 && y0 <= 0 && x1 >= g - 1 && y1 >= g - 1) break;  // whole grid searched
+        if (x0 <= 0 && y0 <= 0 && x1 >= g - 1 && y1 >= g - 1) {  // whole grid searched
+            done = true;
+            break;
+        }
         if (found >= kept) {
             // distance from q to the outside of the searched (2 ring + 1)^2 block
             double lb = INFINITY;
@@ -759,7 +764,37 @@ __global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __rest
 #pragma unroll
             for (int r = 0; r < KM; ++r)
                 if (r == kept - 1) dk = d[r];
-            if (lb > 0.0 && dk < lb * lb) break;
+            if (lb > 0.0 && dk < lb * lb) {
+                done = true;
+                break;
+            }
+        }
+    }
+    if (!done) {  // ring budget exhausted: brute force over the image's keys (same order rule)
+#pragma unroll
+        for (int r = 0; r < KM; ++r) {
+            d[r] = INFINITY;
+            jj[r] = INT32_MAX;
+        }
+        for (int64_t t = 0; t < nk; ++t) {
+            const float2 v = ixy[t];
+            const int j = it[t];
+            const double dx = __dsub_rn(double(v.x), qx), dy = __dsub_rn(double(v.y), qy);
+            const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+            if (!pair_lt(d2, j, d[KM - 1], jj[KM - 1])) continue;
+            double nd = d2;
+            int nj = j;
+#pragma unroll
+            for (int r = 0; r < KM; ++r) {
+                if (pair_lt(nd, nj, d[r], jj[r])) {
+                    const double td = d[r];
+                    const int tj = jj[r];
+                    d[r] = nd;
+                    jj[r] = nj;
+                    nd = td;
+                    nj = tj;
+                }
+            }
         }
     }
 #pragma unroll

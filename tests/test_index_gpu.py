@@ -79,6 +79,22 @@ def test_sfc_order_bit_exact(n):
 
 
 @pytest.mark.gpu
+def test_knn_far_and_clumped_queries():
+    """Grid path safety net: keys clumped in a corner, queries far away (ring budget
+    exhausted -> exact scan), plus many identical keys (index tie-break)."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    rng = np.random.default_rng(77)
+    keys = np.concatenate([rng.uniform(0, 3, (1, 900, 2)), np.full((1, 300, 2), 1.5)], 1).astype(np.float32)
+    q = rng.uniform(500, 2000, (1, 1200, 2)).astype(np.float32)
+    q[0, :200] = rng.uniform(0, 3, (200, 2))
+    idx, valid = ops.knn(_dev(q, torch.float32), _dev(keys, torch.float32), 8)
+    wi, wv = port.knn(q[0], keys[0], 8)
+    np.testing.assert_array_equal(valid.cpu().numpy()[0], wv)
+    np.testing.assert_array_equal(idx.cpu().numpy()[0], wi)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("nq,nk,k", [(10, 40, 12), (50, 7, 10), (64, 300, 32), (5, 5, 3),
                                      # grid-accelerated path (nk >= 512, nq*nk >= 2^20, k <= 16)
                                      (3000, 2000, 8), (1500, 1000, 16), (2100, 600, 5), (2000, 4000, 1),
