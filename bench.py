@@ -428,10 +428,11 @@ def run_ours(a, rank, world, dist):
     e2e = run_e2e(a, host, dev, geom, h, d, ws, world, dist) if a.e2e_steps > 0 else {}
     interp = run_interp(a, host, dev) if a.interp_images > 0 else None
     adamw = run_adamw(dev) if a.interp_images > 0 else None
+    linear = run_linear(dev) if a.interp_images > 0 else None
 
     res = dict(value=value, ms=ms_max, phase_ms={p: float(np.median(v)) for p, v in phase_ms.items()},
                clocks=clocks.summary(), e2e=e2e, N=N, B=B, launches=launches,
-               graph=graph is not None, interp=interp, adamw=adamw)
+               graph=graph is not None, interp=interp, adamw=adamw, linear=linear)
     return res
 
 
@@ -503,6 +504,44 @@ def run_interp(a, host, dev, k=8, reps=10):
             "fwd_queries_per_s": nq / (fwd_ms * 1e-3), "bwd_queries_per_s": nq / (bwd_ms * 1e-3),
             "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
             "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
+
+
+def run_linear(dev, reps=20):
+    """Side measurement: the tcgen05 linear layer at the op sweep's MLP shape
+    (all 32 x 16384 tokens, D = 128 -> 4D with bias + GELU fused; HBM-bound at ~100 flop/B) and
+    at a compute-bound 8192^3, against the measured bf16 tensor peak."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except (OSError, ValueError):
+        peaks = {}
+    tc_peak = float(peaks.get("bf16_tflops") or 1644.8)
+    hbm_peak = float(peaks.get("hbm_gbs") or 6553.6)
+    out = {}
+    for name, (m, n, k, act) in {"mlp_fc1": (32 * 16384, 512, 128, "gelu"),
+                                 "square_8192": (8192, 8192, 8192, "none")}.items():
+        x = torch.randn((m, k), device=dev).to(torch.bfloat16)
+        w = (torch.randn((n, k), device=dev) / k ** 0.5).to(torch.bfloat16)
+        b = torch.zeros(n, dtype=torch.float32, device=dev)
+        for _ in range(2):
+            ops.linear(x, w, b, act=act)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            ops.linear(x, w, b, act=act)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
+        gbs = 2.0 * (m * k + n * k + m * n) / (ms * 1e-3) / 1e9
+        out[name] = {"m": m, "n": n, "k": k, "act": act, "ms": ms, "tflops": tf, "tc_frac": tf / tc_peak,
+                     "gbs": gbs, "hbm_frac": gbs / hbm_peak}
+        del x, w, b
+    out["note"] = "side measurement of SURVEY §8(f) #1 (tcgen05 linear + fused bias/GELU), not part of the step"
+    return out
 
 
 def run_adamw(dev, params=91_000_000, reps=20):
@@ -862,6 +901,8 @@ def main():
         line["next_ops"] = {"interp": res["interp"]}
         if res.get("adamw"):
             line["next_ops"]["adamw"] = res["adamw"]
+        if res.get("linear"):
+            line["next_ops"]["linear"] = res["linear"]
     if not a.no_cpu_baseline and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(a)

@@ -134,6 +134,15 @@ int affmae_adamw_step(const affmae_adamw_cfg* cfg, int64_t step, int64_t n_segme
                       const uint8_t* seg_decay, int64_t n, float* value, const float* grad, float* m, float* v,
                       void* stream);
 
+/* Dense linear layer on the tcgen05 tensor cores (the model's QKV / output /
+ * MLP / merge projections: Tape matmul + bias (+ gelu_erf), src/tape.cpp,
+ * src/pipeline.cpp:388-400,453-458):  y = act(x W^T + b), x [M, K] bf16
+ * row-major, W [N, K] bf16 row-major, b [N] fp32, act 0 = identity, 1 = GELU
+ * (erf); y [M, N] bf16.  K and N multiples of 8. */
+size_t affmae_linear_workspace(int64_t m, int64_t n, int64_t k);
+int affmae_linear_fwd(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
+                      int64_t k, int act, affmae_bf16* y, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------
  * Cluster attention (nbhd_attn_streaming / nbhd_attn_backward,
  * include/affmae/attention.hpp:52-72; AttnOp, src/attention.cpp:374-444).

@@ -28,7 +28,7 @@ EXPORTS = (
     "affmae_retained_count", "affmae_select_retained_workspace", "affmae_select_retained",
     "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
     "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd", "affmae_interp_fwd", "affmae_interp_bwd",
-    "affmae_adamw_lr", "affmae_adamw_step",
+    "affmae_adamw_lr", "affmae_adamw_step", "affmae_linear_workspace", "affmae_linear_fwd",
 )
 
 

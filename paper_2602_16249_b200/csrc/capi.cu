@@ -55,6 +55,8 @@ int interp_bwd(const float*, const float*, const void*, const int32_t*, const ui
                int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
+size_t linear_workspace(int64_t, int64_t, int64_t);
+int linear_fwd(const void*, const void*, const float*, int64_t, int64_t, int64_t, int, void*, void*, size_t, void*);
 int adamw_step(const affmae_adamw_cfg*, int64_t, int64_t, const int64_t*, const uint8_t*, int64_t, float*, const float*,
                float*, float*, void*);
 size_t select_retained_workspace(int64_t, int64_t);
@@ -187,6 +189,13 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream) {
     return interp_bwd(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
                       dfeats, dp, dqueries, stream);
+}
+
+// dense linear layer (Tape matmul + bias + gelu_erf), tcgen05
+size_t affmae_linear_workspace(int64_t m, int64_t n, int64_t k) { return linear_workspace(m, n, k); }
+int affmae_linear_fwd(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
+                      int64_t k, int act, affmae_bf16* y, void* workspace, size_t workspace_bytes, void* stream) {
+    return linear_fwd(x, w, bias, m, n, k, act, y, workspace, workspace_bytes, stream);
 }
 
 // AdamW::lr_at / AdamW::step (proj/src/pipeline.cpp:643-680)

@@ -1,0 +1,130 @@
+// Dense linear layer on the 5th-generation tensor cores:
+//   y = act(x W^T + b),  x [M, K] bf16 row-major, W [N, K] bf16 row-major
+//   (nn.Linear layout), b [N] fp32, act in {identity, GELU(erf)}, y [M, N] bf16,
+// the reference's Tape matmul + bias + gelu_erf chain (proj/src/tape.cpp,
+// proj/src/pipeline.cpp:388-400) fused into one kernel.
+//
+// Built from CUTLASS 4.x SM100 templates (the header tree bundled with
+// flashinfer): TMA loads into a multi-stage shared-memory ring, tcgen05.mma
+// issued by one elected thread with the fp32 accumulator in TMEM, and an
+// epilogue that reads TMEM (tcgen05.ld), adds the per-column bias, applies the
+// activation in fp32 and stores bf16 through TMA.  Tile 256x128x64 over a
+// 2-CTA cluster (cta_group::2: the pair shares one 256-row tile).
+#include <cuda_runtime.h>
+
+#include "cute/tensor.hpp"
+#include "cutlass/cutlass.h"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/epilogue/fusion/operations.hpp"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+
+#include "common.cuh"
+
+namespace affmae_b200 {
+namespace {
+
+using namespace cute;
+
+template <template <class> class Act>
+struct LinearCfg {
+    using ElementA = cutlass::bfloat16_t;
+    using ElementB = cutlass::bfloat16_t;
+    using ElementD = cutlass::bfloat16_t;
+    using ElementC = cutlass::bfloat16_t;
+    using ElementAcc = float;
+    using ElementBias = float;
+    using LayoutA = cutlass::layout::RowMajor;
+    using LayoutB = cutlass::layout::ColumnMajor;  // W [N, K] row-major == B [K, N] K-major
+    using LayoutD = cutlass::layout::RowMajor;
+    static constexpr int kAlign = 8;  // 16 bytes of bf16
+    using MmaTileShape = Shape<_256, _256, _64>;
+    using ClusterShape = Shape<_2, _1, _1>;
+    using Fusion = cutlass::epilogue::fusion::LinCombPerColBiasEltAct<Act, ElementD, float, ElementBias, ElementC,
+                                                                      float>;
+    using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
+        cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, float, ElementC, LayoutD, kAlign, ElementD,
+        LayoutD, kAlign, cutlass::epilogue::TmaWarpSpecialized2Sm, Fusion>::CollectiveOp;
+    using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, LayoutA, kAlign, ElementB, LayoutB, kAlign,
+        ElementAcc, MmaTileShape, ClusterShape,
+        cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(
+            sizeof(typename Epilogue::SharedStorage))>,
+        cutlass::gemm::KernelTmaWarpSpecialized2SmSm100>::CollectiveOp;
+    using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue>;
+    using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+};
+
+template <template <class> class Act>
+typename LinearCfg<Act>::Gemm::Arguments linear_args(const void* x, const void* w, const float* bias, int m, int n,
+                                                     int k, void* y) {
+    using C = LinearCfg<Act>;
+    using StrideA = typename C::Gemm::GemmKernel::StrideA;
+    using StrideB = typename C::Gemm::GemmKernel::StrideB;
+    using StrideC = typename C::Gemm::GemmKernel::StrideC;
+    using StrideD = typename C::Gemm::GemmKernel::StrideD;
+    auto sa = cutlass::make_cute_packed_stride(StrideA{}, cute::make_shape(m, k, 1));
+    auto sb = cutlass::make_cute_packed_stride(StrideB{}, cute::make_shape(n, k, 1));
+    auto sc = cutlass::make_cute_packed_stride(StrideC{}, cute::make_shape(m, n, 1));
+    auto sd = cutlass::make_cute_packed_stride(StrideD{}, cute::make_shape(m, n, 1));
+    typename C::Gemm::Arguments args{
+        cutlass::gemm::GemmUniversalMode::kGemm,
+        {m, n, k, 1},
+        {static_cast<const typename C::ElementA*>(x), sa, static_cast<const typename C::ElementB*>(w), sb},
+        {{}, nullptr, sc, static_cast<typename C::ElementD*>(y), sd}};
+    args.epilogue.thread.alpha = 1.0f;
+    args.epilogue.thread.beta = 0.0f;
+    args.epilogue.thread.bias_ptr = bias;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    args.hw_info.device_id = dev;
+    args.hw_info.sm_count = kNumSMs;
+    return args;
+}
+
+template <template <class> class Act>
+int run_linear(const void* x, const void* w, const float* bias, int m, int n, int k, void* y, void* ws,
+               size_t ws_bytes, cudaStream_t st) {
+    using G = typename LinearCfg<Act>::Gemm;
+    auto args = linear_args<Act>(x, w, bias, m, n, k, y);
+    G gemm;
+    if (gemm.can_implement(args) != cutlass::Status::kSuccess)
+        return fail(AFFMAE_EUNSUPPORTED, "linear: shape not supported by the tcgen05 kernel");
+    if (G::get_workspace_size(args) > ws_bytes) return fail(AFFMAE_ECONFIG, "linear: workspace too small");
+    if (gemm.initialize(args, ws, st) != cutlass::Status::kSuccess)
+        return fail(AFFMAE_ECUDA, "linear: initialize failed");
+    if (gemm.run(st) != cutlass::Status::kSuccess) return fail(AFFMAE_ECUDA, "linear: launch failed");
+    AFFMAE_LAUNCH_CHECK("linear tcgen05 kernel");
+    return AFFMAE_OK;
+}
+
+}  // namespace
+
+size_t linear_workspace(int64_t m, int64_t n, int64_t k) {
+    auto a = linear_args<cutlass::epilogue::thread::GELU>(nullptr, nullptr, nullptr, int(m), int(n), int(k), nullptr);
+    auto b = linear_args<cutlass::epilogue::thread::Identity>(nullptr, nullptr, nullptr, int(m), int(n), int(k),
+                                                              nullptr);
+    const size_t wa = LinearCfg<cutlass::epilogue::thread::GELU>::Gemm::get_workspace_size(a);
+    const size_t wb = LinearCfg<cutlass::epilogue::thread::Identity>::Gemm::get_workspace_size(b);
+    return (wa > wb ? wa : wb) + 256;
+}
+
+int linear_fwd(const void* x, const void* w, const float* bias, int64_t m, int64_t n, int64_t k, int act, void* y,
+               void* ws, size_t ws_bytes, void* stream) {
+    if (!x || !w || !bias || !y) return fail(AFFMAE_ECONFIG, "linear: null pointer");
+    if (m < 1 || n < 1 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return fail(AFFMAE_ECONFIG, "linear: bad shape");
+    if (k % 8 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "linear: K and N must be multiples of 8");
+    cudaStream_t st = as_stream(stream);
+    if (act == 1)
+        return run_linear<cutlass::epilogue::thread::GELU>(x, w, bias, int(m), int(n), int(k), y, ws, ws_bytes, st);
+    if (act == 0)
+        return run_linear<cutlass::epilogue::thread::Identity>(x, w, bias, int(m), int(n), int(k), y, ws, ws_bytes,
+                                                               st);
+    return fail(AFFMAE_EUNSUPPORTED, "linear: act must be 0 (identity) or 1 (GELU)");
+}
+
+}  // namespace affmae_b200

@@ -335,6 +335,27 @@ def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, dfeats
     return dfeats, dp, dqueries
 
 
+# ----------------------------------------------------------- dense linear
+def linear(x, w, bias=None, act="none", stream=None):
+    """y = act(x W^T + b) on the tcgen05 tensor cores (Tape matmul + bias + gelu_erf):
+    x [M, K] bf16, w [N, K] bf16, bias [N] fp32 (zeros if None), act 'none' | 'gelu'."""
+    _req(x, torch.bfloat16, "x")
+    _req(w, torch.bfloat16, "w")
+    M, K = x.shape
+    N = w.shape[0]
+    if bias is None:
+        bias = torch.zeros(N, dtype=torch.float32, device=x.device)
+    _req(bias, torch.float32, "bias")
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=x.device)
+    wsb = int(capi.lib().affmae_linear_workspace(C.c_int64(M), C.c_int64(N), C.c_int64(K)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    capi.check(capi.lib().affmae_linear_fwd(
+        C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(bias.data_ptr()), C.c_int64(M), C.c_int64(N),
+        C.c_int64(K), C.c_int({"none": 0, "gelu": 1}[act]), C.c_void_p(y.data_ptr()), C.c_void_p(ws.data_ptr()),
+        C.c_size_t(ws.numel()), _stream(stream)), "linear")
+    return y
+
+
 # ---------------------------------------------------------------- optimizer
 class AdamW:
     """AdamW (proj/include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680) over a list of
