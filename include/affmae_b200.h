@@ -142,6 +142,13 @@ int affmae_adamw_step(const affmae_adamw_cfg* cfg, int64_t step, int64_t n_segme
 size_t affmae_linear_workspace(int64_t m, int64_t n, int64_t k);
 int affmae_linear_fwd(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
                       int64_t k, int act, affmae_bf16* y, void* workspace, size_t workspace_bytes, void* stream);
+/* Backward of y = x W^T + b given dy (already through the activation): dx [M, K] bf16
+ * (overwritten), dw [N, K] fp32 and db [N] fp32 ACCUMULATED (+=); any output may be NULL.
+ * M, N, K multiples of 8. */
+size_t affmae_linear_bwd_workspace(int64_t m, int64_t n, int64_t k);
+int affmae_linear_bwd(const affmae_bf16* x, const affmae_bf16* w, const affmae_bf16* dy, int64_t m, int64_t n,
+                      int64_t k, affmae_bf16* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
+                      void* stream);
 
 /* ------------------------------------------------------------------------
  * Cluster attention (nbhd_attn_streaming / nbhd_attn_backward,

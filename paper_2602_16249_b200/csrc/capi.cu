@@ -57,6 +57,9 @@ int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
 int linear_fwd(const void*, const void*, const float*, int64_t, int64_t, int64_t, int, void*, void*, size_t, void*);
+size_t linear_bwd_workspace(int64_t, int64_t, int64_t);
+int linear_bwd(const void*, const void*, const void*, int64_t, int64_t, int64_t, void*, float*, float*, void*, size_t,
+               void*);
 int adamw_step(const affmae_adamw_cfg*, int64_t, int64_t, const int64_t*, const uint8_t*, int64_t, float*, const float*,
                float*, float*, void*);
 size_t select_retained_workspace(int64_t, int64_t);
@@ -196,6 +199,13 @@ size_t affmae_linear_workspace(int64_t m, int64_t n, int64_t k) { return linear_
 int affmae_linear_fwd(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
                       int64_t k, int act, affmae_bf16* y, void* workspace, size_t workspace_bytes, void* stream) {
     return linear_fwd(x, w, bias, m, n, k, act, y, workspace, workspace_bytes, stream);
+}
+
+size_t affmae_linear_bwd_workspace(int64_t m, int64_t n, int64_t k) { return linear_bwd_workspace(m, n, k); }
+int affmae_linear_bwd(const affmae_bf16* x, const affmae_bf16* w, const affmae_bf16* dy, int64_t m, int64_t n,
+                      int64_t k, affmae_bf16* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    return linear_bwd(x, w, dy, m, n, k, dx, dw, db, workspace, workspace_bytes, stream);
 }
 
 // AdamW::lr_at / AdamW::step (proj/src/pipeline.cpp:643-680)

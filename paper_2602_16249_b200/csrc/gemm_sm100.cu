@@ -101,7 +101,122 @@ int run_linear(const void* x, const void* w, const float* bias, int m, int n, in
     return AFFMAE_OK;
 }
 
+// ---- backward: dX = dY W (A = dY [M, N] row-major, B = W [N, K] row-major = N-major
+// operand), dW += dY^T X (A = dY^T: column-major view, B = X [M, K] row-major), fp32 dW
+// accumulated in place (beta = 1, CustomOp::backward semantics).
+template <class LayoutA_, class LayoutB_, class ElementD_, int AlignD>
+struct PlainCfg {
+    using ElementA = cutlass::bfloat16_t;
+    using ElementB = cutlass::bfloat16_t;
+    using ElementD = ElementD_;
+    using ElementC = ElementD_;
+    using MmaTileShape = Shape<_256, _256, _64>;
+    using ClusterShape = Shape<_2, _1, _1>;
+    using Fusion = cutlass::epilogue::fusion::LinearCombination<ElementD, float, ElementC, float>;
+    using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
+        cutlass::epilogue::collective::EpilogueTileAuto, float, float, ElementC, cutlass::layout::RowMajor, AlignD,
+        ElementD, cutlass::layout::RowMajor, AlignD, cutlass::epilogue::TmaWarpSpecialized2Sm, Fusion>::CollectiveOp;
+    using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, LayoutA_, 8, ElementB, LayoutB_, 8, float,
+        MmaTileShape, ClusterShape,
+        cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(
+            sizeof(typename Epilogue::SharedStorage))>,
+        cutlass::gemm::KernelTmaWarpSpecialized2SmSm100>::CollectiveOp;
+    using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue>;
+    using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+};
+using DxCfg = PlainCfg<cutlass::layout::RowMajor, cutlass::layout::RowMajor, cutlass::bfloat16_t, 8>;
+using DwCfg = PlainCfg<cutlass::layout::ColumnMajor, cutlass::layout::RowMajor, float, 4>;
+
+template <class Cfg>
+typename Cfg::Gemm::Arguments plain_args(const void* a, const void* b, void* c_and_d, float beta, int m, int n, int k) {
+    using K = typename Cfg::Gemm::GemmKernel;
+    auto sa = cutlass::make_cute_packed_stride(typename K::StrideA{}, cute::make_shape(m, k, 1));
+    auto sb = cutlass::make_cute_packed_stride(typename K::StrideB{}, cute::make_shape(n, k, 1));
+    auto sc = cutlass::make_cute_packed_stride(typename K::StrideC{}, cute::make_shape(m, n, 1));
+    auto sd = cutlass::make_cute_packed_stride(typename K::StrideD{}, cute::make_shape(m, n, 1));
+    typename Cfg::Gemm::Arguments args{
+        cutlass::gemm::GemmUniversalMode::kGemm,
+        {m, n, k, 1},
+        {static_cast<const typename Cfg::ElementA*>(a), sa, static_cast<const typename Cfg::ElementB*>(b), sb},
+        {{}, static_cast<const typename Cfg::ElementC*>(c_and_d), sc, static_cast<typename Cfg::ElementD*>(c_and_d),
+         sd}};
+    args.epilogue.thread.alpha = 1.0f;
+    args.epilogue.thread.beta = beta;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    args.hw_info.device_id = dev;
+    args.hw_info.sm_count = kNumSMs;
+    return args;
+}
+
+template <class Cfg>
+int run_plain(const void* a, const void* b, void* cd, float beta, int m, int n, int k, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+    using G = typename Cfg::Gemm;
+    auto args = plain_args<Cfg>(a, b, cd, beta, m, n, k);
+    G gemm;
+    if (gemm.can_implement(args) != cutlass::Status::kSuccess)
+        return fail(AFFMAE_EUNSUPPORTED, "linear bwd: shape not supported by the tcgen05 kernel");
+    if (G::get_workspace_size(args) > ws_bytes) return fail(AFFMAE_ECONFIG, "linear bwd: workspace too small");
+    if (gemm.initialize(args, ws, st) != cutlass::Status::kSuccess)
+        return fail(AFFMAE_ECUDA, "linear bwd: initialize failed");
+    if (gemm.run(st) != cutlass::Status::kSuccess) return fail(AFFMAE_ECUDA, "linear bwd: launch failed");
+    AFFMAE_LAUNCH_CHECK("linear bwd tcgen05 kernel");
+    return AFFMAE_OK;
+}
+
+// db[n] += sum_m dY[m, n]: per (column block, row chunk) partials, then a fixed-order sum
+__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t m, int64_t n, int64_t rows_per,
+                                      float* __restrict__ part) {
+    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (col >= n) return;
+    const int64_t r0 = int64_t(blockIdx.y) * rows_per, r1 = r0 + rows_per < m ? r0 + rows_per : m;
+    float s = 0.f;
+    for (int64_t r = r0; r < r1; ++r) s += __bfloat162float(dy[r * n + col]);
+    part[int64_t(blockIdx.y) * n + col] = s;
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int64_t n, int chunks, float* __restrict__ db) {
+    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (col >= n) return;
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[int64_t(c) * n + col];
+    db[col] += s;
+}
+constexpr int kColsumChunks = 64;
+
 }  // namespace
+
+size_t linear_bwd_workspace(int64_t m, int64_t n, int64_t k) {
+    auto a = plain_args<DxCfg>(nullptr, nullptr, nullptr, 0.f, int(m), int(k), int(n));
+    auto b = plain_args<DwCfg>(nullptr, nullptr, nullptr, 1.f, int(n), int(k), int(m));
+    const size_t wa = DxCfg::Gemm::get_workspace_size(a), wb = DwCfg::Gemm::get_workspace_size(b);
+    return (wa > wb ? wa : wb) + 256 + size_t(kColsumChunks) * size_t(n) * 4 + 256;
+}
+
+int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t n, int64_t k, void* dx, float* dw,
+               float* db, void* ws, size_t ws_bytes, void* stream) {
+    if (!x || !w || !dy) return fail(AFFMAE_ECONFIG, "linear bwd: null pointer");
+    if (m < 1 || n < 1 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return fail(AFFMAE_ECONFIG, "linear bwd: bad shape");
+    if (k % 8 || n % 8 || m % 8) return fail(AFFMAE_EUNSUPPORTED, "linear bwd: M, N, K must be multiples of 8");
+    if (ws_bytes < linear_bwd_workspace(m, n, k)) return fail(AFFMAE_ECONFIG, "linear bwd: workspace too small");
+    cudaStream_t st = as_stream(stream);
+    const size_t gws = ws_bytes - size_t(kColsumChunks) * size_t(n) * 4 - 256;
+    float* part = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + gws + 255) & ~uintptr_t(255));
+    int rc = AFFMAE_OK;
+    if (dx && (rc = run_plain<DxCfg>(dy, w, dx, 0.f, int(m), int(k), int(n), ws, gws, st))) return rc;
+    if (dw && (rc = run_plain<DwCfg>(dy, x, dw, 1.f, int(n), int(k), int(m), ws, gws, st))) return rc;
+    if (db) {
+        const int64_t rows_per = (m + kColsumChunks - 1) / kColsumChunks;
+        const dim3 grid(unsigned((n + 255) / 256), kColsumChunks);
+        colsum_partial_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), m, n, rows_per, part);
+        colsum_final_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, n, kColsumChunks, db);
+        AFFMAE_LAUNCH_CHECK("linear bwd bias");
+    }
+    return AFFMAE_OK;
+}
 
 size_t linear_workspace(int64_t m, int64_t n, int64_t k) {
     auto a = linear_args<cutlass::epilogue::thread::GELU>(nullptr, nullptr, nullptr, int(m), int(n), int(k), nullptr);

@@ -356,6 +356,30 @@ def linear(x, w, bias=None, act="none", stream=None):
     return y
 
 
+def linear_bwd(x, w, dy, dw=None, db=None, need_dx=True, stream=None):
+    """Backward of y = x W^T + b (dy already through the activation) on tcgen05: returns
+    (dx bf16 [M, K], dw fp32 [N, K] +=, db fp32 [N] +=); dw/db are zeros if not given."""
+    _req(x, torch.bfloat16, "x")
+    _req(w, torch.bfloat16, "w")
+    _req(dy, torch.bfloat16, "dy")
+    M, K = x.shape
+    N = w.shape[0]
+    dev = x.device
+    dx = torch.empty((M, K), dtype=torch.bfloat16, device=dev) if need_dx else None
+    if dw is None:
+        dw = torch.zeros((N, K), dtype=torch.float32, device=dev)
+    if db is None:
+        db = torch.zeros(N, dtype=torch.float32, device=dev)
+    wsb = int(capi.lib().affmae_linear_bwd_workspace(C.c_int64(M), C.c_int64(N), C.c_int64(K)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    capi.check(capi.lib().affmae_linear_bwd(
+        C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(dy.data_ptr()), C.c_int64(M), C.c_int64(N),
+        C.c_int64(K), C.c_void_p(dx.data_ptr() if dx is not None else 0), C.c_void_p(dw.data_ptr()),
+        C.c_void_p(db.data_ptr()), C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()), _stream(stream)),
+        "linear_bwd")
+    return dx, dw, db
+
+
 # ---------------------------------------------------------------- optimizer
 class AdamW:
     """AdamW (proj/include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680) over a list of

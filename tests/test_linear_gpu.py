@@ -36,3 +36,20 @@ def test_linear_rejects_unaligned():
     w = torch.zeros((8, 12), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError):
         ops.linear(x, w)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k", [(4096, 512, 128), (4096, 128, 512), (1000, 136, 264)])
+def test_linear_backward_matches_fp32_reference(m, n, k):
+    import torch
+    from paper_2602_16249_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(m * 3 + n + k)
+    x = torch.randn((m, k), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((n, k), device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
+    dy = torch.randn((m, n), device="cuda", generator=g).to(torch.bfloat16)
+    dw0 = torch.randn((n, k), device="cuda", generator=g)
+    db0 = torch.randn(n, device="cuda", generator=g)
+    dx, dw, db = ops.linear_bwd(x, w, dy, dw=dw0.clone(), db=db0.clone())
+    assert _rel(dx.float(), dy.float() @ w.float()) <= 1e-2
+    assert _rel(dw, dw0 + dy.float().t() @ x.float()) <= 1e-2  # accumulated (+=)
+    assert _rel(db, db0 + dy.float().sum(0)) <= 1e-3
