@@ -115,6 +115,18 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream);
 
+/* Row LayerNorm (Tape::layer_norm, src/tape.cpp:84-100, VJP :581-617; eps 1e-5):
+ * x, y [rows, cols] bf16, gamma/beta [cols] fp32, stats [rows] float2 {mean, rstd}
+ * (written by the forward, read by the backward); cols in {128, 256, 384, 512,
+ * 768, 1024}.  The backward overwrites dx (bf16; NULL to skip) and ACCUMULATES
+ * dgamma/dbeta (fp32, +=, fixed-order reduction; either may be NULL). */
+int affmae_layernorm_fwd(const affmae_bf16* x, const float* gamma, const float* beta, int64_t rows, int64_t cols,
+                         affmae_bf16* y, float* stats, void* stream);
+size_t affmae_layernorm_bwd_workspace(int64_t rows, int64_t cols);
+int affmae_layernorm_bwd(const affmae_bf16* x, const float* gamma, const float* stats, const affmae_bf16* dy,
+                         int64_t rows, int64_t cols, affmae_bf16* dx, float* dgamma, float* dbeta, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 /* Replaces AdamW (include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680):
  * one optimizer step over every parameter tensor at once.  The tensors live back
  * to back in flat fp32 buffers value/grad/m/v [n] (16-byte aligned; m, v start at

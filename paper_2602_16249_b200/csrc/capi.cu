@@ -58,6 +58,10 @@ double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
 int linear_fwd(const void*, const void*, const float*, int64_t, int64_t, int64_t, int, void*, void*, size_t, void*);
 size_t linear_bwd_workspace(int64_t, int64_t, int64_t);
+int layernorm_fwd(const void*, const float*, const float*, int64_t, int64_t, void*, float*, void*);
+size_t layernorm_bwd_workspace(int64_t, int64_t);
+int layernorm_bwd(const void*, const float*, const float*, const void*, int64_t, int64_t, void*, float*, float*, void*,
+                  size_t, void*);
 int linear_bwd(const void*, const void*, const void*, int64_t, int64_t, int64_t, void*, float*, float*, void*, size_t,
                void*);
 int adamw_step(const affmae_adamw_cfg*, int64_t, int64_t, const int64_t*, const uint8_t*, int64_t, float*, const float*,
@@ -206,6 +210,18 @@ int affmae_linear_bwd(const affmae_bf16* x, const affmae_bf16* w, const affmae_b
                       int64_t k, affmae_bf16* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
                       void* stream) {
     return linear_bwd(x, w, dy, m, n, k, dx, dw, db, workspace, workspace_bytes, stream);
+}
+
+// Tape::layer_norm forward / VJP (proj/src/tape.cpp:84-100,581-617)
+int affmae_layernorm_fwd(const affmae_bf16* x, const float* gamma, const float* beta, int64_t rows, int64_t cols,
+                         affmae_bf16* y, float* stats, void* stream) {
+    return layernorm_fwd(x, gamma, beta, rows, cols, y, stats, stream);
+}
+size_t affmae_layernorm_bwd_workspace(int64_t rows, int64_t cols) { return layernorm_bwd_workspace(rows, cols); }
+int affmae_layernorm_bwd(const affmae_bf16* x, const float* gamma, const float* stats, const affmae_bf16* dy,
+                         int64_t rows, int64_t cols, affmae_bf16* dx, float* dgamma, float* dbeta, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+    return layernorm_bwd(x, gamma, stats, dy, rows, cols, dx, dgamma, dbeta, workspace, workspace_bytes, stream);
 }
 
 // AdamW::lr_at / AdamW::step (proj/src/pipeline.cpp:643-680)

@@ -380,6 +380,37 @@ def linear_bwd(x, w, dy, dw=None, db=None, need_dx=True, stream=None):
     return dx, dw, db
 
 
+def layer_norm(x, gamma, beta, stream=None):
+    """Tape::layer_norm (proj/src/tape.cpp:84-100, eps 1e-5): x [R, C] bf16 -> (y bf16, stats)."""
+    _req(x, torch.bfloat16, "x")
+    R, Cc = x.shape
+    y = torch.empty_like(x)
+    stats = torch.empty((R, 2), dtype=torch.float32, device=x.device)
+    capi.check(capi.lib().affmae_layernorm_fwd(
+        C.c_void_p(x.data_ptr()), C.c_void_p(gamma.data_ptr()), C.c_void_p(beta.data_ptr()), C.c_int64(R),
+        C.c_int64(Cc), C.c_void_p(y.data_ptr()), C.c_void_p(stats.data_ptr()), _stream(stream)), "layer_norm")
+    return y, stats
+
+
+def layer_norm_bwd(x, gamma, stats, dy, dgamma=None, dbeta=None, stream=None):
+    """VJP of layer_norm (proj/src/tape.cpp:581-617): returns (dx bf16, dgamma +=, dbeta +=)."""
+    _req(dy, torch.bfloat16, "dy")
+    R, Cc = x.shape
+    dx = torch.empty_like(x)
+    if dgamma is None:
+        dgamma = torch.zeros(Cc, dtype=torch.float32, device=x.device)
+    if dbeta is None:
+        dbeta = torch.zeros(Cc, dtype=torch.float32, device=x.device)
+    wsb = int(capi.lib().affmae_layernorm_bwd_workspace(C.c_int64(R), C.c_int64(Cc)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    capi.check(capi.lib().affmae_layernorm_bwd(
+        C.c_void_p(x.data_ptr()), C.c_void_p(gamma.data_ptr()), C.c_void_p(stats.data_ptr()),
+        C.c_void_p(dy.data_ptr()), C.c_int64(R), C.c_int64(Cc), C.c_void_p(dx.data_ptr()),
+        C.c_void_p(dgamma.data_ptr()), C.c_void_p(dbeta.data_ptr()), C.c_void_p(ws.data_ptr()),
+        C.c_size_t(ws.numel()), _stream(stream)), "layer_norm_bwd")
+    return dx, dgamma, dbeta
+
+
 # ---------------------------------------------------------------- optimizer
 class AdamW:
     """AdamW (proj/include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680) over a list of

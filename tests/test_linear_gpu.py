@@ -53,3 +53,26 @@ def test_linear_backward_matches_fp32_reference(m, n, k):
     assert _rel(dx.float(), dy.float() @ w.float()) <= 1e-2
     assert _rel(dw, dw0 + dy.float().t() @ x.float()) <= 1e-2  # accumulated (+=)
     assert _rel(db, db0 + dy.float().sum(0)) <= 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols", [(4096, 128), (3000, 256), (1000, 384), (777, 1024), (1, 512)])
+def test_layer_norm_matches_fp32_reference(rows, cols):
+    """Tape::layer_norm and its VJP (proj/src/tape.cpp:84-100,581-617, eps 1e-5)."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    x = (torch.randn((rows, cols), device="cuda", generator=g) * 3 + 1).to(torch.bfloat16)
+    gamma = torch.randn(cols, device="cuda", generator=g)
+    beta = torch.randn(cols, device="cuda", generator=g)
+    dy = torch.randn((rows, cols), device="cuda", generator=g).to(torch.bfloat16)
+    y, stats = ops.layer_norm(x, gamma, beta)
+    xf = x.float().requires_grad_(True)
+    gf, bf = gamma.clone().requires_grad_(True), beta.clone().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xf, (cols,), gf, bf, eps=1e-5)
+    assert _rel(y.float(), ref.detach()) <= 1e-2
+    ref.backward(dy.float())
+    dg0, db0 = torch.ones(cols, device="cuda"), torch.ones(cols, device="cuda")
+    dx, dg, db = ops.layer_norm_bwd(x, gamma, stats, dy, dgamma=dg0.clone(), dbeta=db0.clone())
+    assert _rel(dx.float(), xf.grad) <= 1e-2
+    assert _rel(dg, dg0 + gf.grad) <= 1e-3 and _rel(db, db0 + bf.grad) <= 1e-3
