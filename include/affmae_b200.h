@@ -127,6 +127,21 @@ int affmae_layernorm_bwd(const affmae_bf16* x, const float* gamma, const float* 
                          int64_t rows, int64_t cols, affmae_bf16* dx, float* dgamma, float* dbeta, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* Decoder row ops (§8(f) #2).  NormClampOp (src/pipeline.cpp:75-127): rows of
+ * x [rows, d] bf16 rescaled to norm <= limit; the backward writes dx (bf16,
+ * overwritten).  Reconstruction loss (Tape::mse over the masked cells,
+ * src/tape.cpp:431-446, Model::loss_parts src/pipeline.cpp:581-600): loss = mean
+ * over rows x p of (pred[r] - patches[cells[r]])^2, pred [rows, p] bf16, patches
+ * [n_cells, p] fp32, cells [rows] int32; with dpred != NULL also writes
+ * dpred = 2 (pred - target) dloss / numel (bf16).  Deterministic. */
+int affmae_norm_clamp_fwd(const affmae_bf16* x, int64_t rows, int64_t d, double limit, affmae_bf16* y, void* stream);
+int affmae_norm_clamp_bwd(const affmae_bf16* x, const affmae_bf16* g, int64_t rows, int64_t d, double limit,
+                          affmae_bf16* dx, void* stream);
+size_t affmae_masked_mse_workspace(int64_t rows);
+int affmae_masked_mse(const affmae_bf16* pred, const float* patches, const int32_t* cells, int64_t rows, int64_t p,
+                      float* loss, affmae_bf16* dpred, float dloss, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* Replaces AdamW (include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680):
  * one optimizer step over every parameter tensor at once.  The tensors live back
  * to back in flat fp32 buffers value/grad/m/v [n] (16-byte aligned; m, v start at

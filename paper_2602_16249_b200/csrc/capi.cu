@@ -60,6 +60,10 @@ int linear_fwd(const void*, const void*, const float*, int64_t, int64_t, int64_t
 size_t linear_bwd_workspace(int64_t, int64_t, int64_t);
 int layernorm_fwd(const void*, const float*, const float*, int64_t, int64_t, void*, float*, void*);
 size_t layernorm_bwd_workspace(int64_t, int64_t);
+int norm_clamp_fwd(const void*, int64_t, int64_t, double, void*, void*);
+int norm_clamp_bwd(const void*, const void*, int64_t, int64_t, double, void*, void*);
+size_t masked_mse_workspace(int64_t);
+int masked_mse(const void*, const float*, const int32_t*, int64_t, int64_t, float*, void*, float, void*, size_t, void*);
 int layernorm_bwd(const void*, const float*, const float*, const void*, int64_t, int64_t, void*, float*, float*, void*,
                   size_t, void*);
 int linear_bwd(const void*, const void*, const void*, int64_t, int64_t, int64_t, void*, float*, float*, void*, size_t,
@@ -222,6 +226,21 @@ int affmae_layernorm_bwd(const affmae_bf16* x, const float* gamma, const float* 
                          int64_t rows, int64_t cols, affmae_bf16* dx, float* dgamma, float* dbeta, void* workspace,
                          size_t workspace_bytes, void* stream) {
     return layernorm_bwd(x, gamma, stats, dy, rows, cols, dx, dgamma, dbeta, workspace, workspace_bytes, stream);
+}
+
+// NormClampOp (proj/src/pipeline.cpp:75-127) and the masked reconstruction loss (tape.cpp:431-446)
+int affmae_norm_clamp_fwd(const affmae_bf16* x, int64_t rows, int64_t d, double limit, affmae_bf16* y, void* stream) {
+    return norm_clamp_fwd(x, rows, d, limit, y, stream);
+}
+int affmae_norm_clamp_bwd(const affmae_bf16* x, const affmae_bf16* g, int64_t rows, int64_t d, double limit,
+                          affmae_bf16* dx, void* stream) {
+    return norm_clamp_bwd(x, g, rows, d, limit, dx, stream);
+}
+size_t affmae_masked_mse_workspace(int64_t rows) { return masked_mse_workspace(rows); }
+int affmae_masked_mse(const affmae_bf16* pred, const float* patches, const int32_t* cells, int64_t rows, int64_t p,
+                      float* loss, affmae_bf16* dpred, float dloss, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    return masked_mse(pred, patches, cells, rows, p, loss, dpred, dloss, workspace, workspace_bytes, stream);
 }
 
 // AdamW::lr_at / AdamW::step (proj/src/pipeline.cpp:643-680)

@@ -411,6 +411,44 @@ def layer_norm_bwd(x, gamma, stats, dy, dgamma=None, dbeta=None, stream=None):
     return dx, dgamma, dbeta
 
 
+def norm_clamp(x, limit, stream=None):
+    """NormClampOp forward (proj/src/pipeline.cpp:75-97): rows of x [R, d] bf16 to norm <= limit."""
+    _req(x, torch.bfloat16, "x")
+    y = torch.empty_like(x)
+    capi.check(capi.lib().affmae_norm_clamp_fwd(C.c_void_p(x.data_ptr()), C.c_int64(x.shape[0]),
+                                                C.c_int64(x.shape[1]), C.c_double(limit), C.c_void_p(y.data_ptr()),
+                                                _stream(stream)), "norm_clamp")
+    return y
+
+
+def norm_clamp_bwd(x, g, limit, stream=None):
+    """NormClampOp VJP (proj/src/pipeline.cpp:99-125) -> dx bf16."""
+    _req(g, torch.bfloat16, "g")
+    dx = torch.empty_like(x)
+    capi.check(capi.lib().affmae_norm_clamp_bwd(C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()),
+                                                C.c_int64(x.shape[0]), C.c_int64(x.shape[1]), C.c_double(limit),
+                                                C.c_void_p(dx.data_ptr()), _stream(stream)), "norm_clamp_bwd")
+    return dx
+
+
+def masked_mse(pred, patches, cells, dloss=1.0, need_grad=True, stream=None):
+    """Reconstruction loss (Tape::mse, proj/src/tape.cpp:431-446) of pred [R, p] bf16 against
+    patches[cells] (patches [n_cells, p] fp32, cells [R] int32): (loss [1] fp32, dpred bf16 or None)."""
+    _req(pred, torch.bfloat16, "pred")
+    _req(patches, torch.float32, "patches")
+    _req(cells, torch.int32, "cells")
+    R, P = pred.shape
+    loss = torch.empty(1, dtype=torch.float32, device=pred.device)
+    dpred = torch.empty_like(pred) if need_grad else None
+    wsb = int(capi.lib().affmae_masked_mse_workspace(C.c_int64(R)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=pred.device)
+    capi.check(capi.lib().affmae_masked_mse(
+        C.c_void_p(pred.data_ptr()), C.c_void_p(patches.data_ptr()), C.c_void_p(cells.data_ptr()), C.c_int64(R),
+        C.c_int64(P), C.c_void_p(loss.data_ptr()), C.c_void_p(dpred.data_ptr() if dpred is not None else 0),
+        C.c_float(dloss), C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()), _stream(stream)), "masked_mse")
+    return loss, dpred
+
+
 # ---------------------------------------------------------------- optimizer
 class AdamW:
     """AdamW (proj/include/affmae/pipeline.hpp:112-127; src/pipeline.cpp:639-680) over a list of
