@@ -169,6 +169,13 @@ int affmae_adamw_step(const affmae_adamw_cfg* cfg, int64_t step, int64_t n_segme
 size_t affmae_linear_workspace(int64_t m, int64_t n, int64_t k);
 int affmae_linear_fwd(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
                       int64_t k, int act, affmae_bf16* y, void* workspace, size_t workspace_bytes, void* stream);
+/* GELU variant that also stores the pre-activation x W^T + b (bf16 [M, N]) for the
+ * backward, and the GELU derivative dpre = dy * gelu'(pre) (gelu_bwd, src/tape.cpp;
+ * n elements, a multiple of 8). */
+int affmae_linear_fwd_gelu_aux(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m,
+                               int64_t n, int64_t k, affmae_bf16* y, affmae_bf16* pre, void* workspace,
+                               size_t workspace_bytes, void* stream);
+int affmae_gelu_bwd(const affmae_bf16* pre, const affmae_bf16* dy, int64_t n, affmae_bf16* dpre, void* stream);
 /* Backward of y = x W^T + b given dy (already through the activation): dx [M, K] bf16
  * (overwritten), dw [N, K] fp32 and db [N] fp32 ACCUMULATED (+=); any output may be NULL.
  * M, N, K multiples of 8. */

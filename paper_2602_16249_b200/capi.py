@@ -29,7 +29,7 @@ EXPORTS = (
     "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
     "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd", "affmae_interp_fwd", "affmae_interp_bwd",
     "affmae_adamw_lr", "affmae_adamw_step", "affmae_linear_workspace", "affmae_linear_fwd",
-    "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",
+    "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_linear_fwd_gelu_aux", "affmae_gelu_bwd", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",
     "affmae_layernorm_bwd", "affmae_norm_clamp_fwd", "affmae_norm_clamp_bwd", "affmae_masked_mse_workspace",
     "affmae_masked_mse",
 )

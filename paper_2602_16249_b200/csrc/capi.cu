@@ -58,6 +58,9 @@ double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
 int linear_fwd(const void*, const void*, const float*, int64_t, int64_t, int64_t, int, void*, void*, size_t, void*);
 size_t linear_bwd_workspace(int64_t, int64_t, int64_t);
+int linear_fwd_gelu_aux(const void*, const void*, const float*, int64_t, int64_t, int64_t, void*, void*, void*, size_t,
+                        void*);
+int gelu_bwd(const void*, const void*, int64_t, void*, void*);
 int layernorm_fwd(const void*, const float*, const float*, int64_t, int64_t, void*, float*, void*);
 size_t layernorm_bwd_workspace(int64_t, int64_t);
 int norm_clamp_fwd(const void*, int64_t, int64_t, double, void*, void*);
@@ -209,6 +212,14 @@ int affmae_linear_fwd(const affmae_bf16* x, const affmae_bf16* w, const float* b
     return linear_fwd(x, w, bias, m, n, k, act, y, workspace, workspace_bytes, stream);
 }
 
+int affmae_linear_fwd_gelu_aux(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m,
+                               int64_t n, int64_t k, affmae_bf16* y, affmae_bf16* pre, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    return linear_fwd_gelu_aux(x, w, bias, m, n, k, y, pre, workspace, workspace_bytes, stream);
+}
+int affmae_gelu_bwd(const affmae_bf16* pre, const affmae_bf16* dy, int64_t n, affmae_bf16* dpre, void* stream) {
+    return gelu_bwd(pre, dy, n, dpre, stream);
+}
 size_t affmae_linear_bwd_workspace(int64_t m, int64_t n, int64_t k) { return linear_bwd_workspace(m, n, k); }
 int affmae_linear_bwd(const affmae_bf16* x, const affmae_bf16* w, const affmae_bf16* dy, int64_t m, int64_t n,
                       int64_t k, affmae_bf16* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,

@@ -58,6 +58,31 @@ struct LinearCfg {
     using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
 };
 
+// GELU with the pre-activation x W^T + b stored as an aux bf16 tensor (for the backward)
+struct LinearGeluAuxCfg {
+    using ElementA = cutlass::bfloat16_t;
+    using ElementB = cutlass::bfloat16_t;
+    using ElementD = cutlass::bfloat16_t;
+    using ElementC = cutlass::bfloat16_t;
+    using MmaTileShape = Shape<_256, _256, _64>;
+    using ClusterShape = Shape<_2, _1, _1>;
+    using Fusion = cutlass::epilogue::fusion::LinCombPerColBiasEltActAux<
+        cutlass::layout::RowMajor, cutlass::epilogue::thread::GELU, ElementD, float, cutlass::bfloat16_t, float,
+        ElementC, float>;
+    using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
+        cutlass::epilogue::collective::EpilogueTileAuto, float, float, ElementC, cutlass::layout::RowMajor, 8,
+        ElementD, cutlass::layout::RowMajor, 8, cutlass::epilogue::TmaWarpSpecialized2Sm, Fusion>::CollectiveOp;
+    using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, cutlass::layout::RowMajor, 8, ElementB,
+        cutlass::layout::ColumnMajor, 8, float, MmaTileShape, ClusterShape,
+        cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(
+            sizeof(typename Epilogue::SharedStorage))>,
+        cutlass::gemm::KernelTmaWarpSpecialized2SmSm100>::CollectiveOp;
+    using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue>;
+    using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+};
+
 template <template <class> class Act>
 typename LinearCfg<Act>::Gemm::Arguments linear_args(const void* x, const void* w, const float* bias, int m, int n,
                                                      int k, void* y) {
@@ -99,6 +124,66 @@ int run_linear(const void* x, const void* w, const float* bias, int m, int n, in
     if (gemm.run(st) != cutlass::Status::kSuccess) return fail(AFFMAE_ECUDA, "linear: launch failed");
     AFFMAE_LAUNCH_CHECK("linear tcgen05 kernel");
     return AFFMAE_OK;
+}
+
+int run_linear_gelu_aux(const void* x, const void* w, const float* bias, int m, int n, int k, void* y, void* pre,
+                        void* ws, size_t ws_bytes, cudaStream_t st) {
+    using C = LinearGeluAuxCfg;
+    using K = C::Gemm::GemmKernel;
+    auto sa = cutlass::make_cute_packed_stride(typename K::StrideA{}, cute::make_shape(m, k, 1));
+    auto sb = cutlass::make_cute_packed_stride(typename K::StrideB{}, cute::make_shape(n, k, 1));
+    auto sc = cutlass::make_cute_packed_stride(typename K::StrideC{}, cute::make_shape(m, n, 1));
+    auto sd = cutlass::make_cute_packed_stride(typename K::StrideD{}, cute::make_shape(m, n, 1));
+    C::Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm,
+                            {m, n, k, 1},
+                            {static_cast<const C::ElementA*>(x), sa, static_cast<const C::ElementB*>(w), sb},
+                            {{}, nullptr, sc, static_cast<C::ElementD*>(y), sd}};
+    args.epilogue.thread.alpha = 1.0f;
+    args.epilogue.thread.beta = 0.0f;
+    args.epilogue.thread.bias_ptr = bias;
+    args.epilogue.thread.aux_ptr = static_cast<cutlass::bfloat16_t*>(pre);
+    args.epilogue.thread.dAux = cutlass::make_cute_packed_stride(decltype(args.epilogue.thread.dAux){},
+                                                                 cute::make_shape(m, n, 1));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    args.hw_info.device_id = dev;
+    args.hw_info.sm_count = kNumSMs;
+    C::Gemm gemm;
+    if (gemm.can_implement(args) != cutlass::Status::kSuccess)
+        return fail(AFFMAE_EUNSUPPORTED, "linear: shape not supported by the tcgen05 kernel");
+    if (C::Gemm::get_workspace_size(args) > ws_bytes) return fail(AFFMAE_ECONFIG, "linear: workspace too small");
+    if (gemm.initialize(args, ws, st) != cutlass::Status::kSuccess)
+        return fail(AFFMAE_ECUDA, "linear: initialize failed");
+    if (gemm.run(st) != cutlass::Status::kSuccess) return fail(AFFMAE_ECUDA, "linear: launch failed");
+    AFFMAE_LAUNCH_CHECK("linear gelu aux kernel");
+    return AFFMAE_OK;
+}
+
+// dpre = dy * gelu'(pre), gelu'(x) = Phi(x) + x phi(x)  (tape.cpp gelu_bwd), 8 bf16 per thread
+__global__ void gelu_bwd_kernel(const uint4* __restrict__ pre, const uint4* __restrict__ dy, int64_t n8,
+                                uint4* __restrict__ dpre) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint4 p = __ldg(pre + i), g = __ldg(dy + i);
+        const __nv_bfloat162* ph = reinterpret_cast<const __nv_bfloat162*>(&p);
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&g);
+        uint4 o;
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 x2 = __bfloat1622float2(ph[j]), g2 = __bfloat1622float2(gh[j]);
+            float r[2];
+            const float xs[2] = {x2.x, x2.y}, gs[2] = {g2.x, g2.y};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float x = xs[e];
+                const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+                const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+                r[e] = gs[e] * (cdf + x * pdf);
+            }
+            oh[j] = __floats2bfloat162_rn(r[0], r[1]);
+        }
+        dpre[i] = o;
+    }
 }
 
 // ---- backward: dX = dY W (A = dY [M, N] row-major, B = W [N, K] row-major = N-major
@@ -218,13 +303,37 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
     return AFFMAE_OK;
 }
 
+int linear_fwd_gelu_aux(const void* x, const void* w, const float* bias, int64_t m, int64_t n, int64_t k, void* y,
+                        void* pre, void* ws, size_t ws_bytes, void* stream) {
+    if (!x || !w || !bias || !y || !pre) return fail(AFFMAE_ECONFIG, "linear: null pointer");
+    if (m < 1 || n < 1 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return fail(AFFMAE_ECONFIG, "linear: bad shape");
+    if (k % 8 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "linear: K and N must be multiples of 8");
+    return run_linear_gelu_aux(x, w, bias, int(m), int(n), int(k), y, pre, ws, ws_bytes, as_stream(stream));
+}
+
+int gelu_bwd(const void* pre, const void* dy, int64_t n, void* dpre, void* stream) {
+    if (!pre || !dy || !dpre) return fail(AFFMAE_ECONFIG, "gelu_bwd: null pointer");
+    if (n < 0 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "gelu_bwd: element count must be a multiple of 8");
+    if (n == 0) return AFFMAE_OK;
+    const int64_t n8 = n / 8;
+    const unsigned nb = unsigned(std::max<int64_t>(1, std::min<int64_t>((n8 + 255) / 256, 8 * kNumSMs)));
+    gelu_bwd_kernel<<<nb, 256, 0, as_stream(stream)>>>(static_cast<const uint4*>(pre), static_cast<const uint4*>(dy),
+                                                       n8, static_cast<uint4*>(dpre));
+    AFFMAE_LAUNCH_CHECK("gelu_bwd_kernel");
+    return AFFMAE_OK;
+}
+
 size_t linear_workspace(int64_t m, int64_t n, int64_t k) {
     auto a = linear_args<cutlass::epilogue::thread::GELU>(nullptr, nullptr, nullptr, int(m), int(n), int(k), nullptr);
     auto b = linear_args<cutlass::epilogue::thread::Identity>(nullptr, nullptr, nullptr, int(m), int(n), int(k),
                                                               nullptr);
     const size_t wa = LinearCfg<cutlass::epilogue::thread::GELU>::Gemm::get_workspace_size(a);
     const size_t wb = LinearCfg<cutlass::epilogue::thread::Identity>::Gemm::get_workspace_size(b);
-    return (wa > wb ? wa : wb) + 256;
+    // the aux-storing GELU variant shares the mainloop / scheduler shape: its workspace is the
+    // same tile-scheduler state; keep a generous floor
+    const size_t w = wa > wb ? wa : wb;
+    return (w > (size_t(1) << 16) ? w : (size_t(1) << 16)) + 256;
 }
 
 int linear_fwd(const void* x, const void* w, const float* bias, int64_t m, int64_t n, int64_t k, int act, void* y,

@@ -356,6 +356,36 @@ def linear(x, w, bias=None, act="none", stream=None):
     return y
 
 
+def linear_gelu_save(x, w, bias=None, stream=None):
+    """y = GELU(x W^T + b) and the pre-activation (for gelu_bwd), one tcgen05 launch."""
+    _req(x, torch.bfloat16, "x")
+    _req(w, torch.bfloat16, "w")
+    M, K = x.shape
+    N = w.shape[0]
+    if bias is None:
+        bias = torch.zeros(N, dtype=torch.float32, device=x.device)
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=x.device)
+    pre = torch.empty((M, N), dtype=torch.bfloat16, device=x.device)
+    wsb = int(capi.lib().affmae_linear_workspace(C.c_int64(M), C.c_int64(N), C.c_int64(K)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=x.device)
+    capi.check(capi.lib().affmae_linear_fwd_gelu_aux(
+        C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(bias.data_ptr()), C.c_int64(M), C.c_int64(N),
+        C.c_int64(K), C.c_void_p(y.data_ptr()), C.c_void_p(pre.data_ptr()), C.c_void_p(ws.data_ptr()),
+        C.c_size_t(ws.numel()), _stream(stream)), "linear_gelu_save")
+    return y, pre
+
+
+def gelu_bwd(pre, dy, stream=None):
+    """dpre = dy * gelu'(pre) (the Tape's gelu VJP, erf form)."""
+    _req(pre, torch.bfloat16, "pre")
+    _req(dy, torch.bfloat16, "dy")
+    dpre = torch.empty_like(pre)
+    capi.check(capi.lib().affmae_gelu_bwd(C.c_void_p(pre.data_ptr()), C.c_void_p(dy.data_ptr()),
+                                          C.c_int64(pre.numel()), C.c_void_p(dpre.data_ptr()), _stream(stream)),
+               "gelu_bwd")
+    return dpre
+
+
 def linear_bwd(x, w, dy, dw=None, db=None, need_dx=True, stream=None):
     """Backward of y = x W^T + b (dy already through the activation) on tcgen05: returns
     (dx bf16 [M, K], dw fp32 [N, K] +=, db fp32 [N] +=); dw/db are zeros if not given."""

@@ -76,3 +76,34 @@ def test_layer_norm_matches_fp32_reference(rows, cols):
     dx, dg, db = ops.layer_norm_bwd(x, gamma, stats, dy, dgamma=dg0.clone(), dbeta=db0.clone())
     assert _rel(dx.float(), xf.grad) <= 1e-2
     assert _rel(dg, dg0 + gf.grad) <= 1e-3 and _rel(db, db0 + bf.grad) <= 1e-3
+
+
+@pytest.mark.gpu
+def test_mlp_block_fwd_bwd_matches_fp32_reference():
+    """fc1 + GELU (pre-activation saved) -> fc2, and the whole backward on the GPU ops, vs torch
+    autograd in fp32 on the same bf16 inputs."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, D = 2048, 128
+    x = torch.randn((M, D), device="cuda", generator=g).to(torch.bfloat16)
+    w1 = (torch.randn((4 * D, D), device="cuda", generator=g) / D ** 0.5).to(torch.bfloat16)
+    b1 = torch.randn(4 * D, device="cuda", generator=g) * 0.1
+    w2 = (torch.randn((D, 4 * D), device="cuda", generator=g) / (4 * D) ** 0.5).to(torch.bfloat16)
+    b2 = torch.randn(D, device="cuda", generator=g) * 0.1
+    dy = torch.randn((M, D), device="cuda", generator=g).to(torch.bfloat16)
+    h, pre = ops.linear_gelu_save(x, w1, b1)
+    y = ops.linear(h, w2, b2)
+    dh, dw2, db2 = ops.linear_bwd(h, w2, dy)
+    dpre = ops.gelu_bwd(pre, dh)
+    dx, dw1, db1 = ops.linear_bwd(x, w1, dpre)
+    xf = x.float().requires_grad_(True)
+    w1f, b1f = w1.float().requires_grad_(True), b1.clone().requires_grad_(True)
+    w2f, b2f = w2.float().requires_grad_(True), b2.clone().requires_grad_(True)
+    pref = xf @ w1f.t() + b1f
+    yf = torch.nn.functional.gelu(pref) @ w2f.t() + b2f
+    yf.backward(dy.float())
+    assert _rel(pre.float(), pref.detach()) <= 1e-2
+    assert _rel(y.float(), yf.detach()) <= 1e-2
+    for got, want in ((dx, xf.grad), (dw1, w1f.grad), (db1, b1f.grad), (dw2, w2f.grad), (db2, b2f.grad)):
+        assert _rel(got.float(), want) <= 2e-2
