@@ -51,3 +51,31 @@ def test_single_process_identity():
     assert pdist.max_over_ranks(3.5) == 3.5
     with pytest.raises(ValueError):
         pdist.image_range(4, 2, 2)
+
+
+def _grad_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.arange(1000, dtype=torch.float32) * (rank + 1)  # rank-dependent gradients
+    ar = pdist.GradAllReduce(g, dist, bucket_bytes=1024)       # 256-element buckets
+    ar.launch(0, 2)      # early buckets while "backward" continues
+    ar.launch(2)         # the rest
+    ar.wait()
+    q.put((rank, len(ar.buckets), g.numpy().copy()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_bucketed_gradient_allreduce():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_grad_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    (r0, nb0, g0), (r1, nb1, g1) = res
+    want = (torch.arange(1000, dtype=torch.float32) * 1.5).numpy()  # mean of 1x and 2x
+    assert nb0 == nb1 == 4
+    assert (g0 == want).all() and (g1 == want).all()
