@@ -429,10 +429,11 @@ def run_ours(a, rank, world, dist):
     interp = run_interp(a, host, dev) if a.interp_images > 0 else None
     adamw = run_adamw(dev) if a.interp_images > 0 else None
     linear = run_linear(dev) if a.interp_images > 0 else None
+    gattn = run_gattn(a, host, dev) if a.interp_images > 0 else None
 
     res = dict(value=value, ms=ms_max, phase_ms={p: float(np.median(v)) for p, v in phase_ms.items()},
                clocks=clocks.summary(), e2e=e2e, N=N, B=B, launches=launches,
-               graph=graph is not None, interp=interp, adamw=adamw, linear=linear)
+               graph=graph is not None, interp=interp, adamw=adamw, linear=linear, gattn=gattn)
     return res
 
 
@@ -503,6 +504,52 @@ def run_interp(a, host, dev, k=8, reps=10):
             "k": k, "dim": D, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
             "fwd_queries_per_s": nq / (fwd_ms * 1e-3), "bwd_queries_per_s": nq / (bwd_ms * 1e-3),
             "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
+            "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
+
+
+def run_gattn(a, host, dev, k=8, heads=4, head_dim=16, hidden=8, reps=10):
+    """Side measurement: the decoder's self attention over knn rows
+    (pipeline.cpp:493, 522-525; DecoderConfig defaults dim 64 = 4 heads x 16, self_k 8) on
+    every patch centre of `interp_images` images; fwd and bwd timed with CUDA events."""
+    import torch
+    from paper_2602_16249_b200 import inputs, ops
+    nb = min(a.interp_images, host["coords"].shape[0])
+    g = a.grid
+    cc = (np.arange(g) * 8.0 + 4.0).astype(np.float32)
+    q0 = np.stack(np.meshgrid(cc, cc), -1).reshape(1, -1, 2)
+    coords = torch.as_tensor(np.repeat(q0, nb, 0), device=dev).contiguous()
+    N, D = coords.shape[1], heads * head_dim
+    idx, valid = ops.knn(coords, coords, k)
+    bf = torch.bfloat16
+    q, kk, v, do = (0.5 * torch.randn((nb, N, D), device=dev)).to(bf), (0.5 * torch.randn((nb, N, D), device=dev)).to(bf), \
+        (0.5 * torch.randn((nb, N, D), device=dev)).to(bf), torch.randn((nb, N, D), device=dev).to(bf)
+    bk, bv = torch.zeros((heads, head_dim), dtype=bf, device=dev), torch.zeros((heads, head_dim), dtype=bf, device=dev)
+    rng = np.random.default_rng(7)
+    bias = ops.BiasNet.from_numpy(inputs.bias_params(heads, hidden, rng), device=dev)
+    grads = ops.gattn_bwd(q, kk, v, bk, bv, coords, idx, valid, bias, heads, head_dim, do)
+    for _ in range(2):
+        ops.gattn_fwd(q, kk, v, bk, bv, coords, idx, valid, bias, heads, head_dim)
+        ops.gattn_bwd(q, kk, v, bk, bv, coords, idx, valid, bias, heads, head_dim, do, grads=grads)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    for _ in range(reps):
+        ops.gattn_fwd(q, kk, v, bk, bv, coords, idx, valid, bias, heads, head_dim)
+    ev[1].record()
+    for _ in range(reps):
+        ops.gattn_bwd(q, kk, v, bk, bv, coords, idx, valid, bias, heads, head_dim, do, grads=grads)
+    ev[2].record()
+    torch.cuda.synchronize()
+    fwd_ms, bwd_ms = ev[0].elapsed_time(ev[1]) / reps, ev[1].elapsed_time(ev[2]) / reps
+    nt = nb * N
+    # algorithmic bytes per token: q / k / v rows 2D each, xy 8, rows k*(4+1), out 2D + lse 4h (fwd);
+    # + dout 2D, dq 2D, dk / dv fp32 read-modify-write 16D (bwd)
+    fwd_bytes = nt * (8 * D + 8 + 5 * k + 4 * heads)
+    bwd_bytes = nt * (10 * D + 8 + 5 * k + 16 * D)
+    return {"images": nb, "tokens_per_image": N, "k": k, "heads": heads, "head_dim": head_dim,
+            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "fwd_tokens_per_s": nt / (fwd_ms * 1e-3),
+            "bwd_tokens_per_s": nt / (bwd_ms * 1e-3), "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9,
+            "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
             "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
 
 
@@ -903,6 +950,8 @@ def main():
             line["next_ops"]["adamw"] = res["adamw"]
         if res.get("linear"):
             line["next_ops"]["linear"] = res["linear"]
+        if res.get("gattn"):
+            line["next_ops"]["decoder_attn"] = res["gattn"]
     if not a.no_cpu_baseline and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(a)

@@ -271,6 +271,23 @@ int affmae_attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc
                             affmae_attn_grads* grads, void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* Attention over arbitrary neighbour rows: nbhd_attn_streaming / nbhd_attn_backward
+ * (include/affmae/attention.hpp:52-72) on a general NeighborIndex -- the decoder's
+ * cross attention over one_to_one rows and self attention over knn rows
+ * (src/pipeline.cpp:64-71, 495-535; attn_layer :467-477).  idx / valid [B, N, width]
+ * (width in [1, 31], image-local ids into the same N tokens, e.g. from affmae_knn);
+ * head_dim 16, 32 or 64.  Forward: out [B, N, h*d] bf16, lse [B, N, h] fp32.
+ * Backward: dq [B, N, h*d] bf16 overwritten; dk, dv [B, N, h*d] fp32 and the
+ * parameter gradients ACCUMULATED (+=).  No workspace. */
+int affmae_gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
+                     const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width,
+                     affmae_bf16* out, float* lse, void* stream);
+int affmae_gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
+                     const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width,
+                     const affmae_bf16* dout, affmae_bf16* dq, float* dk, float* dv,
+                     float* dblank_k, float* dblank_v, float* dw1, float* db1, float* dw2,
+                     float* db2, float* dblank, void* stream);
+
 /* ------------------------------------------------------------------------
  * Adaptive KNN merge (src/merging.cpp).
  * ---------------------------------------------------------------------- */

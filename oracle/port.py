@@ -26,6 +26,8 @@ def lib():
         _lib.orc_retained_count.restype = C.c_int64
         _lib.orc_select_retained.restype = C.c_int64
         _lib.orc_bias_eval.restype = C.c_double
+        _lib.orc_adamw_lr.restype = C.c_double
+        _lib.orc_adamw_lr.argtypes = [C.c_double, C.c_int64, C.c_int64, C.c_int64]
     return _lib
 
 

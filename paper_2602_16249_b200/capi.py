@@ -31,7 +31,7 @@ EXPORTS = (
     "affmae_adamw_lr", "affmae_adamw_step", "affmae_linear_workspace", "affmae_linear_fwd",
     "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_linear_fwd_gelu_aux", "affmae_gelu_bwd", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",
     "affmae_layernorm_bwd", "affmae_norm_clamp_fwd", "affmae_norm_clamp_bwd", "affmae_masked_mse_workspace",
-    "affmae_masked_mse",
+    "affmae_masked_mse", "affmae_gattn_fwd", "affmae_gattn_bwd",
 )
 
 

@@ -53,6 +53,11 @@ int interp_fwd(const float*, const float*, const void*, const int32_t*, const ui
                int64_t, int64_t, const float*, double, void*, void*);
 int interp_bwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
                int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*);
+int gattn_fwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
+              int64_t, void*, float*, void*);
+int gattn_bwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
+              int64_t, const void*, void*, float*, float*, float*, float*, float*, float*, float*, float*, float*,
+              void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
@@ -203,6 +208,20 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream) {
     return interp_bwd(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
                       dfeats, dp, dqueries, stream);
+}
+
+// decoder attention over general neighbour rows (src/pipeline.cpp:495-535)
+int affmae_gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
+                     const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width, affmae_bf16* out,
+                     float* lse, void* stream) {
+    return gattn_fwd(a, in, idx, valid, batch, tokens, width, out, lse, stream);
+}
+int affmae_gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
+                     const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width, const affmae_bf16* dout,
+                     affmae_bf16* dq, float* dk, float* dv, float* dblank_k, float* dblank_v, float* dw1,
+                     float* db1, float* dw2, float* db2, float* dblank, void* stream) {
+    return gattn_bwd(a, in, idx, valid, batch, tokens, width, dout, dq, dk, dv, dblank_k, dblank_v, dw1, db1, dw2,
+                     db2, dblank, stream);
 }
 
 // dense linear layer (Tape matmul + bias + gelu_erf), tcgen05

@@ -223,6 +223,48 @@ def attn_bwd(geom, q, k, v, blank_k, blank_v, coords, index: ClusterIndex, bias:
     return grads
 
 
+def gattn_fwd(q, k, v, blank_k, blank_v, coords, idx, valid, bias: BiasNet, heads, head_dim,
+              stream=None):
+    """Attention over general neighbour rows (the decoder's cross / self attention,
+    proj/src/pipeline.cpp:495-535 over nbhd_attn_streaming): q/k/v [B, N, h*d] bf16,
+    coords [B, N, 2], idx/valid [B, N, W] (W <= 31) -> (out [B, N, h*d] bf16, lse [B, N, h])."""
+    desc, ins = _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim)
+    _req(idx, torch.int32, "idx")
+    _req(valid, torch.uint8, "valid")
+    B, N, W = idx.shape
+    out = torch.empty_like(q)
+    lse = torch.empty((B, N, heads), dtype=torch.float32, device=q.device)
+    capi.check(capi.lib().affmae_gattn_fwd(C.byref(desc), C.byref(ins), C.c_void_p(idx.data_ptr()),
+                                           C.c_void_p(valid.data_ptr()), C.c_int64(B), C.c_int64(N),
+                                           C.c_int64(W), C.c_void_p(out.data_ptr()),
+                                           C.c_void_p(lse.data_ptr()), _stream(stream)), "gattn_fwd")
+    return out, lse
+
+
+def gattn_bwd(q, k, v, blank_k, blank_v, coords, idx, valid, bias: BiasNet, heads, head_dim, dout,
+              grads: AttnGrads | None = None, stream=None):
+    """Backward of gattn_fwd (nbhd_attn_backward, proj/src/attention.cpp:241-358): dq bf16
+    overwritten; dk / dv fp32 and the blank / BiasNet gradients accumulate (+=)."""
+    desc, ins = _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim)
+    _req(idx, torch.int32, "idx")
+    _req(valid, torch.uint8, "valid")
+    _req(dout, BF16, "dout")
+    B, N, W = idx.shape
+    if grads is None:
+        grads = AttnGrads.zeros_like(q, blank_k, bias)
+        grads.dk = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+        grads.dv = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+    _req(grads.dk, torch.float32, "dk")
+    _req(grads.dv, torch.float32, "dv")
+    capi.check(capi.lib().affmae_gattn_bwd(
+        C.byref(desc), C.byref(ins), C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()), C.c_int64(B),
+        C.c_int64(N), C.c_int64(W), C.c_void_p(dout.data_ptr()),
+        *[C.c_void_p(getattr(grads, n).data_ptr()) for n in (
+            "dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")],
+        _stream(stream)), "gattn_bwd")
+    return grads
+
+
 # --------------------------------------------------------------- index build
 def cluster_index(coords, cluster, groups, workspace=None, stream=None) -> ClusterIndex:
     """balanced_clusters + cluster_neighborhood on device, batched
