@@ -17,6 +17,7 @@
 namespace affmae_b200 {
 
 constexpr int kGMaxHidden = 32;
+constexpr int kGMaxHeads = 8;  // a block is heads warps (<= 256 threads)
 
 struct GAttnP {
     const __nv_bfloat16 *q, *k, *v, *bk, *bv;
@@ -29,229 +30,344 @@ struct GAttnP {
     float scale, inv_patch;
 };
 
-template <int HD>
-struct GRow {  // a head_dim row, lanes over dims (HD / 32 values per lane; HD 16: lanes 0-15)
-    static constexpr int PL = HD >= 32 ? HD / 32 : 1;
-    static __device__ __forceinline__ bool on(int lane) { return HD >= 32 || lane < HD; }
-};
+__device__ __forceinline__ void gred_v4(float* addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
 
-__device__ __forceinline__ float gdot_row(const __nv_bfloat16* a, const __nv_bfloat16* b, int hd) {
-    // full dot product of two hd-element bf16 rows by one thread (16-byte loads)
-    float s = 0.f;
-    for (int c = 0; c < hd; c += 8) {
-        const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + c)), y = __ldg(reinterpret_cast<const uint4*>(b + c));
-        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
-        const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y);
+template <int HD>
+__device__ __forceinline__ void gload_row(const __nv_bfloat16* r, float (&f)[HD], float mul) {
+#pragma unroll
+    for (int c = 0; c < HD; c += 8) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(r + c));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float2 u = __bfloat1622float2(xh[i]), w = __bfloat1622float2(yh[i]);
-            s = fmaf(u.x, w.x, fmaf(u.y, w.y, s));
+            const float2 t = __bfloat1622float2(h[i]);
+            f[c + 2 * i] = t.x * mul;
+            f[c + 2 * i + 1] = t.y * mul;
+        }
+    }
+}
+
+template <int HD>
+__device__ __forceinline__ float gdot(const float (&a)[HD], const __nv_bfloat16* r) {
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < HD; c += 8) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(r + c));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 t = __bfloat1622float2(h[i]);
+            s = fmaf(a[c + 2 * i], t.x, fmaf(a[c + 2 * i + 1], t.y, s));
         }
     }
     return s;
 }
 
-__device__ __forceinline__ float gbias(const GAttnP& p, int h, float ox, float oy) {
-    float acc = p.b2[h];
-    for (int u = 0; u < p.hidden; ++u) {
-        const float pre = fmaf(p.w1[h * 2 * p.hidden + u], ox, fmaf(p.w1[h * 2 * p.hidden + p.hidden + u], oy,
-                                                                     p.b1[h * p.hidden + u]));
-        acc = fmaf(p.w2[h * p.hidden + u], tanhf(pre), acc);
+// BiasNet of one pair from the head's units {w1x, w1y, b1, w2} in shared memory
+__device__ __forceinline__ float gbias(const float4* un, int hidden, float b2, float ox, float oy) {
+    float acc = b2;
+    for (int u = 0; u < hidden; ++u) {
+        const float4 w = un[u];
+        acc = fmaf(w.w, tanh_fast(fmaf(w.x, ox, fmaf(w.y, oy, w.z))), acc);
     }
     return acc;
 }
 
-// scores of the lane's slot (key slot lane < m, blank at lane m), softmax weight, key id
-struct GSlot {
-    float w;   // softmax weight (0 for invalid / unused lanes)
-    int t;     // key token (image-local), -1 if none
-    float ox, oy, s;
-};
-
-template <int HD>
-__device__ __forceinline__ GSlot gattn_slot(const GAttnP& p, int64_t b, int64_t i, int h, int lane) {
-    const int64_t ld = int64_t(p.heads) * HD;
-    const __nv_bfloat16* qrow = p.q + (b * p.n + i) * ld + h * HD;
-    const float2* xy = reinterpret_cast<const float2*>(p.coords) + b * p.n;
-    GSlot sl{0.f, -1, 0.f, 0.f, -INFINITY};
-    if (lane < p.m) {
-        const int64_t e = (b * p.n + i) * p.m + lane;
-        if (p.valid[e]) {
-            sl.t = p.idx[e];
-            const float2 qx = xy[i], kx = xy[sl.t];
-            sl.ox = (kx.x - qx.x) * p.inv_patch;
-            sl.oy = (kx.y - qx.y) * p.inv_patch;
-            sl.s = p.scale * gdot_row(qrow, p.k + (b * p.n + sl.t) * ld + h * HD, HD) + gbias(p, h, sl.ox, sl.oy);
-        }
-    } else if (lane == p.m) {
-        sl.s = p.scale * gdot_row(qrow, p.bk + h * HD, HD) + p.blank[h];
+__device__ __forceinline__ void gstage_units(const GAttnP& p, float4* units) {
+    const int H = p.hidden;
+    for (int e = threadIdx.x; e < p.heads * H; e += blockDim.x) {
+        const int h = e / H, u = e - h * H;
+        units[e] = make_float4(p.w1[h * 2 * H + u], p.w1[h * 2 * H + H + u], p.b1[h * H + u], p.w2[h * H + u]);
     }
-    float mx = sl.s;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float e = sl.s == -INFINITY ? 0.f : __expf(sl.s - mx);
-    float l = e;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    sl.w = e / l;
-    sl.s = mx + __logf(l);  // lse (every lane)
-    return sl;
+    __syncthreads();
 }
 
+// Thread per (token, head): a block is heads warps over a tile of 32 tokens, warp = head,
+// lane = token, so a warp's BiasNet / blank gradients belong to one head and the heads'
+// 2*HD-byte row segments of one key are read by the same block.
 template <int HD>
 __global__ void __launch_bounds__(256) gattn_fwd_kernel(GAttnP p, __nv_bfloat16* __restrict__ out,
-                                                        float* __restrict__ lse) {
-    constexpr int PL = GRow<HD>::PL;
-    const int lane = threadIdx.x & 31;
-    const int64_t total = p.batch * p.n * p.heads, ws = int64_t(gridDim.x) * (blockDim.x >> 5);
-    const int64_t ld = int64_t(p.heads) * HD;
-    for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total; w += ws) {
-        const int h = int(w % p.heads);
-        const int64_t bi = w / p.heads, b = bi / p.n, i = bi - b * p.n;
-        const GSlot sl = gattn_slot<HD>(p, b, i, h, lane);
-        float acc[PL];
+                                                         float* __restrict__ lse) {
+    extern __shared__ float4 g_units[];
+    gstage_units(p, g_units);
+    const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;
+    const float4* un = g_units + h * p.hidden;
+    const float b2 = p.b2[h], blank = p.blank[h];
+    const int64_t ntok = p.batch * p.n, ld = int64_t(p.heads) * HD;
+    const float2* xy = reinterpret_cast<const float2*>(p.coords);
+    for (int64_t gi = int64_t(blockIdx.x) * 32 + lane; gi < ntok; gi += int64_t(gridDim.x) * 32) {
+        const int64_t b0 = (gi / p.n) * p.n;
+        float qf[HD], acc[HD];
+        gload_row<HD>(p.q + gi * ld + h * HD, qf, p.scale);
 #pragma unroll
-        for (int r = 0; r < PL; ++r) acc[r] = 0.f;
-        for (int j = 0; j < p.m; ++j) {
-            const float wj = __shfl_sync(0xffffffffu, sl.w, j);
-            const int tj = __shfl_sync(0xffffffffu, sl.t, j);
-            if (tj >= 0) {
-                const __nv_bfloat16* vr = p.v + (b * p.n + tj) * ld + h * HD;
+        for (int c = 0; c < HD; ++c) acc[c] = 0.f;
+        const float2 qx = xy[gi];
+        float mx = -INFINITY, l = 0.f;
+        auto take = [&](float s, const __nv_bfloat16* vr) {
+            if (s > mx) {
+                const float c = __expf(mx - s);
+                l *= c;
 #pragma unroll
-                for (int r = 0; r < PL; ++r)
-                    if (GRow<HD>::on(lane)) acc[r] = fmaf(wj, __bfloat162float(vr[lane + 32 * r]), acc[r]);
+                for (int i = 0; i < HD; ++i) acc[i] *= c;
+                mx = s;
             }
-        }
-        const float wb = __shfl_sync(0xffffffffu, sl.w, p.m);
+            const float e = __expf(s - mx);
+            l += e;
+            float vf[HD];
+            gload_row<HD>(vr, vf, 1.f);
 #pragma unroll
-        for (int r = 0; r < PL && GRow<HD>::on(lane); ++r) {
-            acc[r] = fmaf(wb, __bfloat162float(p.bv[h * HD + lane + 32 * r]), acc[r]);
-            out[(b * p.n + i) * ld + h * HD + lane + 32 * r] = __float2bfloat16(acc[r]);
+            for (int i = 0; i < HD; ++i) acc[i] = fmaf(e, vf[i], acc[i]);
+        };
+        const int32_t* ir = p.idx + gi * p.m;
+        const uint8_t* vv = p.valid + gi * p.m;
+        for (int j = 0; j < p.m; ++j) {
+            if (!vv[j]) continue;
+            const int64_t key = b0 + ir[j];
+            const float2 kx = xy[key];
+            const float s = gdot<HD>(qf, p.k + key * ld + h * HD) +
+                            gbias(un, p.hidden, b2, (kx.x - qx.x) * p.inv_patch, (kx.y - qx.y) * p.inv_patch);
+            take(s, p.v + key * ld + h * HD);
         }
-        if (lane == 0) lse[bi * p.heads + h] = sl.s;
+        take(gdot<HD>(qf, p.bk + h * HD) + blank, p.bv + h * HD);
+        const float il = 1.f / l;
+        uint4* o = reinterpret_cast<uint4*>(out + gi * ld + h * HD);
+#pragma unroll
+        for (int c = 0; c < HD; c += 8) {
+            uint4 w;
+            __nv_bfloat162* hw = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) hw[i] = __floats2bfloat162_rn(acc[c + 2 * i] * il, acc[c + 2 * i + 1] * il);
+            o[c / 8] = w;
+        }
+        lse[gi * p.heads + h] = mx + __logf(l);
     }
 }
 
-template <int HD>
+__device__ __forceinline__ float gwarp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Warp reduce-scatter of 32 per-lane values: returns, on lane l, the sum over the
+// warp of v[l] (31 shuffles for 32 sums).  v is clobbered.
+__device__ __forceinline__ float greduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const float send = up ? v[i] : v[i + o];
+            const float keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+// Backward, same layout; MW >= width bounds the per-slot register arrays.
+// Per tile (32 tokens of one head) the warp's blank-k / blank-v gradients (2*HD sums) and,
+// for hidden <= 8, the 4*hidden BiasNet sums are reduce-scattered so lane l keeps sum l.
+template <int HD, int MW>
 __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfloat16* __restrict__ dout,
                                                         __nv_bfloat16* __restrict__ dq, float* __restrict__ dk,
                                                         float* __restrict__ dv, float* __restrict__ dbk,
                                                         float* __restrict__ dbv, float* __restrict__ dw1,
                                                         float* __restrict__ db1, float* __restrict__ dw2,
                                                         float* __restrict__ db2, float* __restrict__ dblank) {
-    constexpr int PL = GRow<HD>::PL;
-    __shared__ float pacc[8][4 * kGMaxHidden + 2];  // per warp: BiasNet grads of its head, blank param
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int G = 4 * p.hidden + 2;
-    for (int e = lane; e < G; e += 32) pacc[warp][e] = 0.f;
-    const int64_t total = p.batch * p.n * p.heads, ws = int64_t(gridDim.x) * (blockDim.x >> 5);
-    const int64_t ld = int64_t(p.heads) * HD;
-    // heads are the fastest index of the warp id and the grid is a multiple of heads
-    // warps, so every warp of this block sees one fixed head (pacc is per head)
-    int head_of_warp = -1;
-    float bkacc[PL], bvacc[PL];
+    constexpr int NB = 2 * HD / 32;  // reduce-scatter rounds for the blank rows
+    extern __shared__ float4 g_units[];
+    gstage_units(p, g_units);
+    const int lane = threadIdx.x & 31, h = threadIdx.x >> 5, H = p.hidden;
+    const bool small_h = H <= 8;
+    const float4* un = g_units + h * H;
+    const float b2 = p.b2[h], blank = p.blank[h];
+    const int64_t ntok = p.batch * p.n, ld = int64_t(p.heads) * HD;
+    const float2* xy = reinterpret_cast<const float2*>(p.coords);
+    float agx = 0.f, agy = 0.f, agb = 0.f, agw = 0.f;  // big-hidden path: lane u = unit u
+    float abias = 0.f;                                 // small-hidden path: lane l = sum l of {gx, gy, gb, gw}[8]
+    float ab2 = 0.f, abl = 0.f, ablk[NB];
 #pragma unroll
-    for (int r = 0; r < PL; ++r) bkacc[r] = bvacc[r] = 0.f;
-    for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total; w += ws) {
-        const int h = int(w % p.heads);
-        head_of_warp = h;
-        const int64_t bi = w / p.heads, b = bi / p.n, i = bi - b * p.n;
-        const GSlot sl = gattn_slot<HD>(p, b, i, h, lane);
-        const __nv_bfloat16* grow = dout + (b * p.n + i) * ld + h * HD;
-        const __nv_bfloat16* qrow = p.q + (b * p.n + i) * ld + h * HD;
-        // dP for the lane's slot
-        float dP = 0.f;
-        if (sl.t >= 0) dP = gdot_row(grow, p.v + (b * p.n + sl.t) * ld + h * HD, HD);
-        else if (lane == p.m) dP = gdot_row(grow, p.bv + h * HD, HD);
-        float D = sl.w * dP;
+    for (int r = 0; r < NB; ++r) ablk[r] = 0.f;
+    for (int64_t base = int64_t(blockIdx.x) * 32; base < ntok; base += int64_t(gridDim.x) * 32) {
+        const int64_t gi = base + lane;
+        const bool act = gi < ntok;
+        const int64_t row = act ? gi : base;
+        const int64_t b0 = (row / p.n) * p.n;
+        float qf[HD], gf[HD];
+        gload_row<HD>(p.q + row * ld + h * HD, qf, 1.f);
+        gload_row<HD>(dout + row * ld + h * HD, gf, 1.f);
+        const float2 qx = xy[row];
+        float w[MW], dS[MW], ox[MW], oy[MW];
+        int key[MW];  // image-local key token, -1 if none
+        const int32_t* ir = p.idx + row * p.m;
+        const uint8_t* vv = p.valid + row * p.m;
+        float mx = -INFINITY;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) D += __shfl_xor_sync(0xffffffffu, D, o);
-        const float dS = sl.w * (dP - D);  // 0 on unused lanes
-        // dq over dims, dk / dv scatter
-        float qv[PL], gv[PL], dqa[PL];
-#pragma unroll
-        for (int r = 0; r < PL; ++r) {
-            const bool on = GRow<HD>::on(lane);
-            qv[r] = on ? __bfloat162float(qrow[lane + 32 * r]) : 0.f;
-            gv[r] = on ? __bfloat162float(grow[lane + 32 * r]) : 0.f;
-            dqa[r] = 0.f;
-        }
-        for (int j = 0; j < p.m; ++j) {
-            const float dSj = __shfl_sync(0xffffffffu, dS, j), wj = __shfl_sync(0xffffffffu, sl.w, j);
-            const int tj = __shfl_sync(0xffffffffu, sl.t, j);
-            if (tj < 0) continue;
-            const __nv_bfloat16* kr = p.k + (b * p.n + tj) * ld + h * HD;
-            float* dkr = dk + (b * p.n + tj) * ld + h * HD;
-            float* dvr = dv + (b * p.n + tj) * ld + h * HD;
-#pragma unroll
-            for (int r = 0; r < PL && GRow<HD>::on(lane); ++r) {
-                dqa[r] = fmaf(dSj, __bfloat162float(kr[lane + 32 * r]), dqa[r]);
-                atomicAdd(dkr + lane + 32 * r, p.scale * dSj * qv[r]);
-                atomicAdd(dvr + lane + 32 * r, wj * gv[r]);
+        for (int j = 0; j < MW; ++j) {
+            w[j] = -INFINITY;
+            key[j] = -1;
+            ox[j] = oy[j] = 0.f;
+            if (act && j < p.m && vv[j]) {
+                key[j] = ir[j];
+                const float2 kx = xy[b0 + key[j]];
+                ox[j] = (kx.x - qx.x) * p.inv_patch;
+                oy[j] = (kx.y - qx.y) * p.inv_patch;
+                w[j] = p.scale * gdot<HD>(qf, p.k + (b0 + key[j]) * ld + h * HD) + gbias(un, H, b2, ox[j], oy[j]);
+                mx = fmaxf(mx, w[j]);
             }
         }
-        const float dSb = __shfl_sync(0xffffffffu, dS, p.m), wb = __shfl_sync(0xffffffffu, sl.w, p.m);
+        float wb = act ? p.scale * gdot<HD>(qf, p.bk + h * HD) + blank : -INFINITY;
+        mx = fmaxf(mx, wb);
+        float l = 0.f;
 #pragma unroll
-        for (int r = 0; r < PL && GRow<HD>::on(lane); ++r) {
-            dqa[r] = fmaf(dSb, __bfloat162float(p.bk[h * HD + lane + 32 * r]), dqa[r]);
-            dq[(b * p.n + i) * ld + h * HD + lane + 32 * r] = __float2bfloat16(p.scale * dqa[r]);
-            bkacc[r] = fmaf(p.scale * dSb, qv[r], bkacc[r]);
-            bvacc[r] = fmaf(wb, gv[r], bvacc[r]);
+        for (int j = 0; j < MW; ++j) {
+            w[j] = key[j] >= 0 ? __expf(w[j] - mx) : 0.f;
+            l += w[j];
         }
-        // BiasNet gradients of the pairs (lane = slot), reduced over the warp
-        const bool pair = sl.t >= 0;
-        for (int u = 0; u < p.hidden; ++u) {
-            float gx = 0.f, gy = 0.f, gb = 0.f, gw = 0.f;
-            if (pair) {
-                const float pre = fmaf(p.w1[h * 2 * p.hidden + u], sl.ox,
-                                       fmaf(p.w1[h * 2 * p.hidden + p.hidden + u], sl.oy, p.b1[h * p.hidden + u]));
-                const float th = tanhf(pre);
-                const float dpre = dS * p.w2[h * p.hidden + u] * (1.f - th * th);
-                gx = dpre * sl.ox;
-                gy = dpre * sl.oy;
-                gb = dpre;
-                gw = dS * th;
-            }
+        wb = act ? __expf(wb - mx) : 0.f;
+        l += wb;
+        const float il = act ? 1.f / l : 0.f;
+        float D = 0.f;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                gx += __shfl_xor_sync(0xffffffffu, gx, o);
-                gy += __shfl_xor_sync(0xffffffffu, gy, o);
-                gb += __shfl_xor_sync(0xffffffffu, gb, o);
-                gw += __shfl_xor_sync(0xffffffffu, gw, o);
-            }
-            if (lane == 0) {
-                pacc[warp][u] += gx;
-                pacc[warp][p.hidden + u] += gy;
-                pacc[warp][2 * p.hidden + u] += gb;
-                pacc[warp][3 * p.hidden + u] += gw;
+        for (int j = 0; j < MW; ++j) {
+            w[j] *= il;
+            dS[j] = key[j] >= 0 ? gdot<HD>(gf, p.v + (b0 + key[j]) * ld + h * HD) : 0.f;
+            D = fmaf(w[j], dS[j], D);
+        }
+        wb *= il;
+        const float dPb = act ? gdot<HD>(gf, p.bv + h * HD) : 0.f;
+        D = fmaf(wb, dPb, D);
+        const float dSb = wb * (dPb - D);
+        float dqa[HD];
+#pragma unroll
+        for (int c = 0; c < HD; ++c) dqa[c] = 0.f;
+        float s2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < MW; ++j) {
+            dS[j] = w[j] * (dS[j] - D);
+            if (key[j] < 0) continue;
+            s2 += dS[j];
+            const int64_t kr = (b0 + key[j]) * ld + h * HD;
+            float kf[HD];
+            gload_row<HD>(p.k + kr, kf, 1.f);
+            const float a = p.scale * dS[j];
+#pragma unroll
+            for (int c = 0; c < HD; c += 4) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dqa[c + i] = fmaf(dS[j], kf[c + i], dqa[c + i]);
+                gred_v4(dk + kr + c, a * qf[c], a * qf[c + 1], a * qf[c + 2], a * qf[c + 3]);
+                gred_v4(dv + kr + c, w[j] * gf[c], w[j] * gf[c + 1], w[j] * gf[c + 2], w[j] * gf[c + 3]);
             }
         }
-        float g2 = pair ? dS : 0.f;
+        if (act) {
+            float bkf[HD];
+            gload_row<HD>(p.bk + h * HD, bkf, 1.f);
+            uint4* o = reinterpret_cast<uint4*>(dq + gi * ld + h * HD);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) g2 += __shfl_xor_sync(0xffffffffu, g2, o);
-        if (lane == 0) {
-            pacc[warp][4 * p.hidden] += g2;
-            pacc[warp][4 * p.hidden + 1] += dSb;
+            for (int c = 0; c < HD; c += 8) {
+                uint4 v;
+                __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    hv[i] = __floats2bfloat162_rn(p.scale * fmaf(dSb, bkf[c + 2 * i], dqa[c + 2 * i]),
+                                                  p.scale * fmaf(dSb, bkf[c + 2 * i + 1], dqa[c + 2 * i + 1]));
+                o[c / 8] = v;
+            }
+            ab2 += s2;
+            abl += dSb;
+        }
+        // blank rows: values {scale dSb q[c]} then {wb g[c]}, 32 per round
+#pragma unroll
+        for (int r = 0; r < NB; ++r) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int e = r * 32 + i;
+                v[i] = e < HD ? p.scale * dSb * qf[e] : wb * gf[e - HD];
+            }
+            ablk[r] += greduce_scatter32(v, lane);
+        }
+        // BiasNet gradients of the tile's pairs
+        if (small_h) {
+            float v[32];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                float gx = 0.f, gy = 0.f, gb = 0.f, gw = 0.f;
+                if (u < H) {
+                    const float4 wu = un[u];
+#pragma unroll
+                    for (int j = 0; j < MW; ++j) {
+                        if (key[j] < 0) continue;
+                        const float th = tanh_fast(fmaf(wu.x, ox[j], fmaf(wu.y, oy[j], wu.z)));
+                        const float dpre = dS[j] * wu.w * (1.f - th * th);
+                        gx = fmaf(dpre, ox[j], gx);
+                        gy = fmaf(dpre, oy[j], gy);
+                        gb += dpre;
+                        gw = fmaf(dS[j], th, gw);
+                    }
+                }
+                v[u] = gx;
+                v[8 + u] = gy;
+                v[16 + u] = gb;
+                v[24 + u] = gw;
+            }
+            abias += greduce_scatter32(v, lane);
+        } else {
+            for (int u = 0; u < H; ++u) {
+                const float4 wu = un[u];
+                float gx = 0.f, gy = 0.f, gb = 0.f, gw = 0.f;
+#pragma unroll
+                for (int j = 0; j < MW; ++j) {
+                    if (key[j] < 0) continue;
+                    const float th = tanh_fast(fmaf(wu.x, ox[j], fmaf(wu.y, oy[j], wu.z)));
+                    const float dpre = dS[j] * wu.w * (1.f - th * th);
+                    gx = fmaf(dpre, ox[j], gx);
+                    gy = fmaf(dpre, oy[j], gy);
+                    gb += dpre;
+                    gw = fmaf(dS[j], th, gw);
+                }
+                gx = gwarp_sum(gx);
+                gy = gwarp_sum(gy);
+                gb = gwarp_sum(gb);
+                gw = gwarp_sum(gw);
+                if (lane == u) {
+                    agx += gx;
+                    agy += gy;
+                    agb += gb;
+                    agw += gw;
+                }
+            }
         }
     }
-    __syncwarp();
-    if (head_of_warp >= 0) {
-        const int h = head_of_warp;
+    if (small_h) {
+        const int u = lane & 7, kind = lane >> 3;
+        if (u < H) {
+            float* dst = kind == 0 ? dw1 + h * 2 * H + u
+                       : kind == 1 ? dw1 + h * 2 * H + H + u
+                       : kind == 2 ? db1 + h * H + u
+                                   : dw2 + h * H + u;
+            atomicAdd(dst, abias);
+        }
+    } else if (lane < H) {
+        atomicAdd(dw1 + h * 2 * H + lane, agx);
+        atomicAdd(dw1 + h * 2 * H + H + lane, agy);
+        atomicAdd(db1 + h * H + lane, agb);
+        atomicAdd(dw2 + h * H + lane, agw);
+    }
+    ab2 = gwarp_sum(ab2);
+    abl = gwarp_sum(abl);
+    if (lane == 0) {
+        atomicAdd(db2 + h, ab2);
+        atomicAdd(dblank + h, abl);
+    }
 #pragma unroll
-        for (int r = 0; r < PL && GRow<HD>::on(lane); ++r) {
-            atomicAdd(dbk + h * HD + lane + 32 * r, bkacc[r]);
-            atomicAdd(dbv + h * HD + lane + 32 * r, bvacc[r]);
-        }
-        for (int e = lane; e < G; e += 32) {
-            const float val = pacc[warp][e];
-            const int H = p.hidden;
-            if (e < H) atomicAdd(dw1 + h * 2 * H + e, val);
-            else if (e < 2 * H) atomicAdd(dw1 + h * 2 * H + H + (e - H), val);
-            else if (e < 3 * H) atomicAdd(db1 + h * H + (e - 2 * H), val);
-            else if (e < 4 * H) atomicAdd(dw2 + h * H + (e - 3 * H), val);
-            else if (e == 4 * H) atomicAdd(db2 + h, val);
-            else atomicAdd(dblank + h, val);
-        }
+    for (int r = 0; r < NB; ++r) {
+        const int e = r * 32 + lane;
+        atomicAdd(e < HD ? dbk + h * HD + e : dbv + h * HD + (e - HD), ablk[r]);
     }
 }
 
@@ -264,6 +380,7 @@ static int gattn_fill(GAttnP& p, const affmae_attn_desc* a, const affmae_attn_in
         return fail(AFFMAE_EUNSUPPORTED, "gattn: head_dim must be 16, 32 or 64");
     if (width < 1 || width > 31) return fail(AFFMAE_EUNSUPPORTED, "gattn: neighbourhood width must be in [1, 31]");
     if (a->bias_hidden < 1 || a->bias_hidden > kGMaxHidden) return fail(AFFMAE_EUNSUPPORTED, "gattn: bias_hidden");
+    if (a->heads > kGMaxHeads) return fail(AFFMAE_EUNSUPPORTED, "gattn: at most 8 heads");
     if (a->heads < 1 || !(a->patch > 0.0) || batch < 0 || tokens < 1) return fail(AFFMAE_ECONFIG, "gattn: bad shape");
     p.q = reinterpret_cast<const __nv_bfloat16*>(in->q);
     p.k = reinterpret_cast<const __nv_bfloat16*>(in->k);
@@ -288,12 +405,10 @@ static int gattn_fill(GAttnP& p, const affmae_attn_desc* a, const affmae_attn_in
     return AFFMAE_OK;
 }
 
-static unsigned gattn_blocks(int64_t warps, int heads) {
-    // 8 warps per block; a whole number of head cycles per grid stride (heads | 8*blocks)
-    int64_t nb = std::min<int64_t>((warps + 7) / 8, 8 * kNumSMs);
-    nb = std::max<int64_t>(nb, 1);
-    while ((nb * 8) % heads) ++nb;
-    return unsigned(nb);
+static unsigned gattn_blocks(int64_t tokens, int heads, int per_sm_threads) {
+    const int64_t tiles = (tokens + 31) / 32;
+    const int64_t resident = std::max<int64_t>(1, per_sm_threads / (32 * heads)) * kNumSMs;
+    return unsigned(std::max<int64_t>(1, std::min(tiles, resident)));
 }
 
 int gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
@@ -303,13 +418,26 @@ int gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
     if (rc) return rc;
     if (!out || !lse) return fail(AFFMAE_ECONFIG, "gattn: null output");
     if (batch == 0) return AFFMAE_OK;
-    const unsigned nb = gattn_blocks(batch * tokens * a->heads, a->heads);
+    const unsigned nb = gattn_blocks(batch * tokens, a->heads, 2048);
+    const dim3 bt(32 * a->heads);
+    const size_t sm = size_t(a->heads) * a->bias_hidden * sizeof(float4);
     auto* o = static_cast<__nv_bfloat16*>(out);
-    if (a->head_dim == 16) gattn_fwd_kernel<16><<<nb, 256, 0, as_stream(stream)>>>(p, o, lse);
-    else if (a->head_dim == 32) gattn_fwd_kernel<32><<<nb, 256, 0, as_stream(stream)>>>(p, o, lse);
-    else gattn_fwd_kernel<64><<<nb, 256, 0, as_stream(stream)>>>(p, o, lse);
+    cudaStream_t st = as_stream(stream);
+    if (a->head_dim == 16) gattn_fwd_kernel<16><<<nb, bt, sm, st>>>(p, o, lse);
+    else if (a->head_dim == 32) gattn_fwd_kernel<32><<<nb, bt, sm, st>>>(p, o, lse);
+    else gattn_fwd_kernel<64><<<nb, bt, sm, st>>>(p, o, lse);
     AFFMAE_LAUNCH_CHECK("gattn_fwd_kernel");
     return AFFMAE_OK;
+}
+
+template <int HD>
+static void gattn_bwd_launch(int mw, unsigned nb, dim3 bt, size_t sm, cudaStream_t st, const GAttnP& p,
+                             const __nv_bfloat16* g, __nv_bfloat16* q, float* dk, float* dv, float* dbk, float* dbv,
+                             float* dw1, float* db1, float* dw2, float* db2, float* dblank) {
+    if (mw <= 1) gattn_bwd_kernel<HD, 1><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else if (mw <= 8) gattn_bwd_kernel<HD, 8><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else if (mw <= 16) gattn_bwd_kernel<HD, 16><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else gattn_bwd_kernel<HD, 31><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
 }
 
 int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
@@ -321,15 +449,16 @@ int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
     if (!dout || !dq || !dk || !dv || !dbk || !dbv || !dw1 || !db1 || !dw2 || !db2 || !dblank)
         return fail(AFFMAE_ECONFIG, "gattn bwd: null output");
     if (batch == 0) return AFFMAE_OK;
-    const unsigned nb = gattn_blocks(batch * tokens * a->heads, a->heads);
+    const unsigned nb = gattn_blocks(batch * tokens, a->heads, 1024);
+    const dim3 bt(32 * a->heads);
+    const size_t sm = size_t(a->heads) * a->bias_hidden * sizeof(float4);
     const auto* g = static_cast<const __nv_bfloat16*>(dout);
     auto* q = static_cast<__nv_bfloat16*>(dq);
-    if (a->head_dim == 16)
-        gattn_bwd_kernel<16><<<nb, 256, 0, as_stream(stream)>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
-    else if (a->head_dim == 32)
-        gattn_bwd_kernel<32><<<nb, 256, 0, as_stream(stream)>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
-    else
-        gattn_bwd_kernel<64><<<nb, 256, 0, as_stream(stream)>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    cudaStream_t st = as_stream(stream);
+    const int mw = int(width);
+    if (a->head_dim == 16) gattn_bwd_launch<16>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else if (a->head_dim == 32) gattn_bwd_launch<32>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else gattn_bwd_launch<64>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
     AFFMAE_LAUNCH_CHECK("gattn_bwd_kernel");
     return AFFMAE_OK;
 }
