@@ -502,4 +502,94 @@ std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, 
     return op;
 }
 
+// Attention over a general NeighborIndex (make_attn_op, include/affmae/attention.hpp:84-86): the
+// decoder's cross (one_to_one) and self (knn) attention layers.  Rows of width <= 31.
+std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim, int bias_hidden,
+                                       double patch, bool streaming, bool half_io) {
+    struct GAttnCudaOp final : CustomOp {
+        Tensor coords;
+        NeighborIndex nbr;
+        int heads, head_dim, hidden;
+        double patch;
+        std::string name() const override { return "nbhd_attention_b200"; }
+        struct Up {
+            std::unique_ptr<Dev> t[10], coords, idx, valid;
+            affmae_attn_inputs ai{};
+        };
+        Up upload_all(const std::vector<const Tensor*>& in) const {
+            if (in.size() != 10) throw ConfigError("attention op: want 10 inputs");
+            if (nbr.width < 1 || nbr.width > 31) throw ConfigError("attention op: neighbour width must be in [1, 31]");
+            if (in[0]->rows() != nbr.queries()) throw ConfigError("attention op: row count does not match neighbor index");
+            Up u;
+            for (int i = 0; i < 5; ++i) u.t[i] = upload(bf16(*in[size_t(i)]));
+            for (int i = 5; i < 10; ++i) u.t[i] = upload(f32(*in[size_t(i)]));
+            u.coords = upload(f32(coords));
+            std::vector<int32_t> idx(nbr.idx.begin(), nbr.idx.end());
+            u.idx = upload(idx);
+            u.valid = upload(nbr.valid);
+            u.ai = {u.t[0]->as<affmae_bf16>(), u.t[1]->as<affmae_bf16>(), u.t[2]->as<affmae_bf16>(),
+                    u.t[3]->as<affmae_bf16>(), u.t[4]->as<affmae_bf16>(), u.coords->as<float>(),
+                    u.t[5]->as<float>(), u.t[6]->as<float>(), u.t[7]->as<float>(), u.t[8]->as<float>(),
+                    u.t[9]->as<float>()};
+            return u;
+        }
+        Tensor forward(const std::vector<const Tensor*>& in) override {
+            Up u = upload_all(in);
+            const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
+            affmae_attn_desc a{heads, head_dim, hidden, patch};
+            Dev out(n * hd * 2), lse(n * heads * 4);
+            check(affmae_gattn_fwd(&a, &u.ai, u.idx->as<int32_t>(), u.valid->as<uint8_t>(), 1, n, nbr.width,
+                                   out.as<affmae_bf16>(), lse.as<float>(), nullptr),
+                  "gattn_fwd");
+            auto h = download<uint16_t>(out, size_t(n * hd));
+            Tensor o = Tensor::zeros({n, hd}, in[0]->precision());
+            for (int64_t i = 0; i < n * hd; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+            return o;
+        }
+        void backward(const Tensor& out_grad, const std::vector<const Tensor*>& in,
+                      const std::vector<Tensor*>& in_grads) override {
+            Up u = upload_all(in);
+            const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
+            affmae_attn_desc a{heads, head_dim, hidden, patch};
+            auto dout = upload(bf16(out_grad));
+            const int64_t sz[10] = {n * hd, n * hd, n * hd, int64_t(heads) * head_dim, int64_t(heads) * head_dim,
+                                    heads * 2 * int64_t(hidden), int64_t(heads) * hidden, int64_t(heads) * hidden,
+                                    heads, heads};
+            Dev dq(n * hd * 2);
+            std::unique_ptr<Dev> g[10];
+            for (int i = 1; i < 10; ++i) {
+                g[i] = std::make_unique<Dev>(sz[i] * 4);
+                ccheck(cudaMemset(g[i]->p, 0, size_t(sz[i] * 4)), "memset");
+            }
+            check(affmae_gattn_bwd(&a, &u.ai, u.idx->as<int32_t>(), u.valid->as<uint8_t>(), 1, n, nbr.width,
+                                   dout->as<affmae_bf16>(), dq.as<affmae_bf16>(), g[1]->as<float>(),
+                                   g[2]->as<float>(), g[3]->as<float>(), g[4]->as<float>(), g[5]->as<float>(),
+                                   g[6]->as<float>(), g[7]->as<float>(), g[8]->as<float>(), g[9]->as<float>(),
+                                   nullptr),
+                  "gattn_bwd");
+            ccheck(cudaDeviceSynchronize(), "sync");
+            if (in_grads[0]) {
+                auto h = download<uint16_t>(dq, size_t(n * hd));
+                for (int64_t j = 0; j < n * hd; ++j) in_grads[0]->set(j, in_grads[0]->get(j) + bf16_to_float(h[size_t(j)]));
+            }
+            for (int i = 1; i < 10; ++i) {
+                Tensor* dst = in_grads[size_t(i)];
+                if (!dst) continue;
+                auto h = download<float>(*g[i], size_t(sz[i]));
+                for (int64_t j = 0; j < sz[i]; ++j) dst->set(j, dst->get(j) + h[size_t(j)]);
+            }
+        }
+    };
+    (void)streaming;  // the device kernel is the streaming formulation; I/O is bf16 either way
+    (void)half_io;
+    auto op = std::make_shared<GAttnCudaOp>();
+    op->coords = std::move(coords);
+    op->nbr = std::move(nbr);
+    op->heads = heads;
+    op->head_dim = head_dim;
+    op->hidden = bias_hidden;
+    op->patch = patch;
+    return op;
+}
+
 }  // namespace affmae::cuda

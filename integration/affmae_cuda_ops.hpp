@@ -38,6 +38,13 @@ std::shared_ptr<CustomOp> make_cluster_attn_op(Tensor coords, int64_t cluster, i
                                                int heads, int head_dim, int bias_hidden,
                                                double patch);
 
+// Attention over a general NeighborIndex, same signature as the reference factory
+// (make_attn_op, include/affmae/attention.hpp:84-86): the decoder's cross / self
+// attention rows (one_to_one, knn; src/pipeline.cpp:515-525), width <= 31.
+std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim,
+                                       int bias_hidden, double patch, bool streaming = true,
+                                       bool half_io = false);
+
 // select_retained / merge_plan / make_merge_pool_op (include/affmae/merging.hpp:32-68)
 std::vector<int64_t> select_retained(const Tensor& scores, double d_s);
 MergePlan merge_plan(const PointSet& ps, std::span<const int64_t> retained, int k_m);

@@ -154,4 +154,29 @@ int integ_interp_tape(int use_cuda, int64_t nk, int64_t nq, int64_t dim, int64_t
     });
 }
 
+// Decoder self attention on the reference Tape: nbr = knn(coords, coords, k) (the
+// decoder's self_nbr, src/pipeline.cpp:493), out = attn(q, k, v, ...), loss = sum(out * w).
+int integ_gattn_tape(int use_cuda, int64_t n, int heads, int d, int hidden, double patch, int64_t k,
+                     const float* coords, const double* const* ins, const double* w, double* out,
+                     double* const* grads) {
+    return guarded([&] {
+        const int64_t hd = int64_t(heads) * d;
+        std::vector<std::vector<int64_t>> dims = {{n, hd}, {n, hd}, {n, hd}, {heads, d}, {heads, d},
+                                                  {heads, 2 * hidden}, {heads, hidden}, {heads, hidden},
+                                                  {heads, 1}, {heads, 1}};
+        Tape t(Precision::b32);
+        std::vector<int> ids;
+        for (int i = 0; i < 10; ++i) ids.push_back(t.leaf(from(ins[i], dims[size_t(i)])));
+        PointSet ps = pts(coords, n);
+        NeighborIndex nb = use_cuda ? cuda::knn(ps.coords, ps, k) : knn(ps.coords, ps, k);
+        auto op = use_cuda ? cuda::make_attn_op(ps.coords, nb, heads, d, hidden, patch)
+                           : make_attn_op(ps.coords, nb, heads, d, hidden, patch);
+        int o = t.custom(op, ids);
+        int loss = t.reduce_sum(t.mul(o, t.input(from(w, {n, hd}))));
+        t.backward(loss);
+        to(t.value(o), out);
+        for (int i = 0; i < 10; ++i) to(t.grad(ids[size_t(i)]), grads[i]);
+    });
+}
+
 }  // extern "C"

@@ -3,7 +3,7 @@
 integration/affmae_cuda_ops.cpp plugged in as CustomOps, against the same Tape
 with the reference's CPU ops (make_attn_op / make_merge_pool_op).  Also checks
 the geometry adapters return the reference's exact ClusterAssignment /
-NeighborIndex / knn results."""
+NeighborIndex / knn results, and the decoder attention (make_attn_op on knn rows)."""
 import ctypes as C
 import os
 
@@ -126,3 +126,33 @@ def test_interp_custom_op_on_reference_tape():
     (o0, f0, p0, q0), (o1, f1, p1, q1) = res
     assert rel_l2(o1, o0) <= 1e-2 and rel_l2(f1, f0) <= 1e-2 and rel_l2(q1, q0) <= 1e-2
     assert abs(p1 - p0) <= 1e-2 * max(1.0, abs(p0))
+
+
+def test_decoder_attention_custom_op_on_reference_tape():
+    """cuda::make_attn_op (general NeighborIndex, here the decoder's knn self_nbr) against
+    the reference's make_attn_op on the reference Tape: output and all 10 input gradients."""
+    L = _lib()
+    rng = np.random.default_rng(23)
+    n, heads, d, hidden, k = 300, 4, 16, 8, 8
+    coords = rng.uniform(0, 200, (n, 2)).astype(np.float32)
+    bf = lambda *s: inputs.bf16_round(0.5 * rng.standard_normal(s).astype(np.float32)).astype(np.float64)
+    b = inputs.bias_params(heads, hidden, rng)
+    ins = [bf(n, heads * d), bf(n, heads * d), bf(n, heads * d), bf(heads, d), bf(heads, d)] + \
+          [b[x].astype(np.float64) for x in ("w1", "b1", "w2", "b2", "blank")]
+    w = inputs.bf16_round(rng.standard_normal((n, heads * d)).astype(np.float32)).astype(np.float64)
+    shapes = [(n, heads * d)] * 3 + [(heads, d)] * 2 + [(heads, 2 * hidden), (heads, hidden),
+                                                         (heads, hidden), (heads, 1), (heads, 1)]
+    res = []
+    for use in (0, 1):
+        out = np.zeros((n, heads * d))
+        grads = [np.zeros(s) for s in shapes]
+        ins_p = (C.c_void_p * 10)(*[_p(x) for x in ins])
+        g_p = (C.c_void_p * 10)(*[_p(x) for x in grads])
+        _ok(L, L.integ_gattn_tape(C.c_int(use), C.c_int64(n), C.c_int(heads), C.c_int(d), C.c_int(hidden),
+                                  C.c_double(8.0), C.c_int64(k), _p(coords), ins_p, _p(w), _p(out), g_p))
+        res.append((out, grads))
+    (o0, g0), (o1, g1) = res
+    assert rel_l2(o1, o0) <= 1e-2
+    names = ("dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")
+    errs = {nm: rel_l2(a, r) for nm, a, r in zip(names, g1, g0)}
+    assert all(e <= 1e-2 for e in errs.values()), errs
