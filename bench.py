@@ -463,9 +463,10 @@ def count_graph_kernels(graph):
 def run_interp(a, host, dev, k=8, reps=10):
     """Side measurement (not part of the step): the decoder's softmax interpolation
     (make_interp_op) of the encoder tokens onto every patch centre of the grid, knn rows
-    built once; fwd and bwd timed with CUDA events over `reps` calls each."""
+    built once; fwd and bwd (scattered reductions, and the reverse-CSR gather variant with
+    its per-call CSR build) timed with CUDA events over `reps` calls each."""
     import torch
-    from paper_2602_16249_b200 import ops
+    from paper_2602_16249_b200 import capi, ops
     nb = min(a.interp_images, host["coords"].shape[0])
     keys = torch.as_tensor(host["coords"][:nb], device=dev).contiguous()
     g = a.grid
@@ -492,8 +493,19 @@ def run_interp(a, host, dev, k=8, reps=10):
     for _ in range(reps):
         ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq)
     ev[2].record()
+    for _ in range(2):
+        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq, gather=True)
+    nbytes = capi.lib().affmae_interp_bwd_gather_workspace(nb, queries.shape[1], keys.shape[1], k)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ev3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev3[0].record()
+    for _ in range(reps):
+        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq, gather=True,
+                       workspace=ws)
+    ev3[1].record()
     torch.cuda.synchronize()
     fwd_ms, bwd_ms = ev[0].elapsed_time(ev[1]) / reps, ev[1].elapsed_time(ev[2]) / reps
+    bwd_gather_ms = ev3[0].elapsed_time(ev3[1]) / reps
     nq = nb * queries.shape[1]
     # algorithmic bytes per query: query xy 8 + k (idx 4 + valid 1) + output row 2D (fwd);
     # + cotangent row 2D and dq 8 (bwd); each key row read once and (bwd) written once in fp32
@@ -501,7 +513,7 @@ def run_interp(a, host, dev, k=8, reps=10):
     fwd_bytes = nq * (8 + 5 * k + 2 * D) + kb * (8 + 2 * D)
     bwd_bytes = nq * (8 + 5 * k + 2 * D + 8) + kb * (8 + 2 * D + 2 * 4 * D)
     return {"images": nb, "queries_per_image": int(queries.shape[1]), "keys_per_image": int(keys.shape[1]),
-            "k": k, "dim": D, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+            "k": k, "dim": D, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "bwd_gather_ms": bwd_gather_ms,
             "fwd_queries_per_s": nq / (fwd_ms * 1e-3), "bwd_queries_per_s": nq / (bwd_ms * 1e-3),
             "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
             "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}

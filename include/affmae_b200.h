@@ -114,6 +114,16 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
                       int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream);
+/* The same backward with dfeats gathered through a reverse CSR of the rows (key -> the
+ * (row, slot) entries naming it, rebuilt per call in the workspace) instead of scattered fp32
+ * reductions: each dfeats row is read and written once.  Same semantics and results
+ * (to fp32 rounding); batch * n_queries * k < 2^31. */
+size_t affmae_interp_bwd_gather_workspace(int64_t batch, int64_t n_queries, int64_t n_keys, int64_t k);
+int affmae_interp_bwd_gather(const float* queries, const float* key_coords, const affmae_bf16* feats,
+                             const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
+                             int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
+                             const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries,
+                             void* workspace, size_t workspace_bytes, void* stream);
 
 /* Row LayerNorm (Tape::layer_norm, src/tape.cpp:84-100, VJP :581-617; eps 1e-5):
  * x, y [rows, cols] bf16, gamma/beta [cols] fp32, stats [rows] float2 {mean, rstd}

@@ -58,6 +58,10 @@ int gattn_fwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*
 int gattn_bwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
               int64_t, const void*, void*, float*, float*, float*, float*, float*, float*, float*, float*, float*,
               void*);
+size_t interp_bwd_gather_workspace(int64_t, int64_t, int64_t, int64_t);
+int interp_bwd_gather(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t,
+                      int64_t, int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*,
+                      size_t, void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
@@ -208,6 +212,18 @@ int affmae_interp_bwd(const float* queries, const float* key_coords, const affma
                       const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* stream) {
     return interp_bwd(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
                       dfeats, dp, dqueries, stream);
+}
+
+size_t affmae_interp_bwd_gather_workspace(int64_t batch, int64_t n_queries, int64_t n_keys, int64_t k) {
+    return interp_bwd_gather_workspace(batch, n_queries, n_keys, k);
+}
+int affmae_interp_bwd_gather(const float* queries, const float* key_coords, const affmae_bf16* feats,
+                             const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t n_queries,
+                             int64_t n_keys, int64_t dim, int64_t k, const float* p, double eps,
+                             const affmae_bf16* dout, float* dfeats, float* dp, float* dqueries, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+    return interp_bwd_gather(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
+                             dfeats, dp, dqueries, workspace, workspace_bytes, stream);
 }
 
 // decoder attention over general neighbour rows (src/pipeline.cpp:495-535)

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) interp_fwd_kernel(const float2* __restric
     }
 }
 
-template <int CPR>
+template <int CPR, bool SCATTER>
 __global__ void __launch_bounds__(256) interp_bwd_kernel(const float2* __restrict__ queries,
                                                          const float2* __restrict__ key_xy,
                                                          const uint4* __restrict__ feats,
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) interp_bwd_kernel(const float2* __restric
                                                          int64_t nq, int64_t nk, int k, const float* __restrict__ p_ptr,
                                                          float eps, const uint4* __restrict__ dout,
                                                          float* __restrict__ dfeats, float* __restrict__ dp,
-                                                         float2* __restrict__ dqueries) {
+                                                         float2* __restrict__ dqueries, float* __restrict__ wout) {
     using G = InterpGeo<CPR>;
     constexpr int D = CPR * 8;
     const int lane = threadIdx.x & 31, sl = lane % G::LPR, base = lane - sl;
@@ -183,9 +183,11 @@ __global__ void __launch_bounds__(256) interp_bwd_kernel(const float2* __restric
                 bf8_to_f32(__ldg(fb + int64_t(jt) * CPR + ch), f);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) part = fmaf(g[cc][i], f[i], part);
-                float* dst = dfb + int64_t(jt) * D + ch * 8;
-                red_add_v4(dst, wt * g[cc][0], wt * g[cc][1], wt * g[cc][2], wt * g[cc][3]);
-                red_add_v4(dst + 4, wt * g[cc][4], wt * g[cc][5], wt * g[cc][6], wt * g[cc][7]);
+                if (SCATTER) {
+                    float* dst = dfb + int64_t(jt) * D + ch * 8;
+                    red_add_v4(dst, wt * g[cc][0], wt * g[cc][1], wt * g[cc][2], wt * g[cc][3]);
+                    red_add_v4(dst + 4, wt * g[cc][4], wt * g[cc][5], wt * g[cc][6], wt * g[cc][7]);
+                }
             }
         }
 #pragma unroll
@@ -193,6 +195,11 @@ __global__ void __launch_bounds__(256) interp_bwd_kernel(const float2* __restric
 #pragma unroll
         for (int i = 0; i < G::MPL; ++i)
             if (t == sl + i * G::LPR) dw[i] = part;
+    }
+    if (!SCATTER && ok) {  // the gather pass reads the weights back (0 for invalid slots)
+#pragma unroll
+        for (int i = 0; i < G::MPL; ++i)
+            if (sl + i * G::LPR < k) wout[rw * k + sl + i * G::LPR] = R.w[i];
     }
     float wdot = 0.f;
 #pragma unroll
@@ -295,8 +302,8 @@ int interp_bwd(const float* queries, const float* key_coords, const void* feats,
     auto* dq2 = reinterpret_cast<float2*>(dqueries);
 #define AFFMAE_IB(CPR_)                                                                                      \
     case CPR_ * 8:                                                                                           \
-        interp_bwd_kernel<CPR_><<<interp_blocks<CPR_>(batch * nq), 256, 0, st>>>(                            \
-            q2, k2, f, idx, valid, batch, nq, nk, int(k), p, float(eps), g, dfeats, dp, dq2);                \
+        interp_bwd_kernel<CPR_, true><<<interp_blocks<CPR_>(batch * nq), 256, 0, st>>>(                      \
+            q2, k2, f, idx, valid, batch, nq, nk, int(k), p, float(eps), g, dfeats, dp, dq2, nullptr);       \
         break;
     switch (dim) {
         AFFMAE_IB(8)
@@ -306,6 +313,191 @@ int interp_bwd(const float* queries, const float* key_coords, const void* feats,
     }
 #undef AFFMAE_IB
     AFFMAE_LAUNCH_CHECK("interp_bwd_kernel");
+    return AFFMAE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Gather backward: dfeats from a reverse CSR of the knn rows (key -> the (row, slot)
+// entries naming it) instead of scattered fp32 reductions.  The query pass writes
+// the softmax weights; rev_count / rev_scan / rev_fill build the CSR per call (the
+// rows change every call); interp_gather_kernel owns each key row (LPR lanes, CPL
+// chunks each), sums w * g over its entries and adds the result once.
+__global__ void interp_rev_count_kernel(const int32_t* __restrict__ idx, const uint8_t* __restrict__ valid,
+                                        int64_t rows, int64_t nq, int64_t nk, int k, int32_t* __restrict__ cnt) {
+    const int64_t n = rows * k;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        if (valid[e]) atomicAdd(cnt + (e / k / nq) * (nk + 1) + idx[e], 1);
+}
+
+// Per-image exclusive scan of the key counts, in place: one 1024-thread block per image,
+// cnt[b*(nk+1) + j] -> offset of key j inside image b's entry range, cnt[b*(nk+1) + nk] = total.
+__global__ void __launch_bounds__(1024) interp_rev_scan_kernel(int32_t* __restrict__ cnt, int64_t nk) {
+    __shared__ int32_t wsum[32];
+    int32_t* c = cnt + int64_t(blockIdx.x) * (nk + 1);
+    const int64_t per = (nk + 1023) / 1024, lo = threadIdx.x * per, hi = lo + per < nk ? lo + per : nk;
+    int32_t s = 0;
+    for (int64_t i = lo; i < hi; ++i) s += c[i];
+    // block-exclusive prefix of the per-thread sums
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += v;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    int32_t run = inc - s + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int64_t i = lo; i < hi; ++i) {
+        const int32_t v = c[i];
+        c[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 1023) c[nk] = wsum[31];
+}
+
+__global__ void interp_rev_fill_kernel(const int32_t* __restrict__ idx, const uint8_t* __restrict__ valid,
+                                       int64_t rows, int64_t nq, int64_t nk, int k, const int32_t* __restrict__ off,
+                                       int32_t* __restrict__ cur, int32_t* __restrict__ ent,
+                                       int32_t* __restrict__ ent_key) {
+    const int64_t n = rows * k;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+        if (valid[e]) {
+            const int64_t b = e / k / nq, j = idx[e];
+            const int64_t pos = b * nq * k + off[b * (nk + 1) + j] + atomicAdd(cur + b * nk + j, 1);
+            ent[pos] = int32_t(e);
+            ent_key[pos] = int32_t(b * nk + j);
+        }
+}
+
+// Balanced gather: warps walk the key-sorted entry array in fixed chunks of 32 (lanes over
+// the D dims, VPL each), so a key named by thousands of queries (the Perlin mask's border
+// tokens) is spread over many warps.  A chunk loads its 32 entries, weights and keys with
+// one instruction each, accumulates w * g while the key stays the same and flushes the
+// running row with one vector reduction per lane at each key change (~2 flushes per chunk
+// instead of one reduction per (entry, dim chunk) in the scattered backward).
+template <int D>
+__global__ void __launch_bounds__(256) interp_gather_kernel(const int32_t* __restrict__ off,
+                                                            const int32_t* __restrict__ ent,
+                                                            const int32_t* __restrict__ ent_key,
+                                                            const float* __restrict__ w, int64_t batch, int64_t nq,
+                                                            int64_t nk, int k, const __nv_bfloat16* __restrict__ dout,
+                                                            float* __restrict__ dfeats) {
+    constexpr int VPL = D / 32;
+    static_assert(VPL % 2 == 0, "VPL");
+    const int lane = threadIdx.x & 31;
+    const int64_t span = nq * k, total = batch * span, nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    auto flush = [&](int32_t key, float (&acc)[VPL]) {
+        float* d = dfeats + int64_t(key) * D + lane * VPL;
+        if constexpr (VPL % 4 == 0) {
+#pragma unroll
+            for (int c = 0; c < VPL; c += 4) red_add_v4(d + c, acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        } else {
+            atomicAdd(d, acc[0]);
+            atomicAdd(d + 1, acc[1]);
+        }
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) acc[i] = 0.f;
+    };
+    for (int64_t c0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; c0 < total; c0 += nwarps * 32) {
+        const int64_t pos = c0 + lane;
+        int32_t mkey = -1, mrow = 0;
+        float mw = 0.f;
+        if (pos < total) {
+            const int64_t b = pos / span;
+            if (pos - b * span < off[b * (nk + 1) + nk]) {
+                const int32_t e = __ldg(ent + pos);
+                mkey = __ldg(ent_key + pos);
+                mw = __ldg(w + e);
+                mrow = e / k;
+            }
+        }
+        if (__ballot_sync(0xffffffffu, mkey >= 0) == 0u) continue;
+        float acc[VPL];
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) acc[i] = 0.f;
+        int32_t cur = -1;
+#pragma unroll 4
+        for (int u = 0; u < 32; ++u) {
+            const int32_t key = __shfl_sync(0xffffffffu, mkey, u);
+            const int32_t row = __shfl_sync(0xffffffffu, mrow, u);
+            const float wt = __shfl_sync(0xffffffffu, mw, u);
+            if (key < 0) continue;  // uniform
+            if (key != cur) {
+                if (cur >= 0) flush(cur, acc);
+                cur = key;
+            }
+            const __nv_bfloat16* g = dout + int64_t(row) * D + lane * VPL;
+#pragma unroll
+            for (int c = 0; c < VPL; c += 2) {
+                const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(g + c));
+                acc[c] = fmaf(wt, t.x, acc[c]);
+                acc[c + 1] = fmaf(wt, t.y, acc[c + 1]);
+            }
+        }
+        if (cur >= 0) flush(cur, acc);
+    }
+}
+
+size_t interp_bwd_gather_workspace(int64_t batch, int64_t nq, int64_t nk, int64_t k) {
+    const int64_t keys = batch * nk, ents = batch * nq * k;
+    return size_t(batch * (nk + 1) + keys + 2 * ents) * 4 + size_t(ents) * 4 + 1024;
+}
+
+int interp_bwd_gather(const float* queries, const float* key_coords, const void* feats, const int32_t* idx,
+                      const uint8_t* valid, int64_t batch, int64_t nq, int64_t nk, int64_t dim, int64_t k,
+                      const float* p, double eps, const void* dout, float* dfeats, float* dp, float* dqueries,
+                      void* workspace, size_t ws_bytes, void* stream) {
+    int rc = interp_check(batch, nq, nk, dim, k);
+    if (rc) return rc;
+    if (!queries || !key_coords || !feats || !idx || !valid || !p || !dout || !dfeats || !dp || !dqueries)
+        return fail(AFFMAE_ECONFIG, "interp bwd: null pointer");
+    if (batch * nq * k >= (int64_t(1) << 31)) return fail(AFFMAE_EUNSUPPORTED, "interp bwd: more than 2^31 entries");
+    if (!workspace || ws_bytes < interp_bwd_gather_workspace(batch, nq, nk, k))
+        return fail(AFFMAE_ECONFIG, "interp bwd: workspace too small");
+    if (batch * nq == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    const int64_t keys = batch * nk, ents = batch * nq * k;
+    int32_t* off = static_cast<int32_t*>(workspace);  // [B, nk + 1] per-image offsets
+    int32_t* cur = off + batch * (nk + 1);
+    int32_t* ent = cur + keys;
+    int32_t* ent_key = ent + ents;
+    float* wbuf = reinterpret_cast<float*>(ent_key + ents);
+    cudaMemsetAsync(off, 0, size_t(batch * (nk + 1) + keys) * 4, st);
+    const unsigned eb = unsigned(std::min<int64_t>((ents + 255) / 256, 8 * kNumSMs));
+    interp_rev_count_kernel<<<eb, 256, 0, st>>>(idx, valid, batch * nq, nq, nk, int(k), off);
+    interp_rev_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(off, nk);
+    interp_rev_fill_kernel<<<eb, 256, 0, st>>>(idx, valid, batch * nq, nq, nk, int(k), off, cur, ent, ent_key);
+    const auto* q2 = reinterpret_cast<const float2*>(queries);
+    const auto* k2 = reinterpret_cast<const float2*>(key_coords);
+    const auto* f = static_cast<const uint4*>(feats);
+    const auto* g = static_cast<const uint4*>(dout);
+    auto* dq2 = reinterpret_cast<float2*>(dqueries);
+#define AFFMAE_IG(CPR_)                                                                                      \
+    case CPR_ * 8:                                                                                           \
+        interp_bwd_kernel<CPR_, false><<<interp_blocks<CPR_>(batch * nq), 256, 0, st>>>(                     \
+            q2, k2, f, idx, valid, batch, nq, nk, int(k), p, float(eps), g, dfeats, dp, dq2, wbuf);          \
+        interp_gather_kernel<CPR_ * 8><<<unsigned(std::min<int64_t>((ents + 255) / 256, 16 * kNumSMs)), 256, 0, st>>>( \
+            off, ent, ent_key, wbuf, batch, nq, nk, int(k), static_cast<const __nv_bfloat16*>(dout), dfeats); \
+        break;
+    switch (dim) {
+        AFFMAE_IG(8)
+        AFFMAE_IG(16)
+        AFFMAE_IG(32)
+        AFFMAE_IG(64)
+    }
+#undef AFFMAE_IG
+    AFFMAE_LAUNCH_CHECK("interp_bwd_gather");
     return AFFMAE_OK;
 }
 

@@ -354,9 +354,11 @@ def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, stream=None)
 
 
 def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, dfeats=None, dp=None, dqueries=None,
-               stream=None):
+               stream=None, gather=False, workspace=None):
     """make_interp_op backward (proj/src/interpolation.cpp:224-251): accumulates into
-    dfeats [B, N, D] fp32, dp [1] fp32 and dqueries [B, Q, 2] fp32 (zeros if not given)."""
+    dfeats [B, N, D] fp32, dp [1] fp32 and dqueries [B, Q, 2] fp32 (zeros if not given).
+    gather=True: dfeats through a per-call reverse CSR (affmae_interp_bwd_gather) instead of
+    scattered fp32 reductions."""
     _req(dout, torch.bfloat16, "dout")
     B, Q, _ = queries.shape
     N, D = feats.shape[1], feats.shape[2]
@@ -368,12 +370,19 @@ def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, dfeats
         dp = torch.zeros(1, dtype=torch.float32, device=dev)
     if dqueries is None:
         dqueries = torch.zeros((B, Q, 2), dtype=torch.float32, device=dev)
-    capi.check(capi.lib().affmae_interp_bwd(
-        C.c_void_p(queries.data_ptr()), C.c_void_p(key_coords.data_ptr()), C.c_void_p(feats.data_ptr()),
-        C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()), C.c_int64(B), C.c_int64(Q), C.c_int64(N),
-        C.c_int64(D), C.c_int64(K), C.c_void_p(p.data_ptr()), C.c_double(eps), C.c_void_p(dout.data_ptr()),
-        C.c_void_p(dfeats.data_ptr()), C.c_void_p(dp.data_ptr()), C.c_void_p(dqueries.data_ptr()),
-        _stream(stream)), "interp_bwd")
+    args = (C.c_void_p(queries.data_ptr()), C.c_void_p(key_coords.data_ptr()), C.c_void_p(feats.data_ptr()),
+            C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()), C.c_int64(B), C.c_int64(Q), C.c_int64(N),
+            C.c_int64(D), C.c_int64(K), C.c_void_p(p.data_ptr()), C.c_double(eps), C.c_void_p(dout.data_ptr()),
+            C.c_void_p(dfeats.data_ptr()), C.c_void_p(dp.data_ptr()), C.c_void_p(dqueries.data_ptr()))
+    L = capi.lib()
+    if gather:
+        nbytes = L.affmae_interp_bwd_gather_workspace(C.c_int64(B), C.c_int64(Q), C.c_int64(N), C.c_int64(K))
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = _workspace(nbytes, dev)
+        capi.check(L.affmae_interp_bwd_gather(*args, C.c_void_p(workspace.data_ptr()), C.c_size_t(workspace.numel()),
+                                              _stream(stream)), "interp_bwd_gather")
+    else:
+        capi.check(L.affmae_interp_bwd(*args, _stream(stream)), "interp_bwd")
     return dfeats, dp, dqueries
 
 

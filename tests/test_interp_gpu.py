@@ -29,8 +29,9 @@ CASES = [
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("gather", [False, True], ids=["scatter", "gather"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_interp_fwd_bwd(case):
+def test_interp_fwd_bwd(case, gather):
     import torch
     from paper_2602_16249_b200 import ops
     name, mk_keys, mk_q, k, dim, p = case
@@ -53,7 +54,7 @@ def test_interp_fwd_bwd(case):
     qd, kd = _dev(q, torch.float32), _dev(keys, torch.float32)
     fd = _dev(feats, torch.bfloat16)
     out = ops.interp_fwd(qd, kd, fd, idx, valid, pd)
-    df, dp, dq = ops.interp_bwd(qd, kd, fd, idx, valid, pd, _dev(dout, torch.bfloat16))
+    df, dp, dq = ops.interp_bwd(qd, kd, fd, idx, valid, pd, _dev(dout, torch.bfloat16), gather=gather)
     torch.cuda.synchronize()
     out, df, dq, dp = out.float().cpu().numpy(), df.cpu().numpy(), dq.cpu().numpy(), float(dp.item())
     ii, vv = idx.cpu().numpy(), valid.cpu().numpy()
@@ -67,6 +68,32 @@ def test_interp_fwd_bwd(case):
         assert dq[b, 0, 0] == dq[b, 0, 0]  # finite at the coincidence
         want_dp += wdp
     assert abs(dp - want_dp) <= 1e-2 * max(1.0, abs(want_dp))
+
+
+@pytest.mark.gpu
+def test_interp_bwd_gather_accumulates_like_scatter():
+    """The reverse-CSR backward adds into existing gradients (CustomOp +=) and matches the
+    scattered-reduction backward to fp32 rounding, at the decoder's size class."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    rng = np.random.default_rng(3)
+    keys = _dev(lattice_coords(3, 64, seed0=11), torch.float32)
+    g = np.stack(np.meshgrid(np.arange(64) * 8.0 + 4.0, np.arange(64) * 8.0 + 4.0), -1).reshape(1, -1, 2)
+    q = _dev(np.repeat(g, 3, 0).astype(np.float32), torch.float32)
+    feats = _dev(rng.standard_normal((3, keys.shape[1], 128)), torch.bfloat16)
+    dout = _dev(rng.standard_normal((3, q.shape[1], 128)), torch.bfloat16)
+    pd = _dev([1.3], torch.float32)
+    idx, valid = ops.knn(q, keys, 8)
+    res = []
+    for gather in (False, True):
+        df = torch.ones((3, keys.shape[1], 128), dtype=torch.float32, device="cuda")
+        dp = torch.full((1,), 0.5, device="cuda")
+        dq = torch.ones((3, q.shape[1], 2), device="cuda")
+        ops.interp_bwd(q, keys, feats, idx, valid, pd, dout, dfeats=df, dp=dp, dqueries=dq, gather=gather)
+        res.append((df.cpu().numpy(), float(dp.item()), dq.cpu().numpy()))
+    (a, ap, aq), (b, bp, bq) = res
+    assert np.abs(a - b).max() <= 1e-4 * max(1.0, np.abs(a).max())
+    assert abs(ap - bp) <= 1e-4 * max(1.0, abs(ap)) and np.array_equal(aq, bq)
 
 
 @pytest.mark.gpu

@@ -28,6 +28,7 @@ bias = ops.BiasNet.from_numpy(inputs.bias_params(heads, 8, np.random.default_rng
 for _ in range(3):
     ops.interp_fwd(coords, keys, feats, iidx, ivalid, p)
     ops.interp_bwd(coords, keys, feats, iidx, ivalid, p, dout)
+    ops.interp_bwd(coords, keys, feats, iidx, ivalid, p, dout, gather=True)
     ops.gattn_fwd(q, k, v, bk, bk, coords, idx, valid, bias, heads, hd)
     ops.gattn_bwd(q, k, v, bk, bk, coords, idx, valid, bias, heads, hd, do)
 torch.cuda.synchronize()
