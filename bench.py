@@ -483,7 +483,7 @@ def run_interp(a, host, dev, k=8, reps=10):
     dq = torch.zeros((nb, queries.shape[1], 2), dtype=torch.float32, device=dev)
     for _ in range(2):
         ops.interp_fwd(queries, keys, feats, idx, valid, p)
-        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq)
+        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq, gather=False)
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     ev[0].record()
@@ -491,7 +491,7 @@ def run_interp(a, host, dev, k=8, reps=10):
         ops.interp_fwd(queries, keys, feats, idx, valid, p)
     ev[1].record()
     for _ in range(reps):
-        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq)
+        ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq, gather=False)
     ev[2].record()
     for _ in range(2):
         ops.interp_bwd(queries, keys, feats, idx, valid, p, dout, dfeats=dfe, dp=dp, dqueries=dq, gather=True)
@@ -516,6 +516,7 @@ def run_interp(a, host, dev, k=8, reps=10):
             "k": k, "dim": D, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "bwd_gather_ms": bwd_gather_ms,
             "fwd_queries_per_s": nq / (fwd_ms * 1e-3), "bwd_queries_per_s": nq / (bwd_ms * 1e-3),
             "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
+            "bwd_gather_gbs": bwd_bytes / (bwd_gather_ms * 1e-3) / 1e9,
             "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
 
 

@@ -288,7 +288,7 @@ int affmae_attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc
  * (width in [1, 31], image-local ids into the same N tokens, e.g. from affmae_knn);
  * head_dim 16, 32 or 64.  Forward: out [B, N, h*d] bf16, lse [B, N, h] fp32.
  * Backward: dq [B, N, h*d] bf16 overwritten; dk, dv [B, N, h*d] fp32 and the
- * parameter gradients ACCUMULATED (+=).  No workspace. */
+ * parameter gradients ACCUMULATED (+=). */
 int affmae_gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
                      const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width,
                      affmae_bf16* out, float* lse, void* stream);
@@ -296,7 +296,12 @@ int affmae_gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, co
                      const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width,
                      const affmae_bf16* dout, affmae_bf16* dq, float* dk, float* dv,
                      float* dblank_k, float* dblank_v, float* dw1, float* db1, float* dw2,
-                     float* db2, float* dblank, void* stream);
+                     float* db2, float* dblank, void* workspace, size_t workspace_bytes,
+                     void* stream);
+/* Workspace for the gather-mode backward (0 if heads*head_dim is not 32..512, power of two).
+ * With a workspace, dk / dv are gathered over a per-call reverse CSR of the rows (key -> the
+ * (row, slot) entries naming it) instead of scattered fp32 reductions; NULL = scatter mode. */
+size_t affmae_gattn_bwd_workspace(const affmae_attn_desc* a, int64_t batch, int64_t tokens, int64_t width);
 
 /* ------------------------------------------------------------------------
  * Adaptive KNN merge (src/merging.cpp).

@@ -480,9 +480,11 @@ std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, 
             ccheck(cudaMemset(df.p, 0, size_t(nk * dim * 4)), "memset");
             ccheck(cudaMemset(dp.p, 0, 4), "memset");
             ccheck(cudaMemset(dq.p, 0, size_t(nq * 2 * 4)), "memset");
-            check(affmae_interp_bwd(q->as<float>(), d.kc->as<float>(), f->as<affmae_bf16>(), d.idx->as<int32_t>(),
-                                    d.valid->as<uint8_t>(), 1, nq, nk, dim, nbrs.width, pt->as<float>(), eps,
-                                    dg->as<affmae_bf16>(), df.as<float>(), dp.as<float>(), dq.as<float>(), nullptr),
+            Dev ws(affmae_interp_bwd_gather_workspace(1, nq, nk, nbrs.width));
+            check(affmae_interp_bwd_gather(q->as<float>(), d.kc->as<float>(), f->as<affmae_bf16>(),
+                                           d.idx->as<int32_t>(), d.valid->as<uint8_t>(), 1, nq, nk, dim, nbrs.width,
+                                           pt->as<float>(), eps, dg->as<affmae_bf16>(), df.as<float>(), dp.as<float>(),
+                                           dq.as<float>(), ws.p, ws.n, nullptr),
                   "interp_bwd");
             if (in_grads[0]) {
                 auto h = download<float>(df, size_t(nk * dim));
@@ -565,7 +567,7 @@ std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int hea
                                    dout->as<affmae_bf16>(), dq.as<affmae_bf16>(), g[1]->as<float>(),
                                    g[2]->as<float>(), g[3]->as<float>(), g[4]->as<float>(), g[5]->as<float>(),
                                    g[6]->as<float>(), g[7]->as<float>(), g[8]->as<float>(), g[9]->as<float>(),
-                                   nullptr),
+                                   nullptr, 0, nullptr),
                   "gattn_bwd");
             ccheck(cudaDeviceSynchronize(), "sync");
             if (in_grads[0]) {

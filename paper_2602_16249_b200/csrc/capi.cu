@@ -57,7 +57,8 @@ int gattn_fwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*
               int64_t, void*, float*, void*);
 int gattn_bwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
               int64_t, const void*, void*, float*, float*, float*, float*, float*, float*, float*, float*, float*,
-              void*);
+              void*, size_t, void*);
+size_t gattn_bwd_workspace(const affmae_attn_desc*, int64_t, int64_t, int64_t);
 size_t interp_bwd_gather_workspace(int64_t, int64_t, int64_t, int64_t);
 int interp_bwd_gather(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t,
                       int64_t, int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*,
@@ -235,9 +236,13 @@ int affmae_gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, co
 int affmae_gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
                      const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width, const affmae_bf16* dout,
                      affmae_bf16* dq, float* dk, float* dv, float* dblank_k, float* dblank_v, float* dw1,
-                     float* db1, float* dw2, float* db2, float* dblank, void* stream) {
+                     float* db1, float* dw2, float* db2, float* dblank, void* workspace, size_t workspace_bytes,
+                     void* stream) {
     return gattn_bwd(a, in, idx, valid, batch, tokens, width, dout, dq, dk, dv, dblank_k, dblank_v, dw1, db1, dw2,
-                     db2, dblank, stream);
+                     db2, dblank, workspace, workspace_bytes, stream);
+}
+size_t affmae_gattn_bwd_workspace(const affmae_attn_desc* a, int64_t batch, int64_t tokens, int64_t width) {
+    return gattn_bwd_workspace(a, batch, tokens, width);
 }
 
 // dense linear layer (Tape matmul + bias + gelu_erf), tcgen05

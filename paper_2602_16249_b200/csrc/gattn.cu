@@ -28,6 +28,7 @@ struct GAttnP {
     int64_t batch, n;
     int m, heads, hidden;
     float scale, inv_patch;
+    float2* dsw;  // backward gather mode: {scale dS, w} per (entry, head); nullptr = scatter dk / dv
 };
 
 __device__ __forceinline__ void gred_v4(float* addr, float a, float b, float c, float d) {
@@ -255,12 +256,15 @@ __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfl
             float kf[HD];
             gload_row<HD>(p.k + kr, kf, 1.f);
             const float a = p.scale * dS[j];
+            if (p.dsw) p.dsw[(gi * p.m + j) * p.heads + h] = make_float2(a, w[j]);
 #pragma unroll
             for (int c = 0; c < HD; c += 4) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) dqa[c + i] = fmaf(dS[j], kf[c + i], dqa[c + i]);
-                gred_v4(dk + kr + c, a * qf[c], a * qf[c + 1], a * qf[c + 2], a * qf[c + 3]);
-                gred_v4(dv + kr + c, w[j] * gf[c], w[j] * gf[c + 1], w[j] * gf[c + 2], w[j] * gf[c + 3]);
+                if (!p.dsw) {
+                    gred_v4(dk + kr + c, a * qf[c], a * qf[c + 1], a * qf[c + 2], a * qf[c + 3]);
+                    gred_v4(dv + kr + c, w[j] * gf[c], w[j] * gf[c + 1], w[j] * gf[c + 2], w[j] * gf[c + 3]);
+                }
             }
         }
         if (act) {
@@ -371,6 +375,101 @@ __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfl
     }
 }
 
+void rev_csr_build(const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t nq, int64_t nk, int k,
+                   int32_t* off, int32_t* cur, int32_t* ent, int32_t* ent_key, cudaStream_t st);
+
+// dk / dv by gathering over the key-sorted reverse CSR of the rows (the interpolation
+// backward's balanced scheme, interp.cu): warps walk chunks of 32 entries, lanes over the
+// D = heads*HD row (VPL dims each, inside one head), flush per key change.
+template <int D>
+__global__ void __launch_bounds__(256) gattn_kv_gather_kernel(const int32_t* __restrict__ off,
+                                                              const int32_t* __restrict__ ent,
+                                                              const int32_t* __restrict__ ent_key,
+                                                              const float2* __restrict__ dsw, int64_t batch,
+                                                              int64_t n, int m, int heads, int hd,
+                                                              const __nv_bfloat16* __restrict__ q,
+                                                              const __nv_bfloat16* __restrict__ dout,
+                                                              float* __restrict__ dk, float* __restrict__ dv) {
+    constexpr int VPL = D / 32;
+    const int lane = threadIdx.x & 31, h = lane * VPL / hd;
+    const int64_t span = n * m, total = batch * span, nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    float ak[VPL], av[VPL];
+    auto flush = [&](int32_t key) {
+        float* pk = dk + int64_t(key) * D + lane * VPL;
+        float* pv = dv + int64_t(key) * D + lane * VPL;
+        if constexpr (VPL % 4 == 0) {
+#pragma unroll
+            for (int c = 0; c < VPL; c += 4) {
+                gred_v4(pk + c, ak[c], ak[c + 1], ak[c + 2], ak[c + 3]);
+                gred_v4(pv + c, av[c], av[c + 1], av[c + 2], av[c + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < VPL; ++c) {
+                atomicAdd(pk + c, ak[c]);
+                atomicAdd(pv + c, av[c]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) ak[i] = av[i] = 0.f;
+    };
+    for (int64_t c0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; c0 < total; c0 += nwarps * 32) {
+        const int64_t pos = c0 + lane;
+        int32_t mkey = -1, me = 0;
+        if (pos < total) {
+            const int64_t b = pos / span;
+            if (pos - b * span < off[b * (n + 1) + n]) {
+                me = __ldg(ent + pos);
+                mkey = __ldg(ent_key + pos);
+            }
+        }
+        if (__ballot_sync(0xffffffffu, mkey >= 0) == 0u) continue;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) ak[i] = av[i] = 0.f;
+        int32_t cur = -1;
+#pragma unroll 4
+        for (int u = 0; u < 32; ++u) {
+            const int32_t key = __shfl_sync(0xffffffffu, mkey, u);
+            const int32_t e = __shfl_sync(0xffffffffu, me, u);
+            if (key < 0) continue;  // uniform
+            if (key != cur) {
+                if (cur >= 0) flush(cur);
+                cur = key;
+            }
+            const float2 sw = __ldg(dsw + int64_t(e) * heads + h);
+            const int64_t row = e / m;
+            const __nv_bfloat16* qr = q + row * D + lane * VPL;
+            const __nv_bfloat16* gr = dout + row * D + lane * VPL;
+            if constexpr (VPL == 1) {
+                ak[0] = fmaf(sw.x, __bfloat162float(qr[0]), ak[0]);
+                av[0] = fmaf(sw.y, __bfloat162float(gr[0]), av[0]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < VPL; c += 2) {
+                    const float2 tq = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qr + c));
+                    const float2 tg = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gr + c));
+                    ak[c] = fmaf(sw.x, tq.x, ak[c]);
+                    ak[c + 1] = fmaf(sw.x, tq.y, ak[c + 1]);
+                    av[c] = fmaf(sw.y, tg.x, av[c]);
+                    av[c + 1] = fmaf(sw.y, tg.y, av[c + 1]);
+                }
+            }
+        }
+        if (cur >= 0) flush(cur);
+    }
+}
+
+static bool gattn_gather_ok(const affmae_attn_desc* a) {
+    const int d = a->heads * a->head_dim;
+    return d == 32 || d == 64 || d == 128 || d == 256 || d == 512;
+}
+
+size_t gattn_bwd_workspace(const affmae_attn_desc* a, int64_t batch, int64_t tokens, int64_t width) {
+    if (!a || !gattn_gather_ok(a)) return 0;
+    const int64_t ents = batch * tokens * width;
+    return size_t(batch * (tokens + 1) + batch * tokens + 2 * ents) * 4 + size_t(ents) * a->heads * 8 + 1024;
+}
+
 static int gattn_fill(GAttnP& p, const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx,
                       const uint8_t* valid, int64_t batch, int64_t tokens, int64_t width) {
     if (!a || !in || !idx || !valid || !in->q || !in->k || !in->v || !in->blank_k || !in->blank_v || !in->coords ||
@@ -442,7 +541,8 @@ static void gattn_bwd_launch(int mw, unsigned nb, dim3 bt, size_t sm, cudaStream
 
 int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
               int64_t batch, int64_t tokens, int64_t width, const void* dout, void* dq, float* dk, float* dv,
-              float* dbk, float* dbv, float* dw1, float* db1, float* dw2, float* db2, float* dblank, void* stream) {
+              float* dbk, float* dbv, float* dw1, float* db1, float* dw2, float* db2, float* dblank, void* workspace,
+              size_t ws_bytes, void* stream) {
     GAttnP p{};
     int rc = gattn_fill(p, a, in, idx, valid, batch, tokens, width);
     if (rc) return rc;
@@ -456,10 +556,44 @@ int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
     auto* q = static_cast<__nv_bfloat16*>(dq);
     cudaStream_t st = as_stream(stream);
     const int mw = int(width);
+    const bool gather = workspace != nullptr;
+    int32_t *off = nullptr, *cur = nullptr, *ent = nullptr, *ent_key = nullptr;
+    if (gather) {
+        if (!gattn_gather_ok(a)) return fail(AFFMAE_EUNSUPPORTED, "gattn bwd: gather mode needs heads*head_dim in {32..512}");
+        if (batch * tokens * width >= (int64_t(1) << 31)) return fail(AFFMAE_EUNSUPPORTED, "gattn bwd: too many entries");
+        if (ws_bytes < gattn_bwd_workspace(a, batch, tokens, width)) return fail(AFFMAE_ECONFIG, "gattn bwd: workspace too small");
+        const int64_t ents = batch * tokens * width;
+        p.dsw = static_cast<float2*>(workspace);  // first: 8-byte aligned
+        off = reinterpret_cast<int32_t*>(p.dsw + ents * a->heads);
+        cur = off + batch * (tokens + 1);
+        ent = cur + batch * tokens;
+        ent_key = ent + ents;
+        rev_csr_build(idx, valid, batch, tokens, tokens, mw, off, cur, ent, ent_key, st);
+    }
     if (a->head_dim == 16) gattn_bwd_launch<16>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
     else if (a->head_dim == 32) gattn_bwd_launch<32>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
     else gattn_bwd_launch<64>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
     AFFMAE_LAUNCH_CHECK("gattn_bwd_kernel");
+    if (gather) {
+        const int64_t ents = batch * tokens * width;
+        const unsigned gb = unsigned(std::max<int64_t>(1, std::min<int64_t>((ents + 255) / 256, 16 * kNumSMs)));
+        const auto* qq = p.q;
+        const int D = a->heads * a->head_dim;
+#define AFFMAE_GG(D_)                                                                                           \
+    case D_:                                                                                                    \
+        gattn_kv_gather_kernel<D_><<<gb, 256, 0, st>>>(off, ent, ent_key, p.dsw, batch, tokens, mw, a->heads,   \
+                                                       a->head_dim, qq, g, dk, dv);                             \
+        break;
+        switch (D) {
+            AFFMAE_GG(32)
+            AFFMAE_GG(64)
+            AFFMAE_GG(128)
+            AFFMAE_GG(256)
+            AFFMAE_GG(512)
+        }
+#undef AFFMAE_GG
+        AFFMAE_LAUNCH_CHECK("gattn_kv_gather_kernel");
+    }
     return AFFMAE_OK;
 }
 

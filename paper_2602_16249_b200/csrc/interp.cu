@@ -329,41 +329,44 @@ __global__ void interp_rev_count_kernel(const int32_t* __restrict__ idx, const u
         if (valid[e]) atomicAdd(cnt + (e / k / nq) * (nk + 1) + idx[e], 1);
 }
 
-// Per-image exclusive scan of the key counts, in place: one 1024-thread block per image,
+// Per-image exclusive scan of the key counts, in place: one 1024-thread block per image walks
+// its nk counts in coalesced tiles of 1024 (one per thread), carrying the running total;
 // cnt[b*(nk+1) + j] -> offset of key j inside image b's entry range, cnt[b*(nk+1) + nk] = total.
 __global__ void __launch_bounds__(1024) interp_rev_scan_kernel(int32_t* __restrict__ cnt, int64_t nk) {
     __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
     int32_t* c = cnt + int64_t(blockIdx.x) * (nk + 1);
-    const int64_t per = (nk + 1023) / 1024, lo = threadIdx.x * per, hi = lo + per < nk ? lo + per : nk;
-    int32_t s = 0;
-    for (int64_t i = lo; i < hi; ++i) s += c[i];
-    // block-exclusive prefix of the per-thread sums
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int32_t inc = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-    }
-    if (lane == 31) wsum[warp] = inc;
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    if (warp == 0) {
-        int32_t t = wsum[lane];
+    for (int64_t t0 = 0; t0 < nk; t0 += 1024) {
+        const int64_t i = t0 + threadIdx.x;
+        const int32_t v = i < nk ? c[i] : 0;
+        int32_t inc = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int32_t v = __shfl_up_sync(0xffffffffu, t, o);
-            if (lane >= o) t += v;
+            const int32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
         }
-        wsum[lane] = t;
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            int32_t t = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            wsum[lane] = t;
+        }
+        __syncthreads();
+        const int32_t base = carry;
+        if (i < nk) c[i] = base + inc - v + (warp > 0 ? wsum[warp - 1] : 0);
+        __syncthreads();
+        if (threadIdx.x == 0) carry = base + wsum[31];
+        __syncthreads();
     }
-    __syncthreads();
-    int32_t run = inc - s + (warp > 0 ? wsum[warp - 1] : 0);
-    for (int64_t i = lo; i < hi; ++i) {
-        const int32_t v = c[i];
-        c[i] = run;
-        run += v;
-    }
-    if (threadIdx.x == 1023) c[nk] = wsum[31];
+    if (threadIdx.x == 0) c[nk] = carry;
 }
 
 __global__ void interp_rev_fill_kernel(const int32_t* __restrict__ idx, const uint8_t* __restrict__ valid,
@@ -449,6 +452,21 @@ __global__ void __launch_bounds__(256) interp_gather_kernel(const int32_t* __res
     }
 }
 
+// Reverse CSR of B images' neighbour rows idx/valid [B, nq, k] over nk keys, in caller
+// buffers: off [B, nk+1] (per-image offsets), cur [B, nk] (scratch), ent / ent_key
+// [B*nq*k] (image b's entries at b*nq*k + off, sorted by key; ent = global row*k + slot,
+// ent_key = global key).  Shared with the decoder attention backward (gattn.cu).
+void rev_csr_build(const int32_t* idx, const uint8_t* valid, int64_t batch, int64_t nq, int64_t nk, int k,
+                   int32_t* off, int32_t* cur, int32_t* ent, int32_t* ent_key, cudaStream_t st) {
+    const int64_t ents = batch * nq * k;
+    cudaMemsetAsync(off, 0, size_t(batch * (nk + 1)) * 4, st);
+    cudaMemsetAsync(cur, 0, size_t(batch * nk) * 4, st);
+    const unsigned eb = unsigned(std::max<int64_t>(1, std::min<int64_t>((ents + 255) / 256, 8 * kNumSMs)));
+    interp_rev_count_kernel<<<eb, 256, 0, st>>>(idx, valid, batch * nq, nq, nk, k, off);
+    interp_rev_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(off, nk);
+    interp_rev_fill_kernel<<<eb, 256, 0, st>>>(idx, valid, batch * nq, nq, nk, k, off, cur, ent, ent_key);
+}
+
 size_t interp_bwd_gather_workspace(int64_t batch, int64_t nq, int64_t nk, int64_t k) {
     const int64_t keys = batch * nk, ents = batch * nq * k;
     return size_t(batch * (nk + 1) + keys + 2 * ents) * 4 + size_t(ents) * 4 + 1024;
@@ -473,11 +491,7 @@ int interp_bwd_gather(const float* queries, const float* key_coords, const void*
     int32_t* ent = cur + keys;
     int32_t* ent_key = ent + ents;
     float* wbuf = reinterpret_cast<float*>(ent_key + ents);
-    cudaMemsetAsync(off, 0, size_t(batch * (nk + 1) + keys) * 4, st);
-    const unsigned eb = unsigned(std::min<int64_t>((ents + 255) / 256, 8 * kNumSMs));
-    interp_rev_count_kernel<<<eb, 256, 0, st>>>(idx, valid, batch * nq, nq, nk, int(k), off);
-    interp_rev_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(off, nk);
-    interp_rev_fill_kernel<<<eb, 256, 0, st>>>(idx, valid, batch * nq, nq, nk, int(k), off, cur, ent, ent_key);
+    rev_csr_build(idx, valid, batch, nq, nk, int(k), off, cur, ent, ent_key, st);
     const auto* q2 = reinterpret_cast<const float2*>(queries);
     const auto* k2 = reinterpret_cast<const float2*>(key_coords);
     const auto* f = static_cast<const uint4*>(feats);

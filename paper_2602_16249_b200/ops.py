@@ -242,9 +242,11 @@ def gattn_fwd(q, k, v, blank_k, blank_v, coords, idx, valid, bias: BiasNet, head
 
 
 def gattn_bwd(q, k, v, blank_k, blank_v, coords, idx, valid, bias: BiasNet, heads, head_dim, dout,
-              grads: AttnGrads | None = None, stream=None):
+              grads: AttnGrads | None = None, stream=None, gather=False, workspace=None):
     """Backward of gattn_fwd (nbhd_attn_backward, proj/src/attention.cpp:241-358): dq bf16
-    overwritten; dk / dv fp32 and the blank / BiasNet gradients accumulate (+=)."""
+    overwritten; dk / dv fp32 and the blank / BiasNet gradients accumulate (+=).  gather:
+    dk / dv through a per-call reverse CSR (when heads*head_dim allows), else scattered (the
+    default: at the decoder's shape the CSR build costs what the reductions save)."""
     desc, ins = _attn_structs(q, k, v, blank_k, blank_v, coords, bias, heads, head_dim)
     _req(idx, torch.int32, "idx")
     _req(valid, torch.uint8, "valid")
@@ -256,12 +258,17 @@ def gattn_bwd(q, k, v, blank_k, blank_v, coords, idx, valid, bias: BiasNet, head
         grads.dv = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
     _req(grads.dk, torch.float32, "dk")
     _req(grads.dv, torch.float32, "dv")
-    capi.check(capi.lib().affmae_gattn_bwd(
+    L = capi.lib()
+    nbytes = L.affmae_gattn_bwd_workspace(C.byref(desc), C.c_int64(B), C.c_int64(N), C.c_int64(W)) if gather else 0
+    if nbytes and (workspace is None or workspace.numel() < nbytes):
+        workspace = _workspace(nbytes, q.device)
+    ws = (C.c_void_p(workspace.data_ptr()), C.c_size_t(workspace.numel())) if nbytes else (None, C.c_size_t(0))
+    capi.check(L.affmae_gattn_bwd(
         C.byref(desc), C.byref(ins), C.c_void_p(idx.data_ptr()), C.c_void_p(valid.data_ptr()), C.c_int64(B),
         C.c_int64(N), C.c_int64(W), C.c_void_p(dout.data_ptr()),
         *[C.c_void_p(getattr(grads, n).data_ptr()) for n in (
             "dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")],
-        _stream(stream)), "gattn_bwd")
+        *ws, _stream(stream)), "gattn_bwd")
     return grads
 
 
@@ -354,11 +361,11 @@ def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, stream=None)
 
 
 def interp_bwd(queries, key_coords, feats, idx, valid, p, dout, eps=1e-6, dfeats=None, dp=None, dqueries=None,
-               stream=None, gather=False, workspace=None):
+               stream=None, gather=True, workspace=None):
     """make_interp_op backward (proj/src/interpolation.cpp:224-251): accumulates into
     dfeats [B, N, D] fp32, dp [1] fp32 and dqueries [B, Q, 2] fp32 (zeros if not given).
-    gather=True: dfeats through a per-call reverse CSR (affmae_interp_bwd_gather) instead of
-    scattered fp32 reductions."""
+    gather=True (default): dfeats through a per-call reverse CSR (affmae_interp_bwd_gather);
+    gather=False: scattered fp32 reductions (affmae_interp_bwd, no workspace)."""
     _req(dout, torch.bfloat16, "dout")
     B, Q, _ = queries.shape
     N, D = feats.shape[1], feats.shape[2]

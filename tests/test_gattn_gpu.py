@@ -53,7 +53,7 @@ def _problem(case):
     return pb
 
 
-def _run(pb):
+def _run(pb, gather=True):
     import torch
     from paper_2602_16249_b200 import ops
     dev = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device="cuda").contiguous()
@@ -63,7 +63,7 @@ def _run(pb):
     idx, valid = dev(pb["idx"], torch.int32), dev(pb["valid"], torch.uint8)
     bias = ops.BiasNet.from_numpy(pb["bias"])
     out, lse = ops.gattn_fwd(q, k, v, bk, bv, c, idx, valid, bias, pb["heads"], pb["head_dim"])
-    g = ops.gattn_bwd(q, k, v, bk, bv, c, idx, valid, bias, pb["heads"], pb["head_dim"], do)
+    g = ops.gattn_bwd(q, k, v, bk, bv, c, idx, valid, bias, pb["heads"], pb["head_dim"], do, gather=gather)
     torch.cuda.synchronize()
     f = lambda t: t.float().cpu().numpy()
     return f(out), f(lse), {n: f(getattr(g, n)) for n in (
@@ -89,10 +89,11 @@ def _oracle(pb):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("gather", [True, False], ids=["gather", "scatter"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_gattn_matches_oracle(case):
+def test_gattn_matches_oracle(case, gather):
     pb = _problem(case)
-    out, lse, got = _run(pb)
+    out, lse, got = _run(pb, gather)
     want_out, want = _oracle(pb)
     assert np.isfinite(out).all() and np.isfinite(lse).all()
     assert rel_l2(out.reshape(want_out.shape), want_out) <= REL_TOL
