@@ -173,7 +173,7 @@ __device__ __forceinline__ float greduce_scatter32(float (&v)[32], int lane) {
 // Per tile (32 tokens of one head) the warp's blank-k / blank-v gradients (2*HD sums) and,
 // for hidden <= 8, the 4*hidden BiasNet sums are reduce-scattered so lane l keeps sum l.
 template <int HD, int MW>
-__global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfloat16* __restrict__ dout,
+__global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_kernel(GAttnP p, const __nv_bfloat16* __restrict__ dout,
                                                         __nv_bfloat16* __restrict__ dq, float* __restrict__ dk,
                                                         float* __restrict__ dv, float* __restrict__ dbk,
                                                         float* __restrict__ dbv, float* __restrict__ dw1,
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfl
         gload_row<HD>(p.q + row * ld + h * HD, qf, 1.f);
         gload_row<HD>(dout + row * ld + h * HD, gf, 1.f);
         const float2 qx = xy[row];
-        float w[MW], dS[MW], ox[MW], oy[MW];
+        float w[MW], dS[MW];
         int key[MW];  // image-local key token, -1 if none
         const int32_t* ir = p.idx + row * p.m;
         const uint8_t* vv = p.valid + row * p.m;
@@ -211,13 +211,11 @@ __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfl
         for (int j = 0; j < MW; ++j) {
             w[j] = -INFINITY;
             key[j] = -1;
-            ox[j] = oy[j] = 0.f;
             if (act && j < p.m && vv[j]) {
                 key[j] = ir[j];
                 const float2 kx = xy[b0 + key[j]];
-                ox[j] = (kx.x - qx.x) * p.inv_patch;
-                oy[j] = (kx.y - qx.y) * p.inv_patch;
-                w[j] = p.scale * gdot<HD>(qf, p.k + (b0 + key[j]) * ld + h * HD) + gbias(un, H, b2, ox[j], oy[j]);
+                w[j] = p.scale * gdot<HD>(qf, p.k + (b0 + key[j]) * ld + h * HD) +
+                       gbias(un, H, b2, (kx.x - qx.x) * p.inv_patch, (kx.y - qx.y) * p.inv_patch);
                 mx = fmaxf(mx, w[j]);
             }
         }
@@ -306,10 +304,12 @@ __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfl
 #pragma unroll
                     for (int j = 0; j < MW; ++j) {
                         if (key[j] < 0) continue;
-                        const float th = tanh_fast(fmaf(wu.x, ox[j], fmaf(wu.y, oy[j], wu.z)));
+                        const float2 kx = xy[b0 + key[j]];
+                        const float ox = (kx.x - qx.x) * p.inv_patch, oy = (kx.y - qx.y) * p.inv_patch;
+                        const float th = tanh_fast(fmaf(wu.x, ox, fmaf(wu.y, oy, wu.z)));
                         const float dpre = dS[j] * wu.w * (1.f - th * th);
-                        gx = fmaf(dpre, ox[j], gx);
-                        gy = fmaf(dpre, oy[j], gy);
+                        gx = fmaf(dpre, ox, gx);
+                        gy = fmaf(dpre, oy, gy);
                         gb += dpre;
                         gw = fmaf(dS[j], th, gw);
                     }
@@ -327,10 +327,12 @@ __global__ void __launch_bounds__(256) gattn_bwd_kernel(GAttnP p, const __nv_bfl
 #pragma unroll
                 for (int j = 0; j < MW; ++j) {
                     if (key[j] < 0) continue;
-                    const float th = tanh_fast(fmaf(wu.x, ox[j], fmaf(wu.y, oy[j], wu.z)));
+                    const float2 kx = xy[b0 + key[j]];
+                    const float ox = (kx.x - qx.x) * p.inv_patch, oy = (kx.y - qx.y) * p.inv_patch;
+                    const float th = tanh_fast(fmaf(wu.x, ox, fmaf(wu.y, oy, wu.z)));
                     const float dpre = dS[j] * wu.w * (1.f - th * th);
-                    gx = fmaf(dpre, ox[j], gx);
-                    gy = fmaf(dpre, oy[j], gy);
+                    gx = fmaf(dpre, ox, gx);
+                    gy = fmaf(dpre, oy, gy);
                     gb += dpre;
                     gw = fmaf(dS[j], th, gw);
                 }
