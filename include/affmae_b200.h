@@ -304,6 +304,24 @@ int affmae_gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, co
 size_t affmae_gattn_bwd_workspace(const affmae_attn_desc* a, int64_t batch, int64_t tokens, int64_t width);
 
 /* ------------------------------------------------------------------------
+ * Inputs on the device.
+ * ---------------------------------------------------------------------- */
+/* Replaces perlin_field + mask_from_field (include/affmae/masking.hpp; src/masking.cpp:34-92),
+ * batched: seeds_host [B] (HOST array, the per-image MaskSpec seeds), grid h x w, octaves /
+ * base_freq / persistence as perlin_field, ratio as mask_from_field -> masked [B, h, w] uint8
+ * (1 = hidden), exactly llround(ratio*h*w) per image, largest field first, ties to the lower
+ * cell.  Bit-exact with the reference (the corner gradients are computed on the host). */
+size_t affmae_perlin_mask_workspace(int64_t batch, int64_t h, int64_t w, int octaves, double base_freq);
+int affmae_perlin_mask(const uint64_t* seeds_host, int64_t batch, int64_t h, int64_t w, int octaves,
+                       double base_freq, double persistence, double ratio, uint8_t* masked,
+                       void* workspace, size_t workspace_bytes, void* stream);
+/* Stage-0 coordinates of the visible cells in ascending cell index (src/geometry.cpp:44-50,
+ * src/pipeline.cpp:412-427): coords [B, nvis, 2] float32 pixel centres c*patch + patch/2;
+ * count [B] (optional) receives each image's visible count; rows beyond nvis are dropped. */
+int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch,
+                          int64_t nvis, float* coords, int32_t* count, void* stream);
+
+/* ------------------------------------------------------------------------
  * Adaptive KNN merge (src/merging.cpp).
  * ---------------------------------------------------------------------- */
 

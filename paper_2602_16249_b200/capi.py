@@ -32,7 +32,8 @@ EXPORTS = (
     "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_linear_fwd_gelu_aux", "affmae_gelu_bwd", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",
     "affmae_layernorm_bwd", "affmae_norm_clamp_fwd", "affmae_norm_clamp_bwd", "affmae_masked_mse_workspace",
     "affmae_masked_mse", "affmae_gattn_fwd", "affmae_gattn_bwd", "affmae_gattn_bwd_workspace",
-    "affmae_interp_bwd_gather_workspace", "affmae_interp_bwd_gather",
+    "affmae_interp_bwd_gather_workspace", "affmae_interp_bwd_gather", "affmae_perlin_mask_workspace",
+    "affmae_perlin_mask", "affmae_visible_coords",
 )
 
 
@@ -100,7 +101,8 @@ def lib():
                   "affmae_attn_fwd_planned_workspace", "affmae_attn_bwd_planned_workspace",
                   "affmae_attn_bwd_workspace", "affmae_select_retained_workspace",
                   "affmae_merge_plan_workspace", "affmae_merge_pool_bwd_workspace",
-                  "affmae_interp_bwd_gather_workspace", "affmae_gattn_bwd_workspace"):
+                  "affmae_interp_bwd_gather_workspace", "affmae_gattn_bwd_workspace",
+                  "affmae_perlin_mask_workspace"):
             if hasattr(L, f):
                 getattr(L, f).restype = C.c_size_t
         _lib = L

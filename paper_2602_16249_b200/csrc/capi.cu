@@ -63,6 +63,10 @@ size_t interp_bwd_gather_workspace(int64_t, int64_t, int64_t, int64_t);
 int interp_bwd_gather(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t,
                       int64_t, int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*,
                       size_t, void*);
+size_t perlin_mask_workspace(int64_t, int64_t, int64_t, int, double);
+int perlin_mask(const uint64_t*, int64_t, int64_t, int64_t, int, double, double, double, uint8_t*, void*, size_t,
+                void*);
+int visible_coords(const uint8_t*, int64_t, int64_t, int64_t, double, int64_t, float*, int32_t*, void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
@@ -225,6 +229,21 @@ int affmae_interp_bwd_gather(const float* queries, const float* key_coords, cons
                              size_t workspace_bytes, void* stream) {
     return interp_bwd_gather(queries, key_coords, feats, idx, valid, batch, n_queries, n_keys, dim, k, p, eps, dout,
                              dfeats, dp, dqueries, workspace, workspace_bytes, stream);
+}
+
+// device-side inputs (src/masking.cpp:34-92, src/geometry.cpp:44-50)
+size_t affmae_perlin_mask_workspace(int64_t batch, int64_t h, int64_t w, int octaves, double base_freq) {
+    return perlin_mask_workspace(batch, h, w, octaves, base_freq);
+}
+int affmae_perlin_mask(const uint64_t* seeds_host, int64_t batch, int64_t h, int64_t w, int octaves,
+                       double base_freq, double persistence, double ratio, uint8_t* masked, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+    return perlin_mask(seeds_host, batch, h, w, octaves, base_freq, persistence, ratio, masked, workspace,
+                       workspace_bytes, stream);
+}
+int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch, int64_t nvis,
+                          float* coords, int32_t* count, void* stream) {
+    return visible_coords(masked, batch, h, w, patch, nvis, coords, count, stream);
 }
 
 // decoder attention over general neighbour rows (src/pipeline.cpp:495-535)

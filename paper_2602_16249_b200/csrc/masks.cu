@@ -1,0 +1,288 @@
+// Device-side Perlin patch masks and stage-0 coordinates:
+// perlin_field + mask_from_field (proj/src/masking.cpp:34-92) and the visible
+// patch-centre lattice (proj/src/geometry.cpp:44-50, proj/src/pipeline.cpp:412-427),
+// batched over images so a training step needs no host-side mask work.
+//
+// Bit-exact with the reference: the corner gradients need cos / sin of the hashed
+// angle, whose correctly rounded host values (glibc) the device libm does not
+// guarantee, so the host computes the few gradients a grid touches ((freq+1)^2 per
+// octave) and the device evaluates the field with explicitly rounded binary64 ops
+// (__dmul_rn / __dadd_rn: no FMA contraction), in the reference's operation order.
+// Selection: exactly round(ratio * cells) cells, largest field value first, ties to
+// the lower cell index -- a per-image 8-pass radix select over the order-preserving
+// 64-bit image of the doubles, then the equal-to-threshold cells ranked by index
+// with a block scan.  One 1024-thread block per image.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace affmae_b200 {
+
+constexpr int kMaskThreads = 1024;
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ double fade_rn(double t) {
+    // t * t * t * (t * (t * 6.0 - 15.0) + 10.0), left to right
+    const double t3 = dm(dm(t, t), t);
+    return dm(t3, da(dm(t, ds(dm(t, 6.0), 15.0)), 10.0));
+}
+__device__ __forceinline__ double lerp_rn(double a, double b, double t) { return da(a, dm(ds(b, a), t)); }
+
+// grads: per image, per octave, (side x side) corners {gx, gy}, side = freq + 1 (+1 spare)
+struct PerlinGeo {
+    int64_t h, w;
+    int octaves;
+    double base_freq;
+    int64_t corners;  // per image, all octaves
+};
+
+__global__ void perlin_field_kernel(const double2* __restrict__ grads, const int64_t* __restrict__ oct_off,
+                                    const int32_t* __restrict__ oct_side, const double* __restrict__ amp,
+                                    PerlinGeo g, int64_t batch, double* __restrict__ field) {
+    const int64_t cells = g.h * g.w, n = batch * cells;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = t / cells, c = t - b * cells, i = c / g.w, j = c - i * g.w;
+        const double2* gb = grads + b * g.corners;
+        double acc = 0.0;
+        for (int o = 0; o < g.octaves; ++o) {
+            const double freq = g.base_freq * double(1 << o);
+            const double py = __ddiv_rn(dm(double(i), freq), double(g.h));
+            const double px = __ddiv_rn(dm(double(j), freq), double(g.w));
+            const double fx0 = floor(px), fy0 = floor(py);
+            const int x0 = int(fx0), y0 = int(fy0), side = oct_side[o];
+            const double tx = ds(px, fx0), ty = ds(py, fy0);
+            const double2* go = gb + oct_off[o];
+            const double2 g00 = go[y0 * side + x0], g10 = go[y0 * side + x0 + 1];
+            const double2 g01 = go[(y0 + 1) * side + x0], g11 = go[(y0 + 1) * side + x0 + 1];
+            const double n00 = da(dm(g00.x, tx), dm(g00.y, ty));
+            const double n10 = da(dm(g10.x, ds(tx, 1.0)), dm(g10.y, ty));
+            const double n01 = da(dm(g01.x, tx), dm(g01.y, ds(ty, 1.0)));
+            const double n11 = da(dm(g11.x, ds(tx, 1.0)), dm(g11.y, ds(ty, 1.0)));
+            const double u = fade_rn(tx), v = fade_rn(ty);
+            const double val = lerp_rn(lerp_rn(n00, n10, u), lerp_rn(n01, n11, u), v);
+            acc = da(acc, dm(amp[o], val));
+        }
+        field[t] = acc;
+    }
+}
+
+// order-preserving image of a double, complemented so that larger values get smaller keys
+__device__ __forceinline__ uint64_t desc_key(double v) {
+    uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
+    u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+    return ~u;
+}
+
+__global__ void __launch_bounds__(kMaskThreads) mask_select_kernel(const double* __restrict__ field, int64_t cells,
+                                                                   int64_t want, uint8_t* __restrict__ masked) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t s_prefix;
+    __shared__ int64_t s_rank;
+    __shared__ int32_t wsum[32];
+    const double* f = field + int64_t(blockIdx.x) * cells;
+    uint8_t* m = masked + int64_t(blockIdx.x) * cells;
+    if (threadIdx.x == 0) {
+        s_prefix = 0;
+        s_rank = want;  // 1-based rank of the threshold among the keys matching the prefix
+    }
+    __syncthreads();
+    if (want <= 0) {
+        for (int64_t i = threadIdx.x; i < cells; i += kMaskThreads) m[i] = 0;
+        return;
+    }
+    // radix select (ascending keys = descending values) of the want-th smallest key
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        const uint64_t hi_mask = pass == 0 ? 0ull : (~0ull << (64 - 8 * pass));
+        for (int i = threadIdx.x; i < 256; i += kMaskThreads) hist[i] = 0;
+        __syncthreads();
+        const uint64_t pre = s_prefix;
+        for (int64_t i = threadIdx.x; i < cells; i += kMaskThreads) {
+            const uint64_t k = desc_key(f[i]);
+            if ((k & hi_mask) == pre) atomicAdd(&hist[(k >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t r = s_rank;
+            int d = 0;
+            for (; d < 256; ++d) {
+                if (r <= int64_t(hist[d])) break;
+                r -= hist[d];
+            }
+            s_prefix = pre | (uint64_t(d) << shift);
+            s_rank = r;
+        }
+        __syncthreads();
+    }
+    const uint64_t T = s_prefix;
+    const int64_t take_eq = s_rank;  // equal-to-T cells to take, lowest index first
+    // rank the equal cells by index: contiguous chunks per thread + block scan
+    const int64_t per = (cells + kMaskThreads - 1) / kMaskThreads;
+    const int64_t lo = threadIdx.x * per, hi = lo + per < cells ? lo + per : cells;
+    int32_t eq = 0;
+    for (int64_t i = lo; i < hi; ++i) eq += desc_key(f[i]) == T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t inc = eq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += v;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    int64_t before = inc - eq + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int64_t i = lo; i < hi; ++i) {
+        const uint64_t k = desc_key(f[i]);
+        uint8_t out = k < T;
+        if (k == T) out = before++ < take_eq;
+        m[i] = out;
+    }
+}
+
+// visible cells' pixel centres in ascending cell index: per-image block scan
+__global__ void __launch_bounds__(kMaskThreads) visible_coords_kernel(const uint8_t* __restrict__ masked, int64_t h,
+                                                                      int64_t w, double patch, int64_t nvis,
+                                                                      float2* __restrict__ coords,
+                                                                      int32_t* __restrict__ count) {
+    __shared__ int32_t wsum[32];
+    const int64_t cells = h * w;
+    const uint8_t* m = masked + int64_t(blockIdx.x) * cells;
+    float2* out = coords + int64_t(blockIdx.x) * nvis;
+    const int64_t per = (cells + kMaskThreads - 1) / kMaskThreads;
+    const int64_t lo = threadIdx.x * per, hi = lo + per < cells ? lo + per : cells;
+    int32_t vis = 0;
+    for (int64_t i = lo; i < hi; ++i) vis += m[i] == 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t inc = vis;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += v;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    int64_t pos = inc - vis + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int64_t i = lo; i < hi; ++i)
+        if (m[i] == 0) {
+            if (pos < nvis) {
+                const int64_t r = i / w, c = i - r * w;
+                out[pos] = make_float2(float(double(c) * patch + patch * 0.5), float(double(r) * patch + patch * 0.5));
+            }
+            ++pos;
+        }
+    if (threadIdx.x == kMaskThreads - 1 && count) count[blockIdx.x] = wsum[31];
+}
+
+static uint64_t mix64_h(uint64_t z) {  // proj/include/affmae/rng.hpp:8-13
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+size_t perlin_mask_workspace(int64_t batch, int64_t h, int64_t w, int octaves, double base_freq) {
+    int64_t corners = 0;
+    for (int o = 0; o < octaves; ++o) {
+        const int64_t side = int64_t(std::ceil(base_freq * double(1 << o))) + 2;
+        corners += side * side;
+    }
+    return size_t(batch * h * w) * 8 + size_t(batch * corners) * 16 + size_t(octaves) * 32 + 1024;
+}
+
+int perlin_mask(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int octaves, double base_freq,
+                double persistence, double ratio, uint8_t* masked, void* workspace, size_t ws_bytes, void* stream) {
+    if (!seeds || !masked) return fail(AFFMAE_ECONFIG, "perlin_mask: null pointer");
+    if (h < 2 || w < 2) return fail(AFFMAE_ECONFIG, "perlin_field: grid must be at least 2x2");
+    if (octaves < 1 || octaves > 16) return fail(AFFMAE_ECONFIG, "perlin_field: octaves must be in [1, 16]");
+    if (!(ratio >= 0.0 && ratio <= 1.0)) return fail(AFFMAE_ECONFIG, "mask_from_field: ratio must be in [0, 1]");
+    if (!(base_freq > 0.0)) return fail(AFFMAE_ECONFIG, "perlin_field: base_freq must be positive");
+    if (batch < 0) return fail(AFFMAE_ECONFIG, "perlin_mask: bad batch");
+    if (!workspace || ws_bytes < perlin_mask_workspace(batch, h, w, octaves, base_freq))
+        return fail(AFFMAE_ECONFIG, "perlin_mask: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    // host: the corner gradients a grid touches (proj/src/masking.cpp:21-26, 51-69)
+    const size_t no = static_cast<size_t>(octaves);
+    std::vector<int64_t> off(no);
+    std::vector<int32_t> side(no);
+    std::vector<double> amp(no);
+    int64_t corners = 0;
+    for (int o = 0; o < octaves; ++o) {
+        side[size_t(o)] = int32_t(std::ceil(base_freq * double(1 << o))) + 2;
+        off[size_t(o)] = corners;
+        corners += int64_t(side[size_t(o)]) * side[size_t(o)];
+        amp[size_t(o)] = std::pow(persistence, o);
+    }
+    std::vector<double> grads(size_t(batch * corners) * 2);
+    for (int64_t b = 0; b < batch; ++b)
+        for (int o = 0; o < octaves; ++o) {
+            const uint64_t os = mix64_h(seeds[b] + 0x9E3779B97F4A7C15ull * uint64_t(o + 1));
+            const int s = side[size_t(o)];
+            for (int iy = 0; iy < s; ++iy)
+                for (int ix = 0; ix < s; ++ix) {
+                    const uint64_t k = mix64_h(mix64_h(uint64_t(ix) * 0x9E3779B97F4A7C15ull ^ uint64_t(iy)) ^ os);
+                    const double ang = double(k >> 11) * 0x1.0p-53 * 6.283185307179586476925287;
+                    const size_t e = size_t(b * corners + off[size_t(o)] + iy * s + ix) * 2;
+                    grads[e] = std::cos(ang);
+                    grads[e + 1] = std::sin(ang);
+                }
+        }
+    char* ws = static_cast<char*>(workspace);
+    double* field = reinterpret_cast<double*>(ws);
+    double2* dgr = reinterpret_cast<double2*>(ws + size_t(batch * h * w) * 8);
+    char* meta = reinterpret_cast<char*>(dgr + batch * corners);
+    int64_t* doff = reinterpret_cast<int64_t*>(meta);
+    double* damp = reinterpret_cast<double*>(doff + octaves);
+    int32_t* dside = reinterpret_cast<int32_t*>(damp + octaves);
+    // pageable copies are staged by the driver before returning: the host vectors may die
+    if (cudaMemcpyAsync(dgr, grads.data(), grads.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(doff, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(damp, amp.data(), amp.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(dside, side.data(), side.size() * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return fail(AFFMAE_ECUDA, "perlin_mask: H2D of the gradient table failed");
+    PerlinGeo g{h, w, octaves, base_freq, corners};
+    const int64_t n = batch * h * w;
+    perlin_field_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 16 * kNumSMs)), 256, 0, st>>>(
+        dgr, doff, dside, damp, g, batch, field);
+    const int64_t want = std::llround(ratio * double(h * w));
+    mask_select_kernel<<<unsigned(batch), kMaskThreads, 0, st>>>(field, h * w, want, masked);
+    AFFMAE_LAUNCH_CHECK("perlin_mask");
+    return AFFMAE_OK;
+}
+
+int visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch, int64_t nvis,
+                   float* coords, int32_t* count, void* stream) {
+    if (!masked || !coords) return fail(AFFMAE_ECONFIG, "visible_coords: null pointer");
+    if (batch < 0 || h < 1 || w < 1 || nvis < 0) return fail(AFFMAE_ECONFIG, "visible_coords: bad shape");
+    if (batch == 0) return AFFMAE_OK;
+    visible_coords_kernel<<<unsigned(batch), kMaskThreads, 0, as_stream(stream)>>>(
+        masked, h, w, patch, nvis, reinterpret_cast<float2*>(coords), count);
+    AFFMAE_LAUNCH_CHECK("visible_coords_kernel");
+    return AFFMAE_OK;
+}
+
+}  // namespace affmae_b200

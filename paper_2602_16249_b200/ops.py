@@ -337,6 +337,40 @@ def knn(queries, keys, k, stream=None):
     return idx, valid
 
 
+# ------------------------------------------------------------ device inputs
+def perlin_masks(seeds, grid, ratio, octaves=2, base_freq=4.0, persistence=0.5, device="cuda", stream=None):
+    """perlin_field + mask_from_field (proj/src/masking.cpp:34-92) for len(seeds) images on the
+    device: -> masked [B, grid, grid] uint8 (1 = hidden), bit-exact with the reference."""
+    B = len(seeds)
+    sd = (C.c_uint64 * max(B, 1))(*[int(s) for s in seeds])
+    L = capi.lib()
+    nbytes = L.affmae_perlin_mask_workspace(C.c_int64(B), C.c_int64(grid), C.c_int64(grid), C.c_int(octaves),
+                                            C.c_double(base_freq))
+    ws = _workspace(nbytes, device)
+    masked = torch.empty((B, grid, grid), dtype=torch.uint8, device=device)
+    capi.check(L.affmae_perlin_mask(sd, C.c_int64(B), C.c_int64(grid), C.c_int64(grid), C.c_int(octaves),
+                                    C.c_double(base_freq), C.c_double(persistence), C.c_double(ratio),
+                                    C.c_void_p(masked.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                    C.c_size_t(ws.numel()), _stream(stream)), "perlin_mask")
+    return masked
+
+
+def visible_coords(masked, patch=8, nvis=None, stream=None):
+    """Visible patch centres in ascending cell index (proj/src/geometry.cpp:44-50):
+    masked [B, h, w] uint8 -> (coords [B, nvis, 2] fp32, count [B] int32)."""
+    _req(masked, torch.uint8, "masked")
+    B, h, w = masked.shape
+    if nvis is None:
+        nvis = h * w - int(masked[0].sum().item())
+    coords = torch.empty((B, nvis, 2), dtype=torch.float32, device=masked.device)
+    count = torch.empty(B, dtype=torch.int32, device=masked.device)
+    capi.check(capi.lib().affmae_visible_coords(C.c_void_p(masked.data_ptr()), C.c_int64(B), C.c_int64(h),
+                                                C.c_int64(w), C.c_double(patch), C.c_int64(nvis),
+                                                C.c_void_p(coords.data_ptr()), C.c_void_p(count.data_ptr()),
+                                                _stream(stream)), "visible_coords")
+    return coords, count
+
+
 # ------------------------------------------------------------ interpolation
 def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, stream=None):
     """make_interp_op forward (proj/src/interpolation.cpp:192-222), batched:

@@ -1,0 +1,52 @@
+"""Device-side Perlin masks and stage-0 coordinates (perlin_field +
+mask_from_field, proj/src/masking.cpp:34-92; the visible lattice, proj/src/geometry.cpp:44-50)
+against the reference's golden mask and the numpy restatement pinned to it
+(tests/test_inputs.py): bit-exact masks and coordinates."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2602_16249_b200 import inputs
+
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+
+
+@pytest.mark.gpu
+def test_device_mask_matches_reference_golden():
+    from paper_2602_16249_b200 import ops
+    m = ops.perlin_masks([3], 64, 0.75)
+    np.testing.assert_array_equal(m[0].cpu().numpy(), G["perlin64_r075_s3"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid,ratio,seed0,batch", [(256, 0.75, 1000, 4), (128, 0.5, 7, 3), (37, 0.4, 123, 2),
+                                                    (64, 0.0, 1, 1), (64, 1.0, 2, 1), (2, 0.5, 9, 2)])
+def test_device_masks_bit_exact(grid, ratio, seed0, batch):
+    from paper_2602_16249_b200 import ops
+    seeds = [seed0 + b for b in range(batch)]
+    m = ops.perlin_masks(seeds, grid, ratio).cpu().numpy()
+    for b, s in enumerate(seeds):
+        want = inputs.perlin_mask(grid, ratio, s).astype(np.uint8)
+        np.testing.assert_array_equal(m[b], want)
+        assert m[b].sum() == int(np.floor(ratio * grid * grid + 0.5))
+
+
+@pytest.mark.gpu
+def test_device_visible_coords_match_lattice_batch():
+    from paper_2602_16249_b200 import ops
+    seeds = [1000 + b for b in range(5)]
+    m = ops.perlin_masks(seeds, 256, 0.75)
+    coords, count = ops.visible_coords(m, patch=8)
+    want = inputs.lattice_batch(5, 256, 0.75, 8, seed0=1000)
+    np.testing.assert_array_equal(coords.cpu().numpy(), want)
+    assert (count.cpu().numpy() == want.shape[1]).all()
+
+
+@pytest.mark.gpu
+def test_device_mask_rejects_bad_args():
+    from paper_2602_16249_b200 import ops
+    with pytest.raises(ValueError, match="ratio"):
+        ops.perlin_masks([1], 64, 1.5)
+    with pytest.raises(ValueError, match="2x2"):
+        ops.perlin_masks([1], 1, 0.5)
