@@ -430,10 +430,11 @@ def run_ours(a, rank, world, dist):
     adamw = run_adamw(dev) if a.interp_images > 0 else None
     linear = run_linear(dev) if a.interp_images > 0 else None
     gattn = run_gattn(a, host, dev) if a.interp_images > 0 else None
+    masks = run_masks(a, dev) if a.interp_images > 0 else None
 
     res = dict(value=value, ms=ms_max, phase_ms={p: float(np.median(v)) for p, v in phase_ms.items()},
                clocks=clocks.summary(), e2e=e2e, N=N, B=B, launches=launches,
-               graph=graph is not None, interp=interp, adamw=adamw, linear=linear, gattn=gattn)
+               graph=graph is not None, interp=interp, adamw=adamw, linear=linear, gattn=gattn, masks=masks)
     return res
 
 
@@ -564,6 +565,32 @@ def run_gattn(a, host, dev, k=8, heads=4, head_dim=16, hidden=8, reps=10):
             "bwd_tokens_per_s": nt / (bwd_ms * 1e-3), "fwd_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9,
             "bwd_gbs": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
             "note": "side measurement of SURVEY §8(f) #2, not part of the step or its value"}
+
+
+def run_masks(a, dev, reps=10):
+    """Side measurement: the step's Perlin masks and stage-0 coordinates built
+    on the device for all `batch` images (host gradient table + field + exact-count select +
+    lattice compaction), against the host numpy restatement's time for the same masks."""
+    import torch
+    from paper_2602_16249_b200 import inputs, ops
+    seeds = [1000 + b for b in range(a.batch)]
+    for _ in range(2):
+        m = ops.perlin_masks(seeds, a.grid, 0.75, device=dev)
+        ops.visible_coords(m, nvis=a.grid * a.grid - int(round(0.75 * a.grid * a.grid)))
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(reps):
+        m = ops.perlin_masks(seeds, a.grid, 0.75, device=dev)
+        ops.visible_coords(m, nvis=a.grid * a.grid - int(round(0.75 * a.grid * a.grid)))
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / reps
+    t0 = time.perf_counter()
+    inputs.lattice_batch(4, a.grid, 0.75, 8, seed0=1000)
+    host_ms = (time.perf_counter() - t0) * 1e3 * a.batch / 4
+    return {"images": a.batch, "grid": a.grid, "ms": ms, "host_numpy_ms": host_ms,
+            "note": "side measurement of SURVEY §8(f) #4 (includes the per-call workspace allocation), not part of the step"}
 
 
 def run_linear(dev, reps=20):
@@ -965,6 +992,8 @@ def main():
             line["next_ops"]["linear"] = res["linear"]
         if res.get("gattn"):
             line["next_ops"]["decoder_attn"] = res["gattn"]
+        if res.get("masks"):
+            line["next_ops"]["masks"] = res["masks"]
     if not a.no_cpu_baseline and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(a)
