@@ -321,6 +321,24 @@ int affmae_perlin_mask(const uint64_t* seeds_host, int64_t batch, int64_t h, int
 int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch,
                           int64_t nvis, float* coords, int32_t* count, void* stream);
 
+/* AFT1 tensor files (write_aft / read_aft, src/tensor_io.cpp:60-105; format
+ * include/affmae/tensor_io.hpp:11-13) from / into DEVICE buffers.  write: dev_src holds fp32
+ * values (dtype 0 = b32, 1 = b16emu) or bytes (dtype 2); the file is byte-identical to the
+ * reference's for the same values.  read: fp32 values (u8 payloads as byte values) into
+ * dev_dst[capacity]; *numel_out (optional) gets the element count.  Both synchronise `stream`. */
+int affmae_aft_write(const char* path, const void* dev_src, const int64_t* dims, int ndim, int dtype,
+                     void* stream);
+int affmae_aft_read_header(const char* path, int* dtype, int* ndim, int64_t* dims /* [8] */);
+int affmae_aft_read(const char* path, float* dev_dst, int64_t capacity, int64_t* numel_out, void* stream);
+/* save_checkpoint / load_checkpoint (src/pipeline.cpp:757-797) over device fp32 parameter
+ * buffers: <dir>/<name>.aft per parameter + manifest.tsv ("name\td0xd1\tprec\tfile"), prec
+ * codes 0 b32 / 1 b16emu / 2 b64 (stored as b32).  load: unknown, missing or mis-sized
+ * parameters are ConfigErrors, as in the reference. */
+int affmae_checkpoint_save(const char* dir, int n, const char* const* names, const float* const* dev_vals,
+                           const int64_t* const* dims, const int* ndims, const int* precs, void* stream);
+int affmae_checkpoint_load(const char* dir, int n, const char* const* names, float* const* dev_vals,
+                           const int64_t* numels, void* stream);
+
 /* ------------------------------------------------------------------------
  * Adaptive KNN merge (src/merging.cpp).
  * ---------------------------------------------------------------------- */

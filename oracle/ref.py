@@ -247,6 +247,27 @@ def adamw(shapes, values, grads, lr=1e-3, warmup=100, wd=0.05, beta1=0.883, beta
     return vals
 
 
+def write_aft(path, vals, prec=0):
+    """write_aft (proj/src/tensor_io.cpp:60-66) of a tensor of precision `prec` (0 b32, 1 b16emu)."""
+    vals = _f64(vals)
+    dims = np.asarray(vals.shape, np.int64)
+    _check(lib().ref_write_aft(path.encode(), _p(vals), _p(dims), C.c_int(vals.ndim), C.c_int(prec)))
+
+
+def write_aft_u8(path, data):
+    data = np.ascontiguousarray(data, np.uint8)
+    dims = np.asarray(data.shape, np.int64)
+    _check(lib().ref_write_aft_u8(path.encode(), _p(data), _p(dims), C.c_int(data.ndim)))
+
+
+def read_aft(path, cap=1 << 24):
+    """read_aft (proj/src/tensor_io.cpp:78-105): (flat float64 values, on-disk dtype code)."""
+    out = np.empty(cap)
+    n, dt = C.c_int64(), C.c_int()
+    _check(lib().ref_read_aft(path.encode(), _p(out), C.c_int64(cap), C.byref(n), C.byref(dt)))
+    return out[:n.value].copy(), dt.value
+
+
 def perlin_mask(grid, ratio, seed):
     m = np.empty(grid * grid, np.uint8)
     _check(lib().ref_perlin_mask(C.c_int64(grid), C.c_double(ratio), C.c_uint64(seed), _p(m)))

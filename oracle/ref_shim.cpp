@@ -14,6 +14,7 @@
 //   ref_merge_plan           -> merge_plan                   (merging.cpp:71-116)
 //   ref_merge_pool_fwd/bwd   -> make_merge_pool_op forward/backward (merging.cpp:151-220)
 //   ref_perlin_mask          -> perlin_field + mask_from_field (proj/src/masking.cpp:51-92)
+//   ref_write_aft / _u8, ref_read_aft -> write_aft / write_aft_u8 / read_aft (proj/src/tensor_io.cpp:60-105)
 //   ref_hotpath_batch        -> the whole hot path over B images on T std::threads
 //                               (the multi-core CPU baseline of BASELINE.md §4)
 //
@@ -36,6 +37,7 @@
 #include "affmae/pipeline.hpp"
 #include "affmae/tape.hpp"
 #include "affmae/tensor.hpp"
+#include "affmae/tensor_io.hpp"
 
 using namespace affmae;
 
@@ -397,6 +399,34 @@ int ref_adamw(double lr, int64_t warmup, double wd, double beta1, double beta2, 
             for (int64_t e = 0; e < q.value.numel(); ++e) values[o + e] = q.value.get(e);
             o += q.value.numel();
         }
+    });
+}
+
+int ref_write_aft(const char* path, const double* vals, const int64_t* dims, int ndim, int prec) {
+    return guarded([&] {
+        Tensor t = Tensor::zeros(std::vector<int64_t>(dims, dims + ndim), Precision(prec));
+        for (int64_t i = 0; i < t.numel(); ++i) t.set(i, vals[i]);
+        write_aft(path, t);
+    });
+}
+
+int ref_write_aft_u8(const char* path, const uint8_t* bytes, const int64_t* dims, int ndim) {
+    return guarded([&] {
+        std::vector<int64_t> d(dims, dims + ndim);
+        int64_t n = 1;
+        for (int64_t x : d) n *= x;
+        write_aft_u8(path, d, std::vector<uint8_t>(bytes, bytes + n));
+    });
+}
+
+int ref_read_aft(const char* path, double* out, int64_t cap, int64_t* numel, int* dtype) {
+    return guarded([&] {
+        uint8_t dt = 0;
+        Tensor t = read_aft(path, &dt);
+        if (t.numel() > cap) throw ConfigError("ref_read_aft: capacity");
+        for (int64_t i = 0; i < t.numel(); ++i) out[i] = t.get(i);
+        *numel = t.numel();
+        *dtype = dt;
     });
 }
 

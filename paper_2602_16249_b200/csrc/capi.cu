@@ -67,6 +67,12 @@ size_t perlin_mask_workspace(int64_t, int64_t, int64_t, int, double);
 int perlin_mask(const uint64_t*, int64_t, int64_t, int64_t, int, double, double, double, uint8_t*, void*, size_t,
                 void*);
 int visible_coords(const uint8_t*, int64_t, int64_t, int64_t, double, int64_t, float*, int32_t*, void*);
+int aft_write(const char*, const void*, const int64_t*, int, int, void*);
+int aft_read_header(const char*, int*, int*, int64_t*);
+int aft_read(const char*, float*, int64_t, int64_t*, void*);
+int checkpoint_save(const char*, int, const char* const*, const float* const*, const int64_t* const*, const int*,
+                    const int*, void*);
+int checkpoint_load(const char*, int, const char* const*, float* const*, const int64_t*, void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
@@ -244,6 +250,25 @@ int affmae_perlin_mask(const uint64_t* seeds_host, int64_t batch, int64_t h, int
 int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch, int64_t nvis,
                           float* coords, int32_t* count, void* stream) {
     return visible_coords(masked, batch, h, w, patch, nvis, coords, count, stream);
+}
+
+// AFT1 files and checkpoints (src/tensor_io.cpp:60-105, src/pipeline.cpp:757-797)
+int affmae_aft_write(const char* path, const void* dev_src, const int64_t* dims, int ndim, int dtype, void* stream) {
+    return aft_write(path, dev_src, dims, ndim, dtype, stream);
+}
+int affmae_aft_read_header(const char* path, int* dtype, int* ndim, int64_t* dims) {
+    return aft_read_header(path, dtype, ndim, dims);
+}
+int affmae_aft_read(const char* path, float* dev_dst, int64_t capacity, int64_t* numel_out, void* stream) {
+    return aft_read(path, dev_dst, capacity, numel_out, stream);
+}
+int affmae_checkpoint_save(const char* dir, int n, const char* const* names, const float* const* dev_vals,
+                           const int64_t* const* dims, const int* ndims, const int* precs, void* stream) {
+    return checkpoint_save(dir, n, names, dev_vals, dims, ndims, precs, stream);
+}
+int affmae_checkpoint_load(const char* dir, int n, const char* const* names, float* const* dev_vals,
+                           const int64_t* numels, void* stream) {
+    return checkpoint_load(dir, n, names, dev_vals, numels, stream);
 }
 
 // decoder attention over general neighbour rows (src/pipeline.cpp:495-535)

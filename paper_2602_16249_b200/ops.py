@@ -371,6 +371,62 @@ def visible_coords(masked, patch=8, nvis=None, stream=None):
     return coords, count
 
 
+# ------------------------------------------------------------ AFT1 files / checkpoints
+def aft_write(path, t, dtype=0, stream=None):
+    """write_aft (proj/src/tensor_io.cpp:60-66) from a device tensor: fp32 (dtype 0 b32 /
+    1 b16emu) or uint8 (dtype 2, write_aft_u8)."""
+    _req(t, torch.uint8 if dtype == 2 else torch.float32, "t")
+    dims = (C.c_int64 * max(t.dim(), 1))(*t.shape)
+    capi.check(capi.lib().affmae_aft_write(str(path).encode(), C.c_void_p(t.data_ptr()), dims, C.c_int(t.dim()),
+                                           C.c_int(dtype), _stream(stream)), "aft_write")
+
+
+def aft_read(path, device="cuda", stream=None):
+    """read_aft (proj/src/tensor_io.cpp:78-105) into a device fp32 tensor -> (tensor, dtype code)."""
+    L = capi.lib()
+    dt, nd = C.c_int(), C.c_int()
+    dims = (C.c_int64 * 8)()
+    capi.check(L.affmae_aft_read_header(str(path).encode(), C.byref(dt), C.byref(nd), dims), "aft_read")
+    shape = tuple(dims[i] for i in range(nd.value))
+    out = torch.empty(shape, dtype=torch.float32, device=device)
+    capi.check(L.affmae_aft_read(str(path).encode(), C.c_void_p(out.data_ptr()), C.c_int64(out.numel()), None,
+                                 _stream(stream)), "aft_read")
+    return out, dt.value
+
+
+_PREC = {"b32": 0, "b16emu": 1, "b64": 2}
+
+
+def save_checkpoint(directory, params, stream=None):
+    """save_checkpoint (proj/src/pipeline.cpp:757-770): params = {name: (fp32 device tensor,
+    precision name)} in ParamStore order."""
+    names = list(params)
+    n = len(names)
+    ts = [params[k][0] for k in names]
+    for t, k in zip(ts, names):
+        _req(t, torch.float32, k)
+    dim_arrs = [(C.c_int64 * max(t.dim(), 1))(*t.shape) for t in ts]
+    capi.check(capi.lib().affmae_checkpoint_save(
+        str(directory).encode(), C.c_int(n), (C.c_char_p * max(n, 1))(*[k.encode() for k in names]),
+        (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in ts]),
+        (C.POINTER(C.c_int64) * max(n, 1))(*[C.cast(d, C.POINTER(C.c_int64)) for d in dim_arrs]),
+        (C.c_int * max(n, 1))(*[t.dim() for t in ts]), (C.c_int * max(n, 1))(*[_PREC[params[k][1]] for k in names]),
+        _stream(stream)), "checkpoint_save")
+
+
+def load_checkpoint(directory, params, stream=None):
+    """load_checkpoint (proj/src/pipeline.cpp:772-797) into {name: fp32 device tensor}."""
+    names = list(params)
+    n = len(names)
+    ts = [params[k] for k in names]
+    for t, k in zip(ts, names):
+        _req(t, torch.float32, k)
+    capi.check(capi.lib().affmae_checkpoint_load(
+        str(directory).encode(), C.c_int(n), (C.c_char_p * max(n, 1))(*[k.encode() for k in names]),
+        (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in ts]), (C.c_int64 * max(n, 1))(*[t.numel() for t in ts]),
+        _stream(stream)), "checkpoint_load")
+
+
 # ------------------------------------------------------------ interpolation
 def interp_fwd(queries, key_coords, feats, idx, valid, p, eps=1e-6, stream=None):
     """make_interp_op forward (proj/src/interpolation.cpp:192-222), batched:

@@ -33,6 +33,19 @@ def test_device_masks_bit_exact(grid, ratio, seed0, batch):
 
 
 @pytest.mark.gpu
+def test_device_masks_match_compiled_reference():
+    """Directly against the compiled reference's perlin_field + mask_from_field (oracle/_ref)."""
+    from oracle import ref
+    from paper_2602_16249_b200 import ops
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    seeds = [5, 77, 1234]
+    m = ops.perlin_masks(seeds, 96, 0.6).cpu().numpy()
+    for b, s in enumerate(seeds):
+        np.testing.assert_array_equal(m[b], ref.perlin_mask(96, 0.6, s))
+
+
+@pytest.mark.gpu
 def test_device_visible_coords_match_lattice_batch():
     from paper_2602_16249_b200 import ops
     seeds = [1000 + b for b in range(5)]
