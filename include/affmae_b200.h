@@ -320,6 +320,12 @@ int affmae_perlin_mask(const uint64_t* seeds_host, int64_t batch, int64_t h, int
  * count [B] (optional) receives each image's visible count; rows beyond nvis are dropped. */
 int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch,
                           int64_t nvis, float* coords, int32_t* count, void* stream);
+/* Replaces synth_image (src/pipeline.cpp:169-227), batched: img [B, size, size] float64 for
+ * seeds_host [B].  Matches the reference to ~1e-15 (device exp() is within 1 ulp of glibc's);
+ * synchronises `stream` before returning (the per-image draws are staged from the host). */
+size_t affmae_synth_images_workspace(int64_t batch, int64_t size);
+int affmae_synth_images(const uint64_t* seeds_host, int64_t batch, int64_t size, double* img, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* AFT1 tensor files (write_aft / read_aft, src/tensor_io.cpp:60-105; format
  * include/affmae/tensor_io.hpp:11-13) from / into DEVICE buffers.  write: dev_src holds fp32

@@ -247,6 +247,12 @@ def adamw(shapes, values, grads, lr=1e-3, warmup=100, wd=0.05, beta1=0.883, beta
     return vals
 
 
+def synth_image(size, seed):
+    out = np.empty(size * size)
+    _check(lib().ref_synth_image(C.c_int64(size), C.c_uint64(seed), _p(out)))
+    return out.reshape(size, size)
+
+
 def write_aft(path, vals, prec=0):
     """write_aft (proj/src/tensor_io.cpp:60-66) of a tensor of precision `prec` (0 b32, 1 b16emu)."""
     vals = _f64(vals)

@@ -14,6 +14,7 @@
 //   ref_merge_plan           -> merge_plan                   (merging.cpp:71-116)
 //   ref_merge_pool_fwd/bwd   -> make_merge_pool_op forward/backward (merging.cpp:151-220)
 //   ref_perlin_mask          -> perlin_field + mask_from_field (proj/src/masking.cpp:51-92)
+//   ref_synth_image          -> synth_image                  (proj/src/pipeline.cpp:169-227)
 //   ref_write_aft / _u8, ref_read_aft -> write_aft / write_aft_u8 / read_aft (proj/src/tensor_io.cpp:60-105)
 //   ref_hotpath_batch        -> the whole hot path over B images on T std::threads
 //                               (the multi-core CPU baseline of BASELINE.md §4)
@@ -399,6 +400,13 @@ int ref_adamw(double lr, int64_t warmup, double wd, double beta1, double beta2, 
             for (int64_t e = 0; e < q.value.numel(); ++e) values[o + e] = q.value.get(e);
             o += q.value.numel();
         }
+    });
+}
+
+int ref_synth_image(int64_t size, uint64_t seed, double* out) {
+    return guarded([&] {
+        Tensor t = synth_image(size, seed);
+        for (int64_t i = 0; i < t.numel(); ++i) out[i] = t.get(i);
     });
 }
 

@@ -73,6 +73,8 @@ int aft_read(const char*, float*, int64_t, int64_t*, void*);
 int checkpoint_save(const char*, int, const char* const*, const float* const*, const int64_t* const*, const int*,
                     const int*, void*);
 int checkpoint_load(const char*, int, const char* const*, float* const*, const int64_t*, void*);
+size_t synth_images_workspace(int64_t, int64_t);
+int synth_images(const uint64_t*, int64_t, int64_t, double*, void*, size_t, void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
@@ -250,6 +252,12 @@ int affmae_perlin_mask(const uint64_t* seeds_host, int64_t batch, int64_t h, int
 int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, double patch, int64_t nvis,
                           float* coords, int32_t* count, void* stream) {
     return visible_coords(masked, batch, h, w, patch, nvis, coords, count, stream);
+}
+
+size_t affmae_synth_images_workspace(int64_t batch, int64_t size) { return synth_images_workspace(batch, size); }
+int affmae_synth_images(const uint64_t* seeds_host, int64_t batch, int64_t size, double* img, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    return synth_images(seeds_host, batch, size, img, workspace, workspace_bytes, stream);
 }
 
 // AFT1 files and checkpoints (src/tensor_io.cpp:60-105, src/pipeline.cpp:757-797)

@@ -210,21 +210,14 @@ size_t perlin_mask_workspace(int64_t batch, int64_t h, int64_t w, int octaves, d
         const int64_t side = int64_t(std::ceil(base_freq * double(1 << o))) + 2;
         corners += side * side;
     }
-    return size_t(batch * h * w) * 8 + size_t(batch * corners) * 16 + size_t(octaves) * 32 + 1024;
+    return ((size_t(batch * h * w) * 8 + 255) & ~size_t(255)) + size_t(batch * corners) * 16 + size_t(octaves) * 32 +
+           1024;
 }
 
-int perlin_mask(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int octaves, double base_freq,
-                double persistence, double ratio, uint8_t* masked, void* workspace, size_t ws_bytes, void* stream) {
-    if (!seeds || !masked) return fail(AFFMAE_ECONFIG, "perlin_mask: null pointer");
-    if (h < 2 || w < 2) return fail(AFFMAE_ECONFIG, "perlin_field: grid must be at least 2x2");
-    if (octaves < 1 || octaves > 16) return fail(AFFMAE_ECONFIG, "perlin_field: octaves must be in [1, 16]");
-    if (!(ratio >= 0.0 && ratio <= 1.0)) return fail(AFFMAE_ECONFIG, "mask_from_field: ratio must be in [0, 1]");
-    if (!(base_freq > 0.0)) return fail(AFFMAE_ECONFIG, "perlin_field: base_freq must be positive");
-    if (batch < 0) return fail(AFFMAE_ECONFIG, "perlin_mask: bad batch");
-    if (!workspace || ws_bytes < perlin_mask_workspace(batch, h, w, octaves, base_freq))
-        return fail(AFFMAE_ECONFIG, "perlin_mask: workspace too small");
-    if (batch == 0) return AFFMAE_OK;
-    cudaStream_t st = as_stream(stream);
+// The Perlin field of `batch` images into the start of `workspace` (perlin_mask_workspace
+// layout): host gradient table + amplitudes, uploaded on `st`, then perlin_field_kernel.
+static int perlin_field_only(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int octaves,
+                             double base_freq, double persistence, void* workspace, cudaStream_t st) {
     // host: the corner gradients a grid touches (proj/src/masking.cpp:21-26, 51-69)
     const size_t no = static_cast<size_t>(octaves);
     std::vector<int64_t> off(no);
@@ -237,7 +230,7 @@ int perlin_mask(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int 
         corners += int64_t(side[size_t(o)]) * side[size_t(o)];
         amp[size_t(o)] = std::pow(persistence, o);
     }
-    std::vector<double> grads(size_t(batch * corners) * 2);
+    std::vector<double> grads(static_cast<size_t>(batch * corners) * 2);
     for (int64_t b = 0; b < batch; ++b)
         for (int o = 0; o < octaves; ++o) {
             const uint64_t os = mix64_h(seeds[b] + 0x9E3779B97F4A7C15ull * uint64_t(o + 1));
@@ -253,7 +246,7 @@ int perlin_mask(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int 
         }
     char* ws = static_cast<char*>(workspace);
     double* field = reinterpret_cast<double*>(ws);
-    double2* dgr = reinterpret_cast<double2*>(ws + size_t(batch * h * w) * 8);
+    double2* dgr = reinterpret_cast<double2*>(ws + ((size_t(batch * h * w) * 8 + 255) & ~size_t(255)));
     char* meta = reinterpret_cast<char*>(dgr + batch * corners);
     int64_t* doff = reinterpret_cast<int64_t*>(meta);
     double* damp = reinterpret_cast<double*>(doff + octaves);
@@ -263,13 +256,32 @@ int perlin_mask(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int 
         cudaMemcpyAsync(doff, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
         cudaMemcpyAsync(damp, amp.data(), amp.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
         cudaMemcpyAsync(dside, side.data(), side.size() * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return fail(AFFMAE_ECUDA, "perlin_mask: H2D of the gradient table failed");
+        return fail(AFFMAE_ECUDA, "perlin_field: H2D of the gradient table failed");
     PerlinGeo g{h, w, octaves, base_freq, corners};
     const int64_t n = batch * h * w;
     perlin_field_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 16 * kNumSMs)), 256, 0, st>>>(
         dgr, doff, dside, damp, g, batch, field);
+    AFFMAE_LAUNCH_CHECK("perlin_field_kernel");
+    return AFFMAE_OK;
+}
+
+int perlin_mask(const uint64_t* seeds, int64_t batch, int64_t h, int64_t w, int octaves, double base_freq,
+                double persistence, double ratio, uint8_t* masked, void* workspace, size_t ws_bytes, void* stream) {
+    if (!seeds || !masked) return fail(AFFMAE_ECONFIG, "perlin_mask: null pointer");
+    if (h < 2 || w < 2) return fail(AFFMAE_ECONFIG, "perlin_field: grid must be at least 2x2");
+    if (octaves < 1 || octaves > 16) return fail(AFFMAE_ECONFIG, "perlin_field: octaves must be in [1, 16]");
+    if (!(ratio >= 0.0 && ratio <= 1.0)) return fail(AFFMAE_ECONFIG, "mask_from_field: ratio must be in [0, 1]");
+    if (!(base_freq > 0.0)) return fail(AFFMAE_ECONFIG, "perlin_field: base_freq must be positive");
+    if (batch < 0) return fail(AFFMAE_ECONFIG, "perlin_mask: bad batch");
+    if (!workspace || ws_bytes < perlin_mask_workspace(batch, h, w, octaves, base_freq))
+        return fail(AFFMAE_ECONFIG, "perlin_mask: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    int rc = perlin_field_only(seeds, batch, h, w, octaves, base_freq, persistence, workspace, st);
+    if (rc) return rc;
     const int64_t want = std::llround(ratio * double(h * w));
-    mask_select_kernel<<<unsigned(batch), kMaskThreads, 0, st>>>(field, h * w, want, masked);
+    mask_select_kernel<<<unsigned(batch), kMaskThreads, 0, st>>>(static_cast<const double*>(workspace), h * w, want,
+                                                                 masked);
     AFFMAE_LAUNCH_CHECK("perlin_mask");
     return AFFMAE_OK;
 }
@@ -282,6 +294,164 @@ int visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64_t w, d
     visible_coords_kernel<<<unsigned(batch), kMaskThreads, 0, as_stream(stream)>>>(
         masked, h, w, patch, nvis, reinterpret_cast<float2*>(coords), count);
     AFFMAE_LAUNCH_CHECK("visible_coords_kernel");
+    return AFFMAE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// synth_image (proj/src/pipeline.cpp:169-227) on the device, batched: the Perlin base
+// (perlin_field(size, size, 2, 2.0, 0.5, mix64(seed ^ 0xba5e11)) through the same host
+// gradient table + explicitly rounded field kernel as the masks), then per curve the
+// max-of-stamps ink buffer (the stamps scatter with a 64-bit atomic max on the bit
+// pattern: the weights are positive, so the order of the doubles is the order of their
+// bits) added in curve order, the Gaussian blobs, and the clamp.  The RNG draws (splitmix64
+// stream, include/affmae/rng.hpp) stay on the host: a few dozen numbers per image.  exp()
+// is the device libm (<= 1 ulp from glibc), so pixels match the reference to ~1e-15, not
+// bitwise.
+namespace {
+struct HostRng {  // include/affmae/rng.hpp:18-44
+    uint64_t s;
+    uint64_t next() {
+        s += 0x9e3779b97f4a7c15ull;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    double uniform() { return double(next() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    uint64_t below(uint64_t n) { return n ? next() % n : 0; }
+};
+}  // namespace
+
+constexpr int kSynthMaxCurves = 4, kSynthMaxBlobs = 5;
+
+struct SynthParams {          // per image
+    int curves, blobs;
+    double cpx[kSynthMaxCurves][3], cpy[kSynthMaxCurves][3], csig[kSynthMaxCurves], camp[kSynthMaxCurves];
+    double bx[kSynthMaxBlobs], by[kSynthMaxBlobs], bsig[kSynthMaxBlobs], bamp[kSynthMaxBlobs];
+};
+
+__global__ void synth_base_kernel(const double* __restrict__ field, int64_t n, double* __restrict__ img) {
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x)
+        img[t] = da(0.5, dm(0.3, field[t]));
+}
+
+// one thread per (image, step, box cell); box side <= 2*ceil(3*sigma)+2 <= 14 for sigma < 1.8
+constexpr int kStampSide = 16;
+__global__ void synth_stamp_kernel(const SynthParams* __restrict__ prm, int c, int64_t size, int64_t batch,
+                                   unsigned long long* __restrict__ ink) {
+    const int64_t nsteps = 3 * size, per_img = (nsteps + 1) * kStampSide * kStampSide;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < batch * per_img;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = t / per_img, rem = t - b * per_img, st = rem / (kStampSide * kStampSide);
+        const int cell = int(rem - st * kStampSide * kStampSide), rr = cell / kStampSide, cc0 = cell % kStampSide;
+        const SynthParams& P = prm[b];
+        if (c >= P.curves) continue;
+        const double u = __ddiv_rn(double(st), double(nsteps));
+        const double a = dm(ds(1.0, u), ds(1.0, u)), bq = dm(dm(2.0, u), ds(1.0, u)), c2 = dm(u, u);
+        const double cx = da(da(dm(a, P.cpx[c][0]), dm(bq, P.cpx[c][1])), dm(c2, P.cpx[c][2]));
+        const double cy = da(da(dm(a, P.cpy[c][0]), dm(bq, P.cpy[c][1])), dm(c2, P.cpy[c][2]));
+        const double sg = P.csig[c], s3 = dm(3.0, sg);
+        const int64_t r0 = max(int64_t(0), int64_t(floor(ds(cy, s3))));
+        const int64_t r1 = min(size - 1, int64_t(ceil(da(cy, s3))));
+        const int64_t c0 = max(int64_t(0), int64_t(floor(ds(cx, s3))));
+        const int64_t c1 = min(size - 1, int64_t(ceil(da(cx, s3))));
+        const int64_t r = r0 + rr, col = c0 + cc0;
+        if (r > r1 || col > c1) continue;
+        const double dx = ds(da(double(col), 0.5), cx), dy = ds(da(double(r), 0.5), cy);
+        const double wgt = exp(__ddiv_rn(-da(dm(dx, dx), dm(dy, dy)), dm(dm(2.0, sg), sg)));
+        if (wgt > 0.0) atomicMax(ink + b * size * size + r * size + col, (unsigned long long)__double_as_longlong(wgt));
+    }
+}
+
+__global__ void synth_ink_add_kernel(const SynthParams* __restrict__ prm, int c, int64_t size, int64_t batch,
+                                     unsigned long long* __restrict__ ink, double* __restrict__ img) {
+    const int64_t cells = size * size;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < batch * cells;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = t / cells;
+        if (c < prm[b].curves) img[t] = da(img[t], dm(prm[b].camp[c], __longlong_as_double((long long)ink[t])));
+        ink[t] = 0ull;
+    }
+}
+
+__global__ void synth_blobs_kernel(const SynthParams* __restrict__ prm, int64_t size, int64_t batch,
+                                   double* __restrict__ img) {
+    const int64_t cells = size * size;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < batch * cells;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = t / cells, i = t - b * cells, r = i / size, c = i - r * size;
+        const SynthParams& P = prm[b];
+        double v = img[t];
+        for (int k = 0; k < P.blobs; ++k) {
+            const double dx = ds(da(double(c), 0.5), P.bx[k]), dy = ds(da(double(r), 0.5), P.by[k]);
+            v = da(v, dm(P.bamp[k], exp(__ddiv_rn(-da(dm(dx, dx), dm(dy, dy)), dm(dm(2.0, P.bsig[k]), P.bsig[k])))));
+        }
+        img[t] = fmin(fmax(v, 0.0), 1.0);
+    }
+}
+
+size_t synth_images_workspace(int64_t batch, int64_t size) {
+    return perlin_mask_workspace(batch, size, size, 2, 2.0) + size_t(batch * size * size) * 8 +
+           size_t(batch) * sizeof(SynthParams) + 1280;
+}
+
+int synth_images(const uint64_t* seeds, int64_t batch, int64_t size, double* img, void* workspace, size_t ws_bytes,
+                 void* stream) {
+    if (!seeds || !img) return fail(AFFMAE_ECONFIG, "synth_image: null pointer");
+    if (size < 2) return fail(AFFMAE_ECONFIG, "synth_image: size must be >= 2");
+    if (batch < 0) return fail(AFFMAE_ECONFIG, "synth_image: bad batch");
+    if (!workspace || ws_bytes < synth_images_workspace(batch, size))
+        return fail(AFFMAE_ECONFIG, "synth_image: workspace too small");
+    if (batch == 0) return AFFMAE_OK;
+    cudaStream_t st = as_stream(stream);
+    std::vector<uint64_t> fseeds(static_cast<size_t>(batch));
+    std::vector<SynthParams> prm(static_cast<size_t>(batch));
+    for (int64_t b = 0; b < batch; ++b) {
+        fseeds[size_t(b)] = mix64_h(seeds[b] ^ 0xba5e11ull);
+        HostRng rng{mix64_h(seeds[b]) ^ 0x5ca1ab1eull};
+        SynthParams& P = prm[size_t(b)];
+        P.curves = 2 + int(rng.below(3));
+        for (int c = 0; c < P.curves; ++c) {
+            for (int j = 0; j < 3; ++j) {
+                P.cpx[c][j] = rng.uniform(0.0, double(size));
+                P.cpy[c][j] = rng.uniform(0.0, double(size));
+            }
+            P.csig[c] = rng.uniform(0.8, 1.8);
+            P.camp[c] = rng.uniform(0.25, 0.45) * (rng.below(2) ? 1.0 : -1.0);
+        }
+        P.blobs = 2 + int(rng.below(4));
+        for (int k = 0; k < P.blobs; ++k) {
+            P.bx[k] = rng.uniform(0.0, double(size));
+            P.by[k] = rng.uniform(0.0, double(size));
+            P.bsig[k] = rng.uniform(2.0, std::max(3.0, double(size) / 8.0));
+            P.bamp[k] = rng.uniform(0.3, 0.5) * (rng.below(2) ? 1.0 : -1.0);
+        }
+    }
+    char* ws = static_cast<char*>(workspace);
+    const size_t pws = perlin_mask_workspace(batch, size, size, 2, 2.0);
+    auto* ink = reinterpret_cast<unsigned long long*>(ws + ((pws + 255) & ~size_t(255)));
+    auto* dprm = reinterpret_cast<SynthParams*>(ink + batch * size * size);
+    // the Perlin field of perlin_mask's pipeline, without the selection (field at ws start)
+    int rc = perlin_field_only(fseeds.data(), batch, size, size, 2, 2.0, 0.5, ws, st);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(dprm, prm.data(), prm.size() * sizeof(SynthParams), cudaMemcpyHostToDevice, st) !=
+            cudaSuccess ||
+        cudaMemsetAsync(ink, 0, size_t(batch * size * size) * 8, st) != cudaSuccess)
+        return fail(AFFMAE_ECUDA, "synth_image: staging failed");
+    const int64_t n = batch * size * size;
+    const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 16 * kNumSMs));
+    synth_base_kernel<<<nb, 256, 0, st>>>(reinterpret_cast<const double*>(ws), n, img);
+    const int64_t stamps = batch * (3 * size + 1) * kStampSide * kStampSide;
+    const unsigned sb = unsigned(std::min<int64_t>((stamps + 255) / 256, 32 * kNumSMs));
+    for (int c = 0; c < kSynthMaxCurves; ++c) {
+        synth_stamp_kernel<<<sb, 256, 0, st>>>(dprm, c, size, batch, ink);
+        synth_ink_add_kernel<<<nb, 256, 0, st>>>(dprm, c, size, batch, ink, img);
+    }
+    synth_blobs_kernel<<<nb, 256, 0, st>>>(dprm, size, batch, img);
+    AFFMAE_LAUNCH_CHECK("synth_images");
+    // the host staging vectors must outlive the async copies
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(AFFMAE_ECUDA, "synth_image: sync failed");
     return AFFMAE_OK;
 }
 

@@ -355,6 +355,20 @@ def perlin_masks(seeds, grid, ratio, octaves=2, base_freq=4.0, persistence=0.5, 
     return masked
 
 
+def synth_images(seeds, size, device="cuda", stream=None):
+    """synth_image (proj/src/pipeline.cpp:169-227) for len(seeds) images on the device:
+    -> [B, size, size] float64."""
+    B = len(seeds)
+    sd = (C.c_uint64 * max(B, 1))(*[int(s) for s in seeds])
+    L = capi.lib()
+    ws = _workspace(L.affmae_synth_images_workspace(C.c_int64(B), C.c_int64(size)), device)
+    img = torch.empty((B, size, size), dtype=torch.float64, device=device)
+    capi.check(L.affmae_synth_images(sd, C.c_int64(B), C.c_int64(size), C.c_void_p(img.data_ptr()),
+                                     C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()), _stream(stream)),
+               "synth_images")
+    return img
+
+
 def visible_coords(masked, patch=8, nvis=None, stream=None):
     """Visible patch centres in ascending cell index (proj/src/geometry.cpp:44-50):
     masked [B, h, w] uint8 -> (coords [B, nvis, 2] fp32, count [B] int32)."""
