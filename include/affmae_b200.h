@@ -323,6 +323,14 @@ int affmae_visible_coords(const uint8_t* masked, int64_t batch, int64_t h, int64
 /* Replaces synth_image (src/pipeline.cpp:169-227), batched: img [B, size, size] float64 for
  * seeds_host [B].  Matches the reference to ~1e-15 (device exp() is within 1 ulp of glibc's);
  * synchronises `stream` before returning (the per-image draws are staged from the host). */
+/* patchify (src/pipeline.cpp:131-150): img [B, h, w] float64 -> vectors [B, (h/p)*(w/p), p*p]
+ * float32 row-major patches.  affmae_masked_rows: the masked cells of each image in ascending
+ * index as global rows b*cells + cell -> rows [B, nmask] (Model::loss_parts target rows,
+ * src/pipeline.cpp:588-596; the `cells` argument of affmae_masked_mse). */
+int affmae_patchify(const double* img, int64_t batch, int64_t h, int64_t w, int64_t patch, float* vectors,
+                    void* stream);
+int affmae_masked_rows(const uint8_t* masked, int64_t batch, int64_t cells, int64_t nmask, int32_t* rows,
+                       void* stream);
 size_t affmae_synth_images_workspace(int64_t batch, int64_t size);
 int affmae_synth_images(const uint64_t* seeds_host, int64_t batch, int64_t size, double* img, void* workspace,
                         size_t workspace_bytes, void* stream);

@@ -33,7 +33,8 @@ EXPORTS = (
     "affmae_layernorm_bwd", "affmae_norm_clamp_fwd", "affmae_norm_clamp_bwd", "affmae_masked_mse_workspace",
     "affmae_masked_mse", "affmae_gattn_fwd", "affmae_gattn_bwd", "affmae_gattn_bwd_workspace",
     "affmae_interp_bwd_gather_workspace", "affmae_interp_bwd_gather", "affmae_perlin_mask_workspace",
-    "affmae_perlin_mask", "affmae_visible_coords", "affmae_synth_images_workspace", "affmae_synth_images", "affmae_aft_write", "affmae_aft_read_header",
+    "affmae_perlin_mask", "affmae_visible_coords", "affmae_synth_images_workspace", "affmae_synth_images",
+    "affmae_patchify", "affmae_masked_rows", "affmae_aft_write", "affmae_aft_read_header",
     "affmae_aft_read", "affmae_checkpoint_save", "affmae_checkpoint_load",
 )
 

@@ -75,6 +75,8 @@ int checkpoint_save(const char*, int, const char* const*, const float* const*, c
 int checkpoint_load(const char*, int, const char* const*, float* const*, const int64_t*, void*);
 size_t synth_images_workspace(int64_t, int64_t);
 int synth_images(const uint64_t*, int64_t, int64_t, double*, void*, size_t, void*);
+int patchify(const double*, int64_t, int64_t, int64_t, int64_t, float*, void*);
+int masked_rows(const uint8_t*, int64_t, int64_t, int64_t, int32_t*, void*);
 int64_t retained_count_impl(int64_t, double);
 double adamw_lr(const affmae_adamw_cfg*, int64_t);
 size_t linear_workspace(int64_t, int64_t, int64_t);
@@ -258,6 +260,15 @@ size_t affmae_synth_images_workspace(int64_t batch, int64_t size) { return synth
 int affmae_synth_images(const uint64_t* seeds_host, int64_t batch, int64_t size, double* img, void* workspace,
                         size_t workspace_bytes, void* stream) {
     return synth_images(seeds_host, batch, size, img, workspace, workspace_bytes, stream);
+}
+
+int affmae_patchify(const double* img, int64_t batch, int64_t h, int64_t w, int64_t patch, float* vectors,
+                    void* stream) {
+    return patchify(img, batch, h, w, patch, vectors, stream);
+}
+int affmae_masked_rows(const uint8_t* masked, int64_t batch, int64_t cells, int64_t nmask, int32_t* rows,
+                       void* stream) {
+    return masked_rows(masked, batch, cells, nmask, rows, stream);
 }
 
 // AFT1 files and checkpoints (src/tensor_io.cpp:60-105, src/pipeline.cpp:757-797)

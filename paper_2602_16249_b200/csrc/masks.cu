@@ -455,4 +455,78 @@ int synth_images(const uint64_t* seeds, int64_t batch, int64_t size, double* img
     return AFFMAE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// patchify (proj/src/pipeline.cpp:131-150) and the masked-cell target rows of the loss
+// (Model::loss_parts, :588-596): image [B, H, W] float64 -> vectors [B, T, patch^2] float32
+// (the b32 tape's rounding of Tensor::set), and the masked cells of every image in
+// ascending index as GLOBAL rows b*T + cell (what affmae_masked_mse gathers).
+__global__ void patchify_kernel(const double* __restrict__ img, int64_t batch, int64_t h, int64_t w, int patch,
+                                float* __restrict__ vec) {
+    const int64_t gw = w / patch, cells = (h / patch) * gw, p2 = int64_t(patch) * patch, per = cells * p2;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < batch * per;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = t / per, r = t - b * per, tix = r / p2, e = r - tix * p2;
+        const int64_t gr = tix / gw, gc = tix - gr * gw, pr = e / patch, pc = e - pr * patch;
+        vec[t] = float(img[(b * h + gr * patch + pr) * w + gc * patch + pc]);
+    }
+}
+
+__global__ void __launch_bounds__(kMaskThreads) masked_rows_kernel(const uint8_t* __restrict__ masked, int64_t cells,
+                                                                   int64_t nmask, int32_t* __restrict__ rows) {
+    __shared__ int32_t wsum[32];
+    const uint8_t* m = masked + int64_t(blockIdx.x) * cells;
+    int32_t* out = rows + int64_t(blockIdx.x) * nmask;
+    const int64_t per = (cells + kMaskThreads - 1) / kMaskThreads;
+    const int64_t lo = threadIdx.x * per, hi = lo + per < cells ? lo + per : cells;
+    int32_t cnt = 0;
+    for (int64_t i = lo; i < hi; ++i) cnt += m[i] != 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += v;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    int64_t pos = inc - cnt + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int64_t i = lo; i < hi; ++i)
+        if (m[i] != 0) {
+            if (pos < nmask) out[pos] = int32_t(int64_t(blockIdx.x) * cells + i);
+            ++pos;
+        }
+}
+
+int patchify(const double* img, int64_t batch, int64_t h, int64_t w, int64_t patch, float* vectors, void* stream) {
+    if (!img || !vectors) return fail(AFFMAE_ECONFIG, "patchify: null pointer");
+    if (patch < 1 || h % patch || w % patch || h < patch || w < patch)
+        return fail(AFFMAE_ECONFIG, "patchify: image extents must be positive multiples of the patch");
+    if (batch <= 0) return batch == 0 ? AFFMAE_OK : fail(AFFMAE_ECONFIG, "patchify: bad batch");
+    const int64_t n = batch * h * w;
+    patchify_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 16 * kNumSMs)), 256, 0, as_stream(stream)>>>(
+        img, batch, h, w, int(patch), vectors);
+    AFFMAE_LAUNCH_CHECK("patchify_kernel");
+    return AFFMAE_OK;
+}
+
+int masked_rows(const uint8_t* masked, int64_t batch, int64_t cells, int64_t nmask, int32_t* rows, void* stream) {
+    if (!masked || !rows) return fail(AFFMAE_ECONFIG, "masked_rows: null pointer");
+    if (batch < 0 || cells < 1 || nmask < 0 || batch * cells >= (int64_t(1) << 31))
+        return fail(AFFMAE_ECONFIG, "masked_rows: bad shape");
+    if (batch == 0) return AFFMAE_OK;
+    masked_rows_kernel<<<unsigned(batch), kMaskThreads, 0, as_stream(stream)>>>(masked, cells, nmask, rows);
+    AFFMAE_LAUNCH_CHECK("masked_rows_kernel");
+    return AFFMAE_OK;
+}
+
 }  // namespace affmae_b200

@@ -369,6 +369,31 @@ def synth_images(seeds, size, device="cuda", stream=None):
     return img
 
 
+def patchify(img, patch=8, stream=None):
+    """patchify (proj/src/pipeline.cpp:131-150): [B, H, W] float64 -> [B, T, patch^2] float32."""
+    _req(img, torch.float64, "img")
+    B, H, W = img.shape
+    out = torch.empty((B, (H // patch) * (W // patch), patch * patch), dtype=torch.float32, device=img.device)
+    capi.check(capi.lib().affmae_patchify(C.c_void_p(img.data_ptr()), C.c_int64(B), C.c_int64(H), C.c_int64(W),
+                                          C.c_int64(patch), C.c_void_p(out.data_ptr()), _stream(stream)),
+               "patchify")
+    return out
+
+
+def masked_rows(masked, nmask=None, stream=None):
+    """Global target rows b*T + cell of the masked cells, ascending per image -> [B, nmask] int32."""
+    _req(masked, torch.uint8, "masked")
+    B = masked.shape[0]
+    cells = masked[0].numel()
+    if nmask is None:
+        nmask = int(masked[0].sum().item())
+    rows = torch.empty((B, nmask), dtype=torch.int32, device=masked.device)
+    capi.check(capi.lib().affmae_masked_rows(C.c_void_p(masked.data_ptr()), C.c_int64(B), C.c_int64(cells),
+                                             C.c_int64(nmask), C.c_void_p(rows.data_ptr()), _stream(stream)),
+               "masked_rows")
+    return rows
+
+
 def visible_coords(masked, patch=8, nvis=None, stream=None):
     """Visible patch centres in ascending cell index (proj/src/geometry.cpp:44-50):
     masked [B, h, w] uint8 -> (coords [B, nvis, 2] fp32, count [B] int32)."""

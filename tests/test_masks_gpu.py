@@ -78,3 +78,28 @@ def test_device_synth_images_match_reference(size, seeds):
     for b, s in enumerate(seeds):
         want = ref.synth_image(size, s)
         assert np.abs(img[b] - want).max() <= 1e-12, (s, np.abs(img[b] - want).max())
+
+
+@pytest.mark.gpu
+def test_device_targets_patchify_masked_rows_and_loss():
+    """The step's reconstruction targets built on the device: synth_image -> patchify
+    (proj/src/pipeline.cpp:131-150) -> masked rows (Model::loss_parts, :588-596) -> masked MSE,
+    against a numpy restatement of patchify on the same images."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    seeds, size, patch, ratio = [21, 22], 64, 8, 0.75
+    img = ops.synth_images(seeds, size)
+    vec = ops.patchify(img, patch)
+    g = size // patch
+    want = img.cpu().numpy().reshape(2, g, patch, g, patch).transpose(0, 1, 3, 2, 4).reshape(2, g * g, patch * patch)
+    np.testing.assert_array_equal(vec.cpu().numpy(), want.astype(np.float32))
+    m = ops.perlin_masks(seeds, g, ratio)
+    rows = ops.masked_rows(m)
+    mm = m.cpu().numpy().reshape(2, -1)
+    for b in range(2):
+        np.testing.assert_array_equal(rows[b].cpu().numpy(), b * g * g + np.nonzero(mm[b])[0])
+    r = rows.reshape(-1)
+    pred = torch.zeros((r.numel(), patch * patch), dtype=torch.bfloat16, device="cuda")
+    loss, _ = ops.masked_mse(pred, vec.reshape(-1, patch * patch), r)
+    tgt = want.reshape(-1, patch * patch)[r.cpu().numpy()]
+    assert abs(float(loss.item()) - float((tgt.astype(np.float32) ** 2).mean())) <= 1e-5
