@@ -699,6 +699,34 @@ class AdamW:
             _stream(stream)), "adamw_step")
         self.t += 1
 
+    def save(self, directory, names, stream=None):
+        """save_checkpoint (proj/src/pipeline.cpp:757-770) of the parameters under `names`, plus
+        the state the reference omits: the moments as "<name>.adam_m" / "<name>.adam_v" entries
+        and the step count as "adamw.step" (AFT1 b32, one value)."""
+        entries = {}
+        offs = [0] + [p.numel() for p in self.params]
+        pos = np.cumsum([(z + 3) // 4 * 4 for z in offs[1:]])
+        for i, (nm, p) in enumerate(zip(names, self.params)):
+            o = int(pos[i - 1]) if i else 0
+            entries[nm] = (p, "b32")
+            entries[nm + ".adam_m"] = (self.m[o:o + p.numel()].view(p.shape), "b32")
+            entries[nm + ".adam_v"] = (self.v[o:o + p.numel()].view(p.shape), "b32")
+        entries["adamw.step"] = (torch.tensor([float(self.t)], device=self.value.device), "b32")
+        save_checkpoint(directory, entries, stream=stream)
+
+    def load(self, directory, names, stream=None):
+        """load_checkpoint into the parameters, moments and step count written by save()."""
+        entries, offs = {}, 0
+        for nm, p in zip(names, self.params):
+            entries[nm] = p
+            entries[nm + ".adam_m"] = self.m[offs:offs + p.numel()].view(p.shape)
+            entries[nm + ".adam_v"] = self.v[offs:offs + p.numel()].view(p.shape)
+            offs += (p.numel() + 3) // 4 * 4
+        step = torch.zeros(1, device=self.value.device)
+        entries["adamw.step"] = step
+        load_checkpoint(directory, entries, stream=stream)
+        self.t = int(step.item())
+
 
 # -------------------------------------------------------------------- merge
 def retained_count(n, d_s):

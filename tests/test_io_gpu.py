@@ -96,3 +96,34 @@ def test_checkpoint_round_trip_and_reference_format(tmp_path):
         ops.load_checkpoint(str(d), {k: dst[k] for k in list(dst)[:2]})
     with pytest.raises(ValueError, match="size mismatch|too small"):
         ops.load_checkpoint(str(d), {**dst, "enc.s0.ln1.g": torch.zeros(4, device="cuda")})
+
+
+def test_adamw_checkpoint_resumes_bit_identically(tmp_path):
+    """Parameters + AdamW moments + step through the AFT1 checkpoint: a resumed optimizer takes
+    the same next step as the uninterrupted one (the reference saves values only)."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    shapes, names = [(16, 8), (8,), (3, 5)], ["w", "b", "u"]
+    rng = np.random.default_rng(8)
+
+    def run(opt, steps):
+        for _ in range(steps):
+            for g in opt.grads:
+                g.copy_(torch.as_tensor(rng.standard_normal(tuple(g.shape)), dtype=torch.float32))
+            opt.step()
+
+    a = ops.AdamW(shapes, warmup=2, total_steps=10)
+    for p in a.params:
+        p.copy_(torch.as_tensor(rng.standard_normal(tuple(p.shape)), dtype=torch.float32))
+    run(a, 3)
+    a.save(str(tmp_path / "ck"), names)
+    b = ops.AdamW(shapes, warmup=2, total_steps=10)
+    b.load(str(tmp_path / "ck"), names)
+    assert b.t == 3 and torch.equal(b.value, a.value) and torch.equal(b.m, a.m) and torch.equal(b.v, a.v)
+    g = [torch.as_tensor(rng.standard_normal(tuple(x.shape)), dtype=torch.float32) for x in a.grads]
+    for opt in (a, b):
+        for dst, src in zip(opt.grads, g):
+            dst.copy_(src)
+        opt.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.value, b.value)
