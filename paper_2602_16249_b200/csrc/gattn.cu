@@ -124,13 +124,23 @@ __global__ void __launch_bounds__(256) gattn_fwd_kernel(GAttnP p, __nv_bfloat16*
         };
         const int32_t* ir = p.idx + gi * p.m;
         const uint8_t* vv = p.valid + gi * p.m;
-        for (int j = 0; j < p.m; ++j) {
-            if (!vv[j]) continue;
-            const int64_t key = b0 + ir[j];
+        auto slot = [&](int32_t t) {
+            const int64_t key = b0 + t;
             const float2 kx = xy[key];
             const float s = gdot<HD>(qf, p.k + key * ld + h * HD) +
                             gbias(un, p.hidden, b2, (kx.x - qx.x) * p.inv_patch, (kx.y - qx.y) * p.inv_patch);
             take(s, p.v + key * ld + h * HD);
+        };
+        if (p.m == 8) {  // the decoder's self_k rows: two 16-byte index loads and one 8-byte valid load
+            const int4 i0 = __ldg(reinterpret_cast<const int4*>(ir)), i1 = __ldg(reinterpret_cast<const int4*>(ir) + 1);
+            const uint2 vb = __ldg(reinterpret_cast<const uint2*>(vv));
+            const int32_t ids[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (((j < 4 ? vb.x >> (8 * j) : vb.y >> (8 * (j - 4))) & 0xffu) != 0u) slot(ids[j]);
+        } else {
+            for (int j = 0; j < p.m; ++j)
+                if (vv[j]) slot(ir[j]);
         }
         take(gdot<HD>(qf, p.bk + h * HD) + blank, p.bv + h * HD);
         const float il = 1.f / l;
