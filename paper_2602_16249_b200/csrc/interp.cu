@@ -324,9 +324,10 @@ int interp_bwd(const float* queries, const float* key_coords, const void* feats,
 // chunks each), sums w * g over its entries and adds the result once.
 __global__ void interp_rev_count_kernel(const int32_t* __restrict__ idx, const uint8_t* __restrict__ valid,
                                         int64_t rows, int64_t nq, int64_t nk, int k, int32_t* __restrict__ cnt) {
-    const int64_t n = rows * k;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
-        if (valid[e]) atomicAdd(cnt + (e / k / nq) * (nk + 1) + idx[e], 1);
+    // entries < 2^31 (checked by the callers): 32-bit index math, the image from one division
+    const uint32_t n = uint32_t(rows * k), span = uint32_t(nq * k);
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+        if (valid[e]) atomicAdd(cnt + int64_t(e / span) * (nk + 1) + idx[e], 1);
 }
 
 // Per-image exclusive scan of the key counts, in place: one 1024-thread block per image walks
@@ -373,10 +374,10 @@ __global__ void interp_rev_fill_kernel(const int32_t* __restrict__ idx, const ui
                                        int64_t rows, int64_t nq, int64_t nk, int k, const int32_t* __restrict__ off,
                                        int32_t* __restrict__ cur, int32_t* __restrict__ ent,
                                        int32_t* __restrict__ ent_key) {
-    const int64_t n = rows * k;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+    const uint32_t n = uint32_t(rows * k), span = uint32_t(nq * k);
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
         if (valid[e]) {
-            const int64_t b = e / k / nq, j = idx[e];
+            const int64_t b = e / span, j = idx[e];
             const int64_t pos = b * nq * k + off[b * (nk + 1) + j] + atomicAdd(cur + b * nk + j, 1);
             ent[pos] = int32_t(e);
             ent_key[pos] = int32_t(b * nk + j);
