@@ -217,12 +217,34 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
         const int32_t* ir = p.idx + row * p.m;
         const uint8_t* vv = p.valid + row * p.m;
         float mx = -INFINITY;
+        bool vec8 = false;
+        int4 i0 = make_int4(0, 0, 0, 0), i1 = i0;
+        uint2 vb = make_uint2(0u, 0u);
+        if constexpr (MW == 8) {
+            vec8 = p.m == 8;
+            if (vec8) {  // the decoder's self_k rows: two 16-byte index loads, one 8-byte valid load
+                i0 = __ldg(reinterpret_cast<const int4*>(ir));
+                i1 = __ldg(reinterpret_cast<const int4*>(ir) + 1);
+                vb = __ldg(reinterpret_cast<const uint2*>(vv));
+            }
+        }
 #pragma unroll
         for (int j = 0; j < MW; ++j) {
             w[j] = -INFINITY;
             key[j] = -1;
-            if (act && j < p.m && vv[j]) {
-                key[j] = ir[j];
+            bool ok;
+            int32_t id;
+            if (vec8) {
+                const int4& iv = j < 4 ? i0 : i1;
+                const int jj = j & 3;
+                id = jj == 0 ? iv.x : jj == 1 ? iv.y : jj == 2 ? iv.z : iv.w;
+                ok = act && ((j < 4 ? vb.x >> (8 * j) : vb.y >> (8 * (j - 4))) & 0xffu) != 0u;
+            } else {
+                ok = act && j < p.m && vv[j];
+                id = ok ? ir[j] : 0;
+            }
+            if (ok) {
+                key[j] = id;
                 const float2 kx = xy[b0 + key[j]];
                 w[j] = p.scale * gdot<HD>(qf, p.k + (b0 + key[j]) * ld + h * HD) +
                        gbias(un, H, b2, (kx.x - qx.x) * p.inv_patch, (kx.y - qx.y) * p.inv_patch);
