@@ -56,3 +56,26 @@ def test_workspace_queries_are_host_side():
     assert L.affmae_attn_bwd_workspace(C.byref(geo), C.byref(d)) > L.affmae_attn_fwd_workspace(C.byref(geo), C.byref(d))
     d_bad = capi.AttnDesc(4, 24, 8, 8.0)
     assert L.affmae_attn_fwd_workspace(C.byref(geo), C.byref(d_bad)) == 0
+
+
+def test_aft_header_parsing_is_host_only(tmp_path):
+    """affmae_aft_read_header (write_aft's header, proj/src/tensor_io.cpp:51-57,78-92) on files
+    written by the compiled reference, and the ConfigError cases -- no device needed."""
+    import numpy as np
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    L = capi.lib()
+    p = str(tmp_path / "t.aft")
+    ref.write_aft(p, np.zeros((3, 4, 5)), 1)
+    dt, nd, dims = C.c_int(), C.c_int(), (C.c_int64 * 8)()
+    capi.check(L.affmae_aft_read_header(p.encode(), C.byref(dt), C.byref(nd), dims))
+    assert (dt.value, nd.value, list(dims[:3])) == (1, 3, [3, 4, 5])
+    (tmp_path / "bad.aft").write_bytes(b"AFT1" + bytes([7]) + bytes(4))
+    with pytest.raises(ValueError, match="bad AFT1 dtype"):
+        capi.check(L.affmae_aft_read_header(str(tmp_path / "bad.aft").encode(), C.byref(dt), C.byref(nd), dims))
+    (tmp_path / "nd.aft").write_bytes(b"AFT1" + bytes([0]) + (9).to_bytes(4, "little"))
+    with pytest.raises(ValueError, match="implausible AFT1 ndim"):
+        capi.check(L.affmae_aft_read_header(str(tmp_path / "nd.aft").encode(), C.byref(dt), C.byref(nd), dims))
+    with pytest.raises(ValueError, match="no checkpoint index"):
+        capi.check(L.affmae_checkpoint_load(str(tmp_path / "none").encode(), 0, None, None, None, None))
