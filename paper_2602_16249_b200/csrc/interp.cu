@@ -327,7 +327,12 @@ __global__ void interp_rev_count_kernel(const int32_t* __restrict__ idx, const u
     // entries < 2^31 (checked by the callers): 32-bit index math, the image from one division
     const uint32_t n = uint32_t(rows * k), span = uint32_t(nq * k);
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
-        if (valid[e]) atomicAdd(cnt + int64_t(e / span) * (nk + 1) + idx[e], 1);
+        if (valid[e]) {
+            // neighbouring rows share keys: one atomic per distinct key of the warp
+            const int64_t slot = int64_t(e / span) * (nk + 1) + idx[e];
+            const unsigned peers = __match_any_sync(__activemask(), (unsigned long long)slot);
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + slot, __popc(peers));
+        }
 }
 
 // Per-image exclusive scan of the key counts, in place: one 1024-thread block per image walks
@@ -378,7 +383,12 @@ __global__ void interp_rev_fill_kernel(const int32_t* __restrict__ idx, const ui
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
         if (valid[e]) {
             const int64_t b = e / span, j = idx[e];
-            const int64_t pos = b * nq * k + off[b * (nk + 1) + j] + atomicAdd(cur + b * nk + j, 1);
+            const unsigned peers = __match_any_sync(__activemask(), (unsigned long long)(b * nk + j));
+            const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+            int32_t base = 0;
+            if (lane == leader) base = atomicAdd(cur + b * nk + j, __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            const int64_t pos = b * nq * k + off[b * (nk + 1) + j] + base + __popc(peers & ((1u << lane) - 1u));
             ent[pos] = int32_t(e);
             ent_key[pos] = int32_t(b * nk + j);
         }
