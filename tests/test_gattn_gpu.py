@@ -41,6 +41,8 @@ CASES = [  # name, B, N, heads, head_dim, hidden, kind, width
     ("self_holes_d32", 1, 400, 2, 32, 16, "holes", 12),
     ("self_wide_d64", 2, 300, 2, 64, 8, "self", 31),
     ("self_d32_h8", 3, 257, 8, 32, 4, "self", 5),
+    ("self_h2_d16", 1, 200, 2, 16, 8, "self", 6),   # 32-wide rows: one dim per lane in the gather
+    ("self_h8_d64", 1, 150, 8, 64, 8, "holes", 4),  # 512-wide rows
 ]
 
 
