@@ -594,4 +594,27 @@ std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int hea
     return op;
 }
 
+MaskSpec perlin_mask(int64_t hp, int64_t wp, double ratio, uint64_t seed) {
+    if (hp != wp) throw ConfigError("cuda::perlin_mask: square grids only");
+    Dev ws(affmae_perlin_mask_workspace(1, hp, wp, kPerlinOctaves, kPerlinBaseFreq)), out(size_t(hp * wp));
+    check(affmae_perlin_mask(&seed, 1, hp, wp, kPerlinOctaves, kPerlinBaseFreq, kPerlinPersistence, ratio,
+                             out.as<uint8_t>(), ws.p, ws.n, nullptr),
+          "perlin_mask");
+    MaskSpec m;  // as mask_from_field fills it (src/masking.cpp:71-92)
+    m.hp = hp;
+    m.wp = wp;
+    m.ratio = ratio;
+    m.masked = download<uint8_t>(out, size_t(hp * wp));
+    return m;
+}
+
+Tensor synth_image(int64_t size, uint64_t seed) {
+    Dev ws(affmae_synth_images_workspace(1, size)), img(size_t(size * size) * 8);
+    check(affmae_synth_images(&seed, 1, size, img.as<double>(), ws.p, ws.n, nullptr), "synth_image");
+    auto h = download<double>(img, size_t(size * size));
+    Tensor t = Tensor::zeros({size, size}, Precision::b64);
+    for (int64_t i = 0; i < size * size; ++i) t.set(i, h[size_t(i)]);
+    return t;
+}
+
 }  // namespace affmae::cuda

@@ -18,6 +18,7 @@
 #include "affmae/attention.hpp"
 #include "affmae/geometry.hpp"
 #include "affmae/interpolation.hpp"
+#include "affmae/masking.hpp"
 #include "affmae/merging.hpp"
 #include "affmae/tape.hpp"
 
@@ -44,6 +45,12 @@ std::shared_ptr<CustomOp> make_cluster_attn_op(Tensor coords, int64_t cluster, i
 std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim,
                                        int bias_hidden, double patch, bool streaming = true,
                                        bool half_io = false);
+
+// Device-generated inputs: mask_from_field(perlin_field(hp, wp, kPerlinOctaves, kPerlinBaseFreq,
+// kPerlinPersistence, seed), ratio) (include/affmae/masking.hpp:31-40; bit-exact) and
+// synth_image (include/affmae/pipeline.hpp:30; within 1e-12).
+MaskSpec perlin_mask(int64_t hp, int64_t wp, double ratio, uint64_t seed);
+Tensor synth_image(int64_t size, uint64_t seed);
 
 // select_retained / merge_plan / make_merge_pool_op (include/affmae/merging.hpp:32-68)
 std::vector<int64_t> select_retained(const Tensor& scores, double d_s);

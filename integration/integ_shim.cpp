@@ -8,7 +8,9 @@
 #include "affmae/attention.hpp"
 #include "affmae/errors.hpp"
 #include "affmae/geometry.hpp"
+#include "affmae/masking.hpp"
 #include "affmae/merging.hpp"
+#include "affmae/pipeline.hpp"
 #include "affmae/tape.hpp"
 #include "affmae_cuda_ops.hpp"
 
@@ -176,6 +178,20 @@ int integ_gattn_tape(int use_cuda, int64_t n, int heads, int d, int hidden, doub
         t.backward(loss);
         to(t.value(o), out);
         for (int i = 0; i < 10; ++i) to(t.grad(ids[size_t(i)]), grads[i]);
+    });
+}
+
+// Perlin mask and synthetic image through either side's public functions.
+int integ_inputs(int use_cuda, int64_t grid, double ratio, uint64_t seed, uint8_t* mask, int64_t img_size,
+                 double* img) {
+    return guarded([&] {
+        MaskSpec m = use_cuda ? cuda::perlin_mask(grid, grid, ratio, seed)
+                              : mask_from_field(perlin_field(grid, grid, kPerlinOctaves, kPerlinBaseFreq,
+                                                             kPerlinPersistence, seed),
+                                                ratio);
+        for (size_t i = 0; i < m.masked.size(); ++i) mask[i] = m.masked[i];
+        Tensor t = use_cuda ? cuda::synth_image(img_size, seed) : synth_image(img_size, seed);
+        to(t, img);
     });
 }
 

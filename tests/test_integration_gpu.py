@@ -156,3 +156,17 @@ def test_decoder_attention_custom_op_on_reference_tape():
     names = ("dq", "dk", "dv", "dblank_k", "dblank_v", "dw1", "db1", "dw2", "db2", "dblank")
     errs = {nm: rel_l2(a, r) for nm, a, r in zip(names, g1, g0)}
     assert all(e <= 1e-2 for e in errs.values()), errs
+
+
+def test_device_inputs_adapters_match_reference():
+    """cuda::perlin_mask (bit-exact MaskSpec) and cuda::synth_image (within 1e-12) against the
+    reference's mask_from_field(perlin_field(...)) and synth_image."""
+    L = _lib()
+    res = []
+    for use in (0, 1):
+        m, img = np.zeros(96 * 96, np.uint8), np.zeros(80 * 80)
+        _ok(L, L.integ_inputs(C.c_int(use), C.c_int64(96), C.c_double(0.75), C.c_uint64(42), _p(m),
+                              C.c_int64(80), _p(img)))
+        res.append((m, img))
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    assert np.abs(res[0][1] - res[1][1]).max() <= 1e-12
