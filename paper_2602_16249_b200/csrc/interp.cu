@@ -95,9 +95,12 @@ __device__ __forceinline__ void interp_row_weights(InterpRow<CPR>& R, const floa
     }
 #pragma unroll
     for (int i = 0; i < G::MPL; ++i) R.w[i] = R.w[i] == -INFINITY ? 0.f : __expf(R.w[i] - mx);
-    float s = 0.f;  // normaliser in neighbour order
+    float s = 0.f;  // normaliser in neighbour order (slots >= k hold 0: stop at k, k is uniform)
 #pragma unroll
-    for (int t = 0; t < kInterpMaxK; ++t) s += __shfl_sync(0xffffffffu, R.w[t / G::LPR], base + t % G::LPR);
+    for (int t = 0; t < kInterpMaxK; ++t) {
+        if (t >= k) break;
+        s += __shfl_sync(0xffffffffu, R.w[t / G::LPR], base + t % G::LPR);
+    }
     const float is = nv > 0 ? 1.f / s : 0.f;
 #pragma unroll
     for (int i = 0; i < G::MPL; ++i) R.w[i] *= is;
