@@ -110,3 +110,29 @@ def test_interp_rejects_unsupported():
         big = torch.zeros((1, 4, 33), dtype=torch.int32, device="cuda")
         ops.interp_fwd(z, z, torch.zeros((1, 4, 64), dtype=torch.bfloat16, device="cuda"), big,
                        torch.ones((1, 4, 33), dtype=torch.uint8, device="cuda"), torch.ones(1, device="cuda"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gather", [False, True], ids=["scatter", "gather"])
+def test_interp_bwd_empty_rows_and_unreferenced_keys(gather):
+    """A row with no valid neighbour contributes nothing, keys no row names keep their
+    accumulated gradient untouched (+= semantics), in both backward forms."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    rng = np.random.default_rng(17)
+    keys = _dev(random_coords(1, 64, 40.0, rng), torch.float32)
+    q = _dev(random_coords(1, 20, 10.0, rng), torch.float32)  # a corner: far keys unreferenced
+    feats = _dev(rng.standard_normal((1, 64, 64)), torch.bfloat16)
+    dout = _dev(rng.standard_normal((1, 20, 64)), torch.bfloat16)
+    idx, valid = ops.knn(q, keys, 4)
+    valid[0, 5] = 0  # an empty row
+    pd = _dev([1.0], torch.float32)
+    df = torch.full((1, 64, 64), 0.25, device="cuda")
+    dq = torch.zeros((1, 20, 2), device="cuda")
+    ops.interp_bwd(q, keys, feats, idx, valid, pd, dout, dfeats=df, dqueries=dq, gather=gather)
+    out = ops.interp_fwd(q, keys, feats, idx, valid, pd)
+    torch.cuda.synchronize()
+    named = set(idx[valid.bool()].cpu().numpy().tolist())
+    untouched = [j for j in range(64) if j not in named]
+    assert untouched and (df[0, untouched] == 0.25).all()
+    assert (dq[0, 5] == 0).all() and (out[0, 5].float() == 0).all()
