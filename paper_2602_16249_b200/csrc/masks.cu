@@ -79,15 +79,21 @@ __device__ __forceinline__ uint64_t desc_key(double v) {
 
 __global__ void __launch_bounds__(kMaskThreads) mask_select_kernel(const double* __restrict__ field, int64_t cells,
                                                                    int64_t want, uint8_t* __restrict__ masked) {
+    constexpr int kCand = 4096;  // candidates kept in shared memory once they fit
     __shared__ uint32_t hist[256];
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_rank;
     __shared__ int32_t wsum[32];
+    __shared__ uint64_t cand[kCand];
+    __shared__ int32_t s_ncand, s_cnt;
+    __shared__ bool s_use;
     const double* f = field + int64_t(blockIdx.x) * cells;
     uint8_t* m = masked + int64_t(blockIdx.x) * cells;
     if (threadIdx.x == 0) {
         s_prefix = 0;
         s_rank = want;  // 1-based rank of the threshold among the keys matching the prefix
+        s_ncand = 0;
+        s_use = false;
     }
     __syncthreads();
     if (want <= 0) {
@@ -101,9 +107,16 @@ __global__ void __launch_bounds__(kMaskThreads) mask_select_kernel(const double*
         for (int i = threadIdx.x; i < 256; i += kMaskThreads) hist[i] = 0;
         __syncthreads();
         const uint64_t pre = s_prefix;
-        for (int64_t i = threadIdx.x; i < cells; i += kMaskThreads) {
-            const uint64_t k = desc_key(f[i]);
-            if ((k & hi_mask) == pre) atomicAdd(&hist[(k >> shift) & 255], 1u);
+        if (s_use) {
+            for (int i = threadIdx.x; i < s_ncand; i += kMaskThreads) {
+                const uint64_t k = cand[i];
+                if ((k & hi_mask) == pre) atomicAdd(&hist[(k >> shift) & 255], 1u);
+            }
+        } else {
+            for (int64_t i = threadIdx.x; i < cells; i += kMaskThreads) {
+                const uint64_t k = desc_key(f[i]);
+                if ((k & hi_mask) == pre) atomicAdd(&hist[(k >> shift) & 255], 1u);
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -115,8 +128,20 @@ __global__ void __launch_bounds__(kMaskThreads) mask_select_kernel(const double*
             }
             s_prefix = pre | (uint64_t(d) << shift);
             s_rank = r;
+            s_cnt = int32_t(hist[d < 256 ? d : 255]);
         }
         __syncthreads();
+        // once the keys under the new prefix fit, keep only them (later passes stop re-reading)
+        if (!s_use && s_cnt <= kCand && pass < 7) {
+            const uint64_t npre = s_prefix, nmask = ~0ull << shift;
+            for (int64_t i = threadIdx.x; i < cells; i += kMaskThreads) {
+                const uint64_t k = desc_key(f[i]);
+                if ((k & nmask) == npre) cand[atomicAdd(&s_ncand, 1)] = k;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_use = true;
+            __syncthreads();
+        }
     }
     const uint64_t T = s_prefix;
     const int64_t take_eq = s_rank;  // equal-to-T cells to take, lowest index first
