@@ -253,6 +253,13 @@ int affmae_attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc
                             const affmae_attn_inputs* in, const affmae_attn_plan* plan, affmae_bf16* out,
                             float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* flop_count_attn / flop_count_attn_dense (include/affmae/attention.hpp:77-79,
+ * src/attention.cpp:360-370): closed-form forward flops of neighbourhood attention,
+ * 4 n (m+1) h d + 6 n (m+1) h, and of dense attention, 4 n^2 h d + 6 n^2 h.  Returns 0
+ * (and sets ConfigError's message) when an argument is not positive. */
+uint64_t affmae_flop_count_attn(int64_t n, int64_t m, int64_t h, int64_t d);
+uint64_t affmae_flop_count_attn_dense(int64_t n, int64_t h, int64_t d);
+
 typedef struct affmae_attn_grads {
     affmae_bf16* dq;  /* [B, N, h*d]  overwritten */
     affmae_bf16* dk;  /* [B, N, h*d]  overwritten */

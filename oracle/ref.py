@@ -274,6 +274,20 @@ def read_aft(path, cap=1 << 24):
     return out[:n.value].copy(), dt.value
 
 
+def load_checkpoint(directory, names, numels):
+    """load_checkpoint (proj/src/pipeline.cpp:772-797) of the named parameters (flat
+    float64 arrays); raises ValueError on the reference's ConfigError."""
+    out = np.empty(int(sum(numels)))
+    arr_names = (C.c_char_p * len(names))(*[n.encode() for n in names])
+    nums = np.asarray(numels, np.int64)
+    _check(lib().ref_load_checkpoint(str(directory).encode(), C.c_int(len(names)), arr_names, _p(nums), _p(out)))
+    res, o = {}, 0
+    for n, z in zip(names, numels):
+        res[n] = out[o:o + z].copy()
+        o += z
+    return res
+
+
 def perlin_mask(grid, ratio, seed):
     m = np.empty(grid * grid, np.uint8)
     _check(lib().ref_perlin_mask(C.c_int64(grid), C.c_double(ratio), C.c_uint64(seed), _p(m)))

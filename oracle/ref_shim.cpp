@@ -438,6 +438,24 @@ int ref_read_aft(const char* path, double* out, int64_t cap, int64_t* numel, int
     });
 }
 
+// load_checkpoint (proj/src/pipeline.cpp:772-797) into a ParamStore of `n` parameters
+// named names[i] with numels[i] elements (1 x numel b32 tensors); values concatenated
+// into out.  Checks that a directory written by our side loads in the reference.
+int ref_load_checkpoint(const char* dir, int n, const char* const* names, const int64_t* numels,
+                        double* out) {
+    return guarded([&] {
+        ParamStore store;
+        for (int i = 0; i < n; ++i) store.add(names[i], Tensor::zeros({1, numels[i]}, Precision::b32));
+        load_checkpoint(dir, store);
+        int64_t o = 0;
+        for (int i = 0; i < n; ++i) {
+            const Tensor& v = store.find(names[i])->value;
+            for (int64_t e = 0; e < v.numel(); ++e) out[o + e] = v.get(e);
+            o += v.numel();
+        }
+    });
+}
+
 // masked [grid*grid] (1 = hidden) from perlin_field(grid, grid, 2, 4.0, 0.5, seed)
 int ref_perlin_mask(int64_t grid, double ratio, uint64_t seed, uint8_t* masked) {
     return guarded([&] {

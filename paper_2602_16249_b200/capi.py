@@ -36,6 +36,7 @@ EXPORTS = (
     "affmae_perlin_mask", "affmae_visible_coords", "affmae_synth_images_workspace", "affmae_synth_images",
     "affmae_patchify", "affmae_masked_rows", "affmae_aft_write", "affmae_aft_read_header",
     "affmae_aft_read", "affmae_checkpoint_save", "affmae_checkpoint_load",
+    "affmae_flop_count_attn", "affmae_flop_count_attn_dense",
 )
 
 
@@ -96,16 +97,15 @@ def lib():
         L.affmae_last_error.restype = C.c_char_p
         L.affmae_retained_count.restype = C.c_int64
         L.affmae_retained_count.argtypes = [C.c_int64, C.c_double]
+        for f in ("affmae_flop_count_attn", "affmae_flop_count_attn_dense"):
+            if hasattr(L, f):
+                getattr(L, f).restype = C.c_uint64
         if hasattr(L, "affmae_adamw_lr"):
             L.affmae_adamw_lr.restype = C.c_double
-        for f in ("affmae_cluster_index_workspace", "affmae_sfc_order_workspace",
-                  "affmae_attn_fwd_workspace", "affmae_attn_plan_workspace",
-                  "affmae_attn_fwd_planned_workspace", "affmae_attn_bwd_planned_workspace",
-                  "affmae_attn_bwd_workspace", "affmae_select_retained_workspace",
-                  "affmae_merge_plan_workspace", "affmae_merge_pool_bwd_workspace",
-                  "affmae_interp_bwd_gather_workspace", "affmae_gattn_bwd_workspace",
-                  "affmae_perlin_mask_workspace", "affmae_synth_images_workspace"):
-            if hasattr(L, f):
+        # every size query returns size_t: without the restype ctypes would truncate it to a
+        # 32-bit int (a >= 2 GiB workspace would come back wrong)
+        for f in EXPORTS:
+            if f.endswith("_workspace") and hasattr(L, f):
                 getattr(L, f).restype = C.c_size_t
         _lib = L
     return _lib
@@ -137,3 +137,19 @@ def geometry(batch: int, tokens: int, cluster: int, groups: int) -> ClusterGeom:
     g = ClusterGeom(batch, tokens, cluster, groups, 0, 0, 0, 0)
     check(lib().affmae_cluster_geometry(C.byref(g)), "cluster_geometry")
     return g
+
+
+def flop_count_attn(n: int, m: int, h: int, d: int) -> int:
+    """flop_count_attn (proj/src/attention.cpp:360-364); ValueError on non-positive args."""
+    r = lib().affmae_flop_count_attn(C.c_int64(n), C.c_int64(m), C.c_int64(h), C.c_int64(d))
+    if r == 0:
+        check(ECONFIG, "flop_count_attn")
+    return int(r)
+
+
+def flop_count_attn_dense(n: int, h: int, d: int) -> int:
+    """flop_count_attn_dense (proj/src/attention.cpp:366-370)."""
+    r = lib().affmae_flop_count_attn_dense(C.c_int64(n), C.c_int64(h), C.c_int64(d))
+    if r == 0:
+        check(ECONFIG, "flop_count_attn_dense")
+    return int(r)

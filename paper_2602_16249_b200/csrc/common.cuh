@@ -33,7 +33,16 @@ int cuda_status(cudaError_t e, const char* where);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// B200 SM count: the compile-time sizing bound of persistent grids and per-CTA partial
+// buffers.  Library calls that take a live SM count (the GEMM's tile scheduler) use
+// device_sms(), which queries the current device.
 constexpr int kNumSMs = 148;
+inline int device_sms() {
+    int dev = 0, n = kNumSMs;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        n = kNumSMs;
+    return n;
+}
 constexpr int kMaxCtasPerGroup = 4 * kNumSMs;  // cap of a persistent grid (sizes per-CTA partials)
 
 // ------------------------------------------------------------ cluster shape

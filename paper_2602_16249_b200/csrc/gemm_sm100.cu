@@ -106,7 +106,7 @@ typename LinearCfg<Act>::Gemm::Arguments linear_args(const void* x, const void* 
     int dev = 0;
     cudaGetDevice(&dev);
     args.hw_info.device_id = dev;
-    args.hw_info.sm_count = kNumSMs;
+    args.hw_info.sm_count = device_sms();
     return args;
 }
 
@@ -147,7 +147,7 @@ int run_linear_gelu_aux(const void* x, const void* w, const float* bias, int m, 
     int dev = 0;
     cudaGetDevice(&dev);
     args.hw_info.device_id = dev;
-    args.hw_info.sm_count = kNumSMs;
+    args.hw_info.sm_count = device_sms();
     C::Gemm gemm;
     if (gemm.can_implement(args) != cutlass::Status::kSuccess)
         return fail(AFFMAE_EUNSUPPORTED, "linear: shape not supported by the tcgen05 kernel");
@@ -232,7 +232,7 @@ typename Cfg::Gemm::Arguments plain_args(const void* a, const void* b, void* c_a
     int dev = 0;
     cudaGetDevice(&dev);
     args.hw_info.device_id = dev;
-    args.hw_info.sm_count = kNumSMs;
+    args.hw_info.sm_count = device_sms();
     return args;
 }
 

@@ -380,7 +380,7 @@ static int launch_nbr(const double2* cent, int64_t batch, const ClusterShape& cs
     switch (cs.g) {
 #define AFFMAE_NBR(G_)                                                                                       \
     case G_: {                                                                                               \
-        if (smem > 48 * 1024)                                                                                \
+        if (smem > 40 * 1024) /* + static shared memory must fit too */                                    \
             AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(nbr_v2_kernel<G_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                                    int(smem)));                                              \
         nbr_v2_kernel<G_><<<grid, kNbrWarps * 32, smem, st>>>(cent, cs, nbr);                                \

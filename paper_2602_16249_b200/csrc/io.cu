@@ -13,6 +13,8 @@
 
 #include <sys/stat.h>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace affmae_b200 {
@@ -33,6 +35,34 @@ uint64_t rd64(const unsigned char* b) {
     uint64_t v = 0;
     for (int i = 0; i < 8; ++i) v |= uint64_t(b[i]) << (8 * i);
     return v;
+}
+
+// product of the extents, false on a negative extent or int64 overflow (payload bytes
+// up to 4 * numel must fit too)
+bool checked_numel(const int64_t* dims, int nd, int64_t* out) {
+    int64_t n = 1;
+    for (int i = 0; i < nd; ++i) {
+        if (dims[i] < 0) return false;
+        if (dims[i] && n > (INT64_MAX / 4) / dims[i]) return false;
+        n *= dims[i];
+    }
+    *out = n;
+    return true;
+}
+
+// create_directories (the reference's save_checkpoint, proj/src/pipeline.cpp:759)
+bool make_dirs(const std::string& path) {
+    std::string cur;
+    size_t pos = 0;
+    while (pos <= path.size()) {
+        size_t nx = path.find('/', pos);
+        if (nx == std::string::npos) nx = path.size();
+        cur = path.substr(0, nx);
+        if (!cur.empty() && ::mkdir(cur.c_str(), 0755) != 0 && errno != EEXIST) return false;
+        pos = nx + 1;
+    }
+    struct stat st;
+    return ::stat(path.c_str(), &st) == 0 && S_ISDIR(st.st_mode);
 }
 
 struct File {
@@ -64,17 +94,21 @@ int aft_write(const char* path, const void* dev_src, const int64_t* dims, int nd
     if (!path || !dims || (ndim > 0 && !dev_src)) return fail(AFFMAE_ECONFIG, "aft_write: null pointer");
     if (ndim < 0 || ndim > 8) return fail(AFFMAE_ECONFIG, "aft_write: ndim must be in [0, 8]");
     if (dtype < 0 || dtype > 2) return fail(AFFMAE_ECONFIG, "aft_write: dtype must be 0, 1 or 2");
-    int64_t numel = 1;
-    for (int i = 0; i < ndim; ++i) {
-        if (dims[i] < 0) return fail(AFFMAE_ECONFIG, "aft_write: negative extent");
-        numel *= dims[i];
-    }
+    int64_t numel = 0;
+    if (!checked_numel(dims, ndim, &numel)) return fail(AFFMAE_ECONFIG, "aft_write: bad extents");
     const size_t bytes = size_t(numel) * (dtype == 2 ? 1 : 4);
     std::vector<unsigned char> host(bytes);
     if (bytes && (cudaMemcpyAsync(host.data(), dev_src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)) !=
                       cudaSuccess ||
                   cudaStreamSynchronize(as_stream(stream)) != cudaSuccess))
         return fail(AFFMAE_ECUDA, "aft_write: D2H failed");
+    // b16emu tensors hold binary16-representable values (round_b16, proj/src/tensor.cpp:167-172):
+    // round the fp32 payload to nearest-even binary16 so the file matches the reference's
+    if (dtype == 1) {
+        float* f = reinterpret_cast<float*>(host.data());
+        for (int64_t i = 0; i < numel; ++i)
+            if (f[i] == f[i]) f[i] = __half2float(__float2half_rn(f[i]));  // NaN passes through (round_b16_scalar)
+    }
     // the payload is little-endian f32 / bytes, which is the device layout (x86-64 / aarch64 hosts)
     return write_file(path, dtype, dims, ndim, host.data(), bytes);
 }
@@ -91,7 +125,11 @@ int aft_read_header(const char* path, int* dtype, int* ndim, int64_t* dims) {
     if (nd > 8) return fail(AFFMAE_ECONFIG, std::string("implausible AFT1 ndim in ") + path);
     unsigned char e[64];
     if (std::fread(e, 1, 8 * nd, in.f) != 8 * nd) return fail(AFFMAE_ECONFIG, std::string("truncated AFT1 file: ") + path);
-    for (uint32_t i = 0; i < nd; ++i) dims[i] = int64_t(rd64(e + 8 * i));
+    for (uint32_t i = 0; i < nd; ++i) {
+        const uint64_t x = rd64(e + 8 * i);
+        if (x > uint64_t(INT64_MAX)) return fail(AFFMAE_ECONFIG, std::string("implausible AFT1 extent in ") + path);
+        dims[i] = int64_t(x);
+    }
     *dtype = b[4];
     *ndim = int(nd);
     return AFFMAE_OK;
@@ -103,13 +141,17 @@ int aft_read(const char* path, float* dev_dst, int64_t capacity, int64_t* numel_
     int64_t dims[8];
     int rc = aft_read_header(path, &dtype, &nd, dims);
     if (rc) return rc;
-    int64_t numel = 1;
-    for (int i = 0; i < nd; ++i) numel *= dims[i];
+    int64_t numel = 0;
+    if (!checked_numel(dims, nd, &numel)) return fail(AFFMAE_ECONFIG, std::string("implausible AFT1 extents in ") + path);
     if (numel > capacity) return fail(AFFMAE_ECONFIG, std::string("aft_read: destination too small for ") + path);
     if (numel > 0 && !dev_dst) return fail(AFFMAE_ECONFIG, "aft_read: null destination");
     File in(path, "rb");
-    if (!in.f || std::fseek(in.f, long(9 + 8 * nd), SEEK_SET) != 0)
-        return fail(AFFMAE_ECONFIG, std::string("cannot open: ") + path);
+    if (!in.f || std::fseek(in.f, 0, SEEK_END) != 0) return fail(AFFMAE_ECONFIG, std::string("cannot open: ") + path);
+    const long fsize = std::ftell(in.f);
+    const int64_t payload = numel * (dtype == 2 ? 1 : 4);
+    if (fsize < 0 || int64_t(fsize) - int64_t(9 + 8 * nd) < payload)
+        return fail(AFFMAE_ECONFIG, std::string("truncated AFT1 file: ") + path);
+    if (std::fseek(in.f, long(9 + 8 * nd), SEEK_SET) != 0) return fail(AFFMAE_ECONFIG, std::string("cannot seek: ") + path);
     std::vector<float> host(static_cast<size_t>(numel));
     if (dtype == 2) {
         std::vector<unsigned char> raw(static_cast<size_t>(numel));
@@ -138,8 +180,7 @@ int checkpoint_save(const char* dir, int n, const char* const* names, const floa
                     const int64_t* const* dims, const int* ndims, const int* precs, void* stream) {
     if (!dir || (n > 0 && (!names || !dev_vals || !dims || !ndims || !precs)))
         return fail(AFFMAE_ECONFIG, "checkpoint_save: null pointer");
-    if (::mkdir(dir, 0755) != 0 && errno != EEXIST)
-        return fail(AFFMAE_ECONFIG, std::string("cannot create checkpoint dir ") + dir);
+    if (!make_dirs(dir)) return fail(AFFMAE_ECONFIG, std::string("cannot create checkpoint dir ") + dir);
     const std::string d(dir);
     std::string manifest;
     static const char* kPrec[3] = {"b32", "b16emu", "b64"};
@@ -196,10 +237,15 @@ int checkpoint_load(const char* dir, int n, const char* const* names, float* con
         for (int i = 0; i < n; ++i)
             if (f[0] == names[i]) which = i;
         if (which < 0) return fail(AFFMAE_ECONFIG, "checkpoint has unknown parameter: " + f[0]);
-        int64_t numel = 0;
-        int rc = aft_read((d + "/" + f[3]).c_str(), dev_vals[which], numels[which], &numel, stream);
+        // size check from the header BEFORE any payload reaches the live parameter
+        int dt = 0, nd = 0;
+        int64_t hd[8], numel = 0;
+        int rc = aft_read_header((d + "/" + f[3]).c_str(), &dt, &nd, hd);
         if (rc) return rc;
-        if (numel != numels[which]) return fail(AFFMAE_ECONFIG, "checkpoint size mismatch for " + f[0]);
+        if (!checked_numel(hd, nd, &numel) || numel != numels[which])
+            return fail(AFFMAE_ECONFIG, "checkpoint size mismatch for " + f[0]);
+        rc = aft_read((d + "/" + f[3]).c_str(), dev_vals[which], numels[which], &numel, stream);
+        if (rc) return rc;
         seen[size_t(which)] = 1;
     }
     for (int i = 0; i < n; ++i)

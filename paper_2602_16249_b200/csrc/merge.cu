@@ -1057,12 +1057,9 @@ int select_retained(const float* scores, int64_t batch, int64_t n, double d_s, i
     cudaStream_t st = as_stream(stream);
     if (n <= kSegSortMax) {
         const size_t smem = size_t(n) * 4;
-        static bool attr = false;
-        if (!attr) {
-            AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(kSegSortMax * 4)));
-            attr = true;
-        }
+        // per-call (the attribute is per device and the call is a cheap host-side set)
+        AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(select_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(kSegSortMax * 4)));
         select_topk_kernel<<<unsigned(batch), kSelWarps * 32, smem, st>>>(scores, n, r, retained);
         AFFMAE_LAUNCH_CHECK("select_topk_kernel");
         return AFFMAE_OK;

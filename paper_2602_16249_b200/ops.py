@@ -8,6 +8,7 @@ is absent the first call raises (there is no CPU fallback).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -699,33 +700,49 @@ class AdamW:
             _stream(stream)), "adamw_step")
         self.t += 1
 
-    def save(self, directory, names, stream=None):
-        """save_checkpoint (proj/src/pipeline.cpp:757-770) of the parameters under `names`, plus
-        the state the reference omits: the moments as "<name>.adam_m" / "<name>.adam_v" entries
-        and the step count as "adamw.step" (AFT1 b32, one value)."""
-        entries = {}
-        offs = [0] + [p.numel() for p in self.params]
-        pos = np.cumsum([(z + 3) // 4 * 4 for z in offs[1:]])
-        for i, (nm, p) in enumerate(zip(names, self.params)):
-            o = int(pos[i - 1]) if i else 0
-            entries[nm] = (p, "b32")
-            entries[nm + ".adam_m"] = (self.m[o:o + p.numel()].view(p.shape), "b32")
-            entries[nm + ".adam_v"] = (self.v[o:o + p.numel()].view(p.shape), "b32")
-        entries["adamw.step"] = (torch.tensor([float(self.t)], device=self.value.device), "b32")
+    def _state_views(self, names):
+        offs, out = 0, []
+        for nm, p in zip(names, self.params):
+            out.append((nm, p, self.m[offs:offs + p.numel()].view(p.shape), self.v[offs:offs + p.numel()].view(p.shape)))
+            offs += (p.numel() + 3) // 4 * 4
+        return out
+
+    def save(self, directory, names, precs=None, stream=None):
+        """save_checkpoint (proj/src/pipeline.cpp:757-770) of the parameters under `names`
+        (precision names per parameter, default "b32"): <dir>/manifest.tsv holds ONLY the
+        parameters, so the reference's load_checkpoint reads the directory unchanged.  The
+        state the reference omits goes to its own checkpoint in <dir>/optim/: the moments as
+        "<name>.m" / "<name>.v" and the step count as "step" (AFT1 b32)."""
+        precs = precs or ["b32"] * len(names)
+        entries, state = {}, {}
+        for (nm, p, m, v), pr in zip(self._state_views(names), precs):
+            entries[nm] = (p, pr)
+            state[nm + ".m"] = (m, "b32")
+            state[nm + ".v"] = (v, "b32")
+        state["step"] = (torch.tensor([float(self.t)], device=self.value.device), "b32")
         save_checkpoint(directory, entries, stream=stream)
+        save_checkpoint(os.path.join(str(directory), "optim"), state, stream=stream)
 
     def load(self, directory, names, stream=None):
-        """load_checkpoint into the parameters, moments and step count written by save()."""
-        entries, offs = {}, 0
-        for nm, p in zip(names, self.params):
+        """load_checkpoint into the parameters; the moments and step count come from
+        <dir>/optim/ when present (written by save()), else the optimizer restarts from zero
+        moments at step 0 -- a plain reference checkpoint loads too."""
+        entries, state = {}, {}
+        for nm, p, m, v in self._state_views(names):
             entries[nm] = p
-            entries[nm + ".adam_m"] = self.m[offs:offs + p.numel()].view(p.shape)
-            entries[nm + ".adam_v"] = self.v[offs:offs + p.numel()].view(p.shape)
-            offs += (p.numel() + 3) // 4 * 4
-        step = torch.zeros(1, device=self.value.device)
-        entries["adamw.step"] = step
+            state[nm + ".m"] = m
+            state[nm + ".v"] = v
         load_checkpoint(directory, entries, stream=stream)
-        self.t = int(step.item())
+        optim_dir = os.path.join(str(directory), "optim")
+        if os.path.exists(os.path.join(optim_dir, "manifest.tsv")):
+            step = torch.zeros(1, device=self.value.device)
+            state["step"] = step
+            load_checkpoint(optim_dir, state, stream=stream)
+            self.t = int(step.item())
+        else:
+            self.m.zero_()
+            self.v.zero_()
+            self.t = 0
 
 
 # -------------------------------------------------------------------- merge

@@ -79,3 +79,28 @@ def test_aft_header_parsing_is_host_only(tmp_path):
         capi.check(L.affmae_aft_read_header(str(tmp_path / "nd.aft").encode(), C.byref(dt), C.byref(nd), dims))
     with pytest.raises(ValueError, match="no checkpoint index"):
         capi.check(L.affmae_checkpoint_load(str(tmp_path / "none").encode(), 0, None, None, None, None))
+
+
+def test_flop_count_attn_golden():
+    """Golden values of proj/tests/test_attention.cpp:193-198."""
+    assert capi.flop_count_attn(4096, 192, 6, 64) == 1242710016
+    assert capi.flop_count_attn(1, 1, 1, 1) == 4 * 2 + 6 * 2
+    assert capi.flop_count_attn_dense(256, 2, 8) == 4 * 256 * 256 * 2 * 8 + 6 * 256 * 256 * 2
+    with pytest.raises(ValueError, match="positive"):
+        capi.flop_count_attn(0, 48, 4, 32)
+
+
+def test_malformed_aft1_is_a_config_error(tmp_path):
+    """Extents whose product overflows int64 (or exceeds INT64_MAX) are rejected with
+    ConfigError before any allocation, instead of aborting the host process."""
+    import struct
+    L = capi.lib()
+    for dims in ([1 << 62, 4], [1 << 63, 1], [3, 5]):
+        p = tmp_path / "bad.aft"
+        p.write_bytes(b"AFT1" + bytes([0]) + struct.pack("<I", len(dims)) +
+                      b"".join(struct.pack("<Q", d) for d in dims))
+        rc = L.affmae_aft_read(str(p).encode(), None, C.c_int64(1 << 40), None, None)
+        assert rc == capi.ECONFIG, dims
+        msg = L.affmae_last_error().decode()
+        if dims[0] > 3:
+            assert "implausible" in msg, msg

@@ -59,11 +59,12 @@ def _attn(L, use_cuda, n, heads, d, hidden, coords, ins, w):
     return out, grads
 
 
-def test_attention_custom_op_on_reference_tape():
+@pytest.mark.parametrize("grid,heads", [(64, 2), (128, 4)], ids=["g64_D64", "g128_D128"])
+def test_attention_custom_op_on_reference_tape(grid, heads):
     L = _lib()
-    rng = np.random.default_rng(11)
-    coords = inputs.lattice_batch(1, 64, 0.75, 8, seed0=21)[0]
-    n, heads, d, hidden = len(coords), 2, 32, 8
+    rng = np.random.default_rng(11 + grid)
+    coords = inputs.lattice_batch(1, grid, 0.75, 8, seed0=21)[0]
+    n, d, hidden = len(coords), 32, 8
     bf = lambda *s: inputs.bf16_round(0.5 * rng.standard_normal(s).astype(np.float32)).astype(np.float64)
     b = inputs.bias_params(heads, hidden, rng)
     ins = [bf(n, heads * d), bf(n, heads * d), bf(n, heads * d), bf(heads, d), bf(heads, d)] + \
@@ -77,11 +78,12 @@ def test_attention_custom_op_on_reference_tape():
     assert all(e <= 1e-2 for e in errs.values()), errs
 
 
-def test_merge_custom_op_on_reference_tape():
+@pytest.mark.parametrize("grid,dim", [(64, 32), (128, 128)], ids=["g64_D32", "g128_D128"])
+def test_merge_custom_op_on_reference_tape(grid, dim):
     L = _lib()
-    rng = np.random.default_rng(5)
-    coords = inputs.lattice_batch(1, 64, 0.75, 8, seed0=4)[0]
-    n, dim, k_m, d_s, p = len(coords), 32, 8, 0.4, 1.2
+    rng = np.random.default_rng(5 + grid)
+    coords = inputs.lattice_batch(1, grid, 0.75, 8, seed0=4)[0]
+    n, k_m, d_s, p = len(coords), 8, 0.4, 1.2
     feats = inputs.bf16_round(rng.standard_normal((n, dim)).astype(np.float32)).astype(np.float64)
     scores = rng.uniform(0.1, 0.9, n).astype(np.float32).astype(np.float64)
     R = int(np.floor(d_s * n + 0.5))

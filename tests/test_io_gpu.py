@@ -118,6 +118,11 @@ def test_adamw_checkpoint_resumes_bit_identically(tmp_path):
         p.copy_(torch.as_tensor(rng.standard_normal(tuple(p.shape)), dtype=torch.float32))
     run(a, 3)
     a.save(str(tmp_path / "ck"), names)
+    # the parameter manifest stays loadable by the reference (optimizer state lives in optim/)
+    if ref.available():
+        got = ref.load_checkpoint(str(tmp_path / "ck"), names, [p.numel() for p in a.params])
+        for nm, p in zip(names, a.params):
+            np.testing.assert_array_equal(got[nm], p.cpu().numpy().ravel().astype(np.float64))
     b = ops.AdamW(shapes, warmup=2, total_steps=10)
     b.load(str(tmp_path / "ck"), names)
     assert b.t == 3 and torch.equal(b.value, a.value) and torch.equal(b.m, a.m) and torch.equal(b.v, a.v)
@@ -128,3 +133,25 @@ def test_adamw_checkpoint_resumes_bit_identically(tmp_path):
         opt.step()
     torch.cuda.synchronize()
     assert torch.equal(a.value, b.value)
+
+
+def test_adamw_loads_plain_reference_checkpoint(tmp_path):
+    """A checkpoint without optimizer state (the reference's save_checkpoint layout) loads
+    into AdamW: parameters restored, moments zero, step 0."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    shapes, names = [(4, 3), (3,)], ["w", "b"]
+    vals = [np.arange(12, dtype=np.float64).reshape(4, 3) / 7, np.array([0.5, -1.0, 2.0])]
+    d = tmp_path / "plain"
+    d.mkdir()
+    with open(d / "manifest.tsv", "w") as f:
+        for nm, v in zip(names, vals):
+            ref.write_aft(str(d / f"{nm}.aft"), v)
+            f.write(f"{nm}\t{'x'.join(map(str, v.shape))}\tb32\t{nm}.aft\n")
+    a = ops.AdamW(shapes)
+    a.m.fill_(3.0)
+    a.t = 5
+    a.load(str(d), names)
+    assert a.t == 0 and float(a.m.abs().sum()) == 0.0
+    for p, v in zip(a.params, vals):
+        np.testing.assert_array_equal(p.cpu().numpy(), v.astype(np.float32))

@@ -1,0 +1,90 @@
+"""Small-shape run of every hand-written kernel family, for compute-sanitizer
+(racecheck / synccheck / memcheck / initcheck).  Usage (GPU box):
+
+    PYTORCH_NO_CUDA_MEMORY_CACHING=1 compute-sanitizer --tool racecheck \
+        python tools/sanitize_probe.py
+
+Shapes are chosen to reach the interesting code paths while staying small:
+the clustered DSMEM segment sort (several images over CTA clusters), the lattice
+fast and general attention kernels (cp.async rings, the bias-table RMW and its
+duplicate-coordinate atomic fallback), the radix select, merge plan and the
+staged pool kernels, masks, interpolation and decoder attention.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_16249_b200 import inputs, ops  # noqa: E402
+
+
+def dev(a, dt):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device="cuda")
+
+
+def attn_round(coords, heads, hd, rng):
+    B, N, _ = coords.shape
+    bf = torch.bfloat16
+    r = lambda *s: dev(0.5 * rng.standard_normal(s), bf)
+    q, k, v, bk, bv = r(B, N, heads * hd), r(B, N, heads * hd), r(B, N, heads * hd), r(heads, hd), r(heads, hd)
+    c = dev(coords, torch.float32)
+    geom = ops.geometry(B, N, 16, 3)
+    index = ops.cluster_index(c, 16, 3)
+    bias = ops.BiasNet.from_numpy(inputs.bias_params(heads, 8, rng))
+    plan = ops.attn_plan(geom, c, index, heads, hd, 8)
+    o, l = ops.attn_fwd(geom, q, k, v, bk, bv, c, None, None, bias, heads, hd, plan=plan)
+    ops.attn_bwd(geom, q, k, v, bk, bv, c, index, bias, heads, hd, o, l, r(B, N, heads * hd), plan=plan)
+    torch.cuda.synchronize()
+
+
+def main():
+    rng = np.random.default_rng(0)
+    which = sys.argv[1:] or ["index", "attn", "merge", "masks", "decoder"]
+    lat = inputs.lattice_batch(3, 48, 0.75, 8, 1000)  # N = 576, 3 images
+    if "index" in which:
+        ops.cluster_index(dev(lat, torch.float32), 16, 3)
+        ops.cluster_index(dev(rng.uniform(0, 300, (6, 3000, 2)), torch.float32), 16, 3)
+        ops.knn(dev(rng.uniform(0, 50, (2, 1500, 2)), torch.float32),
+                dev(rng.uniform(0, 50, (2, 800, 2)), torch.float32), 8)
+        torch.cuda.synchronize()
+        print("index ok", flush=True)
+    if "attn" in which:
+        attn_round(lat, 4, 32, rng)
+        attn_round(rng.uniform(0, 120, (2, 400, 2)).astype(np.float32), 2, 32, rng)
+        dup = lat.copy()
+        dup[:, 1::2] = dup[:, 0::2]
+        attn_round(dup, 2, 32, rng)
+        print("attention ok", flush=True)
+    if "merge" in which:
+        n = lat.shape[1]
+        s = dev(rng.uniform(0.1, 0.9, (3, n)), torch.float32)
+        ret = ops.select_retained(s, 0.4)
+        plan = ops.merge_plan(dev(lat, torch.float32), ret, 8)
+        f = dev(rng.standard_normal((3, n, 128)), torch.bfloat16)
+        p = dev([1.0], torch.float32)
+        out = ops.merge_pool_fwd(f, s, p, plan)
+        ops.merge_pool_bwd(f, s, p, plan, torch.randn_like(out))
+        torch.cuda.synchronize()
+        print("merge ok", flush=True)
+    if "masks" in which:
+        m = ops.perlin_masks([11, 12], 40, 0.75)
+        ops.visible_coords(m)
+        ops.synth_images([400, 401], 64)
+        torch.cuda.synchronize()
+        print("masks ok", flush=True)
+    if "decoder" in which:
+        keys = dev(lat, torch.float32)
+        qs = dev(rng.uniform(0, 384, (3, 300, 2)), torch.float32)
+        idx, valid = ops.knn(qs, keys, 8)
+        f = dev(rng.standard_normal((3, lat.shape[1], 128)), torch.bfloat16)
+        p = dev([1.0], torch.float32)
+        out = ops.interp_fwd(qs, keys, f, idx, valid, p)
+        ops.interp_bwd(qs, keys, f, idx, valid, p, torch.randn_like(out))
+        torch.cuda.synchronize()
+        print("decoder ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
