@@ -407,6 +407,100 @@ int affmae_merge_pool_bwd(const affmae_bf16* feats, const float* scores, const f
                           const affmae_bf16* dout, affmae_bf16* dfeats, float* dscores,
                           float* dp, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Device-resident training step (SURVEY.md §8(a) Model::encode stage loop, §8(f) #1-#3):
+ * Model::encode / decode / deep_sup / loss_parts (src/pipeline.cpp:402-610), the Tape's
+ * reverse sweep over them (src/tape.cpp:466-724) and AdamW (src/pipeline.cpp:639-680) over a
+ * batch of images, every op on this library's kernels.  Parameters are fp32 masters (the
+ * reference's b32 tape) with bf16 shadows for the tensor-core GEMMs; activations bf16 with an
+ * fp32 residual stream.  Batched semantics: the loss is the mean over the batch of the
+ * reference's per-image loss, so B = 1 is the reference's step.
+ * ---------------------------------------------------------------------- */
+typedef struct affmae_stage_cfg {   /* StageConfig (include/affmae/config.hpp:9-17) */
+    int64_t dim;
+    int heads;
+    int blocks;
+    int64_t cluster;
+    int groups;
+    double d_s;
+    int interp_k;
+} affmae_stage_cfg;
+
+#define AFFMAE_MAX_STAGES 8
+typedef struct affmae_model_cfg {   /* PipelineConfig (include/affmae/config.hpp:35-52) */
+    int64_t image, patch;
+    int n_stages;
+    affmae_stage_cfg stages[AFFMAE_MAX_STAGES];
+    int64_t dec_dim;                /* DecoderConfig */
+    int dec_depth, dec_heads, gather_k, self_k;
+    double lambda_aux;
+    int mask_strategy;              /* 0 = "perlin", 1 = "random" */
+    double mask_ratio;
+    affmae_adamw_cfg optim;         /* OptimConfig + the trainer's total step count */
+    uint64_t seed;
+    int bias_hidden, scorer_hidden, merge_k;
+    int64_t batch;                  /* images per step on this device */
+} affmae_model_cfg;
+
+typedef struct affmae_model affmae_model;   /* opaque: parameters, optimizer state, activations */
+
+typedef struct affmae_model_info {
+    int n_params;          /* parameter tensors (ParamStore order) */
+    int64_t n_values;      /* their total element count */
+    int64_t tokens[AFFMAE_MAX_STAGES];  /* visible tokens per image entering each stage */
+    int64_t masked;        /* masked cells per image (decoder queries) */
+    int64_t device_bytes;  /* device memory held by the model */
+    int64_t steps_taken;   /* AdamW::steps_taken */
+} affmae_model_info;
+
+/* Model(cfg) (src/pipeline.cpp:255-371): validates (ConfigError cases of
+ * PipelineConfig::validate, src/config.cpp:37-66, plus the compiled kernel variants) and
+ * initialises the parameters exactly as the reference (same splitmix64 draws, fp32). */
+int affmae_model_create(const affmae_model_cfg* cfg, affmae_model** out);
+void affmae_model_destroy(affmae_model* m);
+int affmae_model_get_info(const affmae_model* m, affmae_model_info* info);
+/* parameter i: reference name and dims (rows x cols, the reference's layout) */
+const char* affmae_model_param_name(const affmae_model* m, int i);
+int affmae_model_param_dims(const affmae_model* m, int i, int64_t* rows, int64_t* cols);
+/* all parameters (or their gradients) concatenated in ParamStore order, reference layout,
+ * HOST fp32 buffers of n_values (synchronous) */
+int affmae_model_get_params(affmae_model* m, float* host);
+int affmae_model_set_params(affmae_model* m, const float* host);
+int affmae_model_get_grads(affmae_model* m, float* host);
+/* Model-owned device input buffers (stable addresses, so a captured step graph can replay):
+ * images [B, image, image] float64 (synth_image layout), masked [B, g, g] uint8 (1 = hidden). */
+int affmae_model_inputs(affmae_model* m, double** images, uint8_t** masked);
+/* Model::make_mask (src/pipeline.cpp:625-637) of B images from seeds_host [B] into the
+ * model's mask buffer (perlin: device kernel, bit-exact; random: host shuffle). */
+int affmae_model_make_masks(affmae_model* m, const uint64_t* seeds_host, void* stream);
+/* zero_grads + encode + decode + deep_sup + loss_parts + Tape::backward on the model's
+ * input buffers; gradients of the batch-mean loss left in the model.  loss3 (device fp32
+ * [3] or NULL) receives {total, main, aux}. */
+int affmae_model_forward_backward(affmae_model* m, float* loss3, void* stream);
+/* AdamW::step over every parameter (src/pipeline.cpp:650-680) + bf16 shadow refresh */
+int affmae_model_apply_step(affmae_model* m, void* stream);
+/* forward_backward + apply_step; with use_graph the whole step is captured into a CUDA
+ * graph on the first call and replayed afterwards */
+int affmae_model_train_step(affmae_model* m, float* loss3, int use_graph, void* stream);
+/* after forward_backward: stage s's entering coordinates [B, N_s, 2], its features before
+ * the merge (EncodeStage::coords / ::feats, include/affmae/pipeline.hpp:57-62) [B, N_s, D_s]
+ * and its merge scores [B, N_s] (stages with a merge), copied to HOST fp32 buffers
+ * (synchronous; any pointer may be NULL) */
+int affmae_model_stage_output(affmae_model* m, int stage, float* coords_host, float* feats_host,
+                              float* scores_host);
+/* Parity-test hook (teacher forcing): stage s's merge uses retained_host [B, R_s] (ascending
+ * token indices, e.g. the reference's retained set) instead of select_retained on the device
+ * scores; NULL restores the model's own selection.  Everything else is unchanged. */
+int affmae_model_force_retained(affmae_model* m, int stage, const int32_t* retained_host);
+/* flat fp32 gradient arena on the device (for the data-parallel all-reduce between
+ * forward_backward and apply_step) */
+int affmae_model_grad_buffer(affmae_model* m, float** grad, int64_t* n);
+/* save_checkpoint / load_checkpoint (src/pipeline.cpp:757-797): <dir>/manifest.tsv holds
+ * the parameters only (the reference loads it unchanged); the AdamW moments and step go to
+ * <dir>/optim/ (absent -> the optimizer restarts). */
+int affmae_model_save(affmae_model* m, const char* dir);
+int affmae_model_load(affmae_model* m, const char* dir);
+
 #ifdef __cplusplus
 }
 #endif

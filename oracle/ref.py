@@ -309,3 +309,90 @@ def hotpath_batch(images, threads, stages, coords, q, k, v, dout, scores, bk, bv
                                    C.c_int64(groups), C.c_double(d_s), C.c_int(k_m),
                                    *[_p(a) for a in arrs], C.c_double(p), C.byref(cs)))
     return cs.value
+
+
+class RefModel:
+    """The reference Model (proj/src/pipeline.cpp:255-746) through ref_shim.cpp, built from the
+    same affmae_model_cfg struct the device model takes (paper_2602_16249_b200.model.ModelCfg)."""
+
+    def __init__(self, cfg_struct):
+        L = lib()
+        L.ref_model_create.restype = C.c_void_p
+        L.ref_model_param_name.restype = C.c_char_p
+        L.ref_model_param_numel.restype = C.c_int64
+        for f in ("ref_model_destroy", "ref_model_param_count", "ref_model_param_name", "ref_model_param_numel",
+                  "ref_model_get", "ref_model_set", "ref_model_fwd_bwd", "ref_model_train", "ref_model_make_mask"):
+            getattr(L, f).argtypes = None
+        self._cs = cfg_struct
+        self.h = C.c_void_p(L.ref_model_create(C.byref(cfg_struct)))
+        if not self.h.value:
+            raise ValueError(L.ref_last_error().decode())
+        n = L.ref_model_param_count(self.h)
+        self.names = [L.ref_model_param_name(self.h, C.c_int(i)).decode() for i in range(n)]
+        self.numel = [int(L.ref_model_param_numel(self.h, C.c_int(i))) for i in range(n)]
+
+    def __del__(self):
+        try:
+            lib().ref_model_destroy(self.h)
+        except Exception:
+            pass
+
+    def _get(self, which):
+        out = np.empty(int(sum(self.numel)))
+        _check(lib().ref_model_get(self.h, C.c_int(which), _p(out)))
+        res, o = {}, 0
+        for n, z in zip(self.names, self.numel):
+            res[n] = out[o:o + z].copy()
+            o += z
+        return res
+
+    def params(self):
+        return self._get(0)
+
+    def grads(self):
+        return self._get(1)
+
+    def set_params(self, values):
+        flat = np.concatenate([np.asarray(values[n], np.float64).ravel() for n in self.names])
+        _check(lib().ref_model_set(self.h, _p(flat)))
+
+    def fwd_bwd(self, image, masked, tokens_per_stage, dims):
+        """-> ((total, main, aux), [coords of each stage], [stage features (pre-merge)]);
+        the gradients are left in the model."""
+        image = _f64(image)
+        masked = np.ascontiguousarray(masked, np.uint8)
+        loss = np.zeros(3)
+        coords = np.zeros(int(sum(tokens_per_stage)) * 2, np.float32)
+        feats = np.zeros(int(sum(n * d for n, d in zip(tokens_per_stage, dims))))
+        _check(lib().ref_model_fwd_bwd(self.h, _p(image), C.c_int64(image.shape[0]), _p(masked), _p(loss),
+                                       _p(coords), _p(feats)))
+        co, fo, a, b = [], [], 0, 0
+        for n, d in zip(tokens_per_stage, dims):
+            co.append(coords[a:a + 2 * n].reshape(n, 2))
+            fo.append(feats[b:b + n * d].reshape(n, d))
+            a += 2 * n
+            b += n * d
+        return tuple(loss), co, fo
+
+    def train(self, steps, images):
+        images = _f64(images)
+        losses = np.zeros(steps)
+        _check(lib().ref_model_train(self.h, C.c_int64(steps), C.c_int64(images.shape[0]), _p(images),
+                                     C.c_int64(images.shape[1]), _p(losses)))
+        return losses
+
+    def make_mask(self, seed):
+        g = self._cs.image // self._cs.patch
+        m = np.zeros(g * g, np.uint8)
+        _check(lib().ref_model_make_mask(self.h, C.c_uint64(seed), _p(m)))
+        return m.reshape(g, g)
+
+
+
+def model_train_threads(cfg_struct, threads, images_per_thread, image):
+    image = _f64(image)
+    cs = C.c_double()
+    lib().ref_model_train_threads.argtypes = None
+    _check(lib().ref_model_train_threads(C.byref(cfg_struct), C.c_int(threads), C.c_int64(images_per_thread),
+                                         _p(image), C.c_int64(image.shape[0]), C.byref(cs)))
+    return cs.value

@@ -456,6 +456,193 @@ int ref_load_checkpoint(const char* dir, int n, const char* const* names, const 
     });
 }
 
+// ---- the reference Model (proj/src/pipeline.cpp) for the training-step parity tests.
+// Mirrors affmae_model_cfg (include/affmae_b200.h) field for field (plain C layout).
+struct RefStageCfg {
+    int64_t dim;
+    int heads;
+    int blocks;
+    int64_t cluster;
+    int groups;
+    double d_s;
+    int interp_k;
+};
+struct RefAdamCfg {
+    double lr;
+    int64_t warmup;
+    double weight_decay, beta1, beta2;
+    int64_t total_steps;
+};
+struct RefModelCfg {
+    int64_t image, patch;
+    int n_stages;
+    RefStageCfg stages[8];
+    int64_t dec_dim;
+    int dec_depth, dec_heads, gather_k, self_k;
+    double lambda_aux;
+    int mask_strategy;
+    double mask_ratio;
+    RefAdamCfg optim;
+    uint64_t seed;
+    int bias_hidden, scorer_hidden, merge_k;
+    int64_t batch;
+};
+
+static PipelineConfig to_pipeline(const RefModelCfg& c) {
+    PipelineConfig p;
+    p.image = c.image;
+    p.patch = c.patch;
+    for (int s = 0; s < c.n_stages; ++s) {
+        StageConfig st;
+        st.dim = c.stages[s].dim;
+        st.heads = c.stages[s].heads;
+        st.blocks = c.stages[s].blocks;
+        st.cluster = c.stages[s].cluster;
+        st.groups = c.stages[s].groups;
+        st.d_s = c.stages[s].d_s;
+        st.interp_k = c.stages[s].interp_k;
+        p.stages.push_back(st);
+    }
+    p.decoder.dim = c.dec_dim;
+    p.decoder.depth = c.dec_depth;
+    p.decoder.heads = c.dec_heads;
+    p.decoder.gather_k = c.gather_k;
+    p.decoder.self_k = c.self_k;
+    p.lambda_aux = c.lambda_aux;
+    p.mask_strategy = c.mask_strategy == 0 ? "perlin" : "random";
+    p.mask_ratio = c.mask_ratio;
+    p.optim.lr = c.optim.lr;
+    p.optim.warmup = c.optim.warmup;
+    p.optim.weight_decay = c.optim.weight_decay;
+    p.optim.beta1 = c.optim.beta1;
+    p.optim.beta2 = c.optim.beta2;
+    p.seed = c.seed;
+    p.bias_hidden = c.bias_hidden;
+    p.scorer_hidden = c.scorer_hidden;
+    p.merge_k = c.merge_k;
+    return p;
+}
+
+void* ref_model_create(const RefModelCfg* cfg) {
+    Model* m = nullptr;
+    int rc = guarded([&] { m = new Model(to_pipeline(*cfg)); });
+    return rc ? nullptr : m;
+}
+void ref_model_destroy(void* h) { delete static_cast<Model*>(h); }
+int ref_model_param_count(void* h) { return int(static_cast<Model*>(h)->params().size()); }
+const char* ref_model_param_name(void* h, int i) { return static_cast<Model*>(h)->params().all()[size_t(i)]->name.c_str(); }
+int64_t ref_model_param_numel(void* h, int i) { return static_cast<Model*>(h)->params().all()[size_t(i)]->value.numel(); }
+int ref_model_get(void* h, int which, double* out) {  // 0 values, 1 grads
+    return guarded([&] {
+        int64_t o = 0;
+        for (Parameter* p : static_cast<Model*>(h)->params().all()) {
+            const Tensor& t = which ? p->grad : p->value;
+            for (int64_t i = 0; i < p->value.numel(); ++i) out[o + i] = which && t.numel() == 0 ? 0.0 : t.get(i);
+            o += p->value.numel();
+        }
+    });
+}
+int ref_model_set(void* h, const double* in) {
+    return guarded([&] {
+        int64_t o = 0;
+        for (Parameter* p : static_cast<Model*>(h)->params().all()) {
+            for (int64_t i = 0; i < p->value.numel(); ++i) p->value.set(i, in[o + i]);
+            o += p->value.numel();
+        }
+    });
+}
+
+// One image: encode + decode + deep_sup + loss_parts + backward (the body of train(),
+// pipeline.cpp:702-727, without the optimizer).  image [S*S] (b64 like synth_image),
+// masked [g*g] (1 = hidden).  loss3 = {total, main, aux}; coords_out receives every
+// stage's entering coordinates concatenated (N_s x 2 each).
+int ref_model_fwd_bwd(void* h, const double* image, int64_t size, const uint8_t* masked, double* loss3,
+                      float* coords_out, double* feats_out) {
+    return guarded([&] {
+        Model& m = *static_cast<Model*>(h);
+        Tensor img = Tensor::zeros({size, size}, Precision::b64);
+        for (int64_t i = 0; i < img.numel(); ++i) img.set(i, image[i]);
+        MaskSpec mask;
+        mask.hp = mask.wp = size / m.config().patch;
+        mask.patch = m.config().patch;
+        mask.ratio = m.config().mask_ratio;
+        mask.masked.assign(masked, masked + mask.hp * mask.wp);
+        Tape t(m.precision());
+        EncodeResult enc = m.encode(t, img, mask);
+        int recon = m.decode(t, enc, mask);
+        std::vector<int> aux;
+        if (m.config().lambda_aux > 0.0) aux = m.deep_sup(t, enc, mask);
+        Model::LossNodes ln = m.loss_parts(t, recon, aux, img, mask);
+        loss3[0] = t.value(ln.total).get(0);
+        loss3[1] = ln.main >= 0 ? t.value(ln.main).get(0) : 0.0;
+        loss3[2] = ln.aux >= 0 ? t.value(ln.aux).get(0) : 0.0;
+        int64_t o = 0;
+        for (const EncodeStage& st : enc.stages)
+            for (int64_t i = 0; i < st.coords.numel(); ++i) coords_out[o++] = float(st.coords.get(i));
+        if (feats_out) {
+            o = 0;
+            for (const EncodeStage& st : enc.stages) {
+                const Tensor& f = t.value(st.feats);
+                for (int64_t i = 0; i < f.numel(); ++i) feats_out[o++] = f.get(i);
+            }
+        }
+        m.params().zero_grads();
+        t.backward(ln.total);
+    });
+}
+
+// train() (pipeline.cpp:682-746) for `steps` steps over `n_images` images; losses [steps]
+int ref_model_train(void* h, int64_t steps, int64_t n_images, const double* images, int64_t size, double* losses) {
+    return guarded([&] {
+        Model& m = *static_cast<Model*>(h);
+        std::vector<Tensor> imgs;
+        for (int64_t k = 0; k < n_images; ++k) {
+            Tensor t = Tensor::zeros({size, size}, Precision::b64);
+            for (int64_t i = 0; i < t.numel(); ++i) t.set(i, images[k * size * size + i]);
+            imgs.push_back(std::move(t));
+        }
+        TrainResult r = train(m, steps, imgs);
+        for (int64_t s = 0; s < steps; ++s) losses[s] = r.log[size_t(s)].loss;
+    });
+}
+
+// mask of Model::make_mask(seed) (pipeline.cpp:625-637)
+int ref_model_make_mask(void* h, uint64_t seed, uint8_t* masked) {
+    return guarded([&] {
+        MaskSpec ms = static_cast<Model*>(h)->make_mask(seed);
+        std::memcpy(masked, ms.masked.data(), ms.masked.size());
+    });
+}
+
+// Multi-core CPU baseline of the pretraining step: `threads` std::threads, each with its own
+// Model replica (Parameter::grad is single-writer), each running train() over
+// its share of `images` one-step images; returns the images processed.
+int ref_model_train_threads(const RefModelCfg* cfg, int threads, int64_t images_per_thread, const double* image,
+                            int64_t size, double* checksum) {
+    return guarded([&] {
+        std::vector<std::thread> pool;
+        std::vector<double> sums(size_t(threads), 0.0);
+        std::atomic<int> err{0};
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    Model m(to_pipeline(*cfg));
+                    Tensor img = Tensor::zeros({size, size}, Precision::b64);
+                    for (int64_t i = 0; i < img.numel(); ++i) img.set(i, image[i]);
+                    TrainResult r = train(m, images_per_thread, {img});
+                    sums[size_t(t)] = r.last_loss;
+                } catch (...) {
+                    err = 1;
+                }
+            });
+        for (auto& th : pool) th.join();
+        if (err) throw std::runtime_error("ref_model_train_threads: a worker failed");
+        double s = 0;
+        for (double v : sums) s += v;
+        *checksum = s;
+    });
+}
+
 // masked [grid*grid] (1 = hidden) from perlin_field(grid, grid, 2, 4.0, 0.5, seed)
 int ref_perlin_mask(int64_t grid, double ratio, uint64_t seed, uint8_t* masked) {
     return guarded([&] {

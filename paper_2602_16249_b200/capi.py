@@ -37,6 +37,11 @@ EXPORTS = (
     "affmae_patchify", "affmae_masked_rows", "affmae_aft_write", "affmae_aft_read_header",
     "affmae_aft_read", "affmae_checkpoint_save", "affmae_checkpoint_load",
     "affmae_flop_count_attn", "affmae_flop_count_attn_dense",
+    "affmae_model_create", "affmae_model_destroy", "affmae_model_get_info", "affmae_model_param_name",
+    "affmae_model_param_dims", "affmae_model_get_params", "affmae_model_set_params", "affmae_model_get_grads",
+    "affmae_model_inputs", "affmae_model_make_masks", "affmae_model_forward_backward", "affmae_model_apply_step",
+    "affmae_model_train_step", "affmae_model_grad_buffer", "affmae_model_save", "affmae_model_load",
+    "affmae_model_stage_output", "affmae_model_force_retained",
 )
 
 

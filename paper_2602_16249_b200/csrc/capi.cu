@@ -8,6 +8,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "internal.h"
 
 namespace affmae_b200 {
 
@@ -24,93 +25,6 @@ int cuda_status(cudaError_t e, const char* where) {
     g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
     return AFFMAE_ECUDA;
 }
-
-// implemented in attention.cu / index.cu / merge.cu
-size_t attn_fwd_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
-size_t attn_bwd_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
-int attn_fwd(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
-             const int32_t*, const int32_t*, affmae_bf16*, float*, void*, size_t, void*);
-int attn_bwd(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
-             const affmae_cluster_index*, const affmae_bf16*, const float*, const affmae_bf16*,
-             affmae_attn_grads*, void*, size_t, void*);
-size_t attn_plan_workspace(const affmae_cluster_geom*, int);
-int attn_plan_build(const affmae_cluster_geom*, const affmae_attn_desc*, const float*,
-                    const affmae_cluster_index*, int, affmae_attn_plan*, void*);
-size_t attn_fwd_planned_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
-size_t attn_bwd_planned_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
-int attn_fwd_planned(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
-                     const affmae_attn_plan*, affmae_bf16*, float*, void*, size_t, void*);
-int attn_bwd_planned(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
-                     const affmae_attn_plan*, const affmae_bf16*, const float*, const affmae_bf16*,
-                     affmae_attn_grads*, void*, size_t, void*);
-size_t cluster_index_workspace(const affmae_cluster_geom*);
-int cluster_index_build(const affmae_cluster_geom*, const float*, affmae_cluster_index*, void*,
-                        size_t, void*);
-size_t sfc_order_workspace(int64_t, int64_t);
-int sfc_order(const float*, int64_t, int64_t, int32_t*, void*, size_t, void*);
-int neighbor_expand(const affmae_cluster_geom*, const int32_t*, const int32_t*, int32_t*, uint8_t*,
-                    void*);
-int knn(const float*, const float*, int64_t, int64_t, int64_t, int64_t, int32_t*, uint8_t*, void*);
-int interp_fwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
-               int64_t, int64_t, const float*, double, void*, void*);
-int interp_bwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
-               int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*);
-int gattn_fwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
-              int64_t, void*, float*, void*);
-int gattn_bwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
-              int64_t, const void*, void*, float*, float*, float*, float*, float*, float*, float*, float*, float*,
-              void*, size_t, void*);
-size_t gattn_bwd_workspace(const affmae_attn_desc*, int64_t, int64_t, int64_t);
-size_t interp_bwd_gather_workspace(int64_t, int64_t, int64_t, int64_t);
-int interp_bwd_gather(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t,
-                      int64_t, int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*,
-                      size_t, void*);
-size_t perlin_mask_workspace(int64_t, int64_t, int64_t, int, double);
-int perlin_mask(const uint64_t*, int64_t, int64_t, int64_t, int, double, double, double, uint8_t*, void*, size_t,
-                void*);
-int visible_coords(const uint8_t*, int64_t, int64_t, int64_t, double, int64_t, float*, int32_t*, void*);
-int aft_write(const char*, const void*, const int64_t*, int, int, void*);
-int aft_read_header(const char*, int*, int*, int64_t*);
-int aft_read(const char*, float*, int64_t, int64_t*, void*);
-int checkpoint_save(const char*, int, const char* const*, const float* const*, const int64_t* const*, const int*,
-                    const int*, void*);
-int checkpoint_load(const char*, int, const char* const*, float* const*, const int64_t*, void*);
-size_t synth_images_workspace(int64_t, int64_t);
-int synth_images(const uint64_t*, int64_t, int64_t, double*, void*, size_t, void*);
-int patchify(const double*, int64_t, int64_t, int64_t, int64_t, float*, void*);
-int masked_rows(const uint8_t*, int64_t, int64_t, int64_t, int32_t*, void*);
-int64_t retained_count_impl(int64_t, double);
-double adamw_lr(const affmae_adamw_cfg*, int64_t);
-size_t linear_workspace(int64_t, int64_t, int64_t);
-int linear_fwd(const void*, const void*, const float*, int64_t, int64_t, int64_t, int, void*, void*, size_t, void*);
-size_t linear_bwd_workspace(int64_t, int64_t, int64_t);
-int linear_fwd_gelu_aux(const void*, const void*, const float*, int64_t, int64_t, int64_t, void*, void*, void*, size_t,
-                        void*);
-int gelu_bwd(const void*, const void*, int64_t, void*, void*);
-int layernorm_fwd(const void*, const float*, const float*, int64_t, int64_t, void*, float*, void*);
-size_t layernorm_bwd_workspace(int64_t, int64_t);
-int norm_clamp_fwd(const void*, int64_t, int64_t, double, void*, void*);
-int norm_clamp_bwd(const void*, const void*, int64_t, int64_t, double, void*, void*);
-size_t masked_mse_workspace(int64_t);
-int masked_mse(const void*, const float*, const int32_t*, int64_t, int64_t, float*, void*, float, void*, size_t, void*);
-int layernorm_bwd(const void*, const float*, const float*, const void*, int64_t, int64_t, void*, float*, float*, void*,
-                  size_t, void*);
-int linear_bwd(const void*, const void*, const void*, int64_t, int64_t, int64_t, void*, float*, float*, void*, size_t,
-               void*);
-int adamw_step(const affmae_adamw_cfg*, int64_t, int64_t, const int64_t*, const uint8_t*, int64_t, float*, const float*,
-               float*, float*, void*);
-size_t select_retained_workspace(int64_t, int64_t);
-int select_retained(const float*, int64_t, int64_t, double, int32_t*, void*, size_t, void*);
-size_t merge_plan_workspace(int64_t, int64_t, int64_t);
-int merge_plan_build(const float*, const int32_t*, int64_t, int64_t, int64_t, int, affmae_merge_plan*,
-                     void*, size_t, void*);
-int merge_pool_fwd(const affmae_bf16*, const float*, const float*, const int32_t*,
-                   const affmae_merge_plan*, int64_t, int64_t, int64_t, int64_t, int, affmae_bf16*,
-                   void*);
-size_t merge_pool_bwd_workspace(int64_t, int64_t);
-int merge_pool_bwd(const affmae_bf16*, const float*, const float*, const int32_t*,
-                   const affmae_merge_plan*, int64_t, int64_t, int64_t, int64_t, int,
-                   const affmae_bf16*, affmae_bf16*, float*, float*, void*, size_t, void*);
 
 }  // namespace affmae_b200
 

@@ -22,6 +22,7 @@
 #include "cutlass/util/packed_stride.hpp"
 
 #include "common.cuh"
+#include "internal.h"
 
 namespace affmae_b200 {
 namespace {
@@ -85,7 +86,7 @@ struct LinearGeluAuxCfg {
 
 template <template <class> class Act>
 typename LinearCfg<Act>::Gemm::Arguments linear_args(const void* x, const void* w, const float* bias, int m, int n,
-                                                     int k, void* y) {
+                                                     int k, void* y, const void* c_add = nullptr) {
     using C = LinearCfg<Act>;
     using StrideA = typename C::Gemm::GemmKernel::StrideA;
     using StrideB = typename C::Gemm::GemmKernel::StrideB;
@@ -99,9 +100,9 @@ typename LinearCfg<Act>::Gemm::Arguments linear_args(const void* x, const void* 
         cutlass::gemm::GemmUniversalMode::kGemm,
         {m, n, k, 1},
         {static_cast<const typename C::ElementA*>(x), sa, static_cast<const typename C::ElementB*>(w), sb},
-        {{}, nullptr, sc, static_cast<typename C::ElementD*>(y), sd}};
+        {{}, static_cast<const typename C::ElementC*>(c_add), sc, static_cast<typename C::ElementD*>(y), sd}};
     args.epilogue.thread.alpha = 1.0f;
-    args.epilogue.thread.beta = 0.0f;
+    args.epilogue.thread.beta = c_add ? 1.0f : 0.0f;
     args.epilogue.thread.bias_ptr = bias;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -112,9 +113,9 @@ typename LinearCfg<Act>::Gemm::Arguments linear_args(const void* x, const void* 
 
 template <template <class> class Act>
 int run_linear(const void* x, const void* w, const float* bias, int m, int n, int k, void* y, void* ws,
-               size_t ws_bytes, cudaStream_t st) {
+               size_t ws_bytes, cudaStream_t st, const void* c_add = nullptr) {
     using G = typename LinearCfg<Act>::Gemm;
-    auto args = linear_args<Act>(x, w, bias, m, n, k, y);
+    auto args = linear_args<Act>(x, w, bias, m, n, k, y, c_add);
     G gemm;
     if (gemm.can_implement(args) != cutlass::Status::kSuccess)
         return fail(AFFMAE_EUNSUPPORTED, "linear: shape not supported by the tcgen05 kernel");
@@ -213,6 +214,9 @@ struct PlainCfg {
 };
 using DxCfg = PlainCfg<cutlass::layout::RowMajor, cutlass::layout::RowMajor, cutlass::bfloat16_t, 8>;
 using DwCfg = PlainCfg<cutlass::layout::ColumnMajor, cutlass::layout::RowMajor, float, 4>;
+// dX = dY W straight into an fp32 buffer with beta (the model's residual-stream gradients:
+// several GEMMs -- q/k/v, the scorer, the decoder's key/value projections -- sum into one dX)
+using DxF32Cfg = PlainCfg<cutlass::layout::RowMajor, cutlass::layout::RowMajor, float, 4>;
 
 template <class Cfg>
 typename Cfg::Gemm::Arguments plain_args(const void* a, const void* b, void* c_and_d, float beta, int m, int n, int k) {
@@ -285,7 +289,7 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
     if (!x || !w || !dy) return fail(AFFMAE_ECONFIG, "linear bwd: null pointer");
     if (m < 1 || n < 1 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
         return fail(AFFMAE_ECONFIG, "linear bwd: bad shape");
-    if (k % 8 || n % 8 || m % 8) return fail(AFFMAE_EUNSUPPORTED, "linear bwd: M, N, K must be multiples of 8");
+    if (k % 8 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "linear bwd: N and K must be multiples of 8");
     if (ws_bytes < linear_bwd_workspace(m, n, k)) return fail(AFFMAE_ECONFIG, "linear bwd: workspace too small");
     cudaStream_t st = as_stream(stream);
     const size_t gws = ws_bytes - size_t(kColsumChunks) * size_t(n) * 4 - 256;
@@ -301,6 +305,26 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
         AFFMAE_LAUNCH_CHECK("linear bwd bias");
     }
     return AFFMAE_OK;
+}
+
+// y = x W^T + b + c (c bf16 [M, N], summed in fp32 before the one rounding to bf16)
+int linear_fwd_add(const void* x, const void* w, const float* bias, int64_t m, int64_t n, int64_t k, const void* c,
+                   void* y, void* ws, size_t ws_bytes, void* stream) {
+    if (!x || !w || !bias || !y || !c) return fail(AFFMAE_ECONFIG, "linear: null pointer");
+    if (m < 1 || n < 1 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return fail(AFFMAE_ECONFIG, "linear: bad shape");
+    if (k % 8 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "linear: K and N must be multiples of 8");
+    return run_linear<cutlass::epilogue::thread::Identity>(x, w, bias, int(m), int(n), int(k), y, ws, ws_bytes,
+                                                           as_stream(stream), c);
+}
+
+int linear_dx_f32(const void* dy, const void* w, int64_t m, int64_t n, int64_t k, float* dx, float beta, void* ws,
+                  size_t ws_bytes, void* stream) {
+    if (!dy || !w || !dx) return fail(AFFMAE_ECONFIG, "linear dx: null pointer");
+    if (m < 1 || n < 1 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return fail(AFFMAE_ECONFIG, "linear dx: bad shape");
+    if (k % 8 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "linear dx: N and K must be multiples of 8");
+    return run_plain<DxF32Cfg>(dy, w, dx, beta, int(m), int(k), int(n), ws, ws_bytes, as_stream(stream));
 }
 
 int linear_fwd_gelu_aux(const void* x, const void* w, const float* bias, int64_t m, int64_t n, int64_t k, void* y,

@@ -85,6 +85,90 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ value, c
     }
 }
 
+// ---- step-count-on-device variant (the training step's CUDA graph replays it unchanged):
+// a one-thread prologue derives the step's scalars from *step (AdamW::t_) in binary64 and
+// advances it; the update kernel also refreshes the bf16 shadow of the first n_shadow
+// values (the tensor-core operands of the model's GEMMs).
+__global__ void adamw_scalars_kernel(affmae_adamw_cfg c, int64_t* __restrict__ step, AdamwF* __restrict__ out) {
+    const int64_t t = *step;
+    double lr;
+    if (t < c.warmup) {
+        lr = c.lr * double(t + 1) / double(c.warmup);
+    } else {
+        const int64_t span = c.total_steps - c.warmup > 1 ? c.total_steps - c.warmup : 1;
+        double prog = double(t - c.warmup) / double(span);
+        prog = prog < 1.0 ? prog : 1.0;
+        lr = c.lr * 0.5 * (1.0 + cos(3.14159265358979323846 * prog));
+    }
+    const double nn = double(t + 1);
+    AdamwF f;
+    f.b1 = float(c.beta1);
+    f.omb1 = float(1.0 - c.beta1);
+    f.b2 = float(c.beta2);
+    f.omb2 = float(1.0 - c.beta2);
+    f.ibc1 = float(1.0 / (1.0 - pow(c.beta1, nn)));
+    f.ibc2 = float(1.0 / (1.0 - pow(c.beta2, nn)));
+    f.eps = 1e-8f;
+    f.lr = float(lr);
+    f.lrwd = float(lr * c.weight_decay);
+    *out = f;
+    *step = t + 1;
+}
+
+__global__ void __launch_bounds__(256) adamw_dev_kernel(float* __restrict__ value, const float* __restrict__ grad,
+                                                        float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                                        const int64_t* __restrict__ off,
+                                                        const uint8_t* __restrict__ decay, int nseg,
+                                                        const AdamwF* __restrict__ sp, __nv_bfloat16* __restrict__ shadow,
+                                                        int64_t n_shadow) {
+    const AdamwF s = *sp;
+    const int64_t nv = n / 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const int64_t e = 4 * i;
+        const bool d0 = seg_decay_of(off, decay, nseg, e), d3 = seg_decay_of(off, decay, nseg, e + 3);
+        float4 x = reinterpret_cast<float4*>(value)[i];
+        const float4 g = __ldg(reinterpret_cast<const float4*>(grad) + i);
+        float4 mm = reinterpret_cast<float4*>(m)[i], vv = reinterpret_cast<float4*>(v)[i];
+        bool dd[4] = {d0, d0, d0, d3};
+        if (d0 != d3) {
+            dd[1] = seg_decay_of(off, decay, nseg, e + 1);
+            dd[2] = seg_decay_of(off, decay, nseg, e + 2);
+        }
+        x.x = adamw_one(x.x, g.x, mm.x, vv.x, dd[0], s);
+        x.y = adamw_one(x.y, g.y, mm.y, vv.y, dd[1], s);
+        x.z = adamw_one(x.z, g.z, mm.z, vv.z, dd[2], s);
+        x.w = adamw_one(x.w, g.w, mm.w, vv.w, dd[3], s);
+        reinterpret_cast<float4*>(value)[i] = x;
+        reinterpret_cast<float4*>(m)[i] = mm;
+        reinterpret_cast<float4*>(v)[i] = vv;
+        if (e < n_shadow) {
+            __nv_bfloat162 h[2] = {__floats2bfloat162_rn(x.x, x.y), __floats2bfloat162_rn(x.z, x.w)};
+            *reinterpret_cast<uint2*>(shadow + e) = *reinterpret_cast<const uint2*>(h);
+        }
+    }
+}
+
+int adamw_step_dev(const affmae_adamw_cfg* c, int64_t* step_dev, void* scalars_dev, int64_t n_segments,
+                   const int64_t* seg_off, const uint8_t* seg_decay, int64_t n, float* value, const float* grad,
+                   float* m, float* v, void* shadow, int64_t n_shadow, void* stream) {
+    if (!c || !step_dev || !scalars_dev || !seg_off || !seg_decay || !value || !grad || !m || !v)
+        return fail(AFFMAE_ECONFIG, "adamw: null pointer");
+    if (c->total_steps < 1) return fail(AFFMAE_ECONFIG, "optimizer needs at least one step");
+    if (n % 4 || n_shadow % 4 || n_shadow > n || (n_shadow && !shadow))
+        return fail(AFFMAE_ECONFIG, "adamw: sizes must be multiples of 4");
+    cudaStream_t st = as_stream(stream);
+    adamw_scalars_kernel<<<1, 1, 0, st>>>(*c, step_dev, static_cast<AdamwF*>(scalars_dev));
+    const int64_t work = n / 4;
+    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8 * kNumSMs)));
+    adamw_dev_kernel<<<blocks, 256, 0, st>>>(value, grad, m, v, n, seg_off, seg_decay, int(n_segments),
+                                             static_cast<const AdamwF*>(scalars_dev),
+                                             static_cast<__nv_bfloat16*>(shadow), n_shadow);
+    AFFMAE_LAUNCH_CHECK("adamw_dev_kernel");
+    return AFFMAE_OK;
+}
+size_t adamw_scalars_bytes() { return sizeof(AdamwF); }
+
 double adamw_lr(const affmae_adamw_cfg* c, int64_t step) {
     if (step < c->warmup) return c->lr * double(step + 1) / double(c->warmup);
     const int64_t span = c->total_steps - c->warmup > 1 ? c->total_steps - c->warmup : 1;
