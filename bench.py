@@ -66,6 +66,10 @@ def parse():
     ap.add_argument("--interp-images", type=int, default=8,
                     help="images of the side measurement of the interpolation op (SURVEY §8(f) #2); 0 = off")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
+    ap.add_argument("--pretrain-batch", type=int, default=32, help="AFFMAE-B 1024^2 images per step (0: skip)")
+    ap.add_argument("--pretrain-steps", type=int, default=5)
+    ap.add_argument("--tiny-batch", type=int, default=64, help="AFF-tiny 224^2 images per step (0: skip)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the same-run oracle check")
     return ap.parse_args()
 
 
@@ -853,6 +857,177 @@ def run_e2e(a, host, dev, geom, h, d, ws, world, dist):
 
 
 # ------------------------------------------------------------- reference
+# ------------------------------------------------------------------ pretraining step
+def model_flops(cfg, tokens, q):
+    """Closed-form flops of one training step per image (BASELINE metric's '% bf16 peak'):
+    GEMMs 2*m*n*k forward and twice that backward (dX, dW); attention flop_count_attn
+    (proj/src/attention.cpp:360-364) forward and 2.5x that backward (SURVEY §8(d):
+    490 D vs 196 D per token)."""
+    from paper_2602_16249_b200 import capi
+    p2, dd = cfg.patch * cfg.patch, cfg.dec_dim
+    gemm, attn = 0, 0
+    st = cfg.stages
+    gemm += 2 * tokens[0] * (p2 + 16) * st[0].dim
+    for s, sc in enumerate(st):
+        n, d = tokens[s], sc.dim
+        c = -(-n // min(sc.cluster, n))
+        width = min(sc.groups, c) * -(-n // c)
+        gemm += sc.blocks * 24 * n * d * d
+        attn += sc.blocks * capi.flop_count_attn(n, width, sc.heads, d // sc.heads)
+        if s + 1 < len(st):
+            gemm += 2 * n * d * 16 + 2 * tokens[s + 1] * 2 * d * st[s + 1].dim
+            gemm += 2 * q * d * p2  # deep-supervision head
+        gemm += 2 * n * (d + 16) * dd  # decoder in-projection + positional MLP
+    gemm += 2 * q * 16 * dd + 2 * q * dd * p2
+    gemm += len(st) * cfg.dec_depth * 24 * q * dd * dd
+    h = cfg.dec_heads
+    attn += len(st) * cfg.dec_depth * (capi.flop_count_attn(q, 1, h, dd // h) +
+                                       capi.flop_count_attn(q, cfg.self_k, h, dd // h))
+    return 3 * gemm + 3.5 * attn, gemm, attn
+
+
+def run_pretrain(cfg, steps, warmup=2, e2e_steps=3, label=""):
+    """One training step of `cfg` (masks -> encode -> decode -> deep supervision -> loss ->
+    backward -> AdamW) through the torch-free model API, captured as one CUDA graph; device
+    img/s, plus e2e img/s with the step's images copied H2D from pinned host memory and the
+    loss read back D2H inside the timed region."""
+    import ctypes as C
+    from paper_2602_16249_b200 import capi, devmem
+    from paper_2602_16249_b200.model import Model, step_mask_seed
+    t0 = time.perf_counter()
+    m = Model(cfg)
+    create_s = time.perf_counter() - t0
+    B = cfg.batch
+    st = devmem.stream_create()
+    L = capi.lib()
+    wsb = L.affmae_synth_images_workspace(C.c_int64(B), C.c_int64(cfg.image))
+    ws = devmem.DeviceBuffer(wsb)
+    seeds = np.arange(400, 400 + B, dtype=np.uint64)
+    capi.check(L.affmae_synth_images(seeds.ctypes.data_as(C.c_void_p), C.c_int64(B), C.c_int64(cfg.image),
+                                     C.c_void_p(m.images_ptr), C.c_void_p(ws.ptr), C.c_size_t(wsb), C.c_void_p(st)))
+    devmem.sync(st)
+    img_bytes = B * cfg.image * cfg.image * 8
+    pinned = devmem.PinnedBuffer((B, cfg.image, cfg.image), np.float64)
+    pinned.array[...] = devmem.d2h(m.images_ptr, (B, cfg.image, cfg.image), np.float64)
+    loss_host = devmem.PinnedBuffer((3,), np.float32)
+    step = [0]
+
+    def one(e2e=False):
+        if e2e:
+            devmem.h2d_async(m.images_ptr, pinned.ptr, img_bytes, st)
+        m.make_masks([step_mask_seed(cfg.seed, step[0] * B + i) for i in range(B)], stream=st)
+        m.train_step(use_graph=True, stream=st, read_loss=False)
+        if e2e:
+            devmem.d2h_async(loss_host.ptr, m._loss_buf().ptr, 12, st)
+        step[0] += 1
+
+    for _ in range(warmup):
+        one()
+    devmem.sync(st)
+    e0, e1 = devmem.Event(), devmem.Event()
+    e0.record(st)
+    for _ in range(steps):
+        one()
+    e1.record(st)
+    e1.synchronize()
+    ms = e0.elapsed_ms(e1) / steps
+    e0.record(st)
+    for _ in range(e2e_steps):
+        one(e2e=True)
+    e1.record(st)
+    e1.synchronize()
+    ms_e2e = e0.elapsed_ms(e1) / e2e_steps
+    loss = devmem.d2h(m._loss_buf().ptr, (3,), np.float32)
+    flops, gemm_f, attn_f = model_flops(cfg, m.tokens, m.masked)
+    peak = load_bf16_peak()
+    tflops = flops * B / (ms * 1e-3) / 1e12
+    out = {"config": label, "image": cfg.image, "batch": B, "params": int(m.n_values),
+           "tokens_per_stage": [int(t) for t in m.tokens], "masked_per_image": int(m.masked),
+           "ms_per_step": ms, "img_s": B / (ms * 1e-3),
+           "e2e": {"img_s": B / (ms_e2e * 1e-3), "ms_per_step": ms_e2e, "h2d_bytes_per_step": img_bytes,
+                   "d2h_bytes_per_step": 12},
+           "flops_per_image": flops, "tflops": tflops, "bf16_peak_tflops": peak,
+           "frac_bf16_peak": tflops / peak, "loss": [float(x) for x in loss],
+           "device_gib": m.device_bytes / 2 ** 30, "create_s": create_s, "cuda_graph": True,
+           "step": "masks + encode + decode + deep sup + loss + backward + AdamW (one graph)"}
+    m.close()
+    pinned.free()
+    loss_host.free()
+    return out
+
+
+def load_bf16_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return 2250.0
+
+
+def ref_pretrain_sample(cfg, threads):
+    """The reference's train() (proj/src/pipeline.cpp:682-746) on all host threads, one Model
+    replica and one one-step image per thread -> img/s."""
+    from oracle import ref
+    img = ref.synth_image(cfg.image, 400)
+    t0 = time.perf_counter()
+    ref.model_train_threads(cfg.c_struct(), threads, 1, img)
+    dt = time.perf_counter() - t0
+    return threads / dt, dt
+
+
+# ------------------------------------------------------------- same-run parity
+def same_run_parity(a):
+    """one image of the timed workload through the same device ops,
+    checked against the oracle in this run: index + selection + merge plan bit-exact,
+    attention output and dQ/dK/dV rel-L2."""
+    import torch
+    from oracle import port
+    from paper_2602_16249_b200 import ops
+    host = make_inputs(argparse.Namespace(**{**vars(a), "batch": 1}), 0)
+    dev = torch.device("cuda")
+    bf = torch.bfloat16
+    t = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)
+    c = host["coords"]
+    N = c.shape[1]
+    h, d = a.heads, a.head_dim
+    geom = ops.geometry(1, N, a.cluster, a.groups)
+    idx = ops.cluster_index(t(c, torch.float32), a.cluster, a.groups)
+    plan = ops.attn_plan(geom, t(c, torch.float32), idx, h, d, a.hidden)
+    bias = ops.BiasNet.from_numpy(host["bias"], device=dev)
+    q, k, v, do = (t(host[n], bf) for n in ("q", "k", "v", "dout"))
+    bk, bv = t(host["bk"], bf), t(host["bv"], bf)
+    out, lse = ops.attn_fwd(geom, q, k, v, bk, bv, t(c, torch.float32), None, None, bias, h, d, plan=plan)
+    g = ops.attn_bwd(geom, q, k, v, bk, bv, t(c, torch.float32), idx, bias, h, d, out, lse, do, plan=plan)
+    ret = ops.select_retained(t(host["scores"], torch.float32), a.d_s)
+    mp = ops.merge_plan(t(c, torch.float32), ret, a.k_m)
+    torch.cuda.synchronize()
+    ci = port.cluster_index(c[0], a.cluster, a.groups)
+    f32 = lambda x: np.asarray(x, np.float32)
+    wo = port.attn_fwd(f32(host["q"][0]), f32(host["k"][0]), f32(host["v"][0]), f32(host["bk"]), f32(host["bv"]),
+                       c[0], ci["idx"], ci["valid"], host["bias"], h, d)
+    wg = port.attn_bwd(f32(host["q"][0]), f32(host["k"][0]), f32(host["v"][0]), f32(host["bk"]), f32(host["bv"]),
+                       c[0], ci["idx"], ci["valid"], host["bias"], h, d, f32(host["dout"][0]), prec=32)
+    r = port.select_retained(np.asarray(host["scores"][0], np.float64), a.d_s)
+    pl = port.merge_plan(c[0], r, a.k_m)
+
+    def rl2(x, y):
+        x, y = np.asarray(x, np.float64).ravel(), np.asarray(y, np.float64).ravel()
+        return float(np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-30))
+    res = {"image": 0, "tokens": int(N),
+           "index_bit_exact": bool(np.array_equal(idx.perm[0].cpu().numpy(), ci["members"]) and
+                                   np.array_equal(idx.nbr_cl[0].cpu().numpy(), ci["nbr_cl"])),
+           "retained_bit_exact": bool(np.array_equal(ret[0].cpu().numpy(), r)),
+           "merge_plan_bit_exact": bool(np.array_equal(mp.pool_idx[0].cpu().numpy(), pl["pool_idx"]) and
+                                        np.array_equal(mp.pool_dist[0].cpu().numpy(), pl["pool_dist"])),
+           "attn_out_rel_l2": rl2(out[0].float().cpu().numpy(), wo)}
+    for n in ("dq", "dk", "dv"):
+        res[f"attn_{n}_rel_l2"] = rl2(getattr(g, n)[0].float().cpu().numpy(), wg[n])
+    res["max_rel_l2"] = max(v for kk, v in res.items() if kk.endswith("rel_l2"))
+    res["pass"] = bool(res["index_bit_exact"] and res["retained_bit_exact"] and res["merge_plan_bit_exact"]
+                       and res["max_rel_l2"] <= 1e-2)
+    return res
+
+
 def ref_sample(a, images, threads):
     """Times oracle/_ref (the unmodified reference, compiled) on `images` images."""
     from oracle import ref
@@ -994,6 +1169,44 @@ def main():
             line["next_ops"]["decoder_attn"] = res["gattn"]
         if res.get("masks"):
             line["next_ops"]["masks"] = res["masks"]
+    # attention tensor flops (flop_count_attn) of the timed step -> fraction of bf16 peak
+    from paper_2602_16249_b200 import capi as _capi
+    width = res.get("width") or a.cluster * a.groups
+    f_fwd = _capi.flop_count_attn(N, width, a.heads, a.head_dim) * B
+    bf16_peak = load_bf16_peak()
+    line["tensor"] = {"attn_fwd_flops_per_step": f_fwd, "attn_bwd_flops_per_step": 2.5 * f_fwd,
+                      "attn_fwd_tflops": f_fwd / (ph["attn_fwd"] * 1e-3) / 1e12,
+                      "attn_bwd_tflops": 2.5 * f_fwd / (ph["attn_bwd"] * 1e-3) / 1e12,
+                      "frac_bf16_peak_fwd_bwd": 3.5 * f_fwd / ((ph["attn_fwd"] + ph["attn_bwd"]) * 1e-3) / 1e12
+                      / bf16_peak, "bf16_peak_tflops": bf16_peak,
+                      "note": "HBM-bound op (AI ~25-31 flop/B, SURVEY §0.6): the roofline object is HBM"}
+    if not a.no_parity and world == 1:
+        try:
+            line["parity"] = same_run_parity(a)
+        except Exception as e:  # pragma: no cover
+            line["parity"] = {"error": str(e)}
+    if world == 1 and (a.pretrain_batch > 0 or a.tiny_batch > 0):
+        from paper_2602_16249_b200.model import aff_tiny, affmae_b
+        pre = {}
+        try:
+            if a.pretrain_batch > 0:
+                pre["affmae_b_1024"] = run_pretrain(affmae_b(image=1024, batch=a.pretrain_batch),
+                                                    a.pretrain_steps, label="AFFMAE-B 1024^2, 75% mask, deep sup")
+            if a.tiny_batch > 0:
+                cfg_t = aff_tiny(batch=a.tiny_batch)
+                pre["aff_tiny_224"] = run_pretrain(cfg_t, a.pretrain_steps, label="AFF-tiny 224^2, 75% mask")
+                if not a.no_cpu_baseline:
+                    from oracle import ref
+                    if ref.available():
+                        th = host_threads()
+                        v, dt = ref_pretrain_sample(cfg_t, th)
+                        pre["aff_tiny_224"]["cpu_reference"] = {
+                            "img_s": v, "cores": th, "kind": "reference",
+                            "sample": f"{th} images, one train() step each on its own Model replica, {dt:.1f} s"}
+                        pre["aff_tiny_224"]["speedup_vs_reference"] = pre["aff_tiny_224"]["img_s"] / v
+        except Exception as e:  # pragma: no cover
+            pre["error"] = str(e)
+        line["pretrain"] = pre
     if not a.no_cpu_baseline and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(a)

@@ -218,16 +218,20 @@ using DwCfg = PlainCfg<cutlass::layout::ColumnMajor, cutlass::layout::RowMajor, 
 // several GEMMs -- q/k/v, the scorer, the decoder's key/value projections -- sum into one dX)
 using DxF32Cfg = PlainCfg<cutlass::layout::RowMajor, cutlass::layout::RowMajor, float, 4>;
 
+// `batches` > 1: L independent GEMMs over consecutive packed [M, K] / [K, N] / [M, N] blocks
+// (the weight gradient's split-K: batch l covers tokens [l c, (l+1) c), packed strides
+// c * M and c * N are exactly the contiguous token chunks of dY and X)
 template <class Cfg>
-typename Cfg::Gemm::Arguments plain_args(const void* a, const void* b, void* c_and_d, float beta, int m, int n, int k) {
+typename Cfg::Gemm::Arguments plain_args(const void* a, const void* b, void* c_and_d, float beta, int m, int n, int k,
+                                         int batches = 1) {
     using K = typename Cfg::Gemm::GemmKernel;
-    auto sa = cutlass::make_cute_packed_stride(typename K::StrideA{}, cute::make_shape(m, k, 1));
-    auto sb = cutlass::make_cute_packed_stride(typename K::StrideB{}, cute::make_shape(n, k, 1));
-    auto sc = cutlass::make_cute_packed_stride(typename K::StrideC{}, cute::make_shape(m, n, 1));
-    auto sd = cutlass::make_cute_packed_stride(typename K::StrideD{}, cute::make_shape(m, n, 1));
+    auto sa = cutlass::make_cute_packed_stride(typename K::StrideA{}, cute::make_shape(m, k, batches));
+    auto sb = cutlass::make_cute_packed_stride(typename K::StrideB{}, cute::make_shape(n, k, batches));
+    auto sc = cutlass::make_cute_packed_stride(typename K::StrideC{}, cute::make_shape(m, n, batches));
+    auto sd = cutlass::make_cute_packed_stride(typename K::StrideD{}, cute::make_shape(m, n, batches));
     typename Cfg::Gemm::Arguments args{
-        cutlass::gemm::GemmUniversalMode::kGemm,
-        {m, n, k, 1},
+        batches > 1 ? cutlass::gemm::GemmUniversalMode::kBatched : cutlass::gemm::GemmUniversalMode::kGemm,
+        {m, n, k, batches},
         {static_cast<const typename Cfg::ElementA*>(a), sa, static_cast<const typename Cfg::ElementB*>(b), sb},
         {{}, static_cast<const typename Cfg::ElementC*>(c_and_d), sc, static_cast<typename Cfg::ElementD*>(c_and_d),
          sd}};
@@ -242,9 +246,9 @@ typename Cfg::Gemm::Arguments plain_args(const void* a, const void* b, void* c_a
 
 template <class Cfg>
 int run_plain(const void* a, const void* b, void* cd, float beta, int m, int n, int k, void* ws, size_t ws_bytes,
-              cudaStream_t st) {
+              cudaStream_t st, int batches = 1) {
     using G = typename Cfg::Gemm;
-    auto args = plain_args<Cfg>(a, b, cd, beta, m, n, k);
+    auto args = plain_args<Cfg>(a, b, cd, beta, m, n, k, batches);
     G gemm;
     if (gemm.can_implement(args) != cutlass::Status::kSuccess)
         return fail(AFFMAE_EUNSUPPORTED, "linear bwd: shape not supported by the tcgen05 kernel");
@@ -256,24 +260,72 @@ int run_plain(const void* a, const void* b, void* cd, float beta, int m, int n, 
     return AFFMAE_OK;
 }
 
-// db[n] += sum_m dY[m, n]: per (column block, row chunk) partials, then a fixed-order sum
-__global__ void colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t m, int64_t n, int64_t rows_per,
-                                      float* __restrict__ part) {
-    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// db[n] += sum_m dY[m, n]: per (256-column block, row chunk) partials -- two columns per
+// thread (bf16x2), 2 x 148 row chunks so even a 64-column bias fills the GPU -- then a
+// fixed-order sum over the chunks
+__global__ void __launch_bounds__(128) colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t m, int64_t n,
+                                                             int64_t rows_per, float* __restrict__ part) {
+    const int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
     if (col >= n) return;
     const int64_t r0 = int64_t(blockIdx.y) * rows_per, r1 = r0 + rows_per < m ? r0 + rows_per : m;
-    float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) s += __bfloat162float(dy[r * n + col]);
-    part[int64_t(blockIdx.y) * n + col] = s;
+    float s0 = 0.f, s1 = 0.f;
+    for (int64_t r = r0; r < r1; ++r) {
+        const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + r * n + col));
+        s0 += v.x;
+        s1 += v.y;
+    }
+    part[int64_t(blockIdx.y) * n + col] = s0;
+    part[int64_t(blockIdx.y) * n + col + 1] = s1;
 }
+// one warp per column: lane-strided partial sums, then a fixed butterfly (deterministic)
 __global__ void colsum_final_kernel(const float* __restrict__ part, int64_t n, int chunks, float* __restrict__ db) {
-    const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (col >= n) return;
     float s = 0.f;
-    for (int c = 0; c < chunks; ++c) s += part[int64_t(c) * n + col];
-    db[col] += s;
+    for (int c = lane; c < chunks; c += 32) s += part[int64_t(c) * n + col];
+    s = warp_sum(s);
+    if (lane == 0) db[col] += s;
 }
-constexpr int kColsumChunks = 64;
+constexpr int kColsumChunks = 2 * kNumSMs;
+
+// dW += sum_l part[l]   (fixed order over l, float4 lanes)
+__global__ void splitk_reduce_kernel(const float4* __restrict__ part, int64_t n4, int parts, float4* __restrict__ dw) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+        float4 s = dw[i];
+        for (int l = 0; l < parts; ++l) {
+            const float4 p = __ldg(part + int64_t(l) * n4 + i);
+            s.x += p.x;
+            s.y += p.y;
+            s.z += p.z;
+            s.w += p.w;
+        }
+        dw[i] = s;
+    }
+}
+
+// Split-K of the weight gradient dW [n, k] = dY^T X over m tokens: its output has few 256 x 256
+// tiles (one for a 256 x 256 weight) while K = m is the whole batch, so one data-parallel GEMM
+// would occupy 2 of the 148 SMs.  L token chunks of c tokens run as one batched GEMM into
+// fp32 partials (+ one GEMM for the remainder), reduced into dW in a fixed order.
+struct SplitK {
+    int L;      // full chunks
+    int64_t c;  // tokens per chunk (multiple of 64)
+    int64_t rem;
+};
+SplitK splitk_plan(int64_t m, int64_t n, int64_t k) {
+    const int64_t tiles = ((n + 255) / 256) * ((k + 255) / 256);
+    const int64_t clusters = kNumSMs / 2;
+    int64_t L = clusters / tiles;
+    L = std::min<int64_t>(L, m / 512);
+    if (L < 2) return SplitK{1, m, 0};
+    const int64_t c = (m / L) / 64 * 64;
+    return SplitK{int(L), c, m - L * c};
+}
+size_t splitk_part_bytes(int64_t m, int64_t n, int64_t k) {
+    const SplitK p = splitk_plan(m, n, k);
+    return p.L < 2 ? 0 : (size_t(p.L) + 1) * size_t(n) * size_t(k) * 4 + 256;
+}
 
 }  // namespace
 
@@ -281,7 +333,7 @@ size_t linear_bwd_workspace(int64_t m, int64_t n, int64_t k) {
     auto a = plain_args<DxCfg>(nullptr, nullptr, nullptr, 0.f, int(m), int(k), int(n));
     auto b = plain_args<DwCfg>(nullptr, nullptr, nullptr, 1.f, int(n), int(k), int(m));
     const size_t wa = DxCfg::Gemm::get_workspace_size(a), wb = DwCfg::Gemm::get_workspace_size(b);
-    return (wa > wb ? wa : wb) + 256 + size_t(kColsumChunks) * size_t(n) * 4 + 256;
+    return (wa > wb ? wa : wb) + 256 + size_t(kColsumChunks) * size_t(n) * 4 + 256 + splitk_part_bytes(m, n, k);
 }
 
 int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t n, int64_t k, void* dx, float* dw,
@@ -292,16 +344,40 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
     if (k % 8 || n % 8) return fail(AFFMAE_EUNSUPPORTED, "linear bwd: N and K must be multiples of 8");
     if (ws_bytes < linear_bwd_workspace(m, n, k)) return fail(AFFMAE_ECONFIG, "linear bwd: workspace too small");
     cudaStream_t st = as_stream(stream);
-    const size_t gws = ws_bytes - size_t(kColsumChunks) * size_t(n) * 4 - 256;
+    const size_t skb = splitk_part_bytes(m, n, k);
+    const size_t gws = ws_bytes - size_t(kColsumChunks) * size_t(n) * 4 - 256 - skb;
     float* part = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ws) + gws + 255) & ~uintptr_t(255));
+    float* skpart = reinterpret_cast<float*>(
+        (reinterpret_cast<uintptr_t>(ws) + gws + size_t(kColsumChunks) * size_t(n) * 4 + 256 + 255) & ~uintptr_t(255));
     int rc = AFFMAE_OK;
     if (dx && (rc = run_plain<DxCfg>(dy, w, dx, 0.f, int(m), int(k), int(n), ws, gws, st))) return rc;
-    if (dw && (rc = run_plain<DwCfg>(dy, x, dw, 1.f, int(n), int(k), int(m), ws, gws, st))) return rc;
+    if (dw) {
+        const SplitK sk = splitk_plan(m, n, k);
+        if (sk.L < 2) {
+            if ((rc = run_plain<DwCfg>(dy, x, dw, 1.f, int(n), int(k), int(m), ws, gws, st))) return rc;
+        } else {
+            const auto* dyb = static_cast<const __nv_bfloat16*>(dy);
+            const auto* xb = static_cast<const __nv_bfloat16*>(x);
+            if ((rc = run_plain<DwCfg>(dy, x, skpart, 0.f, int(n), int(k), int(sk.c), ws, gws, st, sk.L))) return rc;
+            int parts = sk.L;
+            if (sk.rem > 0) {
+                const int64_t t0 = int64_t(sk.L) * sk.c;
+                if ((rc = run_plain<DwCfg>(dyb + t0 * n, xb + t0 * k, skpart + int64_t(sk.L) * n * k, 0.f, int(n),
+                                           int(k), int(sk.rem), ws, gws, st)))
+                    return rc;
+                ++parts;
+            }
+            const int64_t n4 = n * k / 4;
+            splitk_reduce_kernel<<<unsigned(std::min<int64_t>((n4 + 255) / 256, 4 * kNumSMs)), 256, 0, st>>>(
+                reinterpret_cast<const float4*>(skpart), n4, parts, reinterpret_cast<float4*>(dw));
+            AFFMAE_LAUNCH_CHECK("splitk_reduce_kernel");
+        }
+    }
     if (db) {
         const int64_t rows_per = (m + kColsumChunks - 1) / kColsumChunks;
         const dim3 grid(unsigned((n + 255) / 256), kColsumChunks);
-        colsum_partial_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), m, n, rows_per, part);
-        colsum_final_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(part, n, kColsumChunks, db);
+        colsum_partial_kernel<<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), m, n, rows_per, part);
+        colsum_final_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, st>>>(part, n, kColsumChunks, db);
         AFFMAE_LAUNCH_CHECK("linear bwd bias");
     }
     return AFFMAE_OK;

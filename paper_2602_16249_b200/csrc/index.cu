@@ -590,6 +590,46 @@ __global__ void knn_kernel(const float* __restrict__ queries, const float* __res
     }
 }
 
+// Few keys per image (<= 1024) and k <= 8: the image's keys staged once per block in shared
+// memory as binary64, one query per thread scanning all of them with a register top-K --
+// the same (d^2 binary64 without FMA, index) order as the reference's scan, no warp merge.
+template <int K>
+__global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__ queries, const float* __restrict__ keys,
+                                                       int64_t nq, int64_t nk, int k, int32_t* __restrict__ idx,
+                                                       uint8_t* __restrict__ valid) {
+    extern __shared__ double2 skeys[];
+    const int64_t b = blockIdx.y;
+    const float2* kb = reinterpret_cast<const float2*>(keys) + b * nk;
+    for (int64_t j = threadIdx.x; j < nk; j += blockDim.x) {
+        const float2 p = kb[j];
+        skeys[j] = make_double2(double(p.x), double(p.y));
+    }
+    __syncthreads();
+    const int64_t qi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (qi >= nq) return;
+    const int64_t w = b * nq + qi;
+    const float2 q = reinterpret_cast<const float2*>(queries)[w];
+    const double qx = double(q.x), qy = double(q.y);
+    const int kept = int(k < nk ? k : nk);
+    double d[K];
+    int jj[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+        d[r] = INFINITY;
+        jj[r] = INT32_MAX;
+    }
+    for (int j = 0; j < int(nk); ++j) {
+        const double2 p = skeys[j];
+        const double dx = __dsub_rn(p.x, qx), dy = __dsub_rn(p.y, qy);
+        const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        if (d2 < d[K - 1]) topk_insert<K>(d, jj, kept, d2, j);  // slots >= kept stay +inf
+    }
+    for (int t = 0; t < k; ++t) {
+        idx[w * k + t] = t < kept ? jj[t] : 0;
+        valid[w * k + t] = t < kept ? 1 : 0;
+    }
+}
+
 // ---------------------------------------------- grid-accelerated exact knn
 // Large key sets: the image's keys are bucketed once into a uniform grid of
 // ~2 keys per cell (counting sort in global memory); each query (one thread)
@@ -959,6 +999,16 @@ int knn(const float* queries, const float* keys, int64_t batch, int64_t nq, int6
     if (!queries || !keys || !idx || !valid) return fail(AFFMAE_ECONFIG, "knn: null pointer");
     if (batch * nq == 0) return AFFMAE_OK;
     cudaStream_t st = as_stream(stream);
+    if (k <= 8 && nk <= 1024 && nq >= 256) {  // few keys, many queries: keys in shared memory
+        const dim3 grid(unsigned((nq + 255) / 256), unsigned(batch));
+        const size_t smem = size_t(nk) * sizeof(double2);
+        if (smem > 40 * 1024)
+            AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(knn_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(smem)));
+        knn_smem_kernel<8><<<grid, 256, smem, st>>>(queries, keys, nq, nk, int(k), idx, valid);
+        AFFMAE_LAUNCH_CHECK("knn_smem_kernel");
+        return AFFMAE_OK;
+    }
     if (nk < 512 || nq * nk < (int64_t(1) << 20)) {  // small problems: brute force
         knn_kernel<<<blocks(batch * nq * 32), 256, 0, st>>>(queries, keys, batch, nq, nk, int(k), idx, valid);
         AFFMAE_LAUNCH_CHECK("knn_kernel");

@@ -420,39 +420,99 @@ __global__ void pool_fill_kernel(const int32_t* __restrict__ best_of, const doub
     lidx[pos] = int32_t(i - b * n);
 }
 
-// per retained token: sort its list by (dist, index), keep k_m
-__global__ void pool_sort_kernel(const int32_t* __restrict__ off, int64_t batch, int64_t n, int64_t r,
-                                 int k_m, double* __restrict__ ldist, int32_t* __restrict__ lidx,
-                                 int32_t* __restrict__ pool_idx, double* __restrict__ pool_dist,
-                                 int32_t* __restrict__ pool_cnt, int32_t* __restrict__ row_of,
-                                 const int32_t* __restrict__ retained) {
-    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// per retained token (one warp): the k_m smallest (dist, index) pairs of its candidate list,
+// ascending (the reference sorts the whole pool and truncates, merging.cpp:102-114; only the
+// kept prefix is observable).  Lanes stride over the list keeping a register-sorted top-K,
+// then K rounds of a warp-wide lexicographic minimum.  O(list) per pool: with spatially
+// clustered retained tokens one pool can collect thousands of candidates.
+constexpr int kPoolK = 16;
+__device__ __forceinline__ bool pair_less(double da, int ja, double db, int jb) {
+    return da < db || (da == db && ja < jb);
+}
+__global__ void __launch_bounds__(256) pool_topk_kernel(const int32_t* __restrict__ off, int64_t batch, int64_t n,
+                                                        int64_t r, int k_m, const double* __restrict__ ldist,
+                                                        const int32_t* __restrict__ lidx,
+                                                        int32_t* __restrict__ pool_idx, double* __restrict__ pool_dist,
+                                                        int32_t* __restrict__ pool_cnt, int32_t* __restrict__ row_of,
+                                                        const int32_t* __restrict__ retained) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (i >= batch * r) return;
-    int64_t b = i / r;
-    int ri = int(i - b * r);
+    const int64_t b = i / r;
+    const int ri = int(i - b * r);
     const int32_t* o = off + b * (r + 1);
-    double* ld = ldist + b * n;
-    int32_t* li = lidx + b * n;
+    const double* ld = ldist + b * n;
+    const int32_t* li = lidx + b * n;
     const int s = o[ri], e = o[ri + 1];
-    for (int x = s + 1; x < e; ++x) {
+    double d[kPoolK];
+    int j[kPoolK];
+#pragma unroll
+    for (int t = 0; t < kPoolK; ++t) {
+        d[t] = INFINITY;
+        j[t] = INT_MAX;
+    }
+    for (int x = s + lane; x < e; x += 32) {
         double dv = ld[x];
-        int iv = li[x], y = x;
-        while (y > s && (ld[y - 1] > dv || (ld[y - 1] == dv && li[y - 1] > iv))) {
-            ld[y] = ld[y - 1];
-            li[y] = li[y - 1];
-            --y;
+        int jv = li[x];
+        if (!pair_less(dv, jv, d[k_m - 1], j[k_m - 1])) continue;
+#pragma unroll
+        for (int t = 0; t < kPoolK; ++t) {  // insertion into the sorted prefix
+            if (t < k_m && pair_less(dv, jv, d[t], j[t])) {
+                const double td = d[t];
+                const int tj = j[t];
+                d[t] = dv;
+                j[t] = jv;
+                dv = td;
+                jv = tj;
+            }
         }
-        ld[y] = dv;
-        li[y] = iv;
     }
     const int keep = min(e - s, k_m);
-    pool_cnt[i] = keep;
-    for (int t = 0; t < k_m; ++t) {
-        pool_idx[i * k_m + t] = t < keep ? li[s + t] : -1;
-        pool_dist[i * k_m + t] = t < keep ? ld[s + t] : 0.0;
+    double thr_d = -INFINITY;
+    int thr_j = -1;
+    int head = 0;
+    for (int t = 0; t < keep; ++t) {
+        double cd = INFINITY;
+        int cj = INT_MAX;
+#pragma unroll
+        for (int q = 0; q < kPoolK; ++q)
+            if (q == head) {
+                cd = d[q];
+                cj = j[q];
+            }
+        if (head >= k_m) {
+            cd = INFINITY;
+            cj = INT_MAX;
+        }
+        double md = cd;
+        int mj = cj;
+#pragma unroll
+        for (int ofs = 16; ofs > 0; ofs >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, md, ofs);
+            const int oj = __shfl_xor_sync(0xffffffffu, mj, ofs);
+            if (pair_less(od, oj, md, mj)) {
+                md = od;
+                mj = oj;
+            }
+        }
+        if (cd == md && cj == mj) ++head;  // pairs are unique: exactly one lane owns the minimum
+        if (lane == 0) {
+            pool_idx[i * k_m + t] = mj;
+            pool_dist[i * k_m + t] = md;
+        }
+        thr_d = md;
+        thr_j = mj;
     }
-    row_of[b * n + retained[i]] = ri;
-    for (int t = 0; t < e - s; ++t) row_of[b * n + li[s + t]] = t < keep ? ri : -1;
+    if (lane == 0) {
+        for (int t = keep; t < k_m; ++t) {
+            pool_idx[i * k_m + t] = -1;
+            pool_dist[i * k_m + t] = 0.0;
+        }
+        pool_cnt[i] = keep;
+        row_of[b * n + retained[i]] = ri;
+    }
+    for (int x = s + lane; x < e; x += 32)
+        row_of[b * n + li[x]] = pair_less(thr_d, thr_j, ld[x], li[x]) ? -1 : ri;
 }
 
 // ---------------------------------------------------- pool forward/backward
@@ -1160,9 +1220,9 @@ int merge_plan_build(const float* coords, const int32_t* retained, int64_t batch
     seg_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(w.pool_off, r + 1);
     pool_fill_kernel<<<blocks_of(batch * n), 256, 0, st>>>(w.best_of, w.d2_of, batch, n, r, w.pool_off,
                                                            w.pool_cur, w.ldist, w.lidx);
-    pool_sort_kernel<<<blocks_of(batch * r, 128), 128, 0, st>>>(w.pool_off, batch, n, r, k_m, w.ldist, w.lidx,
-                                                           plan->pool_idx, plan->pool_dist,
-                                                           plan->pool_cnt, plan->row_of, retained);
+    pool_topk_kernel<<<blocks_of(batch * r * 32, 256), 256, 0, st>>>(w.pool_off, batch, n, r, k_m, w.ldist, w.lidx,
+                                                                     plan->pool_idx, plan->pool_dist,
+                                                                     plan->pool_cnt, plan->row_of, retained);
     AFFMAE_LAUNCH_CHECK("merge_plan");
     return AFFMAE_OK;
 }

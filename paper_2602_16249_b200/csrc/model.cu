@@ -575,6 +575,10 @@ size_t misc_ws_bytes(const Model& m) {
         }
     }
     upd(perlin_mask_workspace(m.B, m.g, m.g, 2, 4.0));
+    for (int s = 0; s < m.ns; ++s) {
+        upd(interp_bwd_gather_workspace(m.B, m.Q, m.st[size_t(s)].N, c.gather_k));
+        upd(interp_bwd_gather_workspace(m.B, m.Q, m.st[size_t(s)].N, c.stages[s].interp_k));
+    }
     (void)c;
     return w;
 }
@@ -587,7 +591,7 @@ size_t gemm_ws_bytes(const Model& m) {
         Nmax = std::max(Nmax, 4 * S.D);
     }
     size_t w = std::max(linear_workspace(round8(Mmax), Nmax, Nmax), linear_bwd_workspace(round8(Mmax), Nmax, Nmax));
-    return std::max<size_t>(w, size_t(32) << 20);
+    return std::max<size_t>(w, size_t(256) << 20);
 }
 
 // ------------------------------------------------------------------ GEMMs
@@ -932,8 +936,8 @@ int round_bwd(const Ctx& x, int si, int r) {
     // virtual tokens: interpolation of z at the deformed points (gradients into z, p, qpos)
     CK(mk::cast_bf16(m.F4, Mq * dd, m.B6, x.st));
     CK(cudaMemsetAsync(m.dqpos, 0, size_t(Mq * 2) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
-    CK(interp_bwd(R.qpos, S.coords, d.z, R.gidx, R.gval, B, Q, S.N, dd, c.gather_k, PF(m, pre + "p"), kInterpEps,
-                  m.B6, m.dz, GF(m, pre + "p"), m.dqpos, x.sv()));
+    CK(interp_bwd_gather(R.qpos, S.coords, d.z, R.gidx, R.gval, B, Q, S.N, dd, c.gather_k, PF(m, pre + "p"),
+                         kInterpEps, m.B6, m.dz, GF(m, pre + "p"), m.dqpos, m.ws, m.ws_bytes, x.sv()));
     // qpos = refs + NormClamp(fq W_off + b_off): += dfq in place
     CK(mk::offset_bwd(R.fq_in, Mq, dd, PF(m, pre + "off.w"), 2.0 * double(c.patch), R.offpre, m.dqpos, m.dfq,
                       GF(m, pre + "off.w"), GF(m, pre + "off.b"), m.part, x.st));
@@ -970,8 +974,9 @@ int backward(const Ctx& x) {
             const std::string pre = "aux.s" + std::to_string(s) + ".";
             const int k = c.stages[s].interp_k;
             CK(x.bwd_wx(S.avirt, PBF(m, pre + "w"), S.daux, Mq, p2, S.D, m.B1, GF(m, pre + "w"), GF(m, pre + "b")));
-            CK(interp_bwd(m.refs, S.coords, S.fout_bf, S.aidx, S.aval, B, m.Q, S.N, S.D, k, PF(m, pre + "p"),
-                          kInterpEps, m.B1, S.df, GF(m, pre + "p"), m.dqjunk, x.sv()));
+            CK(interp_bwd_gather(m.refs, S.coords, S.fout_bf, S.aidx, S.aval, B, m.Q, S.N, S.D, k,
+                                 PF(m, pre + "p"), kInterpEps, m.B1, S.df, GF(m, pre + "p"), m.dqjunk, m.ws,
+                                 m.ws_bytes, x.sv()));
         }
     }
     // decoder stages, reverse of the forward order (shallowest first)

@@ -157,12 +157,16 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     for (int c = threadIdx.x; c < 2 * C; c += blockDim.x) part[int64_t(blockIdx.x) * 2 * C + c] = red[c];
 }
 
-// out[c] += sum_p part[p * width + c]   (fixed order over p)
+// out[c] += sum_p part[p * width + c]: one warp per column, lane-strided partial sums and a
+// fixed butterfly (deterministic)
 __global__ void colsum_partials_kernel(const float* __restrict__ part, int nparts, int width, float* __restrict__ out0,
                                        int split, float* __restrict__ out1) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < width; c += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < width; c += (gridDim.x * blockDim.x) >> 5) {
         float s = 0.f;
-        for (int p = 0; p < nparts; ++p) s += part[int64_t(p) * width + c];
+        for (int p = lane; p < nparts; p += 32) s += part[int64_t(p) * width + c];
+        s = warp_sum(s);
+        if (lane) continue;
         if (c < split) {
             if (out0) out0[c] += s;
         } else if (out1) {
@@ -170,6 +174,7 @@ __global__ void colsum_partials_kernel(const float* __restrict__ part, int npart
         }
     }
 }
+static unsigned colsum_blocks(int64_t width) { return unsigned((width * 32 + 255) / 256); }
 
 template <typename XT>
 static int ln_fwd_t(const XT* x, const __nv_bfloat16* add, float* xo, __nv_bfloat16* xo_bf, const float* g,
@@ -204,7 +209,7 @@ int ln_fwd_bf(const __nv_bfloat16* x, float* xo, const float* g, const float* b,
     return ln_fwd_t<__nv_bfloat16>(x, nullptr, xo, nullptr, g, b, rows, C, y, stats, st);
 }
 
-unsigned ln_bwd_blocks(int64_t rows) { return row_blocks(rows, 4 * kRowWarps, kNumSMs); }
+unsigned ln_bwd_blocks(int64_t rows) { return row_blocks(rows, 4 * kRowWarps, 4 * kNumSMs); }
 
 template <typename XT>
 static int ln_bwd_t(const float* dy, const XT* x, const float2* stats, const float* g, int64_t rows, int64_t C,
@@ -230,7 +235,7 @@ static int ln_bwd_t(const float* dy, const XT* x, const float2* stats, const flo
         default:
             return fail(AFFMAE_EUNSUPPORTED, "model layer_norm: width must be 64 * {1,2,3,4,6,8,12,16}");
     }
-    if (pp) colsum_partials_kernel<<<unsigned((2 * C + 255) / 256), 256, 0, st>>>(pp, int(nb), int(2 * C), dgamma,
+    if (pp) colsum_partials_kernel<<<colsum_blocks(2 * C), 256, 0, st>>>(pp, int(nb), int(2 * C), dgamma,
                                                                                    int(C), dbeta);
     AFFMAE_LAUNCH_CHECK("ln_bwd_kernel");
     return AFFMAE_OK;
@@ -322,7 +327,7 @@ int pos_hidden_bwd(const float* coords, int64_t rows, float inv_image, const flo
     const unsigned nb = pos_bwd_blocks(rows);
     pos_hidden_bwd_kernel<<<nb, kPosBlock, 0, st>>>(reinterpret_cast<const float2*>(coords), rows, inv_image, w1, b1,
                                                     dh, part);
-    colsum_partials_kernel<<<1, 64, 0, st>>>(part, int(nb), 48, dw1, 32, db1);
+    colsum_partials_kernel<<<colsum_blocks(48), 256, 0, st>>>(part, int(nb), 48, dw1, 32, db1);
     AFFMAE_LAUNCH_CHECK("pos_hidden_bwd_kernel");
     return AFFMAE_OK;
 }
@@ -396,7 +401,7 @@ int scorer_out_bwd(const __nv_bfloat16* hid, const float* scores, const float* d
     if (rows <= 0) return AFFMAE_OK;
     const unsigned nb = pos_bwd_blocks(rows);
     scorer_out_bwd_kernel<<<nb, kPosBlock, 0, st>>>(hid, scores, dscores, rows, w2, dhid, part);
-    colsum_partials_kernel<<<1, 32, 0, st>>>(part, int(nb), 17, dw2, 16, db2);
+    colsum_partials_kernel<<<colsum_blocks(17), 256, 0, st>>>(part, int(nb), 17, dw2, 16, db2);
     AFFMAE_LAUNCH_CHECK("scorer_out_bwd_kernel");
     return AFFMAE_OK;
 }
@@ -535,7 +540,7 @@ int offset_bwd(const float* fq, int64_t rows, int64_t C, const float* w, double 
         default:
             return fail(AFFMAE_EUNSUPPORTED, "decoder offset head: width must be 64, 128, 256, 512 or 1024");
     }
-    colsum_partials_kernel<<<unsigned((2 * C + 2 + 255) / 256), 256, 0, st>>>(part, int(nb), int(2 * C + 2), dw,
+    colsum_partials_kernel<<<colsum_blocks(2 * C + 2), 256, 0, st>>>(part, int(nb), int(2 * C + 2), dw,
                                                                              int(2 * C), db);
     AFFMAE_LAUNCH_CHECK("offset_bwd_kernel");
     return AFFMAE_OK;
@@ -694,7 +699,7 @@ int colsum_f32(const float* x, int64_t rows, int64_t cols, float* out, float* pa
     const int64_t rows_per = (rows + kColChunks - 1) / kColChunks;
     colsum_f32_partial_kernel<<<dim3(unsigned((cols + 255) / 256), kColChunks), 256, 0, st>>>(x, rows, cols, rows_per,
                                                                                            part);
-    colsum_partials_kernel<<<unsigned((cols + 255) / 256), 256, 0, st>>>(part, kColChunks, int(cols), out, int(cols),
+    colsum_partials_kernel<<<colsum_blocks(cols), 256, 0, st>>>(part, kColChunks, int(cols), out, int(cols),
                                                                           nullptr);
     AFFMAE_LAUNCH_CHECK("colsum_f32");
     return AFFMAE_OK;
