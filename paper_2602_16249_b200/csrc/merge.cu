@@ -429,15 +429,12 @@ constexpr int kPoolK = 16;
 __device__ __forceinline__ bool pair_less(double da, int ja, double db, int jb) {
     return da < db || (da == db && ja < jb);
 }
-__global__ void __launch_bounds__(256) pool_topk_kernel(const int32_t* __restrict__ off, int64_t batch, int64_t n,
-                                                        int64_t r, int k_m, const double* __restrict__ ldist,
-                                                        const int32_t* __restrict__ lidx,
-                                                        int32_t* __restrict__ pool_idx, double* __restrict__ pool_dist,
-                                                        int32_t* __restrict__ pool_cnt, int32_t* __restrict__ row_of,
-                                                        const int32_t* __restrict__ retained) {
-    const int lane = threadIdx.x & 31;
-    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (i >= batch * r) return;
+// warp-cooperative top-k_m of one long candidate list (the list of pool i)
+__device__ void pool_topk_warp(int64_t i, int lane, const int32_t* __restrict__ off, int64_t n, int64_t r, int k_m,
+                               const double* __restrict__ ldist, const int32_t* __restrict__ lidx,
+                               int32_t* __restrict__ pool_idx, double* __restrict__ pool_dist,
+                               int32_t* __restrict__ pool_cnt, int32_t* __restrict__ row_of,
+                               const int32_t* __restrict__ retained) {
     const int64_t b = i / r;
     const int ri = int(i - b * r);
     const int32_t* o = off + b * (r + 1);
@@ -454,10 +451,10 @@ __global__ void __launch_bounds__(256) pool_topk_kernel(const int32_t* __restric
     for (int x = s + lane; x < e; x += 32) {
         double dv = ld[x];
         int jv = li[x];
-        if (!pair_less(dv, jv, d[k_m - 1], j[k_m - 1])) continue;
+        if (!pair_less(dv, jv, d[kPoolK - 1], j[kPoolK - 1])) continue;
 #pragma unroll
-        for (int t = 0; t < kPoolK; ++t) {  // insertion into the sorted prefix
-            if (t < k_m && pair_less(dv, jv, d[t], j[t])) {
+        for (int t = 0; t < kPoolK; ++t) {  // insertion into the sorted list
+            if (pair_less(dv, jv, d[t], j[t])) {
                 const double td = d[t];
                 const int tj = j[t];
                 d[t] = dv;
@@ -480,10 +477,6 @@ __global__ void __launch_bounds__(256) pool_topk_kernel(const int32_t* __restric
                 cd = d[q];
                 cj = j[q];
             }
-        if (head >= k_m) {
-            cd = INFINITY;
-            cj = INT_MAX;
-        }
         double md = cd;
         int mj = cj;
 #pragma unroll
@@ -513,6 +506,61 @@ __global__ void __launch_bounds__(256) pool_topk_kernel(const int32_t* __restric
     }
     for (int x = s + lane; x < e; x += 32)
         row_of[b * n + li[x]] = pair_less(thr_d, thr_j, ld[x], li[x]) ? -1 : ri;
+}
+
+// A warp per 32 pools: each lane sorts its own (short) candidate list by insertion, the lists
+// longer than 32 are then taken one at a time by the whole warp.  Balanced pools (random
+// scores: ~1.5 candidates) stay one-thread work; spatially clustered retained tokens (the
+// model's learned scores) can give one pool thousands of candidates.
+constexpr int kPoolShort = 32;
+__global__ void __launch_bounds__(256) pool_topk_kernel(const int32_t* __restrict__ off, int64_t batch, int64_t n,
+                                                        int64_t r, int k_m, double* __restrict__ ldist,
+                                                        int32_t* __restrict__ lidx, int32_t* __restrict__ pool_idx,
+                                                        double* __restrict__ pool_dist, int32_t* __restrict__ pool_cnt,
+                                                        int32_t* __restrict__ row_of,
+                                                        const int32_t* __restrict__ retained) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool ok = i < batch * r;
+    bool is_long = false;
+    if (ok) {
+        const int64_t b = i / r;
+        const int ri = int(i - b * r);
+        const int32_t* o = off + b * (r + 1);
+        double* ld = ldist + b * n;
+        int32_t* li = lidx + b * n;
+        const int s = o[ri], e = o[ri + 1];
+        is_long = e - s > kPoolShort;
+        if (!is_long) {
+            for (int x = s + 1; x < e; ++x) {
+                const double dv = ld[x];
+                const int iv = li[x];
+                int y = x;
+                while (y > s && (ld[y - 1] > dv || (ld[y - 1] == dv && li[y - 1] > iv))) {
+                    ld[y] = ld[y - 1];
+                    li[y] = li[y - 1];
+                    --y;
+                }
+                ld[y] = dv;
+                li[y] = iv;
+            }
+            const int keep = min(e - s, k_m);
+            pool_cnt[i] = keep;
+            for (int t = 0; t < k_m; ++t) {
+                pool_idx[i * k_m + t] = t < keep ? li[s + t] : -1;
+                pool_dist[i * k_m + t] = t < keep ? ld[s + t] : 0.0;
+            }
+            row_of[b * n + retained[i]] = ri;
+            for (int t = 0; t < e - s; ++t) row_of[b * n + li[s + t]] = t < keep ? ri : -1;
+        }
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, is_long);
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t i2 = __shfl_sync(0xffffffffu, i, src);
+        pool_topk_warp(i2, lane, off, n, r, k_m, ldist, lidx, pool_idx, pool_dist, pool_cnt, row_of, retained);
+    }
 }
 
 // ---------------------------------------------------- pool forward/backward
@@ -1220,7 +1268,7 @@ int merge_plan_build(const float* coords, const int32_t* retained, int64_t batch
     seg_scan_kernel<<<unsigned(batch), 1024, 0, st>>>(w.pool_off, r + 1);
     pool_fill_kernel<<<blocks_of(batch * n), 256, 0, st>>>(w.best_of, w.d2_of, batch, n, r, w.pool_off,
                                                            w.pool_cur, w.ldist, w.lidx);
-    pool_topk_kernel<<<blocks_of(batch * r * 32, 256), 256, 0, st>>>(w.pool_off, batch, n, r, k_m, w.ldist, w.lidx,
+    pool_topk_kernel<<<blocks_of(batch * r, 256), 256, 0, st>>>(w.pool_off, batch, n, r, k_m, w.ldist, w.lidx,
                                                                      plan->pool_idx, plan->pool_dist,
                                                                      plan->pool_cnt, plan->row_of, retained);
     AFFMAE_LAUNCH_CHECK("merge_plan");
