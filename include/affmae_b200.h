@@ -138,8 +138,8 @@ int affmae_layernorm_bwd(const affmae_bf16* x, const float* gamma, const float* 
                          size_t workspace_bytes, void* stream);
 
 /* Decoder row ops (§8(f) #2).  NormClampOp (src/pipeline.cpp:75-127): rows of
- * x [rows, d] bf16 rescaled to norm <= limit; the backward writes dx (bf16,
- * overwritten).  Reconstruction loss (Tape::mse over the masked cells,
+ * x [rows, d] bf16 rescaled to norm <= limit; the backward ACCUMULATES into dx (bf16,
+ * +=, CustomOp::backward semantics, include/affmae/tape.hpp:29-31).  Reconstruction loss (Tape::mse over the masked cells,
  * src/tape.cpp:431-446, Model::loss_parts src/pipeline.cpp:581-600): loss = mean
  * over rows x p of (pred[r] - patches[cells[r]])^2, pred [rows, p] bf16, patches
  * [n_cells, p] fp32, cells [rows] int32; with dpred != NULL also writes
@@ -252,6 +252,9 @@ size_t affmae_attn_fwd_planned_workspace(const affmae_cluster_geom* g, const aff
 int affmae_attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a,
                             const affmae_attn_inputs* in, const affmae_attn_plan* plan, affmae_bf16* out,
                             float* lse, void* workspace, size_t workspace_bytes, void* stream);
+
+/* hilbert_index (include/affmae/geometry.hpp:51; src/geometry.cpp:15-30), host side */
+uint64_t affmae_hilbert_index(uint32_t n, uint32_t x, uint32_t y);
 
 /* flop_count_attn / flop_count_attn_dense (include/affmae/attention.hpp:77-79,
  * src/attention.cpp:360-370): closed-form forward flops of neighbourhood attention,
@@ -477,6 +480,11 @@ int affmae_model_make_masks(affmae_model* m, const uint64_t* seeds_host, void* s
  * input buffers; gradients of the batch-mean loss left in the model.  loss3 (device fp32
  * [3] or NULL) receives {total, main, aux}. */
 int affmae_model_forward_backward(affmae_model* m, float* loss3, void* stream);
+/* encode + decode + deep_sup + loss_parts only (masked_mse, src/pipeline.cpp:748-755): loss3 as above */
+int affmae_model_forward(affmae_model* m, float* loss3, void* stream);
+/* a fresh AdamW(cfg.optim, total_steps) as train() constructs per call (src/pipeline.cpp:686):
+ * zero moments, step 0 */
+int affmae_model_reset_optimizer(affmae_model* m, int64_t total_steps);
 /* AdamW::step over every parameter (src/pipeline.cpp:650-680) + bf16 shadow refresh */
 int affmae_model_apply_step(affmae_model* m, void* stream);
 /* forward_backward + apply_step; with use_graph the whole step is captured into a CUDA

@@ -69,6 +69,29 @@ float bf16_to_float(uint16_t u) {
     return f;
 }
 
+// [rows, groups*w] -> bf16 [rows, groups*wp] (each group zero-padded to wp, times scale): head
+// dims / feature widths the reference allows but the kernels are not compiled for (e.g. the
+// toy() config's head_dim 12) run on the next compiled width with zero padding
+std::vector<uint16_t> bf16_pad(const Tensor& t, int64_t groups, int64_t w, int64_t wp, float scale = 1.f) {
+    const int64_t rows = t.numel() / (groups * w);
+    std::vector<uint16_t> v(size_t(rows * groups * wp), 0);
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t g = 0; g < groups; ++g)
+            for (int64_t e = 0; e < w; ++e) {
+                __nv_bfloat16 b = __float2bfloat16(float(t.get((r * groups + g) * w + e)) * scale);
+                std::memcpy(&v[size_t((r * groups + g) * wp + e)], &b, 2);
+            }
+    return v;
+}
+// value of padded element (r, g, e) of a [rows, groups*wp] array
+inline int64_t pad_at(int64_t r, int64_t g, int64_t e, int64_t groups, int64_t wp) { return (r * groups + g) * wp + e; }
+int padded_head_dim(int d) {
+    if (d <= 16) return 16;
+    if (d <= 32) return 32;
+    if (d <= 64) return 64;
+    throw ConfigError("attention op: head_dim > 64 not compiled");
+}
+
 struct DeviceIndex {
     affmae_cluster_geom g{};
     std::unique_ptr<Dev> perm, cof, nbr, roff, rcl;
@@ -132,6 +155,16 @@ NeighborIndex cluster_neighborhood_from_coords(const PointSet& points, int64_t s
     return nb;
 }
 
+NeighborIndex cluster_neighborhood(const ClusterAssignment& assign, const PointSet& points, int64_t groups) {
+    // the device rebuilds the assignment from the coordinates (balanced_clusters(points,
+    // assign.target)); an assignment from anywhere else is a ConfigError, not a silent mismatch
+    if (groups < 1) throw ConfigError("cluster_neighborhood: groups must be >= 1");
+    ClusterAssignment mine = cuda::balanced_clusters(points, assign.target);
+    if (mine.cluster_of != assign.cluster_of)
+        throw ConfigError("cuda::cluster_neighborhood: assignment is not balanced_clusters(points, target)");
+    return cluster_neighborhood_from_coords(points, assign.target, groups);
+}
+
 std::vector<int64_t> sfc_order(const PointSet& points) {
     const int64_t n = points.count();
     if (n < 1) throw ConfigError("sfc_order: empty point set");
@@ -180,7 +213,11 @@ struct ClusterAttnOp final : CustomOp {
 
     std::string name() const override { return "cluster_attention_b200"; }
 
-    affmae_attn_desc desc() const { return {heads, head_dim, hidden, patch}; }
+    // the device head dim (head_dim zero-padded to a compiled width); q carries the scale
+    // sqrt(dp / head_dim) so the kernel's 1/sqrt(dp) gives the reference's 1/sqrt(head_dim)
+    int dp() const { return padded_head_dim(head_dim); }
+    float qscale() const { return float(std::sqrt(double(dp()) / double(head_dim))); }
+    affmae_attn_desc desc() const { return {heads, dp(), hidden, patch}; }
 
     Geometry& geometry(int64_t n) {
         if (!geo) {
@@ -200,7 +237,9 @@ struct ClusterAttnOp final : CustomOp {
 
     // uploads the 10 inputs; `t` owns the device copies
     affmae_attn_inputs inputs(const std::vector<const Tensor*>& in, Geometry& G, std::unique_ptr<Dev> (&t)[10]) {
-        for (int i = 0; i < 5; ++i) t[i] = upload(bf16(*in[size_t(i)]));
+        t[0] = upload(bf16_pad(*in[0], heads, head_dim, dp(), qscale()));
+        for (int i = 1; i < 3; ++i) t[i] = upload(bf16_pad(*in[size_t(i)], heads, head_dim, dp()));
+        for (int i = 3; i < 5; ++i) t[i] = upload(bf16_pad(*in[size_t(i)], 1, head_dim, dp()));
         for (int i = 5; i < 10; ++i) t[i] = upload(f32(*in[size_t(i)]));
         return {t[0]->as<affmae_bf16>(), t[1]->as<affmae_bf16>(), t[2]->as<affmae_bf16>(),
                 t[3]->as<affmae_bf16>(), t[4]->as<affmae_bf16>(), G.coords->as<float>(),
@@ -216,34 +255,62 @@ struct ClusterAttnOp final : CustomOp {
               "attn_fwd");
     }
 
+    // Activations of the last forward, kept on the device for the backward (the Tape calls
+    // backward with the same inputs, include/affmae/tape.hpp:32-38): the inputs' device copies,
+    // O and LSE -- the backward neither re-uploads nor recomputes the forward.
+    struct Saved {
+        std::unique_ptr<Dev> t[10], out, lse;
+        affmae_attn_inputs ai{};
+        const Tensor* src[10] = {};
+    };
+    std::unique_ptr<Saved> saved;
+
+    bool same_inputs(const std::vector<const Tensor*>& in) const {
+        if (!saved) return false;
+        for (int i = 0; i < 10; ++i)
+            if (saved->src[i] != in[size_t(i)]) return false;
+        return true;
+    }
+
     Tensor forward(const std::vector<const Tensor*>& in) override {
         if (in.size() != 10) throw ConfigError("attention op: want 10 inputs");
-        const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
+        const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim, hdp = int64_t(heads) * dp();
         Geometry& G = geometry(n);
-        std::unique_ptr<Dev> t[10];
-        affmae_attn_inputs ai = inputs(in, G, t);
-        Dev out(n * hd * 2), lse(n * heads * 4);
-        run_forward(G, ai, out, lse);
-        auto h = download<uint16_t>(out, size_t(n * hd));
+        auto sv = std::make_unique<Saved>();
+        sv->ai = inputs(in, G, sv->t);
+        for (int i = 0; i < 10; ++i) sv->src[i] = in[size_t(i)];
+        sv->out = std::make_unique<Dev>(n * hdp * 2);
+        sv->lse = std::make_unique<Dev>(n * heads * 4);
+        run_forward(G, sv->ai, *sv->out, *sv->lse);
+        auto h = download<uint16_t>(*sv->out, size_t(n * hdp));
         Tensor o = Tensor::zeros({n, hd}, in[0]->precision());
-        for (int64_t i = 0; i < n * hd; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+        for (int64_t r = 0; r < n; ++r)
+            for (int g = 0; g < heads; ++g)
+                for (int e = 0; e < head_dim; ++e)
+                    o.set((r * heads + g) * head_dim + e, bf16_to_float(h[size_t(pad_at(r, g, e, heads, dp()))]));
+        saved = std::move(sv);
         return o;
     }
 
     void backward(const Tensor& out_grad, const std::vector<const Tensor*>& in,
                   const std::vector<Tensor*>& in_grads) override {
-        const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
+        const int64_t n = in[0]->rows(), hd = int64_t(heads) * dp();
         Geometry& G = geometry(n);
-        std::unique_ptr<Dev> t[10];
-        affmae_attn_inputs ai = inputs(in, G, t);
         affmae_attn_desc a = desc();
-        // the backward needs O and LSE: recomputed from the inputs (the op keeps no activations)
-        Dev out(n * hd * 2), lse(n * heads * 4);
-        run_forward(G, ai, out, lse);
-        auto dout = upload(bf16(out_grad));
+        if (!same_inputs(in)) {  // not the tensors of the last forward: rebuild the saved state
+            auto sv = std::make_unique<Saved>();
+            sv->ai = inputs(in, G, sv->t);
+            for (int i = 0; i < 10; ++i) sv->src[i] = in[size_t(i)];
+            sv->out = std::make_unique<Dev>(n * hd * 2);
+            sv->lse = std::make_unique<Dev>(n * heads * 4);
+            run_forward(G, sv->ai, *sv->out, *sv->lse);
+            saved = std::move(sv);
+        }
+        Saved& S = *saved;
+        auto dout = upload(bf16_pad(out_grad, heads, head_dim, dp()));
         Dev dq(n * hd * 2), dk(n * hd * 2), dv(n * hd * 2);
         std::unique_ptr<Dev> pg[7];
-        const int64_t psz[7] = {int64_t(heads) * head_dim, int64_t(heads) * head_dim, heads * 2 * int64_t(hidden),
+        const int64_t psz[7] = {int64_t(heads) * dp(), int64_t(heads) * dp(), heads * 2 * int64_t(hidden),
                                 int64_t(heads) * hidden, int64_t(heads) * hidden, heads, heads};
         for (int i = 0; i < 7; ++i) {
             pg[i] = std::make_unique<Dev>(psz[i] * 4);
@@ -253,22 +320,34 @@ struct ClusterAttnOp final : CustomOp {
                             pg[0]->as<float>(), pg[1]->as<float>(), pg[2]->as<float>(), pg[3]->as<float>(),
                             pg[4]->as<float>(), pg[5]->as<float>(), pg[6]->as<float>()};
         Dev wsb(affmae_attn_bwd_planned_workspace(&G.d.g, &a));
-        check(affmae_attn_bwd_planned(&G.d.g, &a, &ai, &G.plan, out.as<affmae_bf16>(), lse.as<float>(),
+        check(affmae_attn_bwd_planned(&G.d.g, &a, &S.ai, &G.plan, S.out->as<affmae_bf16>(), S.lse->as<float>(),
                                       dout->as<affmae_bf16>(), &g, wsb.p, wsb.n, nullptr),
               "attn_bwd");
         ccheck(cudaDeviceSynchronize(), "sync");
-        // accumulate (+=) into non-null in_grads (include/affmae/tape.hpp:29-31)
+        // accumulate (+=) into non-null in_grads (include/affmae/tape.hpp:29-31), padded columns dropped
         const Dev* act[3] = {&dq, &dk, &dv};
+        const float sc[3] = {qscale(), 1.f, 1.f};
         for (int i = 0; i < 3; ++i) {
             if (!in_grads[size_t(i)]) continue;
             auto h = download<uint16_t>(*act[i], size_t(n * hd));
-            for (int64_t j = 0; j < n * hd; ++j)
-                in_grads[size_t(i)]->set(j, in_grads[size_t(i)]->get(j) + bf16_to_float(h[size_t(j)]));
+            for (int64_t r = 0; r < n; ++r)
+                for (int gq = 0; gq < heads; ++gq)
+                    for (int e = 0; e < head_dim; ++e) {
+                        const int64_t j = (r * heads + gq) * head_dim + e;
+                        in_grads[size_t(i)]->set(j, in_grads[size_t(i)]->get(j) +
+                                                        sc[i] * bf16_to_float(h[size_t(pad_at(r, gq, e, heads, dp()))]));
+                    }
         }
         for (int i = 0; i < 7; ++i) {
             Tensor* dst = in_grads[size_t(3 + i)];
             if (!dst) continue;
             auto h = download<float>(*pg[i], size_t(psz[i]));
+            if (i < 2) {  // blank rows [heads, dp] -> [heads, head_dim]
+                for (int gq = 0; gq < heads; ++gq)
+                    for (int e = 0; e < head_dim; ++e)
+                        dst->set(gq * head_dim + e, dst->get(gq * head_dim + e) + h[size_t(gq * dp() + e)]);
+                continue;
+            }
             for (int64_t j = 0; j < psz[i]; ++j) dst->set(j, dst->get(j) + h[size_t(j)]);
         }
     }
@@ -333,11 +412,10 @@ MergePlan merge_plan(const PointSet& ps, std::span<const int64_t> retained, int 
     return plan;
 }
 
-std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords) {
+std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan) {
     // The device pool kernels consume the device plan; rebuild it from the host plan.
     struct PoolOp final : CustomOp {
         MergePlan plan;
-        Tensor coords;
         std::string name() const override { return "merge_pool_b200"; }
         int km() const {
             size_t m = 1;
@@ -419,7 +497,6 @@ std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords) {
     };
     auto op = std::make_shared<PoolOp>();
     op->plan = std::move(plan);
-    op->coords = std::move(coords);
     return op;
 }
 
@@ -449,12 +526,18 @@ std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, 
                 if (nbrs.row(qi).empty()) throw ConfigError("interp_softmax: no valid neighbors");
             (void)feats;
         }
+        // feature widths the kernels are not compiled for run zero-padded to the next of 64..512
+        static int64_t padded(int64_t dim) {
+            for (int64_t w : {64, 128, 256, 512})
+                if (dim <= w) return w;
+            throw ConfigError("interp op: feature width > 512 not compiled");
+        }
         Tensor forward(const std::vector<const Tensor*>& in) override {
             const Tensor& feats = *in[0];
             validate(feats, *in[1], *in[2]);
-            const int64_t nk = feats.rows(), dim = feats.cols(), nq = in[2]->dim(0);
+            const int64_t nk = feats.rows(), dim0 = feats.cols(), dim = padded(dim0), nq = in[2]->dim(0);
             DevRows d = upload_rows();
-            auto f = upload(bf16(feats));
+            auto f = upload(bf16_pad(feats, 1, dim0, dim));
             auto pt = upload(f32(*in[1]));
             auto q = upload(f32(*in[2]));
             Dev out(nq * dim * 2);
@@ -463,19 +546,20 @@ std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, 
                                     out.as<affmae_bf16>(), nullptr),
                   "interp_fwd");
             auto h = download<uint16_t>(out, size_t(nq * dim));
-            Tensor o = Tensor::zeros({nq, dim}, feats.precision());
-            for (int64_t i = 0; i < nq * dim; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+            Tensor o = Tensor::zeros({nq, dim0}, feats.precision());
+            for (int64_t r = 0; r < nq; ++r)
+                for (int64_t e = 0; e < dim0; ++e) o.set(r * dim0 + e, bf16_to_float(h[size_t(r * dim + e)]));
             return o;
         }
         void backward(const Tensor& g, const std::vector<const Tensor*>& in,
                       const std::vector<Tensor*>& in_grads) override {
             const Tensor& feats = *in[0];
-            const int64_t nk = feats.rows(), dim = feats.cols(), nq = in[2]->dim(0);
+            const int64_t nk = feats.rows(), dim0 = feats.cols(), dim = padded(dim0), nq = in[2]->dim(0);
             DevRows d = upload_rows();
-            auto f = upload(bf16(feats));
+            auto f = upload(bf16_pad(feats, 1, dim0, dim));
             auto pt = upload(f32(*in[1]));
             auto q = upload(f32(*in[2]));
-            auto dg = upload(bf16(g));
+            auto dg = upload(bf16_pad(g, 1, dim0, dim));
             Dev df(nk * dim * 4), dp(4), dq(nq * 2 * 4);
             ccheck(cudaMemset(df.p, 0, size_t(nk * dim * 4)), "memset");
             ccheck(cudaMemset(dp.p, 0, 4), "memset");
@@ -488,7 +572,9 @@ std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, 
                   "interp_bwd");
             if (in_grads[0]) {
                 auto h = download<float>(df, size_t(nk * dim));
-                for (int64_t i = 0; i < nk * dim; ++i) in_grads[0]->set(i, in_grads[0]->get(i) + h[size_t(i)]);
+                for (int64_t r = 0; r < nk; ++r)
+                    for (int64_t e = 0; e < dim0; ++e)
+                        in_grads[0]->set(r * dim0 + e, in_grads[0]->get(r * dim0 + e) + h[size_t(r * dim + e)]);
             }
             if (in_grads[1]) in_grads[1]->set(0, in_grads[1]->get(0) + download<float>(dp, 1)[0]);
             if (in_grads[2]) {
@@ -504,16 +590,18 @@ std::shared_ptr<CustomOp> make_interp_op(Tensor key_coords, NeighborIndex nbrs, 
     return op;
 }
 
-// Attention over a general NeighborIndex (make_attn_op, include/affmae/attention.hpp:84-86): the
-// decoder's cross (one_to_one) and self (knn) attention layers.  Rows of width <= 31.
-std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim, int bias_hidden,
-                                       double patch, bool streaming, bool half_io) {
+// Attention over a general NeighborIndex: the decoder's cross (one_to_one) and self (knn)
+// attention layers.  Rows of width <= 31.
+std::shared_ptr<CustomOp> make_general_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim,
+                                               int bias_hidden, double patch) {
     struct GAttnCudaOp final : CustomOp {
         Tensor coords;
         NeighborIndex nbr;
         int heads, head_dim, hidden;
         double patch;
         std::string name() const override { return "nbhd_attention_b200"; }
+        int dp() const { return padded_head_dim(head_dim); }
+        float qscale() const { return float(std::sqrt(double(dp()) / double(head_dim))); }
         struct Up {
             std::unique_ptr<Dev> t[10], coords, idx, valid;
             affmae_attn_inputs ai{};
@@ -523,7 +611,9 @@ std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int hea
             if (nbr.width < 1 || nbr.width > 31) throw ConfigError("attention op: neighbour width must be in [1, 31]");
             if (in[0]->rows() != nbr.queries()) throw ConfigError("attention op: row count does not match neighbor index");
             Up u;
-            for (int i = 0; i < 5; ++i) u.t[i] = upload(bf16(*in[size_t(i)]));
+            u.t[0] = upload(bf16_pad(*in[0], heads, head_dim, dp(), qscale()));
+            for (int i = 1; i < 3; ++i) u.t[i] = upload(bf16_pad(*in[size_t(i)], heads, head_dim, dp()));
+            for (int i = 3; i < 5; ++i) u.t[i] = upload(bf16_pad(*in[size_t(i)], 1, head_dim, dp()));
             for (int i = 5; i < 10; ++i) u.t[i] = upload(f32(*in[size_t(i)]));
             u.coords = upload(f32(coords));
             std::vector<int32_t> idx(nbr.idx.begin(), nbr.idx.end());
@@ -537,27 +627,30 @@ std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int hea
         }
         Tensor forward(const std::vector<const Tensor*>& in) override {
             Up u = upload_all(in);
-            const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
-            affmae_attn_desc a{heads, head_dim, hidden, patch};
-            Dev out(n * hd * 2), lse(n * heads * 4);
+            const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim, hdp = int64_t(heads) * dp();
+            affmae_attn_desc a{heads, dp(), hidden, patch};
+            Dev out(n * hdp * 2), lse(n * heads * 4);
             check(affmae_gattn_fwd(&a, &u.ai, u.idx->as<int32_t>(), u.valid->as<uint8_t>(), 1, n, nbr.width,
                                    out.as<affmae_bf16>(), lse.as<float>(), nullptr),
                   "gattn_fwd");
-            auto h = download<uint16_t>(out, size_t(n * hd));
+            auto h = download<uint16_t>(out, size_t(n * hdp));
             Tensor o = Tensor::zeros({n, hd}, in[0]->precision());
-            for (int64_t i = 0; i < n * hd; ++i) o.set(i, bf16_to_float(h[size_t(i)]));
+            for (int64_t r = 0; r < n; ++r)
+                for (int g = 0; g < heads; ++g)
+                    for (int e = 0; e < head_dim; ++e)
+                        o.set((r * heads + g) * head_dim + e, bf16_to_float(h[size_t(pad_at(r, g, e, heads, dp()))]));
             return o;
         }
         void backward(const Tensor& out_grad, const std::vector<const Tensor*>& in,
                       const std::vector<Tensor*>& in_grads) override {
             Up u = upload_all(in);
-            const int64_t n = in[0]->rows(), hd = int64_t(heads) * head_dim;
-            affmae_attn_desc a{heads, head_dim, hidden, patch};
-            auto dout = upload(bf16(out_grad));
-            const int64_t sz[10] = {n * hd, n * hd, n * hd, int64_t(heads) * head_dim, int64_t(heads) * head_dim,
+            const int64_t n = in[0]->rows(), hdp = int64_t(heads) * dp();
+            affmae_attn_desc a{heads, dp(), hidden, patch};
+            auto dout = upload(bf16_pad(out_grad, heads, head_dim, dp()));
+            const int64_t sz[10] = {n * hdp, n * hdp, n * hdp, int64_t(heads) * dp(), int64_t(heads) * dp(),
                                     heads * 2 * int64_t(hidden), int64_t(heads) * hidden, int64_t(heads) * hidden,
                                     heads, heads};
-            Dev dq(n * hd * 2);
+            Dev dq(n * hdp * 2);
             std::unique_ptr<Dev> g[10];
             for (int i = 1; i < 10; ++i) {
                 g[i] = std::make_unique<Dev>(sz[i] * 4);
@@ -570,20 +663,31 @@ std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int hea
                                    nullptr, 0, nullptr),
                   "gattn_bwd");
             ccheck(cudaDeviceSynchronize(), "sync");
+            auto put_rows = [&](Tensor* dst, const std::vector<float>& h, int64_t rows, int64_t groups, float sc) {
+                for (int64_t r = 0; r < rows; ++r)
+                    for (int64_t gq = 0; gq < groups; ++gq)
+                        for (int e = 0; e < head_dim; ++e) {
+                            const int64_t j = (r * groups + gq) * head_dim + e;
+                            dst->set(j, dst->get(j) + sc * h[size_t(pad_at(r, gq, e, groups, dp()))]);
+                        }
+            };
             if (in_grads[0]) {
-                auto h = download<uint16_t>(dq, size_t(n * hd));
-                for (int64_t j = 0; j < n * hd; ++j) in_grads[0]->set(j, in_grads[0]->get(j) + bf16_to_float(h[size_t(j)]));
+                auto h = download<uint16_t>(dq, size_t(n * hdp));
+                std::vector<float> f(h.size());
+                for (size_t j = 0; j < h.size(); ++j) f[j] = bf16_to_float(h[j]);
+                put_rows(in_grads[0], f, n, heads, qscale());
             }
             for (int i = 1; i < 10; ++i) {
                 Tensor* dst = in_grads[size_t(i)];
                 if (!dst) continue;
                 auto h = download<float>(*g[i], size_t(sz[i]));
-                for (int64_t j = 0; j < sz[i]; ++j) dst->set(j, dst->get(j) + h[size_t(j)]);
+                if (i <= 2) put_rows(dst, h, n, heads, 1.f);
+                else if (i <= 4) put_rows(dst, h, heads, 1, 1.f);
+                else
+                    for (int64_t j = 0; j < sz[i]; ++j) dst->set(j, dst->get(j) + h[size_t(j)]);
             }
         }
     };
-    (void)streaming;  // the device kernel is the streaming formulation; I/O is bf16 either way
-    (void)half_io;
     auto op = std::make_shared<GAttnCudaOp>();
     op->coords = std::move(coords);
     op->nbr = std::move(nbr);
@@ -592,6 +696,51 @@ std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int hea
     op->hidden = bias_hidden;
     op->patch = patch;
     return op;
+}
+
+// The (cluster size, groups) whose cluster_neighborhood (src/geometry.cpp:133-186) on `coords`
+// is exactly `nbr`, if any: the NeighborIndex rebuilt on the device for every (size, groups)
+// consistent with its width (width = groups_eff * ceil(n / C)) and compared entry for entry.
+bool detect_cluster_index(const Tensor& coords, const NeighborIndex& nbr, int64_t* size_out, int64_t* groups_out) {
+    const int64_t n = nbr.queries(), m = nbr.width;
+    if (n < 1 || m < 1 || coords.rows() != n) return false;
+    auto c = upload(f32(coords));
+    for (int64_t g = 1; g <= m; ++g) {
+        if (m % g) continue;
+        const int64_t mx = m / g;  // largest cluster
+        if (mx > 16) continue;     // compiled cluster kernels
+        for (int64_t s = mx; s <= 2 * mx + 1; ++s) {
+            affmae_cluster_geom geo{1, n, s, g, 0, 0, 0, 0};
+            if (affmae_cluster_geometry(&geo) != AFFMAE_OK || geo.width != m || geo.groups_eff != g) continue;
+            DeviceIndex d = build_index(*c, n, s, g);
+            Dev idx(n * m * 4), valid(n * m);
+            check(affmae_neighbor_expand(&d.g, d.perm->as<int32_t>(), d.nbr->as<int32_t>(), idx.as<int32_t>(),
+                                         valid.as<uint8_t>(), nullptr), "neighbor_expand");
+            ccheck(cudaDeviceSynchronize(), "sync");
+            auto hi = download<int32_t>(idx, size_t(n * m));
+            auto hv = download<uint8_t>(valid, size_t(n * m));
+            bool same = true;
+            for (size_t e = 0; same && e < hi.size(); ++e)
+                same = (hv[e] != 0) == (nbr.valid[e] != 0) && (!hv[e] || int64_t(hi[e]) == nbr.idx[e]);
+            if (same) {
+                *size_out = s;
+                *groups_out = g;
+                return true;
+            }
+        }
+    }
+    return false;
+}
+
+std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim, int bias_hidden,
+                                       double patch, bool streaming, bool half_io) {
+    (void)streaming;  // the device kernels are the streaming (online softmax) formulation
+    (void)half_io;    // activations are bf16 on the device either way
+    int64_t size = 0, groups = 0;
+    if (detect_cluster_index(coords, nbr, &size, &groups))
+        return make_cluster_attn_op(std::move(coords), size, groups, heads, head_dim, bias_hidden, patch);
+    if (nbr.width <= 31) return make_general_attn_op(std::move(coords), std::move(nbr), heads, head_dim, bias_hidden, patch);
+    throw ConfigError("cuda::make_attn_op: neighbour rows wider than 31 must be a cluster_neighborhood index");
 }
 
 MaskSpec perlin_mask(int64_t hp, int64_t wp, double ratio, uint64_t seed) {

@@ -27,6 +27,8 @@ namespace affmae::cuda {
 // balanced_clusters / cluster_neighborhood (include/affmae/geometry.hpp:61-68)
 ClusterAssignment balanced_clusters(const PointSet& points, int64_t size);
 NeighborIndex cluster_neighborhood_from_coords(const PointSet& points, int64_t size, int64_t groups);
+// cluster_neighborhood with the reference's signature (include/affmae/geometry.hpp:67)
+NeighborIndex cluster_neighborhood(const ClusterAssignment& assign, const PointSet& points, int64_t groups);
 // sfc_order / knn (include/affmae/geometry.hpp:59,72)
 std::vector<int64_t> sfc_order(const PointSet& points);
 NeighborIndex knn(const Tensor& queries, const PointSet& keys, int64_t k);
@@ -39,12 +41,18 @@ std::shared_ptr<CustomOp> make_cluster_attn_op(Tensor coords, int64_t cluster, i
                                                int heads, int head_dim, int bias_hidden,
                                                double patch);
 
-// Attention over a general NeighborIndex, same signature as the reference factory
-// (make_attn_op, include/affmae/attention.hpp:84-86): the decoder's cross / self
-// attention rows (one_to_one, knn; src/pipeline.cpp:515-525), width <= 31.
+// make_attn_op with the reference's exact signature (include/affmae/attention.hpp:84-86), a
+// drop-in for Model::attn_layer (src/pipeline.cpp:379-386).  A NeighborIndex that is a
+// cluster_neighborhood index of `coords` (detected: rebuilt on the device for the (size,
+// groups) its width allows and compared entry for entry) runs on the cluster kernels with
+// the frozen plan; any other index of width <= 31 (the decoder's one_to_one / knn rows,
+// src/pipeline.cpp:515-525) on the general-row kernels; anything else is a ConfigError.
 std::shared_ptr<CustomOp> make_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim,
                                        int bias_hidden, double patch, bool streaming = true,
                                        bool half_io = false);
+// the two device paths, explicitly
+std::shared_ptr<CustomOp> make_general_attn_op(Tensor coords, NeighborIndex nbr, int heads, int head_dim,
+                                               int bias_hidden, double patch);
 
 // Device-generated inputs: mask_from_field(perlin_field(hp, wp, kPerlinOctaves, kPerlinBaseFreq,
 // kPerlinPersistence, seed), ratio) (include/affmae/masking.hpp:31-40; bit-exact) and
@@ -55,7 +63,7 @@ Tensor synth_image(int64_t size, uint64_t seed);
 // select_retained / merge_plan / make_merge_pool_op (include/affmae/merging.hpp:32-68)
 std::vector<int64_t> select_retained(const Tensor& scores, double d_s);
 MergePlan merge_plan(const PointSet& ps, std::span<const int64_t> retained, int k_m);
-std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan, Tensor coords);
+std::shared_ptr<CustomOp> make_merge_pool_op(MergePlan plan);
 
 // Softmax interpolation tape op (make_interp_op, include/affmae/interpolation.hpp:60):
 // inputs {feats NxD, p 1x1, queries Qx2}; neighbour rows frozen at construction

@@ -91,7 +91,10 @@ int integ_attn_tape(int use_cuda, int64_t n, int heads, int d, int hidden, doubl
         for (int i = 0; i < 10; ++i) ids.push_back(t.leaf(from(ins[i], dims[size_t(i)])));
         PointSet ps = pts(coords, n);
         std::shared_ptr<CustomOp> op;
-        if (use_cuda) {
+        if (use_cuda == 2) {  // the reference's exact call, namespace-qualified (drop-in detection)
+            ClusterAssignment a = cuda::balanced_clusters(ps, cluster);
+            op = cuda::make_attn_op(ps.coords, cuda::cluster_neighborhood(a, ps, groups), heads, d, hidden, patch);
+        } else if (use_cuda) {
             op = cuda::make_cluster_attn_op(ps.coords, cluster, groups, heads, d, hidden, patch);
         } else {
             ClusterAssignment a = balanced_clusters(ps, cluster);
@@ -123,7 +126,7 @@ int integ_merge_tape(int use_cuda, int64_t n, int64_t dim, double d_s, int k_m, 
                 pool_idx[i * size_t(k_m) + size_t(t2)] = size_t(t2) < plan.pool[i].size() ? plan.pool[i][size_t(t2)] : -1;
         Tape t(Precision::b32);
         int f = t.leaf(from(feats, {n, dim})), s = t.leaf(sc), pp = t.leaf(Tensor::full({1, 1}, p, Precision::b32));
-        auto op = use_cuda ? cuda::make_merge_pool_op(plan, ps.coords) : make_merge_pool_op(plan);
+        auto op = use_cuda ? cuda::make_merge_pool_op(plan) : make_merge_pool_op(plan);
         int o = t.custom(op, {f, s, pp});
         int loss = t.reduce_sum(t.mul(o, t.input(from(w, {int64_t(r.size()), 2 * dim}))));
         t.backward(loss);

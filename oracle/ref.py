@@ -315,8 +315,14 @@ class RefModel:
     """The reference Model (proj/src/pipeline.cpp:255-746) through ref_shim.cpp, built from the
     same affmae_model_cfg struct the device model takes (paper_2602_16249_b200.model.ModelCfg)."""
 
-    def __init__(self, cfg_struct):
-        L = lib()
+    def __init__(self, cfg_struct, library=None):
+        """library: a ctypes CDLL exporting the ref_model_* shim (default oracle/_ref; the
+        drop-in test passes integration/libaffmae_model_b200.so -- the same reference Model
+        with its hot-path calls on the B200 adapters)."""
+        L = library or lib()
+        if not hasattr(L, "ref_last_error") or L.ref_last_error.restype is not C.c_char_p:
+            L.ref_last_error.restype = C.c_char_p
+        self.L = L
         L.ref_model_create.restype = C.c_void_p
         L.ref_model_param_name.restype = C.c_char_p
         L.ref_model_param_numel.restype = C.c_int64
@@ -331,15 +337,20 @@ class RefModel:
         self.names = [L.ref_model_param_name(self.h, C.c_int(i)).decode() for i in range(n)]
         self.numel = [int(L.ref_model_param_numel(self.h, C.c_int(i))) for i in range(n)]
 
+    def _check(self, rc):
+        if rc != 0:
+            msg = self.L.ref_last_error().decode()
+            raise (ValueError if rc == 2 else ArithmeticError if rc == 3 else RuntimeError)(msg)
+
     def __del__(self):
         try:
-            lib().ref_model_destroy(self.h)
+            self.L.ref_model_destroy(self.h)
         except Exception:
             pass
 
     def _get(self, which):
         out = np.empty(int(sum(self.numel)))
-        _check(lib().ref_model_get(self.h, C.c_int(which), _p(out)))
+        self._check(self.L.ref_model_get(self.h, C.c_int(which), _p(out)))
         res, o = {}, 0
         for n, z in zip(self.names, self.numel):
             res[n] = out[o:o + z].copy()
@@ -354,7 +365,7 @@ class RefModel:
 
     def set_params(self, values):
         flat = np.concatenate([np.asarray(values[n], np.float64).ravel() for n in self.names])
-        _check(lib().ref_model_set(self.h, _p(flat)))
+        self._check(self.L.ref_model_set(self.h, _p(flat)))
 
     def fwd_bwd(self, image, masked, tokens_per_stage, dims):
         """-> ((total, main, aux), [coords of each stage], [stage features (pre-merge)]);
@@ -364,7 +375,7 @@ class RefModel:
         loss = np.zeros(3)
         coords = np.zeros(int(sum(tokens_per_stage)) * 2, np.float32)
         feats = np.zeros(int(sum(n * d for n, d in zip(tokens_per_stage, dims))))
-        _check(lib().ref_model_fwd_bwd(self.h, _p(image), C.c_int64(image.shape[0]), _p(masked), _p(loss),
+        self._check(self.L.ref_model_fwd_bwd(self.h, _p(image), C.c_int64(image.shape[0]), _p(masked), _p(loss),
                                        _p(coords), _p(feats)))
         co, fo, a, b = [], [], 0, 0
         for n, d in zip(tokens_per_stage, dims):
@@ -377,16 +388,32 @@ class RefModel:
     def train(self, steps, images):
         images = _f64(images)
         losses = np.zeros(steps)
-        _check(lib().ref_model_train(self.h, C.c_int64(steps), C.c_int64(images.shape[0]), _p(images),
+        self._check(self.L.ref_model_train(self.h, C.c_int64(steps), C.c_int64(images.shape[0]), _p(images),
                                      C.c_int64(images.shape[1]), _p(losses)))
         return losses
 
     def make_mask(self, seed):
         g = self._cs.image // self._cs.patch
         m = np.zeros(g * g, np.uint8)
-        _check(lib().ref_model_make_mask(self.h, C.c_uint64(seed), _p(m)))
+        self._check(self.L.ref_model_make_mask(self.h, C.c_uint64(seed), _p(m)))
         return m.reshape(g, g)
 
+
+
+_model_b200 = None
+
+
+def model_b200_lib():
+    """integration/libaffmae_model_b200.so: the reference's pipeline.cpp compiled unmodified
+    with its hot-path calls redirected to the B200 adapters (integration/redirect_b200.hpp)."""
+    global _model_b200
+    if _model_b200 is None:
+        path = os.path.join(os.path.dirname(_HERE), "integration", "libaffmae_model_b200.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"drop-in model library not built: {path} (make -C integration)")
+        _model_b200 = C.CDLL(path)
+        _model_b200.ref_last_error.restype = C.c_char_p
+    return _model_b200
 
 
 def model_train_threads(cfg_struct, threads, images_per_thread, image):

@@ -41,7 +41,8 @@ EXPORTS = (
     "affmae_model_param_dims", "affmae_model_get_params", "affmae_model_set_params", "affmae_model_get_grads",
     "affmae_model_inputs", "affmae_model_make_masks", "affmae_model_forward_backward", "affmae_model_apply_step",
     "affmae_model_train_step", "affmae_model_grad_buffer", "affmae_model_save", "affmae_model_load",
-    "affmae_model_stage_output", "affmae_model_force_retained",
+    "affmae_model_stage_output", "affmae_model_force_retained", "affmae_model_forward",
+    "affmae_model_reset_optimizer", "affmae_hilbert_index",
 )
 
 
@@ -102,6 +103,9 @@ def lib():
         L.affmae_last_error.restype = C.c_char_p
         L.affmae_retained_count.restype = C.c_int64
         L.affmae_retained_count.argtypes = [C.c_int64, C.c_double]
+        if hasattr(L, "affmae_hilbert_index"):
+            L.affmae_hilbert_index.restype = C.c_uint64
+            L.affmae_hilbert_index.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
         for f in ("affmae_flop_count_attn", "affmae_flop_count_attn_dense"):
             if hasattr(L, f):
                 getattr(L, f).restype = C.c_uint64

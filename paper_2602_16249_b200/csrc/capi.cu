@@ -79,6 +79,9 @@ int affmae_attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a,
     )
 }
 
+// hilbert_index (proj/src/geometry.cpp:15-30): d of cell (x, y) on a side-n grid (n a power of 2)
+uint64_t affmae_hilbert_index(uint32_t n, uint32_t x, uint32_t y) { return hilbert_index_host(n, x, y); }
+
 // flop_count_attn / flop_count_attn_dense (proj/src/attention.cpp:360-370)
 uint64_t affmae_flop_count_attn(int64_t n, int64_t m, int64_t h, int64_t d) {
     if (n < 1 || m < 1 || h < 1 || d < 1) {

@@ -55,12 +55,15 @@ __global__ void __launch_bounds__(kDecWarps * 32) norm_clamp_bwd_kernel(const __
         s = warp_sum_f(s);
         dot = warp_sum_f(dot);
         const float nrm = sqrtf(s);
+        // ACCUMULATES into dx (NormClampOp::backward, pipeline.cpp:104-125: dx += J^T g)
         if (nrm <= limit) {
-            for (int j = lane; j < d; j += 32) dx[r * d + j] = gr[j];
+            for (int j = lane; j < d; j += 32)
+                dx[r * d + j] = __float2bfloat16(__bfloat162float(dx[r * d + j]) + __bfloat162float(gr[j]));
         } else {
             const float f = limit / nrm, c = dot / s;
             for (int j = lane; j < d; j += 32)
-                dx[r * d + j] = __float2bfloat16(f * (__bfloat162float(gr[j]) - c * __bfloat162float(xr[j])));
+                dx[r * d + j] = __float2bfloat16(__bfloat162float(dx[r * d + j]) +
+                                                 f * (__bfloat162float(gr[j]) - c * __bfloat162float(xr[j])));
         }
     }
 }

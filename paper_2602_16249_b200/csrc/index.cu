@@ -21,7 +21,7 @@
 namespace affmae_b200 {
 
 // hilbert_index, proj/src/geometry.cpp:15-30
-__device__ __forceinline__ uint64_t hilbert(uint32_t n, uint32_t x, uint32_t y) {
+__host__ __device__ __forceinline__ uint64_t hilbert(uint32_t n, uint32_t x, uint32_t y) {
     uint64_t d = 0;
     for (uint32_t s = n / 2; s > 0; s /= 2) {
         uint32_t rx = (x & s) ? 1u : 0u;
@@ -39,6 +39,8 @@ __device__ __forceinline__ uint64_t hilbert(uint32_t n, uint32_t x, uint32_t y) 
     }
     return d;
 }
+
+uint64_t hilbert_index_host(uint32_t n, uint32_t x, uint32_t y) { return hilbert(n, x, y); }
 
 // ---------------------------------------------------------- sfc_order
 __global__ void axis_keys_kernel(const float* __restrict__ coords, int64_t batch, int64_t n,

@@ -97,6 +97,8 @@ int merge_pool_bwd(const affmae_bf16*, const float*, const float*, const int32_t
                    const affmae_bf16*, affmae_bf16*, float*, float*, void*, size_t, void*);
 
 
+// index.cu: hilbert_index (proj/src/geometry.cpp:15-30) on the host
+uint64_t hilbert_index_host(uint32_t n, uint32_t x, uint32_t y);
 // optim.cu: AdamW with the step count on the device (advanced by the call) and the bf16
 // shadow of the first n_shadow values refreshed in the same pass
 int adamw_step_dev(const affmae_adamw_cfg* c, int64_t* step_dev, void* scalars_dev, int64_t n_segments,

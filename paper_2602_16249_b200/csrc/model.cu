@@ -1282,6 +1282,34 @@ int affmae_model_forward_backward(affmae_model* m, float* loss3, void* stream) {
         return AFFMAE_OK;)
 }
 
+int affmae_model_forward(affmae_model* m, float* loss3, void* stream) {
+    if (!m) return fail(AFFMAE_ECONFIG, "model_forward: null model");
+    AFFMAE_MGUARD(
+        cudaStream_t st = as_stream(stream);
+        Ctx x{*m, st};
+        if (int rc = forward(x)) return rc;
+        if (loss3 && cudaMemcpyAsync(loss3, m->loss, 12, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "model loss copy");
+        return AFFMAE_OK;)
+}
+
+int affmae_model_reset_optimizer(affmae_model* m, int64_t total_steps) {
+    if (!m) return fail(AFFMAE_ECONFIG, "model_reset_optimizer: null model");
+    if (total_steps < 1) return fail(AFFMAE_ECONFIG, "optimizer needs at least one step");
+    m->cfg.optim.total_steps = total_steps;
+    const int64_t zero = 0;
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemset(m->M1, 0, size_t(m->nvals) * 4) != cudaSuccess ||
+        cudaMemset(m->V1, 0, size_t(m->nvals) * 4) != cudaSuccess ||
+        cudaMemcpy(m->step_dev, &zero, 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        return cuda_status(cudaGetLastError(), "model_reset_optimizer");
+    m->steps = 0;
+    if (m->gexec) {  // the captured step bakes the schedule's total_steps
+        cudaGraphExecDestroy(m->gexec);
+        m->gexec = nullptr;
+    }
+    return AFFMAE_OK;
+}
+
 int affmae_model_apply_step(affmae_model* m, void* stream) {
     if (!m) return fail(AFFMAE_ECONFIG, "model_apply_step: null model");
     AFFMAE_MGUARD(

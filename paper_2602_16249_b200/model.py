@@ -144,7 +144,8 @@ def _lib():
                   "affmae_model_get_grads", "affmae_model_inputs", "affmae_model_make_masks",
                   "affmae_model_forward_backward", "affmae_model_apply_step", "affmae_model_train_step",
                   "affmae_model_grad_buffer", "affmae_model_save", "affmae_model_load",
-                  "affmae_model_stage_output", "affmae_model_force_retained"):
+                  "affmae_model_stage_output", "affmae_model_force_retained", "affmae_model_forward",
+                  "affmae_model_reset_optimizer"):
             getattr(L, f).argtypes = None
         L._model_bound = True
     return L
@@ -250,6 +251,17 @@ class Model:
         capi.check(_lib().affmae_model_forward_backward(self._h, C.c_void_p(lb.ptr), C.c_void_p(stream)),
                    "model_forward_backward")
         return tuple(float(x) for x in devmem.d2h(lb.ptr, (3,), np.float32, stream))
+
+    def forward(self, stream=None):
+        """encode + decode + deep_sup + loss_parts without the backward -> (total, main, aux)."""
+        from . import devmem
+        lb = self._loss_buf()
+        capi.check(_lib().affmae_model_forward(self._h, C.c_void_p(lb.ptr), C.c_void_p(stream)), "model_forward")
+        return tuple(float(x) for x in devmem.d2h(lb.ptr, (3,), np.float32, stream))
+
+    def reset_optimizer(self, total_steps):
+        """A fresh AdamW(cfg.optim, total_steps), as the reference's train() builds per call."""
+        capi.check(_lib().affmae_model_reset_optimizer(self._h, C.c_int64(total_steps)), "model_reset_optimizer")
 
     def apply_step(self, stream=None):
         capi.check(_lib().affmae_model_apply_step(self._h, C.c_void_p(stream)), "model_apply_step")

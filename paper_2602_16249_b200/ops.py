@@ -639,10 +639,11 @@ def norm_clamp(x, limit, stream=None):
     return y
 
 
-def norm_clamp_bwd(x, g, limit, stream=None):
-    """NormClampOp VJP (proj/src/pipeline.cpp:99-125) -> dx bf16."""
+def norm_clamp_bwd(x, g, limit, dx=None, stream=None):
+    """NormClampOp VJP (proj/src/pipeline.cpp:99-125): dx (bf16) += J^T g; a new zero dx
+    unless one is given to accumulate into."""
     _req(g, torch.bfloat16, "g")
-    dx = torch.empty_like(x)
+    dx = torch.zeros_like(x) if dx is None else dx
     capi.check(capi.lib().affmae_norm_clamp_bwd(C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()),
                                                 C.c_int64(x.shape[0]), C.c_int64(x.shape[1]), C.c_double(limit),
                                                 C.c_void_p(dx.data_ptr()), _stream(stream)), "norm_clamp_bwd")

@@ -28,6 +28,12 @@ def test_norm_clamp_fwd_bwd(rows, d, limit):
     dot = (g64 * x64).sum(1, keepdims=True) / np.maximum(r * r, 1e-300)
     want = np.where(r <= limit, g64, f * (g64 - dot * x64))
     assert _rel(dx, want) <= 1e-2
+    # CustomOp::backward semantics: a second call accumulates into the same dx
+    base = bf16_round(rng.standard_normal((rows, d)).astype(np.float32))
+    acc = torch.as_tensor(base, device="cuda").to(torch.bfloat16)
+    ops.norm_clamp_bwd(torch.as_tensor(x, device="cuda").to(torch.bfloat16),
+                       torch.as_tensor(g, device="cuda").to(torch.bfloat16), limit, dx=acc)
+    assert _rel(acc.float().cpu().numpy(), base + want) <= 1e-2
 
 
 @pytest.mark.gpu
