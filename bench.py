@@ -190,11 +190,13 @@ def make_inputs(a, rank):
 
 
 def algorithmic_bytes(a, N):
-    """Per-token algorithmic HBM bytes: what each op must read/write once."""
+    """Per-token algorithmic HBM bytes, SURVEY.md §8(d)'s figures."""
     D, h = a.heads * a.head_dim, a.heads
     return {
         "attn_fwd": 8 * D + 4 * h + 8,         # q,k,v read + o write (bf16), lse write, coords
-        "attn_bwd": 14 * D + 4 * h + 8,        # q,k,v,dO read + dq,dk,dv write, lse, coords
+        # §8(d): 16 D + 4h -- q,k,v,o,dO read + dq,dk,dv write (bf16) + lse; this backward does
+        # not read o (D = rowsum(P dP) is recomputed), so it moves 14 D + 4h + 8 of them
+        "attn_bwd": 16 * D + 4 * h,
         "index": 8 + 4 + 4 + 4 * a.groups / a.cluster,  # coords in; perm, cluster_of, nbr ids out
         "merge": 4 + 8 + 2 * D + 4 + a.d_s * (4 + 4 * D + 12 * a.k_m),  # fwd side (SURVEY §8d)
     }
@@ -886,7 +888,7 @@ def model_flops(cfg, tokens, q):
     return 3 * gemm + 3.5 * attn, gemm, attn
 
 
-def run_pretrain(cfg, steps, warmup=2, e2e_steps=3, label=""):
+def run_pretrain(cfg, steps, warmup=2, e2e_steps=3, label="", rank=0, world=1, dist=None):
     """One training step of `cfg` (masks -> encode -> decode -> deep supervision -> loss ->
     backward -> AdamW) through the torch-free model API, captured as one CUDA graph; device
     img/s, plus e2e img/s with the step's images copied H2D from pinned host memory and the
@@ -898,11 +900,19 @@ def run_pretrain(cfg, steps, warmup=2, e2e_steps=3, label=""):
     m = Model(cfg)
     create_s = time.perf_counter() - t0
     B = cfg.batch
+    if world > 1:  # images shard over ranks; NCCL all-reduce of the gradients inside the step graph
+        import torch
+        from paper_2602_16249_b200.model import nccl_unique_id
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        m.set_world(world, rank, bytes(idt.cpu().numpy()))
     st = devmem.stream_create()
     L = capi.lib()
     wsb = L.affmae_synth_images_workspace(C.c_int64(B), C.c_int64(cfg.image))
     ws = devmem.DeviceBuffer(wsb)
-    seeds = np.arange(400, 400 + B, dtype=np.uint64)
+    seeds = np.arange(400 + rank * B, 400 + (rank + 1) * B, dtype=np.uint64)  # global image index
     capi.check(L.affmae_synth_images(seeds.ctypes.data_as(C.c_void_p), C.c_int64(B), C.c_int64(cfg.image),
                                      C.c_void_p(m.images_ptr), C.c_void_p(ws.ptr), C.c_size_t(wsb), C.c_void_p(st)))
     devmem.sync(st)
@@ -915,39 +925,53 @@ def run_pretrain(cfg, steps, warmup=2, e2e_steps=3, label=""):
     def one(e2e=False):
         if e2e:
             devmem.h2d_async(m.images_ptr, pinned.ptr, img_bytes, st)
-        m.make_masks([step_mask_seed(cfg.seed, step[0] * B + i) for i in range(B)], stream=st)
+        m.make_masks([step_mask_seed(cfg.seed, (step[0] * world + rank) * B + i) for i in range(B)], stream=st)
         m.train_step(use_graph=True, stream=st, read_loss=False)
         if e2e:
             devmem.d2h_async(loss_host.ptr, m._loss_buf().ptr, 12, st)
         step[0] += 1
 
+    def maxr(v):
+        if dist is None:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(warmup):
         one()
     devmem.sync(st)
+    if dist is not None:
+        dist.barrier()
     e0, e1 = devmem.Event(), devmem.Event()
     e0.record(st)
     for _ in range(steps):
         one()
     e1.record(st)
     e1.synchronize()
-    ms = e0.elapsed_ms(e1) / steps
+    ms = maxr(e0.elapsed_ms(e1) / steps)
+    if dist is not None:
+        dist.barrier()
     e0.record(st)
     for _ in range(e2e_steps):
         one(e2e=True)
     e1.record(st)
     e1.synchronize()
-    ms_e2e = e0.elapsed_ms(e1) / e2e_steps
+    ms_e2e = maxr(e0.elapsed_ms(e1) / e2e_steps)
     loss = devmem.d2h(m._loss_buf().ptr, (3,), np.float32)
     flops, gemm_f, attn_f = model_flops(cfg, m.tokens, m.masked)
     peak = load_bf16_peak()
     tflops = flops * B / (ms * 1e-3) / 1e12
-    out = {"config": label, "image": cfg.image, "batch": B, "params": int(m.n_values),
+    tflops = tflops * world
+    out = {"config": label, "image": cfg.image, "batch_per_gpu": B, "n_gpus": world, "params": int(m.n_values),
            "tokens_per_stage": [int(t) for t in m.tokens], "masked_per_image": int(m.masked),
-           "ms_per_step": ms, "img_s": B / (ms * 1e-3),
-           "e2e": {"img_s": B / (ms_e2e * 1e-3), "ms_per_step": ms_e2e, "h2d_bytes_per_step": img_bytes,
+           "ms_per_step": ms, "img_s": world * B / (ms * 1e-3), "scaling": "weak",
+           "grad_allreduce": "ncclAllReduce(sum) of the fp32 gradient arena in the step graph" if world > 1 else None,
+           "e2e": {"img_s": world * B / (ms_e2e * 1e-3), "ms_per_step": ms_e2e, "h2d_bytes_per_step": img_bytes,
                    "d2h_bytes_per_step": 12},
            "flops_per_image": flops, "tflops": tflops, "bf16_peak_tflops": peak,
-           "frac_bf16_peak": tflops / peak, "loss": [float(x) for x in loss],
+           "frac_bf16_peak": tflops / (peak * world), "loss": [float(x) for x in loss],
            "device_gib": m.device_bytes / 2 ** 30, "create_s": create_s, "cuda_graph": True,
            "step": "masks + encode + decode + deep sup + loss + backward + AdamW (one graph)"}
     m.close()
@@ -1116,6 +1140,35 @@ def load_traffic(kernel, cfg_key):
         return None
 
 
+def run_pretrain_legs(a, rank, world, dist):
+    """BASELINE configs[2] (and configs[0]'s shape): the device training step, all ranks."""
+    pre = None
+    if a.pretrain_batch > 0 or a.tiny_batch > 0:
+        from paper_2602_16249_b200.model import aff_tiny, affmae_b
+        pre = {}
+        try:
+            if a.pretrain_batch > 0:
+                pre["affmae_b_1024"] = run_pretrain(affmae_b(image=1024, batch=a.pretrain_batch),
+                                                    a.pretrain_steps, label="AFFMAE-B 1024^2, 75% mask, deep sup",
+                                                    rank=rank, world=world, dist=dist)
+            if a.tiny_batch > 0:
+                cfg_t = aff_tiny(batch=a.tiny_batch)
+                pre["aff_tiny_224"] = run_pretrain(cfg_t, a.pretrain_steps, label="AFF-tiny 224^2, 75% mask",
+                                                   rank=rank, world=world, dist=dist)
+                if not a.no_cpu_baseline and world == 1:
+                    from oracle import ref
+                    if ref.available():
+                        th = host_threads()
+                        v, dt = ref_pretrain_sample(cfg_t, th)
+                        pre["aff_tiny_224"]["cpu_reference"] = {
+                            "img_s": v, "cores": th, "kind": "reference",
+                            "sample": f"{th} images, one train() step each on its own Model replica, {dt:.1f} s"}
+                        pre["aff_tiny_224"]["speedup_vs_reference"] = pre["aff_tiny_224"]["img_s"] / v
+        except Exception as e:  # pragma: no cover
+            pre["error"] = str(e)
+    return pre
+
+
 def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -1131,6 +1184,7 @@ def main():
         tdist.init_process_group("nccl")
         dist = tdist
     res = run_ours(a, rank, world, dist)
+    pre = run_pretrain_legs(a, rank, world, dist)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -1185,27 +1239,7 @@ def main():
             line["parity"] = same_run_parity(a)
         except Exception as e:  # pragma: no cover
             line["parity"] = {"error": str(e)}
-    if world == 1 and (a.pretrain_batch > 0 or a.tiny_batch > 0):
-        from paper_2602_16249_b200.model import aff_tiny, affmae_b
-        pre = {}
-        try:
-            if a.pretrain_batch > 0:
-                pre["affmae_b_1024"] = run_pretrain(affmae_b(image=1024, batch=a.pretrain_batch),
-                                                    a.pretrain_steps, label="AFFMAE-B 1024^2, 75% mask, deep sup")
-            if a.tiny_batch > 0:
-                cfg_t = aff_tiny(batch=a.tiny_batch)
-                pre["aff_tiny_224"] = run_pretrain(cfg_t, a.pretrain_steps, label="AFF-tiny 224^2, 75% mask")
-                if not a.no_cpu_baseline:
-                    from oracle import ref
-                    if ref.available():
-                        th = host_threads()
-                        v, dt = ref_pretrain_sample(cfg_t, th)
-                        pre["aff_tiny_224"]["cpu_reference"] = {
-                            "img_s": v, "cores": th, "kind": "reference",
-                            "sample": f"{th} images, one train() step each on its own Model replica, {dt:.1f} s"}
-                        pre["aff_tiny_224"]["speedup_vs_reference"] = pre["aff_tiny_224"]["img_s"] / v
-        except Exception as e:  # pragma: no cover
-            pre["error"] = str(e)
+    if pre is not None:
         line["pretrain"] = pre
     if not a.no_cpu_baseline and world == 1:
         try:

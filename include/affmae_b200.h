@@ -500,6 +500,14 @@ int affmae_model_stage_output(affmae_model* m, int stage, float* coords_host, fl
  * token indices, e.g. the reference's retained set) instead of select_retained on the device
  * scores; NULL restores the model's own selection.  Everything else is unchanged. */
 int affmae_model_force_retained(affmae_model* m, int stage, const int32_t* retained_host);
+/* Data parallelism: images shard over `world` ranks (one process per GPU).
+ * The loss gradient is seeded with 1/world, so the SUM of the ranks' gradients is the gradient
+ * of the global batch mean.  nccl_id (from affmae_nccl_unique_id on rank 0, broadcast by the
+ * caller) makes every forward_backward end with an ncclAllReduce(sum) of the gradient arena
+ * on the model's stream (inside the step's graph); NULL leaves the sum to the caller (e.g. a
+ * host-staged gloo all-reduce between forward_backward and apply_step). */
+int affmae_nccl_unique_id(uint8_t* out128);
+int affmae_model_set_world(affmae_model* m, int world, int rank, const uint8_t* nccl_id);
 /* flat fp32 gradient arena on the device (for the data-parallel all-reduce between
  * forward_backward and apply_step) */
 int affmae_model_grad_buffer(affmae_model* m, float** grad, int64_t* n);

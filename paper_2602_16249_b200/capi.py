@@ -42,7 +42,7 @@ EXPORTS = (
     "affmae_model_inputs", "affmae_model_make_masks", "affmae_model_forward_backward", "affmae_model_apply_step",
     "affmae_model_train_step", "affmae_model_grad_buffer", "affmae_model_save", "affmae_model_load",
     "affmae_model_stage_output", "affmae_model_force_retained", "affmae_model_forward",
-    "affmae_model_reset_optimizer", "affmae_hilbert_index",
+    "affmae_model_reset_optimizer", "affmae_hilbert_index", "affmae_nccl_unique_id", "affmae_model_set_world",
 )
 
 

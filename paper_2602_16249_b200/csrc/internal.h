@@ -5,6 +5,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "affmae_b200.h"
 
 namespace affmae_b200 {
@@ -99,6 +101,11 @@ int merge_pool_bwd(const affmae_bf16*, const float*, const float*, const int32_t
 
 // index.cu: hilbert_index (proj/src/geometry.cpp:15-30) on the host
 uint64_t hilbert_index_host(uint32_t n, uint32_t x, uint32_t y);
+// dist.cu: NCCL loaded at run time (no link-time dependency)
+int nccl_unique_id(uint8_t* out128);
+int nccl_comm_init(const uint8_t* id128, int nranks, int rank, void** comm);
+int nccl_allreduce_sum_f32(void* comm, float* buf, int64_t n, cudaStream_t st);
+void nccl_comm_destroy(void* comm);
 // optim.cu: AdamW with the step count on the device (advanced by the call) and the bf16
 // shadow of the first n_shadow values refreshed in the same pass
 int adamw_step_dev(const affmae_adamw_cfg* c, int64_t* step_dev, void* scalars_dev, int64_t n_segments,

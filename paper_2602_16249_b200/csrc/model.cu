@@ -203,6 +203,8 @@ struct affmae_model {
                   *B6 = nullptr, *dfbf = nullptr, *dfq_bf = nullptr;
 
     int64_t steps = 0;
+    int world = 1;          // data-parallel ranks: the loss gradient is seeded with 1/world
+    void* comm = nullptr;   // NCCL communicator (dist.cu) or null (single GPU / caller reduces)
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t gstream = nullptr;
     float* gloss = nullptr;
@@ -809,11 +811,14 @@ int forward(const Ctx& x) {
         }
     }
     // loss_parts (pipeline.cpp:581-610): the mse gradients are written here too
-    CK(masked_mse(m.recon, m.patches, m.msk_rows, Mq, p2, m.loss + 1, m.drecon, 1.0f, m.ws, m.ws_bytes, x.sv()));
+    // gradient seed 1/world: after the sum over ranks the gradient is that of the GLOBAL batch mean
+    const double seed = 1.0 / double(m.world);
+    CK(masked_mse(m.recon, m.patches, m.msk_rows, Mq, p2, m.loss + 1, m.drecon, float(seed), m.ws, m.ws_bytes,
+                  x.sv()));
     for (int s = 0; s < n_aux; ++s) {
         Stage& S = m.st[size_t(s)];
         CK(masked_mse(S.aout, m.patches, m.msk_rows, Mq, p2, m.loss + 3 + s, S.daux,
-                      float(c.lambda_aux / double(n_aux)), m.ws, m.ws_bytes, x.sv()));
+                      float(seed * c.lambda_aux / double(n_aux)), m.ws, m.ws_bytes, x.sv()));
     }
     loss_combine_kernel<<<1, 1, 0, x.st>>>(m.loss, n_aux, float(c.lambda_aux));
     AFFMAE_LAUNCH_CHECK("loss_combine_kernel");
@@ -1014,7 +1019,10 @@ int forward_backward(Model& m, cudaStream_t st) {
     if (cudaMemsetAsync(m.G, 0, size_t(m.nvals) * 4, st) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "model zero_grads");
     CK(forward(x));
-    return backward(x);
+    CK(backward(x));
+    // the step's one exchange: sum the gradient arena over the data-parallel ranks
+    if (m.comm) return nccl_allreduce_sum_f32(m.comm, m.G, m.nvals, st);
+    return AFFMAE_OK;
 }
 
 int apply_step(Model& m, cudaStream_t st) {
@@ -1189,6 +1197,7 @@ int affmae_model_create(const affmae_model_cfg* cfg, affmae_model** out) { AFFMA
 void affmae_model_destroy(affmae_model* m) {
     if (!m) return;
     if (m->gexec) cudaGraphExecDestroy(m->gexec);
+    if (m->comm) nccl_comm_destroy(m->comm);
     if (m->dmem) cudaFree(m->dmem);
     delete m;
 }
@@ -1388,6 +1397,25 @@ int affmae_model_force_retained(affmae_model* m, int stage, const int32_t* retai
         return cuda_status(cudaGetLastError(), "model_force_retained");
     S.forced = true;
     return AFFMAE_OK;
+}
+
+int affmae_nccl_unique_id(uint8_t* out128) { AFFMAE_MGUARD(return nccl_unique_id(out128);) }
+
+int affmae_model_set_world(affmae_model* m, int world, int rank, const uint8_t* nccl_id) {
+    if (!m || world < 1 || rank < 0 || rank >= world) return fail(AFFMAE_ECONFIG, "model_set_world: bad arguments");
+    AFFMAE_MGUARD(
+        if (m->comm) {
+            nccl_comm_destroy(m->comm);
+            m->comm = nullptr;
+        }
+        if (nccl_id && world > 1)
+            if (int rc = nccl_comm_init(nccl_id, world, rank, &m->comm)) return rc;
+        m->world = world;
+        if (m->gexec) {  // the captured step bakes the loss seed and the exchange
+            cudaGraphExecDestroy(m->gexec);
+            m->gexec = nullptr;
+        }
+        return AFFMAE_OK;)
 }
 
 int affmae_model_grad_buffer(affmae_model* m, float** grad, int64_t* n) {

@@ -145,7 +145,7 @@ def _lib():
                   "affmae_model_forward_backward", "affmae_model_apply_step", "affmae_model_train_step",
                   "affmae_model_grad_buffer", "affmae_model_save", "affmae_model_load",
                   "affmae_model_stage_output", "affmae_model_force_retained", "affmae_model_forward",
-                  "affmae_model_reset_optimizer"):
+                  "affmae_model_reset_optimizer", "affmae_nccl_unique_id", "affmae_model_set_world"):
             getattr(L, f).argtypes = None
         L._model_bound = True
     return L
@@ -297,6 +297,27 @@ class Model:
         capi.check(_lib().affmae_model_force_retained(self._h, C.c_int(stage), r.ctypes.data_as(C.c_void_p)),
                    "model_force_retained")
 
+    def set_world(self, world, rank, nccl_id=None):
+        """Data-parallel rank `rank` of `world`: the loss gradient is seeded with 1/world;
+        with nccl_id (bytes of nccl_unique_id() from rank 0) every forward_backward ends with
+        an NCCL all-reduce of the gradients, without it the caller sums them."""
+        idb = None
+        if nccl_id is not None:
+            idb = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+        capi.check(_lib().affmae_model_set_world(self._h, C.c_int(world), C.c_int(rank), idb), "model_set_world")
+
+    def grads_device_to_host(self):
+        """the flat gradient arena (device layout) as a host fp32 array"""
+        from . import devmem
+        p, n = self.grad_buffer()
+        return devmem.d2h(p, (n,), np.float32)
+
+    def grads_host_to_device(self, flat):
+        from . import devmem
+        p, n = self.grad_buffer()
+        assert flat.size == n
+        devmem.h2d(p, np.ascontiguousarray(flat, np.float32))
+
     def grad_buffer(self):
         p, n = C.c_void_p(), C.c_int64()
         capi.check(_lib().affmae_model_grad_buffer(self._h, C.byref(p), C.byref(n)))
@@ -307,6 +328,13 @@ class Model:
 
     def load(self, directory):
         capi.check(_lib().affmae_model_load(self._h, str(directory).encode()), "model_load")
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0; broadcast it to the other ranks)."""
+    buf = (C.c_uint8 * 128)()
+    capi.check(_lib().affmae_nccl_unique_id(buf), "nccl_unique_id")
+    return bytes(buf)
 
 
 def with_batch(cfg: PipelineConfig, batch: int) -> PipelineConfig:
