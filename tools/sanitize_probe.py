@@ -41,7 +41,7 @@ def attn_round(coords, heads, hd, rng):
 
 def main():
     rng = np.random.default_rng(0)
-    which = sys.argv[1:] or ["index", "attn", "merge", "masks", "decoder"]
+    which = sys.argv[1:] or ["index", "attn", "merge", "masks", "decoder", "model"]
     lat = inputs.lattice_batch(3, 48, 0.75, 8, 1000)  # N = 576, 3 images
     if "index" in which:
         ops.cluster_index(dev(lat, torch.float32), 16, 3)
@@ -84,6 +84,22 @@ def main():
         ops.interp_bwd(qs, keys, f, idx, valid, p, torch.randn_like(out))
         torch.cuda.synchronize()
         print("decoder ok", flush=True)
+    if "model" in which:
+        model_round()
+        print("model ok", flush=True)
+
+
+def model_round():
+    """one training step of a small two-stage model: every model kernel (row LN fwd/bwd, pos
+    MLP, scorer, offset head, gathers, bias column sums, AdamW with the device step)"""
+    from paper_2602_16249_b200.model import Model, PipelineConfig, StageConfig, step_mask_seed
+    st = [StageConfig(64, 2, 2, 16, 3, 0.4, 8), StageConfig(128, 4, 1, 8, 3, 0.4, 8)]
+    m = Model(PipelineConfig(image=64, patch=8, stages=st, dec_dim=64, dec_heads=2, mask_ratio=0.5, batch=2))
+    rng = np.random.default_rng(1)
+    m.set_images(rng.uniform(0, 1, (2, 64, 64)))
+    m.make_masks([step_mask_seed(1, 0), step_mask_seed(1, 1)])
+    m.train_step()
+    m.close()
 
 
 if __name__ == "__main__":
