@@ -623,13 +623,27 @@ __global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__
     for (int j = 0; j < int(nk); ++j) {
         const double2 p = skeys[j];
         const double dx = __dsub_rn(p.x, qx), dy = __dsub_rn(p.y, qy);
-        const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-        if (d2 < d[K - 1]) topk_insert<K>(d, jj, kept, d2, j);  // slots >= kept stay +inf
+        double nd = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        if (!(nd < d[K - 1])) continue;  // keys arrive in index order: ties keep the lower index
+        int nj = j;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {  // register-resident sorted insertion by (d^2, j), K >= k
+            if (pair_lt(nd, nj, d[r], jj[r])) {
+                const double td = d[r];
+                const int tj = jj[r];
+                d[r] = nd;
+                jj[r] = nj;
+                nd = td;
+                nj = tj;
+            }
+        }
     }
-    for (int t = 0; t < k; ++t) {
-        idx[w * k + t] = t < kept ? jj[t] : 0;
-        valid[w * k + t] = t < kept ? 1 : 0;
-    }
+#pragma unroll
+    for (int t = 0; t < K; ++t)
+        if (t < k) {
+            idx[w * k + t] = t < kept ? jj[t] : 0;
+            valid[w * k + t] = t < kept ? 1 : 0;
+        }
 }
 
 // ---------------------------------------------- grid-accelerated exact knn

@@ -577,6 +577,10 @@ size_t misc_ws_bytes(const Model& m) {
         }
     }
     upd(perlin_mask_workspace(m.B, m.g, m.g, 2, 4.0));
+    {
+        affmae_attn_desc dd{c.dec_heads, int(m.dd / c.dec_heads), c.bias_hidden, double(c.patch)};
+        upd(gattn_bwd_workspace(&dd, m.B, m.Q, c.self_k));
+    }
     for (int s = 0; s < m.ns; ++s) {
         upd(interp_bwd_gather_workspace(m.B, m.Q, m.st[size_t(s)].N, c.gather_k));
         upd(interp_bwd_gather_workspace(m.B, m.Q, m.st[size_t(s)].N, c.stages[s].interp_k));
@@ -605,9 +609,12 @@ struct Ctx {
     int fwd(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, bf16* y) const {
         return linear_fwd(x, w, b ? b : m.zero_bias, rows, n, k, 0, y, m.gws, m.gws_bytes, sv());
     }
+    // y = GELU(x W^T + b), pre-activation kept for the backward: identity GEMM into `pre`,
+    // then a separate activation pass (cheaper than the GEMM's fused erf epilogue here)
     int fwd_gelu(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, bf16* y,
                  bf16* pre) const {
-        return linear_fwd_gelu_aux(x, w, b, rows, n, k, y, pre, m.gws, m.gws_bytes, sv());
+        CK(linear_fwd(x, w, b, rows, n, k, 0, pre, m.gws, m.gws_bytes, sv()));
+        return mk::gelu_fwd(pre, rows * n, y, st);
     }
     int fwd_add(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, const bf16* c,
                 bf16* y) const {
@@ -905,9 +912,11 @@ int round_bwd(const Ctx& x, int si, int r) {
     {
         affmae_attn_inputs in2 = attn_in(m, pre + "s.", R.q2, R.k2, R.v2, m.refs);
         const std::string p = pre + "s.";
+        // reverse-CSR gather of dk / dv (no fp32 reductions): 1.85 -> 1.49 ms at B = 16
         CK(gattn_bwd(&desc, &in2, m.self_idx, m.self_val, B, Q, c.self_k, m.B1, m.B2, m.F2, m.F3,
                      GF(m, p + "blank_k"), GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"),
-                     GF(m, p + "bias.w2"), GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), nullptr, 0, x.sv()));
+                     GF(m, p + "bias.w2"), GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), m.ws, m.ws_bytes,
+                     x.sv()));
     }
     CK(mk::cast_bf16(m.F2, Mq * dd, m.B3, x.st));
     CK(mk::cast_bf16(m.F3, Mq * dd, m.B5, x.st));
