@@ -5,13 +5,13 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 tail -1 gpurun_out/bench.json
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 tail -1 gpurun_out/bench_ref.json
-B="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-graph --interp-images 0"
+B="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-graph --interp-images 0 --pretrain-batch 0 --tiny-batch 0 --no-parity"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_bench.log 2>&1; echo "ncu launches rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'attn_(fwd|bwd_q|bwd_kv)_kernel' -s 5 -c 5 \
   -o gpurun_out/prof_attn -f $B > gpurun_out/ncu_full.log 2>&1; echo "ncu attn rc=$?"
