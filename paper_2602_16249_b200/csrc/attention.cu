@@ -685,6 +685,7 @@ static void fill_common(AttnParams& p, const affmae_cluster_geom* g, const affma
     p.hidden = a->bias_hidden;
     p.inv_patch = float(1.0 / a->patch);
     p.scale = float(1.0 / sqrt(double(a->head_dim)));
+    p.ldq = p.ldo = int64_t(a->heads) * a->head_dim;
 }
 
 static int check_inputs(const affmae_attn_inputs* in) {
@@ -846,9 +847,10 @@ int attn_plan_build(const affmae_cluster_geom* g, const affmae_attn_desc* a, con
 }
 
 static int run_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
-                   const AttnWs& w, affmae_bf16* out, float* lse, cudaStream_t st) {
+                   const AttnWs& w, affmae_bf16* out, float* lse, cudaStream_t st, int64_t ldq = 0) {
     AttnParams p;
     fill_common(p, g, a, in);
+    if (ldq) p.ldq = ldq;
     p.out = reinterpret_cast<__nv_bfloat16*>(out);
     p.lse = lse;
     int rc = prepare_run(p, w, st);
@@ -858,10 +860,11 @@ static int run_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, cons
 
 static int run_bwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
                    const AttnWs& w, const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
-                   affmae_attn_grads* gr, cudaStream_t st) {
+                   affmae_attn_grads* gr, cudaStream_t st, int64_t ldq = 0) {
     (void)out;
     AttnParams p;
     fill_common(p, g, a, in);
+    if (ldq) p.ldq = ldq;
     p.lse = const_cast<float*>(lse);
     p.dout = reinterpret_cast<const __nv_bfloat16*>(dout);
     p.dq = reinterpret_cast<__nv_bfloat16*>(gr->dq);
@@ -930,7 +933,7 @@ static int check_plan(const affmae_cluster_geom* g, const affmae_attn_desc* a, c
 
 int attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
                      const affmae_attn_plan* plan, affmae_bf16* out, float* lse, void* workspace, size_t ws_bytes,
-                     void* stream) {
+                     void* stream, int64_t ldq) {
     int rc = attn_check(g, a);
     if (rc) return rc;
     if ((rc = check_inputs(in))) return rc;
@@ -941,12 +944,13 @@ int attn_fwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a, co
     carve_run(g, a, workspace, false, w);
     if (!workspace || ws_bytes < w.run_bytes) return fail(AFFMAE_ECONFIG, "attn_fwd: workspace too small");
     if (g->batch == 0) return AFFMAE_OK;
-    return run_fwd(g, a, in, w, out, lse, st);
+    if (ldq && ldq < int64_t(a->heads) * a->head_dim) return fail(AFFMAE_ECONFIG, "attn_fwd: row stride too small");
+    return run_fwd(g, a, in, w, out, lse, st, ldq);
 }
 
 int attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,
                      const affmae_attn_plan* plan, const affmae_bf16* out, const float* lse, const affmae_bf16* dout,
-                     affmae_attn_grads* gr, void* workspace, size_t ws_bytes, void* stream) {
+                     affmae_attn_grads* gr, void* workspace, size_t ws_bytes, void* stream, int64_t ldq) {
     int rc = attn_check(g, a);
     if (rc) return rc;
     if ((rc = check_inputs(in))) return rc;
@@ -957,7 +961,8 @@ int attn_bwd_planned(const affmae_cluster_geom* g, const affmae_attn_desc* a, co
     carve_run(g, a, workspace, true, w);
     if (!workspace || ws_bytes < w.run_bytes) return fail(AFFMAE_ECONFIG, "attn_bwd: workspace too small");
     if (g->batch == 0) return AFFMAE_OK;
-    return run_bwd(g, a, in, w, out, lse, dout, gr, st);
+    if (ldq && ldq < int64_t(a->heads) * a->head_dim) return fail(AFFMAE_ECONFIG, "attn_bwd: row stride too small");
+    return run_bwd(g, a, in, w, out, lse, dout, gr, st, ldq);
 }
 
 int attn_fwd(const affmae_cluster_geom* g, const affmae_attn_desc* a, const affmae_attn_inputs* in,

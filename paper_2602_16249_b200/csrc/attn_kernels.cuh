@@ -112,6 +112,9 @@ struct AttnParams {
     int hidden;
     float inv_patch;
     float scale;      // 1/sqrt(d)
+    int64_t ldq;      // elements between token rows of q, k, v, dq, dk, dv (heads*d, or 3*heads*d
+                      // when the three live interleaved in one [N, 3D] QKV buffer)
+    int64_t ldo;      // elements between token rows of out / dout (heads*d)
 };
 // per-warp partial: window dT [kWs2] | MLP grads [kMG] | blank {dbk[d], dbv[d], dblank}
 __host__ __device__ constexpr int part_width(int hd) { return kWs2 + kMG + 2 * hd + 1; }
@@ -533,8 +536,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
     const int32_t* list = p.items + (FAST ? 0 : p.batch * p.cs.c);
     const int n_items = __ldg(p.item_count + (FAST ? 0 : 1)), stride = gridDim.x;
-    const int64_t ld = int64_t(p.heads) * HD;
-    const uint32_t rowb = uint32_t(ld * 2);
+    const int64_t ld = p.ldq, ldo = p.ldo;
+    const uint32_t rowb = uint32_t(ld * 2), rowbo = uint32_t(ldo * 2);
     const __nv_bfloat16* qg = p.q + h * HD;
     const __nv_bfloat16* kg = p.k + h * HD;
     const __nv_bfloat16* vg = p.v + h * HD;
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
             if (r0 + 8 < qlen) lse_img[uint32_t(rec[R::QTOK + r0 + 8]) * uint32_t(p.heads)] = (m1 + __log2f(l1)) * kLn2;
         }
         __syncwarp();
-        sw_rows_to_global<HD>(p.out + io_cur + h * HD, rowb, sm.O, rec + R::QTOK, qlen, lane);
+        sw_rows_to_global<HD>(p.out + img_tok * ldo + h * HD, rowbo, sm.O, rec + R::QTOK, qlen, lane);
     }
     cp_async_wait<0>();
 }
@@ -701,8 +704,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
     const int32_t* list = p.items + (FAST ? 0 : p.batch * p.cs.c);
     const int n_items = __ldg(p.item_count + (FAST ? 0 : 1)), stride = gridDim.x;
-    const int64_t ld = int64_t(p.heads) * HD;
-    const uint32_t rowb = uint32_t(ld * 2);
+    const int64_t ld = p.ldq, ldo = p.ldo;
+    const uint32_t rowb = uint32_t(ld * 2), rowbo = uint32_t(ldo * 2);
     const __nv_bfloat16* qg = p.q + h * HD;
     const __nv_bfloat16* og = p.dout + h * HD;
     const __nv_bfloat16* kg = p.k + h * HD;
@@ -730,7 +733,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
     };
     auto issue_qo = [&](const int32_t* rec, int64_t img_tok) {
         sw_gather<HD, 16>(sm.Q, qg + img_tok * ld, rowb, rec + R::QTOK, lane);
-        sw_gather<HD, 16>(sm.dO, og + img_tok * ld, rowb, rec + R::QTOK, lane);
+        sw_gather<HD, 16>(sm.dO, og + img_tok * ldo, rowbo, rec + R::QTOK, lane);
         if (lane < 16) {
             const int qt = rec[R::QTOK + lane];
             if (qt >= 0) cp_async4(sm.lse + lane, p.lse + (img_tok + qt) * p.heads + h);
@@ -982,8 +985,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
     const int lane = threadIdx.x, h = blockIdx.y;
     const int r0 = lane >> 2, c0 = 2 * (lane & 3);
     const int n_items = p.batch * p.cs.c, stride = gridDim.x;
-    const int64_t ld = int64_t(p.heads) * HD;
-    const uint32_t rowb = uint32_t(ld * 2);
+    const int64_t ld = p.ldq, ldo = p.ldo;
+    const uint32_t rowb = uint32_t(ld * 2), rowbo = uint32_t(ldo * 2);
     using S = Swz<HD>;
 
     zero_shared(&sm, sizeof(sm));
@@ -1018,7 +1021,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
         const int64_t img_tok = int64_t(item_tok(rec, p));
         const int64_t base = img_tok * ld + h * HD;
         sw_gather<HD, 16>(sm.Q[buf], p.q + base, rowb, rec + PRec::QTOK, lane);
-        sw_gather<HD, 16>(sm.dO[buf], p.dout + base, rowb, rec + PRec::QTOK, lane);
+        sw_gather<HD, 16>(sm.dO[buf], p.dout + img_tok * ldo + h * HD, rowbo, rec + PRec::QTOK, lane);
         if (rec[PRec::HDR + kPFirst]) {
             sw_gather<HD, 16>(sm.K, p.k + base, rowb, rec + KR + KRec::KTOK, lane);
             sw_gather<HD, 16>(sm.V, p.v + base, rowb, rec + KR + KRec::KTOK, lane);

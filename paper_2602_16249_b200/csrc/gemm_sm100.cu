@@ -319,6 +319,10 @@ SplitK splitk_plan(int64_t m, int64_t n, int64_t k) {
     int64_t L = clusters / tiles;
     L = std::min<int64_t>(L, m / 512);
     if (L < 2) return SplitK{1, m, 0};
+    // prefer an exact divisor of m in [L/2, L]: equal chunks (any length -- TMA zero-fills the
+    // K tail of each batch), no remainder GEMM on 2 SMs
+    for (int64_t d = L; d >= (L + 1) / 2 && d >= 2; --d)
+        if (m % d == 0) return SplitK{int(d), m / d, 0};
     const int64_t c = (m / L) / 64 * 64;
     return SplitK{int(L), c, m - L * c};
 }

@@ -24,11 +24,13 @@ int attn_plan_build(const affmae_cluster_geom*, const affmae_attn_desc*, const f
                     const affmae_cluster_index*, int, affmae_attn_plan*, void*);
 size_t attn_fwd_planned_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
 size_t attn_bwd_planned_workspace(const affmae_cluster_geom*, const affmae_attn_desc*);
+// ldq: elements between token rows of q/k/v (and dq/dk/dv), 0 = heads*head_dim (an
+// interleaved [N, 3D] QKV buffer passes 3*heads*head_dim)
 int attn_fwd_planned(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
-                     const affmae_attn_plan*, affmae_bf16*, float*, void*, size_t, void*);
+                     const affmae_attn_plan*, affmae_bf16*, float*, void*, size_t, void*, int64_t ldq = 0);
 int attn_bwd_planned(const affmae_cluster_geom*, const affmae_attn_desc*, const affmae_attn_inputs*,
                      const affmae_attn_plan*, const affmae_bf16*, const float*, const affmae_bf16*,
-                     affmae_attn_grads*, void*, size_t, void*);
+                     affmae_attn_grads*, void*, size_t, void*, int64_t ldq = 0);
 size_t cluster_index_workspace(const affmae_cluster_geom*);
 int cluster_index_build(const affmae_cluster_geom*, const float*, affmae_cluster_index*, void*,
                         size_t, void*);

@@ -88,7 +88,7 @@ struct Param {
 };
 
 struct Blk {
-    bf16 *h1, *q, *k, *v, *a, *h2, *pre, *m;
+    bf16 *h1, *qkv, *a, *h2, *pre, *m;  // qkv: [M, 3D] rows q | k | v (one GEMM, attention reads strided)
     float2 *st1, *st2;
     float* lse;
     float* fmid;
@@ -434,9 +434,7 @@ void layout(Model& m, Arena& a) {
         S.blk.resize(size_t(sc.blocks));
         for (Blk& k : S.blk) {
             k.h1 = a.take<bf16>(Mp * D);
-            k.q = a.take<bf16>(Mp * D);
-            k.k = a.take<bf16>(Mp * D);
-            k.v = a.take<bf16>(Mp * D);
+            k.qkv = a.take<bf16>(Mp * 3 * D);
             k.a = a.take<bf16>(Mp * D);
             k.h2 = a.take<bf16>(Mp * D);
             k.pre = a.take<bf16>(Mp * 4 * D);
@@ -676,12 +674,11 @@ int block_fwd(const Ctx& x, int s, int b) {
     Blk& k = S.blk[size_t(b)];
     const std::string pre = blk_name(s, b);
     const int64_t M = S.M, D = S.D;
-    CK(x.fwd(k.h1, M, D, PBF(m, pre + "wq"), D, nullptr, k.q));
-    CK(x.fwd(k.h1, M, D, PBF(m, pre + "wk"), D, nullptr, k.k));
-    CK(x.fwd(k.h1, M, D, PBF(m, pre + "wv"), D, nullptr, k.v));
-    affmae_attn_inputs in = attn_in(m, pre, k.q, k.k, k.v, S.coords);
+    // Q, K, V in one GEMM: [wq; wk; wv] are adjacent [D, D] blocks of the shadow arena
+    CK(x.fwd(k.h1, M, D, PBF(m, pre + "wq"), 3 * D, nullptr, k.qkv));
+    affmae_attn_inputs in = attn_in(m, pre, k.qkv, k.qkv + D, k.qkv + 2 * D, S.coords);
     CK(attn_fwd_planned(&S.geom, &S.desc, &in, &S.plan, reinterpret_cast<affmae_bf16*>(k.a), k.lse, m.ws, m.ws_bytes,
-                        x.sv()));
+                        x.sv(), 3 * D));
     CK(x.fwd(k.a, M, D, PBF(m, pre + "wo"), D, nullptr, m.T1));
     CK(mk::ln_fwd(S.f[size_t(b)], m.T1, k.fmid, nullptr, PF(m, pre + "ln2.g"), PF(m, pre + "ln2.b"), M, D, k.h2, k.st2,
                   x.st));
@@ -849,16 +846,13 @@ int block_bwd(const Ctx& x, int s, int b) {
                   GF(m, pre + "ln2.b"), m.part, x.st));
     // attention branch: fmid = f + attn(h1 Wq, h1 Wk, h1 Wv) Wo
     CK(x.bwd_wx(k.a, PBF(m, pre + "wo"), m.dfbf, M, D, D, m.B1, GF(m, pre + "wo"), nullptr));
-    affmae_attn_inputs in = attn_in(m, pre, k.q, k.k, k.v, S.coords);
-    affmae_attn_grads g = attn_g(m, pre, m.B2, m.B3, m.B5);
+    affmae_attn_inputs in = attn_in(m, pre, k.qkv, k.qkv + D, k.qkv + 2 * D, S.coords);
+    // dQ | dK | dV interleaved in one [M, 3D] buffer: one dX GEMM (K = 3D), one dW GEMM (N = 3D)
+    affmae_attn_grads g = attn_g(m, pre, m.B4, m.B4 + D, m.B4 + 2 * D);
     CK(attn_bwd_planned(&S.geom, &S.desc, &in, &S.plan, reinterpret_cast<const affmae_bf16*>(k.a), k.lse,
-                        reinterpret_cast<const affmae_bf16*>(m.B1), &g, m.ws, m.ws_bytes, x.sv()));
-    CK(x.bwd_x(m.B2, PBF(m, pre + "wq"), M, D, D, m.F1, 0.f));
-    CK(x.bwd_x(m.B3, PBF(m, pre + "wk"), M, D, D, m.F1, 1.f));
-    CK(x.bwd_x(m.B5, PBF(m, pre + "wv"), M, D, D, m.F1, 1.f));
-    CK(x.bwd_w(k.h1, PBF(m, pre + "wq"), m.B2, M, D, D, GF(m, pre + "wq"), nullptr));
-    CK(x.bwd_w(k.h1, PBF(m, pre + "wk"), m.B3, M, D, D, GF(m, pre + "wk"), nullptr));
-    CK(x.bwd_w(k.h1, PBF(m, pre + "wv"), m.B5, M, D, D, GF(m, pre + "wv"), nullptr));
+                        reinterpret_cast<const affmae_bf16*>(m.B1), &g, m.ws, m.ws_bytes, x.sv(), 3 * D));
+    CK(x.bwd_x(m.B4, PBF(m, pre + "wq"), M, 3 * D, D, m.F1, 0.f));
+    CK(x.bwd_w(k.h1, PBF(m, pre + "wq"), m.B4, M, 3 * D, D, GF(m, pre + "wq"), nullptr));
     return mk::ln_bwd(m.F1, S.f[size_t(b)], k.st1, PF(m, pre + "ln1.g"), M, D, S.df, S.df, m.dfbf,
                       GF(m, pre + "ln1.g"), GF(m, pre + "ln1.b"), m.part, x.st);
 }
@@ -1131,6 +1125,14 @@ int create(const affmae_model_cfg* cfg, Model** out) {
         S.desc = affmae_attn_desc{sc.heads, int(sc.dim / sc.heads), c.bias_hidden, double(c.patch)};
     }
     build_params(m);
+    for (const Param& p : m.params)  // fused QKV GEMMs need [wq; wk; wv] adjacent in the arena
+        if (p.name.size() > 2 && p.name.compare(p.name.size() - 2, 2, "wq") == 0) {
+            const std::string base = p.name.substr(0, p.name.size() - 2);
+            const int64_t dd2 = p.r * p.c;
+            if (m.params[size_t(m.pidx.at(base + "wk"))].off != p.off + dd2 ||
+                m.params[size_t(m.pidx.at(base + "wv"))].off != p.off + 2 * dd2)
+                return bad(AFFMAE_ECONFIG, "model: internal parameter layout (q/k/v not adjacent)");
+        }
     Arena a;
     layout(m, a);
     const size_t part_f = part_floats(m);

@@ -114,7 +114,16 @@ def afftiny_full_cfg(**kw):
     return aff_tiny(batch=1, **kw)
 
 
-CASES = [(small_cfg, 400), (small_cfg, 412), (tiny_cfg, 408), (tiny_cfg, 411), (afftiny_full_cfg, 402)]
+def affmae_b_small_cfg(**kw):
+    """The benchmarked AFFMAE-B widths (dims 128/256/512/1024, heads 4/8/16/32, blocks
+    3/4/18/2, decoder 256 x 8 heads) on a 128^2 image (64 -> 26 -> 10 -> 4 tokens) so the b32
+    reference runs in seconds: every LN / GEMM / attention width of the 1024^2 bench."""
+    from paper_2602_16249_b200.model import affmae_b
+    return affmae_b(image=128, batch=1, **kw)
+
+
+CASES = [(small_cfg, 400), (small_cfg, 412), (tiny_cfg, 408), (tiny_cfg, 411), (afftiny_full_cfg, 402),
+         (affmae_b_small_cfg, 403)]
 
 
 @pytest.mark.parametrize("cfg_fn,img_seed", CASES, ids=[f"{f.__name__[:-4]}_{s}" for f, s in CASES])
