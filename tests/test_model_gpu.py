@@ -122,8 +122,18 @@ def affmae_b_small_cfg(**kw):
     return affmae_b(image=128, batch=1, **kw)
 
 
+def small_depth2_cfg(**kw):
+    """two decoder rounds per stage level (DecoderConfig::depth = 2)"""
+    return small_cfg(dec_depth=2, **kw)
+
+
+def small_random_noaux_cfg(**kw):
+    """random masks (random_mask, src/masking.cpp:94-110) and no deep supervision (lambda 0)"""
+    return small_cfg(mask_strategy="random", lambda_aux=0.0, **kw)
+
+
 CASES = [(small_cfg, 400), (small_cfg, 412), (tiny_cfg, 408), (tiny_cfg, 411), (afftiny_full_cfg, 402),
-         (affmae_b_small_cfg, 403)]
+         (affmae_b_small_cfg, 403), (small_depth2_cfg, 400), (small_random_noaux_cfg, 401)]
 
 
 @pytest.mark.parametrize("cfg_fn,img_seed", CASES, ids=[f"{f.__name__[:-4]}_{s}" for f, s in CASES])
