@@ -16,6 +16,7 @@
 //   * batched semantics: the loss is the mean over images of the reference's per-image
 //     loss, so B = 1 reproduces the reference's step.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
@@ -201,6 +202,12 @@ struct affmae_model {
     float *dfq = nullptr, *dqpos = nullptr, *dqjunk = nullptr;
     __nv_bfloat16 *T1 = nullptr, *B1 = nullptr, *B2 = nullptr, *B3 = nullptr, *B4 = nullptr, *B5 = nullptr,
                   *B6 = nullptr, *dfbf = nullptr, *dfq_bf = nullptr;
+    // second copies of the scratch the side-stream weight gradients read, so the main stream's
+    // next writer does not have to wait for them (see Ctx::side_dw)
+    __nv_bfloat16 *B4b = nullptr, *dfbf2 = nullptr, *dfq_bf2 = nullptr, *B2x = nullptr, *B3x = nullptr, *B5x = nullptr;
+    cudaStream_t side = nullptr;       // weight-gradient GEMMs of the backward
+    std::vector<cudaEvent_t> events;   // fork / join events of one step (reused every step)
+    uint8_t* gws2 = nullptr;           // GEMM workspace of the side stream
 
     int64_t steps = 0;
     int world = 1;          // data-parallel ranks: the loss gradient is seeded with 1/world
@@ -414,13 +421,10 @@ void layout(Model& m, Arena& a) {
     m.ypos0 = a.take<bf16>(round8(M0) * c.stages[0].dim);
     m.emb = a.take<bf16>(round8(M0) * c.stages[0].dim);
 
-    int64_t Mmax = Mq, Dmax = dd;
     for (int s = 0; s < m.ns; ++s) {
         Stage& S = m.st[size_t(s)];
         const affmae_stage_cfg& sc = c.stages[s];
         const int64_t M = S.M, D = S.D, Mp = round8(M);
-        Mmax = std::max(Mmax, Mp);
-        Dmax = std::max(Dmax, D);
         S.coords = a.take<float>(M * 2);
         S.idx.perm = a.take<int32_t>(M);
         S.idx.cluster_of = a.take<int32_t>(M);
@@ -462,7 +466,6 @@ void layout(Model& m, Arena& a) {
             S.ymerge = a.take<bf16>(Mn * Dn);
             S.ylnm = a.take<bf16>(Mn * Dn);
             S.stm = a.take<float2>(Mn);
-            Mmax = std::max(Mmax, Mn);
             if (c.lambda_aux > 0.0) {
                 const int k = c.stages[s].interp_k;
                 S.aidx = a.take<int32_t>(Mq * k);
@@ -519,25 +522,50 @@ void layout(Model& m, Arena& a) {
     m.recon = a.take<bf16>(Mqp * p2);
     m.drecon = a.take<bf16>(Mqp * p2);
 
-    // scratch
-    m.F1 = a.take<float>(Mmax * Dmax);
+    // scratch, each sized for its largest use (rows rounded to 8)
+    int64_t eMD = Mqp * dd, e16 = Mqp * kPosHidden, e4 = Mqp * 2 * dd, eB1 = Mqp * dd, eB6 = Mqp * dd, eRows = Mqp,
+            eZ = 0, eDf = 0;
+    for (int s = 0; s < m.ns; ++s) {
+        const Stage& S = m.st[size_t(s)];
+        const int64_t Mp = round8(S.M);
+        eMD = std::max(eMD, Mp * S.D);
+        e16 = std::max(e16, Mp * kPosHidden);
+        e4 = std::max(e4, Mp * 4 * S.D);
+        eB1 = std::max(eB1, std::max(Mp * S.D, Mqp * S.D));
+        eB6 = std::max(eB6, Mp * dd);
+        eRows = std::max(eRows, Mp);
+        eZ = std::max(eZ, Mp * dd);
+        eDf = std::max(eDf, Mp * S.D);
+        if (s + 1 < m.ns) {
+            const int64_t Mn = round8(m.B * S.R);
+            eB1 = std::max(eB1, Mn * m.st[size_t(s + 1)].D);
+            e4 = std::max(e4, Mn * 2 * S.D);
+        }
+    }
+    m.F1 = a.take<float>(eMD);
     m.F2 = a.take<float>(Mqp * dd);
     m.F3 = a.take<float>(Mqp * dd);
     m.F4 = a.take<float>(Mqp * dd);
-    m.F5 = a.take<float>(Mmax * kPosHidden);
-    m.dz = a.take<float>(Mmax * dd);
-    m.dscores = a.take<float>(Mmax);
+    m.F5 = a.take<float>(e16);
+    m.dz = a.take<float>(eZ);
+    m.dscores = a.take<float>(eRows);
     m.dfq = a.take<float>(Mqp * dd);
     m.dqpos = a.take<float>(Mq * 2);
     m.dqjunk = a.take<float>(Mq * 2);
-    m.T1 = a.take<bf16>(Mmax * Dmax);
-    m.B1 = a.take<bf16>(Mmax * Dmax);
-    m.B2 = a.take<bf16>(Mmax * std::max<int64_t>(Dmax, kPosHidden));
-    m.B3 = a.take<bf16>(Mmax * Dmax);
-    m.B4 = a.take<bf16>(Mmax * 4 * Dmax);
-    m.B5 = a.take<bf16>(Mmax * Dmax);
-    m.B6 = a.take<bf16>(Mmax * Dmax);
-    m.dfbf = a.take<bf16>(Mmax * Dmax);
+    m.T1 = a.take<bf16>(eMD);
+    m.B1 = a.take<bf16>(eB1);
+    m.B2 = a.take<bf16>(std::max(e16, Mqp * dd));
+    m.B3 = a.take<bf16>(Mqp * dd);
+    m.B4 = a.take<bf16>(e4);
+    m.B5 = a.take<bf16>(Mqp * dd);
+    m.B6 = a.take<bf16>(eB6);
+    m.dfbf = a.take<bf16>(eDf);
+    m.dfbf2 = a.take<bf16>(eDf);
+    m.B4b = a.take<bf16>(e4);
+    m.dfq_bf2 = a.take<bf16>(Mqp * dd);
+    m.B2x = a.take<bf16>(Mqp * dd);
+    m.B3x = a.take<bf16>(Mqp * dd);
+    m.B5x = a.take<bf16>(Mqp * dd);
     m.dfq_bf = a.take<bf16>(Mqp * dd);
 }
 
@@ -602,7 +630,64 @@ size_t gemm_ws_bytes(const Model& m) {
 struct Ctx {
     Model& m;
     cudaStream_t st;
+    // backward only: weight gradients on m.side (off the critical dX chain); `pending` maps a
+    // dY buffer to the side-stream event after its last reader, waited for before the main
+    // stream overwrites it (guard)
+    bool overlap = false;
+    mutable std::vector<std::pair<const void*, cudaEvent_t>> pending;
+    mutable size_t next_event = 0;
     void* sv() const { return reinterpret_cast<void*>(st); }
+    cudaEvent_t event() const {
+        if (next_event >= m.events.size()) return nullptr;
+        return m.events[next_event++];
+    }
+    // the main stream is about to write `buf`: wait for the side-stream readers of it
+    int guard(const void* buf) const {
+        for (size_t i = 0; i < pending.size(); ++i)
+            if (pending[i].first == buf) {
+                if (cudaStreamWaitEvent(st, pending[i].second, 0) != cudaSuccess)
+                    return cuda_status(cudaGetLastError(), "model guard");
+                pending.erase(pending.begin() + int64_t(i));
+                return AFFMAE_OK;
+            }
+        return AFFMAE_OK;
+    }
+    // dW (+db) += from x [rows, k], dy [rows, n] on the side stream (dy must stay unchanged
+    // until the guard of the buffer); falls back to the main stream without overlap
+    int side_dw(const bf16* x, const bf16* w, const bf16* dy, int64_t rows, int64_t n, int64_t k, float* dw,
+                float* db) const {
+        cudaEvent_t fork = overlap ? event() : nullptr, done = overlap ? event() : nullptr;
+        if (!fork || !done) return linear_bwd(x, w, dy, rows, n, k, nullptr, dw, db, m.gws, m.gws_bytes, sv());
+        if (cudaEventRecord(fork, st) != cudaSuccess || cudaStreamWaitEvent(m.side, fork, 0) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "model side fork");
+        CK(linear_bwd(x, w, dy, rows, n, k, nullptr, dw, db, m.gws2, m.gws_bytes, reinterpret_cast<void*>(m.side)));
+        if (cudaEventRecord(done, m.side) != cudaSuccess) return cuda_status(cudaGetLastError(), "model side record");
+        for (auto& pe : pending)
+            if (pe.first == dy) {
+                pe.second = done;  // the side stream is in order: the latest reader implies the earlier ones
+                return AFFMAE_OK;
+            }
+        pending.emplace_back(dy, done);
+        return AFFMAE_OK;
+    }
+    // dX = dy W (bf16) on the main stream, dW / db on the side stream
+    int bwd_xw(const bf16* x, const bf16* w, const bf16* dy, int64_t rows, int64_t n, int64_t k, bf16* dx, float* dw,
+               float* db) const {
+        if (!overlap) return linear_bwd(x, w, dy, rows, n, k, dx, dw, db, m.gws, m.gws_bytes, sv());
+        CK(side_dw(x, w, dy, rows, n, k, dw, db));
+        CK(guard(dx));
+        return linear_bwd(x, w, dy, rows, n, k, dx, nullptr, nullptr, m.gws, m.gws_bytes, sv());
+    }
+    // main stream waits for every side-stream weight gradient
+    int join() const {
+        if (!overlap) return AFFMAE_OK;
+        cudaEvent_t e = event();
+        if (!e) return fail(AFFMAE_ECUDA, "model: event pool exhausted");
+        if (cudaEventRecord(e, m.side) != cudaSuccess || cudaStreamWaitEvent(st, e, 0) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "model side join");
+        pending.clear();
+        return AFFMAE_OK;
+    }
     // y = x W^T (+ b); W [n, k] (arena layout of a transposed parameter)
     int fwd(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, bf16* y) const {
         return linear_fwd(x, w, b ? b : m.zero_bias, rows, n, k, 0, y, m.gws, m.gws_bytes, sv());
@@ -838,21 +923,26 @@ int block_bwd(const Ctx& x, int s, int b) {
     const std::string pre = blk_name(s, b);
     const int64_t M = S.M, D = S.D;
     // MLP branch: out = fmid + GELU(h2 W1 + b1) W2 + b2
-    CK(x.bwd_wx(k.m, PBF(m, pre + "mlp.w2"), m.dfbf, M, D, 4 * D, m.B4, GF(m, pre + "mlp.w2"), GF(m, pre + "mlp.b2")));
+    // (weight gradients fork to the side stream; dy buffers alternate dfbf -> dfbf2 -> dfbf and
+    // dm (B4) / dqkv (B4b) so the next writer rarely waits for them)
+    CK(x.bwd_xw(k.m, PBF(m, pre + "mlp.w2"), m.dfbf, M, D, 4 * D, m.B4, GF(m, pre + "mlp.w2"), GF(m, pre + "mlp.b2")));
     CK(gelu_bwd(k.pre, m.B4, M * 4 * D, m.B4, x.sv()));
+    CK(x.side_dw(k.h2, PBF(m, pre + "mlp.w1"), m.B4, M, 4 * D, D, GF(m, pre + "mlp.w1"), GF(m, pre + "mlp.b1")));
     CK(x.bwd_x(m.B4, PBF(m, pre + "mlp.w1"), M, 4 * D, D, m.F1, 0.f));
-    CK(x.bwd_w(k.h2, PBF(m, pre + "mlp.w1"), m.B4, M, 4 * D, D, GF(m, pre + "mlp.w1"), GF(m, pre + "mlp.b1")));
-    CK(mk::ln_bwd(m.F1, k.fmid, k.st2, PF(m, pre + "ln2.g"), M, D, S.df, S.df, m.dfbf, GF(m, pre + "ln2.g"),
+    CK(x.guard(m.dfbf2));
+    CK(mk::ln_bwd(m.F1, k.fmid, k.st2, PF(m, pre + "ln2.g"), M, D, S.df, S.df, m.dfbf2, GF(m, pre + "ln2.g"),
                   GF(m, pre + "ln2.b"), m.part, x.st));
     // attention branch: fmid = f + attn(h1 Wq, h1 Wk, h1 Wv) Wo
-    CK(x.bwd_wx(k.a, PBF(m, pre + "wo"), m.dfbf, M, D, D, m.B1, GF(m, pre + "wo"), nullptr));
+    CK(x.bwd_xw(k.a, PBF(m, pre + "wo"), m.dfbf2, M, D, D, m.B1, GF(m, pre + "wo"), nullptr));
     affmae_attn_inputs in = attn_in(m, pre, k.qkv, k.qkv + D, k.qkv + 2 * D, S.coords);
     // dQ | dK | dV interleaved in one [M, 3D] buffer: one dX GEMM (K = 3D), one dW GEMM (N = 3D)
-    affmae_attn_grads g = attn_g(m, pre, m.B4, m.B4 + D, m.B4 + 2 * D);
+    CK(x.guard(m.B4b));
+    affmae_attn_grads g = attn_g(m, pre, m.B4b, m.B4b + D, m.B4b + 2 * D);
     CK(attn_bwd_planned(&S.geom, &S.desc, &in, &S.plan, reinterpret_cast<const affmae_bf16*>(k.a), k.lse,
                         reinterpret_cast<const affmae_bf16*>(m.B1), &g, m.ws, m.ws_bytes, x.sv(), 3 * D));
-    CK(x.bwd_x(m.B4, PBF(m, pre + "wq"), M, 3 * D, D, m.F1, 0.f));
-    CK(x.bwd_w(k.h1, PBF(m, pre + "wq"), m.B4, M, 3 * D, D, GF(m, pre + "wq"), nullptr));
+    CK(x.side_dw(k.h1, PBF(m, pre + "wq"), m.B4b, M, 3 * D, D, GF(m, pre + "wq"), nullptr));
+    CK(x.bwd_x(m.B4b, PBF(m, pre + "wq"), M, 3 * D, D, m.F1, 0.f));
+    CK(x.guard(m.dfbf));
     return mk::ln_bwd(m.F1, S.f[size_t(b)], k.st1, PF(m, pre + "ln1.g"), M, D, S.df, S.df, m.dfbf,
                       GF(m, pre + "ln1.g"), GF(m, pre + "ln1.b"), m.part, x.st);
 }
@@ -866,6 +956,8 @@ int merge_bwd(const Ctx& x, int s) {
     const std::string pre = "merge.s" + std::to_string(s) + ".";
     const int64_t M = S.M, D = S.D, R = S.R, Dn = Sn.D, Mn = m.B * R;
     // f_next = LN(pooled Wproj): dy of the projection (bf16)
+    CK(x.guard(m.B4));
+    CK(x.guard(m.B2));
     CK(mk::ln_bwd_bf(Sn.df, S.ymerge, S.stm, PF(m, pre + "ln.g"), Mn, Dn, nullptr, nullptr, m.B1, GF(m, pre + "ln.g"),
                      GF(m, pre + "ln.b"), m.part, x.st));
     CK(x.bwd_wx(S.pooled, PBF(m, pre + "proj"), m.B1, Mn, Dn, 2 * D, m.B4, GF(m, pre + "proj"), nullptr));
@@ -892,56 +984,67 @@ int round_bwd(const Ctx& x, int si, int r) {
     const int64_t Mq = m.Mq, dd = m.dd, B = m.B, Q = m.Q;
     affmae_attn_desc desc{c.dec_heads, int(dd / c.dec_heads), c.bias_hidden, double(c.patch)};
     // MLP
-    CK(x.bwd_wx(R.m, PBF(m, pre + "mlp.w2"), m.dfq_bf, Mq, dd, 2 * dd, m.B4, GF(m, pre + "mlp.w2"),
+    // (weight gradients on the side stream; dfq's bf16 copy goes dfq_bf -> dfq_bf2 -> dfq_bf,
+    // the cross attention's dq / dk / dv use their own B2x / B3x / B5x)
+    CK(x.bwd_xw(R.m, PBF(m, pre + "mlp.w2"), m.dfq_bf, Mq, dd, 2 * dd, m.B4, GF(m, pre + "mlp.w2"),
                 GF(m, pre + "mlp.b2")));
     CK(gelu_bwd(R.pre, m.B4, Mq * 2 * dd, m.B4, x.sv()));
+    CK(x.side_dw(R.h3, PBF(m, pre + "mlp.w1"), m.B4, Mq, 2 * dd, dd, GF(m, pre + "mlp.w1"), GF(m, pre + "mlp.b1")));
     CK(x.bwd_x(m.B4, PBF(m, pre + "mlp.w1"), Mq, 2 * dd, dd, m.F1, 0.f));
-    CK(x.bwd_w(R.h3, PBF(m, pre + "mlp.w1"), m.B4, Mq, 2 * dd, dd, GF(m, pre + "mlp.w1"), GF(m, pre + "mlp.b1")));
-    CK(mk::ln_bwd(m.F1, R.fq_s, R.st3, PF(m, pre + "ln3.g"), Mq, dd, m.dfq, m.dfq, m.dfq_bf, GF(m, pre + "ln3.g"),
+    CK(x.guard(m.dfq_bf2));
+    CK(mk::ln_bwd(m.F1, R.fq_s, R.st3, PF(m, pre + "ln3.g"), Mq, dd, m.dfq, m.dfq, m.dfq_bf2, GF(m, pre + "ln3.g"),
                   GF(m, pre + "ln3.b"), m.part, x.st));
     // self attention over the knn rows
-    CK(x.bwd_wx(R.a2, PBF(m, pre + "s.wo"), m.dfq_bf, Mq, dd, dd, m.B1, GF(m, pre + "s.wo"), nullptr));
+    CK(x.bwd_xw(R.a2, PBF(m, pre + "s.wo"), m.dfq_bf2, Mq, dd, dd, m.B1, GF(m, pre + "s.wo"), nullptr));
     CK(cudaMemsetAsync(m.F2, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     CK(cudaMemsetAsync(m.F3, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     {
         affmae_attn_inputs in2 = attn_in(m, pre + "s.", R.q2, R.k2, R.v2, m.refs);
         const std::string p = pre + "s.";
         // reverse-CSR gather of dk / dv (no fp32 reductions): 1.85 -> 1.49 ms at B = 16
+        CK(x.guard(m.B2));
         CK(gattn_bwd(&desc, &in2, m.self_idx, m.self_val, B, Q, c.self_k, m.B1, m.B2, m.F2, m.F3,
                      GF(m, p + "blank_k"), GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"),
                      GF(m, p + "bias.w2"), GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), m.ws, m.ws_bytes,
                      x.sv()));
     }
+    CK(x.guard(m.B3));
     CK(mk::cast_bf16(m.F2, Mq * dd, m.B3, x.st));
+    CK(x.guard(m.B5));
     CK(mk::cast_bf16(m.F3, Mq * dd, m.B5, x.st));
+    CK(x.side_dw(R.h2, PBF(m, pre + "s.wq"), m.B2, Mq, dd, dd, GF(m, pre + "s.wq"), nullptr));
+    CK(x.side_dw(R.h2, PBF(m, pre + "s.wk"), m.B3, Mq, dd, dd, GF(m, pre + "s.wk"), nullptr));
+    CK(x.side_dw(R.h2, PBF(m, pre + "s.wv"), m.B5, Mq, dd, dd, GF(m, pre + "s.wv"), nullptr));
     CK(x.bwd_x(m.B2, PBF(m, pre + "s.wq"), Mq, dd, dd, m.F1, 0.f));
     CK(x.bwd_x(m.B3, PBF(m, pre + "s.wk"), Mq, dd, dd, m.F1, 1.f));
     CK(x.bwd_x(m.B5, PBF(m, pre + "s.wv"), Mq, dd, dd, m.F1, 1.f));
-    CK(x.bwd_w(R.h2, PBF(m, pre + "s.wq"), m.B2, Mq, dd, dd, GF(m, pre + "s.wq"), nullptr));
-    CK(x.bwd_w(R.h2, PBF(m, pre + "s.wk"), m.B3, Mq, dd, dd, GF(m, pre + "s.wk"), nullptr));
-    CK(x.bwd_w(R.h2, PBF(m, pre + "s.wv"), m.B5, Mq, dd, dd, GF(m, pre + "s.wv"), nullptr));
+    CK(x.guard(m.dfq_bf));
     CK(mk::ln_bwd(m.F1, R.fq_x, R.st2, PF(m, pre + "ln2.g"), Mq, dd, m.dfq, m.dfq, m.dfq_bf, GF(m, pre + "ln2.g"),
                   GF(m, pre + "ln2.b"), m.part, x.st));
     // cross attention over (virtual token, blank)
-    CK(x.bwd_wx(R.a1, PBF(m, pre + "x.wo"), m.dfq_bf, Mq, dd, dd, m.B1, GF(m, pre + "x.wo"), nullptr));
+    CK(x.bwd_xw(R.a1, PBF(m, pre + "x.wo"), m.dfq_bf, Mq, dd, dd, m.B1, GF(m, pre + "x.wo"), nullptr));
     CK(cudaMemsetAsync(m.F2, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     CK(cudaMemsetAsync(m.F3, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     {
         affmae_attn_inputs in1 = attn_in(m, pre + "x.", R.q1, R.k1, R.v1, m.refs);
         const std::string p = pre + "x.";
-        CK(gattn_bwd(&desc, &in1, m.one_idx, m.one_val, B, Q, 1, m.B1, m.B2, m.F2, m.F3, GF(m, p + "blank_k"),
+        CK(x.guard(m.B2x));
+        CK(gattn_bwd(&desc, &in1, m.one_idx, m.one_val, B, Q, 1, m.B1, m.B2x, m.F2, m.F3, GF(m, p + "blank_k"),
                      GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"), GF(m, p + "bias.w2"),
                      GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), nullptr, 0, x.sv()));
     }
-    CK(mk::cast_bf16(m.F2, Mq * dd, m.B3, x.st));
-    CK(mk::cast_bf16(m.F3, Mq * dd, m.B5, x.st));
-    CK(x.bwd_x(m.B2, PBF(m, pre + "x.wq"), Mq, dd, dd, m.F1, 0.f));
-    CK(x.bwd_w(R.h1, PBF(m, pre + "x.wq"), m.B2, Mq, dd, dd, GF(m, pre + "x.wq"), nullptr));
-    CK(x.bwd_x(m.B3, PBF(m, pre + "x.wk"), Mq, dd, dd, m.F4, 0.f));
-    CK(x.bwd_x(m.B5, PBF(m, pre + "x.wv"), Mq, dd, dd, m.F4, 1.f));
-    CK(x.bwd_w(R.virt, PBF(m, pre + "x.wk"), m.B3, Mq, dd, dd, GF(m, pre + "x.wk"), nullptr));
-    CK(x.bwd_w(R.virt, PBF(m, pre + "x.wv"), m.B5, Mq, dd, dd, GF(m, pre + "x.wv"), nullptr));
+    CK(x.guard(m.B3x));
+    CK(mk::cast_bf16(m.F2, Mq * dd, m.B3x, x.st));
+    CK(x.guard(m.B5x));
+    CK(mk::cast_bf16(m.F3, Mq * dd, m.B5x, x.st));
+    CK(x.side_dw(R.h1, PBF(m, pre + "x.wq"), m.B2x, Mq, dd, dd, GF(m, pre + "x.wq"), nullptr));
+    CK(x.side_dw(R.virt, PBF(m, pre + "x.wk"), m.B3x, Mq, dd, dd, GF(m, pre + "x.wk"), nullptr));
+    CK(x.side_dw(R.virt, PBF(m, pre + "x.wv"), m.B5x, Mq, dd, dd, GF(m, pre + "x.wv"), nullptr));
+    CK(x.bwd_x(m.B2x, PBF(m, pre + "x.wq"), Mq, dd, dd, m.F1, 0.f));
+    CK(x.bwd_x(m.B3x, PBF(m, pre + "x.wk"), Mq, dd, dd, m.F4, 0.f));
+    CK(x.bwd_x(m.B5x, PBF(m, pre + "x.wv"), Mq, dd, dd, m.F4, 1.f));
     // virtual tokens: interpolation of z at the deformed points (gradients into z, p, qpos)
+    CK(x.guard(m.B6));
     CK(mk::cast_bf16(m.F4, Mq * dd, m.B6, x.st));
     CK(cudaMemsetAsync(m.dqpos, 0, size_t(Mq * 2) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     CK(interp_bwd_gather(R.qpos, S.coords, d.z, R.gidx, R.gval, B, Q, S.N, dd, c.gather_k, PF(m, pre + "p"),
@@ -949,6 +1052,7 @@ int round_bwd(const Ctx& x, int si, int r) {
     // qpos = refs + NormClamp(fq W_off + b_off): += dfq in place
     CK(mk::offset_bwd(R.fq_in, Mq, dd, PF(m, pre + "off.w"), 2.0 * double(c.patch), R.offpre, m.dqpos, m.dfq,
                       GF(m, pre + "off.w"), GF(m, pre + "off.b"), m.part, x.st));
+    CK(x.guard(m.dfq_bf));
     return mk::ln_bwd(m.F1, R.fq_in, R.st1, PF(m, pre + "ln1.g"), Mq, dd, m.dfq, m.dfq, m.dfq_bf, GF(m, pre + "ln1.g"),
                       GF(m, pre + "ln1.b"), m.part, x.st);
 }
@@ -971,8 +1075,8 @@ int backward(const Ctx& x) {
         if (cudaMemsetAsync(S.df, 0, size_t(S.M * S.D) * 4, x.st) != cudaSuccess)
             return cuda_status(cudaGetLastError(), "model backward memset");
     // decoder head: recon = LN(fq) W + b
+    CK(x.side_dw(m.hh, PBF(m, "dec.head.w"), m.drecon, Mq, p2, dd, GF(m, "dec.head.w"), GF(m, "dec.head.b")));
     CK(x.bwd_x(m.drecon, PBF(m, "dec.head.w"), Mq, p2, dd, m.F1, 0.f));
-    CK(x.bwd_w(m.hh, PBF(m, "dec.head.w"), m.drecon, Mq, p2, dd, GF(m, "dec.head.w"), GF(m, "dec.head.b")));
     CK(mk::ln_bwd(m.F1, m.fq_final, m.sth, PF(m, "dec.head.ln.g"), Mq, dd, nullptr, m.dfq, m.dfq_bf,
                   GF(m, "dec.head.ln.g"), GF(m, "dec.head.ln.b"), m.part, x.st));
     // deep-supervision heads -> stage features
@@ -981,7 +1085,7 @@ int backward(const Ctx& x) {
             Stage& S = m.st[size_t(s)];
             const std::string pre = "aux.s" + std::to_string(s) + ".";
             const int k = c.stages[s].interp_k;
-            CK(x.bwd_wx(S.avirt, PBF(m, pre + "w"), S.daux, Mq, p2, S.D, m.B1, GF(m, pre + "w"), GF(m, pre + "b")));
+            CK(x.bwd_xw(S.avirt, PBF(m, pre + "w"), S.daux, Mq, p2, S.D, m.B1, GF(m, pre + "w"), GF(m, pre + "b")));
             CK(interp_bwd_gather(m.refs, S.coords, S.fout_bf, S.aidx, S.aval, B, m.Q, S.N, S.D, k,
                                  PF(m, pre + "p"), kInterpEps, m.B1, S.df, GF(m, pre + "p"), m.dqjunk, m.ws,
                                  m.ws_bytes, x.sv()));
@@ -996,8 +1100,9 @@ int backward(const Ctx& x) {
             return cuda_status(cudaGetLastError(), "model backward memset");
         for (int r = c.dec_depth - 1; r >= 0; --r) CK(round_bwd(x, si, r));
         // z = f W_in + b_in + pos(coords)
+        CK(x.guard(m.B6));
         CK(mk::cast_bf16(m.dz, S.M * dd, m.B6, x.st));
-        CK(x.bwd_w(S.fout_bf, PBF(m, sp + "in.w"), m.B6, S.M, dd, S.D, GF(m, sp + "in.w"), GF(m, sp + "in.b")));
+        CK(x.side_dw(S.fout_bf, PBF(m, sp + "in.w"), m.B6, S.M, dd, S.D, GF(m, sp + "in.w"), GF(m, sp + "in.b")));
         CK(x.bwd_x(m.B6, PBF(m, sp + "in.w"), S.M, dd, S.D, S.df, 1.f));
         CK(pos_bwd(x, "dec.pos", d.hz, S.coords, S.M, dd, m.B6));
     }
@@ -1008,12 +1113,13 @@ int backward(const Ctx& x) {
     for (int s = m.ns - 1; s >= 0; --s) {
         Stage& S = m.st[size_t(s)];
         if (s + 1 < m.ns) CK(merge_bwd(x, s));
+        CK(x.guard(m.dfbf));
         CK(mk::cast_bf16(S.df, S.M * S.D, m.dfbf, x.st));
         for (int b = int(S.blk.size()) - 1; b >= 0; --b) CK(block_bwd(x, s, b));
     }
     // stage-0 input: f0 = vec W_e + b_e + pos0(coords)
     Stage& S0 = m.st[0];
-    CK(x.bwd_w(m.vec, PBF(m, "embed.w"), m.dfbf, S0.M, S0.D, p2, GF(m, "embed.w"), GF(m, "embed.b")));
+    CK(x.side_dw(m.vec, PBF(m, "embed.w"), m.dfbf, S0.M, S0.D, p2, GF(m, "embed.w"), GF(m, "embed.b")));
     return pos_bwd(x, "pos0", m.h0, S0.coords, S0.M, S0.D, m.dfbf);
 }
 
@@ -1022,7 +1128,9 @@ int forward_backward(Model& m, cudaStream_t st) {
     if (cudaMemsetAsync(m.G, 0, size_t(m.nvals) * 4, st) != cudaSuccess)
         return cuda_status(cudaGetLastError(), "model zero_grads");
     CK(forward(x));
+    x.overlap = m.side != nullptr;
     CK(backward(x));
+    CK(x.join());
     // the step's one exchange: sum the gradient arena over the data-parallel ranks
     if (m.comm) return nccl_allreduce_sum_f32(m.comm, m.G, m.nvals, st);
     return AFFMAE_OK;
@@ -1140,7 +1248,7 @@ int create(const affmae_model_cfg* cfg, Model** out) {
     m.gws_bytes = gemm_ws_bytes(m);
     const size_t main_bytes = a.off;
     m.dbytes = main_bytes + ((part_f * 4 + 255) & ~size_t(255)) + ((m.ws_bytes + 255) & ~size_t(255)) +
-               ((m.gws_bytes + 255) & ~size_t(255));
+               2 * ((m.gws_bytes + 255) & ~size_t(255));
     if (cudaMalloc(&m.dmem, m.dbytes) != cudaSuccess) {
         cudaGetLastError();
         return bad(AFFMAE_ECUDA, "model_create: cudaMalloc of " + std::to_string(m.dbytes >> 20) + " MiB failed");
@@ -1150,6 +1258,23 @@ int create(const affmae_model_cfg* cfg, Model** out) {
     m.part = reinterpret_cast<float*>(m.dmem + main_bytes);
     m.ws = m.dmem + main_bytes + ((part_f * 4 + 255) & ~size_t(255));
     m.gws = m.ws + ((m.ws_bytes + 255) & ~size_t(255));
+    m.gws2 = m.gws + ((m.gws_bytes + 255) & ~size_t(255));
+    // the side stream of the backward's weight gradients and its fork / join events (two per
+    // weight-gradient GEMM at most, plus the joins)
+    if (!std::getenv("AFFMAE_NO_DW_OVERLAP")) {
+        if (cudaStreamCreateWithFlags(&m.side, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            m.side = nullptr;
+        }
+        for (size_t i = 0; m.side && i < 2 * m.params.size() + 8; ++i) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+                cudaFree(m.dmem);
+                return bad(AFFMAE_ECUDA, "model_create: event creation failed");
+            }
+            m.events.push_back(e);
+        }
+    }
     for (Stage& S : m.st) {
         S.plan.batch = S.plan.tokens = S.plan.n_clusters = S.plan.groups_eff = S.plan.width = 0;
         S.plan.has_reverse = 0;
@@ -1209,6 +1334,8 @@ void affmae_model_destroy(affmae_model* m) {
     if (!m) return;
     if (m->gexec) cudaGraphExecDestroy(m->gexec);
     if (m->comm) nccl_comm_destroy(m->comm);
+    for (cudaEvent_t e : m->events) cudaEventDestroy(e);
+    if (m->side) cudaStreamDestroy(m->side);
     if (m->dmem) cudaFree(m->dmem);
     delete m;
 }
