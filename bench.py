@@ -1210,6 +1210,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_token": algo[dom]},
         "phase_ms": ph,
+        # every phase against the same HBM roofline (SURVEY §8(d) algorithmic bytes per token)
+        "phase_hbm_frac": {k: algo[k] * B * N / (ph[k] * 1e-3) / 1e9 / peak for k in ph if k in algo and ph[k] > 0},
         "clocks": res["clocks"],
         "cuda_graph": res["graph"],
     }
