@@ -606,6 +606,8 @@ size_t misc_ws_bytes(const Model& m) {
     {
         affmae_attn_desc dd{c.dec_heads, int(m.dd / c.dec_heads), c.bias_hidden, double(c.patch)};
         upd(gattn_bwd_workspace(&dd, m.B, m.Q, c.self_k));
+        // cross attention (one-to-one): per-block parameter-gradient rows
+        upd(size_t(16) * device_sms() * size_t(2 * m.dd + 4 * c.dec_heads * c.bias_hidden + 2 * c.dec_heads) * 4);
     }
     for (int s = 0; s < m.ns; ++s) {
         upd(interp_bwd_gather_workspace(m.B, m.Q, m.st[size_t(s)].N, c.gather_k));
@@ -1023,20 +1025,16 @@ int round_bwd(const Ctx& x, int si, int r) {
                   GF(m, pre + "ln2.b"), m.part, x.st));
     // cross attention over (virtual token, blank)
     CK(x.bwd_xw(R.a1, PBF(m, pre + "x.wo"), m.dfq_bf, Mq, dd, dd, m.B1, GF(m, pre + "x.wo"), nullptr));
-    CK(cudaMemsetAsync(m.F2, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
-    CK(cudaMemsetAsync(m.F3, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
-    {
+    {   // one-to-one rows: dq, dk, dv straight to bf16 (every key row has exactly one query)
         affmae_attn_inputs in1 = attn_in(m, pre + "x.", R.q1, R.k1, R.v1, m.refs);
         const std::string p = pre + "x.";
         CK(x.guard(m.B2x));
-        CK(gattn_bwd(&desc, &in1, m.one_idx, m.one_val, B, Q, 1, m.B1, m.B2x, m.F2, m.F3, GF(m, p + "blank_k"),
-                     GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"), GF(m, p + "bias.w2"),
-                     GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), nullptr, 0, x.sv()));
+        CK(x.guard(m.B3x));
+        CK(x.guard(m.B5x));
+        CK(gattn_bwd_o2o(&desc, &in1, m.one_idx, m.one_val, B, Q, m.B1, m.B2x, m.B3x, m.B5x, GF(m, p + "blank_k"),
+                         GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"), GF(m, p + "bias.w2"),
+                         GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), m.ws, m.ws_bytes, x.sv()));
     }
-    CK(x.guard(m.B3x));
-    CK(mk::cast_bf16(m.F2, Mq * dd, m.B3x, x.st));
-    CK(x.guard(m.B5x));
-    CK(mk::cast_bf16(m.F3, Mq * dd, m.B5x, x.st));
     CK(x.side_dw(R.h1, PBF(m, pre + "x.wq"), m.B2x, Mq, dd, dd, GF(m, pre + "x.wq"), nullptr));
     CK(x.side_dw(R.virt, PBF(m, pre + "x.wk"), m.B3x, Mq, dd, dd, GF(m, pre + "x.wk"), nullptr));
     CK(x.side_dw(R.virt, PBF(m, pre + "x.wv"), m.B5x, Mq, dd, dd, GF(m, pre + "x.wv"), nullptr));

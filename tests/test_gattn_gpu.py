@@ -43,6 +43,8 @@ CASES = [  # name, B, N, heads, head_dim, hidden, kind, width
     ("self_d32_h8", 3, 257, 8, 32, 4, "self", 5),
     ("self_h2_d16", 1, 200, 2, 16, 8, "self", 6),   # 32-wide rows: one dim per lane in the gather
     ("self_h8_d64", 1, 150, 8, 64, 8, "holes", 4),  # 512-wide rows
+    ("dec_b_self", 2, 600, 8, 32, 8, "self", 8),    # the AFFMAE-B decoder: 256-wide rows, 8 dims per lane
+    ("dec_b_cross", 2, 600, 8, 32, 8, "one", 1),
 ]
 
 

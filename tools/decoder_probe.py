@@ -52,6 +52,11 @@ def main():
     ws = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
     print("gattn bwd gather     %.3f ms" % timeit(lambda: ops.gattn_bwd(q, k, v, bk, bv, refs, idx, valid, bias, heads, hd,
                                                                     dout, gather=True, workspace=ws)))
+    i1 = torch.arange(Q, dtype=torch.int32, device="cuda").repeat(B, 1).reshape(B, Q, 1).contiguous()
+    v1 = torch.ones(B, Q, 1, dtype=torch.uint8, device="cuda")
+    print("gattn cross fwd      %.3f ms" % timeit(lambda: ops.gattn_fwd(q, k, v, bk, bv, refs, i1, v1, bias, heads, hd)))
+    print("gattn cross bwd      %.3f ms" % timeit(lambda: ops.gattn_bwd(q, k, v, bk, bv, refs, i1, v1, bias, heads, hd,
+                                                                    dout, gather=True, workspace=ws)))
     M = B * Q
     x = t(M, 256)
     w1 = t(512, 256)
