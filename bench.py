@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--interp-images", type=int, default=8,
                     help="images of the side measurement of the interpolation op (SURVEY §8(f) #2); 0 = off")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget")
-    ap.add_argument("--pretrain-batch", type=int, default=32, help="AFFMAE-B 1024^2 images per step (0: skip)")
+    ap.add_argument("--pretrain-batch", type=int, default=64, help="AFFMAE-B 1024^2 images per step (0: skip)")
     ap.add_argument("--pretrain-steps", type=int, default=5)
     ap.add_argument("--tiny-batch", type=int, default=64, help="AFF-tiny 224^2 images per step (0: skip)")
     ap.add_argument("--no-parity", action="store_true", help="skip the same-run oracle check")
@@ -888,7 +888,7 @@ def model_flops(cfg, tokens, q):
     return 3 * gemm + 3.5 * attn, gemm, attn
 
 
-def run_pretrain(cfg, steps, warmup=2, e2e_steps=3, label="", rank=0, world=1, dist=None):
+def run_pretrain(cfg, steps, warmup=3, e2e_steps=3, label="", rank=0, world=1, dist=None):
     """One training step of `cfg` (masks -> encode -> decode -> deep supervision -> loss ->
     backward -> AdamW) through the torch-free model API, captured as one CUDA graph; device
     img/s, plus e2e img/s with the step's images copied H2D from pinned host memory and the
