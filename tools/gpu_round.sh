@@ -15,5 +15,7 @@ B="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-gra
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_bench.log 2>&1; echo "ncu launches rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'attn_(fwd|bwd_q|bwd_kv)_kernel' -s 5 -c 5 \
   -o gpurun_out/prof_attn -f $B > gpurun_out/ncu_full.log 2>&1; echo "ncu attn rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'pool_fwd_v2|pool_bwd_v2|seg_sort|select_topk|nbr_v2_kernel|nbr_kernel|assign_kernel|attn_qrec|attn_krec' -s 9 -c 9 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'pool_fwd_v3|pool_bwd_v3|select_topk|assign_kernel|pool_topk|seg_sort|nbr_v2_kernel|attn_qrec|attn_krec' -s 9 -c 9 \
   -o gpurun_out/prof_merge -f $B > gpurun_out/ncu_full2.log 2>&1; echo "ncu index/merge rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/pretrain_launches.csv \
+  python tools/pretrain_probe.py --batch 16 --steps 1 --no-graph > gpurun_out/ncu_pretrain.log 2>&1; echo "ncu pretrain rc=$?"
