@@ -592,6 +592,20 @@ __global__ void knn_kernel(const float* __restrict__ queries, const float* __res
     }
 }
 
+// fp32 pre-filter of the exact binary64 scan.  d2f = the squared distance in fp32 is within a
+// relative 2^-21 of the binary64 d^2 the reference compares (exact float differences, three
+// roundings of 2^-24 each), so a key with d2f > (1 + 2^-17) * (current K-th binary64 d^2)
+// cannot enter the top-K: it is skipped without the binary64 arithmetic (the FP64 pipe is the
+// scan's bottleneck).  Every key that survives takes the exact path, so the selection and
+// its tie order are unchanged.
+__device__ __forceinline__ float knn_d2f(float2 p, float2 q) {
+    const float dx = __fsub_rn(p.x, q.x), dy = __fsub_rn(p.y, q.y);
+    return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+}
+__device__ __forceinline__ float knn_prune_bound(double kth) {
+    return kth < 1e37 ? __double2float_ru(kth * (1.0 + 0x1p-17)) : INFINITY;
+}
+
 // Few keys per image (<= 1024) and k <= 8: the image's keys staged once per block in shared
 // memory as binary64, one query per thread scanning all of them with a register top-K --
 // the same (d^2 binary64 without FMA, index) order as the reference's scan, no warp merge.
@@ -600,11 +614,13 @@ __global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__
                                                        int64_t nq, int64_t nk, int k, int32_t* __restrict__ idx,
                                                        uint8_t* __restrict__ valid) {
     extern __shared__ double2 skeys[];
+    float2* fkeys = reinterpret_cast<float2*>(skeys + nk);
     const int64_t b = blockIdx.y;
     const float2* kb = reinterpret_cast<const float2*>(keys) + b * nk;
     for (int64_t j = threadIdx.x; j < nk; j += blockDim.x) {
         const float2 p = kb[j];
         skeys[j] = make_double2(double(p.x), double(p.y));
+        fkeys[j] = p;
     }
     __syncthreads();
     const int64_t qi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -620,7 +636,29 @@ __global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__
         d[r] = INFINITY;
         jj[r] = INT32_MAX;
     }
+    // Prune bound before the scan: the K-th smallest fp32 d^2 over an evenly spaced sample of
+    // 4K keys is >= the true K-th (a subset's K-th is never smaller), so keys beyond it (with
+    // the knn_prune_bound margin) are skipped from the first key on -- the scan's register
+    // insertions, and the warp divergence they cause, drop to the few keys inside it.
+    float thr = INFINITY;
+    if (nk >= 8 * K) {
+        float sd[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) sd[r] = INFINITY;
+        for (int i = 0; i < 4 * K; ++i) {
+            float v = knn_d2f(fkeys[int(int64_t(i) * nk / (4 * K))], q);
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                const float lo = fminf(v, sd[r]);
+                v = fmaxf(v, sd[r]);
+                sd[r] = lo;
+            }
+        }
+        thr = sd[K - 1] < 1e37f ? __fmul_ru(sd[K - 1], 1.f + 0x1p-16f) : INFINITY;
+    }
     for (int j = 0; j < int(nk); ++j) {
+        const float2 pf = fkeys[j];
+        if (knn_d2f(pf, q) > thr) continue;
         const double2 p = skeys[j];
         const double dx = __dsub_rn(p.x, qx), dy = __dsub_rn(p.y, qy);
         double nd = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
@@ -637,6 +675,7 @@ __global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__
                 nj = tj;
             }
         }
+        thr = fminf(thr, knn_prune_bound(d[K - 1]));
     }
 #pragma unroll
     for (int t = 0; t < K; ++t)
@@ -764,6 +803,7 @@ __global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __rest
         d[r] = INFINITY;
         jj[r] = INT32_MAX;
     }
+    float thr = INFINITY;  // fp32 pre-filter (knn_prune_bound)
     const int g = p.g;
     const int qcx = knn_cell(qx, p.x0, p.w, g), qcy = knn_cell(qy, p.y0, p.w, g);
     int found = 0;
@@ -783,10 +823,11 @@ __global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __rest
                 const int t1 = co[cell + 1];
                 for (int t = co[cell]; t < t1; ++t) {
                     const float2 v = ixy[t];
+                    ++found;
+                    if (knn_d2f(v, q) > thr) continue;
                     const int j = it[t];
                     const double dx = __dsub_rn(double(v.x), qx), dy = __dsub_rn(double(v.y), qy);
                     const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-                    ++found;
                     if (!pair_lt(d2, j, d[KM - 1], jj[KM - 1])) continue;
                     double nd = d2;
                     int nj = j;
@@ -801,6 +842,7 @@ __global__ void __launch_bounds__(128) knn_grid_query_kernel(const float* __rest
                             nj = tj;
                         }
                     }
+                    thr = knn_prune_bound(d[KM - 1]);
                 }
             }
         }
@@ -1017,7 +1059,7 @@ int knn(const float* queries, const float* keys, int64_t batch, int64_t nq, int6
     cudaStream_t st = as_stream(stream);
     if (k <= 8 && nk <= 1024 && nq >= 256) {  // few keys, many queries: keys in shared memory
         const dim3 grid(unsigned((nq + 255) / 256), unsigned(batch));
-        const size_t smem = size_t(nk) * sizeof(double2);
+        const size_t smem = size_t(nk) * (sizeof(double2) + sizeof(float2));
         if (smem > 40 * 1024)
             AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(knn_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    int(smem)));

@@ -334,6 +334,13 @@ __global__ void cell_fill_kernel(const float* __restrict__ coords, const int32_t
 __device__ __forceinline__ bool better(double d, int ri, double bd, int bri) {
     return bri < 0 || d < bd || (d == bd && ri < bri);
 }
+// fp32 pre-filter of the binary64 distance (index.cu knn_d2f): the fp32 squared distance is
+// within a relative 2^-21 of the binary64 one, so a candidate whose fp32 value exceeds
+// (1 + 2^-17) * best cannot win (nor tie) and skips the FP64 arithmetic.
+__device__ __forceinline__ float d2_f32(float2 p, float2 q) {
+    const float dx = __fsub_rn(p.x, q.x), dy = __fsub_rn(p.y, q.y);
+    return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+}
 
 // exact nearest retained token of every dropped token (first-minimum rule)
 __global__ void assign_kernel(const float* __restrict__ coords, const int32_t* __restrict__ retained,
@@ -362,18 +369,21 @@ __global__ void assign_kernel(const float* __restrict__ coords, const int32_t* _
     const int qcx = cell_of(qx, p.x0, p.w, g), qcy = cell_of(qy, p.y0, p.w, g);
     double bd = 0.0;
     int bri = -1;
+    float thr = INFINITY;
     for (int ring = 0; ring <= g; ++ring) {
         const int x0 = qcx - ring, x1 = qcx + ring, y0 = qcy - ring, y1 = qcy + ring;
         auto visit = [&](int cx, int cy) {
             const int cell = cy * g + cx;
             for (int t = co[cell]; t < co[cell + 1]; ++t) {
-                const int ri = it[t];
                 const float2 v = ixy[t];
+                if (d2_f32(v, q) > thr) continue;
+                const int ri = it[t];
                 const double dx = __dsub_rn(double(v.x), qx), dy = __dsub_rn(double(v.y), qy);
                 const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
                 if (better(d2, ri, bd, bri)) {
                     bd = d2;
                     bri = ri;
+                    thr = bd < 1e37 ? __double2float_ru(bd * (1.0 + 0x1p-17)) : INFINITY;
                 }
             }
         };
