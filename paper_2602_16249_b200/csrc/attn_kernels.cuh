@@ -554,13 +554,17 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
         bvr[nd][1] = __bfloat162float(p.bv[h * HD + nd * 8 + c0 + 1]);
     }
     auto rec_of = [&](int it) -> int32_t* { return sm.rec[it % 3]; };
-    auto copy_item_rec = [&](int item, int it) {
-        if (item < n_items) copy_rec<C::QW>(rec_of(it), p.qrec + size_t(__ldg(list + item)) * C::QW, lane);
+    // list entries are read one iteration before their record is copied (a dependent global
+    // load off the critical path)
+    auto list_at = [&](int item) -> int { return item < n_items ? __ldg(list + item) : 0; };
+    auto copy_item_rec = [&](int item, int entry, int it) {
+        if (item < n_items) copy_rec<C::QW>(rec_of(it), p.qrec + size_t(entry) * C::QW, lane);
     };
 
     const int i0 = blockIdx.x;
-    copy_item_rec(i0, 0);
-    copy_item_rec(i0 + stride, 1);
+    copy_item_rec(i0, list_at(i0), 0);
+    copy_item_rec(i0 + stride, list_at(i0 + stride), 1);
+    int next_entry = list_at(i0 + 2 * stride);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
@@ -580,7 +584,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
         const int i1 = item + stride;
         cp_async_wait<1>();  // Q, K (and record i+1) landed; V may be in flight
         __syncwarp();
-        copy_item_rec(item + 2 * stride, it + 2);
+        copy_item_rec(item + 2 * stride, next_entry, it + 2);
+        next_entry = list_at(item + 3 * stride);
         cp_async_commit();
         const int32_t* rec = rec_of(it);
         const int32_t* rec1 = rec_of(it + 1);
@@ -728,8 +733,9 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
     for (int nd = 0; nd < HD / 8; ++nd) gbk[nd][0] = gbk[nd][1] = gbv[nd][0] = gbv[nd][1] = 0.f;
     float gblank = 0.f;
 
-    auto copy_item_rec = [&](int item, int32_t* dst) {
-        if (item < n_items) copy_rec<C::QW>(dst, p.qrec + size_t(__ldg(list + item)) * C::QW, lane);
+    auto list_at = [&](int item) -> int { return item < n_items ? __ldg(list + item) : 0; };
+    auto copy_item_rec = [&](int item, int entry, int32_t* dst) {
+        if (item < n_items) copy_rec<C::QW>(dst, p.qrec + size_t(entry) * C::QW, lane);
     };
     auto issue_qo = [&](const int32_t* rec, int64_t img_tok) {
         sw_gather<HD, 16>(sm.Q, qg + img_tok * ld, rowb, rec + R::QTOK, lane);
@@ -743,8 +749,9 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
 
     const int i0 = blockIdx.x;
     int rc = 0;  // ring slot of the current item's record
-    copy_item_rec(i0, sm.rec[0]);
-    copy_item_rec(i0 + stride, sm.rec[1]);
+    copy_item_rec(i0, list_at(i0), sm.rec[0]);
+    copy_item_rec(i0 + stride, list_at(i0 + stride), sm.rec[1]);
+    int next_entry = list_at(i0 + 2 * stride);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
@@ -761,7 +768,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         const int r1 = rc == 2 ? 0 : rc + 1, r2 = r1 == 2 ? 0 : r1 + 1;
         cp_async_wait<0>();  // rows of this item and the record of the next one landed
         __syncwarp();
-        copy_item_rec(item + 2 * stride, sm.rec[r2]);
+        copy_item_rec(item + 2 * stride, next_entry, sm.rec[r2]);
+        next_entry = list_at(item + 3 * stride);
         cp_async_commit();
         const int32_t* rec = sm.rec[rc];
         const int32_t* rec1 = sm.rec[r1];
