@@ -452,30 +452,51 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     float g0 = 0.f, g1 = 0.f;
 #pragma unroll
     for (int j = 0; j < V; ++j) a0[j] = a1[j] = make_float2(0.f, 0.f);
-    for (int64_t r = int64_t(blockIdx.x) * kRowWarps + warp; r < rows; r += int64_t(gridDim.x) * kRowWarps) {
-        const float2 p = pre[r], g = dqpos[r];
-        const double rr = sqrt(double(p.x) * double(p.x) + double(p.y) * double(p.y));
-        float d0 = g.x, d1 = g.y;
-        if (rr > limit) {
-            const double f = limit / rr;
-            const double dot = (double(g.x) * p.x + double(g.y) * p.y) / (rr * rr);
-            d0 = float(f * (g.x - dot * p.x));
-            d1 = float(f * (g.y - dot * p.y));
+    // R rows per warp iteration: their loads are independent (memory-level parallelism)
+    constexpr int R = 4;
+    const int64_t step = int64_t(gridDim.x) * kRowWarps * R;
+    for (int64_t r0 = (int64_t(blockIdx.x) * kRowWarps + warp) * R; r0 < rows; r0 += step) {
+        float d0[R], d1[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            d0[i] = d1[i] = 0.f;
+            const int64_t r = r0 + i;
+            if (r >= rows) continue;
+            const float2 p = pre[r], g = dqpos[r];
+            const double rr = sqrt(double(p.x) * double(p.x) + double(p.y) * double(p.y));
+            d0[i] = g.x;
+            d1[i] = g.y;
+            if (rr > limit) {
+                const double f = limit / rr;
+                const double dot = (double(g.x) * p.x + double(g.y) * p.y) / (rr * rr);
+                d0[i] = float(f * (g.x - dot * p.x));
+                d1[i] = float(f * (g.y - dot * p.y));
+            }
+            g0 += d0[i];
+            g1 += d1[i];
         }
-        g0 += d0;
-        g1 += d1;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const int c = 2 * (lane + 32 * j);
-            const float2 x = ld2(fq, r * C + c), w0 = ld2(w, c), w1 = ld2(w, C + c);
-            a0[j].x += d0 * x.x;
-            a0[j].y += d0 * x.y;
-            a1[j].x += d1 * x.x;
-            a1[j].y += d1 * x.y;
-            float2 o = ld2(dfq, r * C + c);
-            o.x += d0 * w0.x + d1 * w1.x;
-            o.y += d0 * w0.y + d1 * w1.y;
-            st2(dfq, r * C + c, o);
+            const float2 w0 = ld2(w, c), w1 = ld2(w, C + c);
+            float2 x[R], o[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (r0 + i < rows) {
+                    x[i] = ld2(fq, (r0 + i) * C + c);
+                    o[i] = ld2(dfq, (r0 + i) * C + c);
+                }
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                if (r0 + i < rows) {
+                    a0[j].x += d0[i] * x[i].x;
+                    a0[j].y += d0[i] * x[i].y;
+                    a1[j].x += d1[i] * x[i].x;
+                    a1[j].y += d1[i] * x[i].y;
+                    o[i].x += d0[i] * w0.x + d1[i] * w1.x;
+                    o[i].y += d0[i] * w0.y + d1[i] * w1.y;
+                    st2(dfq, (r0 + i) * C + c, o[i]);
+                }
         }
     }
     for (int ww = 0; ww < kRowWarps; ++ww) {
@@ -716,11 +737,18 @@ __global__ void colsum_f32_partial_kernel(const float* __restrict__ x, int64_t r
     const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= cols) return;
     const int64_t r0 = int64_t(blockIdx.y) * rows_per, r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
-    float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) s += x[r * cols + c];
-    part[int64_t(blockIdx.y) * cols + c] = s;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // four independent loads in flight
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4) {
+        s0 += x[r * cols + c];
+        s1 += x[(r + 1) * cols + c];
+        s2 += x[(r + 2) * cols + c];
+        s3 += x[(r + 3) * cols + c];
+    }
+    for (; r < r1; ++r) s0 += x[r * cols + c];
+    part[int64_t(blockIdx.y) * cols + c] = (s0 + s1) + (s2 + s3);
 }
-constexpr int kColChunks = 64;
+constexpr int kColChunks = 1024;  // row chunks: enough blocks to fill the GPU for narrow rows
 int colsum_f32(const float* x, int64_t rows, int64_t cols, float* out, float* part, cudaStream_t st) {
     if (rows <= 0) return AFFMAE_OK;
     const int64_t rows_per = (rows + kColChunks - 1) / kColChunks;
