@@ -30,6 +30,10 @@ struct GAttnP {
     float scale, inv_patch;
     float2* dsw;  // backward gather mode: {scale dS, w} per (entry, head); nullptr = scatter dk / dv
     int o2o;      // backward: row i's only key is token i (bf16 dk / dv stored directly)
+    // row strides (elements): q rows, k / v rows, and the bf16 gradient outputs dq (and the
+    // one-to-one dk / dv): D for dense tensors, 3D / 2D when they are column slices of one
+    // fused QKV / KV projection.  out / dout / fp32 dk, dv are always dense.
+    int64_t ldq, ldkv, ldd, lddkv;
     float* part;  // row backward: per-block parameter-gradient rows (fixed-order reduce), else atomics
     int part_blocks;  // rows in `part` (caps the grid)
 };
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(256) gattn_fwd_kernel(GAttnP p, __nv_bfloat16*
     for (int64_t gi = int64_t(blockIdx.x) * 32 + lane; gi < ntok; gi += int64_t(gridDim.x) * 32) {
         const int64_t b0 = (gi / p.n) * p.n;
         float qf[HD], acc[HD];
-        gload_row<HD>(p.q + gi * ld + h * HD, qf, p.scale);
+        gload_row<HD>(p.q + gi * p.ldq + h * HD, qf, p.scale);
 #pragma unroll
         for (int c = 0; c < HD; ++c) acc[c] = 0.f;
         const float2 qx = xy[gi];
@@ -155,9 +159,9 @@ __global__ void __launch_bounds__(256) gattn_fwd_kernel(GAttnP p, __nv_bfloat16*
         auto slot = [&](int32_t t) {
             const int64_t key = b0 + t;
             const float2 kx = xy[key];
-            const float s = gdot<HD>(qf, p.k + key * ld + h * HD) +
+            const float s = gdot<HD>(qf, p.k + key * p.ldkv + h * HD) +
                             gbias(un, p.hidden, b2, (kx.x - qx.x) * p.inv_patch, (kx.y - qx.y) * p.inv_patch);
-            take(s, p.v + key * ld + h * HD);
+            take(s, p.v + key * p.ldkv + h * HD);
         };
         if (p.m == 8) {  // the decoder's self_k rows: two 16-byte index loads and one 8-byte valid load
             const int4 i0 = __ldg(reinterpret_cast<const int4*>(ir)), i1 = __ldg(reinterpret_cast<const int4*>(ir) + 1);
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
         const int64_t row = act ? gi : base;
         const int64_t b0 = (row / p.n) * p.n;
         float qf[HD], gf[HD];
-        gload_row<HD>(p.q + row * ld + h * HD, qf, 1.f);
+        gload_row<HD>(p.q + row * p.ldq + h * HD, qf, 1.f);
         gload_row<HD>(dout + row * ld + h * HD, gf, 1.f);
         const float2 qx = xy[row];
         float w[MW], dS[MW];
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
             if (ok) {
                 key[j] = id;
                 const float2 kx = xy[b0 + key[j]];
-                w[j] = p.scale * gdot<HD>(qf, p.k + (b0 + key[j]) * ld + h * HD) +
+                w[j] = p.scale * gdot<HD>(qf, p.k + (b0 + key[j]) * p.ldkv + h * HD) +
                        gbias(un, H, b2, (kx.x - qx.x) * p.inv_patch, (kx.y - qx.y) * p.inv_patch);
                 mx = fmaxf(mx, w[j]);
             }
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
 #pragma unroll
         for (int j = 0; j < MW; ++j) {
             w[j] *= il;
-            dS[j] = key[j] >= 0 ? gdot<HD>(gf, p.v + (b0 + key[j]) * ld + h * HD) : 0.f;
+            dS[j] = key[j] >= 0 ? gdot<HD>(gf, p.v + (b0 + key[j]) * p.ldkv + h * HD) : 0.f;
             D = fmaf(w[j], dS[j], D);
         }
         wb *= il;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
             s2 += dS[j];
             const int64_t kr = (b0 + key[j]) * ld + h * HD;
             float kf[HD];
-            gload_row<HD>(p.k + kr, kf, 1.f);
+            gload_row<HD>(p.k + (b0 + key[j]) * p.ldkv + h * HD, kf, 1.f);
             const float a = p.scale * dS[j];
             if (p.dsw) p.dsw[(gi * p.m + j) * p.heads + h] = make_float2(a, w[j]);
 #pragma unroll
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
         if (act) {
             float bkf[HD];
             gload_row<HD>(p.bk + h * HD, bkf, 1.f);
-            uint4* o = reinterpret_cast<uint4*>(dq + gi * ld + h * HD);
+            uint4* o = reinterpret_cast<uint4*>(dq + gi * p.ldd + h * HD);
 #pragma unroll
             for (int c = 0; c < HD; c += 8) {
                 uint4 v;
@@ -547,13 +551,13 @@ __global__ void __launch_bounds__(256, 2) gattn_fwd_reg_kernel(GAttnP p, __nv_bf
         int key[MW];
         row_ids<MW>(p, gi, key);
         uint32_t qw[VPL / 2];
-        ld_slice<VPL>(p.q + gi * D + lane * VPL, qw);
+        ld_slice<VPL>(p.q + gi * p.ldq + lane * VPL, qw);
         uint32_t kw[MW][VPL / 2], vw[MW][VPL / 2];
 #pragma unroll
         for (int j = 0; j < MW; ++j)
             if (key[j] >= 0) {
-                ld_slice<VPL>(p.k + (b0 + key[j]) * D + lane * VPL, kw[j]);
-                ld_slice<VPL>(p.v + (b0 + key[j]) * D + lane * VPL, vw[j]);
+                ld_slice<VPL>(p.k + (b0 + key[j]) * p.ldkv + lane * VPL, kw[j]);
+                ld_slice<VPL>(p.v + (b0 + key[j]) * p.ldkv + lane * VPL, vw[j]);
             }
         float qf[VPL];
         unpack_slice<VPL>(qw, qf, p.scale);
@@ -652,13 +656,13 @@ __device__ __forceinline__ void g_issue(uint8_t* st, const GAttnP& p, const __nv
     using G = GStage<VPL, MW, BWD>;
     constexpr int D = G::D;
     auto* rows = reinterpret_cast<__nv_bfloat16*>(st) + lane * VPL;
-    cp_slice<VPL>(rows, p.q + gi * D + lane * VPL);
+    cp_slice<VPL>(rows, p.q + gi * p.ldq + lane * VPL);
     if constexpr (BWD) cp_slice<VPL>(rows + D, dout + gi * D + lane * VPL);
 #pragma unroll
     for (int j = 0; j < MW; ++j)
         if (key[j] >= 0) {
-            cp_slice<VPL>(rows + (G::KR + j) * D, p.k + (b0 + key[j]) * D + lane * VPL);
-            cp_slice<VPL>(rows + (G::VR + j) * D, p.v + (b0 + key[j]) * D + lane * VPL);
+            cp_slice<VPL>(rows + (G::KR + j) * D, p.k + (b0 + key[j]) * p.ldkv + lane * VPL);
+            cp_slice<VPL>(rows + (G::VR + j) * D, p.v + (b0 + key[j]) * p.ldkv + lane * VPL);
         }
     // coordinates: lane 0 the query's, lane 1 + j neighbour j's
     float2* cx = reinterpret_cast<float2*>(st + G::ROW_BYTES);
@@ -883,8 +887,8 @@ __global__ void __launch_bounds__(256) gattn_bwd_row_kernel(GAttnP p, const __nv
                 float t[VPL];
 #pragma unroll
                 for (int i = 0; i < VPL; ++i) t[i] = a * qf[i];
-                st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dk) + gi * D + lane * VPL, t, 1.f);
-                st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dv) + gi * D + lane * VPL, gf, s[j]);
+                st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dk) + gi * p.lddkv + lane * VPL, t, 1.f);
+                st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dv) + gi * p.lddkv + lane * VPL, gf, s[j]);
             } else {
                 float* pk = dk + (b0 + key0[j]) * D + lane * VPL;
                 float* pv = dv + (b0 + key0[j]) * D + lane * VPL;
@@ -908,10 +912,10 @@ __global__ void __launch_bounds__(256) gattn_bwd_row_kernel(GAttnP p, const __nv
             float z[VPL];
 #pragma unroll
             for (int i = 0; i < VPL; ++i) z[i] = 0.f;
-            st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dk) + gi * D + lane * VPL, z, 1.f);
-            st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dv) + gi * D + lane * VPL, z, 1.f);
+            st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dk) + gi * p.lddkv + lane * VPL, z, 1.f);
+            st_slice<VPL>(reinterpret_cast<__nv_bfloat16*>(dv) + gi * p.lddkv + lane * VPL, z, 1.f);
         }
-        st_slice<VPL>(dq + gi * D + lane * VPL, dqa, p.scale);
+        st_slice<VPL>(dq + gi * p.ldd + lane * VPL, dqa, p.scale);
         // parameter gradients
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
@@ -990,7 +994,7 @@ __global__ void __launch_bounds__(256) gattn_kv_gather_kernel(const int32_t* __r
                                                               const int32_t* __restrict__ ent_key,
                                                               const float2* __restrict__ dsw, int64_t batch,
                                                               int64_t n, int m, int heads, int hd,
-                                                              const __nv_bfloat16* __restrict__ q,
+                                                              const __nv_bfloat16* __restrict__ q, int64_t ldq,
                                                               const __nv_bfloat16* __restrict__ dout,
                                                               float* __restrict__ dk, float* __restrict__ dv) {
     constexpr int VPL = D / 32;
@@ -1041,7 +1045,7 @@ __global__ void __launch_bounds__(256) gattn_kv_gather_kernel(const int32_t* __r
             }
             const float2 sw = __ldg(dsw + int64_t(e) * heads + h);
             const int64_t row = e / m;
-            const __nv_bfloat16* qr = q + row * D + lane * VPL;
+            const __nv_bfloat16* qr = q + row * ldq + lane * VPL;
             const __nv_bfloat16* gr = dout + row * D + lane * VPL;
             if constexpr (VPL == 1) {
                 ak[0] = fmaf(sw.x, __bfloat162float(qr[0]), ak[0]);
@@ -1104,6 +1108,20 @@ static int gattn_fill(GAttnP& p, const affmae_attn_desc* a, const affmae_attn_in
     p.hidden = a->bias_hidden;
     p.scale = float(1.0 / std::sqrt(double(a->head_dim)));
     p.inv_patch = float(1.0 / a->patch);
+    p.ldq = p.ldkv = p.ldd = p.lddkv = int64_t(a->heads) * a->head_dim;
+    return AFFMAE_OK;
+}
+// optional strides (0 = dense); row starts stay 16-byte aligned for the vector row loads
+static int gattn_strides(GAttnP& p, int64_t ldq, int64_t ldkv, int64_t ldd, int64_t lddkv) {
+    const int64_t D = p.ldq;
+    for (int64_t* f : {&ldq, &ldkv, &ldd, &lddkv}) {
+        if (*f == 0) *f = D;
+        if (*f < D || *f % 8) return fail(AFFMAE_ECONFIG, "gattn: row stride below D or not a multiple of 8");
+    }
+    p.ldq = ldq;
+    p.ldkv = ldkv;
+    p.ldd = ldd;
+    p.lddkv = lddkv;
     return AFFMAE_OK;
 }
 
@@ -1197,10 +1215,12 @@ static int row_bwd_launch(const GAttnP& p, int upl, cudaStream_t st, const __nv_
 }
 
 int gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
-              int64_t batch, int64_t tokens, int64_t width, void* out, float* lse, void* stream) {
+              int64_t batch, int64_t tokens, int64_t width, void* out, float* lse, void* stream, int64_t ldq,
+              int64_t ldkv) {
     GAttnP p{};
     int rc = gattn_fill(p, a, in, idx, valid, batch, tokens, width);
     if (rc) return rc;
+    if ((rc = gattn_strides(p, ldq, ldkv, 0, 0))) return rc;
     if (!out || !lse) return fail(AFFMAE_ECONFIG, "gattn: null output");
     if (batch == 0) return AFFMAE_OK;
     const size_t sm = size_t(a->heads) * a->bias_hidden * sizeof(float4);
@@ -1237,10 +1257,11 @@ static void gattn_bwd_launch(int mw, unsigned nb, dim3 bt, size_t sm, cudaStream
 int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
               int64_t batch, int64_t tokens, int64_t width, const void* dout, void* dq, float* dk, float* dv,
               float* dbk, float* dbv, float* dw1, float* db1, float* dw2, float* db2, float* dblank, void* workspace,
-              size_t ws_bytes, void* stream) {
+              size_t ws_bytes, void* stream, int64_t ldq, int64_t ldkv, int64_t ldd) {
     GAttnP p{};
     int rc = gattn_fill(p, a, in, idx, valid, batch, tokens, width);
     if (rc) return rc;
+    if ((rc = gattn_strides(p, ldq, ldkv, ldd, 0))) return rc;
     if (!dout || !dq || !dk || !dv || !dbk || !dbv || !dw1 || !db1 || !dw2 || !db2 || !dblank)
         return fail(AFFMAE_ECONFIG, "gattn bwd: null output");
     if (batch == 0) return AFFMAE_OK;
@@ -1287,7 +1308,7 @@ int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
 #define AFFMAE_GG(D_)                                                                                           \
     case D_:                                                                                                    \
         gattn_kv_gather_kernel<D_><<<gb, 256, 0, st>>>(off, ent, ent_key, p.dsw, batch, tokens, mw, a->heads,   \
-                                                       a->head_dim, qq, g, dk, dv);                             \
+                                                       a->head_dim, qq, p.ldq, g, dk, dv);                      \
         break;
         switch (D) {
             AFFMAE_GG(32)
@@ -1305,10 +1326,11 @@ int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
 int gattn_bwd_o2o(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
                   int64_t batch, int64_t tokens, const void* dout, void* dq, void* dk_bf16, void* dv_bf16, float* dbk,
                   float* dbv, float* dw1, float* db1, float* dw2, float* db2, float* dblank, void* workspace,
-                  size_t ws_bytes, void* stream) {
+                  size_t ws_bytes, void* stream, int64_t ldq, int64_t ldkv, int64_t ldd, int64_t lddkv) {
     GAttnP p{};
     int rc = gattn_fill(p, a, in, idx, valid, batch, tokens, 1);
     if (rc) return rc;
+    if ((rc = gattn_strides(p, ldq, ldkv, ldd, lddkv))) return rc;
     if (!dout || !dq || !dk_bf16 || !dv_bf16 || !dbk || !dbv || !dw1 || !db1 || !dw2 || !db2 || !dblank)
         return fail(AFFMAE_ECONFIG, "gattn bwd o2o: null output");
     const int vpl = row_vpl(a, 1);

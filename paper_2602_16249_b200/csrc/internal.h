@@ -43,18 +43,20 @@ int interp_fwd(const float*, const float*, const void*, const int32_t*, const ui
                int64_t, int64_t, const float*, double, void*, void*);
 int interp_bwd(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t, int64_t,
                int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*);
+// trailing strides (elements, 0 = dense): q rows, k / v rows, dq rows (see GAttnP)
 int gattn_fwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
-              int64_t, void*, float*, void*);
+              int64_t, void*, float*, void*, int64_t ldq = 0, int64_t ldkv = 0);
 int gattn_bwd(const affmae_attn_desc*, const affmae_attn_inputs*, const int32_t*, const uint8_t*, int64_t, int64_t,
               int64_t, const void*, void*, float*, float*, float*, float*, float*, float*, float*, float*, float*,
-              void*, size_t, void*);
+              void*, size_t, void*, int64_t ldq = 0, int64_t ldkv = 0, int64_t ldd = 0);
 size_t gattn_bwd_workspace(const affmae_attn_desc*, int64_t, int64_t, int64_t);
 // one-to-one rows (idx[i] = i, all valid: the decoder's cross attention): bf16 dk / dv stored
 // directly, every row written (no zero fill, reductions or cast pass)
 int gattn_bwd_o2o(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
                   int64_t batch, int64_t tokens, const void* dout, void* dq, void* dk_bf16, void* dv_bf16, float* dbk,
                   float* dbv, float* dw1, float* db1, float* dw2, float* db2, float* dblank, void* workspace,
-                  size_t ws_bytes, void* stream);
+                  size_t ws_bytes, void* stream, int64_t ldq = 0, int64_t ldkv = 0, int64_t ldd = 0,
+                  int64_t lddkv = 0);
 size_t interp_bwd_gather_workspace(int64_t, int64_t, int64_t, int64_t);
 int interp_bwd_gather(const float*, const float*, const void*, const int32_t*, const uint8_t*, int64_t, int64_t,
                       int64_t, int64_t, int64_t, const float*, double, const void*, float*, float*, float*, void*,

@@ -127,7 +127,9 @@ struct DecRound {
     int32_t* gidx;
     uint8_t* gval;
     bf16* virt;
-    bf16 *h1, *q1, *k1, *v1, *a1, *h2, *q2, *k2, *v2, *a2, *h3, *pre, *m;
+    // q1 [M, dd]; kv1 [M, 2dd] = k1 | v1 (one GEMM from the virtual tokens); qkv2 [M, 3dd]
+    // = q2 | k2 | v2 (one GEMM from h2): the attention kernels read them as strided slices
+    bf16 *h1, *q1, *kv1, *a1, *h2, *qkv2, *a2, *h3, *pre, *m;
     float *lse1, *lse2;
     float2 *st1, *st2, *st3;
 };
@@ -200,11 +202,13 @@ struct affmae_model {
     float* part = nullptr;
     float *F1 = nullptr, *F2 = nullptr, *F3 = nullptr, *F4 = nullptr, *F5 = nullptr, *dz = nullptr, *dscores = nullptr;
     float *dfq = nullptr, *dqpos = nullptr, *dqjunk = nullptr;
-    __nv_bfloat16 *T1 = nullptr, *B1 = nullptr, *B2 = nullptr, *B3 = nullptr, *B4 = nullptr, *B5 = nullptr,
+    __nv_bfloat16 *T1 = nullptr, *B1 = nullptr, *B2 = nullptr, *B4 = nullptr,
                   *B6 = nullptr, *dfbf = nullptr, *dfq_bf = nullptr;
     // second copies of the scratch the side-stream weight gradients read, so the main stream's
     // next writer does not have to wait for them (see Ctx::side_dw)
-    __nv_bfloat16 *B4b = nullptr, *dfbf2 = nullptr, *dfq_bf2 = nullptr, *B2x = nullptr, *B3x = nullptr, *B5x = nullptr;
+    __nv_bfloat16 *B4b = nullptr, *dfbf2 = nullptr, *dfq_bf2 = nullptr, *B2x = nullptr;
+    // decoder: dY of the fused self-attention q | k | v and cross-attention k | v projections
+    __nv_bfloat16 *dqkv = nullptr, *dkv = nullptr;
     cudaStream_t side = nullptr;       // weight-gradient GEMMs of the backward
     std::vector<cudaEvent_t> events;   // fork / join events of one step (reused every step)
     uint8_t* gws2 = nullptr;           // GEMM workspace of the side stream
@@ -505,8 +509,9 @@ void layout(Model& m, Arena& a) {
             r.gidx = a.take<int32_t>(Mq * c.gather_k);
             r.gval = a.take<uint8_t>(Mq * c.gather_k);
             r.virt = a.take<bf16>(Mqp * dd);
-            for (bf16** b : {&r.h1, &r.q1, &r.k1, &r.v1, &r.a1, &r.h2, &r.q2, &r.k2, &r.v2, &r.a2, &r.h3})
-                *b = a.take<bf16>(Mqp * dd);
+            for (bf16** b : {&r.h1, &r.q1, &r.a1, &r.h2, &r.a2, &r.h3}) *b = a.take<bf16>(Mqp * dd);
+            r.kv1 = a.take<bf16>(Mqp * 2 * dd);
+            r.qkv2 = a.take<bf16>(Mqp * 3 * dd);
             r.pre = a.take<bf16>(Mqp * 2 * dd);
             r.m = a.take<bf16>(Mqp * 2 * dd);
             r.lse1 = a.take<float>(Mq * c.dec_heads);
@@ -554,18 +559,16 @@ void layout(Model& m, Arena& a) {
     m.dqjunk = a.take<float>(Mq * 2);
     m.T1 = a.take<bf16>(eMD);
     m.B1 = a.take<bf16>(eB1);
-    m.B2 = a.take<bf16>(std::max(e16, Mqp * dd));
-    m.B3 = a.take<bf16>(Mqp * dd);
+    m.B2 = a.take<bf16>(e16);
     m.B4 = a.take<bf16>(e4);
-    m.B5 = a.take<bf16>(Mqp * dd);
     m.B6 = a.take<bf16>(eB6);
     m.dfbf = a.take<bf16>(eDf);
     m.dfbf2 = a.take<bf16>(eDf);
     m.B4b = a.take<bf16>(e4);
     m.dfq_bf2 = a.take<bf16>(Mqp * dd);
     m.B2x = a.take<bf16>(Mqp * dd);
-    m.B3x = a.take<bf16>(Mqp * dd);
-    m.B5x = a.take<bf16>(Mqp * dd);
+    m.dqkv = a.take<bf16>(Mqp * 3 * dd);
+    m.dkv = a.take<bf16>(Mqp * 2 * dd);
     m.dfq_bf = a.take<bf16>(Mqp * dd);
 }
 
@@ -823,18 +826,16 @@ int round_fwd(const Ctx& x, int si, int r, bool last) {
     CK(mk::ln_fwd(R.fq_in, nullptr, nullptr, nullptr, PF(m, pre + "ln1.g"), PF(m, pre + "ln1.b"), Mq, dd, R.h1, R.st1,
                   x.st));
     CK(x.fwd(R.h1, Mq, dd, PBF(m, pre + "x.wq"), dd, nullptr, R.q1));
-    CK(x.fwd(R.virt, Mq, dd, PBF(m, pre + "x.wk"), dd, nullptr, R.k1));
-    CK(x.fwd(R.virt, Mq, dd, PBF(m, pre + "x.wv"), dd, nullptr, R.v1));
-    affmae_attn_inputs in1 = attn_in(m, pre + "x.", R.q1, R.k1, R.v1, m.refs);
-    CK(gattn_fwd(&desc, &in1, m.one_idx, m.one_val, B, Q, 1, R.a1, R.lse1, x.sv()));
+    // wk | wv are adjacent in the arena (create checks): one [2dd, dd] projection
+    CK(x.fwd(R.virt, Mq, dd, PBF(m, pre + "x.wk"), 2 * dd, nullptr, R.kv1));
+    affmae_attn_inputs in1 = attn_in(m, pre + "x.", R.q1, R.kv1, R.kv1 + dd, m.refs);
+    CK(gattn_fwd(&desc, &in1, m.one_idx, m.one_val, B, Q, 1, R.a1, R.lse1, x.sv(), dd, 2 * dd));
     CK(x.fwd(R.a1, Mq, dd, PBF(m, pre + "x.wo"), dd, nullptr, m.T1));
     CK(mk::ln_fwd(R.fq_in, m.T1, R.fq_x, nullptr, PF(m, pre + "ln2.g"), PF(m, pre + "ln2.b"), Mq, dd, R.h2, R.st2,
                   x.st));
-    CK(x.fwd(R.h2, Mq, dd, PBF(m, pre + "s.wq"), dd, nullptr, R.q2));
-    CK(x.fwd(R.h2, Mq, dd, PBF(m, pre + "s.wk"), dd, nullptr, R.k2));
-    CK(x.fwd(R.h2, Mq, dd, PBF(m, pre + "s.wv"), dd, nullptr, R.v2));
-    affmae_attn_inputs in2 = attn_in(m, pre + "s.", R.q2, R.k2, R.v2, m.refs);
-    CK(gattn_fwd(&desc, &in2, m.self_idx, m.self_val, B, Q, c.self_k, R.a2, R.lse2, x.sv()));
+    CK(x.fwd(R.h2, Mq, dd, PBF(m, pre + "s.wq"), 3 * dd, nullptr, R.qkv2));  // wq | wk | wv
+    affmae_attn_inputs in2 = attn_in(m, pre + "s.", R.qkv2, R.qkv2 + dd, R.qkv2 + 2 * dd, m.refs);
+    CK(gattn_fwd(&desc, &in2, m.self_idx, m.self_val, B, Q, c.self_k, R.a2, R.lse2, x.sv(), 3 * dd, 3 * dd));
     CK(x.fwd(R.a2, Mq, dd, PBF(m, pre + "s.wo"), dd, nullptr, m.T1));
     CK(mk::ln_fwd(R.fq_x, m.T1, R.fq_s, nullptr, PF(m, pre + "ln3.g"), PF(m, pre + "ln3.b"), Mq, dd, R.h3, R.st3,
                   x.st));
@@ -987,7 +988,7 @@ int round_bwd(const Ctx& x, int si, int r) {
     affmae_attn_desc desc{c.dec_heads, int(dd / c.dec_heads), c.bias_hidden, double(c.patch)};
     // MLP
     // (weight gradients on the side stream; dfq's bf16 copy goes dfq_bf -> dfq_bf2 -> dfq_bf,
-    // the cross attention's dq / dk / dv use their own B2x / B3x / B5x)
+    // the cross attention's dq / dk | dv use their own B2x / dkv)
     CK(x.bwd_xw(R.m, PBF(m, pre + "mlp.w2"), m.dfq_bf, Mq, dd, 2 * dd, m.B4, GF(m, pre + "mlp.w2"),
                 GF(m, pre + "mlp.b2")));
     CK(gelu_bwd(R.pre, m.B4, Mq * 2 * dd, m.B4, x.sv()));
@@ -1001,46 +1002,41 @@ int round_bwd(const Ctx& x, int si, int r) {
     CK(cudaMemsetAsync(m.F2, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     CK(cudaMemsetAsync(m.F3, 0, size_t(Mq * dd) * 4, x.st) == cudaSuccess ? 0 : AFFMAE_ECUDA);
     {
-        affmae_attn_inputs in2 = attn_in(m, pre + "s.", R.q2, R.k2, R.v2, m.refs);
+        affmae_attn_inputs in2 = attn_in(m, pre + "s.", R.qkv2, R.qkv2 + dd, R.qkv2 + 2 * dd, m.refs);
         const std::string p = pre + "s.";
-        // reverse-CSR gather of dk / dv (no fp32 reductions): 1.85 -> 1.49 ms at B = 16
-        CK(x.guard(m.B2));
-        CK(gattn_bwd(&desc, &in2, m.self_idx, m.self_val, B, Q, c.self_k, m.B1, m.B2, m.F2, m.F3,
+        // reverse-CSR gather of dk / dv (no fp32 reductions): 1.85 -> 1.49 ms at B = 16; dq goes
+        // straight into the dq | dk | dv buffer of the fused projection's backward
+        CK(x.guard(m.dqkv));
+        CK(gattn_bwd(&desc, &in2, m.self_idx, m.self_val, B, Q, c.self_k, m.B1, m.dqkv, m.F2, m.F3,
                      GF(m, p + "blank_k"), GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"),
                      GF(m, p + "bias.w2"), GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), m.ws, m.ws_bytes,
-                     x.sv()));
+                     x.sv(), 3 * dd, 3 * dd, 3 * dd));
     }
-    CK(x.guard(m.B3));
-    CK(mk::cast_bf16(m.F2, Mq * dd, m.B3, x.st));
-    CK(x.guard(m.B5));
-    CK(mk::cast_bf16(m.F3, Mq * dd, m.B5, x.st));
-    CK(x.side_dw(R.h2, PBF(m, pre + "s.wq"), m.B2, Mq, dd, dd, GF(m, pre + "s.wq"), nullptr));
-    CK(x.side_dw(R.h2, PBF(m, pre + "s.wk"), m.B3, Mq, dd, dd, GF(m, pre + "s.wk"), nullptr));
-    CK(x.side_dw(R.h2, PBF(m, pre + "s.wv"), m.B5, Mq, dd, dd, GF(m, pre + "s.wv"), nullptr));
-    CK(x.bwd_x(m.B2, PBF(m, pre + "s.wq"), Mq, dd, dd, m.F1, 0.f));
-    CK(x.bwd_x(m.B3, PBF(m, pre + "s.wk"), Mq, dd, dd, m.F1, 1.f));
-    CK(x.bwd_x(m.B5, PBF(m, pre + "s.wv"), Mq, dd, dd, m.F1, 1.f));
+    CK(mk::cast_bf16_2d(m.F2, Mq, dd, m.dqkv + dd, 3 * dd, x.st));
+    CK(mk::cast_bf16_2d(m.F3, Mq, dd, m.dqkv + 2 * dd, 3 * dd, x.st));
+    // one dW GEMM (N = 3dd) and one dX GEMM (K = 3dd) for the fused q | k | v projection
+    CK(x.side_dw(R.h2, PBF(m, pre + "s.wq"), m.dqkv, Mq, 3 * dd, dd, GF(m, pre + "s.wq"), nullptr));
+    CK(x.bwd_x(m.dqkv, PBF(m, pre + "s.wq"), Mq, 3 * dd, dd, m.F1, 0.f));
     CK(x.guard(m.dfq_bf));
     CK(mk::ln_bwd(m.F1, R.fq_x, R.st2, PF(m, pre + "ln2.g"), Mq, dd, m.dfq, m.dfq, m.dfq_bf, GF(m, pre + "ln2.g"),
                   GF(m, pre + "ln2.b"), m.part, x.st));
     // cross attention over (virtual token, blank)
     CK(x.bwd_xw(R.a1, PBF(m, pre + "x.wo"), m.dfq_bf, Mq, dd, dd, m.B1, GF(m, pre + "x.wo"), nullptr));
-    {   // one-to-one rows: dq, dk, dv straight to bf16 (every key row has exactly one query)
-        affmae_attn_inputs in1 = attn_in(m, pre + "x.", R.q1, R.k1, R.v1, m.refs);
+    {   // one-to-one rows: dq, dk, dv straight to bf16 (every key row has exactly one query);
+        // dk | dv land in one [Mq, 2dd] buffer, the fused k | v projection's dY
+        affmae_attn_inputs in1 = attn_in(m, pre + "x.", R.q1, R.kv1, R.kv1 + dd, m.refs);
         const std::string p = pre + "x.";
         CK(x.guard(m.B2x));
-        CK(x.guard(m.B3x));
-        CK(x.guard(m.B5x));
-        CK(gattn_bwd_o2o(&desc, &in1, m.one_idx, m.one_val, B, Q, m.B1, m.B2x, m.B3x, m.B5x, GF(m, p + "blank_k"),
-                         GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"), GF(m, p + "bias.w2"),
-                         GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), m.ws, m.ws_bytes, x.sv()));
+        CK(x.guard(m.dkv));
+        CK(gattn_bwd_o2o(&desc, &in1, m.one_idx, m.one_val, B, Q, m.B1, m.B2x, m.dkv, m.dkv + dd,
+                         GF(m, p + "blank_k"), GF(m, p + "blank_v"), GF(m, p + "bias.w1"), GF(m, p + "bias.b1"),
+                         GF(m, p + "bias.w2"), GF(m, p + "bias.b2"), GF(m, p + "bias.blank"), m.ws, m.ws_bytes,
+                         x.sv(), dd, 2 * dd, dd, 2 * dd));
     }
     CK(x.side_dw(R.h1, PBF(m, pre + "x.wq"), m.B2x, Mq, dd, dd, GF(m, pre + "x.wq"), nullptr));
-    CK(x.side_dw(R.virt, PBF(m, pre + "x.wk"), m.B3x, Mq, dd, dd, GF(m, pre + "x.wk"), nullptr));
-    CK(x.side_dw(R.virt, PBF(m, pre + "x.wv"), m.B5x, Mq, dd, dd, GF(m, pre + "x.wv"), nullptr));
+    CK(x.side_dw(R.virt, PBF(m, pre + "x.wk"), m.dkv, Mq, 2 * dd, dd, GF(m, pre + "x.wk"), nullptr));
     CK(x.bwd_x(m.B2x, PBF(m, pre + "x.wq"), Mq, dd, dd, m.F1, 0.f));
-    CK(x.bwd_x(m.B3x, PBF(m, pre + "x.wk"), Mq, dd, dd, m.F4, 0.f));
-    CK(x.bwd_x(m.B5x, PBF(m, pre + "x.wv"), Mq, dd, dd, m.F4, 1.f));
+    CK(x.bwd_x(m.dkv, PBF(m, pre + "x.wk"), Mq, 2 * dd, dd, m.F4, 0.f));
     // virtual tokens: interpolation of z at the deformed points (gradients into z, p, qpos)
     CK(x.guard(m.B6));
     CK(mk::cast_bf16(m.F4, Mq * dd, m.B6, x.st));

@@ -731,6 +731,23 @@ int cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
     return AFFMAE_OK;
 }
 
+// dense fp32 [rows, cols] -> bf16 rows of stride ldy (a column slice of a wider matrix)
+__global__ void cast_bf16_2d_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ y,
+                                    int64_t ldy) {
+    const int64_t half = cols / 2, n = rows * half;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = t / half, c = 2 * (t - r * half);
+        st2(y, r * ldy + c, ld2(x, r * cols + c));
+    }
+}
+int cast_bf16_2d(const float* x, int64_t rows, int64_t cols, __nv_bfloat16* y, int64_t ldy, cudaStream_t st) {
+    if (rows <= 0) return AFFMAE_OK;
+    if (cols % 2 || ldy % 2) return fail(AFFMAE_EUNSUPPORTED, "cast_bf16_2d: even widths required");
+    cast_bf16_2d_kernel<<<row_blocks(rows * cols / 2, 256, 16 * kNumSMs), 256, 0, st>>>(x, rows, cols, y, ldy);
+    AFFMAE_LAUNCH_CHECK("cast_bf16_2d_kernel");
+    return AFFMAE_OK;
+}
+
 // column sums of an fp32 [rows, cols] matrix into out (+=): per-block partials + fixed-order sum
 __global__ void colsum_f32_partial_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t rows_per,
                                           float* __restrict__ part) {

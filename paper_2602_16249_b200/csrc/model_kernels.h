@@ -61,6 +61,7 @@ int gather_coords(const float* coords, const int32_t* ret, int64_t batch, int64_
 int add_f32_bf16(const float* a, int a_row, const bf16* b, int64_t rows, int64_t cols, float* out, bf16* out_bf,
                  cudaStream_t st);
 int cast_bf16(const float* x, int64_t n, bf16* y, cudaStream_t st);
+int cast_bf16_2d(const float* x, int64_t rows, int64_t cols, bf16* y, int64_t ldy, cudaStream_t st);
 int gelu_fwd(const bf16* pre, int64_t n, bf16* y, cudaStream_t st);
 int colsum_f32(const float* x, int64_t rows, int64_t cols, float* out, float* part, cudaStream_t st);
 size_t colsum_part_floats(int64_t cols);
