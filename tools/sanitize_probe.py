@@ -82,6 +82,22 @@ def main():
         p = dev([1.0], torch.float32)
         out = ops.interp_fwd(qs, keys, f, idx, valid, p)
         ops.interp_bwd(qs, keys, f, idx, valid, p, torch.randn_like(out))
+        # decoder attention at the AFFMAE-B row width (8 heads x 32): the register row forward
+        # (8-wide knn rows), the shared-memory-staged row kernels (one-to-one rows), the thread
+        # backward with the reverse-CSR gather
+        heads, hd, n = 8, 32, 300
+        c = dev(rng.uniform(0, 200, (2, n, 2)), torch.float32)
+        r = lambda *sh: dev(0.5 * rng.standard_normal(sh), torch.bfloat16)
+        q, k, v, bk, bv = r(2, n, heads * hd), r(2, n, heads * hd), r(2, n, heads * hd), r(heads, hd), r(heads, hd)
+        bias = ops.BiasNet.from_numpy(inputs.bias_params(heads, 8, rng))
+        si, sv = ops.knn(c, c, 8)
+        oi = torch.arange(n, dtype=torch.int32, device="cuda").repeat(2, 1).reshape(2, n, 1).contiguous()
+        ov = torch.ones(2, n, 1, dtype=torch.uint8, device="cuda")
+        for ii, vv in ((si, sv), (oi, ov)):
+            o, _ = ops.gattn_fwd(q, k, v, bk, bv, c, ii, vv, bias, heads, hd)
+            ops.gattn_bwd(q, k, v, bk, bv, c, ii, vv, bias, heads, hd, torch.randn_like(o), gather=True,
+                          workspace=torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
+            ops.gattn_bwd(q, k, v, bk, bv, c, ii, vv, bias, heads, hd, torch.randn_like(o))
         torch.cuda.synchronize()
         print("decoder ok", flush=True)
     if "model" in which:
