@@ -44,7 +44,8 @@ uint64_t hilbert_index_host(uint32_t n, uint32_t x, uint32_t y) { return hilbert
 
 // ---------------------------------------------------------- sfc_order
 __global__ void axis_keys_kernel(const float* __restrict__ coords, int64_t batch, int64_t n,
-                                 uint64_t* __restrict__ keys) {
+                                 uint64_t* __restrict__ keys, const int* __restrict__ run_flag) {
+    if (run_flag && *run_flag == 0) return;
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= batch * n * 2) return;
     int64_t tok = i >> 1;
@@ -67,6 +68,110 @@ __global__ void gap_kernel(const uint64_t* __restrict__ sorted, int64_t segs, in
     if (d > 0.0) atomicMin(gap_bits + i / n, (unsigned long long)__double_as_longlong(d));
 }
 
+// min_gap without the axis sort (images of <= 16384 tokens): per (image, axis), one block
+// takes min / max, drops every value into one of 4096 equal-width buckets (ordered-bit atomic
+// min / max in shared memory; the bucket map is monotone), and reads the gaps between
+// consecutive non-empty buckets -- each such pair of bucket max / next bucket min IS a pair
+// of consecutive distinct sorted values, so every candidate is an exact min_gap candidate.
+// Gaps between distinct values inside one bucket are invisible to it: such a bucket raises
+// `hard`, and the (gated) segmented sort then runs and min-merges the exact gaps.  Lattice
+// coordinates (patch centres) never share a bucket, so the sort is skipped.
+constexpr int kAxisBuckets = 4096;
+__global__ void __launch_bounds__(1024) axis_stats_kernel(const float* __restrict__ coords, int64_t n,
+                                                          float2* __restrict__ minmax,
+                                                          unsigned long long* __restrict__ gap_bits,
+                                                          int* __restrict__ hard) {
+    __shared__ uint32_t bmin[kAxisBuckets], bmax[kAxisBuckets];
+    __shared__ float rlo[32], rhi[32];
+    __shared__ uint32_t rlast[32];
+    __shared__ double rgap[32];
+    __shared__ int rhard;
+    const int seg = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const float* c = coords + int64_t(seg >> 1) * n * 2 + (seg & 1);
+    // each thread holds a contiguous chunk of <= 16 tokens in registers (one global read;
+    // contiguous chunks put the lanes of a warp in different raster rows, so the bucket atomics
+    // below do not pile onto one address -- a raster row shares its y)
+    constexpr int kChunk = kSegSortMax / 1024;
+    const int chunk = int((n + blockDim.x - 1) / blockDim.x);
+    const int64_t j0 = int64_t(t) * chunk;
+    float vals[kChunk];
+    float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) {
+        vals[i] = 0.f;
+        if (i < chunk && j0 + i < n) {
+            vals[i] = c[2 * (j0 + i)];
+            lo = fminf(lo, vals[i]);
+            hi = fmaxf(hi, vals[i]);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+        rlo[warp] = lo;
+        rhi[warp] = hi;
+    }
+    for (int b = t; b < kAxisBuckets; b += blockDim.x) {
+        bmin[b] = 0xffffffffu;
+        bmax[b] = 0u;
+    }
+    if (t == 0) rhard = 0;
+    __syncthreads();
+    lo = rlo[0];
+    hi = rhi[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+        lo = fminf(lo, rlo[w]);
+        hi = fmaxf(hi, rhi[w]);
+    }
+    const float span = hi - lo, inv = span > 0.f ? float(kAxisBuckets) / span : 0.f;
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) {
+        if (i < chunk && j0 + i < n) {
+            const int b = min(kAxisBuckets - 1, int((vals[i] - lo) * inv));
+            const uint32_t u = float_order(vals[i]);
+            atomicMin(&bmin[b], u);
+            atomicMax(&bmax[b], u);
+        }
+    }
+    __syncthreads();
+    // thread t: buckets [t*per, (t+1)*per): first / last value, gaps between its non-empty ones
+    const int per = kAxisBuckets / int(blockDim.x);
+    uint32_t first = 0u, last = 0u;
+    double g = INFINITY;
+    bool h = false;
+    for (int b = t * per; b < (t + 1) * per; ++b) {
+        if (bmax[b] == 0u) continue;  // empty (float_order of a real value is never 0)
+        h |= bmin[b] != bmax[b];
+        if (last) g = fmin(g, __dsub_rn(double(float_unorder(bmin[b])), double(float_unorder(last))));
+        if (!first) first = bmin[b];
+        last = bmax[b];
+    }
+    // exclusive max-scan of `last` over the threads: the previous non-empty value
+    uint32_t inc = last;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = max(inc, y);
+    }
+    if (lane == 31) rlast[warp] = inc;
+    __syncthreads();
+    uint32_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) prev = 0u;
+    for (int w = 0; w < warp; ++w) prev = max(prev, rlast[w]);
+    if (first && prev) g = fmin(g, __dsub_rn(double(float_unorder(first)), double(float_unorder(prev))));
+    for (int o = 16; o > 0; o >>= 1) g = fmin(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if (__any_sync(0xffffffffu, h) && lane == 0) rhard = 1;
+    if (lane == 0) rgap[warp] = g;
+    __syncthreads();
+    if (t == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) g = fmin(g, rgap[w]);
+        if (g > 0.0 && g < INFINITY) atomicMin(gap_bits + seg, (unsigned long long)__double_as_longlong(g));
+        minmax[seg] = make_float2(lo, hi);
+        if (rhard) atomicOr(hard, 1);
+    }
+}
+
 struct SfcParams {
     double xmin, ymin, scale;
     uint32_t side;  // 0 -> identity order (n == 1 or all points coincide)
@@ -84,13 +189,24 @@ __device__ int ceil_log2_cr(double x) {
 
 // sfc_order quantisation parameters of image b (geometry.cpp:87-101) from its
 // sorted axes and min gaps
-__device__ SfcParams sfc_params(const uint64_t* __restrict__ sorted, int64_t b, int64_t n,
-                                const unsigned long long* __restrict__ gap_bits) {
+__device__ SfcParams sfc_params(const uint64_t* __restrict__ sorted, const float2* __restrict__ minmax, int64_t b,
+                                int64_t n, const unsigned long long* __restrict__ gap_bits) {
     SfcParams p{};
-    const uint64_t* xs = sorted + (b * 2) * n;
-    const uint64_t* ys = sorted + (b * 2 + 1) * n;
-    double xmin = float_unorder(uint32_t(xs[0])), xmax = float_unorder(uint32_t(xs[n - 1]));
-    double ymin = float_unorder(uint32_t(ys[0])), ymax = float_unorder(uint32_t(ys[n - 1]));
+    double xmin, xmax, ymin, ymax;
+    if (minmax) {  // axis statistics pass (axis_stats_kernel)
+        const float2 mx = minmax[b * 2], my = minmax[b * 2 + 1];
+        xmin = mx.x;
+        xmax = mx.y;
+        ymin = my.x;
+        ymax = my.y;
+    } else {  // ends of the sorted axes
+        const uint64_t* xs = sorted + (b * 2) * n;
+        const uint64_t* ys = sorted + (b * 2 + 1) * n;
+        xmin = float_unorder(uint32_t(xs[0]));
+        xmax = float_unorder(uint32_t(xs[n - 1]));
+        ymin = float_unorder(uint32_t(ys[0]));
+        ymax = float_unorder(uint32_t(ys[n - 1]));
+    }
     double ex = __dsub_rn(xmax, xmin), ey = __dsub_rn(ymax, ymin);
     double extent = ex < ey ? ey : ex;
     p.xmin = xmin;
@@ -116,13 +232,13 @@ __device__ SfcParams sfc_params(const uint64_t* __restrict__ sorted, int64_t b, 
 // Hilbert keys; every thread derives its image's parameters (a few broadcast
 // loads and binary64 ops) instead of a separate one-thread-per-image kernel.
 __global__ void hilbert_keys_kernel(const float* __restrict__ coords, int64_t batch, int64_t n,
-                                    const uint64_t* __restrict__ sorted_axes,
+                                    const uint64_t* __restrict__ sorted_axes, const float2* __restrict__ minmax,
                                     const unsigned long long* __restrict__ gap_bits, uint64_t* __restrict__ keys,
                                     uint32_t* __restrict__ vals) {
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= batch * n) return;
     int64_t b = i / n;
-    const SfcParams p = sfc_params(sorted_axes, b, n, gap_bits);
+    const SfcParams p = sfc_params(sorted_axes, minmax, b, n, gap_bits);
     uint64_t key = 0;
     if (p.side) {
         double x = coords[2 * i], y = coords[2 * i + 1];
@@ -913,6 +1029,8 @@ struct IndexWs {
     unsigned long long* gaps;
     double2* cent;
     int32_t* cursor;
+    float2* minmax;  // per (image, axis) {min, max} of the axis statistics pass
+    int* hard;       // 1: some image needs the axis sort for its min_gap
     size_t bytes;
 };
 
@@ -934,6 +1052,8 @@ static IndexWs carve(int64_t batch, int64_t n, int64_t c, void* base) {
     w.gaps = reinterpret_cast<unsigned long long*>(take(size_t(batch) * 2 * 8));
     w.cent = reinterpret_cast<double2*>(take(size_t(batch) * c * sizeof(double2)));
     w.cursor = reinterpret_cast<int32_t*>(take(size_t(batch) * (c + 1) * 4));
+    w.minmax = reinterpret_cast<float2*>(take(size_t(batch) * 2 * sizeof(float2)));
+    w.hard = reinterpret_cast<int*>(take(16));
     w.bytes = off;
     return w;
 }
@@ -944,19 +1064,30 @@ static unsigned blocks(int64_t n, int t = 256) { return unsigned((n + t - 1) / t
 static int sfc_core(const float* coords, int64_t batch, int64_t n, IndexWs& w, uint32_t** sorted_vals,
                     cudaStream_t st) {
     const int64_t e = batch * n * 2;
-    axis_keys_kernel<<<blocks(e), 256, 0, st>>>(coords, batch, n, w.keys[0]);
+    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.gaps, 0xFF, size_t(batch) * 2 * 8, st));
+    // images of <= kSegSortMax tokens: min / max and min_gap from the bucket pass, the axis
+    // sort only when a bucket holds two distinct values (device-side gate)
+    const bool stats = n <= kSegSortMax;
+    const int* gate = nullptr;
+    if (stats) {
+        AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.hard, 0, sizeof(int), st));
+        axis_stats_kernel<<<unsigned(batch * 2), 1024, 0, st>>>(coords, n, w.minmax, w.gaps, w.hard);
+        AFFMAE_LAUNCH_CHECK("axis_stats_kernel");
+        gate = w.hard;
+    }
+    axis_keys_kernel<<<blocks(e), 256, 0, st>>>(coords, batch, n, w.keys[0], gate);
     AFFMAE_LAUNCH_CHECK("axis_keys_kernel");
     uint64_t* k = w.keys[0];
     uint32_t* v = nullptr;
-    AFFMAE_CUDA_CHECK(cudaMemsetAsync(w.gaps, 0xFF, size_t(batch) * 2 * 8, st));
     bool gaps_done = false;
     int rc = segmented_sort(k, v, w.keys[1], nullptr, batch * 2, n, 32 + bits_for(batch * 2), w.hist, st,
-                            w.gaps, &gaps_done);
+                            w.gaps, &gaps_done, gate);
     if (rc) return rc;
     if (!gaps_done) gap_kernel<<<blocks(e), 256, 0, st>>>(k, batch * 2, n, w.gaps);
     // the sorted axes live in w.keys[0] or w.keys[1]; the Hilbert keys go to the other buffer
     uint64_t* hk = k == w.keys[0] ? w.keys[1] : w.keys[0];
-    hilbert_keys_kernel<<<blocks(batch * n), 256, 0, st>>>(coords, batch, n, k, w.gaps, hk, w.vals[0]);
+    hilbert_keys_kernel<<<blocks(batch * n), 256, 0, st>>>(coords, batch, n, k, stats ? w.minmax : nullptr, w.gaps,
+                                                           hk, w.vals[0]);
     AFFMAE_LAUNCH_CHECK("hilbert_keys_kernel");
     k = hk;
     v = w.vals[0];

@@ -223,7 +223,11 @@ template <bool WRITE_VALS, int CL>
 __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_cl_kernel(const uint64_t* __restrict__ kin,
                                                                      int64_t seglen, uint64_t* __restrict__ kout,
                                                                      uint32_t* __restrict__ vout,
-                                                                     unsigned long long* __restrict__ gap_out) {
+                                                                     unsigned long long* __restrict__ gap_out,
+                                                                     const int* __restrict__ run_flag) {
+    // a device-side gate (graph-capturable): every CTA of the cluster reads the same flag and
+    // leaves before the first cluster barrier
+    if (run_flag && *run_flag == 0) return;
     extern __shared__ __align__(16) uint8_t sraw[];
     __shared__ SegClusterSmem<CL> cs;
     const int rank = cluster_rank();
@@ -401,16 +405,13 @@ __global__ void __launch_bounds__(kSegWarps * 32) seg_sort_cl_kernel(const uint6
 
 template <bool WRITE_VALS, int CL>
 inline int launch_seg_sort_cl(const uint64_t* kin, int64_t nseg, int64_t seglen, uint64_t* kout, uint32_t* vout,
-                              unsigned long long* gap_out, cudaStream_t st) {
+                              unsigned long long* gap_out, cudaStream_t st, const int* run_flag) {
     auto kern = seg_sort_cl_kernel<WRITE_VALS, CL>;
     const size_t smem = seg_sort_cl_smem(seglen, CL);
-    static bool attr = false;
-    if (!attr) {
-        AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(seg_sort_cl_smem(kSegSortMax, 1))));
-        AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attr = true;
-    }
+    // per call (cheap, and right for whichever device is current)
+    AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(seg_sort_cl_smem(kSegSortMax, 1))));
+    AFFMAE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(nseg * CL));
     cfg.blockDim = dim3(kSegWarps * 32);
@@ -423,7 +424,7 @@ inline int launch_seg_sort_cl(const uint64_t* kin, int64_t nseg, int64_t seglen,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    AFFMAE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, kin, seglen, kout, vout, gap_out));
+    AFFMAE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, kin, seglen, kout, vout, gap_out, run_flag));
     return AFFMAE_OK;
 }
 
@@ -436,12 +437,12 @@ inline int seg_cluster_size(int64_t nseg, int64_t seglen) {
 
 template <bool WRITE_VALS>
 inline int launch_seg_sort(const uint64_t* kin, int64_t nseg, int64_t seglen, uint64_t* kout, uint32_t* vout,
-                           unsigned long long* gap_out, cudaStream_t st) {
+                           unsigned long long* gap_out, cudaStream_t st, const int* run_flag) {
     switch (seg_cluster_size(nseg, seglen)) {
-        case 8: return launch_seg_sort_cl<WRITE_VALS, 8>(kin, nseg, seglen, kout, vout, gap_out, st);
-        case 4: return launch_seg_sort_cl<WRITE_VALS, 4>(kin, nseg, seglen, kout, vout, gap_out, st);
-        case 2: return launch_seg_sort_cl<WRITE_VALS, 2>(kin, nseg, seglen, kout, vout, gap_out, st);
-        default: return launch_seg_sort_cl<WRITE_VALS, 1>(kin, nseg, seglen, kout, vout, gap_out, st);
+        case 8: return launch_seg_sort_cl<WRITE_VALS, 8>(kin, nseg, seglen, kout, vout, gap_out, st, run_flag);
+        case 4: return launch_seg_sort_cl<WRITE_VALS, 4>(kin, nseg, seglen, kout, vout, gap_out, st, run_flag);
+        case 2: return launch_seg_sort_cl<WRITE_VALS, 2>(kin, nseg, seglen, kout, vout, gap_out, st, run_flag);
+        default: return launch_seg_sort_cl<WRITE_VALS, 1>(kin, nseg, seglen, kout, vout, gap_out, st, run_flag);
     }
 }
 
@@ -451,15 +452,17 @@ inline int launch_seg_sort(const uint64_t* kin, int64_t nseg, int64_t seglen, ui
 // keys/vals point at the sorted data (vals only if non-null).  With `gap_out`
 // the shared-memory path also writes the per-segment min_gap and sets
 // *gaps_done; the global fallback leaves that to the caller.
+// `run_flag` (shared-memory path only): a device int; the sort is skipped when it reads 0.
 inline int segmented_sort(uint64_t*& keys, uint32_t*& vals, uint64_t* keys_alt, uint32_t* vals_alt,
                           int64_t nseg, int64_t seglen, int end_bit, uint32_t* hist, cudaStream_t st,
-                          unsigned long long* gap_out = nullptr, bool* gaps_done = nullptr) {
+                          unsigned long long* gap_out = nullptr, bool* gaps_done = nullptr,
+                          const int* run_flag = nullptr) {
     if (gaps_done) *gaps_done = false;
     if (nseg <= 0 || seglen <= 0) return AFFMAE_OK;
     if (seglen > kSegSortMax || seglen > 65536)
         return radix_sort(keys, vals, keys_alt, vals_alt, nseg * seglen, end_bit, hist, st);
-    const int rc = vals ? launch_seg_sort<true>(keys, nseg, seglen, keys_alt, vals_alt, gap_out, st)
-                        : launch_seg_sort<false>(keys, nseg, seglen, keys_alt, nullptr, gap_out, st);
+    const int rc = vals ? launch_seg_sort<true>(keys, nseg, seglen, keys_alt, vals_alt, gap_out, st, run_flag)
+                        : launch_seg_sort<false>(keys, nseg, seglen, keys_alt, nullptr, gap_out, st, run_flag);
     if (gaps_done) *gaps_done = gap_out != nullptr;
     if (rc) return rc;
     AFFMAE_LAUNCH_CHECK("seg_sort_cl_kernel");
