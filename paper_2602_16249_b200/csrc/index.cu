@@ -398,9 +398,12 @@ constexpr int kNbrWarps = 8, kNbrPerWarp = 4;
 template <int G>
 __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* __restrict__ cent, ClusterShape cs,
                                                                  int32_t* __restrict__ nbr_cl) {
-    // smem: binary64 centroids, then their fp32 copies
+    // smem: binary64 centroids, their fp32 copies, the fp32 bounding box of every run of 32
+    // clusters in curve order
     extern __shared__ double2 sc[];
     float2* sf = reinterpret_cast<float2*>(sc + cs.c);
+    const int nchunk = (cs.c + 31) / 32;
+    float4* sbox = reinterpret_cast<float4*>(sf + ((cs.c + 1) & ~1));
     __shared__ unsigned int smax;
     const int b = blockIdx.y;
     const double2* cb = cent + int64_t(b) * cs.c;
@@ -414,6 +417,22 @@ __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* _
         lmax = fmaxf(lmax, fmaxf(fabsf(float(c.x)), fabsf(float(c.y))));
     }
     atomicMax(&smax, __float_as_uint(lmax));  // non-negative floats order like their bits
+    __syncthreads();
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int q = warp; q < nchunk; q += kNbrWarps) {
+            const int j = q * 32 + lane;
+            const float2 f = j < cs.c ? sf[j] : sf[q * 32];
+            float x0 = f.x, x1 = f.x, y0 = f.y, y1 = f.y;
+            for (int o = 16; o > 0; o >>= 1) {
+                x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+                x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+                y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+                y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+            }
+            if (lane == 0) sbox[q] = make_float4(x0, x1, y0, y1);
+        }
+    }
     __syncthreads();
     // |d2_fp32 - d2_fp64| <= ~5e-7 * maxc^2 (rounding of the coordinates and of d2): margin 4x that
     const float maxc = __uint_as_float(smax) + 1.f;
@@ -468,14 +487,28 @@ __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* _
             d[r] = INFINITY;
             jj[r] = INT32_MAX;
         }
-        for (int j = lane; j < cs.c; j += 32) {
-            const float2 fj = sf[j];
-            const float fx = fj.x - fk.x, fy = fj.y - fk.y;
-            if (fmaf(fx, fx, fy * fy) > thr) continue;
-            const double2 cj = sc[j];
-            const double dx = __dsub_rn(cj.x, ck.x), dy = __dsub_rn(cj.y, ck.y);
-            const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-            if (pair_lt(d2, j, d[G - 1], jj[G - 1])) topk_push<G>(d, jj, d2, j);
+        // only the 32-cluster runs whose box comes within the threshold (a lower bound of the
+        // fp32 distance to every member, with a relative margin) are scanned
+        const float bthr = thr * (1.f + 1e-5f);
+        for (int q0 = 0; q0 < nchunk; q0 += 32) {
+            bool near = false;
+            if (q0 + lane < nchunk) {
+                const float4 bx = sbox[q0 + lane];
+                const float ex = fmaxf(0.f, fmaxf(bx.x - fk.x, fk.x - bx.y));
+                const float ey = fmaxf(0.f, fmaxf(bx.z - fk.y, fk.y - bx.w));
+                near = ex * ex + ey * ey <= bthr;
+            }
+            for (unsigned m = __ballot_sync(0xffffffffu, near); m; m &= m - 1) {
+                const int j = (q0 + __ffs(m) - 1) * 32 + lane;
+                if (j >= cs.c) continue;
+                const float2 fj = sf[j];
+                const float fx = fj.x - fk.x, fy = fj.y - fk.y;
+                if (fmaf(fx, fx, fy * fy) > thr) continue;
+                const double2 cj = sc[j];
+                const double dx = __dsub_rn(cj.x, ck.x), dy = __dsub_rn(cj.y, ck.y);
+                const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+                if (pair_lt(d2, j, d[G - 1], jj[G - 1])) topk_push<G>(d, jj, d2, j);
+            }
         }
         double od[G];
         int oj[G];
@@ -492,7 +525,8 @@ __global__ void __launch_bounds__(kNbrWarps * 32) nbr_v2_kernel(const double2* _
 }
 
 static int launch_nbr(const double2* cent, int64_t batch, const ClusterShape& cs, int32_t* nbr, cudaStream_t st) {
-    const size_t smem = size_t(cs.c) * (sizeof(double2) + sizeof(float2));
+    const size_t smem = size_t(cs.c) * sizeof(double2) + size_t((cs.c + 1) & ~1) * sizeof(float2) +
+                        size_t((cs.c + 31) / 32) * sizeof(float4);
     if (smem > 200 * 1024) return -1;  // very large images: the generic kernel
     const dim3 grid(unsigned((cs.c + kNbrWarps * kNbrPerWarp - 1) / (kNbrWarps * kNbrPerWarp)), unsigned(batch));
     switch (cs.g) {
