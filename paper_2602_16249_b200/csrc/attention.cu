@@ -146,6 +146,9 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     const int32_t* nb = nbr_cl + item * cs.g;
     int32_t* out = qrec + item * R::WORDS;
     const int qlen = cs.len(c);
+    // snapshot of the grid-wide radius max, read up front so its latency overlaps the gathers
+    // (only used to skip atomics that cannot raise it; a stale value just costs an atomic)
+    const int rmax_seen = lane == 0 ? *reinterpret_cast<volatile int*>(rmax) : 0;
     // equal-size clusters (N divisible by C, the lattice case): slot s is member s % base
     // of neighbour s / base, no per-slot walk over the groups
     const bool uniform = cs.rem == 0;
@@ -194,7 +197,7 @@ __global__ void attn_qrec_kernel(const float* __restrict__ coords, const int32_t
     const int cls = agg.cls(&radius);
     {   // one address for the whole grid: skip the atomic when it cannot raise the max
         const int rv = cls == 0 ? kRg : radius;
-        if (lane == 0 && rv > *reinterpret_cast<volatile int*>(rmax)) atomicMax(rmax, rv);
+        if (lane == 0 && rv > rmax_seen) atomicMax(rmax, rv);
     }
     __syncwarp();
     if (cls == 1) {
