@@ -541,7 +541,7 @@ int offset_fwd(const float* fq, int64_t rows, int64_t C, const float* w, const f
     AFFMAE_LAUNCH_CHECK("offset_fwd_kernel");
     return AFFMAE_OK;
 }
-unsigned offset_bwd_blocks(int64_t rows) { return row_blocks(rows, 4 * kRowWarps, kNumSMs); }
+unsigned offset_bwd_blocks(int64_t rows) { return row_blocks(rows, 4 * kRowWarps, 4 * kNumSMs); }
 int offset_bwd(const float* fq, int64_t rows, int64_t C, const float* w, double limit, const float* pre,
                const float* dqpos, float* dfq, float* dw, float* db, float* part, cudaStream_t st) {
     if (rows <= 0) return AFFMAE_OK;
