@@ -1176,6 +1176,9 @@ static int row_fwd_launch2(const GAttnP& p, __nv_bfloat16* o, float* lse, cudaSt
 template <int VPL>
 static int row_fwd_launch(const GAttnP& p, int64_t width, __nv_bfloat16* o, float* lse, cudaStream_t st) {
     if (width <= 1) return row_fwd_launch2<VPL, 1>(p, o, lse, st);
+    if constexpr (VPL >= 16) {  // not instantiated: 512-wide 8-slot rows take the thread kernel
+        return fail(AFFMAE_EUNSUPPORTED, "gattn: internal routing");
+    } else {
     auto k = gattn_fwd_reg_kernel<VPL, 8>;
     const size_t sm = size_t(p.heads) * p.hidden * sizeof(float4);
     unsigned nb = 0;
@@ -1183,6 +1186,7 @@ static int row_fwd_launch(const GAttnP& p, int64_t width, __nv_bfloat16* o, floa
     k<<<nb, 256, sm, st>>>(p, o, lse);
     AFFMAE_LAUNCH_CHECK("gattn_fwd_reg_kernel");
     return AFFMAE_OK;
+    }
 }
 
 template <int VPL, int MW, int UPL>
