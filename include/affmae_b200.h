@@ -400,6 +400,27 @@ int affmae_merge_pool_fwd(const affmae_bf16* feats, const float* scores, const f
                           int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
                           affmae_bf16* out, void* stream);
 
+/* importance_scores (src/merging.cpp:31-48): scores[i] = sigmoid(GELU(f_i W1 + b1) w2 + b2)
+ * for feats [rows, dim] fp32, W1 [dim, hidden] (the reference's MergeParams layout), b1
+ * [hidden], w2 [hidden], b2 [1], hidden <= 32; binary64 in the reference's operation order,
+ * rounded once to fp32 (equal to the reference's b32 output up to the device erf / exp's
+ * last binary64 bit). */
+int affmae_importance_scores(const float* feats, int64_t rows, int64_t dim, const float* w1, const float* b1,
+                             const float* w2, const float* b2, int hidden, float* scores, void* stream);
+
+/* merge_tokens (src/merging.cpp:242-273), batched: per image, the merge plan of `retained`
+ * (bit-exact), the pool rows [f_r ; agg], the [2D -> D] projection on the tensor cores and
+ * layer_norm_rows (eps 1e-5).  feats [B, N, D] bf16, coords [B, N, 2], scores [B, N],
+ * retained [B, R] ascending, proj_wt [D, 2D] bf16 = the reference's proj_w [2D, D]
+ * transposed, ln_gamma / ln_beta [D] fp32, p_merge a device scalar.  Outputs: merged
+ * feats [B, R, D] bf16, the retained coords [B, R, 2].  D a multiple of 64 up to 1024. */
+size_t affmae_merge_tokens_workspace(int64_t batch, int64_t tokens, int64_t n_retained, int64_t dim, int k_m);
+int affmae_merge_tokens(const float* coords, const affmae_bf16* feats, const float* scores, const int32_t* retained,
+                        int64_t batch, int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
+                        const float* p_merge, const affmae_bf16* proj_wt, const float* ln_gamma,
+                        const float* ln_beta, affmae_bf16* out_feats, float* out_coords, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
 size_t affmae_merge_pool_bwd_workspace(int64_t batch, int64_t n_retained);
 /* MergePoolOp::backward (src/merging.cpp:169-219): dfeats [B, N, D] bf16 and
  * dscores [B, N] fp32 are overwritten (every token receives at most one

@@ -190,6 +190,32 @@ def merge_pool_fwd(plan, feats, scores, p, prec=64):
     return out
 
 
+def importance_scores(feats, w1, b1, w2, b2, prec=32):
+    """importance_scores (merging.cpp:31-48) of the compiled reference: feats [n, d],
+    w1 [d, h], b1 [h], w2 [h], b2 scalar -> [n]."""
+    feats = _f64(feats)
+    n, d = feats.shape
+    h = np.asarray(w1).shape[1]
+    out = np.empty(n)
+    _check(lib().ref_importance_scores(_p(feats), C.c_int64(n), C.c_int64(d), _p(_f64(w1)), _p(_f64(b1)),
+                                       _p(_f64(w2)), C.c_double(float(b2)), C.c_int(h), C.c_int(prec), _p(out)))
+    return out
+
+
+def merge_tokens(coords, feats, scores, retained, k_m, p, proj_w, gamma, beta, prec=32):
+    """merge_tokens (merging.cpp:242-273) of the compiled reference -> (coords [r, 2],
+    feats [r, d])."""
+    feats = _f64(feats)
+    n, d = feats.shape
+    r = len(retained)
+    of, oc = np.empty((r, d)), np.empty((r, 2))
+    _check(lib().ref_merge_tokens(_p(_f32(coords)), _p(feats), C.c_int64(n), C.c_int64(d),
+                                  _p(_f64(scores).reshape(-1)), _p(_i64(retained)), C.c_int64(r), C.c_int(k_m),
+                                  C.c_double(p), _p(_f64(proj_w)), _p(_f64(gamma)), _p(_f64(beta)), C.c_int(prec),
+                                  _p(of), _p(oc)))
+    return oc, of
+
+
 def merge_pool_bwd(plan, feats, scores, p, dout, prec=64):
     feats, scores, dout = _f64(feats), _f64(scores).reshape(-1), _f64(dout)
     n, dim = feats.shape

@@ -329,6 +329,41 @@ int ref_merge_pool_bwd(int64_t n, int64_t dim, int64_t r, int k_m, const int64_t
     });
 }
 
+// importance_scores (merging.cpp:31-48): feats [n, d], w1 [d, h], b1 [h], w2 [h], b2
+int ref_importance_scores(const double* feats, int64_t n, int64_t d, const double* w1, const double* b1,
+                          const double* w2, double b2, int h, int prec, double* out) {
+    return guarded([&] {
+        MergeParams mp;
+        mp.scorer_w1 = from(w1, {d, h}, Precision::b32);
+        mp.scorer_b1 = from(b1, {1, h}, Precision::b32);
+        mp.scorer_w2 = from(w2, {h, 1}, Precision::b32);
+        mp.scorer_b2 = Tensor::full({1, 1}, b2, Precision::b32);
+        Tensor f = from(feats, {n, d}, prec_of(prec));
+        to(importance_scores(f, mp), out);
+    });
+}
+
+// merge_tokens (merging.cpp:242-273): coords [n, 2], feats [n, d], scores [n], retained [r]
+// ascending, proj_w [2d, d], gamma / beta [d] -> merged feats [r, d], coords [r, 2]
+int ref_merge_tokens(const float* coords, const double* feats, int64_t n, int64_t d, const double* scores,
+                     const int64_t* retained, int64_t r, int k_m, double p, const double* proj_w,
+                     const double* gamma, const double* beta, int prec, double* out_feats, double* out_coords) {
+    return guarded([&] {
+        PointSet ps = points(coords, n);
+        ps.feats = from(feats, {n, d}, prec_of(prec));
+        Tensor s = from(scores, {n, 1}, prec_of(prec));
+        MergeParams mp;
+        mp.k_m = k_m;
+        mp.p_merge = Tensor::full({1, 1}, p, prec_of(prec));
+        mp.proj_w = from(proj_w, {2 * d, d}, prec_of(prec));
+        mp.ln_gamma = from(gamma, {1, d}, prec_of(prec));
+        mp.ln_beta = from(beta, {1, d}, prec_of(prec));
+        MergeResult res = merge_tokens(ps, s, std::span<const int64_t>(retained, size_t(r)), mp);
+        to(res.points.feats, out_feats);
+        to(res.points.coords, out_coords);
+    });
+}
+
 // make_interp_op (interpolation.hpp:60) forward / backward: queries [nq,2],
 // key coords [nk,2], feats [nk,dim], neighbour rows idx/valid [nq,k]
 int ref_interp_fwd(int64_t nq, int64_t nk, int64_t dim, int64_t k, const double* queries,

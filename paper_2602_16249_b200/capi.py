@@ -27,6 +27,7 @@ EXPORTS = (
     "affmae_attn_fwd_planned", "affmae_attn_bwd_planned_workspace", "affmae_attn_bwd_planned",
     "affmae_retained_count", "affmae_select_retained_workspace", "affmae_select_retained",
     "affmae_merge_plan_workspace", "affmae_merge_plan_build", "affmae_merge_pool_fwd",
+    "affmae_importance_scores", "affmae_merge_tokens_workspace", "affmae_merge_tokens",
     "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd", "affmae_interp_fwd", "affmae_interp_bwd",
     "affmae_adamw_lr", "affmae_adamw_step", "affmae_linear_workspace", "affmae_linear_fwd",
     "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_linear_fwd_gelu_aux", "affmae_gelu_bwd", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",

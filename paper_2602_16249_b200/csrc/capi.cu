@@ -414,6 +414,25 @@ int affmae_merge_plan_build(const float* coords, const int32_t* retained, int64_
     )
 }
 
+int affmae_importance_scores(const float* feats, int64_t rows, int64_t dim, const float* w1, const float* b1,
+                             const float* w2, const float* b2, int hidden, float* scores, void* stream) {
+    AFFMAE_GUARD(return importance_scores(feats, rows, dim, w1, b1, w2, b2, hidden, scores, stream);)
+}
+
+size_t affmae_merge_tokens_workspace(int64_t batch, int64_t tokens, int64_t n_retained, int64_t dim, int k_m) {
+    return merge_tokens_workspace(batch, tokens, n_retained, dim, k_m);
+}
+
+int affmae_merge_tokens(const float* coords, const affmae_bf16* feats, const float* scores, const int32_t* retained,
+                        int64_t batch, int64_t tokens, int64_t n_retained, int64_t dim, int k_m,
+                        const float* p_merge, const affmae_bf16* proj_wt, const float* ln_gamma,
+                        const float* ln_beta, affmae_bf16* out_feats, float* out_coords, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    AFFMAE_GUARD(return merge_tokens(coords, feats, scores, retained, batch, tokens, n_retained, dim, k_m, p_merge,
+                                     proj_wt, ln_gamma, ln_beta, out_feats, out_coords, workspace, workspace_bytes,
+                                     stream);)
+}
+
 int affmae_merge_pool_fwd(const affmae_bf16* feats, const float* scores, const float* p_merge,
                           const int32_t* retained, const affmae_merge_plan* plan, int64_t batch,
                           int64_t tokens, int64_t n_retained, int64_t dim, int k_m,

@@ -98,6 +98,13 @@ int adamw_step(const affmae_adamw_cfg*, int64_t, int64_t, const int64_t*, const 
 size_t select_retained_workspace(int64_t, int64_t);
 int select_retained(const float*, int64_t, int64_t, double, int32_t*, void*, size_t, void*);
 size_t merge_plan_workspace(int64_t, int64_t, int64_t);
+int importance_scores(const float* feats, int64_t rows, int64_t dim, const float* w1, const float* b1,
+                      const float* w2, const float* b2, int hidden, float* out, void* stream);
+size_t merge_tokens_workspace(int64_t batch, int64_t n, int64_t r, int64_t dim, int k_m);
+int merge_tokens(const float* coords, const void* feats, const float* scores, const int32_t* retained, int64_t batch,
+                 int64_t n, int64_t r, int64_t dim, int k_m, const float* p_merge, const void* proj_wt,
+                 const float* gamma, const float* beta, void* out_feats, float* out_coords, void* workspace,
+                 size_t ws_bytes, void* stream);
 int merge_plan_build(const float*, const int32_t*, int64_t, int64_t, int64_t, int, affmae_merge_plan*,
                      void*, size_t, void*);
 int merge_pool_fwd(const affmae_bf16*, const float*, const float*, const int32_t*,

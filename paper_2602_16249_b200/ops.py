@@ -830,6 +830,51 @@ def merge_pool_fwd(feats, scores, p_merge, plan: MergePlan, out=None, stream=Non
     return out
 
 
+def importance_scores(feats, w1, b1, w2, b2, stream=None):
+    """importance_scores (proj/src/merging.cpp:31-48): feats [..., D] fp32, w1 [D, H], b1 [H],
+    w2 [H], b2 [1] fp32 (MergeParams layout) -> scores [...] fp32 (binary64 inside)."""
+    _req(feats, torch.float32, "feats")
+    for t, n in ((w1, "w1"), (b1, "b1"), (w2, "w2"), (b2, "b2")):
+        _req(t, torch.float32, n)
+    D, H = w1.shape
+    if feats.shape[-1] != D:
+        raise ValueError("importance_scores: feature width does not match the scorer")
+    rows = feats.numel() // D
+    out = torch.empty(feats.shape[:-1], dtype=torch.float32, device=feats.device)
+    capi.check(capi.lib().affmae_importance_scores(
+        C.c_void_p(feats.data_ptr()), C.c_int64(rows), C.c_int64(D), C.c_void_p(w1.data_ptr()),
+        C.c_void_p(b1.data_ptr()), C.c_void_p(w2.data_ptr()), C.c_void_p(b2.data_ptr()), C.c_int(H),
+        C.c_void_p(out.data_ptr()), _stream(stream)), "importance_scores")
+    return out
+
+
+def merge_tokens(coords, feats, scores, retained, k_m, p_merge, proj_wt, ln_gamma, ln_beta, stream=None):
+    """merge_tokens (proj/src/merging.cpp:242-273), batched: coords [B, N, 2] fp32, feats
+    [B, N, D] bf16, scores [B, N] fp32, retained [B, R] int32 ascending, p_merge [1] fp32,
+    proj_wt [D, 2D] bf16 (the reference's proj_w transposed), ln_gamma / ln_beta [D] fp32 ->
+    (retained coords [B, R, 2] fp32, merged feats [B, R, D] bf16)."""
+    _req(coords, torch.float32, "coords")
+    _req(feats, BF16, "feats")
+    _req(scores, torch.float32, "scores")
+    _req(retained, torch.int32, "retained")
+    _req(proj_wt, BF16, "proj_wt")
+    B, N, D = feats.shape
+    R = retained.shape[1]
+    dev = feats.device
+    out_f = torch.empty((B, R, D), dtype=BF16, device=dev)
+    out_c = torch.empty((B, R, 2), dtype=torch.float32, device=dev)
+    L = capi.lib()
+    nbytes = L.affmae_merge_tokens_workspace(C.c_int64(B), C.c_int64(N), C.c_int64(R), C.c_int64(D), C.c_int(k_m))
+    ws = _workspace(nbytes, dev)
+    capi.check(L.affmae_merge_tokens(
+        C.c_void_p(coords.data_ptr()), C.c_void_p(feats.data_ptr()), C.c_void_p(scores.data_ptr()),
+        C.c_void_p(retained.data_ptr()), C.c_int64(B), C.c_int64(N), C.c_int64(R), C.c_int64(D), C.c_int(k_m),
+        C.c_void_p(p_merge.data_ptr()), C.c_void_p(proj_wt.data_ptr()), C.c_void_p(ln_gamma.data_ptr()),
+        C.c_void_p(ln_beta.data_ptr()), C.c_void_p(out_f.data_ptr()), C.c_void_p(out_c.data_ptr()),
+        C.c_void_p(ws.data_ptr()), C.c_size_t(ws.numel()), _stream(stream)), "merge_tokens")
+    return out_c, out_f
+
+
 def merge_pool_bwd(feats, scores, p_merge, plan: MergePlan, dout, dfeats=None, dscores=None,
                    dp=None, workspace=None, stream=None):
     """MergePoolOp::backward (proj/src/merging.cpp:169-219): dfeats [B, N, D] bf16 and
