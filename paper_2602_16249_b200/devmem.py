@@ -87,6 +87,16 @@ def d2h_async(dst_ptr: int, src_ptr: int, nbytes: int, stream):
         "d2h_async")
 
 
+def d2d_async(dst_ptr: int, src_ptr: int, nbytes: int, stream):
+    _ok(rt().cudaMemcpyAsync(C.c_void_p(dst_ptr), C.c_void_p(src_ptr), C.c_size_t(nbytes), 3, C.c_void_p(stream)),
+        "d2d_async")  # cudaMemcpyDeviceToDevice
+
+
+def stream_wait(stream, event: "Event"):
+    """`stream` waits for the work recorded in `event`."""
+    _ok(rt().cudaStreamWaitEvent(C.c_void_p(stream), event.e, 0), "cudaStreamWaitEvent")
+
+
 def d2h(src_ptr: int, shape, dtype, stream=None) -> np.ndarray:
     out = np.empty(shape, dtype)
     if stream is not None:
