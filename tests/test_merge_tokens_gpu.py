@@ -67,3 +67,36 @@ def test_merge_tokens_matches_reference(kind, n, d, k_m, p):
         np.testing.assert_array_equal(oc[b], wc.astype(np.float32))
         rel = np.linalg.norm(of[b] - wf) / np.linalg.norm(wf)
         assert rel <= 1e-2, (b, rel)
+
+
+def test_merge_tokens_all_retained_and_single_contributor():
+    """d_s = 1 (every token retained: pools hold only the empty aggregate) and k_m = 1."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    rng = np.random.default_rng(7)
+    n, d = 200, 64
+    coords = _lattice(n, 32, rng)[None]
+    feats = _bf16_round(rng.standard_normal((1, n, d)))
+    scores = rng.uniform(0.1, 0.9, (1, n)).astype(np.float32)
+    proj_w = _bf16_round(rng.standard_normal((2 * d, d)) / np.sqrt(2 * d))
+    gamma, beta = np.ones(d, np.float32), np.zeros(d, np.float32)
+    for retained, k_m in ((np.arange(n), 8), (np.sort(rng.choice(n, 80, replace=False)), 1)):
+        retained = retained.astype(np.int32)[None]
+        oc, of = ops.merge_tokens(_dev(coords, torch.float32), _dev(feats, torch.bfloat16),
+                                  _dev(scores, torch.float32), _dev(retained, torch.int32), k_m,
+                                  _dev([1.0], torch.float32), _dev(proj_w.T, torch.bfloat16),
+                                  _dev(gamma, torch.float32), _dev(beta, torch.float32))
+        wc, wf = ref.merge_tokens(coords[0], feats[0], scores[0], retained[0], k_m, 1.0, proj_w, gamma, beta)
+        np.testing.assert_array_equal(oc.cpu().numpy()[0], wc.astype(np.float32))
+        got = of.float().cpu().numpy()[0]
+        assert np.linalg.norm(got - wf) / np.linalg.norm(wf) <= 1e-2
+
+
+def test_importance_scores_rejects_mismatched_width():
+    import torch
+    from paper_2602_16249_b200 import ops
+    f = torch.zeros((4, 32), dtype=torch.float32, device="cuda")
+    w1 = torch.zeros((16, 8), dtype=torch.float32, device="cuda")
+    z = torch.zeros(8, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError, match="feature width"):
+        ops.importance_scores(f, w1, z, z, z[:1])
