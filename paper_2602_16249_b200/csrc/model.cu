@@ -1540,7 +1540,8 @@ int affmae_model_set_world(affmae_model* m, int world, int rank, const uint8_t* 
             nccl_comm_destroy(m->comm);
             m->comm = nullptr;
         }
-        if (nccl_id && world > 1)
+        // (a one-rank communicator is allowed: it runs the same captured exchange, a no-op sum)
+        if (nccl_id)
             if (int rc = nccl_comm_init(nccl_id, world, rank, &m->comm)) return rc;
         m->world = world;
         if (m->gexec) {  // the captured step bakes the loss seed and the exchange

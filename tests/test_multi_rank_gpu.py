@@ -77,3 +77,29 @@ def test_two_rank_step_equals_one_rank_step(tmp_path):
     assert worst <= 2.0 * lr + 1e-7, worst  # an element whose tiny gradient flips sign moves by <= 2 lr
     frac = np.mean(np.concatenate([(np.abs(p1[n] - p2[n]) <= 1e-6).ravel() for n in p1]))
     assert frac >= 0.999, frac
+
+
+def test_nccl_exchange_in_the_step_graph_single_rank():
+    """The NCCL path of the step (runtime-loaded libnccl, communicator init, ncclAllReduce of the
+    gradient arena captured in the step's CUDA graph) on a one-rank communicator -- the only
+    NCCL topology a one-GPU box offers: the sum over one rank is the identity, so the step
+    equals the step without a communicator (to the step's own run-to-run rounding: the
+    reverse-CSR fills are order-nondeterministic, see test_graph_replay_matches_eager)."""
+    from paper_2602_16249_b200.model import Model, nccl_unique_id
+    imgs, seeds = _inputs([0, 1])
+    out = []
+    for use_nccl in (False, True):
+        m = Model(_cfg(2))
+        if use_nccl:
+            m.set_world(1, 0, nccl_unique_id())
+        m.set_images(imgs)
+        m.make_masks(seeds)
+        m.train_step()
+        m.make_masks(seeds)
+        m.train_step()
+        out.append(m.params())
+        m.close()
+    worst = max(float(np.abs(out[0][n] - out[1][n]).max()) for n in out[0])
+    assert worst <= 4e-3, worst  # 2 steps, an element whose tiny gradient flips sign moves <= 2 lr
+    frac = np.mean(np.concatenate([(np.abs(out[0][n] - out[1][n]) <= 1e-6).ravel() for n in out[0]]))
+    assert frac >= 0.99, frac
