@@ -732,18 +732,28 @@ int cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
 }
 
 // dense fp32 [rows, cols] -> bf16 rows of stride ldy (a column slice of a wider matrix)
+// four columns per thread (16-byte loads, 8-byte stores); blockIdx.y walks the 4-column groups
+// of a row block, so no per-element 64-bit division
 __global__ void cast_bf16_2d_kernel(const float* __restrict__ x, int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ y,
                                     int64_t ldy) {
-    const int64_t half = cols / 2, n = rows * half;
-    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = t / half, c = 2 * (t - r * half);
-        st2(y, r * ldy + c, ld2(x, r * cols + c));
+    const int64_t q4 = cols / 4;
+    for (int64_t r = int64_t(blockIdx.x) * (blockDim.x / q4) + threadIdx.x / q4; r < rows;
+         r += int64_t(gridDim.x) * (blockDim.x / q4)) {
+        const int64_t c = 4 * (threadIdx.x % q4);
+        const float4 v = *reinterpret_cast<const float4*>(x + r * cols + c);
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 o;
+        o.x = *reinterpret_cast<const uint32_t*>(&lo);
+        o.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(y + r * ldy + c) = o;
     }
 }
 int cast_bf16_2d(const float* x, int64_t rows, int64_t cols, __nv_bfloat16* y, int64_t ldy, cudaStream_t st) {
     if (rows <= 0) return AFFMAE_OK;
-    if (cols % 2 || ldy % 2) return fail(AFFMAE_EUNSUPPORTED, "cast_bf16_2d: even widths required");
-    cast_bf16_2d_kernel<<<row_blocks(rows * cols / 2, 256, 16 * kNumSMs), 256, 0, st>>>(x, rows, cols, y, ldy);
+    if (cols % 4 || ldy % 4 || cols / 4 > 256) return fail(AFFMAE_EUNSUPPORTED, "cast_bf16_2d: width");
+    const int64_t per = 256 / (cols / 4);  // rows per 256-thread block
+    cast_bf16_2d_kernel<<<row_blocks(rows, int(per), 16 * kNumSMs), unsigned(per * (cols / 4)), 0, st>>>(
+        x, rows, cols, y, ldy);
     AFFMAE_LAUNCH_CHECK("cast_bf16_2d_kernel");
     return AFFMAE_OK;
 }
