@@ -287,20 +287,25 @@ template <int HD, int NROWS>
 __device__ __forceinline__ void sw_gather(__nv_bfloat16* dst, const __nv_bfloat16* src, uint32_t rowbytes,
                                           const int32_t* tok, int lane) {
     using S = Swz<HD>;
-    constexpr int CPR = S::CPR, RPI = 32 / CPR;
+    constexpr int CPR = S::CPR, RPI = 32 / CPR, NJ = (NROWS + RPI - 1) / RPI;
     const int sub = lane / CPR, ch = lane - sub * CPR;
     const char* base = reinterpret_cast<const char*>(src) + ch * 16;
     const uint32_t sdst = smem_u32(dst);
+    // all token ids first: the cp.async statements are compiler memory barriers, so a token
+    // load between two of them would wait out its full shared-memory latency every row
+    int t[NJ];
 #pragma unroll
-    for (int j = 0; j < (NROWS + RPI - 1) / RPI; ++j) {
+    for (int j = 0; j < NJ; ++j) {
         const int r = sub + j * RPI;
-        if (NROWS % RPI == 0 || r < NROWS) {
-            const int t = tok[r];
-            if (t >= 0)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + 2 * S::at(r, ch)),
-                             "l"(base + uint32_t(t) * rowbytes)
-                             : "memory");
-        }
+        t[j] = (NROWS % RPI == 0 || r < NROWS) ? tok[r] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int r = sub + j * RPI;
+        if (t[j] >= 0)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst + 2 * S::at(r, ch)),
+                         "l"(base + uint32_t(t[j]) * rowbytes)
+                         : "memory");
     }
 }
 // Static blank tile (swizzled): row 0 = blank vector of head h, rows 1..7 zero.
