@@ -308,6 +308,36 @@ __device__ __forceinline__ void sw_gather(__nv_bfloat16* dst, const __nv_bfloat1
                          : "memory");
     }
 }
+// Two tiles gathered by the same token list (Q and dO, or K and V): the ids are loaded once.
+template <int HD, int NROWS>
+__device__ __forceinline__ void sw_gather2(__nv_bfloat16* dst0, const __nv_bfloat16* src0, uint32_t rowbytes0,
+                                           __nv_bfloat16* dst1, const __nv_bfloat16* src1, uint32_t rowbytes1,
+                                           const int32_t* tok, int lane) {
+    using S = Swz<HD>;
+    constexpr int CPR = S::CPR, RPI = 32 / CPR, NJ = (NROWS + RPI - 1) / RPI;
+    const int sub = lane / CPR, ch = lane - sub * CPR;
+    const char* base0 = reinterpret_cast<const char*>(src0) + ch * 16;
+    const char* base1 = reinterpret_cast<const char*>(src1) + ch * 16;
+    const uint32_t d0 = smem_u32(dst0), d1 = smem_u32(dst1);
+    int t[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int r = sub + j * RPI;
+        t[j] = (NROWS % RPI == 0 || r < NROWS) ? tok[r] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int r = sub + j * RPI;
+        if (t[j] >= 0) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + 2 * S::at(r, ch)),
+                         "l"(base0 + uint32_t(t[j]) * rowbytes0)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d1 + 2 * S::at(r, ch)),
+                         "l"(base1 + uint32_t(t[j]) * rowbytes1)
+                         : "memory");
+        }
+    }
+}
 // Static blank tile (swizzled): row 0 = blank vector of head h, rows 1..7 zero.
 template <int HD>
 __device__ __forceinline__ void sw_init_blank_tile(__nv_bfloat16* t, const __nv_bfloat16* blank, int h) {
@@ -743,8 +773,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         if (item < n_items) copy_rec<C::QW>(dst, p.qrec + size_t(entry) * C::QW, lane);
     };
     auto issue_qo = [&](const int32_t* rec, int64_t img_tok) {
-        sw_gather<HD, 16>(sm.Q, qg + img_tok * ld, rowb, rec + R::QTOK, lane);
-        sw_gather<HD, 16>(sm.dO, og + img_tok * ldo, rowbo, rec + R::QTOK, lane);
+        sw_gather2<HD, 16>(sm.Q, qg + img_tok * ld, rowb, sm.dO, og + img_tok * ldo, rowbo, rec + R::QTOK, lane);
         if (lane < 16) {
             const int qt = rec[R::QTOK + lane];
             if (qt >= 0) cp_async4(sm.lse + lane, p.lse + (img_tok + qt) * p.heads + h);
@@ -763,8 +792,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
     if (i0 < n_items) {
         const int64_t it0 = sm.rec[0][R::HDR + kHImgTok];
         issue_qo(sm.rec[0], it0);
-        sw_gather<HD, KP>(sm.K, kg + it0 * ld, rowb, sm.rec[0] + R::KTOK, lane);
-        sw_gather<HD, KP>(sm.V, vg + it0 * ld, rowb, sm.rec[0] + R::KTOK, lane);
+        sw_gather2<HD, KP>(sm.K, kg + it0 * ld, rowb, sm.V, vg + it0 * ld, rowb, sm.rec[0] + R::KTOK, lane);
     }
     cp_async_commit();
 
@@ -1033,15 +1061,14 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 16) attn_bwd_kv_kernel(Attn
     auto issue_rows = [&](int buf, const int32_t* rec) {
         const int64_t img_tok = int64_t(item_tok(rec, p));
         const int64_t base = img_tok * ld + h * HD;
-        sw_gather<HD, 16>(sm.Q[buf], p.q + base, rowb, rec + PRec::QTOK, lane);
-        sw_gather<HD, 16>(sm.dO[buf], p.dout + img_tok * ldo + h * HD, rowbo, rec + PRec::QTOK, lane);
-        if (rec[PRec::HDR + kPFirst]) {
-            sw_gather<HD, 16>(sm.K, p.k + base, rowb, rec + KR + KRec::KTOK, lane);
-            sw_gather<HD, 16>(sm.V, p.v + base, rowb, rec + KR + KRec::KTOK, lane);
-        }
-        if (lane < 8)
-            cp_async16(sm.lsd[buf] + 2 * lane,
-                       p.lsd + (size_t(rec[PRec::HDR + kPQItem]) * p.heads + h) * 16 + 2 * lane);
+        // record fields read before the copies (each cp.async is a compiler memory barrier)
+        const bool first = rec[PRec::HDR + kPFirst] != 0;
+        const float2* lsd_src = p.lsd + (size_t(rec[PRec::HDR + kPQItem]) * p.heads + h) * 16 + 2 * lane;
+        if (lane < 8) cp_async16(sm.lsd[buf] + 2 * lane, lsd_src);
+        sw_gather2<HD, 16>(sm.Q[buf], p.q + base, rowb, sm.dO[buf], p.dout + img_tok * ldo + h * HD, rowbo,
+                           rec + PRec::QTOK, lane);
+        if (first)
+            sw_gather2<HD, 16>(sm.K, p.k + base, rowb, sm.V, p.v + base, rowb, rec + KR + KRec::KTOK, lane);
     };
 
     // prologue: records of rounds 0 and 1, rows of round 0
