@@ -619,17 +619,18 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
         const int i1 = item + stride;
         cp_async_wait<1>();  // Q, K (and record i+1) landed; V may be in flight
         __syncwarp();
-        copy_item_rec(item + 2 * stride, next_entry, it + 2);
-        next_entry = list_at(item + 3 * stride);
-        cp_async_commit();
+        // record fields and the Q fragments before the next record's copy (cp.async is a
+        // compiler memory barrier: loads after it would wait out their latency behind it)
         const int32_t* rec = rec_of(it);
         const int32_t* rec1 = rec_of(it + 1);
         const int nk = rec[R::HDR + kHNk], qlen = rec[R::HDR + kHQlen];
         const int64_t img_tok = rec[R::HDR + kHImgTok], io_cur = img_tok * ld;
         const int64_t io_nxt = int64_t(rec1[R::HDR + kHImgTok]) * ld;
-
         uint32_t qa[HD / 16][4];
         sw_load_a16<HD>(qa, sm.Q, lane);
+        copy_item_rec(item + 2 * stride, next_entry, it + 2);
+        next_entry = list_at(item + 3 * stride);
+        cp_async_commit();
         float s[NT][4];
         sw_mma_abt<HD, NT>(s, qa, sm.K, sm.Kb, lane);
         __syncwarp();  // Q, K consumed: reload them for item i+1
@@ -801,19 +802,19 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         const int r1 = rc == 2 ? 0 : rc + 1, r2 = r1 == 2 ? 0 : r1 + 1;
         cp_async_wait<0>();  // rows of this item and the record of the next one landed
         __syncwarp();
-        copy_item_rec(item + 2 * stride, next_entry, sm.rec[r2]);
-        next_entry = list_at(item + 3 * stride);
-        cp_async_commit();
+        // record fields and the Q / dO fragments before the next record's copy (see the forward)
         const int32_t* rec = sm.rec[rc];
         const int32_t* rec1 = sm.rec[r1];
         const bool more = item + stride < n_items;
         const int nk = rec[R::HDR + kHNk], qlen = rec[R::HDR + kHQlen];
         const int64_t img_tok = rec[R::HDR + kHImgTok];
         const int64_t nxt_tok = rec1[R::HDR + kHImgTok];
-
         uint32_t qa[HD / 16][4], oa[HD / 16][4];
         sw_load_a16<HD>(qa, sm.Q, lane);
         sw_load_a16<HD>(oa, sm.dO, lane);
+        copy_item_rec(item + 2 * stride, next_entry, sm.rec[r2]);
+        next_entry = list_at(item + 3 * stride);
+        cp_async_commit();
         float s[NT][4], dp[NT][4];
         sw_mma_abt<HD, NT>(s, qa, sm.K, sm.Kb, lane);
         sw_mma_abt<HD, NT>(dp, oa, sm.V, sm.Vb, lane);
