@@ -633,12 +633,8 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
         cp_async_commit();
         float s[NT][4];
         sw_mma_abt<HD, NT>(s, qa, sm.K, sm.Kb, lane);
-        __syncwarp();  // Q, K consumed: reload them for item i+1
-        if (i1 < n_items) {
-            sw_gather<HD, 16>(sm.Q, qg + io_nxt, rowb, rec1 + R::QTOK, lane);
-            sw_gather<HD, KP>(sm.K, kg + io_nxt, rowb, rec1 + R::KTOK, lane);
-        }
-        cp_async_commit();
+        // the bias lookups (cell ids, table) before the next item's copies: each cp.async is a
+        // compiler memory barrier, shared loads behind it would wait on their full latency
         if constexpr (FAST) {
             fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
         } else {
@@ -650,6 +646,12 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 9 : 14) attn_fwd_kernel(AttnPar
                                        scale2, lane);
         }
         mask_slots<KP, NT>(s, nk, scale2, blank2, lane);
+        __syncwarp();  // Q, K consumed: reload them for item i+1
+        if (i1 < n_items) {
+            sw_gather<HD, 16>(sm.Q, qg + io_nxt, rowb, rec1 + R::QTOK, lane);
+            sw_gather<HD, KP>(sm.K, kg + io_nxt, rowb, rec1 + R::KTOK, lane);
+        }
+        cp_async_commit();
 
         float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
@@ -818,9 +820,7 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
         float s[NT][4], dp[NT][4];
         sw_mma_abt<HD, NT>(s, qa, sm.K, sm.Kb, lane);
         sw_mma_abt<HD, NT>(dp, oa, sm.V, sm.Vb, lane);
-        __syncwarp();  // V consumed
-        if (more) sw_gather<HD, KP>(sm.V, vg + nxt_tok * ld, rowb, rec1 + R::KTOK, lane);
-        cp_async_commit();
+        // bias lookups and LSE before the next item's V copies (cp.async = compiler memory barrier)
         const int cls = rec[R::HDR + kHFast];
         if constexpr (FAST) {
             fast_bias_frag<KP, NT>(s, rec + R::QCELL, rec + R::KCELL, sm.tab, scale2, lane);
@@ -833,9 +833,12 @@ __global__ void __launch_bounds__(32, HD >= 64 ? 7 : 11) attn_bwd_q_kernel(AttnP
                                        scale2, lane);
         }
         mask_slots<KP, NT>(s, nk, scale2, blank2, lane);
+        const float ls0 = sm.lse[r0] * kLog2e, ls1 = sm.lse[r0 + 8] * kLog2e;
+        __syncwarp();  // V consumed
+        if (more) sw_gather<HD, KP>(sm.V, vg + nxt_tok * ld, rowb, rec1 + R::KTOK, lane);
+        cp_async_commit();
 
         // P = exp(S - LSE);  D = rowsum(P o dP)
-        const float ls0 = sm.lse[r0] * kLog2e, ls1 = sm.lse[r0 + 8] * kLog2e;
         float D0 = 0.f, D1 = 0.f;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
