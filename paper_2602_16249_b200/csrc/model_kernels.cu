@@ -88,49 +88,69 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 
 // VJP: dx = inv (g*gamma - mean(g*gamma) - xh mean(g*gamma*xh)); dres_out = dres_in + dx
 // (fp32, dres_in may alias dres_out), optional bf16 copy; dgamma/dbeta per-block partials
-// [block][2C] (warps summed in a fixed order through shared memory).
+// [block][2C] (warps summed in a fixed order through shared memory).  A warp takes R rows per
+// iteration and issues every load of them (stats, x, dy, dres_in) before the first reduction,
+// so each iteration waits out one DRAM round trip instead of 2R.
+template <int V>
+constexpr int ln_bwd_rows() { return V <= 2 ? 4 : V <= 4 ? 2 : 1; }
+
 template <int V, typename XT>
 __global__ void __launch_bounds__(kRowWarps * 32)
     ln_bwd_kernel(const float* __restrict__ dy, const XT* __restrict__ x, const float2* __restrict__ stats,
                   const float* __restrict__ gamma, int64_t rows, const float* dres_in, float* dres_out,
                   __nv_bfloat16* __restrict__ dres_bf, float* __restrict__ part) {
-    constexpr int C = 64 * V;
+    constexpr int C = 64 * V, R = ln_bwd_rows<V>();
     __shared__ float red[2 * C];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float2 dg[V], db[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) dg[j] = db[j] = make_float2(0.f, 0.f);
-    for (int64_t r = int64_t(blockIdx.x) * kRowWarps + warp; r < rows; r += int64_t(gridDim.x) * kRowWarps) {
-        const float2 st = stats[r];
-        float2 xh[V], gg[V];
-        float s1 = 0.f, s2 = 0.f;
+    for (int64_t r0 = (int64_t(blockIdx.x) * kRowWarps + warp) * R; r0 < rows;
+         r0 += int64_t(gridDim.x) * kRowWarps * R) {
+        float2 st[R], xv[R][V], g[R][V], o[R][V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int c = 2 * (lane + 32 * j);
-            const float2 xv = ld2(x, r * C + c), g = ld2(dy, r * C + c), ga = ld2(gamma, c);
-            xh[j] = make_float2((xv.x - st.x) * st.y, (xv.y - st.x) * st.y);
-            gg[j] = make_float2(g.x * ga.x, g.y * ga.y);
-            s1 += gg[j].x + gg[j].y;
-            s2 += gg[j].x * xh[j].x + gg[j].y * xh[j].y;
-            dg[j].x += g.x * xh[j].x;
-            dg[j].y += g.y * xh[j].y;
-            db[j].x += g.x;
-            db[j].y += g.y;
-        }
-        s1 = warp_sum(s1);
-        s2 = warp_sum(s2);
-        const float m1 = s1 / float(C), m2 = s2 / float(C);
+        for (int q = 0; q < R; ++q) {
+            const int64_t r = r0 + q;
+            if (r >= rows) break;
+            st[q] = stats[r];
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-            const int64_t i = r * C + 2 * (lane + 32 * j);
-            float2 d = make_float2(st.y * (gg[j].x - m1 - xh[j].x * m2), st.y * (gg[j].y - m1 - xh[j].y * m2));
-            if (dres_in) {
-                const float2 o = ld2(dres_in, i);
-                d.x += o.x;
-                d.y += o.y;
+            for (int j = 0; j < V; ++j) {
+                const int64_t i = r * C + 2 * (lane + 32 * j);
+                xv[q][j] = ld2(x, i);
+                g[q][j] = ld2(dy, i);
+                o[q][j] = dres_in ? ld2(dres_in, i) : make_float2(0.f, 0.f);
             }
-            if (dres_out) st2(dres_out, i, d);
-            if (dres_bf) st2(dres_bf, i, d);
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int64_t r = r0 + q;
+            if (r >= rows) break;
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const float2 ga = ld2(gamma, 2 * (lane + 32 * j));
+                const float2 xh = make_float2((xv[q][j].x - st[q].x) * st[q].y, (xv[q][j].y - st[q].x) * st[q].y);
+                const float2 gg = make_float2(g[q][j].x * ga.x, g[q][j].y * ga.y);
+                s1 += gg.x + gg.y;
+                s2 += gg.x * xh.x + gg.y * xh.y;
+                dg[j].x += g[q][j].x * xh.x;
+                dg[j].y += g[q][j].y * xh.y;
+                db[j].x += g[q][j].x;
+                db[j].y += g[q][j].y;
+                xv[q][j] = xh;  // x-hat from here on
+                g[q][j] = gg;   // g * gamma
+            }
+            s1 = warp_sum(s1);
+            s2 = warp_sum(s2);
+            const float m1 = s1 / float(C), m2 = s2 / float(C);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const int64_t i = r * C + 2 * (lane + 32 * j);
+                const float2 d = make_float2(st[q].y * (g[q][j].x - m1 - xv[q][j].x * m2) + o[q][j].x,
+                                             st[q].y * (g[q][j].y - m1 - xv[q][j].y * m2) + o[q][j].y);
+                if (dres_out) st2(dres_out, i, d);
+                if (dres_bf) st2(dres_bf, i, d);
+            }
         }
     }
     if (!part) return;
@@ -209,14 +229,16 @@ int ln_fwd_bf(const __nv_bfloat16* x, float* xo, const float* g, const float* b,
     return ln_fwd_t<__nv_bfloat16>(x, nullptr, xo, nullptr, g, b, rows, C, y, stats, st);
 }
 
-unsigned ln_bwd_blocks(int64_t rows) { return row_blocks(rows, 4 * kRowWarps, 4 * kNumSMs); }
+// one iteration per warp while the grid stays under 4 blocks per SM
+static int ln_bwd_rows_of(int64_t C) { return C <= 128 ? 4 : C <= 256 ? 2 : 1; }
+unsigned ln_bwd_blocks(int64_t rows, int64_t C) { return row_blocks(rows, kRowWarps * ln_bwd_rows_of(C), 4 * kNumSMs); }
 
 template <typename XT>
 static int ln_bwd_t(const float* dy, const XT* x, const float2* stats, const float* g, int64_t rows, int64_t C,
                     const float* dres_in, float* dres_out, __nv_bfloat16* dres_bf, float* dgamma, float* dbeta,
                     float* part, cudaStream_t st) {
     if (rows <= 0) return AFFMAE_OK;
-    const unsigned nb = ln_bwd_blocks(rows);
+    const unsigned nb = ln_bwd_blocks(rows, C);
     float* pp = (dgamma || dbeta) ? part : nullptr;
     switch (C) {
 #define AFFMAE_LNB(V_)                                                                                           \
@@ -251,7 +273,7 @@ int ln_bwd_bf(const float* dy, const __nv_bfloat16* x, const float2* stats, cons
               cudaStream_t st) {
     return ln_bwd_t<__nv_bfloat16>(dy, x, stats, g, rows, C, dres_in, dres_out, dres_bf, dgamma, dbeta, part, st);
 }
-size_t ln_bwd_part_floats(int64_t rows, int64_t C) { return size_t(ln_bwd_blocks(rows)) * 2 * size_t(C); }
+size_t ln_bwd_part_floats(int64_t rows, int64_t C) { return size_t(ln_bwd_blocks(rows, C)) * 2 * size_t(C); }
 
 // ------------------------------------------------------------ positional MLP
 // hidden = GELU(c W1^T + b1), c = coords / image (scaled_coords, pipeline.cpp:48-52);
