@@ -193,6 +193,17 @@ size_t affmae_linear_bwd_workspace(int64_t m, int64_t n, int64_t k);
 int affmae_linear_bwd(const affmae_bf16* x, const affmae_bf16* w, const affmae_bf16* dy, int64_t m, int64_t n,
                       int64_t k, affmae_bf16* dx, float* dw, float* db, void* workspace, size_t workspace_bytes,
                       void* stream);
+/* Fused variants of the block's layers (the training step's GEMM epilogues):
+ *   affmae_linear_fwd_add:  y = x W^T + b + c   (c bf16 [M, N], the residual, summed in fp32)
+ *   affmae_linear_dx_gelu:  dh = (dy W) * gelu'(pre)   (dy [M, N], pre / dh bf16 [M, K]):
+ *                           linear_bwd's dX and gelu_bwd in one pass
+ *   affmae_linear_dx_f32:   dx = dy W + beta * dx   (dx fp32 [M, K]; beta 0 overwrites) */
+int affmae_linear_fwd_add(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
+                          int64_t k, const affmae_bf16* c, affmae_bf16* y, void* stream);
+int affmae_linear_dx_gelu(const affmae_bf16* dy, const affmae_bf16* w, const affmae_bf16* pre, int64_t m, int64_t n,
+                          int64_t k, affmae_bf16* dh, void* stream);
+int affmae_linear_dx_f32(const affmae_bf16* dy, const affmae_bf16* w, int64_t m, int64_t n, int64_t k, float* dx,
+                         float beta, void* stream);
 
 /* ------------------------------------------------------------------------
  * Cluster attention (nbhd_attn_streaming / nbhd_attn_backward,

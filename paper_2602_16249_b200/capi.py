@@ -30,7 +30,7 @@ EXPORTS = (
     "affmae_importance_scores", "affmae_merge_tokens_workspace", "affmae_merge_tokens",
     "affmae_merge_pool_bwd_workspace", "affmae_merge_pool_bwd", "affmae_interp_fwd", "affmae_interp_bwd",
     "affmae_adamw_lr", "affmae_adamw_step", "affmae_linear_workspace", "affmae_linear_fwd",
-    "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_linear_fwd_gelu_aux", "affmae_gelu_bwd", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",
+    "affmae_linear_bwd_workspace", "affmae_linear_bwd", "affmae_linear_fwd_gelu_aux", "affmae_gelu_bwd", "affmae_linear_fwd_add", "affmae_linear_dx_gelu", "affmae_linear_dx_f32", "affmae_layernorm_fwd", "affmae_layernorm_bwd_workspace",
     "affmae_layernorm_bwd", "affmae_norm_clamp_fwd", "affmae_norm_clamp_bwd", "affmae_masked_mse_workspace",
     "affmae_masked_mse", "affmae_gattn_fwd", "affmae_gattn_bwd", "affmae_gattn_bwd_workspace",
     "affmae_interp_bwd_gather_workspace", "affmae_interp_bwd_gather", "affmae_perlin_mask_workspace",

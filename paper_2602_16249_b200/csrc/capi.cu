@@ -335,6 +335,24 @@ int affmae_linear_bwd(const affmae_bf16* x, const affmae_bf16* w, const affmae_b
         return linear_bwd(x, w, dy, m, n, k, dx, dw, db, workspace, workspace_bytes, stream);
     )
 }
+int affmae_linear_fwd_add(const affmae_bf16* x, const affmae_bf16* w, const float* bias, int64_t m, int64_t n,
+                          int64_t k, const affmae_bf16* c, affmae_bf16* y, void* stream) {
+    AFFMAE_GUARD(
+        return linear_fwd_add(x, w, bias, m, n, k, c, y, nullptr, 0, stream);
+    )
+}
+int affmae_linear_dx_gelu(const affmae_bf16* dy, const affmae_bf16* w, const affmae_bf16* pre, int64_t m, int64_t n,
+                          int64_t k, affmae_bf16* dh, void* stream) {
+    AFFMAE_GUARD(
+        return linear_dx_gelu(dy, w, pre, m, n, k, dh, stream);
+    )
+}
+int affmae_linear_dx_f32(const affmae_bf16* dy, const affmae_bf16* w, int64_t m, int64_t n, int64_t k, float* dx,
+                         float beta, void* stream) {
+    AFFMAE_GUARD(
+        return linear_dx_f32(dy, w, m, n, k, dx, beta, nullptr, 0, stream);
+    )
+}
 
 // Tape::layer_norm forward / VJP (proj/src/tape.cpp:84-100,581-617)
 int affmae_layernorm_fwd(const affmae_bf16* x, const float* gamma, const float* beta, int64_t rows, int64_t cols,

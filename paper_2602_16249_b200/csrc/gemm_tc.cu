@@ -1,0 +1,611 @@
+// Hand-written tcgen05 GEMM for the training step's dense layers:
+//
+//   D[M, N] = A[M, K] · B[N, K]^T   (bf16 operands, fp32 accumulation in TMEM)
+//
+// with the epilogues the step needs fused into the TMEM read-back:
+//   kStore     y   = acc (+ bias[n])                               bf16
+//   kGeluAux   pre = acc + bias[n] (bf16), y = GELU(pre)            bf16, bf16
+//   kAdd       y   = acc + bias[n] + c[m, n]                        bf16
+//   kGeluBwd   y   = acc · GELU'(pre[m, n])                          bf16
+//   kF32       y   = acc (+ beta · y)                               fp32
+//   kGelu      y   = GELU(acc + bias[n])  (fp32 pre-activation)     bf16
+// This is the reference Tape's matmul + bias (+ gelu_erf) (proj/src/tape.cpp:24-114) and its
+// VJPs: the forward x W^T (A = x K-major, B = W [N, K] K-major), the input gradient dY W
+// (B = W read N-major), the weight gradient dY^T X (A = dY^T and B = X both read M/N-major).
+//
+// Structure (one CTA per SM, persistent over output tiles, 10 warps):
+//   warp 0      TMA producer: 128x64 A and BNx64 B tiles (128-byte swizzle) into a
+//               kStages-deep shared-memory ring, one mbarrier (complete_tx) per stage
+//   warp 1      TMEM allocator + MMA issuer: one thread issues tcgen05.mma.cta_group::1
+//               (M = 128, N = BN, K = 16) from shared-memory descriptors into one of two
+//               TMEM accumulators, tcgen05.commit frees the ring slot / signals the epilogue
+//   warps 2-9   epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes 32·(w%4)..), the
+//               fused elementwise op in fp32, 16-byte global stores; two warps per lane
+//               quarter split the tile's 32-column chunks; the accumulator is released as
+//               soon as its last chunk is read, so tile t's epilogue overlaps tile t+1's MMAs
+// Work items are (split, m-block, n-block) with m-block outermost within a split, so the
+// CTAs working at one time share A rows through L2.  The weight gradient's long K (= tokens)
+// is split over `splits` work ranges (multiples of 64) written as fp32 partials.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace affmae_b200 {
+namespace tc {
+
+constexpr int BM = 128, BK = 64, UK = 16;
+constexpr int kThreads = 320;  // producer, MMA, 8 epilogue warps
+constexpr int kEpiWarps = 8;
+constexpr int kStageBuf = 32 * 128;  // one epilogue staging buffer: 32 rows x 128 B
+
+enum Epi { kStore = 0, kGeluAux = 1, kAdd = 2, kGeluBwd = 3, kF32 = 4, kGelu = 5 };
+
+struct Params {
+    int M, N, K;
+    int tiles_m, tiles_n, splits, kblocks_per_split, kblocks_total;
+    const float* bias;        // [N] or null
+    const __nv_bfloat16* aux;  // kAdd: c [M, N]; kGeluBwd: pre [M, N]
+    void* out;                // bf16 [M, N] (kGeluAux: pre) or fp32 [splits][M, N]
+    __nv_bfloat16* out2;      // kGeluAux: GELU(pre)
+    float beta;
+    int64_t ldo;              // row stride of out / out2 / aux (elements)
+};
+
+template <int BN, int EPI>
+struct Cfg {
+    // one 4 KB staging buffer per epilogue warp (two for the two outputs of kGeluAux); the rest
+    // of the 227 KB goes to the operand ring
+    static constexpr int kBufs = EPI == 1 /*kGeluAux*/ ? 2 : 1;
+    static constexpr int kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (227 * 1024 - kEpiWarps * kBufs * kStageBuf - 2048) / kStageBytes;
+    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr size_t kSmem =
+        size_t(kStages) * kStageBytes + size_t(kEpiWarps) * kBufs * kStageBuf + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// parity wait; a pipeline bug traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    uint32_t done = 0, spins = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (++spins > (1u << 26)) {
+            printf("tc_gemm: mbarrier wait timed out (block %d thread %d bar %u parity %u)\n", blockIdx.x, threadIdx.x, a,
+                   parity);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptors, 128-byte swizzle (SmemDescriptor, cute/arch/mma_sm100_desc.hpp):
+//   K-major:  rows of 64 K-elements (128 B), 8-row groups 1024 B apart (SBO), LBO unused
+//   MN-major: rows of 64 M/N-elements (128 B) per k, 8-k groups 1024 B apart (SBO), 64-wide
+//             M/N chunks BK·128 B apart (LBO)
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, bool mn_major) {
+    const uint64_t lbo = mn_major ? uint64_t(BK * 128 / 16) : 1ull;
+    return uint64_t((addr >> 4) & 0x3FFF) | (lbo << 16) | (uint64_t(1024 / 16) << 32) | (1ull << 46) | (2ull << 61);
+}
+// advance to the k-th 16-element slice of a 64-wide K block
+__device__ __forceinline__ uint64_t sdesc_k(uint64_t d, int k, bool mn_major) {
+    return d + uint64_t(mn_major ? (k * UK * 128) >> 4 : (k * UK * 2) >> 4);
+}
+
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad(float x) {
+    const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+    const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+    return cdf + x * pdf;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ------------------------------------------------------------------- kernel
+struct Maps {
+    CUtensorMap a, b;
+    CUtensorMap out;   // bf16 box {64, 32} / fp32 box {32, 32}, 128-byte swizzle, [splits][M][ldo]
+    CUtensorMap out2;  // kGeluAux: GELU(pre)
+    CUtensorMap aux;   // kAdd / kGeluBwd: bf16 box {64, 32}
+};
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// 16-byte chunk c of row r in a 32 x 128 B staging buffer written / read by TMA with the
+// 128-byte swizzle (Swizzle<3,4,3> on a 1024-byte aligned base)
+__device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+template <int BN, int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Maps maps, Params p) {
+    using C = Cfg<BN, EPI>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stage_smem = smem + size_t(C::kStages) * C::kStageBytes;  // 8 warps x kBufs x 4 KB
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + kEpiWarps * C::kBufs * kStageBuf);
+    // full[S], empty[S], tfull[2], tempty[2], aux[8], then the TMEM base address slot
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4 + kEpiWarps);
+    const uint32_t smem_base = smem_u32(smem);
+    const uint32_t bar_base = smem_u32(bars);
+    auto full = [&](int s) { return bar_base + 8u * uint32_t(s); };
+    auto empty = [&](int s) { return bar_base + 8u * uint32_t(C::kStages + s); };
+    auto tfull = [&](int s) { return bar_base + 8u * uint32_t(2 * C::kStages + s); };
+    auto tempty = [&](int s) { return bar_base + 8u * uint32_t(2 * C::kStages + 2 + s); };
+    auto auxbar = [&](int e) { return bar_base + 8u * uint32_t(2 * C::kStages + 4 + e); };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(full(s), 1);
+            mbar_init(empty(s), 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(tfull(s), 1);
+            mbar_init(tempty(s), kEpiWarps);
+        }
+        for (int e = 0; e < kEpiWarps; ++e) mbar_init(auxbar(e), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.b)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.out)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(uint32_t(C::kTmemCols))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles = p.tiles_m * p.tiles_n;
+    const int work = tiles * p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int w = blockIdx.x; w < work; w += gridDim.x) {
+                const int split = w / tiles, t = w - split * tiles;
+                const int mb = t / p.tiles_n, nb = t - mb * p.tiles_n;
+                const int kb0 = split * p.kblocks_per_split;
+                const int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(empty(stage), phase ^ 1);
+                    const uint32_t sa = smem_base + uint32_t(stage) * C::kStageBytes;
+                    const uint32_t sb = sa + C::kABytes;
+                    mbar_expect_tx(full(stage), C::kStageBytes);
+                    if (A_MN) {
+#pragma unroll
+                        for (int c = 0; c < BM / 64; ++c)
+                            tma_load_3d(sa + c * (BK * 128), &maps.a, mb * BM + 64 * c, kb * BK, 0, full(stage));
+                    } else {
+                        tma_load_3d(sa, &maps.a, kb * BK, mb * BM, 0, full(stage));
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int c = 0; c < BN / 64; ++c)
+                            tma_load_3d(sb + c * (BK * 128), &maps.b, nb * BN + 64 * c, kb * BK, 0, full(stage));
+                    } else {
+                        tma_load_3d(sb, &maps.b, kb * BK, nb * BN, 0, full(stage));
+                    }
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // instruction descriptor (InstrDescriptor): fp32 D, bf16 A / B, majors, N >> 3, M >> 4
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(A_MN) << 15) |
+                                   (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int w = blockIdx.x; w < work; w += gridDim.x) {
+                const int split = w / tiles;
+                const int kb0 = split * p.kblocks_per_split;
+                const int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
+                mbar_wait(tempty(acc), acc_phase ^ 1);
+                fence_after();
+                const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(full(stage), phase);
+                    fence_after();
+                    const uint32_t sa = smem_base + uint32_t(stage) * C::kStageBytes;
+                    const uint64_t da = sdesc(sa, A_MN), db = sdesc(sa + C::kABytes, B_MN);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k)
+                        mma_bf16(tmem_d, sdesc_k(da, k, A_MN), sdesc_k(db, k, B_MN), idesc,
+                                 (kb > kb0 || k > 0) ? 1u : 0u);
+                    mma_commit(empty(stage));
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(tfull(acc));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // Epilogue: a warp owns 32 accumulator rows (its TMEM lane quarter) and, per unit, 128
+        // bytes of output columns (64 bf16 / 32 fp32); it converts its rows into a swizzled
+        // 32 x 128 B staging buffer and one lane hands the buffer to a TMA store, so the global
+        // writes are whole lines (the M / N tails are clipped by the tensor map).
+        constexpr bool kF32Out = EPI == kF32;
+        constexpr int kCols = kF32Out ? 32 : 64;  // columns per unit
+        constexpr int kUnits = BN / kCols;
+        constexpr bool kAux = EPI == kAdd || EPI == kGeluBwd;
+        const int ew = warp - 2;       // 0..7
+        const int quarter = warp & 3;  // TMEM lanes 32·quarter .. +31 (tcgen05.ld lane rule)
+        const int half = ew >> 2;      // units half, half + 2, ...
+        const uint32_t buf0 = smem_u32(stage_smem) + uint32_t(ew) * C::kBufs * kStageBuf, buf1 = buf0 + kStageBuf;
+        uint8_t* gbuf0 = stage_smem + size_t(ew) * C::kBufs * kStageBuf;
+        uint8_t* gbuf1 = gbuf0 + kStageBuf;
+        int acc = 0;
+        uint32_t acc_phase = 0, aux_phase = 0;
+        for (int w = blockIdx.x; w < work; w += gridDim.x) {
+            const int split = w / tiles, t = w - split * tiles;
+            const int mb = t / p.tiles_n, nb = t - mb * p.tiles_n;
+            const int row0 = mb * BM + 32 * quarter;
+            mbar_wait(tfull(acc), acc_phase);
+            fence_after();
+            if (half >= kUnits) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty(acc));
+            }
+#pragma unroll 1
+            for (int u = half; u < kUnits; u += 2) {
+                const int n0 = nb * BN + kCols * u;
+                // the staging buffers are free once the previous unit's TMA stores have read them
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+                if (kAux && n0 < p.N) {
+                    if (lane == 0) {
+                        mbar_expect_tx(auxbar(ew), kStageBuf);
+                        tma_load_3d(buf0, &maps.aux, n0, row0, 0, auxbar(ew));
+                    }
+                }
+                float v[kCols];
+                tmem_ld32(tmem_base + (uint32_t(32 * quarter) << 16) + uint32_t(acc * BN + kCols * u), v);
+                if (kCols == 64)
+                    tmem_ld32(tmem_base + (uint32_t(32 * quarter) << 16) + uint32_t(acc * BN + kCols * u + 32), v + 32);
+                if (u + 2 >= kUnits) {
+                    // this warp's last read of the accumulator: release it to the MMA warp
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty(acc));
+                }
+                if (n0 >= p.N) continue;  // warp-uniform
+                if (p.bias && EPI != kGeluBwd && EPI != kF32) {
+#pragma unroll
+                    for (int j = 0; j < kCols; j += 4) {
+                        if (n0 + j < p.N) {
+                            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n0 + j));
+                            v[j] += b.x;
+                            v[j + 1] += b.y;
+                            v[j + 2] += b.z;
+                            v[j + 3] += b.w;
+                        }
+                    }
+                }
+                if (kAux) {
+                    mbar_wait(auxbar(ew), aux_phase);
+                    aux_phase ^= 1;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 a = *reinterpret_cast<const uint4*>(gbuf0 + swz(lane, c));
+                        const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = __bfloat1622float2(ah[e]);
+                            if (EPI == kAdd) {
+                                v[8 * c + 2 * e] += f.x;
+                                v[8 * c + 2 * e + 1] += f.y;
+                            } else {
+                                v[8 * c + 2 * e] *= gelu_grad(f.x);
+                                v[8 * c + 2 * e + 1] *= gelu_grad(f.y);
+                            }
+                        }
+                    }
+                    __syncwarp();  // every lane has read its aux row before the buffer is rewritten
+                }
+                if (kF32Out) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        *reinterpret_cast<float4*>(gbuf0 + swz(lane, c)) =
+                            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        float* x = v + 8 * c;
+                        if (EPI == kGelu) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
+                        }
+                        uint4 r;
+                        r.x = pack_bf16(x[0], x[1]);
+                        r.y = pack_bf16(x[2], x[3]);
+                        r.z = pack_bf16(x[4], x[5]);
+                        r.w = pack_bf16(x[6], x[7]);
+                        *reinterpret_cast<uint4*>(gbuf0 + swz(lane, c)) = r;
+                        if (EPI == kGeluAux) {
+                            // GELU of the stored (bf16-rounded) pre-activation, as the backward sees it
+                            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&r);
+                            uint4 y;
+                            uint32_t* yw = reinterpret_cast<uint32_t*>(&y);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 f = __bfloat1622float2(rh[e]);
+                                yw[e] = pack_bf16(gelu_f(f.x), gelu_f(f.y));
+                            }
+                            *reinterpret_cast<uint4*>(gbuf1 + swz(lane, c)) = y;
+                        }
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    if (kF32Out && p.beta != 0.f)
+                        tma_reduce_add_3d(&maps.out, buf0, n0, row0, split);
+                    else
+                        tma_store_3d(&maps.out, buf0, n0, row0, split);
+                    if (EPI == kGeluAux) tma_store_3d(&maps.out2, buf1, n0, row0, 0);
+                    bulk_commit();
+                }
+            }
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) bulk_wait0();
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(uint32_t(C::kTmemCols))
+                     : "memory");
+    }
+}
+
+// --------------------------------------------------------------------- host
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// row-major [layers][rows][cols] (row stride ld elements, layer stride rows·ld), 128-byte
+// swizzle, box = 128 bytes of columns x box_rows rows x 1 layer
+int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows, bool f32 = false,
+             int64_t layers = 1) {
+    auto enc = encoder();
+    if (!enc) return fail(AFFMAE_ECUDA, "gemm: cuTensorMapEncodeTiled unavailable");
+    const int64_t es = f32 ? 4 : 2;
+    if (reinterpret_cast<uintptr_t>(ptr) % 16 || (ld * es) % 16)
+        return fail(AFFMAE_EUNSUPPORTED, "gemm: operands need 16-byte aligned rows");
+    cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(rows), cuuint64_t(layers)};
+    cuuint64_t strides[2] = {cuuint64_t(ld * es), cuuint64_t(rows * ld * es)};
+    cuuint32_t box[3] = {cuuint32_t(128 / es), cuuint32_t(box_rows), 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                           const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(AFFMAE_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
+    return AFFMAE_OK;
+}
+
+template <int BN, int EPI, bool A_MN, bool B_MN>
+int launch(const Maps& maps, const Params& p, cudaStream_t st) {
+    auto kern = tc_gemm_kernel<BN, EPI, A_MN, B_MN>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg<BN, EPI>::kSmem));
+    });
+    if (attr_err != cudaSuccess) return cuda_status(attr_err, "gemm: smem attribute");
+    const int work = p.tiles_m * p.tiles_n * p.splits;
+    const int grid = std::min(work, device_sms());
+    kern<<<grid, kThreads, Cfg<BN, EPI>::kSmem, st>>>(maps, p);
+    AFFMAE_LAUNCH_CHECK("tc_gemm_kernel");
+    return AFFMAE_OK;
+}
+
+template <int EPI, bool A_MN, bool B_MN>
+int dispatch_bn(int bn, const Maps& maps, const Params& p, cudaStream_t st) {
+    if (bn == 256) return launch<256, EPI, A_MN, B_MN>(maps, p, st);
+    if (bn == 128) return launch<128, EPI, A_MN, B_MN>(maps, p, st);
+    return launch<64, EPI, A_MN, B_MN>(maps, p, st);
+}
+
+int pick_bn(int64_t n) {
+    if (n <= 64) return 64;
+    if (n <= 128) return 128;
+    // least padding; ties to the wider tile
+    const int64_t p256 = (n + 255) / 256 * 256, p128 = (n + 127) / 128 * 128;
+    return p256 <= p128 ? 256 : 128;
+}
+
+}  // namespace tc
+
+// D[M, N] = op(A) op(B)^T (see the file header).
+//   a_mn = 0: A is x [M, K] row-major (lda = K);  a_mn = 1: A is read from a [K, M] row-major buffer
+//   b_mn = 0: B is W [N, K] row-major;            b_mn = 1: B is read from a [K, N] row-major buffer
+// splits > 1 (kF32 only): K is cut into `splits` ranges, split s writes out + s·M·ldo.
+int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K, int epi,
+            const float* bias, const void* aux, void* out, void* out2, float beta, int64_t ldo, int splits,
+            cudaStream_t st) {
+    using namespace tc;
+    if (!a || !b || !out) return fail(AFFMAE_ECONFIG, "gemm: null pointer");
+    if (M < 1 || N < 1 || K < 1 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
+        return fail(AFFMAE_ECONFIG, "gemm: bad shape");
+    // 16-byte aligned rows for every TMA view: N (output / N-major B rows), K of a K-major
+    // operand, M of an M-major A
+    if (N % 8 || ((!a_mn || !b_mn) && K % 8) || (a_mn && M % 8))
+        return fail(AFFMAE_EUNSUPPORTED, "gemm: N, K of a K-major operand and M of an M-major A must be multiples of 8");
+    if ((epi == kGeluAux && !out2) || ((epi == kAdd || epi == kGeluBwd) && !aux))
+        return fail(AFFMAE_ECONFIG, "gemm: epilogue operand missing");
+    if (splits < 1 || (splits > 1 && epi != kF32)) return fail(AFFMAE_ECONFIG, "gemm: split-K needs the fp32 epilogue");
+    if (ldo < N || ldo % 8) return fail(AFFMAE_ECONFIG, "gemm: bad output stride");
+    const int bn = pick_bn(N);
+    Maps maps;
+    int rc;
+    if ((rc = a_mn ? make_map(&maps.a, a, K, M, M, BK) : make_map(&maps.a, a, M, K, K, BM))) return rc;
+    if ((rc = b_mn ? make_map(&maps.b, b, K, N, N, BK) : make_map(&maps.b, b, N, K, K, bn))) return rc;
+    Params p{};
+    p.M = int(M);
+    p.N = int(N);
+    p.K = int(K);
+    p.tiles_m = int((M + BM - 1) / BM);
+    p.tiles_n = int((N + bn - 1) / bn);
+    p.kblocks_total = int((K + BK - 1) / BK);
+    p.splits = std::min(splits, p.kblocks_total);
+    p.kblocks_per_split = (p.kblocks_total + p.splits - 1) / p.splits;
+    p.splits = (p.kblocks_total + p.kblocks_per_split - 1) / p.kblocks_per_split;
+    p.bias = bias;
+    p.aux = static_cast<const __nv_bfloat16*>(aux);
+    p.out = out;
+    p.out2 = static_cast<__nv_bfloat16*>(out2);
+    p.beta = beta;
+    p.ldo = ldo;
+    if (splits > 1 && p.splits != splits) return fail(AFFMAE_ECONFIG, "gemm: split count does not divide K blocks");
+    if (epi == kF32 && beta != 0.f && beta != 1.f) return fail(AFFMAE_EUNSUPPORTED, "gemm: fp32 beta must be 0 or 1");
+    if ((rc = make_map(&maps.out, out, M, N, ldo, 32, epi == kF32, p.splits))) return rc;
+    maps.out2 = maps.out;
+    maps.aux = maps.out;
+    if (epi == kGeluAux && (rc = make_map(&maps.out2, out2, M, N, ldo, 32))) return rc;
+    if ((epi == kAdd || epi == kGeluBwd) && (rc = make_map(&maps.aux, aux, M, N, ldo, 32))) return rc;
+    const int key = (a_mn ? 2 : 0) | (b_mn ? 1 : 0);
+    switch (epi) {
+        case kStore:
+            if (key == 0) return dispatch_bn<kStore, false, false>(bn, maps, p, st);
+            if (key == 1) return dispatch_bn<kStore, false, true>(bn, maps, p, st);
+            break;
+        case kGeluAux:
+            if (key == 0) return dispatch_bn<kGeluAux, false, false>(bn, maps, p, st);
+            break;
+        case kGelu:
+            if (key == 0) return dispatch_bn<kGelu, false, false>(bn, maps, p, st);
+            break;
+        case kAdd:
+            if (key == 0) return dispatch_bn<kAdd, false, false>(bn, maps, p, st);
+            break;
+        case kGeluBwd:
+            if (key == 1) return dispatch_bn<kGeluBwd, false, true>(bn, maps, p, st);
+            break;
+        case kF32:
+            if (key == 1) return dispatch_bn<kF32, false, true>(bn, maps, p, st);
+            if (key == 3) return dispatch_bn<kF32, true, true>(bn, maps, p, st);
+            break;
+        default:
+            break;
+    }
+    return fail(AFFMAE_EUNSUPPORTED, "gemm: epilogue / operand-major combination not instantiated");
+}
+
+// split count that fills the GPU: splits of >= 512 tokens each
+int tc_gemm_pick_splits(int64_t M, int64_t N, int64_t K) {
+    const int64_t tiles = ((M + tc::BM - 1) / tc::BM) * ((N + tc::pick_bn(N) - 1) / tc::pick_bn(N));
+    const int64_t kb = (K + tc::BK - 1) / tc::BK;
+    int64_t s = std::max<int64_t>(1, device_sms() / std::max<int64_t>(tiles, 1));
+    s = std::min<int64_t>(s, std::max<int64_t>(1, kb / 8));
+    // make the split an exact partition of the K blocks (tc_gemm requires it)
+    while (s > 1) {
+        const int64_t per = (kb + s - 1) / s;
+        if ((kb + per - 1) / per == s) break;
+        --s;
+    }
+    return int(s);
+}
+
+}  // namespace affmae_b200

@@ -129,10 +129,14 @@ int adamw_step_dev(const affmae_adamw_cfg* c, int64_t* step_dev, void* scalars_d
                    const int64_t* seg_off, const uint8_t* seg_decay, int64_t n, float* value, const float* grad,
                    float* m, float* v, void* shadow, int64_t n_shadow, void* stream);
 size_t adamw_scalars_bytes();
-// gemm_sm100.cu: y = x W^T + b + c (c bf16 [M, N] added before the rounding)
+// gemm.cu: y = x W^T + b + c (c bf16 [M, N] added before the rounding)
 int linear_fwd_add(const void* x, const void* w, const float* bias, int64_t m, int64_t n, int64_t k, const void* c,
                    void* y, void* ws, size_t ws_bytes, void* stream);
-// gemm_sm100.cu: dX = dY W into fp32 with D = dY W + beta * D (beta 0 overwrites, 1 accumulates)
+// gemm.cu: dH = (dY W) * GELU'(pre) (bf16), the MLP's fc2 input gradient with the
+// activation derivative fused into the GEMM epilogue
+int linear_dx_gelu(const void* dy, const void* w, const void* pre, int64_t m, int64_t n, int64_t k, void* dh,
+                   void* stream);
+// gemm.cu: dX = dY W into fp32 with D = dY W + beta * D (beta 0 overwrites, 1 accumulates)
 int linear_dx_f32(const void* dy, const void* w, int64_t m, int64_t n, int64_t k, float* dx, float beta, void* ws,
                   size_t ws_bytes, void* stream);
 

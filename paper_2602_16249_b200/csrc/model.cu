@@ -683,6 +683,18 @@ struct Ctx {
         CK(guard(dx));
         return linear_bwd(x, w, dy, rows, n, k, dx, nullptr, nullptr, m.gws, m.gws_bytes, sv());
     }
+    // MLP fc2 backward: dH = (dY W) * GELU'(pre) on the main stream (the activation's VJP in the
+    // GEMM epilogue), dW / db on the side stream
+    int bwd_xw_gelu(const bf16* x, const bf16* w, const bf16* dy, int64_t rows, int64_t n, int64_t k, const bf16* pre,
+                    bf16* dh, float* dw, float* db) const {
+        if (!overlap) {
+            CK(linear_bwd(x, w, dy, rows, n, k, nullptr, dw, db, m.gws, m.gws_bytes, sv()));
+        } else {
+            CK(side_dw(x, w, dy, rows, n, k, dw, db));
+            CK(guard(dh));
+        }
+        return linear_dx_gelu(dy, w, pre, rows, n, k, dh, sv());
+    }
     // main stream waits for every side-stream weight gradient
     int join() const {
         if (!overlap) return AFFMAE_OK;
@@ -697,12 +709,11 @@ struct Ctx {
     int fwd(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, bf16* y) const {
         return linear_fwd(x, w, b ? b : m.zero_bias, rows, n, k, 0, y, m.gws, m.gws_bytes, sv());
     }
-    // y = GELU(x W^T + b), pre-activation kept for the backward: identity GEMM into `pre`,
-    // then a separate activation pass (cheaper than the GEMM's fused erf epilogue here)
+    // y = GELU(x W^T + b) with the pre-activation kept for the backward: both written by the
+    // GEMM's epilogue (gemm_tc.cu kGeluAux)
     int fwd_gelu(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, bf16* y,
                  bf16* pre) const {
-        CK(linear_fwd(x, w, b, rows, n, k, 0, pre, m.gws, m.gws_bytes, sv()));
-        return mk::gelu_fwd(pre, rows * n, y, st);
+        return linear_fwd_gelu_aux(x, w, b, rows, n, k, y, pre, m.gws, m.gws_bytes, sv());
     }
     int fwd_add(const bf16* x, int64_t rows, int64_t k, const bf16* w, int64_t n, const float* b, const bf16* c,
                 bf16* y) const {
@@ -928,8 +939,8 @@ int block_bwd(const Ctx& x, int s, int b) {
     // MLP branch: out = fmid + GELU(h2 W1 + b1) W2 + b2
     // (weight gradients fork to the side stream; dy buffers alternate dfbf -> dfbf2 -> dfbf and
     // dm (B4) / dqkv (B4b) so the next writer rarely waits for them)
-    CK(x.bwd_xw(k.m, PBF(m, pre + "mlp.w2"), m.dfbf, M, D, 4 * D, m.B4, GF(m, pre + "mlp.w2"), GF(m, pre + "mlp.b2")));
-    CK(gelu_bwd(k.pre, m.B4, M * 4 * D, m.B4, x.sv()));
+    CK(x.bwd_xw_gelu(k.m, PBF(m, pre + "mlp.w2"), m.dfbf, M, D, 4 * D, k.pre, m.B4, GF(m, pre + "mlp.w2"),
+                     GF(m, pre + "mlp.b2")));
     CK(x.side_dw(k.h2, PBF(m, pre + "mlp.w1"), m.B4, M, 4 * D, D, GF(m, pre + "mlp.w1"), GF(m, pre + "mlp.b1")));
     CK(x.bwd_x(m.B4, PBF(m, pre + "mlp.w1"), M, 4 * D, D, m.F1, 0.f));
     CK(x.guard(m.dfbf2));
@@ -989,9 +1000,8 @@ int round_bwd(const Ctx& x, int si, int r) {
     // MLP
     // (weight gradients on the side stream; dfq's bf16 copy goes dfq_bf -> dfq_bf2 -> dfq_bf,
     // the cross attention's dq / dk | dv use their own B2x / dkv)
-    CK(x.bwd_xw(R.m, PBF(m, pre + "mlp.w2"), m.dfq_bf, Mq, dd, 2 * dd, m.B4, GF(m, pre + "mlp.w2"),
-                GF(m, pre + "mlp.b2")));
-    CK(gelu_bwd(R.pre, m.B4, Mq * 2 * dd, m.B4, x.sv()));
+    CK(x.bwd_xw_gelu(R.m, PBF(m, pre + "mlp.w2"), m.dfq_bf, Mq, dd, 2 * dd, R.pre, m.B4, GF(m, pre + "mlp.w2"),
+                     GF(m, pre + "mlp.b2")));
     CK(x.side_dw(R.h3, PBF(m, pre + "mlp.w1"), m.B4, Mq, 2 * dd, dd, GF(m, pre + "mlp.w1"), GF(m, pre + "mlp.b1")));
     CK(x.bwd_x(m.B4, PBF(m, pre + "mlp.w1"), Mq, 2 * dd, dd, m.F1, 0.f));
     CK(x.guard(m.dfq_bf2));

@@ -574,6 +574,47 @@ def gelu_bwd(pre, dy, stream=None):
     return dpre
 
 
+def linear_add(x, w, bias, c, stream=None):
+    """y = x W^T + b + c (the residual c bf16 [M, N] added in fp32 before the one rounding)."""
+    for t, n in ((x, "x"), (w, "w"), (c, "c")):
+        _req(t, torch.bfloat16, n)
+    _req(bias, torch.float32, "bias")
+    M, K = x.shape
+    N = w.shape[0]
+    y = torch.empty((M, N), dtype=torch.bfloat16, device=x.device)
+    capi.check(capi.lib().affmae_linear_fwd_add(
+        C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(bias.data_ptr()), C.c_int64(M), C.c_int64(N),
+        C.c_int64(K), C.c_void_p(c.data_ptr()), C.c_void_p(y.data_ptr()), _stream(stream)), "linear_add")
+    return y
+
+
+def linear_dx_gelu(dy, w, pre, stream=None):
+    """dh = (dy W) * gelu'(pre): the input gradient of y = GELU(pre) W^T + b, one tcgen05 pass."""
+    for t, n in ((dy, "dy"), (w, "w"), (pre, "pre")):
+        _req(t, torch.bfloat16, n)
+    M, N = dy.shape
+    K = w.shape[1]
+    dh = torch.empty((M, K), dtype=torch.bfloat16, device=dy.device)
+    capi.check(capi.lib().affmae_linear_dx_gelu(
+        C.c_void_p(dy.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(pre.data_ptr()), C.c_int64(M), C.c_int64(N),
+        C.c_int64(K), C.c_void_p(dh.data_ptr()), _stream(stream)), "linear_dx_gelu")
+    return dh
+
+
+def linear_dx_f32(dy, w, dx=None, beta=0.0, stream=None):
+    """dx = dy W + beta dx in fp32 (dx [M, K] fp32; a new zero buffer if None)."""
+    _req(dy, torch.bfloat16, "dy")
+    _req(w, torch.bfloat16, "w")
+    M, N = dy.shape
+    K = w.shape[1]
+    if dx is None:
+        dx = torch.zeros((M, K), dtype=torch.float32, device=dy.device)
+    capi.check(capi.lib().affmae_linear_dx_f32(
+        C.c_void_p(dy.data_ptr()), C.c_void_p(w.data_ptr()), C.c_int64(M), C.c_int64(N), C.c_int64(K),
+        C.c_void_p(dx.data_ptr()), C.c_float(beta), _stream(stream)), "linear_dx_f32")
+    return dx
+
+
 def linear_bwd(x, w, dy, dw=None, db=None, need_dx=True, stream=None):
     """Backward of y = x W^T + b (dy already through the activation) on tcgen05: returns
     (dx bf16 [M, K], dw fp32 [N, K] +=, db fp32 [N] +=); dw/db are zeros if not given."""

@@ -107,3 +107,61 @@ def test_mlp_block_fwd_bwd_matches_fp32_reference():
     assert _rel(y.float(), yf.detach()) <= 1e-2
     for got, want in ((dx, xf.grad), (dw1, w1f.grad), (db1, b1f.grad), (dw2, w2f.grad), (db2, b2f.grad)):
         assert _rel(got.float(), want) <= 2e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k", [(262144, 384, 128),   # stage-0 QKV of the AFFMAE-B step (64 images)
+                                   (41920, 2048, 512),   # stage-2 MLP fc1
+                                   (16768, 1024, 4096),  # stage-3 MLP fc2
+                                   (2050, 16, 256),      # merge scorer (N = 16: one 64-wide tile, masked)
+                                   (300, 72, 40)])       # ragged everything
+def test_linear_step_shapes(m, n, k):
+    """The training step's GEMM shapes on the hand-written tcgen05 kernel (gemm_tc.cu): forward
+    (K-major operands), dX (N-major W), dW over every token (M- and N-major operands, split-K
+    partials reduced in a fixed order) against torch fp32."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(m + 7 * n + k)
+    x = torch.randn((m, k), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((n, k), device="cuda", generator=g) / k ** 0.5).to(torch.bfloat16)
+    b = torch.randn(n, device="cuda", generator=g)
+    dy = torch.randn((m, n), device="cuda", generator=g).to(torch.bfloat16)
+    y = ops.linear(x, w, b).float()
+    assert _rel(y, x.float() @ w.float().t() + b) <= 1e-2
+    dw0 = torch.randn((n, k), device="cuda", generator=g)
+    dx, dw, db = ops.linear_bwd(x, w, dy, dw=dw0.clone())
+    assert _rel(dx.float(), dy.float() @ w.float()) <= 1e-2
+    assert _rel(dw - dw0, dy.float().t() @ x.float()) <= 1e-2
+    assert _rel(db, dy.float().sum(0)) <= 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,d", [(8192, 128), (1000, 256), (4100, 512)])
+def test_linear_fused_epilogues(m, d):
+    """GELU-aux forward, residual-add forward, dX with the GELU derivative fused, and the fp32
+    dX with beta (the model's residual-stream gradient accumulation) against torch fp32."""
+    import torch
+    from paper_2602_16249_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(m + d)
+    x = torch.randn((m, d), device="cuda", generator=g).to(torch.bfloat16)
+    w1 = (torch.randn((4 * d, d), device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    b1 = torch.randn(4 * d, device="cuda", generator=g) * 0.1
+    w2 = (torch.randn((d, 4 * d), device="cuda", generator=g) / (4 * d) ** 0.5).to(torch.bfloat16)
+    b2 = torch.randn(d, device="cuda", generator=g) * 0.1
+    c = torch.randn((m, d), device="cuda", generator=g).to(torch.bfloat16)
+    h, pre = ops.linear_gelu_save(x, w1, b1)
+    pref = x.float() @ w1.float().t() + b1
+    assert _rel(pre.float(), pref) <= 1e-2
+    assert _rel(h.float(), torch.nn.functional.gelu(pre.float())) <= 1e-2
+    y = ops.linear_add(h, w2, b2, c)
+    assert _rel(y.float(), h.float() @ w2.float().t() + b2 + c.float()) <= 1e-2
+    dy = torch.randn((m, d), device="cuda", generator=g).to(torch.bfloat16)
+    dh = ops.linear_dx_gelu(dy, w2, pre)
+    pf = pre.float()
+    gp = 0.5 * (1 + torch.erf(pf / 2 ** 0.5)) + pf * torch.exp(-0.5 * pf * pf) / (2 * torch.pi) ** 0.5
+    assert _rel(dh.float(), (dy.float() @ w2.float()) * gp) <= 1e-2
+    dx0 = torch.randn((m, 4 * d), device="cuda", generator=g)
+    dx = ops.linear_dx_f32(dy, w2, dx=dx0.clone(), beta=1.0)
+    assert _rel(dx, dx0 + dy.float() @ w2.float()) <= 1e-3
+    dx = ops.linear_dx_f32(dy, w2, dx=dx0.clone(), beta=0.0)
+    assert _rel(dx, dy.float() @ w2.float()) <= 1e-3
