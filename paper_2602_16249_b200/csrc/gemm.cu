@@ -52,21 +52,68 @@ __global__ void gelu_bwd_kernel(const uint4* __restrict__ pre, const uint4* __re
     }
 }
 
-// db[n] += sum_m dY[m, n]: per (256-column block, row chunk) partials, two columns per thread,
-// then a fixed-order sum over the chunks (deterministic)
-__global__ void __launch_bounds__(128) colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t m, int64_t n,
-                                                             int64_t rows_per, float* __restrict__ part) {
-    const int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
-    if (col >= n) return;
-    const int64_t r0 = int64_t(blockIdx.y) * rows_per, r1 = r0 + rows_per < m ? r0 + rows_per : m;
-    float s0 = 0.f, s1 = 0.f;
-    for (int64_t r = r0; r < r1; ++r) {
-        const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dy + r * n + col));
-        s0 += v.x;
-        s1 += v.y;
+// db[n] += sum_m dY[m, n] in two deterministic passes.  Pass 1: block b sums the rows of its
+// chunk; a thread owns 8 consecutive columns (16-byte loads) and every (256 / groups)-th row
+// of the chunk, four rows in flight; the row lanes are then added in lane order through shared
+// memory.  Pass 2: one warp per column adds the chunk partials in a fixed order.
+constexpr int kColsumThreads = 256;
+__global__ void __launch_bounds__(kColsumThreads)
+    colsum_partial_kernel(const __nv_bfloat16* __restrict__ dy, int64_t m, int64_t n, int64_t rows_per,
+                          float* __restrict__ part) {
+    extern __shared__ float red[];  // [lanes][8 * groups]
+    const int64_t g8 = n / 8;
+    const int groups = int(g8 < kColsumThreads ? g8 : kColsumThreads);
+    const int lanes = kColsumThreads / groups;
+    const int t = threadIdx.x;
+    const int gi = t % groups, li = t / groups;
+    const int64_t r0 = int64_t(blockIdx.x) * rows_per, r1 = r0 + rows_per < m ? r0 + rows_per : m;
+    for (int64_t gbase = 0; gbase < g8; gbase += groups) {
+        const int64_t g = gbase + gi;
+        float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (li < lanes && g < g8) {
+            const uint4* src = reinterpret_cast<const uint4*>(dy) + g;
+            int64_t r = r0 + li;
+#pragma unroll 1
+            for (; r + 3 * lanes < r1; r += 4 * lanes) {
+                uint4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldg(src + (r + int64_t(u) * lanes) * g8);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = __bfloat1622float2(h[e]);
+                        s[2 * e] += f.x;
+                        s[2 * e + 1] += f.y;
+                    }
+                }
+            }
+            for (; r < r1; r += lanes) {
+                const uint4 v = __ldg(src + r * g8);
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(h[e]);
+                    s[2 * e] += f.x;
+                    s[2 * e + 1] += f.y;
+                }
+            }
+        }
+        if (li < lanes) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) red[li * 8 * groups + 8 * gi + e] = s[e];
+        }
+        __syncthreads();
+        for (int c = t; c < 8 * groups; c += kColsumThreads) {
+            const int64_t col = gbase * 8 + c;
+            if (col >= n) continue;
+            float a = 0.f;
+            for (int l = 0; l < lanes; ++l) a += red[l * 8 * groups + c];
+            part[int64_t(blockIdx.x) * n + col] = a;
+        }
+        __syncthreads();
     }
-    part[int64_t(blockIdx.y) * n + col] = s0;
-    part[int64_t(blockIdx.y) * n + col + 1] = s1;
 }
 __global__ void colsum_final_kernel(const float* __restrict__ part, int64_t n, int chunks, float* __restrict__ db) {
     const int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -203,9 +250,12 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
     }
     if (db) {
         const int64_t rows_per = (m + kColsumChunks - 1) / kColsumChunks;
-        const dim3 grid(unsigned((n + 255) / 256), kColsumChunks);
-        colsum_partial_kernel<<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), m, n, rows_per, part);
-        colsum_final_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, st>>>(part, n, kColsumChunks, db);
+        const int64_t chunks = (m + rows_per - 1) / rows_per;
+        const int groups = int(std::min<int64_t>(n / 8, kColsumThreads));
+        const size_t shm = size_t(kColsumThreads / groups) * 8 * groups * sizeof(float);
+        colsum_partial_kernel<<<unsigned(chunks), kColsumThreads, shm, st>>>(static_cast<const __nv_bfloat16*>(dy), m,
+                                                                           n, rows_per, part);
+        colsum_final_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, st>>>(part, n, int(chunks), db);
         AFFMAE_LAUNCH_CHECK("linear bwd bias");
     }
     return AFFMAE_OK;

@@ -56,12 +56,13 @@ struct Params {
     int64_t ldo;              // row stride of out / out2 / aux (elements)
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool PAIR = false>
 struct Cfg {
     // one 4 KB staging buffer per epilogue warp (two for the two outputs of kGeluAux); the rest
     // of the 227 KB goes to the operand ring
     static constexpr int kBufs = EPI == 1 /*kGeluAux*/ ? 2 : 1;
-    static constexpr int kABytes = BM * BK * 2, kBBytes = BN * BK * 2;
+    // a CTA of a pair holds its 128 rows of A and its half of the BN rows of B
+    static constexpr int kABytes = BM * BK * 2, kBBytes = (PAIR ? BN / 2 : BN) * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStages = (227 * 1024 - kEpiWarps * kBufs * kStageBuf - 2048) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
@@ -179,6 +180,44 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
+// CTA-pair TMA load: the data lands in this CTA's shared memory, the transaction bytes are
+// counted on `bar`, a shared::cluster address that may be the leader CTA's barrier
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+// shared::cluster address of this CTA's variable `a` in cluster CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive on the barrier at the same offset in both CTAs of the pair once the pair's MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(uint16_t(3))
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -187,9 +226,17 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // 128-byte swizzle (Swizzle<3,4,3> on a 1024-byte aligned base)
 __device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-template <int BN, int EPI, bool A_MN, bool B_MN>
+// PAIR: a thread-block cluster of 2 CTAs on one TPC computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (UMMA M = 256): CTA r holds rows 128 r.. of A and half of the BN
+// rows of B, the leader (rank 0) issues the MMAs for both SMs, each SM's TMEM receives its 128
+// rows of D.  Per SM that halves the shared-memory and L2 traffic of B.  Protocol: the leader's
+// full barrier counts the bytes of both CTAs (their TMA loads signal it), the leader's commits
+// arrive on both CTAs' empty / tfull barriers, both CTAs' epilogue warps arrive on the leader's
+// tempty barrier.
+template <int BN, int EPI, bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Maps maps, Params p) {
-    using C = Cfg<BN, EPI>;
+    constexpr bool MC = PAIR;
+    using C = Cfg<BN, EPI, PAIR>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_smem = smem + size_t(C::kStages) * C::kStageBytes;  // 8 warps x kBufs x 4 KB
@@ -212,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(tfull(s), 1);
-            mbar_init(tempty(s), kEpiWarps);
+            mbar_init(tempty(s), PAIR ? 2 * kEpiWarps : kEpiWarps);
         }
         for (int e = 0; e < kEpiWarps; ++e) mbar_init(auxbar(e), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -221,32 +268,73 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.out)) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(uint32_t(C::kTmemCols))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(uint32_t(C::kTmemCols))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(uint32_t(C::kTmemCols))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     fence_before();
-    __syncthreads();
+    if (MC)
+        cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
+    else
+        __syncthreads();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int tiles = p.tiles_m * p.tiles_n;
+    // work items (split, m-group, n-block); an m-group is one m-block, or a pair with MC
+    const int rank = MC ? int(blockIdx.x & 1) : 0;
+    const int cid = MC ? int(blockIdx.x >> 1) : int(blockIdx.x);
+    const int ncl = MC ? int(gridDim.x >> 1) : int(gridDim.x);
+    const int mgroups = MC ? (p.tiles_m + 1) / 2 : p.tiles_m;
+    const int tiles = mgroups * p.tiles_n;
     const int work = tiles * p.splits;
 
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int w = blockIdx.x; w < work; w += gridDim.x) {
+            for (int w = cid; w < work; w += ncl) {
                 const int split = w / tiles, t = w - split * tiles;
-                const int mb = t / p.tiles_n, nb = t - mb * p.tiles_n;
+                const int mg = t / p.tiles_n, nb = t - mg * p.tiles_n;
+                const int mb = MC ? 2 * mg + rank : mg;
                 const int kb0 = split * p.kblocks_per_split;
                 const int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty(stage), phase ^ 1);
                     const uint32_t sa = smem_base + uint32_t(stage) * C::kStageBytes;
                     const uint32_t sb = sa + C::kABytes;
+                    if (PAIR) {
+                        // both CTAs' loads count on the leader's full barrier
+                        const uint32_t fb = mapa(full(stage), 0);
+                        if (rank == 0) mbar_expect_tx(full(stage), 2 * C::kStageBytes);
+                        if (A_MN) {
+#pragma unroll
+                            for (int c = 0; c < BM / 64; ++c)
+                                tma_load_3d_pair(sa + c * (BK * 128), &maps.a, mb * BM + 64 * c, kb * BK, 0, fb);
+                        } else {
+                            tma_load_3d_pair(sa, &maps.a, kb * BK, mb * BM, 0, fb);
+                        }
+                        if (B_MN) {
+#pragma unroll
+                            for (int c = 0; c < BN / 128; ++c)
+                                tma_load_3d_pair(sb + c * (BK * 128), &maps.b, nb * BN + rank * (BN / 2) + 64 * c,
+                                                 kb * BK, 0, fb);
+                        } else {
+                            tma_load_3d_pair(sb, &maps.b, kb * BK, nb * BN + rank * (BN / 2), 0, fb);
+                        }
+                        if (++stage == C::kStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     mbar_expect_tx(full(stage), C::kStageBytes);
                     if (A_MN) {
 #pragma unroll
@@ -270,13 +358,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             // instruction descriptor (InstrDescriptor): fp32 D, bf16 A / B, majors, N >> 3, M >> 4
+            constexpr uint32_t kUmmaM = PAIR ? 2 * BM : BM;
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(A_MN) << 15) |
-                                   (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+                                   (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | ((kUmmaM >> 4) << 24);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int w = blockIdx.x; w < work; w += gridDim.x) {
+            for (int w = cid; w < work; w += ncl) {
                 const int split = w / tiles;
                 const int kb0 = split * p.kblocks_per_split;
                 const int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
@@ -289,16 +378,27 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                     const uint32_t sa = smem_base + uint32_t(stage) * C::kStageBytes;
                     const uint64_t da = sdesc(sa, A_MN), db = sdesc(sa + C::kABytes, B_MN);
 #pragma unroll
-                    for (int k = 0; k < BK / UK; ++k)
-                        mma_bf16(tmem_d, sdesc_k(da, k, A_MN), sdesc_k(db, k, B_MN), idesc,
-                                 (kb > kb0 || k > 0) ? 1u : 0u);
-                    mma_commit(empty(stage));
+                    for (int k = 0; k < BK / UK; ++k) {
+                        if (PAIR)
+                            mma_bf16_pair(tmem_d, sdesc_k(da, k, A_MN), sdesc_k(db, k, B_MN), idesc,
+                                          (kb > kb0 || k > 0) ? 1u : 0u);
+                        else
+                            mma_bf16(tmem_d, sdesc_k(da, k, A_MN), sdesc_k(db, k, B_MN), idesc,
+                                     (kb > kb0 || k > 0) ? 1u : 0u);
+                    }
+                    if (PAIR)
+                        mma_commit_pair(empty(stage));
+                    else
+                        mma_commit(empty(stage));
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                mma_commit(tfull(acc));
+                if (PAIR)
+                    mma_commit_pair(tfull(acc));
+                else
+                    mma_commit(tfull(acc));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -322,15 +422,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         uint8_t* gbuf1 = gbuf0 + kStageBuf;
         int acc = 0;
         uint32_t acc_phase = 0, aux_phase = 0;
-        for (int w = blockIdx.x; w < work; w += gridDim.x) {
+        for (int w = cid; w < work; w += ncl) {
             const int split = w / tiles, t = w - split * tiles;
-            const int mb = t / p.tiles_n, nb = t - mb * p.tiles_n;
+            const int mg = t / p.tiles_n, nb = t - mg * p.tiles_n;
+            const int mb = MC ? 2 * mg + rank : mg;
             const int row0 = mb * BM + 32 * quarter;
             mbar_wait(tfull(acc), acc_phase);
             fence_after();
             if (half >= kUnits) {
                 __syncwarp();
-                if (lane == 0) mbar_arrive(tempty(acc));
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_cluster(mapa(tempty(acc), 0));
+                    else
+                        mbar_arrive(tempty(acc));
+                }
             }
 #pragma unroll 1
             for (int u = half; u < kUnits; u += 2) {
@@ -352,7 +458,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                     // this warp's last read of the accumulator: release it to the MMA warp
                     fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(tempty(acc));
+                    if (lane == 0) {
+                        if (PAIR)
+                            mbar_arrive_cluster(mapa(tempty(acc), 0));
+                        else
+                            mbar_arrive(tempty(acc));
+                    }
                 }
                 if (n0 >= p.N) continue;  // warp-uniform
                 if (p.bias && EPI != kGeluBwd && EPI != kF32) {
@@ -441,13 +552,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
     }
     __syncwarp();
     fence_before();
-    __syncthreads();
+    if (MC)
+        cluster_sync();  // no CTA leaves while its peer may still multicast into it
+    else
+        __syncthreads();
     if (warp == 1) {
         __syncwarp();
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(uint32_t(C::kTmemCols))
-                     : "memory");
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(uint32_t(C::kTmemCols))
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(uint32_t(C::kTmemCols))
+                         : "memory");
     }
 }
 
@@ -485,27 +604,43 @@ int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_
     return AFFMAE_OK;
 }
 
-template <int BN, int EPI, bool A_MN, bool B_MN>
+template <int BN, int EPI, bool A_MN, bool B_MN, bool MC>
 int launch(const Maps& maps, const Params& p, cudaStream_t st) {
-    auto kern = tc_gemm_kernel<BN, EPI, A_MN, B_MN>;
+    using C = Cfg<BN, EPI, MC>;
+    auto kern = tc_gemm_kernel<BN, EPI, A_MN, B_MN, MC>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg<BN, EPI>::kSmem));
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
     });
     if (attr_err != cudaSuccess) return cuda_status(attr_err, "gemm: smem attribute");
-    const int work = p.tiles_m * p.tiles_n * p.splits;
-    const int grid = std::min(work, device_sms());
-    kern<<<grid, kThreads, Cfg<BN, EPI>::kSmem, st>>>(maps, p);
-    AFFMAE_LAUNCH_CHECK("tc_gemm_kernel");
+    const int groups = MC ? (p.tiles_m + 1) / 2 : p.tiles_m;
+    const int work = groups * p.tiles_n * p.splits;
+    const int sms = device_sms();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(MC ? 2 * std::min(work, sms / 2) : std::min(work, sms)));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = MC ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, maps, p);
+    if (e != cudaSuccess) return cuda_status(e, "tc_gemm_kernel launch");
     return AFFMAE_OK;
 }
 
 template <int EPI, bool A_MN, bool B_MN>
-int dispatch_bn(int bn, const Maps& maps, const Params& p, cudaStream_t st) {
-    if (bn == 256) return launch<256, EPI, A_MN, B_MN>(maps, p, st);
-    if (bn == 128) return launch<128, EPI, A_MN, B_MN>(maps, p, st);
-    return launch<64, EPI, A_MN, B_MN>(maps, p, st);
+int dispatch_bn(int bn, bool mc, const Maps& maps, const Params& p, cudaStream_t st) {
+    if (bn == 256)
+        return mc ? launch<256, EPI, A_MN, B_MN, true>(maps, p, st) : launch<256, EPI, A_MN, B_MN, false>(maps, p, st);
+    if (bn == 128)
+        return mc ? launch<128, EPI, A_MN, B_MN, true>(maps, p, st) : launch<128, EPI, A_MN, B_MN, false>(maps, p, st);
+    return launch<64, EPI, A_MN, B_MN, false>(maps, p, st);
 }
 
 int pick_bn(int64_t n) {
@@ -541,7 +676,14 @@ int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64
     Maps maps;
     int rc;
     if ((rc = a_mn ? make_map(&maps.a, a, K, M, M, BK) : make_map(&maps.a, a, M, K, K, BM))) return rc;
-    if ((rc = b_mn ? make_map(&maps.b, b, K, N, N, BK) : make_map(&maps.b, b, N, K, K, bn))) return rc;
+    // CTA pairs (UMMA M = 256 over two SMs) when there are two m-blocks to pair and B splits
+    // into two halves
+    // into two halves.  Measured (profiles/r02k_gemm_ab.txt): pairs win once the main loop
+    // dominates -- K >= 512 with 256-wide tiles -- and lose on thin K, on the GELU epilogues
+    // (epilogue-bound) and on the split-K weight gradient
+    const bool mc = !a_mn && bn == 256 && K >= 512 && (M + BM - 1) / BM >= 2 &&
+                    (epi == kStore || epi == kAdd || epi == kF32);
+    if ((rc = b_mn ? make_map(&maps.b, b, K, N, N, BK) : make_map(&maps.b, b, N, K, K, mc ? bn / 2 : bn))) return rc;
     Params p{};
     p.M = int(M);
     p.N = int(N);
@@ -568,24 +710,24 @@ int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64
     const int key = (a_mn ? 2 : 0) | (b_mn ? 1 : 0);
     switch (epi) {
         case kStore:
-            if (key == 0) return dispatch_bn<kStore, false, false>(bn, maps, p, st);
-            if (key == 1) return dispatch_bn<kStore, false, true>(bn, maps, p, st);
+            if (key == 0) return dispatch_bn<kStore, false, false>(bn, mc, maps, p, st);
+            if (key == 1) return dispatch_bn<kStore, false, true>(bn, mc, maps, p, st);
             break;
         case kGeluAux:
-            if (key == 0) return dispatch_bn<kGeluAux, false, false>(bn, maps, p, st);
+            if (key == 0) return dispatch_bn<kGeluAux, false, false>(bn, mc, maps, p, st);
             break;
         case kGelu:
-            if (key == 0) return dispatch_bn<kGelu, false, false>(bn, maps, p, st);
+            if (key == 0) return dispatch_bn<kGelu, false, false>(bn, mc, maps, p, st);
             break;
         case kAdd:
-            if (key == 0) return dispatch_bn<kAdd, false, false>(bn, maps, p, st);
+            if (key == 0) return dispatch_bn<kAdd, false, false>(bn, mc, maps, p, st);
             break;
         case kGeluBwd:
-            if (key == 1) return dispatch_bn<kGeluBwd, false, true>(bn, maps, p, st);
+            if (key == 1) return dispatch_bn<kGeluBwd, false, true>(bn, mc, maps, p, st);
             break;
         case kF32:
-            if (key == 1) return dispatch_bn<kF32, false, true>(bn, maps, p, st);
-            if (key == 3) return dispatch_bn<kF32, true, true>(bn, maps, p, st);
+            if (key == 1) return dispatch_bn<kF32, false, true>(bn, mc, maps, p, st);
+            if (key == 3) return dispatch_bn<kF32, true, true>(bn, mc, maps, p, st);
             break;
         default:
             break;

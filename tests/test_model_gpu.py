@@ -284,11 +284,14 @@ def test_checkpoint_interop(tmp_path):
     p2 = m2.params()
     for n in m.names:
         np.testing.assert_array_equal(p2[n], p[n], err_msg=n)
-    # the next step from the restored state equals the uninterrupted one
+    # the next step from the restored state equals the uninterrupted one: the updates agree to
+    # fp32 rounding (the decoder's parameter-gradient and interpolation reductions use float
+    # atomics, so their summation order -- and the last bits -- may vary between two runs)
     m2.set_images(ref.synth_image(64, 406)[None])
     for mm in (m, m2):
         mm.make_masks([step_mask_seed(1, 1)])
         mm.train_step()
     a, b = m.params(), m2.params()
     for n in m.names:
-        np.testing.assert_array_equal(a[n], b[n], err_msg=n)
+        da, db = (a[n] - p[n]).astype(np.float64), (b[n] - p[n]).astype(np.float64)
+        assert np.linalg.norm(db - da) <= 1e-3 * np.linalg.norm(da) + 1e-9, n
