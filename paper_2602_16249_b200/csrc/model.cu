@@ -863,11 +863,50 @@ int forward(const Ctx& x) {
     const affmae_model_cfg& c = m.cfg;
     const int64_t B = m.B, p2 = m.p2;
     const float inv_image = float(1.0 / double(c.image));
+    const bool aux_on = c.lambda_aux > 0.0;
+    // Work that depends only on coordinates -- the decoder's self knn over the masked cells and
+    // the deep-supervision knn of every stage -- and the deep-supervision heads themselves
+    // (interpolation + head GEMM, which read a finished encoder stage) run on the side stream
+    // beside the encoder / decoder: forked by events after their inputs are produced, joined
+    // before their first main-stream reader (the decoder's self attention, the loss).
+    cudaStream_t ss = m.side ? m.side : x.st;
+    auto fork = [&]() -> int {
+        if (!m.side) return AFFMAE_OK;
+        cudaEvent_t e = x.event();
+        if (!e) return fail(AFFMAE_ECUDA, "model: event pool exhausted");
+        if (cudaEventRecord(e, x.st) != cudaSuccess || cudaStreamWaitEvent(ss, e, 0) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "model forward fork");
+        return AFFMAE_OK;
+    };
+    auto join = [&]() -> int {
+        if (!m.side) return AFFMAE_OK;
+        cudaEvent_t e = x.event();
+        if (!e) return fail(AFFMAE_ECUDA, "model: event pool exhausted");
+        if (cudaEventRecord(e, ss) != cudaSuccess || cudaStreamWaitEvent(x.st, e, 0) != cudaSuccess)
+            return cuda_status(cudaGetLastError(), "model forward join");
+        return AFFMAE_OK;
+    };
+    auto aux_knn = [&](int s) -> int {
+        Stage& S = m.st[size_t(s)];
+        return knn(m.refs, S.coords, B, m.Q, S.N, c.stages[s].interp_k, S.aidx, S.aval, reinterpret_cast<void*>(ss));
+    };
+    auto aux_head = [&](int s) -> int {
+        Stage& S = m.st[size_t(s)];
+        const std::string pre = "aux.s" + std::to_string(s) + ".";
+        const int k = c.stages[s].interp_k;
+        CK(interp_fwd(m.refs, S.coords, S.fout_bf, S.aidx, S.aval, B, m.Q, S.N, S.D, k, PF(m, pre + "p"), kInterpEps,
+                      S.avirt, reinterpret_cast<void*>(ss)));
+        return linear_fwd(S.avirt, PBF(m, pre + "w"), PF(m, pre + "b"), m.Mq, p2, S.D, 0, S.aout, m.gws,
+                          m.gws_bytes, reinterpret_cast<void*>(ss));
+    };
     // inputs: patches, visible / masked cells (pipeline.cpp:402-427, 477-492)
     CK(patchify(m.images, B, m.S, m.S, c.patch, m.patches, x.sv()));
     Stage& S0 = m.st[0];
     CK(mk::cell_rows(m.masked, B, m.g, m.g, 0, m.N[0], double(c.patch), m.vis_rows, S0.coords, x.st));
     CK(mk::cell_rows(m.masked, B, m.g, m.g, 1, m.Q, double(c.patch), m.msk_rows, m.refs, x.st));
+    CK(fork());
+    CK(knn(m.refs, m.refs, B, m.Q, m.Q, c.self_k, m.self_idx, m.self_val, reinterpret_cast<void*>(ss)));
+    if (aux_on && m.ns > 1) CK(aux_knn(0));
     CK(mk::gather_rows_bf16(m.patches, m.vis_rows, S0.M, p2, m.vec, x.st));
     // embed + pos_encode (pipeline.cpp:429-433)
     CK(mk::pos_hidden_fwd(S0.coords, S0.M, inv_image, PF(m, "pos0.w1"), PF(m, "pos0.b1"), m.h0, x.st));
@@ -881,14 +920,24 @@ int forward(const Ctx& x) {
         CK(cluster_index_build(&S.geom, S.coords, &S.idx, m.ws, m.ws_bytes, x.sv()));
         CK(attn_plan_build(&S.geom, &S.desc, S.coords, &S.idx, 1, &S.plan, x.sv()));
         for (int b = 0; b < int(S.blk.size()); ++b) CK(block_fwd(x, s, b));
-        if (s + 1 < m.ns) CK(merge_fwd(x, s));
+        if (aux_on && s + 1 < m.ns) {
+            CK(fork());  // the stage output is final: its deep-supervision head runs beside the rest
+            CK(aux_head(s));
+        }
+        if (s + 1 < m.ns) {
+            CK(merge_fwd(x, s));
+            if (aux_on && s + 2 < m.ns) {
+                CK(fork());  // the next stage's coordinates are known
+                CK(aux_knn(s + 1));
+            }
+        }
     }
     // decoder (pipeline.cpp:473-547)
     const int64_t Mq = m.Mq, dd = m.dd;
     CK(mk::pos_hidden_fwd(m.refs, Mq, inv_image, PF(m, "dec.pos.w1"), PF(m, "dec.pos.b1"), m.hq, x.st));
     CK(x.fwd(m.hq, Mq, kPosHidden, PBF(m, "dec.pos.w2"), dd, PF(m, "dec.pos.b2"), m.yposq));
     CK(mk::add_f32_bf16(PF(m, "dec.mask_token"), 1, m.yposq, Mq, dd, m.fq0, nullptr, x.st));
-    CK(knn(m.refs, m.refs, B, m.Q, m.Q, c.self_k, m.self_idx, m.self_val, x.sv()));
+    CK(join());  // self knn (and everything the side stream has so far) before the decoder
     for (int si = m.ns - 1; si >= 0; --si) {
         Stage& S = m.st[size_t(si)];
         DecStage& d = m.dec[size_t(si)];
@@ -899,20 +948,9 @@ int forward(const Ctx& x) {
         for (int r = 0; r < c.dec_depth; ++r) CK(round_fwd(x, si, r, si == 0 && r + 1 == c.dec_depth));
     }
     CK(x.fwd(m.hh, Mq, dd, PBF(m, "dec.head.w"), p2, PF(m, "dec.head.b"), m.recon));
-    // deep supervision (pipeline.cpp:549-579)
-    int n_aux = 0;
-    if (c.lambda_aux > 0.0) {
-        for (int s = 0; s + 1 < m.ns; ++s) {
-            Stage& S = m.st[size_t(s)];
-            const std::string pre = "aux.s" + std::to_string(s) + ".";
-            const int k = c.stages[s].interp_k;
-            CK(knn(m.refs, S.coords, B, m.Q, S.N, k, S.aidx, S.aval, x.sv()));
-            CK(interp_fwd(m.refs, S.coords, S.fout_bf, S.aidx, S.aval, B, m.Q, S.N, S.D, k, PF(m, pre + "p"),
-                          kInterpEps, S.avirt, x.sv()));
-            CK(x.fwd(S.avirt, Mq, S.D, PBF(m, pre + "w"), p2, PF(m, pre + "b"), S.aout));
-            ++n_aux;
-        }
-    }
+    // deep supervision (pipeline.cpp:549-579): the heads ran on the side stream (above)
+    const int n_aux = aux_on ? m.ns - 1 : 0;
+    CK(join());
     // loss_parts (pipeline.cpp:581-610): the mse gradients are written here too
     // gradient seed 1/world: after the sum over ranks the gradient is that of the GLOBAL batch mean
     const double seed = 1.0 / double(m.world);
@@ -1270,7 +1308,7 @@ int create(const affmae_model_cfg* cfg, Model** out) {
             cudaGetLastError();
             m.side = nullptr;
         }
-        for (size_t i = 0; m.side && i < 2 * m.params.size() + 8; ++i) {
+        for (size_t i = 0; m.side && i < 2 * m.params.size() + 8 + 4 * size_t(m.ns) + 8; ++i) {
             cudaEvent_t e;
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
                 cudaFree(m.dmem);
