@@ -213,9 +213,15 @@ __device__ __forceinline__ float greduce_scatter32(float (&v)[32], int lane) {
 
 // Backward, same layout; MW >= width bounds the per-slot register arrays.
 // Per tile (32 tokens of one head) the warp's blank-k / blank-v gradients (2*HD sums) and,
-// for hidden <= 8, the 4*hidden BiasNet sums are reduce-scattered so lane l keeps sum l.
-template <int HD, int MW>
-__global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_kernel(GAttnP p, const __nv_bfloat16* __restrict__ dout,
+// for hidden <= 8, the 4*hidden BiasNet sums are reduce-scattered so lane l keeps sum l:
+// each lane writes its 32 values as one row of a per-warp 32 x 33 shared-memory tile as they
+// are produced and lane l adds column l (both conflict-free); a register reduce-scatter would
+// hold 32 more live values and push the thread past the 128 registers of two blocks per SM.
+// G: gather mode (p.dsw set; dk / dv are formed later by the reverse-CSR gather): q and dO
+// rows are dead after the scores and are re-read (L1 / L2) for the blank-row gradients, so the
+// thread never holds q, dO and the dQ accumulator at once.
+template <int HD, int MW, bool G>
+__global__ void __launch_bounds__(256, (MW <= 8 && (HD == 16 || (HD == 32 && G))) ? 2 : 1) gattn_bwd_kernel(GAttnP p, const __nv_bfloat16* __restrict__ dout,
                                                         __nv_bfloat16* __restrict__ dq, float* __restrict__ dk,
                                                         float* __restrict__ dv, float* __restrict__ dbk,
                                                         float* __restrict__ dbv, float* __restrict__ dw1,
@@ -225,6 +231,15 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
     extern __shared__ float4 g_units[];
     gstage_units(p, g_units);
     const int lane = threadIdx.x & 31, h = threadIdx.x >> 5, H = p.hidden;
+    float* rs = reinterpret_cast<float*>(g_units + p.heads * H) + h * (32 * 33);  // this warp's tile
+    auto rs_sum = [&]() {  // column `lane` of the tile (after every lane wrote its row)
+        __syncwarp();
+        float t = 0.f;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) t += rs[r * 33 + lane];
+        __syncwarp();
+        return t;
+    };
     const bool small_h = H <= 8;
     const float4* un = g_units + h * H;
     const float b2 = p.b2[h], blank = p.blank[h];
@@ -242,7 +257,6 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
         const int64_t b0 = (row / p.n) * p.n;
         float qf[HD], gf[HD];
         gload_row<HD>(p.q + row * p.ldq + h * HD, qf, 1.f);
-        gload_row<HD>(dout + row * ld + h * HD, gf, 1.f);
         const float2 qx = xy[row];
         float w[MW], dS[MW];
         int key[MW];  // image-local key token, -1 if none
@@ -294,6 +308,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
         wb = act ? __expf(wb - mx) : 0.f;
         l += wb;
         const float il = act ? 1.f / l : 0.f;
+        gload_row<HD>(dout + row * ld + h * HD, gf, 1.f);
         float D = 0.f;
 #pragma unroll
         for (int j = 0; j < MW; ++j) {
@@ -315,23 +330,35 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
             if (key[j] < 0) continue;
             s2 += dS[j];
             const int64_t kr = (b0 + key[j]) * ld + h * HD;
-            float kf[HD];
-            gload_row<HD>(p.k + (b0 + key[j]) * p.ldkv + h * HD, kf, 1.f);
+            const __nv_bfloat16* krow = p.k + (b0 + key[j]) * p.ldkv + h * HD;
             const float a = p.scale * dS[j];
-            if (p.dsw) p.dsw[(gi * p.m + j) * p.heads + h] = make_float2(a, w[j]);
+            if (G) p.dsw[(gi * p.m + j) * p.heads + h] = make_float2(a, w[j]);
+            // the key row streams through in 8-element chunks (a full row in registers would
+            // double the thread's footprint and halve the resident warps)
 #pragma unroll
-            for (int c = 0; c < HD; c += 4) {
+            for (int c = 0; c < HD; c += 8) {
+                const uint4 kx = __ldg(reinterpret_cast<const uint4*>(krow + c));
+                const __nv_bfloat162* kh = reinterpret_cast<const __nv_bfloat162*>(&kx);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) dqa[c + i] = fmaf(dS[j], kf[c + i], dqa[c + i]);
-                if (!p.dsw) {
-                    gred_v4(dk + kr + c, a * qf[c], a * qf[c + 1], a * qf[c + 2], a * qf[c + 3]);
-                    gred_v4(dv + kr + c, w[j] * gf[c], w[j] * gf[c + 1], w[j] * gf[c + 2], w[j] * gf[c + 3]);
+                for (int i = 0; i < 4; ++i) {
+                    const float2 t = __bfloat1622float2(kh[i]);
+                    dqa[c + 2 * i] = fmaf(dS[j], t.x, dqa[c + 2 * i]);
+                    dqa[c + 2 * i + 1] = fmaf(dS[j], t.y, dqa[c + 2 * i + 1]);
+                }
+                if (!G) {
+#pragma unroll
+                    for (int i = 0; i < 8; i += 4) {
+                        gred_v4(dk + kr + c + i, a * qf[c + i], a * qf[c + i + 1], a * qf[c + i + 2],
+                                a * qf[c + i + 3]);
+                        gred_v4(dv + kr + c + i, w[j] * gf[c + i], w[j] * gf[c + i + 1], w[j] * gf[c + i + 2],
+                                w[j] * gf[c + i + 3]);
+                    }
                 }
             }
         }
         if (act) {
             float bkf[HD];
-            gload_row<HD>(p.bk + h * HD, bkf, 1.f);
+            gload_row<HD>(p.bk + h * HD, bkf, 1.f);  // uniform across the warp: one broadcast line
             uint4* o = reinterpret_cast<uint4*>(dq + gi * p.ldd + h * HD);
 #pragma unroll
             for (int c = 0; c < HD; c += 8) {
@@ -349,17 +376,34 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
         // blank rows: values {scale dSb q[c]} then {wb g[c]}, 32 per round
 #pragma unroll
         for (int r = 0; r < NB; ++r) {
-            float v[32];
+            if (G) {
+                // re-read q / dO in 8-element chunks (dead registers since the scores)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int e = r * 32 + i;
-                v[i] = e < HD ? p.scale * dSb * qf[e] : wb * gf[e - HD];
+                for (int i = 0; i < 32; i += 8) {
+                    const int e = r * 32 + i;
+                    const __nv_bfloat16* src = e < HD ? p.q + row * p.ldq + h * HD + e : dout + row * ld + h * HD + (e - HD);
+                    const float mul = e < HD ? p.scale * dSb : wb;
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
+                    const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float2 f = __bfloat1622float2(xh[t]);
+                        rs[lane * 33 + i + 2 * t] = mul * f.x;
+                        rs[lane * 33 + i + 2 * t + 1] = mul * f.y;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int e = r * 32 + i;
+                    rs[lane * 33 + i] = e < HD ? p.scale * dSb * qf[e] : wb * gf[e - HD];
+                }
             }
-            ablk[r] += greduce_scatter32(v, lane);
+            ablk[r] += rs_sum();
         }
         // BiasNet gradients of the tile's pairs
         if (small_h) {
-            float v[32];
+            float* v = rs + lane * 33;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 float gx = 0.f, gy = 0.f, gb = 0.f, gw = 0.f;
@@ -383,7 +427,7 @@ __global__ void __launch_bounds__(256, (HD == 16 && MW <= 8) ? 2 : 1) gattn_bwd_
                 v[16 + u] = gb;
                 v[24 + u] = gw;
             }
-            abias += greduce_scatter32(v, lane);
+            abias += rs_sum();
         } else {
             for (int u = 0; u < H; ++u) {
                 const float4 wu = un[u];
@@ -1248,14 +1292,23 @@ int gattn_fwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
     return AFFMAE_OK;
 }
 
+template <int HD, bool G>
+static void gattn_bwd_launch_g(int mw, unsigned nb, dim3 bt, size_t sm, cudaStream_t st, const GAttnP& p,
+                               const __nv_bfloat16* g, __nv_bfloat16* q, float* dk, float* dv, float* dbk, float* dbv,
+                               float* dw1, float* db1, float* dw2, float* db2, float* dblank) {
+    if (mw <= 1) gattn_bwd_kernel<HD, 1, G><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else if (mw <= 8) gattn_bwd_kernel<HD, 8, G><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else if (mw <= 16) gattn_bwd_kernel<HD, 16, G><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else gattn_bwd_kernel<HD, 31, G><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+}
 template <int HD>
 static void gattn_bwd_launch(int mw, unsigned nb, dim3 bt, size_t sm, cudaStream_t st, const GAttnP& p,
                              const __nv_bfloat16* g, __nv_bfloat16* q, float* dk, float* dv, float* dbk, float* dbv,
                              float* dw1, float* db1, float* dw2, float* db2, float* dblank) {
-    if (mw <= 1) gattn_bwd_kernel<HD, 1><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
-    else if (mw <= 8) gattn_bwd_kernel<HD, 8><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
-    else if (mw <= 16) gattn_bwd_kernel<HD, 16><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
-    else gattn_bwd_kernel<HD, 31><<<nb, bt, sm, st>>>(p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    if (p.dsw)
+        gattn_bwd_launch_g<HD, true>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
+    else
+        gattn_bwd_launch_g<HD, false>(mw, nb, bt, sm, st, p, g, q, dk, dv, dbk, dbv, dw1, db1, dw2, db2, dblank);
 }
 
 int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int32_t* idx, const uint8_t* valid,
@@ -1271,7 +1324,8 @@ int gattn_bwd(const affmae_attn_desc* a, const affmae_attn_inputs* in, const int
     if (batch == 0) return AFFMAE_OK;
     const unsigned nb = gattn_blocks(batch * tokens, a->heads, 1024);
     const dim3 bt(32 * a->heads);
-    const size_t sm = size_t(a->heads) * a->bias_hidden * sizeof(float4);
+    // BiasNet units, then one 32 x 33 reduce-scatter tile per warp
+    const size_t sm = size_t(a->heads) * a->bias_hidden * sizeof(float4) + size_t(a->heads) * 32 * 33 * sizeof(float);
     const auto* g = static_cast<const __nv_bfloat16*>(dout);
     auto* q = static_cast<__nv_bfloat16*>(dq);
     cudaStream_t st = as_stream(stream);
