@@ -13,14 +13,14 @@
 // VJPs: the forward x W^T (A = x K-major, B = W [N, K] K-major), the input gradient dY W
 // (B = W read N-major), the weight gradient dY^T X (A = dY^T and B = X both read M/N-major).
 //
-// Structure (one CTA per SM, persistent over output tiles, 10 warps):
+// Structure (one CTA per SM, persistent over output tiles, 18 warps):
 //   warp 0      TMA producer: 128x64 A and BNx64 B tiles (128-byte swizzle) into a
 //               kStages-deep shared-memory ring, one mbarrier (complete_tx) per stage
 //   warp 1      TMEM allocator + MMA issuer: one thread issues tcgen05.mma.cta_group::1
 //               (M = 128, N = BN, K = 16) from shared-memory descriptors into one of two
 //               TMEM accumulators, tcgen05.commit frees the ring slot / signals the epilogue
-//   warps 2-9   epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes 32·(w%4)..), the
-//               fused elementwise op in fp32, 16-byte global stores; two warps per lane
+//   warps 2-17  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes 32·(w%4)..), the
+//               fused elementwise op in fp32, TMA stores of 32 x 128 B boxes; four warps per lane
 //               quarter split the tile's 32-column chunks; the accumulator is released as
 //               soon as its last chunk is read, so tile t's epilogue overlaps tile t+1's MMAs
 // Work items are (split, m-block, n-block) with m-block outermost within a split, so the
@@ -39,11 +39,15 @@ namespace affmae_b200 {
 namespace tc {
 
 constexpr int BM = 128, BK = 64, UK = 16;
-constexpr int kThreads = 320;  // producer, MMA, 8 epilogue warps
-constexpr int kEpiWarps = 8;
 constexpr int kStageBuf = 32 * 128;  // one epilogue staging buffer: 32 rows x 128 B
 
 enum Epi { kStore = 0, kGeluAux = 1, kAdd = 2, kGeluBwd = 3, kF32 = 4, kGelu = 5 };
+// epilogue warps: the erf-bound GELU epilogues get four per TMEM lane quarter (they bound the
+// thin-K fc1 forward), the store-bound ones two (their staging buffers go to the operand ring)
+template <int EPI>
+struct EpiWarps {
+    static constexpr int value = (EPI == kGeluAux || EPI == kGeluBwd || EPI == kGelu) ? 16 : 8;
+};
 
 struct Params {
     int M, N, K;
@@ -58,9 +62,10 @@ struct Params {
 
 template <int BN, int EPI, bool PAIR = false>
 struct Cfg {
-    // one 4 KB staging buffer per epilogue warp (two for the two outputs of kGeluAux); the rest
-    // of the 227 KB goes to the operand ring
-    static constexpr int kBufs = EPI == 1 /*kGeluAux*/ ? 2 : 1;
+    // one 4 KB staging buffer per epilogue warp; the rest of the 227 KB goes to the operand ring
+    static constexpr int kEpiWarps = EpiWarps<EPI>::value;
+    static constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, epilogue warps
+    static constexpr int kBufs = 1;
     // a CTA of a pair holds its 128 rows of A and its half of the BN rows of B
     static constexpr int kABytes = BM * BK * 2, kBBytes = (PAIR ? BN / 2 : BN) * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
@@ -142,11 +147,28 @@ __device__ __forceinline__ uint64_t sdesc_k(uint64_t d, int k, bool mn_major) {
     return d + uint64_t(mn_major ? (k * UK * 128) >> 4 : (k * UK * 2) >> 4);
 }
 
-__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+// erf for the GELU epilogues (they bound the fc1 forward, ncu: tensor pipe 27 %): Abramowitz &
+// Stegun 7.1.26, |error| <= 1.5e-7 (+ the approximate reciprocal / exponential, ~1e-7
+// relative) against libm erff's branchy polynomial -- one MUFU.RCP, one MUFU.EX2 and six FMAs;
+// e = exp(-z^2) is handed back for the derivative.  The results are rounded to bf16.
+__device__ __forceinline__ float erf_fast(float z, float& e) {
+    const float a = fabsf(z);
+    float t;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, a, 1.f)));
+    e = __expf(-a * a);
+    const float poly =
+        t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+    return copysignf(fmaf(-poly, e, 1.f), z);
+}
+// GELU(x) = x Phi(x) (the reference's gelu_erf) and its derivative Phi(x) + x phi(x)
+__device__ __forceinline__ float gelu_f(float x) {
+    float e;
+    return 0.5f * x * (1.f + erf_fast(x * 0.70710678118654752f, e));
+}
 __device__ __forceinline__ float gelu_grad(float x) {
-    const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
-    const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
-    return cdf + x * pdf;
+    float e;  // exp(-x^2 / 2)
+    const float cdf = 0.5f * (1.f + erf_fast(x * 0.70710678118654752f, e));
+    return fmaf(x * 0.39894228040143268f, e, cdf);
 }
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -234,12 +256,14 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * 128 
 // arrive on both CTAs' empty / tfull barriers, both CTAs' epilogue warps arrive on the leader's
 // tempty barrier.
 template <int BN, int EPI, bool A_MN, bool B_MN, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ Maps maps, Params p) {
+__global__ void __launch_bounds__(Cfg<BN, EPI, PAIR>::kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ Maps maps, Params p) {
     constexpr bool MC = PAIR;
     using C = Cfg<BN, EPI, PAIR>;
+    constexpr int kEpiWarps = C::kEpiWarps;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* stage_smem = smem + size_t(C::kStages) * C::kStageBytes;  // 8 warps x kBufs x 4 KB
+    uint8_t* stage_smem = smem + size_t(C::kStages) * C::kStageBytes;  // kEpiWarps x kBufs x 4 KB
     uint64_t* bars = reinterpret_cast<uint64_t*>(stage_smem + kEpiWarps * C::kBufs * kStageBuf);
     // full[S], empty[S], tfull[2], tempty[2], aux[8], then the TMEM base address slot
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4 + kEpiWarps);
@@ -411,15 +435,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
         // 32 x 128 B staging buffer and one lane hands the buffer to a TMA store, so the global
         // writes are whole lines (the M / N tails are clipped by the tensor map).
         constexpr bool kF32Out = EPI == kF32;
-        constexpr int kCols = kF32Out ? 32 : 64;  // columns per unit
+        constexpr int kCols = kF32Out ? 32 : 64;  // columns per unit (one 128-byte TMA box)
         constexpr int kUnits = BN / kCols;
+        constexpr int kSlots = kEpiWarps / 4;     // warps per lane quarter
         constexpr bool kAux = EPI == kAdd || EPI == kGeluBwd;
-        const int ew = warp - 2;       // 0..7
+        const int ew = warp - 2;       // 0 .. kEpiWarps-1
         const int quarter = warp & 3;  // TMEM lanes 32·quarter .. +31 (tcgen05.ld lane rule)
-        const int half = ew >> 2;      // units half, half + 2, ...
-        const uint32_t buf0 = smem_u32(stage_smem) + uint32_t(ew) * C::kBufs * kStageBuf, buf1 = buf0 + kStageBuf;
+        const int slot = ew >> 2;      // units slot, slot + kSlots, ...
+        const uint32_t buf0 = smem_u32(stage_smem) + uint32_t(ew) * C::kBufs * kStageBuf;
         uint8_t* gbuf0 = stage_smem + size_t(ew) * C::kBufs * kStageBuf;
-        uint8_t* gbuf1 = gbuf0 + kStageBuf;
+        uint4 pre[EPI == kGeluAux ? 8 : 1];  // kGeluAux: the unit's bf16 pre-activations
+        auto release = [&](int a) {
+            fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR)
+                    mbar_arrive_cluster(mapa(tempty(a), 0));
+                else
+                    mbar_arrive(tempty(a));
+            }
+        };
         int acc = 0;
         uint32_t acc_phase = 0, aux_phase = 0;
         for (int w = cid; w < work; w += ncl) {
@@ -429,85 +464,73 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
             const int row0 = mb * BM + 32 * quarter;
             mbar_wait(tfull(acc), acc_phase);
             fence_after();
-            if (half >= kUnits) {
-                __syncwarp();
-                if (lane == 0) {
-                    if (PAIR)
-                        mbar_arrive_cluster(mapa(tempty(acc), 0));
-                    else
-                        mbar_arrive(tempty(acc));
-                }
-            }
+            if (slot >= kUnits) release(acc);
 #pragma unroll 1
-            for (int u = half; u < kUnits; u += 2) {
+            for (int u = slot; u < kUnits; u += kSlots) {
                 const int n0 = nb * BN + kCols * u;
+                const bool last = u + kSlots >= kUnits;  // this warp's last unit of the tile
                 // the staging buffers are free once the previous unit's TMA stores have read them
                 if (lane == 0) bulk_wait_read0();
                 __syncwarp();
-                if (kAux && n0 < p.N) {
-                    if (lane == 0) {
-                        mbar_expect_tx(auxbar(ew), kStageBuf);
-                        tma_load_3d(buf0, &maps.aux, n0, row0, 0, auxbar(ew));
-                    }
+                if (kAux && n0 < p.N && lane == 0) {
+                    mbar_expect_tx(auxbar(ew), kStageBuf);
+                    tma_load_3d(buf0, &maps.aux, n0, row0, 0, auxbar(ew));
                 }
-                float v[kCols];
-                tmem_ld32(tmem_base + (uint32_t(32 * quarter) << 16) + uint32_t(acc * BN + kCols * u), v);
-                if (kCols == 64)
-                    tmem_ld32(tmem_base + (uint32_t(32 * quarter) << 16) + uint32_t(acc * BN + kCols * u + 32), v + 32);
-                if (u + 2 >= kUnits) {
-                    // this warp's last read of the accumulator: release it to the MMA warp
-                    fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (PAIR)
-                            mbar_arrive_cluster(mapa(tempty(acc), 0));
-                        else
-                            mbar_arrive(tempty(acc));
-                    }
-                }
-                if (n0 >= p.N) continue;  // warp-uniform
-                if (p.bias && EPI != kGeluBwd && EPI != kF32) {
-#pragma unroll
-                    for (int j = 0; j < kCols; j += 4) {
-                        if (n0 + j < p.N) {
-                            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n0 + j));
-                            v[j] += b.x;
-                            v[j + 1] += b.y;
-                            v[j + 2] += b.z;
-                            v[j + 3] += b.w;
-                        }
-                    }
+                if (n0 >= p.N) {  // warp-uniform: nothing to store, only the accumulator to release
+                    if (last) release(acc);
+                    continue;
                 }
                 if (kAux) {
                     mbar_wait(auxbar(ew), aux_phase);
                     aux_phase ^= 1;
+                }
+                // 32 columns at a time: a lane holds one row's 32 fp32 values, so four epilogue
+                // warps per lane quarter fit the register file
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 a = *reinterpret_cast<const uint4*>(gbuf0 + swz(lane, c));
-                        const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+                for (int hh = 0; hh < kCols / 32; ++hh) {
+                    float v[32];
+                    tmem_ld32(tmem_base + (uint32_t(32 * quarter) << 16) + uint32_t(acc * BN + kCols * u + 32 * hh), v);
+                    if (last && hh + 1 == kCols / 32) release(acc);
+                    const int c0 = n0 + 32 * hh;
+                    if (p.bias && EPI != kGeluBwd && EPI != kF32) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 f = __bfloat1622float2(ah[e]);
-                            if (EPI == kAdd) {
-                                v[8 * c + 2 * e] += f.x;
-                                v[8 * c + 2 * e + 1] += f.y;
-                            } else {
-                                v[8 * c + 2 * e] *= gelu_grad(f.x);
-                                v[8 * c + 2 * e + 1] *= gelu_grad(f.y);
+                        for (int j = 0; j < 32; j += 4) {
+                            if (c0 + j < p.N) {
+                                const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + c0 + j));
+                                v[j] += b.x;
+                                v[j + 1] += b.y;
+                                v[j + 2] += b.z;
+                                v[j + 3] += b.w;
                             }
                         }
                     }
-                    __syncwarp();  // every lane has read its aux row before the buffer is rewritten
-                }
-                if (kF32Out) {
+                    if (kF32Out) {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        *reinterpret_cast<float4*>(gbuf0 + swz(lane, c)) =
-                            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-                } else {
+                        for (int c = 0; c < 8; ++c)
+                            *reinterpret_cast<float4*>(gbuf0 + swz(lane, c)) =
+                                make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        continue;
+                    }
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        float* x = v + 8 * c;
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const int c = 4 * hh + cc;  // 16-byte chunk of the 128-byte row
+                        float* x = v + 8 * cc;
+                        if (kAux) {
+                            // the row's own aux chunk (same lane, read before it is overwritten)
+                            const uint4 a = *reinterpret_cast<const uint4*>(gbuf0 + swz(lane, c));
+                            const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 f = __bfloat1622float2(ah[e]);
+                                if (EPI == kAdd) {
+                                    x[2 * e] += f.x;
+                                    x[2 * e + 1] += f.y;
+                                } else {
+                                    x[2 * e] *= gelu_grad(f.x);
+                                    x[2 * e + 1] *= gelu_grad(f.y);
+                                }
+                            }
+                        }
                         if (EPI == kGelu) {
 #pragma unroll
                             for (int e = 0; e < 8; ++e) x[e] = gelu_f(x[e]);
@@ -518,18 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                         r.z = pack_bf16(x[4], x[5]);
                         r.w = pack_bf16(x[6], x[7]);
                         *reinterpret_cast<uint4*>(gbuf0 + swz(lane, c)) = r;
-                        if (EPI == kGeluAux) {
-                            // GELU of the stored (bf16-rounded) pre-activation, as the backward sees it
-                            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&r);
-                            uint4 y;
-                            uint32_t* yw = reinterpret_cast<uint32_t*>(&y);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float2 f = __bfloat1622float2(rh[e]);
-                                yw[e] = pack_bf16(gelu_f(f.x), gelu_f(f.y));
-                            }
-                            *reinterpret_cast<uint4*>(gbuf1 + swz(lane, c)) = y;
-                        }
+                        if (EPI == kGeluAux) pre[c & (EPI == kGeluAux ? 7 : 0)] = r;
                     }
                 }
                 fence_proxy_async();
@@ -539,8 +551,31 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
                         tma_reduce_add_3d(&maps.out, buf0, n0, row0, split);
                     else
                         tma_store_3d(&maps.out, buf0, n0, row0, split);
-                    if (EPI == kGeluAux) tma_store_3d(&maps.out2, buf1, n0, row0, 0);
                     bulk_commit();
+                }
+                if (EPI == kGeluAux) {
+                    // GELU of the stored (bf16-rounded) pre-activation, as the backward sees it,
+                    // through the same staging buffer once the pre-activation store has read it
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&pre[c & 7]);
+                        uint4 y;
+                        uint32_t* yw = reinterpret_cast<uint32_t*>(&y);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = __bfloat1622float2(rh[e]);
+                            yw[e] = pack_bf16(gelu_f(f.x), gelu_f(f.y));
+                        }
+                        *reinterpret_cast<uint4*>(gbuf0 + swz(lane, c)) = y;
+                    }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_3d(&maps.out2, buf0, n0, row0, 0);
+                        bulk_commit();
+                    }
                 }
             }
             if (++acc == 2) {
@@ -619,7 +654,7 @@ int launch(const Maps& maps, const Params& p, cudaStream_t st) {
     const int sms = device_sms();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(MC ? 2 * std::min(work, sms / 2) : std::min(work, sms)));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
