@@ -16,9 +16,11 @@
 
 namespace affmae_b200 {
 
+// cs_out: the weight-gradient form (A = dY read M-major) also sums dY's columns -- the bias
+// gradient -- from its operand ring: cs_accum ? cs_out[m] += : cs_out[split * M + m] =
 int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K, int epi,
             const float* bias, const void* aux, void* out, void* out2, float beta, int64_t ldo, int splits,
-            cudaStream_t st);
+            cudaStream_t st, float* cs_out = nullptr, int cs_accum = 0);
 int tc_gemm_pick_splits(int64_t M, int64_t N, int64_t K);
 
 namespace {
@@ -230,25 +232,36 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
     float* part = align256(ws);
     float* skpart = align256(reinterpret_cast<char*>(ws) + colsum_bytes(n));
     int rc = AFFMAE_OK;
+    bool fused_db = false;
     // dX [m, k] = dY [m, n] · W [n, k]   (B read N-major from W's rows)
     if (dx && (rc = tc_gemm(dy, false, w, true, m, k, n, kStore, nullptr, nullptr, dx, nullptr, 0.f, k, 1, st)))
         return rc;
     if (dw) {
-        // dW [n, k] += dY^T · X: A = dY read M-major, B = X read N-major, K = tokens
+        // dW [n, k] += dY^T · X: A = dY read M-major, B = X read N-major, K = tokens; the same
+        // GEMM sums dY's columns into db (per split, then a fixed-order sum over the splits)
         const int splits = tc_gemm_pick_splits(n, k, m);
+        // the fused column sums pay where the weight gradient is split >= 8 ways (few output
+        // tiles, HBM-bound main loop); a weight gradient with many tiles keeps its main loop on
+        // the tensor pipe and takes the separate column-sum pass (profiles/r02l_gemm_probe.txt)
+        fused_db = db && splits >= 8;
         if (splits < 2) {
             if ((rc = tc_gemm(dy, true, x, true, n, k, m, kF32, nullptr, nullptr, dw, nullptr, 1.f, k, 1, st)))
                 return rc;
         } else {
-            if ((rc = tc_gemm(dy, true, x, true, n, k, m, kF32, nullptr, nullptr, skpart, nullptr, 0.f, k, splits, st)))
+            if ((rc = tc_gemm(dy, true, x, true, n, k, m, kF32, nullptr, nullptr, skpart, nullptr, 0.f, k, splits, st,
+                              fused_db ? part : nullptr, 0)))
                 return rc;
             const int64_t n4 = n * k / 4;
             splitk_reduce_kernel<<<unsigned(std::min<int64_t>((n4 + 31) / 32, 8 * kNumSMs)), 256, 0, st>>>(
                 reinterpret_cast<const float4*>(skpart), n4, splits, reinterpret_cast<float4*>(dw));
             AFFMAE_LAUNCH_CHECK("splitk_reduce_kernel");
+            if (fused_db) {
+                colsum_final_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, st>>>(part, n, splits, db);
+                AFFMAE_LAUNCH_CHECK("linear bwd bias");
+            }
         }
     }
-    if (db) {
+    if (db && !fused_db) {
         const int64_t rows_per = (m + kColsumChunks - 1) / kColsumChunks;
         const int64_t chunks = (m + rows_per - 1) / rows_per;
         const int groups = int(std::min<int64_t>(n / 8, kColsumThreads));

@@ -58,13 +58,18 @@ struct Params {
     __nv_bfloat16* out2;      // kGeluAux: GELU(pre)
     float beta;
     int64_t ldo;              // row stride of out / out2 / aux (elements)
+    // weight-gradient GEMMs (kF32, A read M-major = dY^T): column sums of dY over this call's
+    // tokens, i.e. the bias gradient: cs_accum ? cs_out[m] += sum : cs_out[split * M + m] = sum
+    float* cs_out;
+    int cs_accum;
 };
 
-template <int BN, int EPI, bool PAIR = false>
+template <int BN, int EPI, bool PAIR = false, bool CS = false>
 struct Cfg {
     // one 4 KB staging buffer per epilogue warp; the rest of the 227 KB goes to the operand ring
     static constexpr int kEpiWarps = EpiWarps<EPI>::value;
-    static constexpr int kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, epilogue warps
+    // producer, MMA, epilogue warps (+ the column-sum warp of the weight-gradient GEMMs)
+    static constexpr int kThreads = 64 + 32 * kEpiWarps + (CS ? 32 : 0);
     static constexpr int kBufs = 1;
     // a CTA of a pair holds its 128 rows of A and its half of the BN rows of B
     static constexpr int kABytes = BM * BK * 2, kBBytes = (PAIR ? BN / 2 : BN) * BK * 2;
@@ -256,10 +261,13 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * 128 
 // arrive on both CTAs' empty / tfull barriers, both CTAs' epilogue warps arrive on the leader's
 // tempty barrier.
 template <int BN, int EPI, bool A_MN, bool B_MN, bool PAIR>
-__global__ void __launch_bounds__(Cfg<BN, EPI, PAIR>::kThreads, 1)
+__global__ void __launch_bounds__(Cfg<BN, EPI, PAIR, EPI == kF32 && A_MN && !PAIR>::kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ Maps maps, Params p) {
     constexpr bool MC = PAIR;
-    using C = Cfg<BN, EPI, PAIR>;
+    // CS: the weight gradient's A tile (dY^T, M-major) also feeds a column-sum warp -- the bias
+    // gradient comes out of the operand ring instead of a second pass over dY
+    constexpr bool CS = EPI == kF32 && A_MN && !PAIR;
+    using C = Cfg<BN, EPI, PAIR, CS>;
     constexpr int kEpiWarps = C::kEpiWarps;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -279,7 +287,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, PAIR>::kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(full(s), 1);
-            mbar_init(empty(s), 1);
+            mbar_init(empty(s), CS ? 2 : 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(tfull(s), 1);
@@ -377,6 +385,56 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, PAIR>::kThreads, 1)
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (CS && warp == 2 + kEpiWarps) {
+        // column sums of the A tile (k rows x 128 m, two 64-wide M-major chunks, 128-byte
+        // swizzle): lane l owns m = 4l .. 4l+3 and reads them as one 8-byte load per k row; every
+        // ring slot is released by this warp as well as by the MMA commit
+        int stage = 0;
+        uint32_t phase = 0;
+        const int c = lane >> 4, j = (lane & 15) >> 1;
+        for (int w = cid; w < work; w += ncl) {
+            const int split = w / tiles, t = w - split * tiles;
+            const int mg = t / p.tiles_n, nb = t - mg * p.tiles_n;
+            const int mb = MC ? 2 * mg + rank : mg;
+            const int kb0 = split * p.kblocks_per_split;
+            const int kb1 = min(kb0 + p.kblocks_per_split, p.kblocks_total);
+            const bool active = p.cs_out && nb == 0;
+            float a4[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(full(stage), phase);
+                if (active) {
+                    const uint8_t* tile = smem + size_t(stage) * C::kStageBytes + c * (BK * 128) + 8 * (lane & 1);
+#pragma unroll 8
+                    for (int r = 0; r < BK; ++r) {
+                        const uint2 v = *reinterpret_cast<const uint2*>(tile + r * 128 + ((j ^ (r & 7)) << 4));
+                        const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+                        const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+                        a4[0] += f0.x;
+                        a4[1] += f0.y;
+                        a4[2] += f1.x;
+                        a4[3] += f1.y;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty(stage));
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (active) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int m = mb * BM + 4 * lane + i;
+                    if (m < p.M) {
+                        if (p.cs_accum)
+                            p.cs_out[m] += a4[i];
+                        else
+                            p.cs_out[int64_t(split) * p.M + m] = a4[i];
                     }
                 }
             }
@@ -641,7 +699,7 @@ int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_
 
 template <int BN, int EPI, bool A_MN, bool B_MN, bool MC>
 int launch(const Maps& maps, const Params& p, cudaStream_t st) {
-    using C = Cfg<BN, EPI, MC>;
+    using C = Cfg<BN, EPI, MC, EPI == kF32 && A_MN && !MC>;
     auto kern = tc_gemm_kernel<BN, EPI, A_MN, B_MN, MC>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -694,7 +752,7 @@ int pick_bn(int64_t n) {
 // splits > 1 (kF32 only): K is cut into `splits` ranges, split s writes out + s·M·ldo.
 int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64_t N, int64_t K, int epi,
             const float* bias, const void* aux, void* out, void* out2, float beta, int64_t ldo, int splits,
-            cudaStream_t st) {
+            cudaStream_t st, float* cs_out, int cs_accum) {
     using namespace tc;
     if (!a || !b || !out) return fail(AFFMAE_ECONFIG, "gemm: null pointer");
     if (M < 1 || N < 1 || K < 1 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
@@ -735,6 +793,9 @@ int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64
     p.out2 = static_cast<__nv_bfloat16*>(out2);
     p.beta = beta;
     p.ldo = ldo;
+    if (cs_out && !(epi == kF32 && a_mn)) return fail(AFFMAE_ECONFIG, "gemm: column sums need the weight-gradient form");
+    p.cs_out = cs_out;
+    p.cs_accum = cs_accum;
     if (splits > 1 && p.splits != splits) return fail(AFFMAE_ECONFIG, "gemm: split count does not divide K blocks");
     if (epi == kF32 && beta != 0.f && beta != 1.f) return fail(AFFMAE_EUNSUPPORTED, "gemm: fp32 beta must be 0 or 1");
     if ((rc = make_map(&maps.out, out, M, N, ldo, 32, epi == kF32, p.splits))) return rc;
