@@ -242,7 +242,7 @@ int linear_bwd(const void* x, const void* w, const void* dy, int64_t m, int64_t 
         const int splits = tc_gemm_pick_splits(n, k, m);
         // the fused column sums pay where the weight gradient is split >= 8 ways (few output
         // tiles, HBM-bound main loop); a weight gradient with many tiles keeps its main loop on
-        // the tensor pipe and takes the separate column-sum pass (profiles/r02l_gemm_probe.txt)
+        // the tensor pipe and takes the separate column-sum pass (profiles/r02l_gemm_probe.jsonl)
         fused_db = db && splits >= 8;
         if (splits < 2) {
             if ((rc = tc_gemm(dy, true, x, true, n, k, m, kF32, nullptr, nullptr, dw, nullptr, 1.f, k, 1, st)))
