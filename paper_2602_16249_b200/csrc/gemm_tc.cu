@@ -765,6 +765,8 @@ int tc_gemm(const void* a, bool a_mn, const void* b, bool b_mn, int64_t M, int64
         return fail(AFFMAE_ECONFIG, "gemm: epilogue operand missing");
     if (splits < 1 || (splits > 1 && epi != kF32)) return fail(AFFMAE_ECONFIG, "gemm: split-K needs the fp32 epilogue");
     if (ldo < N || ldo % 8) return fail(AFFMAE_ECONFIG, "gemm: bad output stride");
+    if (bias && reinterpret_cast<uintptr_t>(bias) % 16)
+        return fail(AFFMAE_EUNSUPPORTED, "gemm: the bias must be 16-byte aligned (the epilogue reads it as float4)");
     const int bn = pick_bn(N);
     Maps maps;
     int rc;
