@@ -114,11 +114,13 @@ def test_mlp_block_fwd_bwd_matches_fp32_reference():
                                    (41920, 2048, 512),   # stage-2 MLP fc1
                                    (16768, 1024, 4096),  # stage-3 MLP fc2
                                    (2050, 16, 256),      # merge scorer (N = 16: one 64-wide tile, masked)
+                                   (65536, 136, 64),     # split dW with the fused bias sums, ragged M tile
                                    (300, 72, 40)])       # ragged everything
 def test_linear_step_shapes(m, n, k):
     """The training step's GEMM shapes on the hand-written tcgen05 kernel (gemm_tc.cu): forward
     (K-major operands), dX (N-major W), dW over every token (M- and N-major operands, split-K
-    partials reduced in a fixed order) against torch fp32."""
+    partials reduced in a fixed order, the bias gradient from the operand ring when split >= 8
+    ways) against torch fp32."""
     import torch
     from paper_2602_16249_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(m + 7 * n + k)
