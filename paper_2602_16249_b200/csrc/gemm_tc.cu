@@ -13,16 +13,18 @@
 // VJPs: the forward x W^T (A = x K-major, B = W [N, K] K-major), the input gradient dY W
 // (B = W read N-major), the weight gradient dY^T X (A = dY^T and B = X both read M/N-major).
 //
-// Structure (one CTA per SM, persistent over output tiles, 18 warps):
+// Structure (one CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer: 128x64 A and BNx64 B tiles (128-byte swizzle) into a
 //               kStages-deep shared-memory ring, one mbarrier (complete_tx) per stage
 //   warp 1      TMEM allocator + MMA issuer: one thread issues tcgen05.mma.cta_group::1
-//               (M = 128, N = BN, K = 16) from shared-memory descriptors into one of two
-//               TMEM accumulators, tcgen05.commit frees the ring slot / signals the epilogue
-//   warps 2-17  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes 32·(w%4)..), the
-//               fused elementwise op in fp32, TMA stores of 32 x 128 B boxes; four warps per lane
-//               quarter split the tile's 32-column chunks; the accumulator is released as
-//               soon as its last chunk is read, so tile t's epilogue overlaps tile t+1's MMAs
+//               (M = 128, N = BN, K = 16; cta_group::2 / M = 256 for CTA pairs) from
+//               shared-memory descriptors into one of two TMEM accumulators, tcgen05.commit
+//               frees the ring slot / signals the epilogue
+//   epilogue    8 warps (16 for the erf-bound GELU epilogues): tcgen05.ld 32x32b.x32 (warp w
+//               reads TMEM lanes 32·(w%4)..), the fused elementwise op in fp32, TMA stores of
+//               32 x 128 B boxes; the accumulator is released as soon as its last columns are
+//               read, so tile t's epilogue overlaps tile t+1's MMAs
+//   column sums one more warp in the weight-gradient form: the bias gradient from the A tiles
 // Work items are (split, m-block, n-block) with m-block outermost within a split, so the
 // CTAs working at one time share A rows through L2.  The weight gradient's long K (= tokens)
 // is split over `splits` work ranges (multiples of 64) written as fp32 partials.
