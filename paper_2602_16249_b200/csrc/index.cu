@@ -791,12 +791,24 @@ __global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__
     // the knn_prune_bound margin) are skipped from the first key on -- the scan's register
     // insertions, and the warp divergence they cause, drop to the few keys inside it.
     float thr = INFINITY;
+    // the scan starts at the sample nearest to the query and wraps around: with spatially
+    // ordered keys (the model's token order) the K-th best tightens within the first keys, so
+    // the pre-filter rejects nearly all the rest -- scanning from key 0 let the far keys of a
+    // raster order through the filter and into the binary64 insertion (70 % of the kernel's
+    // instructions).  The selection is by (d², j) and does not depend on the order.
+    int start = 0;
     if (nk >= 8 * K) {
         float sd[K];
+        float best = INFINITY;
 #pragma unroll
         for (int r = 0; r < K; ++r) sd[r] = INFINITY;
         for (int i = 0; i < 4 * K; ++i) {
-            float v = knn_d2f(fkeys[int(int64_t(i) * nk / (4 * K))], q);
+            const int si = int(int64_t(i) * nk / (4 * K));
+            float v = knn_d2f(fkeys[si], q);
+            if (v < best) {
+                best = v;
+                start = si;
+            }
 #pragma unroll
             for (int r = 0; r < K; ++r) {
                 const float lo = fminf(v, sd[r]);
@@ -806,13 +818,13 @@ __global__ void __launch_bounds__(256) knn_smem_kernel(const float* __restrict__
         }
         thr = sd[K - 1] < 1e37f ? __fmul_ru(sd[K - 1], 1.f + 0x1p-16f) : INFINITY;
     }
-    for (int j = 0; j < int(nk); ++j) {
+    for (int c = 0, j = start; c < int(nk); ++c, j = j + 1 < int(nk) ? j + 1 : 0) {
         const float2 pf = fkeys[j];
         if (knn_d2f(pf, q) > thr) continue;
         const double2 p = skeys[j];
         const double dx = __dsub_rn(p.x, qx), dy = __dsub_rn(p.y, qy);
         double nd = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-        if (!(nd < d[K - 1])) continue;  // keys arrive in index order: ties keep the lower index
+        if (!pair_lt(nd, j, d[K - 1], jj[K - 1])) continue;  // (d², j) order: ties keep the lower index
         int nj = j;
 #pragma unroll
         for (int r = 0; r < K; ++r) {  // register-resident sorted insertion by (d^2, j), K >= k
