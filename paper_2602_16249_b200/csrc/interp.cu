@@ -124,23 +124,31 @@ __global__ void __launch_bounds__(256) interp_fwd_kernel(const float2* __restric
     InterpRow<CPR> R;
     interp_row_weights<CPR>(R, key_xy + b * nk, idx + rw * k, valid + rw * k, k, queries[rw], p, eps, ok, lane);
     const uint4* fb = feats + b * nk * CPR;
+    // neighbour-outer: each neighbour's weight and id are shuffled once for all of the lane's
+    // chunks (the chunk-outer order repeated both shuffles per chunk; the kernel is issue-bound)
+    float acc[G::CPL][8];
 #pragma unroll
-    for (int cc = 0; cc < G::CPL; ++cc) {
-        const int ch = sl + cc * G::LPR;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int cc = 0; cc < G::CPL; ++cc)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[cc][i] = 0.f;
 #pragma unroll 8
-        for (int t = 0; t < kInterpMaxK; ++t) {
-            if (t >= k) break;  // uniform
-            const float wt = __shfl_sync(0xffffffffu, R.w[t / G::LPR], base + t % G::LPR);
-            const int jt = __shfl_sync(0xffffffffu, R.j[t / G::LPR], base + t % G::LPR);
-            if (wt != 0.f) {
-                float f[8];
-                bf8_to_f32(__ldg(fb + int64_t(jt) * CPR + ch), f);
+    for (int t = 0; t < kInterpMaxK; ++t) {
+        if (t >= k) break;  // uniform
+        const float wt = __shfl_sync(0xffffffffu, R.w[t / G::LPR], base + t % G::LPR);
+        const int jt = __shfl_sync(0xffffffffu, R.j[t / G::LPR], base + t % G::LPR);
+        if (wt != 0.f) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt, f[i], acc[i]);
+            for (int cc = 0; cc < G::CPL; ++cc) {
+                float f[8];
+                bf8_to_f32(__ldg(fb + int64_t(jt) * CPR + sl + cc * G::LPR), f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[cc][i] = fmaf(wt, f[i], acc[cc][i]);
             }
         }
-        if (ok) out[rw * CPR + ch] = f32_to_bf8(acc);
+    }
+    if (ok) {
+#pragma unroll
+        for (int cc = 0; cc < G::CPL; ++cc) out[rw * CPR + sl + cc * G::LPR] = f32_to_bf8(acc[cc]);
     }
 }
 
