@@ -115,6 +115,7 @@ def test_mlp_block_fwd_bwd_matches_fp32_reference():
                                    (16768, 1024, 4096),  # stage-3 MLP fc2
                                    (2050, 16, 256),      # merge scorer (N = 16: one 64-wide tile, masked)
                                    (65536, 136, 64),     # split dW with the fused bias sums, ragged M tile
+                                   (4100, 512, 520),     # CTA-pair forward with a K tail and a ragged M tile
                                    (300, 72, 40)])       # ragged everything
 def test_linear_step_shapes(m, n, k):
     """The training step's GEMM shapes on the hand-written tcgen05 kernel (gemm_tc.cu): forward
