@@ -703,12 +703,20 @@ template <int BN, int EPI, bool A_MN, bool B_MN, bool MC>
 int launch(const Maps& maps, const Params& p, cudaStream_t st) {
     using C = Cfg<BN, EPI, MC, EPI == kF32 && A_MN && !MC>;
     auto kern = tc_gemm_kernel<BN, EPI, A_MN, B_MN, MC>;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
-    });
-    if (attr_err != cudaSuccess) return cuda_status(attr_err, "gemm: smem attribute");
+    // the shared-memory opt-in is per device: set it once for every device this process uses
+    static std::mutex mu;
+    static uint64_t done_mask = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_status(cudaGetLastError(), "gemm: device");
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        const uint64_t bit = dev < 64 ? uint64_t(1) << dev : 0;
+        if (!bit || !(done_mask & bit)) {
+            const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+            if (e != cudaSuccess) return cuda_status(e, "gemm: smem attribute");
+            done_mask |= bit;
+        }
+    }
     const int groups = MC ? (p.tiles_m + 1) / 2 : p.tiles_m;
     const int work = groups * p.tiles_n * p.splits;
     const int sms = device_sms();
